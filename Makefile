@@ -1,0 +1,40 @@
+# Build of the janus B200 library (sm_100a only) and the oracle checkers.
+#   make            -> paper_2605_18404_b200/libjanus_b200.so + oracle/_ref/*
+# The .so is built in-tree (git-ignored) so it travels to the GPU box.
+NVCC ?= /usr/local/cuda/bin/nvcc
+CXX ?= g++
+PKG := paper_2605_18404_b200
+SRC := $(PKG)/csrc
+OBJ := build/obj
+LIB := $(PKG)/libjanus_b200.so
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := -Iinclude -std=c++20 -O3 $(ARCH) -lineinfo -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
+CXXFLAGS := -Iinclude -std=c++20 -O2 -fPIC -ffp-contract=off -Wall -Wextra -I/usr/local/cuda/include
+CU_SRCS := $(wildcard $(SRC)/*.cu)
+CPP_SRCS := $(wildcard $(SRC)/*.cpp)
+OBJS := $(patsubst $(SRC)/%.cu,$(OBJ)/%.cu.o,$(CU_SRCS)) $(patsubst $(SRC)/%.cpp,$(OBJ)/%.cpp.o,$(CPP_SRCS))
+HDRS := $(wildcard $(SRC)/*.cuh) $(wildcard $(SRC)/*.hpp) $(wildcard include/*.h) $(wildcard include/janus/*.hpp)
+
+.PHONY: all lib oracle clean
+all: lib oracle
+
+lib: $(LIB)
+
+$(OBJ):
+	mkdir -p $(OBJ)
+
+$(OBJ)/%.cu.o: $(SRC)/%.cu $(HDRS) | $(OBJ)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $@.ptxas.log || (cat $@.ptxas.log; exit 1)
+
+$(OBJ)/%.cpp.o: $(SRC)/%.cpp $(HDRS) | $(OBJ)
+	$(CXX) $(CXXFLAGS) -c $< -o $@
+
+$(LIB): $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -L/usr/lib/x86_64-linux-gnu -lnccl -lcudart
+
+oracle:
+	$(MAKE) -s -C oracle
+
+clean:
+	rm -rf build $(LIB)
+	$(MAKE) -s -C oracle clean

@@ -1,0 +1,172 @@
+/* include/janus_cuda.h — the C ABI between the janus C++ host (schedule
+ * executor, include/janus/train.hpp) and the sm_100a kernels.
+ *
+ * The reference has no compute interface at all: its seam is "Schedule in ->
+ * per-instruction cost" (graph.hpp:168 replay(g, durations)
+ * instr_duration).  Each entry point below is what EXECUTES one instruction
+ * kind of reference ir.hpp:21-26 instead of looking up its duration:
+ *   LM  -> janus_stage_load                (ir.hpp:25, graph.hpp:124)
+ *   FE/FF/BF/BE -> janus_stage_{fe,ff,bf,be} (ir.hpp:22, phases PAPER.md:171-178)
+ *   SA./RA./SG./RG. payloads -> janus_stage_port (ir.hpp:23-24; pairing graph.hpp:87-118)
+ *   AR  -> janus_stage_grad_buffer + NCCL  (ir.hpp:25)
+ *   OS  -> janus_stage_reduce_grads + janus_stage_optimizer_step (ir.hpp:25)
+ * plus the transports (janus_comm_*) used by the executor for sends, receives and AR.
+ *
+ * Conventions: plain pointers and sizes, no C++/torch types.  Every function
+ * returns 0 on success or a janus::Status code (include/janus/errors.hpp:47)
+ * and records a thread-local message readable with janus_last_error().
+ * Nothing throws across the ABI.  Streams are cudaStream_t passed as void*.
+ */
+#ifndef JANUS_CUDA_H
+#define JANUS_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define JANUS_ABI_VERSION 1
+
+/* precision of the per-edge contractions */
+enum { JANUS_PREC_FP32 = 0, JANUS_PREC_TF32 = 1 };
+
+typedef struct {
+  int32_t L, H, R, n_species;
+  float r_c, w_E, w_F;
+  int32_t precision; /* JANUS_PREC_* */
+} janus_model_desc;
+
+/* Units: 0 embed, 1+2l msg_l, 2+2l upd_l, 2L+1 readout. */
+typedef struct {
+  janus_model_desc model;
+  int32_t unit_begin, unit_end; /* contiguous unit range [begin, end) */
+  int32_t max_atoms, max_edges, max_struct; /* per micro-batch capacity */
+  int32_t n_micro_batches;                  /* geometry + gradient-ledger slots */
+  int32_t n_slots;                          /* in-flight activation slots */
+  int32_t device;                           /* CUDA ordinal */
+} janus_stage_desc;
+
+/* Host-side micro-batch: the LM payload.  Neighbour list in CSR by receiver
+ * (janus_nbrlist_build), atoms of one structure contiguous. */
+typedef struct {
+  int32_t n_atoms, n_struct, n_edges;
+  const double* pos;        /* [n_atoms*3] */
+  const int32_t* species;   /* [n_atoms] */
+  const int32_t* struct_id; /* [n_atoms] */
+  const double* cell;       /* [n_struct] cubic box length */
+  const float* E_target;    /* [n_struct] */
+  const float* F_target;    /* [n_atoms*3] */
+  const int32_t* row_ptr;   /* [n_atoms+1] */
+  const int32_t* col;       /* [n_edges] */
+  const int32_t* shift;     /* [n_edges*3] */
+  const int32_t* rev;       /* [n_edges] */
+} janus_host_batch;
+
+typedef struct {
+  float lr, beta1, beta2, eps;
+} janus_opt;
+
+typedef struct janus_stage janus_stage;
+typedef struct janus_comm janus_comm;
+
+/* ---- errors / info ---- */
+const char* janus_last_error(void);
+int janus_abi_version(void);
+int janus_device_count(int* n);
+
+/* ---- model / host data (no device needed) ---- */
+int64_t janus_param_count(const janus_model_desc* m);
+int64_t janus_unit_param_offset(const janus_model_desc* m, int unit);
+int janus_num_units(const janus_model_desc* m);
+/* Synthetic parameters ~ N(0, 1/fan_in) from SplitMix64(seed ^ tag*phi). */
+int janus_synth_params(const janus_model_desc* m, uint64_t seed, float* out);
+/* Synthetic cubic cell: n_atoms on a jittered sc/fcc lattice at density rho,
+ * species, targets.  pos[n*3], species[n]; returns box length in *cell. */
+int janus_synth_cell(int32_t n_atoms, double rho, int32_t n_species, uint64_t seed, double* pos,
+                     int32_t* species, double* cell, float* E_target, float* F_target);
+/* Periodic neighbour list, bit-exact with the oracle (oracle/mlip_oracle.c).
+ * Returns the edge count in *n_edges; kDomainError if max_edges is exceeded. */
+int janus_nbrlist_build(int32_t n_atoms, const double* pos, const int32_t* struct_id, const double* cell,
+                        double r_c, int32_t max_edges, int32_t* row_ptr, int32_t* col, int32_t* shift,
+                        int32_t* rev, int32_t* n_edges);
+
+/* ---- stages ---- */
+int janus_stage_create(const janus_stage_desc* desc, const float* unit_params, janus_stage** out);
+int janus_stage_destroy(janus_stage* st);
+int janus_stage_load(janus_stage* st, int mb, const janus_host_batch* hb, void* stream);
+int janus_stage_fe(janus_stage* st, int mb, int slot, void* stream);
+int janus_stage_ff(janus_stage* st, int mb, int slot, void* stream);
+int janus_stage_bf(janus_stage* st, int mb, int slot, void* stream);
+int janus_stage_be(janus_stage* st, int mb, int slot, void* stream);
+
+/* Boundary mailboxes (payloads of the send / receive instructions). */
+enum {
+  JANUS_PORT_ACT_IN = 0,  /* FE input  (RAE): h [, m]        */
+  JANUS_PORT_ACT_OUT = 1, /* FE output (SAE): h [, m]        */
+  JANUS_PORT_ADJ_IN = 2,  /* FF input  (RAF): a_h [, a_m], F */
+  JANUS_PORT_ADJ_OUT = 3, /* FF output (SAF): a_h [, a_m], F */
+  JANUS_PORT_TAN_IN = 4,  /* BF input  (RGF): abar [,], Fbar */
+  JANUS_PORT_TAN_OUT = 5, /* BF output (SGF): abar [,], Fbar */
+  JANUS_PORT_BADJ_IN = 6, /* BE input  (RGE): b_h [, b_m]    */
+  JANUS_PORT_BADJ_OUT = 7 /* BE output (SGE): b_h [, b_m]    */
+};
+int janus_stage_port(janus_stage* st, int mb, int slot, int port, void** dptr, size_t* bytes);
+
+/* Outputs for tests and the executor. */
+int janus_stage_energy(janus_stage* st, int mb, float* E_host, float* loss_E_host, void* stream);
+int janus_stage_forces(janus_stage* st, int mb, float* F_host, float* loss_F_host, void* stream);
+/* which: 0 = total, 1 = BE merged first-order term, 2 = BF second-order term;
+ * mb < 0 sums all micro-batches in index order. */
+int janus_stage_grads(janus_stage* st, int which, int mb, float* host_out, void* stream);
+int janus_stage_params(janus_stage* st, float* host_out, void* stream);
+int64_t janus_stage_param_count(janus_stage* st);
+
+/* OS = reduce per-micro-batch ledgers (fixed order) then Adam; AR between. */
+int janus_stage_reduce_grads(janus_stage* st, void* stream);
+int janus_stage_grad_buffer(janus_stage* st, float** dptr, int64_t* count);
+int janus_stage_optimizer_step(janus_stage* st, const janus_opt* opt, void* stream);
+/* Peak device bytes held by the stage (static + activation arena). */
+int janus_stage_memory(janus_stage* st, int64_t* static_bytes, int64_t* arena_bytes);
+
+/* ---- transports ---- */
+/* NCCL: one communicator per process group; id from rank 0 via any channel. */
+int janus_nccl_unique_id(void* id_out /* 128 bytes */);
+int janus_comm_init_nccl(const void* id, int nranks, int rank, int device, janus_comm** out);
+int janus_comm_destroy(janus_comm* c);
+int janus_comm_send(janus_comm* c, const void* buf, size_t bytes, int peer, void* stream);
+int janus_comm_recv(janus_comm* c, void* buf, size_t bytes, int peer, void* stream);
+int janus_comm_group_start(void);
+int janus_comm_group_end(void);
+int janus_comm_allreduce_sum(janus_comm* c, float* buf, int64_t count, void* stream);
+
+/* ---- whole-step executor (C++ train_step behind a C entry) ---- */
+typedef struct {
+  int32_t n_stages;            /* P */
+  int32_t method;              /* 0 SymFold, 1 WaveK, 2 1F1B-2nd */
+  int32_t wavek_k;
+  int32_t n_micro_batches;
+  int32_t local_stages;        /* 1 = all P stages in this process on one GPU (fake transport) */
+  int32_t use_graphs;          /* capture each device list in a CUDA graph */
+} janus_exec_desc;
+
+typedef struct janus_trainer janus_trainer;
+int janus_trainer_create(const janus_exec_desc* ed, const janus_stage_desc* sd, const float* all_params,
+                         janus_comm* comm, int rank, janus_trainer** out);
+int janus_trainer_destroy(janus_trainer* t);
+int janus_trainer_load(janus_trainer* t, int mb, const janus_host_batch* hb);
+int janus_trainer_step(janus_trainer* t, const janus_opt* opt, double* loss_out);
+/* per-instruction device timeline of the last step: [n][4] = device, kind, start_us, end_us */
+int janus_trainer_timeline(janus_trainer* t, double* out, int32_t cap, int32_t* n);
+int janus_trainer_stage(janus_trainer* t, int stage, janus_stage** out);
+int janus_trainer_schedule_text(janus_trainer* t, char* buf, int64_t cap, int64_t* len);
+
+/* ---- schedule generation (host only) ---- */
+int janus_schedule_generate(int method, int P, int n_mb, int k, char* buf, int64_t cap, int64_t* len);
+int janus_schedule_validate(const char* text, int32_t* n_errors);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,352 @@
+"""paper_2605_18404_b200 — B200-native JanusPipe hot path (four-phase MLIP
+training step under SymFold / WaveK pipeline schedules).
+
+The product is C++ host code (include/janus/*.hpp, csrc/*.cpp) calling
+hand-written sm_100a kernels (csrc/*.cu) through the C ABI in
+include/janus_cuda.h, all inside libjanus_b200.so.  This module is a thin
+ctypes binding of that ABI for the tests and bench.py — plumbing, not the
+product.  There is no Python or CPU fallback: if the library is missing,
+import fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libjanus_b200.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} not built — run `make` (or __graft_entry__.build()) first; "
+                      "there is no fallback implementation")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+c_int, c_i64, c_u64, c_f, c_d, c_vp, c_sz = (ctypes.c_int, ctypes.c_int64, ctypes.c_uint64, ctypes.c_float,
+                                              ctypes.c_double, ctypes.c_void_p, ctypes.c_size_t)
+
+PREC_FP32, PREC_TF32 = 0, 1
+(PORT_ACT_IN, PORT_ACT_OUT, PORT_ADJ_IN, PORT_ADJ_OUT, PORT_TAN_IN, PORT_TAN_OUT, PORT_BADJ_IN,
+ PORT_BADJ_OUT) = range(8)
+METHOD_SYMFOLD, METHOD_WAVEK, METHOD_ONEF1B, METHOD_FIRST = 0, 1, 2, 3
+
+
+class ModelDesc(ctypes.Structure):
+    _fields_ = [("L", ctypes.c_int32), ("H", ctypes.c_int32), ("R", ctypes.c_int32), ("n_species", ctypes.c_int32),
+                ("r_c", c_f), ("w_E", c_f), ("w_F", c_f), ("precision", ctypes.c_int32)]
+
+
+class StageDesc(ctypes.Structure):
+    _fields_ = [("model", ModelDesc), ("unit_begin", ctypes.c_int32), ("unit_end", ctypes.c_int32),
+                ("max_atoms", ctypes.c_int32), ("max_edges", ctypes.c_int32), ("max_struct", ctypes.c_int32),
+                ("n_micro_batches", ctypes.c_int32), ("n_slots", ctypes.c_int32), ("device", ctypes.c_int32)]
+
+
+class HostBatch(ctypes.Structure):
+    _fields_ = [("n_atoms", ctypes.c_int32), ("n_struct", ctypes.c_int32), ("n_edges", ctypes.c_int32),
+                ("pos", c_vp), ("species", c_vp), ("struct_id", c_vp), ("cell", c_vp), ("E_target", c_vp),
+                ("F_target", c_vp), ("row_ptr", c_vp), ("col", c_vp), ("shift", c_vp), ("rev", c_vp)]
+
+
+class Opt(ctypes.Structure):
+    _fields_ = [("lr", c_f), ("beta1", c_f), ("beta2", c_f), ("eps", c_f)]
+
+
+class ExecDesc(ctypes.Structure):
+    _fields_ = [("n_stages", ctypes.c_int32), ("method", ctypes.c_int32), ("wavek_k", ctypes.c_int32),
+                ("n_micro_batches", ctypes.c_int32), ("local_stages", ctypes.c_int32), ("use_graphs", ctypes.c_int32)]
+
+
+def _sig(name, res, *args):
+    f = getattr(_lib, name)
+    f.restype = res
+    f.argtypes = list(args)
+    return f
+
+
+_sig("janus_last_error", ctypes.c_char_p)
+_sig("janus_abi_version", c_int)
+_sig("janus_device_count", c_int, c_vp)
+_sig("janus_param_count", c_i64, c_vp)
+_sig("janus_unit_param_offset", c_i64, c_vp, c_int)
+_sig("janus_num_units", c_int, c_vp)
+_sig("janus_synth_params", c_int, c_vp, c_u64, c_vp)
+_sig("janus_synth_cell", c_int, ctypes.c_int32, c_d, ctypes.c_int32, c_u64, c_vp, c_vp, c_vp, c_vp, c_vp)
+_sig("janus_nbrlist_build", c_int, ctypes.c_int32, c_vp, c_vp, c_vp, c_d, ctypes.c_int32, c_vp, c_vp, c_vp, c_vp,
+     c_vp)
+_sig("janus_stage_create", c_int, c_vp, c_vp, c_vp)
+_sig("janus_stage_destroy", c_int, c_vp)
+_sig("janus_stage_load", c_int, c_vp, c_int, c_vp, c_vp)
+for _p in ("fe", "ff", "bf", "be"):
+    _sig(f"janus_stage_{_p}", c_int, c_vp, c_int, c_int, c_vp)
+_sig("janus_stage_port", c_int, c_vp, c_int, c_int, c_int, c_vp, c_vp)
+_sig("janus_stage_energy", c_int, c_vp, c_int, c_vp, c_vp, c_vp)
+_sig("janus_stage_forces", c_int, c_vp, c_int, c_vp, c_vp, c_vp)
+_sig("janus_stage_grads", c_int, c_vp, c_int, c_int, c_vp, c_vp)
+_sig("janus_stage_params", c_int, c_vp, c_vp, c_vp)
+_sig("janus_stage_param_count", c_i64, c_vp)
+_sig("janus_stage_reduce_grads", c_int, c_vp, c_vp)
+_sig("janus_stage_optimizer_step", c_int, c_vp, c_vp, c_vp)
+_sig("janus_stage_memory", c_int, c_vp, c_vp, c_vp)
+_sig("janus_schedule_generate", c_int, c_int, c_int, c_int, c_int, c_vp, c_i64, c_vp)
+_sig("janus_schedule_validate", c_int, ctypes.c_char_p, c_vp)
+
+
+class JanusError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"janus error {code}: {msg}")
+        self.code = code
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        raise JanusError(rc, (_lib.janus_last_error() or b"").decode())
+
+
+def lib():
+    return _lib
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(c_vp)
+
+
+@dataclass
+class Model:
+    L: int = 4
+    H: int = 64
+    R: int = 64
+    n_species: int = 4
+    r_c: float = 5.0
+    w_E: float = 1.0
+    w_F: float = 10.0
+    precision: int = PREC_FP32
+
+    def desc(self) -> ModelDesc:
+        return ModelDesc(self.L, self.H, self.R, self.n_species, self.r_c, self.w_E, self.w_F, self.precision)
+
+    @property
+    def n_units(self) -> int:
+        return 2 * self.L + 2
+
+    def param_count(self) -> int:
+        d = self.desc()
+        return int(_lib.janus_param_count(ctypes.byref(d)))
+
+    def unit_offset(self, u: int) -> int:
+        d = self.desc()
+        return int(_lib.janus_unit_param_offset(ctypes.byref(d), u))
+
+    def synth_params(self, seed: int) -> np.ndarray:
+        out = np.zeros(self.param_count(), np.float32)
+        d = self.desc()
+        check(_lib.janus_synth_params(ctypes.byref(d), seed, _p(out)))
+        return out
+
+
+class Batch:
+    """One micro-batch: concatenated cubic cells + neighbour list (host arrays)."""
+
+    def __init__(self, pos, species, struct_id, cell, E_target, F_target, nl=None, r_c: float | None = None,
+                 max_edges: int | None = None):
+        self.pos = np.ascontiguousarray(pos, np.float64).reshape(-1, 3)
+        self.species = np.ascontiguousarray(species, np.int32)
+        self.struct_id = np.ascontiguousarray(struct_id, np.int32)
+        self.cell = np.ascontiguousarray(cell, np.float64)
+        self.E_target = np.ascontiguousarray(E_target, np.float32)
+        self.F_target = np.ascontiguousarray(F_target, np.float32).reshape(-1, 3)
+        if nl is None:
+            nl = nbrlist(self.pos, self.struct_id, self.cell, r_c, max_edges)
+        self.row_ptr, self.col, self.shift, self.rev = nl
+
+    @property
+    def n_atoms(self):
+        return self.pos.shape[0]
+
+    @property
+    def n_struct(self):
+        return self.cell.shape[0]
+
+    @property
+    def n_edges(self):
+        return int(self.col.shape[0])
+
+    def c(self) -> HostBatch:
+        return HostBatch(self.n_atoms, self.n_struct, self.n_edges, _p(self.pos), _p(self.species),
+                         _p(self.struct_id), _p(self.cell), _p(self.E_target), _p(self.F_target), _p(self.row_ptr),
+                         _p(self.col), _p(self.shift), _p(self.rev))
+
+
+def nbrlist(pos, struct_id, cell, r_c, max_edges=None):
+    pos = np.ascontiguousarray(pos, np.float64).reshape(-1, 3)
+    n = pos.shape[0]
+    max_edges = max_edges or n * 400
+    row_ptr = np.zeros(n + 1, np.int32)
+    col = np.zeros(max_edges, np.int32)
+    shift = np.zeros(3 * max_edges, np.int32)
+    rev = np.zeros(max_edges, np.int32)
+    ne = ctypes.c_int32(0)
+    sid = np.ascontiguousarray(struct_id, np.int32)
+    cl = np.ascontiguousarray(cell, np.float64)
+    check(_lib.janus_nbrlist_build(n, _p(pos), _p(sid), _p(cl), r_c, max_edges, _p(row_ptr), _p(col), _p(shift),
+                                   _p(rev), ctypes.byref(ne)))
+    E = ne.value
+    return row_ptr, col[:E].copy(), shift[:3 * E].copy(), rev[:E].copy()
+
+
+def synth_cell(n_atoms: int, rho: float, n_species: int, seed: int):
+    pos = np.zeros((n_atoms, 3))
+    sp = np.zeros(n_atoms, np.int32)
+    cell = ctypes.c_double(0)
+    Et = np.zeros(1, np.float32)
+    Ft = np.zeros((n_atoms, 3), np.float32)
+    check(_lib.janus_synth_cell(n_atoms, rho, n_species, seed, _p(pos), _p(sp), ctypes.byref(cell), _p(Et), _p(Ft)))
+    return pos, sp, cell.value, float(Et[0]), Ft
+
+
+def synth_batch(model: Model, atoms_per_cell, rho: float, seed: int) -> Batch:
+    """A micro-batch of one or more synthetic cells (sizes in atoms_per_cell)."""
+    if isinstance(atoms_per_cell, int):
+        atoms_per_cell = [atoms_per_cell]
+    P, S, SID, C, E, F = [], [], [], [], [], []
+    for s, n in enumerate(atoms_per_cell):
+        pos, sp, L, Et, Ft = synth_cell(n, rho, model.n_species, seed * 1000003 + s)
+        P.append(pos); S.append(sp); SID.append(np.full(n, s, np.int32)); C.append(L); E.append(Et); F.append(Ft)
+    return Batch(np.concatenate(P), np.concatenate(S), np.concatenate(SID), np.array(C), np.array(E),
+                 np.concatenate(F), r_c=model.r_c)
+
+
+class Stage:
+    """A pipeline stage on one GPU (units [u0, u1))."""
+
+    def __init__(self, model: Model, params_all: np.ndarray, u0: int, u1: int, max_atoms: int, max_edges: int,
+                 max_struct: int = 8, n_mb: int = 1, n_slots: int = 1, device: int = 0):
+        self.model = model
+        self.u0, self.u1 = u0, u1
+        o0, o1 = model.unit_offset(u0), model.unit_offset(u1)
+        self.param_slice = slice(o0, o1)
+        sl = np.ascontiguousarray(params_all[o0:o1], np.float32)
+        self.desc = StageDesc(model.desc(), u0, u1, max_atoms, max_edges, max_struct, n_mb, n_slots, device)
+        h = c_vp()
+        check(_lib.janus_stage_create(ctypes.byref(self.desc), _p(sl), ctypes.byref(h)))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            check(_lib.janus_stage_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def load(self, mb: int, batch: Batch, stream=None):
+        hb = batch.c()
+        check(_lib.janus_stage_load(self.h, mb, ctypes.byref(hb), stream))
+
+    def fe(self, mb, slot=None, stream=None):
+        check(_lib.janus_stage_fe(self.h, mb, mb if slot is None else slot, stream))
+
+    def ff(self, mb, slot=None, stream=None):
+        check(_lib.janus_stage_ff(self.h, mb, mb if slot is None else slot, stream))
+
+    def bf(self, mb, slot=None, stream=None):
+        check(_lib.janus_stage_bf(self.h, mb, mb if slot is None else slot, stream))
+
+    def be(self, mb, slot=None, stream=None):
+        check(_lib.janus_stage_be(self.h, mb, mb if slot is None else slot, stream))
+
+    def port(self, mb, slot, port):
+        ptr, nb = c_vp(), c_sz()
+        check(_lib.janus_stage_port(self.h, mb, slot, port, ctypes.byref(ptr), ctypes.byref(nb)))
+        return ptr.value, nb.value
+
+    def energy(self, mb, n_struct):
+        E = np.zeros(n_struct, np.float32)
+        l = np.zeros(1, np.float32)
+        check(_lib.janus_stage_energy(self.h, mb, _p(E), _p(l), None))
+        return E, float(l[0])
+
+    def forces(self, mb, n_atoms):
+        F = np.zeros((n_atoms, 3), np.float32)
+        l = np.zeros(1, np.float32)
+        check(_lib.janus_stage_forces(self.h, mb, _p(F), _p(l), None))
+        return F, float(l[0])
+
+    def param_count(self):
+        return int(_lib.janus_stage_param_count(self.h))
+
+    def grads(self, which=0, mb=-1):
+        out = np.zeros(self.param_count(), np.float32)
+        check(_lib.janus_stage_grads(self.h, which, mb, _p(out), None))
+        return out
+
+    def params(self):
+        out = np.zeros(self.param_count(), np.float32)
+        check(_lib.janus_stage_params(self.h, _p(out), None))
+        return out
+
+    def reduce_grads(self, stream=None):
+        check(_lib.janus_stage_reduce_grads(self.h, stream))
+
+    def optimizer_step(self, lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, stream=None):
+        o = Opt(lr, beta1, beta2, eps)
+        check(_lib.janus_stage_optimizer_step(self.h, ctypes.byref(o), stream))
+
+    def memory(self):
+        a, b = c_i64(), c_i64()
+        check(_lib.janus_stage_memory(self.h, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
+
+def schedule_text(method: int, P: int, n_mb: int, k: int = 1) -> str:
+    n = c_i64()
+    check(_lib.janus_schedule_generate(method, P, n_mb, k, None, 0, ctypes.byref(n)))
+    buf = ctypes.create_string_buffer(n.value + 1)
+    check(_lib.janus_schedule_generate(method, P, n_mb, k, buf, n.value + 1, ctypes.byref(n)))
+    return buf.value.decode()
+
+
+def validate_schedule(text: str) -> int:
+    n = ctypes.c_int32()
+    check(_lib.janus_schedule_validate(text.encode(), ctypes.byref(n)))
+    return n.value
+
+
+def device_count() -> int:
+    n = c_int()
+    check(_lib.janus_device_count(ctypes.byref(n)))
+    return n.value
+
+
+# ----------------------------------------------------------- cudart helpers
+_cudart = None
+
+
+def cudart():
+    """libcudart for D2D copies in single-GPU multi-stage tests (fake transport)."""
+    global _cudart
+    if _cudart is None:
+        for name in ("libcudart.so", "libcudart.so.12"):
+            try:
+                _cudart = ctypes.CDLL(name)
+                break
+            except OSError:
+                continue
+        if _cudart is None:
+            raise ImportError("libcudart not found")
+        _cudart.cudaMemcpy.argtypes = [c_vp, c_vp, c_sz, c_int]
+        _cudart.cudaMemcpy.restype = c_int
+        _cudart.cudaDeviceSynchronize.restype = c_int
+    return _cudart
+
+
+def d2d(dst: int, src: int, nbytes: int) -> None:
+    rc = cudart().cudaMemcpy(dst, src, nbytes, 3)  # cudaMemcpyDeviceToDevice
+    if rc != 0:
+        raise RuntimeError(f"cudaMemcpy failed: {rc}")

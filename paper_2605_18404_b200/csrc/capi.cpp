@@ -1,0 +1,246 @@
+// capi.cpp — the extern "C" boundary (include/janus_cuda.h).  Every entry
+// point catches C++ exceptions and maps them onto janus::Status codes
+// (include/janus/errors.hpp) with a thread-local message; nothing throws
+// across the ABI.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "../../include/janus/errors.hpp"
+#include "../../include/janus/schedule_gen.hpp"
+#include "../../include/janus_cuda.h"
+#include "cuda_check.hpp"
+#include "host.hpp"
+#include "stage_api.hpp"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    g_last_error.clear();
+    return janus::kOk;
+  } catch (const janus::domain_error& e) {
+    g_last_error = e.what();
+    return janus::kDomainError;
+  } catch (const janus::config_error& e) {
+    g_last_error = e.what();
+    return janus::kConfigError;
+  } catch (const janus::parse_error& e) {
+    g_last_error = e.what();
+    return janus::kParseError;
+  } catch (const janus::deadlock_error& e) {
+    g_last_error = e.what();
+    return janus::kDeadlockError;
+  } catch (const janus::state_error& e) {
+    g_last_error = e.what();
+    return janus::kStateError;
+  } catch (const janus::cuda_error& e) {
+    g_last_error = e.what();
+    return janus::kCudaError;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "out of host memory";
+    return janus::kOutOfMemory;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return janus::kInternalError;
+  } catch (...) {
+    g_last_error = "unknown exception";
+    return janus::kInternalError;
+  }
+}
+
+cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+void need(const void* p, const char* what) {
+  if (!p) throw janus::domain_error(std::string(what) + " is null");
+}
+
+void check_model(const janus_model_desc* m) {
+  need(m, "model");
+  if (m->L < 1 || m->H < 1 || m->R < 2 || m->n_species < 1) throw janus::config_error("bad model shape");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* janus_last_error(void) { return g_last_error.c_str(); }
+int janus_abi_version(void) { return JANUS_ABI_VERSION; }
+
+int janus_device_count(int* n) {
+  return guard([&] {
+    need(n, "n");
+    const cudaError_t e = cudaGetDeviceCount(n);
+    if (e != cudaSuccess) {
+      *n = 0;
+      cudaGetLastError();
+    }
+  });
+}
+
+int64_t janus_param_count(const janus_model_desc* m) {
+  if (!m) return -1;
+  return janus::host_unit_param_offset(*m, 2 * m->L + 2);
+}
+int64_t janus_unit_param_offset(const janus_model_desc* m, int unit) {
+  if (!m || unit < 0 || unit > 2 * m->L + 2) return -1;
+  return janus::host_unit_param_offset(*m, unit);
+}
+int janus_num_units(const janus_model_desc* m) { return m ? 2 * m->L + 2 : -1; }
+
+int janus_synth_params(const janus_model_desc* m, uint64_t seed, float* out) {
+  return guard([&] {
+    check_model(m);
+    need(out, "out");
+    janus::synth_params(*m, seed, out);
+  });
+}
+
+int janus_synth_cell(int32_t n_atoms, double rho, int32_t n_species, uint64_t seed, double* pos, int32_t* species,
+                     double* cell, float* E_target, float* F_target) {
+  return guard([&] {
+    need(pos, "pos");
+    need(species, "species");
+    need(cell, "cell");
+    need(E_target, "E_target");
+    need(F_target, "F_target");
+    *cell = janus::synth_cell(n_atoms, rho, n_species, seed, pos, species, E_target, F_target);
+  });
+}
+
+int janus_nbrlist_build(int32_t n_atoms, const double* pos, const int32_t* struct_id, const double* cell, double r_c,
+                        int32_t max_edges, int32_t* row_ptr, int32_t* col, int32_t* shift, int32_t* rev,
+                        int32_t* n_edges) {
+  return guard([&] {
+    need(pos, "pos");
+    need(struct_id, "struct_id");
+    need(cell, "cell");
+    need(row_ptr, "row_ptr");
+    need(n_edges, "n_edges");
+    if (n_atoms < 1) throw janus::domain_error("n_atoms must be >= 1");
+    if (!(r_c > 0)) throw janus::domain_error("r_c must be > 0");
+    *n_edges = janus::nbrlist_build(n_atoms, pos, struct_id, cell, r_c, max_edges, row_ptr, col, shift, rev);
+  });
+}
+
+// ------------------------------------------------------------------ stages
+int janus_stage_create(const janus_stage_desc* desc, const float* unit_params, janus_stage** out) {
+  return guard([&] {
+    need(desc, "desc");
+    need(unit_params, "unit_params");
+    need(out, "out");
+    *out = nullptr;
+    *out = janus::stage_create(*desc, unit_params);
+  });
+}
+int janus_stage_destroy(janus_stage* st) {
+  return guard([&] { janus::stage_destroy(st); });
+}
+int janus_stage_load(janus_stage* st, int mb, const janus_host_batch* hb, void* stream) {
+  return guard([&] {
+    need(st, "stage");
+    need(hb, "batch");
+    janus::stage_load(st, mb, *hb, S(stream));
+  });
+}
+int janus_stage_fe(janus_stage* st, int mb, int slot, void* stream) {
+  return guard([&] { need(st, "stage"); janus::stage_fe(st, mb, slot, S(stream)); });
+}
+int janus_stage_ff(janus_stage* st, int mb, int slot, void* stream) {
+  return guard([&] { need(st, "stage"); janus::stage_ff(st, mb, slot, S(stream)); });
+}
+int janus_stage_bf(janus_stage* st, int mb, int slot, void* stream) {
+  return guard([&] { need(st, "stage"); janus::stage_bf(st, mb, slot, S(stream)); });
+}
+int janus_stage_be(janus_stage* st, int mb, int slot, void* stream) {
+  return guard([&] { need(st, "stage"); janus::stage_be(st, mb, slot, S(stream)); });
+}
+int janus_stage_port(janus_stage* st, int mb, int slot, int port, void** dptr, size_t* bytes) {
+  return guard([&] {
+    need(st, "stage");
+    need(dptr, "dptr");
+    need(bytes, "bytes");
+    janus::stage_port(st, mb, slot, port, dptr, bytes);
+  });
+}
+int janus_stage_energy(janus_stage* st, int mb, float* E_host, float* loss_E_host, void* stream) {
+  return guard([&] { need(st, "stage"); janus::stage_energy(st, mb, E_host, loss_E_host, S(stream)); });
+}
+int janus_stage_forces(janus_stage* st, int mb, float* F_host, float* loss_F_host, void* stream) {
+  return guard([&] { need(st, "stage"); janus::stage_forces(st, mb, F_host, loss_F_host, S(stream)); });
+}
+int janus_stage_grads(janus_stage* st, int which, int mb, float* host_out, void* stream) {
+  return guard([&] {
+    need(st, "stage");
+    need(host_out, "host_out");
+    janus::stage_grads(st, which, mb, host_out, S(stream));
+  });
+}
+int janus_stage_params(janus_stage* st, float* host_out, void* stream) {
+  return guard([&] {
+    need(st, "stage");
+    need(host_out, "host_out");
+    janus::stage_params(st, host_out, S(stream));
+  });
+}
+int64_t janus_stage_param_count(janus_stage* st) { return st ? janus::stage_param_count(st) : -1; }
+int janus_stage_reduce_grads(janus_stage* st, void* stream) {
+  return guard([&] { need(st, "stage"); janus::stage_reduce_grads(st, S(stream)); });
+}
+int janus_stage_grad_buffer(janus_stage* st, float** dptr, int64_t* count) {
+  return guard([&] {
+    need(st, "stage");
+    need(dptr, "dptr");
+    need(count, "count");
+    janus::stage_grad_buffer(st, dptr, count);
+  });
+}
+int janus_stage_optimizer_step(janus_stage* st, const janus_opt* opt, void* stream) {
+  return guard([&] {
+    need(st, "stage");
+    need(opt, "opt");
+    janus::stage_optimizer(st, *opt, S(stream));
+  });
+}
+int janus_stage_memory(janus_stage* st, int64_t* static_bytes, int64_t* arena_bytes) {
+  return guard([&] { need(st, "stage"); janus::stage_memory(st, static_bytes, arena_bytes); });
+}
+
+// --------------------------------------------------------------- schedules
+int janus_schedule_generate(int method, int P, int n_mb, int k, char* buf, int64_t cap, int64_t* len) {
+  return guard([&] {
+    need(len, "len");
+    janus::Schedule s;
+    switch (method) {
+      case 0: s = janus::symfold(P, n_mb); break;
+      case 1: s = janus::wavek(P, n_mb, k); break;
+      case 2: s = janus::onef1b_2nd(P, n_mb); break;
+      case 3: s = janus::gen_first_order(P, n_mb); break;
+      default: throw janus::domain_error("unknown schedule method");
+    }
+    const std::string text = janus::serialize(s);
+    *len = static_cast<int64_t>(text.size());
+    if (buf && cap > 0) {
+      const size_t n = std::min<size_t>(text.size(), static_cast<size_t>(cap - 1));
+      std::memcpy(buf, text.data(), n);
+      buf[n] = '\0';
+    }
+  });
+}
+
+int janus_schedule_validate(const char* text, int32_t* n_errors) {
+  return guard([&] {
+    need(text, "text");
+    need(n_errors, "n_errors");
+    const janus::ValidationReport r = janus::validate_schedule(janus::deserialize(text));
+    *n_errors = static_cast<int32_t>(r.total_errors());
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,309 @@
+// node_kernels.cuh — per-atom ([N,H]) kernels: small GEMMs with fused input
+// transforms and epilogues, weight-gradient reductions over atoms,
+// elementwise activation derivatives, energy/force loss seeds, Adam, and the
+// LM geometry kernel.  All reductions are fixed-order (deterministic).
+#pragma once
+
+#include "common.cuh"
+
+namespace janus {
+namespace node {
+
+// --------------------------------------------------------- input transforms
+struct InId {
+  __device__ __forceinline__ float operator()(int, int, float x) const { return x; }
+};
+struct InSilu {
+  __device__ __forceinline__ float operator()(int, int, float x) const { return dev::silu(x); }
+};
+// x * SiLU'(p[i][k])
+struct InMulDsilu {
+  const float* p;
+  int H;
+  __device__ __forceinline__ float operator()(int i, int k, float x) const { return x * dev::dsilu(p[(size_t)i * H + k]); }
+};
+// x * pdot[i][k] * SiLU''(p[i][k])
+struct InMulPdotD2silu {
+  const float* p;
+  const float* pdot;
+  int H;
+  __device__ __forceinline__ float operator()(int i, int k, float x) const {
+    const size_t o = (size_t)i * H + k;
+    return x * pdot[o] * dev::d2silu(p[o]);
+  }
+};
+// SiLU'(x) * omega[k]
+struct InDsiluOmega {
+  const float* omega;
+  __device__ __forceinline__ float operator()(int, int k, float x) const { return dev::dsilu(x) * omega[k]; }
+};
+
+// out[i][n] = sum_k op(X[i][k]) M[k][n] (+ bias[n]) (+ add1[i][n]) (+ add2[i][n])
+// One CTA = 16 rows x all H columns; thread owns H/16 consecutive columns.
+template <int H, typename InOp>
+__global__ void __launch_bounds__(256) gemm_rows_kernel(int rows, const float* __restrict__ X, const float* __restrict__ M,
+                                                        const float* __restrict__ bias, const float* add1, const float* add2,
+                                                        float* out, InOp op) {
+  constexpr int CPT = H / 16;
+  __shared__ __align__(16) float sx[16][H];
+  const int r0 = blockIdx.x * 16;
+  for (int x = threadIdx.x; x < 16 * H; x += 256) {
+    const int r = x / H, k = x % H;
+    sx[r][k] = (r0 + r < rows) ? op(r0 + r, k, X[(size_t)(r0 + r) * H + k]) : 0.f;
+  }
+  __syncthreads();
+  const int r = threadIdx.x / 16, c0 = (threadIdx.x % 16) * CPT;
+  float acc[CPT];
+#pragma unroll
+  for (int j = 0; j < CPT; ++j) acc[j] = 0.f;
+#pragma unroll 4
+  for (int k = 0; k < H; ++k) {
+    const float a = sx[r][k];
+#pragma unroll
+    for (int j = 0; j < CPT; j += 4) {
+      const float4 m = *reinterpret_cast<const float4*>(M + (size_t)k * H + c0 + j);
+      acc[j + 0] = fmaf(a, m.x, acc[j + 0]);
+      acc[j + 1] = fmaf(a, m.y, acc[j + 1]);
+      acc[j + 2] = fmaf(a, m.z, acc[j + 2]);
+      acc[j + 3] = fmaf(a, m.w, acc[j + 3]);
+    }
+  }
+  const int i = r0 + r;
+  if (i >= rows) return;
+#pragma unroll
+  for (int j = 0; j < CPT; ++j) {
+    const size_t o = (size_t)i * H + c0 + j;
+    float y = acc[j];
+    if (bias) y += bias[c0 + j];
+    if (add1) y += add1[o];
+    if (add2) y += add2[o];
+    out[o] = y;
+  }
+}
+
+// G[k][n] (+)= sum_i opA(a[i][k]) b[i][n]  (+ sum_i a2[i][k] b2[i][n]); thread per output.
+template <int H, typename InOp>
+__global__ void wgrad_kernel(int rows, const float* __restrict__ a, const float* __restrict__ b,
+                             const float* __restrict__ a2, const float* __restrict__ b2, float* __restrict__ G,
+                             int accumulate, InOp op) {
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= H * H) return;
+  const int k = o / H, n = o % H;
+  float s = 0.f;
+  for (int i = 0; i < rows; ++i) s = fmaf(op(i, k, a[(size_t)i * H + k]), b[(size_t)i * H + n], s);
+  if (a2)
+    for (int i = 0; i < rows; ++i) s = fmaf(a2[(size_t)i * H + k], b2[(size_t)i * H + n], s);
+  G[o] = accumulate ? G[o] + s : s;
+}
+
+// out[n] = sum_i op(x[i][n])
+template <int H, typename InOp>
+__global__ void colsum_kernel(int rows, const float* __restrict__ x, float* __restrict__ out, InOp op) {
+  const int n = threadIdx.x;
+  if (n >= H) return;
+  float s = 0.f;
+  for (int i = 0; i < rows; ++i) s += op(i, n, x[(size_t)i * H + n]);
+  out[n] = s;
+}
+
+// ------------------------------------------------------------ elementwise
+// upd BF: pbar = r pdot SiLU''(p), pdbar = r SiLU'(p), u = SiLU'(p) pdot
+__global__ void upd_bf_ew_kernel(int n, const float* __restrict__ r, const float* __restrict__ pdot,
+                                 const float* __restrict__ p, float* __restrict__ pbar, float* __restrict__ pdbar,
+                                 float* __restrict__ u) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= n) return;
+  const float pp = p[x], ds = dev::dsilu(pp);
+  pbar[x] = r[x] * pdot[x] * dev::d2silu(pp);
+  pdbar[x] = r[x] * ds;
+  u[x] = ds * pdot[x];
+}
+
+// upd BE: pbar = r SiLU'(p)
+__global__ void upd_be_ew_kernel(int n, const float* __restrict__ r, const float* __restrict__ p, float* __restrict__ pbar) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= n) return;
+  pbar[x] = r[x] * dev::dsilu(p[x]);
+}
+
+// readout BF: tau = tdot omega SiLU''(t), w2 = tdot SiLU'(t), sw = SiLU'(t) omega
+template <int H>
+__global__ void ro_bf_ew_kernel(int n, const float* __restrict__ tdot, const float* __restrict__ t,
+                                const float* __restrict__ omega, float* __restrict__ tau, float* __restrict__ w2,
+                                float* __restrict__ sw) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= n) return;
+  const int k = x % H;
+  const float tt = t[x], ds = dev::dsilu(tt);
+  tau[x] = tdot[x] * omega[k] * dev::d2silu(tt);
+  w2[x] = tdot[x] * ds;
+  sw[x] = ds * omega[k];
+}
+
+// readout BE: tbar = eps_s SiLU'(t) omega, es = eps_s SiLU(t)
+template <int H>
+__global__ void ro_be_ew_kernel(int n, const float* __restrict__ t, const float* __restrict__ omega,
+                                const float* __restrict__ eps, const int* __restrict__ struct_id, float* __restrict__ tbar,
+                                float* __restrict__ es) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= n) return;
+  const int i = x / H, k = x % H;
+  const float ep = eps[struct_id[i]], tt = t[x];
+  tbar[x] = ep * dev::dsilu(tt) * omega[k];
+  es[x] = ep * dev::silu(tt);
+}
+
+// ------------------------------------------------------ embed / readout I/O
+template <int H>
+__global__ void embed_fe_kernel(int n_atoms, const int* __restrict__ species, const float* __restrict__ Emb,
+                                float* __restrict__ h) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= n_atoms * H) return;
+  const int i = x / H, k = x % H;
+  h[x] = Emb[(size_t)species[i] * H + k];
+}
+
+// dEmb[z][k] = sum_{i: Z_i = z} b[i][k]  (thread per (z,k), atom order)
+template <int H>
+__global__ void embed_be_kernel(int n_atoms, int n_species, const int* __restrict__ species, const float* __restrict__ b,
+                                float* __restrict__ dEmb) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= n_species * H) return;
+  const int z = x / H, k = x % H;
+  float s = 0.f;
+  for (int i = 0; i < n_atoms; ++i)
+    if (species[i] == z) s += b[(size_t)i * H + k];
+  dEmb[x] = s;
+}
+
+// e_i = <SiLU(t_i), omega> + bias[Z_i]   (warp per atom)
+template <int H>
+__global__ void readout_energy_kernel(int n_atoms, const float* __restrict__ t, const float* __restrict__ omega,
+                                      const float* __restrict__ bias, const int* __restrict__ species,
+                                      float* __restrict__ e_atom) {
+  const int i = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x & 31;
+  if (i >= n_atoms) return;
+  float s = 0.f;
+  for (int k = lane; k < H; k += 32) s = fmaf(dev::silu(t[(size_t)i * H + k]), omega[k], s);
+  s = dev::warp_sum(s);
+  if (lane == 0) e_atom[i] = s + bias[species[i]];
+}
+
+// E_s, eps_s = 2 w_E (E_s - E*_s), loss_E = sum w_E (E - E*)^2.  One thread per
+// structure for E_s (atoms contiguous: struct_ptr), thread 0 for the loss.
+__global__ void energy_loss_kernel(int n_struct, const int* __restrict__ struct_ptr, const float* __restrict__ e_atom,
+                                   const float* __restrict__ E_target, float w_E, float* __restrict__ E,
+                                   float* __restrict__ eps, float* __restrict__ loss_E) {
+  for (int s = threadIdx.x; s < n_struct; s += blockDim.x) {
+    float acc = 0.f;
+    for (int i = struct_ptr[s]; i < struct_ptr[s + 1]; ++i) acc += e_atom[i];
+    E[s] = acc;
+    eps[s] = 2.0f * w_E * (acc - E_target[s]);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float l = 0.f;
+    for (int s = 0; s < n_struct; ++s) {
+      const float d = E[s] - E_target[s];
+      l += w_E * d * d;
+    }
+    *loss_E = l;
+  }
+}
+
+// Fbar = 2 w_F (F - F*); loss_F = sum w_F |F - F*|^2 (single CTA, fixed tree)
+__global__ void force_loss_kernel(int n3, const float* __restrict__ F, const float* __restrict__ F_target, float w_F,
+                                  float* __restrict__ Fbar, float* __restrict__ loss_F) {
+  __shared__ float red[1024];
+  float l = 0.f;
+  for (int x = threadIdx.x; x < n3; x += blockDim.x) {
+    const float d = F[x] - F_target[x];
+    Fbar[x] = 2.0f * w_F * d;
+    l += w_F * d * d;
+  }
+  red[threadIdx.x] = l;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *loss_F = red[0];
+}
+
+// dbias[z] = sum_{i: Z_i = z} eps_{s(i)}
+__global__ void bias_grad_kernel(int n_atoms, int n_species, const int* __restrict__ species,
+                                 const int* __restrict__ struct_id, const float* __restrict__ eps, float* __restrict__ db) {
+  const int z = threadIdx.x;
+  if (z >= n_species) return;
+  float s = 0.f;
+  for (int i = 0; i < n_atoms; ++i)
+    if (species[i] == z) s += eps[struct_id[i]];
+  db[z] = s;
+}
+
+// ----------------------------------------------------------- optimizer
+// g = sum_mb (g1[mb] + g2[mb]) in micro-batch order (schedule-independent)
+__global__ void ledger_reduce_kernel(int64_t n, int n_mb, const float* __restrict__ g1, const float* __restrict__ g2,
+                                     float* __restrict__ g) {
+  const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= n) return;
+  float s = 0.f;
+  for (int m = 0; m < n_mb; ++m) {
+    s += g1[(size_t)m * n + x];
+    s += g2[(size_t)m * n + x];
+  }
+  g[x] = s;
+}
+
+__global__ void adam_kernel(int64_t n, float* __restrict__ p, float* __restrict__ m1, float* __restrict__ m2,
+                            const float* __restrict__ g, float lr, float b1, float b2, float eps, float c1, float c2) {
+  const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= n) return;
+  const float gg = g[x];
+  const float a = b1 * m1[x] + (1.0f - b1) * gg;
+  const float b = b2 * m2[x] + (1.0f - b2) * gg * gg;
+  m1[x] = a;
+  m2[x] = b;
+  p[x] -= lr * (a / c1) / (sqrtf(b / c2) + eps);
+}
+
+// dst[c][r] = src[r][c] for a square H x H block
+template <int H>
+__global__ void transpose_kernel(const float* __restrict__ src, float* __restrict__ dst) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= H * H) return;
+  const int r = x / H, c = x % H;
+  dst[(size_t)c * H + r] = src[x];
+}
+
+// ------------------------------------------------------------ LM geometry
+// r = x_j + s L - x_i in fp64 (same association as the oracle), then
+// d, u = r/d, cosine cutoff c and c' stored in fp32.
+__global__ void geometry_kernel(int n_atoms, const int* __restrict__ row_ptr, const int* __restrict__ col,
+                                const int* __restrict__ shift, const double* __restrict__ pos,
+                                const int* __restrict__ struct_id, const double* __restrict__ cell, double rc,
+                                int* __restrict__ src, float* __restrict__ d_out, float* __restrict__ u_out,
+                                float* __restrict__ c_out, float* __restrict__ dc_out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_atoms) return;
+  const double L = cell[struct_id[i]];
+  const double xi0 = pos[3 * i], xi1 = pos[3 * i + 1], xi2 = pos[3 * i + 2];
+  for (int e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+    const int j = col[e];
+    const double rx = __dsub_rn(__dadd_rn(pos[3 * j + 0], __dmul_rn((double)shift[3 * e + 0], L)), xi0);
+    const double ry = __dsub_rn(__dadd_rn(pos[3 * j + 1], __dmul_rn((double)shift[3 * e + 1], L)), xi1);
+    const double rz = __dsub_rn(__dadd_rn(pos[3 * j + 2], __dmul_rn((double)shift[3 * e + 2], L)), xi2);
+    const double d = sqrt(rx * rx + ry * ry + rz * rz);
+    src[e] = i;
+    d_out[e] = (float)d;
+    u_out[3 * e + 0] = (float)(rx / d);
+    u_out[3 * e + 1] = (float)(ry / d);
+    u_out[3 * e + 2] = (float)(rz / d);
+    const double arg = 3.14159265358979323846 * d / rc;
+    c_out[e] = d < rc ? (float)(0.5 * (cos(arg) + 1.0)) : 0.f;
+    dc_out[e] = d < rc ? (float)(-0.5 * (3.14159265358979323846 / rc) * sin(arg)) : 0.f;
+  }
+}
+
+}  // namespace node
+}  // namespace janus

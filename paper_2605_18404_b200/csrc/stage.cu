@@ -1,0 +1,729 @@
+// stage.cu — the four phases of one pipeline stage, as kernel sequences.
+//
+// Phase semantics per unit, in the stage's unit order:
+//   FE  units ascending : carrier (h[,m]) up
+//   FF  units descending: adjoint a = dE/d(carrier) down, force F accumulated
+//   BF  units ascending : tangent abar = dL_F/da up, BF->BE injections kept
+//                         on this device (Eq. 2 merged first-order routing,
+//                         graph.hpp:151), second-order grads -> ledger g2
+//   BE  units descending: adjoint b = dL/d(carrier) down, grads -> ledger g1
+// Kernels: edge_kernels.cuh (msg unit), node_kernels.cuh (everything else).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+#include <vector>
+
+#include "../../include/janus/errors.hpp"
+
+#include "edge_kernels.cuh"
+#include "node_kernels.cuh"
+#include "stage.cuh"
+#include "stage_api.hpp"
+
+namespace janus {
+
+int64_t unit_param_count(const janus_model_desc& m, int u) {
+  const int64_t H = m.H, R = m.R, S = m.n_species;
+  switch (unit_kind(u, m.L)) {
+    case kEmbed: return S * H;
+    case kReadout: return H * H + 2 * H + S;
+    case kMsg: return R * H + H + H * H + H + H * H;
+    default: return H * H + H + H * H;
+  }
+}
+
+int64_t unit_param_offset(const janus_model_desc& m, int u) {
+  int64_t o = 0;
+  for (int x = 0; x < u; ++x) o += unit_param_count(m, x);
+  return o;
+}
+
+namespace {
+
+constexpr int kH = 64;
+constexpr int kR = 64;
+using EC = edge::Cfg<kH, kR>;
+
+template <typename T>
+T* dalloc(janus_stage* st, size_t n, bool count_static) {
+  void* p = nullptr;
+  const size_t bytes = std::max<size_t>(n, 1) * sizeof(T);
+  JANUS_CUDA(cudaMalloc(&p, bytes));
+  JANUS_CUDA(cudaMemset(p, 0, bytes));
+  st->allocs.push_back(p);
+  (count_static ? st->static_bytes : st->arena_bytes) += static_cast<int64_t>(bytes);
+  return static_cast<T*>(p);
+}
+
+inline int blocks(int64_t n, int t) { return static_cast<int>((n + t - 1) / t); }
+
+template <typename Op = node::InId>
+void gemm(cudaStream_t s, int rows, const float* X, const float* M, const float* bias, const float* add1,
+          const float* add2, float* out, Op op = Op{}) {
+  if (rows <= 0) return;
+  node::gemm_rows_kernel<kH, Op><<<blocks(rows, 16), 256, 0, s>>>(rows, X, M, bias, add1, add2, out, op);
+  JANUS_LAUNCH_CHECK("gemm_rows");
+}
+
+template <typename Op = node::InId>
+void wgrad(cudaStream_t s, int rows, const float* a, const float* b, const float* a2, const float* b2, float* G,
+           Op op = Op{}) {
+  node::wgrad_kernel<kH, Op><<<blocks(kH * kH, 256), 256, 0, s>>>(rows, a, b, a2, b2, G, 0, op);
+  JANUS_LAUNCH_CHECK("wgrad");
+}
+
+template <typename Op = node::InId>
+void colsum(cudaStream_t s, int rows, const float* x, float* out, Op op = Op{}) {
+  node::colsum_kernel<kH, Op><<<1, kH, 0, s>>>(rows, x, out, op);
+  JANUS_LAUNCH_CHECK("colsum");
+}
+
+void copy(cudaStream_t s, float* dst, const float* src, size_t n) {
+  if (n) JANUS_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(float), cudaMemcpyDeviceToDevice, s));
+}
+
+EdgeGeom edge_geom(const DevGeo& g) {
+  EdgeGeom e;
+  e.n_atoms = g.n_atoms;
+  e.n_edges = g.n_edges;
+  e.n_tiles = g.n_tiles;
+  e.row_ptr = g.row_ptr;
+  e.col = g.col;
+  e.src = g.src;
+  e.rev = g.rev;
+  e.tile_row = g.tile_row;
+  e.d = g.d;
+  e.u = g.u;
+  e.c = g.c;
+  e.dc = g.dc;
+  return e;
+}
+
+MsgParams msg_params(const janus_stage* st, int u) {
+  const int H = kH, R = kR;
+  MsgParams p;
+  p.A = st->P(u);
+  p.alpha = p.A + R * H;
+  p.B = p.alpha + H;
+  p.beta = p.B + H * H;
+  p.Bt = st->tw[static_cast<size_t>(u - st->u0)];
+  return p;
+}
+
+// transposed copies: msg [Bt|Wt], upd [Ut|Vt], readout [Ot]
+void refresh_transposes(janus_stage* st, cudaStream_t s) {
+  const int H = kH, R = kR;
+  for (int u = st->u0; u < st->u1; ++u) {
+    float* t = st->tw[static_cast<size_t>(u - st->u0)];
+    const float* P = st->P(u);
+    const int b = blocks(H * H, 256);
+    switch (unit_kind(u, st->m.L)) {
+      case kMsg:
+        node::transpose_kernel<kH><<<b, 256, 0, s>>>(P + R * H + H, t);
+        node::transpose_kernel<kH><<<b, 256, 0, s>>>(P + R * H + H + H * H + H, t + H * H);
+        break;
+      case kUpd:
+        node::transpose_kernel<kH><<<b, 256, 0, s>>>(P, t);
+        node::transpose_kernel<kH><<<b, 256, 0, s>>>(P + H * H + H, t + H * H);
+        break;
+      case kReadout:
+        node::transpose_kernel<kH><<<b, 256, 0, s>>>(P, t);
+        break;
+      default:
+        break;
+    }
+  }
+  JANUS_LAUNCH_CHECK("transpose");
+}
+
+// pointer into a port for the actual atom count n
+float* port_h(const Port& p, int) { return p.buf; }
+float* port_m(const Port& p, int n) { return p.buf + static_cast<size_t>(n) * kH; }
+float* port_v(const Port& p, int n) { return p.buf + static_cast<size_t>(n) * kH * (p.has_m ? 2 : 1); }
+
+const float* in_h(const janus_stage* st, const Slot& sl, int u, int n) {
+  if (u == st->u0) return port_h(sl.ports[JANUS_PORT_ACT_IN], n);
+  const int prev = u - 1;
+  const UnitKind k = unit_kind(prev, st->m.L);
+  if (k == kEmbed || k == kUpd) return sl.units[static_cast<size_t>(prev - st->u0)].out_h;
+  return in_h(st, sl, prev, n);  // msg passes h through
+}
+const float* in_m(const janus_stage* st, const Slot& sl, int u, int n) {
+  if (u == st->u0) return port_m(sl.ports[JANUS_PORT_ACT_IN], n);
+  return sl.units[static_cast<size_t>(u - 1 - st->u0)].out_m;
+}
+
+float* ledger(janus_stage* st, float* base, int mb, int u) {
+  return base + static_cast<size_t>(mb) * st->n_params + st->uoff[static_cast<size_t>(u - st->u0)];
+}
+
+void check_mb_slot(const janus_stage* st, int mb, int slot) {
+  if (mb < 0 || mb >= st->desc.n_micro_batches) throw domain_error("micro-batch index out of range");
+  if (slot < 0 || slot >= st->desc.n_slots) throw domain_error("slot index out of range");
+  if (st->geo[static_cast<size_t>(mb)].n_atoms <= 0) throw state_error("micro-batch not loaded (LM missing)");
+}
+
+}  // namespace
+
+// ============================================================= creation
+janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
+  const janus_model_desc& m = d.model;
+  if (m.H != kH || m.R != kR) throw config_error("this build supports H=64, R=64 (got H=" + std::to_string(m.H) + ", R=" + std::to_string(m.R) + ")");
+  if (m.L < 1 || m.n_species < 1 || m.n_species > 256) throw config_error("bad model shape");
+  if (m.precision != JANUS_PREC_FP32 && m.precision != JANUS_PREC_TF32) throw config_error("unknown precision");
+  const int U = 2 * m.L + 2;
+  if (d.unit_begin < 0 || d.unit_end > U || d.unit_begin >= d.unit_end) throw domain_error("bad unit range");
+  if (d.max_atoms < 1 || d.max_edges < 0 || d.max_struct < 1 || d.n_micro_batches < 1 || d.n_slots < 1)
+    throw domain_error("bad stage capacity");
+  JANUS_CUDA(cudaSetDevice(d.device));
+  auto* st = new janus_stage();
+  try {
+    st->desc = d;
+    st->m = m;
+    st->u0 = d.unit_begin;
+    st->u1 = d.unit_end;
+    st->U = U;
+    st->has_embed = st->u0 == 0;
+    st->has_readout = st->u1 == U;
+    st->in_has_m = st->u0 > 0 && unit_kind(st->u0 - 1, m.L) == kMsg;
+    st->out_has_m = st->u1 < U && unit_kind(st->u1 - 1, m.L) == kMsg;
+    int64_t off = 0;
+    for (int u = st->u0; u < st->u1; ++u) {
+      st->uoff.push_back(off);
+      off += unit_param_count(m, u);
+    }
+    st->n_params = off;
+    const size_t NP = static_cast<size_t>(off), NMB = static_cast<size_t>(d.n_micro_batches);
+    const size_t NA = static_cast<size_t>(d.max_atoms), NE = static_cast<size_t>(d.max_edges);
+    const size_t NH = NA * kH;
+    st->params = dalloc<float>(st, NP, true);
+    st->grad = dalloc<float>(st, NP, true);
+    st->m1 = dalloc<float>(st, NP, true);
+    st->m2 = dalloc<float>(st, NP, true);
+    st->g1 = dalloc<float>(st, NP * NMB, true);
+    st->g2 = dalloc<float>(st, NP * NMB, true);
+    JANUS_CUDA(cudaMemcpy(st->params, unit_params, NP * sizeof(float), cudaMemcpyHostToDevice));
+    for (int u = st->u0; u < st->u1; ++u) {
+      const UnitKind k = unit_kind(u, m.L);
+      st->tw.push_back(k == kEmbed ? nullptr : dalloc<float>(st, (k == kReadout ? 1 : 2) * kH * kH, true));
+    }
+    // geometry per micro-batch
+    st->geo.resize(NMB);
+    for (auto& g : st->geo) {
+      g.row_ptr = dalloc<int>(st, NA + 1, false);
+      g.col = dalloc<int>(st, NE, false);
+      g.src = dalloc<int>(st, NE, false);
+      g.rev = dalloc<int>(st, NE, false);
+      g.shift = dalloc<int>(st, 3 * NE, false);
+      g.tile_row = dalloc<int>(st, NA + 1, false);
+      g.species = dalloc<int>(st, NA, false);
+      g.struct_id = dalloc<int>(st, NA, false);
+      g.struct_ptr = dalloc<int>(st, static_cast<size_t>(d.max_struct) + 1, false);
+      g.pos = dalloc<double>(st, 3 * NA, false);
+      g.cell = dalloc<double>(st, static_cast<size_t>(d.max_struct), false);
+      g.d = dalloc<float>(st, NE, false);
+      g.u = dalloc<float>(st, 3 * NE, false);
+      g.c = dalloc<float>(st, NE, false);
+      g.dc = dalloc<float>(st, NE, false);
+      g.E_target = dalloc<float>(st, static_cast<size_t>(d.max_struct), false);
+      g.F_target = dalloc<float>(st, 3 * NA, false);
+    }
+    // slots
+    st->slots.resize(static_cast<size_t>(d.n_slots));
+    for (auto& sl : st->slots) {
+      sl.units.resize(static_cast<size_t>(st->u1 - st->u0));
+      for (int u = st->u0; u < st->u1; ++u) {
+        UnitBufs& b = sl.units[static_cast<size_t>(u - st->u0)];
+        switch (unit_kind(u, m.L)) {
+          case kEmbed: b.out_h = dalloc<float>(st, NH, false); break;
+          case kMsg:
+            b.out_m = dalloc<float>(st, NH, false);
+            b.v = dalloc<float>(st, NH, false);
+            b.ff_a = dalloc<float>(st, NH, false);
+            b.ff_Y = dalloc<float>(st, NH, false);
+            b.inj = dalloc<float>(st, NH, false);
+            break;
+          case kUpd:
+            b.out_h = dalloc<float>(st, NH, false);
+            b.p = dalloc<float>(st, NH, false);
+            b.ff_a = dalloc<float>(st, NH, false);
+            b.inj = dalloc<float>(st, NH, false);
+            break;
+          case kReadout:
+            b.p = dalloc<float>(st, NH, false);
+            b.inj = dalloc<float>(st, NH, false);
+            break;
+        }
+      }
+      const bool in_b = st->u0 > 0, out_b = st->u1 < U;
+      for (int p = 0; p < 8; ++p) {
+        const bool at_input = (p == JANUS_PORT_ACT_IN || p == JANUS_PORT_ADJ_OUT || p == JANUS_PORT_TAN_IN || p == JANUS_PORT_BADJ_OUT);
+        if (at_input ? !in_b : !out_b) continue;
+        Port& port = sl.ports[p];
+        port.has_m = at_input ? st->in_has_m : st->out_has_m;
+        port.has_vec = (p >= JANUS_PORT_ADJ_IN && p <= JANUS_PORT_TAN_OUT);
+        port.buf = dalloc<float>(st, NH * (port.has_m ? 2 : 1) + (port.has_vec ? 3 * NA : 0), false);
+      }
+      sl.F = dalloc<float>(st, 3 * NA, false);
+      sl.Fbar = dalloc<float>(st, 3 * NA, false);
+      sl.e_atom = dalloc<float>(st, NA, false);
+      sl.E = dalloc<float>(st, static_cast<size_t>(d.max_struct), false);
+      sl.eps = dalloc<float>(st, static_cast<size_t>(d.max_struct), false);
+      sl.loss = dalloc<float>(st, 2, false);
+    }
+    st->wh = dalloc<float>(st, NH, false);
+    st->wm = dalloc<float>(st, NH, false);
+    st->s1 = dalloc<float>(st, NH, false);
+    st->s2 = dalloc<float>(st, NH, false);
+    st->s3 = dalloc<float>(st, NH, false);
+    st->s4 = dalloc<float>(st, NH, false);
+    st->s5 = dalloc<float>(st, NH, false);
+    st->q = dalloc<float>(st, NE, false);
+    st->partial = dalloc<float>(st, NA * static_cast<size_t>(EC::PE), false);
+    st->zero = dalloc<float>(st, NH, false);
+    JANUS_CUDA(cudaFuncSetAttribute(edge::msg_fe_kernel<kH, kR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge::fe_smem<kH, kR>()));
+    JANUS_CUDA(cudaFuncSetAttribute(edge::msg_ff_kernel<kH, kR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge::ff_smem<kH, kR>()));
+    JANUS_CUDA(cudaFuncSetAttribute(edge::msg_bf_kernel<kH, kR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge::bf_smem<kH, kR>()));
+    JANUS_CUDA(cudaFuncSetAttribute(edge::msg_be_kernel<kH, kR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge::be_smem<kH, kR>()));
+    refresh_transposes(st, nullptr);
+    JANUS_CUDA(cudaDeviceSynchronize());
+  } catch (...) {
+    for (void* p : st->allocs) cudaFree(p);
+    delete st;
+    throw;
+  }
+  return st;
+}
+
+void stage_destroy(janus_stage* st) {
+  if (!st) return;
+  cudaSetDevice(st->desc.device);
+  cudaDeviceSynchronize();
+  for (void* p : st->allocs) cudaFree(p);
+  delete st;
+}
+
+size_t port_elems(const janus_stage* st, int port, int n) {
+  const Port& p = st->slots[0].ports[port];
+  if (!p.buf) return 0;
+  return static_cast<size_t>(n) * kH * (p.has_m ? 2 : 1) + (p.has_vec ? 3 * static_cast<size_t>(n) : 0);
+}
+
+// ================================================================== LM
+void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_t s) {
+  if (mb < 0 || mb >= st->desc.n_micro_batches) throw domain_error("micro-batch index out of range");
+  if (hb.n_atoms < 1 || hb.n_atoms > st->desc.max_atoms) throw domain_error("n_atoms exceeds stage capacity");
+  if (hb.n_edges < 0 || hb.n_edges > st->desc.max_edges) throw domain_error("n_edges exceeds stage capacity");
+  if (hb.n_struct < 1 || hb.n_struct > st->desc.max_struct) throw domain_error("n_struct exceeds stage capacity");
+  JANUS_CUDA(cudaSetDevice(st->desc.device));
+  DevGeo& g = st->geo[static_cast<size_t>(mb)];
+  const int N = hb.n_atoms, E = hb.n_edges;
+  // host-side row tiles (<= 8 rows and <= TE edges, or one long row) and struct offsets
+  std::vector<int> tiles{0};
+  {
+    int rows = 0, edges = 0;
+    for (int i = 0; i < N; ++i) {
+      const int deg = hb.row_ptr[i + 1] - hb.row_ptr[i];
+      if (rows > 0 && (rows == edge::kRowsPerTile || edges + deg > edge::TE)) {
+        tiles.push_back(i);
+        rows = 0;
+        edges = 0;
+      }
+      ++rows;
+      edges += deg;
+    }
+    tiles.push_back(N);
+  }
+  std::vector<int> sptr(static_cast<size_t>(hb.n_struct) + 1, 0);
+  for (int i = 0; i < N; ++i) {
+    const int sid = hb.struct_id[i];
+    if (sid < 0 || sid >= hb.n_struct || (i > 0 && sid < hb.struct_id[i - 1])) throw domain_error("struct_id must be non-decreasing in [0, n_struct)");
+    sptr[static_cast<size_t>(sid) + 1] = i + 1;
+  }
+  for (int x = 1; x <= hb.n_struct; ++x) sptr[static_cast<size_t>(x)] = std::max(sptr[static_cast<size_t>(x)], sptr[static_cast<size_t>(x) - 1]);
+  if (hb.row_ptr[0] != 0 || hb.row_ptr[N] != E) throw domain_error("row_ptr inconsistent with n_edges");
+  g.n_atoms = N;
+  g.n_edges = E;
+  g.n_struct = hb.n_struct;
+  g.n_tiles = static_cast<int>(tiles.size()) - 1;
+  auto h2d = [s](void* dst, const void* src, size_t bytes) {
+    if (bytes) JANUS_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+  };
+  h2d(g.row_ptr, hb.row_ptr, sizeof(int) * (N + 1));
+  h2d(g.col, hb.col, sizeof(int) * E);
+  h2d(g.rev, hb.rev, sizeof(int) * E);
+  h2d(g.shift, hb.shift, sizeof(int) * 3 * E);
+  h2d(g.species, hb.species, sizeof(int) * N);
+  h2d(g.struct_id, hb.struct_id, sizeof(int) * N);
+  h2d(g.pos, hb.pos, sizeof(double) * 3 * N);
+  h2d(g.cell, hb.cell, sizeof(double) * hb.n_struct);
+  h2d(g.E_target, hb.E_target, sizeof(float) * hb.n_struct);
+  h2d(g.F_target, hb.F_target, sizeof(float) * 3 * N);
+  h2d(g.tile_row, tiles.data(), sizeof(int) * tiles.size());
+  h2d(g.struct_ptr, sptr.data(), sizeof(int) * sptr.size());
+  node::geometry_kernel<<<blocks(N, 128), 128, 0, s>>>(N, g.row_ptr, g.col, g.shift, g.pos, g.struct_id, g.cell,
+                                                       static_cast<double>(st->m.r_c), g.src, g.d, g.u, g.c, g.dc);
+  JANUS_LAUNCH_CHECK("geometry");
+  // pageable H2D copies of host vectors: make sure they are consumed before return
+  JANUS_CUDA(cudaStreamSynchronize(s));
+}
+
+// ================================================================== FE
+void stage_fe(janus_stage* st, int mb, int slot, cudaStream_t s) {
+  check_mb_slot(st, mb, slot);
+  const DevGeo& g = st->geo[static_cast<size_t>(mb)];
+  Slot& sl = st->slots[static_cast<size_t>(slot)];
+  sl.mb = mb;
+  const int N = g.n_atoms, H = kH, R = kR, L = st->m.L;
+  const EdgeGeom eg = edge_geom(g);
+  const float* cur_h = st->u0 > 0 ? port_h(sl.ports[JANUS_PORT_ACT_IN], N) : nullptr;
+  const float* cur_m = st->in_has_m ? port_m(sl.ports[JANUS_PORT_ACT_IN], N) : nullptr;
+  for (int u = st->u0; u < st->u1; ++u) {
+    UnitBufs& b = sl.units[static_cast<size_t>(u - st->u0)];
+    const float* P = st->P(u);
+    switch (unit_kind(u, L)) {
+      case kEmbed:
+        node::embed_fe_kernel<kH><<<blocks(N * H, 256), 256, 0, s>>>(N, g.species, P, b.out_h);
+        cur_h = b.out_h;
+        break;
+      case kMsg: {
+        const float* W = P + R * H + H + H * H + H;
+        gemm(s, N, cur_h, W, nullptr, nullptr, nullptr, b.v);
+        if (g.n_tiles > 0)
+          edge::msg_fe_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::fe_smem<kH, kR>(), s>>>(eg, msg_params(st, u), st->m.r_c, b.v, b.out_m);
+        cur_m = b.out_m;
+        break;
+      }
+      case kUpd: {
+        const float *Um = P, *ups = P + H * H, *V = P + H * H + H;
+        gemm(s, N, cur_m, Um, ups, nullptr, nullptr, b.p);
+        gemm(s, N, b.p, V, nullptr, cur_h, nullptr, b.out_h, node::InSilu{});
+        cur_h = b.out_h;
+        cur_m = nullptr;
+        break;
+      }
+      case kReadout: {
+        const float *O = P, *o = P + H * H, *om = P + H * H + H, *bias = P + H * H + 2 * H;
+        gemm(s, N, cur_h, O, o, nullptr, nullptr, b.p);
+        node::readout_energy_kernel<kH><<<blocks(N, 8), 256, 0, s>>>(N, b.p, om, bias, g.species, sl.e_atom);
+        node::energy_loss_kernel<<<1, 128, 0, s>>>(g.n_struct, g.struct_ptr, sl.e_atom, g.E_target, st->m.w_E, sl.E,
+                                                   sl.eps, sl.loss);
+        break;
+      }
+    }
+    JANUS_LAUNCH_CHECK("stage_fe");
+  }
+  if (st->u1 < st->U) {
+    const Port& out = sl.ports[JANUS_PORT_ACT_OUT];
+    copy(s, port_h(out, N), cur_h, static_cast<size_t>(N) * H);
+    if (out.has_m) copy(s, port_m(out, N), cur_m, static_cast<size_t>(N) * H);
+  }
+}
+
+// ================================================================== FF
+void stage_ff(janus_stage* st, int mb, int slot, cudaStream_t s) {
+  check_mb_slot(st, mb, slot);
+  const DevGeo& g = st->geo[static_cast<size_t>(mb)];
+  Slot& sl = st->slots[static_cast<size_t>(slot)];
+  const int N = g.n_atoms, H = kH, R = kR, L = st->m.L;
+  const size_t NH = static_cast<size_t>(N) * H;
+  const EdgeGeom eg = edge_geom(g);
+  float* wh = st->wh;
+  float* wm = st->wm;
+  if (st->has_readout) {
+    JANUS_CUDA(cudaMemsetAsync(sl.F, 0, sizeof(float) * 3 * N, s));
+  } else {
+    const Port& in = sl.ports[JANUS_PORT_ADJ_IN];
+    copy(s, wh, port_h(in, N), NH);
+    if (in.has_m) copy(s, wm, port_m(in, N), NH);
+    copy(s, sl.F, port_v(in, N), 3 * static_cast<size_t>(N));
+  }
+  for (int u = st->u1 - 1; u >= st->u0; --u) {
+    UnitBufs& b = sl.units[static_cast<size_t>(u - st->u0)];
+    const float* P = st->P(u);
+    const float* T = st->tw[static_cast<size_t>(u - st->u0)];
+    switch (unit_kind(u, L)) {
+      case kReadout: {  // a_h = (SiLU'(t) omega) O^T
+        const float* om = P + H * H + H;
+        gemm(s, N, b.p, T, nullptr, nullptr, nullptr, wh, node::InDsiluOmega{om});
+        break;
+      }
+      case kUpd: {  // a_m = ((a' V^T) SiLU'(p)) U^T
+        copy(s, b.ff_a, wh, NH);
+        gemm(s, N, wh, T + H * H, nullptr, nullptr, nullptr, st->s1);
+        gemm(s, N, st->s1, T, nullptr, nullptr, nullptr, wm, node::InMulDsilu{b.p, H});
+        break;
+      }
+      case kMsg: {
+        copy(s, b.ff_a, wm, NH);
+        if (g.n_tiles > 0)
+          edge::msg_ff_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::ff_smem<kH, kR>(), s>>>(eg, msg_params(st, u), st->m.r_c, b.v, b.ff_a, b.ff_Y, st->q);
+        else
+          JANUS_CUDA(cudaMemsetAsync(b.ff_Y, 0, sizeof(float) * NH, s));
+        gemm(s, N, b.ff_Y, T + H * H, nullptr, wh, nullptr, wh);  // a_h += Y W^T
+        edge::msg_force_kernel<<<blocks(N, 128), 128, 0, s>>>(eg, st->q, sl.F);
+        break;
+      }
+      case kEmbed:
+        break;
+    }
+    JANUS_LAUNCH_CHECK("stage_ff");
+    (void)R;
+  }
+  if (st->u0 > 0) {
+    const Port& out = sl.ports[JANUS_PORT_ADJ_OUT];
+    copy(s, port_h(out, N), wh, NH);
+    if (out.has_m) copy(s, port_m(out, N), wm, NH);
+    copy(s, port_v(out, N), sl.F, 3 * static_cast<size_t>(N));
+  } else {  // forces complete on stage 0: L_F seed
+    node::force_loss_kernel<<<1, 1024, 0, s>>>(3 * N, sl.F, g.F_target, st->m.w_F, sl.Fbar, sl.loss + 1);
+    JANUS_LAUNCH_CHECK("force_loss");
+  }
+}
+
+// ================================================================== BF
+void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s) {
+  check_mb_slot(st, mb, slot);
+  const DevGeo& g = st->geo[static_cast<size_t>(mb)];
+  Slot& sl = st->slots[static_cast<size_t>(slot)];
+  const int N = g.n_atoms, H = kH, R = kR, L = st->m.L;
+  const size_t NH = static_cast<size_t>(N) * H;
+  const EdgeGeom eg = edge_geom(g);
+  float* ah = st->wh;
+  float* am = st->wm;
+  const float* Fbar = sl.Fbar;
+  JANUS_CUDA(cudaMemsetAsync(st->g2 + static_cast<size_t>(mb) * st->n_params, 0, sizeof(float) * st->n_params, s));
+  if (st->u0 == 0) {
+    JANUS_CUDA(cudaMemsetAsync(ah, 0, sizeof(float) * NH, s));
+  } else {
+    const Port& in = sl.ports[JANUS_PORT_TAN_IN];
+    copy(s, ah, port_h(in, N), NH);
+    if (in.has_m) copy(s, am, port_m(in, N), NH);
+    Fbar = port_v(in, N);
+  }
+  for (int u = st->u0; u < st->u1; ++u) {
+    UnitBufs& b = sl.units[static_cast<size_t>(u - st->u0)];
+    const float* P = st->P(u);
+    const float* T = st->tw[static_cast<size_t>(u - st->u0)];
+    float* G2 = ledger(st, st->g2, mb, u);
+    switch (unit_kind(u, L)) {
+      case kEmbed:
+        break;
+      case kMsg: {
+        const float* W = P + R * H + H + H * H + H;
+        gemm(s, N, ah, W, nullptr, nullptr, nullptr, st->s1);  // vdot
+        if (g.n_tiles > 0) {
+          edge::msg_bf_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::bf_smem<kH, kR>(), s>>>(
+              eg, msg_params(st, u), st->m.r_c, b.v, st->s1, b.ff_a, Fbar, am, st->s2, st->partial);
+          JANUS_LAUNCH_CHECK("msg_bf");
+          edge::reduce_partials_kernel<<<blocks(EC::PE, 256), 256, 0, s>>>(st->partial, g.n_tiles, EC::PE, G2);
+        } else {
+          JANUS_CUDA(cudaMemsetAsync(am, 0, sizeof(float) * NH, s));
+          JANUS_CUDA(cudaMemsetAsync(st->s2, 0, sizeof(float) * NH, s));
+        }
+        gemm(s, N, st->s2, T + H * H, nullptr, nullptr, nullptr, b.inj);                  // hbar^F = X W^T
+        wgrad(s, N, in_h(st, sl, u, N), st->s2, ah, b.ff_Y, G2 + EC::PE);             // dW2 = h^T X + abar^T Y
+        break;
+      }
+      case kUpd: {
+        const float *Um = P, *V = P + H * H + H;
+        float *dU = G2, *dups = G2 + H * H, *dV = G2 + H * H + H;
+        gemm(s, N, am, Um, nullptr, nullptr, nullptr, st->s1);             // pdot
+        gemm(s, N, b.ff_a, T + H * H, nullptr, nullptr, nullptr, st->s2);  // r = a' V^T
+        node::upd_bf_ew_kernel<<<blocks(NH, 256), 256, 0, s>>>(static_cast<int>(NH), st->s2, st->s1, b.p, st->s3,
+                                                               st->s4, st->s5);
+        gemm(s, N, st->s3, T, nullptr, nullptr, nullptr, b.inj);           // mbar^F = pbar U^T
+        wgrad(s, N, st->s5, b.ff_a, nullptr, nullptr, dV);                 // dV2 = u^T a'
+        wgrad(s, N, in_m(st, sl, u, N), st->s3, am, st->s4, dU);           // dU2 = m^T pbar + abar_m^T pdbar
+        colsum(s, N, st->s3, dups);
+        gemm(s, N, st->s5, V, nullptr, ah, nullptr, ah);                   // abar' = abar_h + u V
+        break;
+      }
+      case kReadout: {
+        const float *O = P, *om = P + H * H + H;
+        float *dO = G2, *dob = G2 + H * H, *dom = G2 + H * H + H;
+        gemm(s, N, ah, O, nullptr, nullptr, nullptr, st->s1);  // tdot
+        node::ro_bf_ew_kernel<kH><<<blocks(NH, 256), 256, 0, s>>>(static_cast<int>(NH), st->s1, b.p, om, st->s2,
+                                                                  st->s3, st->s4);
+        gemm(s, N, st->s2, T, nullptr, nullptr, nullptr, b.inj);  // hbar^F = tau O^T
+        colsum(s, N, st->s3, dom);
+        wgrad(s, N, ah, st->s4, in_h(st, sl, u, N), st->s2, dO);
+        colsum(s, N, st->s2, dob);
+        break;
+      }
+    }
+    JANUS_LAUNCH_CHECK("stage_bf");
+  }
+  if (st->u1 < st->U) {
+    const Port& out = sl.ports[JANUS_PORT_TAN_OUT];
+    copy(s, port_h(out, N), ah, NH);
+    if (out.has_m) copy(s, port_m(out, N), am, NH);
+    copy(s, port_v(out, N), Fbar, 3 * static_cast<size_t>(N));
+  }
+}
+
+// ================================================================== BE
+void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s) {
+  check_mb_slot(st, mb, slot);
+  const DevGeo& g = st->geo[static_cast<size_t>(mb)];
+  Slot& sl = st->slots[static_cast<size_t>(slot)];
+  const int N = g.n_atoms, H = kH, R = kR, L = st->m.L;
+  const size_t NH = static_cast<size_t>(N) * H;
+  const EdgeGeom eg = edge_geom(g);
+  float* bh = st->wh;
+  float* bm = st->wm;
+  JANUS_CUDA(cudaMemsetAsync(st->g1 + static_cast<size_t>(mb) * st->n_params, 0, sizeof(float) * st->n_params, s));
+  if (!st->has_readout) {
+    const Port& in = sl.ports[JANUS_PORT_BADJ_IN];
+    copy(s, bh, port_h(in, N), NH);
+    if (in.has_m) copy(s, bm, port_m(in, N), NH);
+  }
+  for (int u = st->u1 - 1; u >= st->u0; --u) {
+    UnitBufs& b = sl.units[static_cast<size_t>(u - st->u0)];
+    const float* P = st->P(u);
+    const float* T = st->tw[static_cast<size_t>(u - st->u0)];
+    float* G1 = ledger(st, st->g1, mb, u);
+    switch (unit_kind(u, L)) {
+      case kReadout: {
+        const float* om = P + H * H + H;
+        float *dO = G1, *dob = G1 + H * H, *dom = G1 + H * H + H, *dbias = G1 + H * H + 2 * H;
+        node::ro_be_ew_kernel<kH><<<blocks(NH, 256), 256, 0, s>>>(static_cast<int>(NH), b.p, om, sl.eps, g.struct_id,
+                                                                  st->s1, st->s2);
+        gemm(s, N, st->s1, T, nullptr, b.inj, nullptr, bh);  // b_h = tbar O^T + hbar^F
+        wgrad(s, N, in_h(st, sl, u, N), st->s1, nullptr, nullptr, dO);
+        colsum(s, N, st->s1, dob);
+        colsum(s, N, st->s2, dom);
+        node::bias_grad_kernel<<<1, 256, 0, s>>>(N, st->m.n_species, g.species, g.struct_id, sl.eps, dbias);
+        break;
+      }
+      case kUpd: {
+        float *dU = G1, *dups = G1 + H * H, *dV = G1 + H * H + H;
+        gemm(s, N, bh, T + H * H, nullptr, nullptr, nullptr, st->s1);  // r = b' V^T
+        node::upd_be_ew_kernel<<<blocks(NH, 256), 256, 0, s>>>(static_cast<int>(NH), st->s1, b.p, st->s2);
+        gemm(s, N, st->s2, T, nullptr, b.inj, nullptr, bm);             // b_m = pbar U^T + mbar^F
+        wgrad(s, N, b.p, bh, nullptr, nullptr, dV, node::InSilu{});      // dV1 = SiLU(p)^T b'
+        wgrad(s, N, in_m(st, sl, u, N), st->s2, nullptr, nullptr, dU);   // dU1 = m^T pbar
+        colsum(s, N, st->s2, dups);
+        break;
+      }
+      case kMsg: {
+        if (g.n_tiles > 0) {
+          edge::msg_be_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::be_smem<kH, kR>(), s>>>(
+              eg, msg_params(st, u), st->m.r_c, b.v, bm, st->s1, st->partial);
+          JANUS_LAUNCH_CHECK("msg_be");
+          edge::reduce_partials_kernel<<<blocks(EC::PE, 256), 256, 0, s>>>(st->partial, g.n_tiles, EC::PE, G1);
+        } else {
+          JANUS_CUDA(cudaMemsetAsync(st->s1, 0, sizeof(float) * NH, s));
+        }
+        wgrad(s, N, in_h(st, sl, u, N), st->s1, nullptr, nullptr, G1 + EC::PE);  // dW1 = h^T Yb
+        gemm(s, N, st->s1, T + H * H, nullptr, bh, b.inj, bh);                 // b_h += Yb W^T + hbar^F
+        break;
+      }
+      case kEmbed:
+        node::embed_be_kernel<kH><<<blocks(st->m.n_species * H, 256), 256, 0, s>>>(N, st->m.n_species, g.species, bh, G1);
+        break;
+    }
+    JANUS_LAUNCH_CHECK("stage_be");
+    (void)R;
+  }
+  if (st->u0 > 0) {
+    const Port& out = sl.ports[JANUS_PORT_BADJ_OUT];
+    copy(s, port_h(out, N), bh, NH);
+    if (out.has_m) copy(s, port_m(out, N), bm, NH);
+  }
+}
+
+// ============================================================ grads / OS
+void stage_reduce_grads(janus_stage* st, cudaStream_t s) {
+  node::ledger_reduce_kernel<<<blocks(st->n_params, 256), 256, 0, s>>>(st->n_params, st->desc.n_micro_batches, st->g1,
+                                                                       st->g2, st->grad);
+  JANUS_LAUNCH_CHECK("ledger_reduce");
+}
+
+void stage_optimizer(janus_stage* st, const janus_opt& o, cudaStream_t s) {
+  ++st->adam_step;
+  const float c1 = 1.0f - std::pow(o.beta1, static_cast<float>(st->adam_step));
+  const float c2 = 1.0f - std::pow(o.beta2, static_cast<float>(st->adam_step));
+  node::adam_kernel<<<blocks(st->n_params, 256), 256, 0, s>>>(st->n_params, st->params, st->m1, st->m2, st->grad, o.lr,
+                                                              o.beta1, o.beta2, o.eps, c1, c2);
+  JANUS_LAUNCH_CHECK("adam");
+  refresh_transposes(st, s);
+}
+
+void stage_port(janus_stage* st, int mb, int slot, int port, void** dptr, size_t* bytes) {
+  if (port < 0 || port > 7) throw domain_error("bad port");
+  if (slot < 0 || slot >= st->desc.n_slots) throw domain_error("slot index out of range");
+  if (mb < 0 || mb >= st->desc.n_micro_batches) throw domain_error("micro-batch index out of range");
+  const Port& p = st->slots[static_cast<size_t>(slot)].ports[port];
+  if (!p.buf) {
+    *dptr = nullptr;
+    *bytes = 0;
+    return;
+  }
+  *dptr = p.buf;
+  *bytes = port_elems(st, port, st->geo[static_cast<size_t>(mb)].n_atoms) * sizeof(float);
+}
+
+// ============================================================ read-back
+int stage_slot_of_mb(const janus_stage* st, int mb) {
+  for (size_t x = 0; x < st->slots.size(); ++x)
+    if (st->slots[x].mb == mb) return static_cast<int>(x);
+  throw state_error("micro-batch has no live slot (FE not run)");
+}
+
+void stage_energy(janus_stage* st, int mb, float* E_host, float* loss_E, cudaStream_t s) {
+  if (!st->has_readout) throw state_error("energies live on the stage holding the readout unit");
+  const Slot& sl = st->slots[static_cast<size_t>(stage_slot_of_mb(st, mb))];
+  const int ns = st->geo[static_cast<size_t>(mb)].n_struct;
+  if (E_host) JANUS_CUDA(cudaMemcpyAsync(E_host, sl.E, sizeof(float) * ns, cudaMemcpyDeviceToHost, s));
+  if (loss_E) JANUS_CUDA(cudaMemcpyAsync(loss_E, sl.loss, sizeof(float), cudaMemcpyDeviceToHost, s));
+  JANUS_CUDA(cudaStreamSynchronize(s));
+}
+
+void stage_forces(janus_stage* st, int mb, float* F_host, float* loss_F, cudaStream_t s) {
+  if (!st->has_embed) throw state_error("complete forces live on stage 0");
+  const Slot& sl = st->slots[static_cast<size_t>(stage_slot_of_mb(st, mb))];
+  const int n = st->geo[static_cast<size_t>(mb)].n_atoms;
+  if (F_host) JANUS_CUDA(cudaMemcpyAsync(F_host, sl.F, sizeof(float) * 3 * n, cudaMemcpyDeviceToHost, s));
+  if (loss_F) JANUS_CUDA(cudaMemcpyAsync(loss_F, sl.loss + 1, sizeof(float), cudaMemcpyDeviceToHost, s));
+  JANUS_CUDA(cudaStreamSynchronize(s));
+}
+
+void stage_grads(janus_stage* st, int which, int mb, float* host_out, cudaStream_t s) {
+  if (which < 0 || which > 2) throw domain_error("which must be 0, 1 or 2");
+  const size_t NP = static_cast<size_t>(st->n_params), NMB = static_cast<size_t>(st->desc.n_micro_batches);
+  std::vector<float> a(NP * NMB), b(NP * NMB);
+  JANUS_CUDA(cudaMemcpyAsync(a.data(), st->g1, sizeof(float) * NP * NMB, cudaMemcpyDeviceToHost, s));
+  JANUS_CUDA(cudaMemcpyAsync(b.data(), st->g2, sizeof(float) * NP * NMB, cudaMemcpyDeviceToHost, s));
+  JANUS_CUDA(cudaStreamSynchronize(s));
+  const size_t m0 = mb < 0 ? 0 : static_cast<size_t>(mb), m1 = mb < 0 ? NMB : static_cast<size_t>(mb) + 1;
+  if (mb >= static_cast<int>(NMB)) throw domain_error("micro-batch index out of range");
+  for (size_t x = 0; x < NP; ++x) {
+    float acc = 0.f;  // same order as ledger_reduce_kernel
+    for (size_t m = m0; m < m1; ++m) {
+      if (which != 2) acc += a[m * NP + x];
+      if (which != 1) acc += b[m * NP + x];
+    }
+    host_out[x] = acc;
+  }
+}
+
+void stage_params(janus_stage* st, float* host_out, cudaStream_t s) {
+  JANUS_CUDA(cudaMemcpyAsync(host_out, st->params, sizeof(float) * st->n_params, cudaMemcpyDeviceToHost, s));
+  JANUS_CUDA(cudaStreamSynchronize(s));
+}
+
+int64_t stage_param_count(const janus_stage* st) { return st->n_params; }
+
+void stage_grad_buffer(janus_stage* st, float** dptr, int64_t* count) {
+  *dptr = st->grad;
+  *count = st->n_params;
+}
+
+void stage_memory(const janus_stage* st, int64_t* static_bytes, int64_t* arena_bytes) {
+  if (static_bytes) *static_bytes = st->static_bytes;
+  if (arena_bytes) *arena_bytes = st->arena_bytes;
+}
+
+}  // namespace janus

@@ -1,0 +1,88 @@
+// stage.cuh — janus_stage: one pipeline stage (a contiguous unit range) on
+// one GPU.  Owns the parameter slice, Adam state, per-micro-batch gradient
+// ledgers (BE merged-first-order g1 / BF second-order g2, Eq. (2)), the
+// per-micro-batch geometry, and per-slot activation storage + mailboxes.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/janus_cuda.h"
+
+namespace janus {
+
+enum UnitKind { kEmbed = 0, kMsg = 1, kUpd = 2, kReadout = 3 };
+
+inline UnitKind unit_kind(int u, int L) {
+  if (u == 0) return kEmbed;
+  if (u == 2 * L + 1) return kReadout;
+  return (u % 2 == 1) ? kMsg : kUpd;
+}
+
+int64_t unit_param_count(const janus_model_desc& m, int u);
+int64_t unit_param_offset(const janus_model_desc& m, int u);
+
+struct DevGeo {
+  int n_atoms = 0, n_edges = 0, n_struct = 0, n_tiles = 0;
+  int *row_ptr = nullptr, *col = nullptr, *src = nullptr, *rev = nullptr, *tile_row = nullptr, *shift = nullptr;
+  int *species = nullptr, *struct_id = nullptr, *struct_ptr = nullptr;
+  double *pos = nullptr, *cell = nullptr;
+  float *d = nullptr, *u = nullptr, *c = nullptr, *dc = nullptr, *E_target = nullptr, *F_target = nullptr;
+};
+
+struct UnitBufs {  // per slot, per unit
+  float* out_h = nullptr;  // embed / upd output h
+  float* out_m = nullptr;  // msg output m
+  float* v = nullptr;      // msg: h W
+  float* p = nullptr;      // upd: m U + ups ; readout: t
+  float* ff_a = nullptr;   // upd: FF input a' ; msg: FF input a_m
+  float* ff_Y = nullptr;   // msg: Y
+  float* inj = nullptr;    // BF -> BE injection at the unit input (h for msg/readout, m for upd)
+  const float* in_h = nullptr;  // where this unit's input h lives (static)
+  const float* in_m = nullptr;  // upd: input m
+};
+
+struct Port {
+  float* buf = nullptr;  // [h | m | vec3] packed for the actual n_atoms
+  bool has_m = false, has_vec = false;
+};
+
+struct Slot {
+  std::vector<UnitBufs> units;
+  Port ports[8];
+  float* F = nullptr;      // running force [N*3]
+  float* Fbar = nullptr;   // stage 0: force-loss seed
+  float* e_atom = nullptr; // readout per-atom energies
+  float* E = nullptr;      // [n_struct]
+  float* eps = nullptr;    // [n_struct]
+  float* loss = nullptr;   // [2] loss_E, loss_F
+  int mb = -1;
+};
+
+}  // namespace janus
+
+struct janus_stage {
+  janus_stage_desc desc{};
+  janus_model_desc m{};
+  int u0 = 0, u1 = 0, U = 0;
+  bool has_embed = false, has_readout = false, in_has_m = false, out_has_m = false;
+  int64_t n_params = 0;
+  std::vector<int64_t> uoff;  // unit -> offset within the stage slice
+  float *params = nullptr, *grad = nullptr, *m1 = nullptr, *m2 = nullptr;
+  float *g1 = nullptr, *g2 = nullptr;  // [n_mb][n_params]
+  std::vector<float*> tw;              // per unit: transposed weights block
+  int adam_step = 0;
+  std::vector<janus::DevGeo> geo;
+  std::vector<janus::Slot> slots;
+  // scratch
+  float *wh = nullptr, *wm = nullptr, *s1 = nullptr, *s2 = nullptr, *s3 = nullptr, *s4 = nullptr, *s5 = nullptr;
+  float *q = nullptr, *partial = nullptr, *zero = nullptr;
+  std::vector<void*> allocs;
+  int64_t static_bytes = 0, arena_bytes = 0;
+
+  float* P(int u) const { return params + uoff[static_cast<size_t>(u - u0)]; }
+
+};

@@ -1,0 +1,31 @@
+// stage_api.hpp — C++ entry points of stage.cu used by the C ABI and executor.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "../../include/janus_cuda.h"
+
+namespace janus {
+
+janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params);
+void stage_destroy(janus_stage* st);
+void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_t s);
+void stage_fe(janus_stage* st, int mb, int slot, cudaStream_t s);
+void stage_ff(janus_stage* st, int mb, int slot, cudaStream_t s);
+void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s);
+void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s);
+void stage_reduce_grads(janus_stage* st, cudaStream_t s);
+void stage_optimizer(janus_stage* st, const janus_opt& o, cudaStream_t s);
+void stage_port(janus_stage* st, int mb, int slot, int port, void** dptr, size_t* bytes);
+
+// read-back helpers (synchronous on the stream)
+void stage_energy(janus_stage* st, int mb, float* E_host, float* loss_E, cudaStream_t s);
+void stage_forces(janus_stage* st, int mb, float* F_host, float* loss_F, cudaStream_t s);
+void stage_grads(janus_stage* st, int which, int mb, float* host_out, cudaStream_t s);
+void stage_params(janus_stage* st, float* host_out, cudaStream_t s);
+int64_t stage_param_count(const janus_stage* st);
+void stage_grad_buffer(janus_stage* st, float** dptr, int64_t* count);
+void stage_memory(const janus_stage* st, int64_t* static_bytes, int64_t* arena_bytes);
+int stage_slot_of_mb(const janus_stage* st, int mb);
+
+}  // namespace janus
