@@ -1,0 +1,328 @@
+#!/usr/bin/env python3
+"""bench.py — four-phase (FE/FF/BF/BE) training step of the canonical
+conservative MLIP under the JanusPipe schedules, on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1]): L=4 interaction layers, H=64, R=64,
+r_c=5 A, synthetic periodic 256-atom fcc cells (rho 0.095 /A^3, ~50
+neighbours), 32 micro-batches of one cell each.  N=1 runs the whole model on
+one GPU (P=1, SymFold == WaveK); N>1 pipelines it over N GPUs (P=N stages,
+WaveK k=2P; NCCL P2P over NVLink), strong scaling (total work fixed).
+Metric: structures/s (whole job).  "value" is device-timed (CUDA events, max
+over ranks) with inputs resident in HBM and an L2 flush (512 MiB memset)
+between timed steps; "e2e" re-uploads every micro-batch from pinned host
+memory through the trainer API (janus_trainer_load) and reads the loss back,
+timed on the host around load+step.
+--impl reference times the reference's CPU path: the reference has no numeric
+implementation, so it is the fp64 C oracle restatement
+(oracle/mlip_oracle.c), one structure per thread on all host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIG = dict(L=4, H=64, R=64, r_c=5.0, atoms=256, rho=0.095, n_mb=32, seed=7)
+METRIC = "structures/sec"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.proc, self.lines = gpu, None, []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------- helpers
+def pin(arrays):
+    """cudaHostRegister host arrays so the e2e H2D copies come from pinned memory."""
+    import paper_2605_18404_b200 as J
+    rt = J.cudart()
+    rt.cudaHostRegister.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_uint]
+    for a in arrays:
+        if a.nbytes:
+            rt.cudaHostRegister(a.ctypes.data, a.nbytes, 0)
+
+
+def flush_l2(buf_holder):
+    import paper_2605_18404_b200 as J
+    rt = J.cudart()
+    if not buf_holder:
+        p = ctypes.c_void_p()
+        rt.cudaMalloc.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+        assert rt.cudaMalloc(ctypes.byref(p), 512 << 20) == 0
+        buf_holder.append(p.value)
+    rt.cudaMemset.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t]
+    rt.cudaMemset(buf_holder[0], 1, 512 << 20)
+    rt.cudaDeviceSynchronize()
+
+
+def batch_bytes(b):
+    return sum(a.nbytes for a in (b.pos, b.species, b.struct_id, b.cell, b.E_target, b.F_target, b.row_ptr, b.col,
+                                  b.shift, b.rev))
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
+    except (OSError, ValueError):
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+# ------------------------------------------------------------ CPU oracle
+class CpuOracle:
+    """The fp64 C oracle (test infrastructure) timed on host threads, one
+    structure (full four-phase step) per call; ctypes releases the GIL."""
+
+    def __init__(self, model_kw, batches, params):
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle as O
+        self.O, self.om, self.params = O, O.Model(**model_kw), params
+        self.work = []
+        for b in batches:
+            ob = O.Batch(b.pos, b.species, b.struct_id, b.cell, b.E_target.astype(float), b.F_target.astype(float))
+            self.work.append((ob, O.build_nbrlist(self.om, ob)))
+
+    def run(self, threads, per_thread=1):
+        """Return structures/s over `threads` x `per_thread` structures."""
+        def worker(k):
+            for i in range(per_thread):
+                ob, nl = self.work[(k + i * threads) % len(self.work)]
+                self.O.step(self.om, ob, nl, self.params)
+
+        ts = [threading.Thread(target=worker, args=(k,)) for k in range(threads)]
+        t0 = time.perf_counter()
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        return threads * per_thread / (time.perf_counter() - t0)
+
+
+# ------------------------------------------------------------------ main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--method", default=None, choices=[None, "symfold", "wavek", "onef1b"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank, world, local_rank = dist_env()
+    N = args.gpus
+    if args.warmup < 3:
+        args.warmup = 3
+
+    import paper_2605_18404_b200 as J
+
+    model = J.Model(L=CONFIG["L"], H=CONFIG["H"], R=CONFIG["R"], r_c=CONFIG["r_c"])
+    params = model.synth_params(CONFIG["seed"])
+    n_mb = CONFIG["n_mb"]
+    batches = [J.synth_batch(model, [CONFIG["atoms"]], CONFIG["rho"], CONFIG["seed"] * 100 + m) for m in range(n_mb)]
+    cfg = {"workload": "configs[1]: L=4 H=64 R=64 r_c=5, 256-atom periodic cells, 32 micro-batches",
+           "model": "canonical conservative MLIP (SURVEY.md App. A), random-init", "global_batch": n_mb,
+           "atoms_per_structure": CONFIG["atoms"], "edges_per_structure": batches[0].n_edges,
+           "n_micro_batches": n_mb, "l2": "flushed (512 MiB memset) between timed steps"}
+    model_kw = dict(L=model.L, H=model.H, R=model.R, n_species=model.n_species, r_c=model.r_c, w_E=model.w_E,
+                    w_F=model.w_F)
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        threads = os.cpu_count() or 1
+        cpu = CpuOracle(model_kw, batches[:threads], params.astype(float))
+        vals = []
+        for i in range(args.warmup + args.steps):
+            v = cpu.run(threads)
+            if i >= args.warmup:
+                vals.append(v)
+        val = statistics.median(vals)
+        sample = f"{threads} structures per step (one 256-atom cell per thread, full FE+FF+BF+BE step)"
+        out = {"impl": "reference", "metric": METRIC, "value": val, "unit": "structures/s", "n_gpus": N,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * n_mb / val,
+               "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+               "data": "synthetic", "config": cfg,
+               "cpu_baseline": {"value": val, "unit": "structures/s", "cores": threads, "kind": "port",
+                                "sample": sample},
+               "e2e": {"value": val, "unit": "structures/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+               "note": "reference has no numeric path (SPEC.md:15); its CPU restatement is the fp64 oracle"}
+        print(json.dumps(out), flush=True)
+        return
+
+    # ---------------------------------------------------------------- ours
+    comm = None
+    if N > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo", init_method="env://")
+        uid = J.Comm.unique_id() if rank == 0 else None
+        obj = [uid]
+        dist.broadcast_object_list(obj, src=0)
+        comm = J.Comm(obj[0], world, rank, local_rank)
+    method_name = args.method or ("wavek" if N > 1 else "symfold")
+    method = {"symfold": J.METHOD_SYMFOLD, "wavek": J.METHOD_WAVEK, "onef1b": J.METHOD_ONEF1B}[method_name]
+    P = N
+    k = min(n_mb, 2 * P)
+    max_edges = max(b.n_edges for b in batches) + 64
+    tr = J.Trainer(model, params, P, method, n_mb, k=k, max_atoms=CONFIG["atoms"], max_edges=max_edges,
+                   max_struct=1, local=(N == 1), graphs=(N == 1), comm=comm, rank=rank, device=local_rank)
+    for m, b in enumerate(batches):
+        tr.load(m, b)
+    for _ in range(args.warmup):
+        tr.step()
+
+    def barrier():
+        if N > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    l2 = []
+    times, launches, stats = [], 0, None
+    with ClockSampler(local_rank) as clk:
+        for _ in range(args.steps):
+            flush_l2(l2)
+            barrier()
+            s = tr.step()
+            times.append(s.makespan_ms)
+            launches += s.kernel_launches
+            stats = s
+        # e2e: re-upload every micro-batch from pinned host memory + read the loss back
+        pin([a for b in batches for a in (b.pos, b.species, b.struct_id, b.cell, b.E_target, b.F_target,
+                                          b.row_ptr, b.col, b.shift, b.rev)])
+        e2e_t = []
+        for _ in range(max(3, args.steps // 2)):
+            barrier()
+            t0 = time.perf_counter()
+            for m, b in enumerate(batches):
+                tr.load(m, b)
+            tr.step()  # synchronises and reads the loss back (D2H)
+            e2e_t.append(time.perf_counter() - t0)
+    clocks = clk.summary()
+    total_ms = sum(times)
+    if N > 1:
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor([total_ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t[0])
+        e = torch.tensor([max(e2e_t)], dtype=torch.float64)
+        dist.all_reduce(e, op=dist.ReduceOp.MAX)
+        e2e_max = float(e[0])
+    else:
+        e2e_max = None
+    ms_per_step = total_ms / args.steps
+    value = n_mb / (ms_per_step / 1000.0)
+    e2e_val = n_mb / (statistics.median(e2e_t) if e2e_max is None else e2e_max)
+    h2d = sum(batch_bytes(b) for b in batches) // max(1, 1 if N == 1 else 1)
+
+    # roofline of the dominant kernel (msg BF edge kernel) on the first stage holding a msg unit
+    peaks, peak_src = load_peaks()
+    roof = None
+    if rank == 0:
+        st = tr.stage(0 if P == 1 else min(1, P - 1))
+        try:
+            ms_bf, ne, fl = st.time_edge_kernel(2, 0, iters=50)
+            achieved = fl / (ms_bf * 1e-3) / 1e12
+            roof = {"kernel": "msg_bf_kernel (SIMT fp32)", "bound": "tensor", "achieved": achieved,
+                    "peak": peaks["bf16_tflops"], "unit": "TFLOP/s", "frac": achieved / peaks["bf16_tflops"],
+                    "traffic": None, "peak_source": f"{peak_src} bf16 dense (MEASURED_PEAKS.json)",
+                    "launch_ms": ms_bf, "edges_per_launch": ne, "flops_per_launch": fl,
+                    "fp32_simt_nominal_tflops": 74.4}
+            fe = st.time_edge_kernel(0, 0, iters=50)
+            roof["fe_kernel_tflops"] = fe[2] / (fe[0] * 1e-3) / 1e12
+        except J.JanusError as ex:
+            roof = {"error": str(ex)}
+
+    cpu = None
+    if rank == 0 and N == 1 and not args.no_cpu_baseline:
+        v = CpuOracle(model_kw, batches[:2], params.astype(float)).run(1, per_thread=2)
+        cpu = {"value": v, "unit": "structures/s", "cores": 1, "kind": "port",
+               "sample": "2 x 256-atom structures, full four-phase step, fp64 oracle, 1 thread"}
+
+    if rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": "structures/s", "n_gpus": N, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+               "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+               "config": dict(cfg, parallelism=f"pp{P}" if P > 1 else "single-gpu", schedule=method_name,
+                              wavek_k=k if method == J.METHOD_WAVEK else None, cuda_graph=(N == 1)),
+               "e2e": {"value": e2e_val, "unit": "structures/s", "h2d_bytes_per_step": h2d,
+                       "d2h_bytes_per_step": 8 * n_mb},
+               "gpu_launches": int(launches), "gpu_launches_per_step": int(stats.kernel_launches),
+               "roofline": roof, "cpu_baseline": cpu, "clocks": clocks,
+               "p2p_bytes_per_step": int(stats.p2p_bytes), "loss": stats.loss,
+               "peak_hbm_bytes_per_stage": [int(stats.peak_bytes[d]) for d in range(P)]}
+        print(json.dumps(out), flush=True)
+    tr.close()
+    if comm:
+        comm.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -127,6 +127,13 @@ int64_t janus_stage_param_count(janus_stage* st);
 int janus_stage_reduce_grads(janus_stage* st, void* stream);
 int janus_stage_grad_buffer(janus_stage* st, float** dptr, int64_t* count);
 int janus_stage_optimizer_step(janus_stage* st, const janus_opt* opt, void* stream);
+/* Time one edge kernel of the stage's first msg unit in isolation (CUDA
+ * events on `stream`, back-to-back launches after one warm-up): which = 0 FE,
+ * 1 FF, 2 BF, 3 BE.  Requires the phase's inputs to exist (run the step once
+ * first).  Returns the mean launch time, the launch's edge count and
+ * algorithmic FLOPs (DESIGN.md §4 per-edge counts). */
+int janus_stage_time_edge_kernel(janus_stage* st, int which, int mb, int slot, int iters, void* stream,
+                                 float* avg_ms, int64_t* edges, double* flops);
 /* Peak device bytes held by the stage (static + activation arena). */
 int janus_stage_memory(janus_stage* st, int64_t* static_bytes, int64_t* arena_bytes);
 
@@ -141,26 +148,44 @@ int janus_comm_group_start(void);
 int janus_comm_group_end(void);
 int janus_comm_allreduce_sum(janus_comm* c, float* buf, int64_t count, void* stream);
 
-/* ---- whole-step executor (C++ train_step behind a C entry) ---- */
+/* ---- whole-step executor (C++ train_step behind a C entry) ----
+ * Walks Schedule::device_lists[d] (ir.hpp:147) in seq order (the sole
+ * intra-device order, ir.hpp:131) and executes every instruction.  Local mode
+ * runs all P stages in this process on one GPU with one stream set per
+ * virtual device and device-to-device copies as the transport; NCCL mode runs
+ * the stage(s) of rank r over janus_comm (P2P per flow + allreduce). */
 typedef struct {
-  int32_t n_stages;            /* P */
-  int32_t method;              /* 0 SymFold, 1 WaveK, 2 1F1B-2nd */
+  int32_t n_stages;        /* P */
+  int32_t method;          /* 0 SymFold, 1 WaveK, 2 1F1B-2nd */
   int32_t wavek_k;
-  int32_t n_micro_batches;
-  int32_t local_stages;        /* 1 = all P stages in this process on one GPU (fake transport) */
-  int32_t use_graphs;          /* capture each device list in a CUDA graph */
+  int32_t n_micro_batches; /* per replica */
+  int32_t local_stages;    /* 1 = all P stages in this process on one GPU */
+  int32_t use_graphs;      /* capture the step once as a CUDA graph, replay it */
+  int32_t dp_degree;       /* data-parallel replicas (NCCL mode), >= 1 */
+  int32_t record_timeline; /* per-instruction CUDA events (disables graphs) */
 } janus_exec_desc;
+
+typedef struct {
+  double makespan_ms;      /* device time of the last step (anchor -> end) */
+  double bubble_ratio;     /* sum idle / (P makespan), SPEC.md:436 (timeline only) */
+  double busy_ms[64];      /* per (virtual) device compute time (timeline only) */
+  int64_t p2p_bytes;       /* bytes moved between stages in the last step */
+  int64_t kernel_launches; /* kernels issued by the last step */
+  int64_t peak_bytes[64];  /* per device: static + arena bytes of its stages */
+  double loss;             /* sum of loss_E + loss_F held by this process */
+} janus_step_stats;
 
 typedef struct janus_trainer janus_trainer;
 int janus_trainer_create(const janus_exec_desc* ed, const janus_stage_desc* sd, const float* all_params,
                          janus_comm* comm, int rank, janus_trainer** out);
 int janus_trainer_destroy(janus_trainer* t);
 int janus_trainer_load(janus_trainer* t, int mb, const janus_host_batch* hb);
-int janus_trainer_step(janus_trainer* t, const janus_opt* opt, double* loss_out);
-/* per-instruction device timeline of the last step: [n][4] = device, kind, start_us, end_us */
+int janus_trainer_step(janus_trainer* t, const janus_opt* opt, janus_step_stats* stats);
+/* per compute instruction of the last timed step: [n][5] = device, kind, mb, start_us, end_us */
 int janus_trainer_timeline(janus_trainer* t, double* out, int32_t cap, int32_t* n);
-int janus_trainer_stage(janus_trainer* t, int stage, janus_stage** out);
+int janus_trainer_stage(janus_trainer* t, int block, int force_replica, janus_stage** out);
 int janus_trainer_schedule_text(janus_trainer* t, char* buf, int64_t cap, int64_t* len);
+int janus_trainer_plan(janus_trainer* t, int32_t* unit_ranges /* [P][2] */);
 
 /* ---- schedule generation (host only) ---- */
 int janus_schedule_generate(int method, int P, int n_mb, int k, char* buf, int64_t cap, int64_t* len);

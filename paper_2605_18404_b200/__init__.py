@@ -55,10 +55,6 @@ class Opt(ctypes.Structure):
     _fields_ = [("lr", c_f), ("beta1", c_f), ("beta2", c_f), ("eps", c_f)]
 
 
-class ExecDesc(ctypes.Structure):
-    _fields_ = [("n_stages", ctypes.c_int32), ("method", ctypes.c_int32), ("wavek_k", ctypes.c_int32),
-                ("n_micro_batches", ctypes.c_int32), ("local_stages", ctypes.c_int32), ("use_graphs", ctypes.c_int32)]
-
 
 def _sig(name, res, *args):
     f = getattr(_lib, name)
@@ -91,6 +87,7 @@ _sig("janus_stage_param_count", c_i64, c_vp)
 _sig("janus_stage_reduce_grads", c_int, c_vp, c_vp)
 _sig("janus_stage_optimizer_step", c_int, c_vp, c_vp, c_vp)
 _sig("janus_stage_memory", c_int, c_vp, c_vp, c_vp)
+_sig("janus_stage_time_edge_kernel", c_int, c_vp, c_int, c_int, c_int, c_int, c_vp, c_vp, c_vp, c_vp)
 _sig("janus_schedule_generate", c_int, c_int, c_int, c_int, c_int, c_vp, c_i64, c_vp)
 _sig("janus_schedule_validate", c_int, ctypes.c_char_p, c_vp)
 
@@ -298,6 +295,13 @@ class Stage:
         o = Opt(lr, beta1, beta2, eps)
         check(_lib.janus_stage_optimizer_step(self.h, ctypes.byref(o), stream))
 
+    def time_edge_kernel(self, which: int, mb: int = 0, slot: int | None = None, iters: int = 20):
+        """Mean launch time (ms), edges and algorithmic FLOPs of one msg edge kernel."""
+        ms, ne, fl = c_f(), c_i64(), c_d()
+        check(_lib.janus_stage_time_edge_kernel(self.h, which, mb, mb if slot is None else slot, iters, None,
+                                                ctypes.byref(ms), ctypes.byref(ne), ctypes.byref(fl)))
+        return ms.value, ne.value, fl.value
+
     def memory(self):
         a, b = c_i64(), c_i64()
         check(_lib.janus_stage_memory(self.h, ctypes.byref(a), ctypes.byref(b)))
@@ -350,3 +354,130 @@ def d2d(dst: int, src: int, nbytes: int) -> None:
     rc = cudart().cudaMemcpy(dst, src, nbytes, 3)  # cudaMemcpyDeviceToDevice
     if rc != 0:
         raise RuntimeError(f"cudaMemcpy failed: {rc}")
+
+
+# ------------------------------------------------------------------ trainer
+class StepStats(ctypes.Structure):
+    _fields_ = [("makespan_ms", c_d), ("bubble_ratio", c_d), ("busy_ms", c_d * 64), ("p2p_bytes", c_i64),
+                ("kernel_launches", c_i64), ("peak_bytes", c_i64 * 64), ("loss", c_d)]
+
+
+class ExecDesc(ctypes.Structure):
+    _fields_ = [("n_stages", ctypes.c_int32), ("method", ctypes.c_int32), ("wavek_k", ctypes.c_int32),
+                ("n_micro_batches", ctypes.c_int32), ("local_stages", ctypes.c_int32), ("use_graphs", ctypes.c_int32),
+                ("dp_degree", ctypes.c_int32), ("record_timeline", ctypes.c_int32)]
+
+
+_sig("janus_trainer_create", c_int, c_vp, c_vp, c_vp, c_vp, c_int, c_vp)
+_sig("janus_trainer_destroy", c_int, c_vp)
+_sig("janus_trainer_load", c_int, c_vp, c_int, c_vp)
+_sig("janus_trainer_step", c_int, c_vp, c_vp, c_vp)
+_sig("janus_trainer_timeline", c_int, c_vp, c_vp, ctypes.c_int32, c_vp)
+_sig("janus_trainer_stage", c_int, c_vp, c_int, c_int, c_vp)
+_sig("janus_trainer_schedule_text", c_int, c_vp, c_vp, c_i64, c_vp)
+_sig("janus_trainer_plan", c_int, c_vp, c_vp)
+_sig("janus_nccl_unique_id", c_int, c_vp)
+_sig("janus_comm_init_nccl", c_int, c_vp, c_int, c_int, c_int, c_vp)
+_sig("janus_comm_destroy", c_int, c_vp)
+
+
+class _StageView(Stage):
+    """Non-owning view of a stage held by a trainer."""
+
+    def __init__(self, model, handle, u0, u1):  # no super().__init__: the trainer owns it
+        self.model, self.h, self.u0, self.u1 = model, handle, u0, u1
+
+    def close(self):
+        self.h = None
+
+
+class Comm:
+    """NCCL communicator (one per process; rank r holds pipeline device r % P)."""
+
+    def __init__(self, uid: bytes, nranks: int, rank: int, device: int):
+        h = c_vp()
+        buf = ctypes.create_string_buffer(uid, 128)
+        check(_lib.janus_comm_init_nccl(buf, nranks, rank, device, ctypes.byref(h)))
+        self.h = h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        check(_lib.janus_nccl_unique_id(buf))
+        return buf.raw
+
+    def close(self):
+        if self.h:
+            check(_lib.janus_comm_destroy(self.h))
+            self.h = None
+
+
+class Trainer:
+    """janus_trainer: executes a SymFold / WaveK / 1F1B-2nd schedule (C++)."""
+
+    def __init__(self, model: Model, params: np.ndarray, P: int, method: int, n_mb: int, k: int = 1,
+                 max_atoms: int = 256, max_edges: int = 256 * 120, max_struct: int = 8, local: bool = True,
+                 graphs: bool = False, timeline: bool = False, dp: int = 1, comm: "Comm | None" = None,
+                 rank: int = 0, device: int = 0):
+        self.model, self.P, self.n_mb = model, P, n_mb
+        self.ed = ExecDesc(P, method, k, n_mb, 1 if local else 0, 1 if graphs else 0, dp, 1 if timeline else 0)
+        self.sd = StageDesc(model.desc(), 0, model.n_units, max_atoms, max_edges, max_struct, n_mb, n_mb, device)
+        p = np.ascontiguousarray(params, np.float32)
+        h = c_vp()
+        check(_lib.janus_trainer_create(ctypes.byref(self.ed), ctypes.byref(self.sd), _p(p),
+                                        comm.h if comm else None, rank, ctypes.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            check(_lib.janus_trainer_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def load(self, mb: int, batch: Batch):
+        hb = batch.c()
+        check(_lib.janus_trainer_load(self.h, mb, ctypes.byref(hb)))
+
+    def step(self, lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8) -> StepStats:
+        o = Opt(lr, beta1, beta2, eps)
+        s = StepStats()
+        check(_lib.janus_trainer_step(self.h, ctypes.byref(o), ctypes.byref(s)))
+        return s
+
+    def timeline(self):
+        n = ctypes.c_int32()
+        check(_lib.janus_trainer_timeline(self.h, None, 0, ctypes.byref(n)))
+        out = np.zeros((max(n.value, 1), 5))
+        check(_lib.janus_trainer_timeline(self.h, _p(out), n.value, ctypes.byref(n)))
+        return out[:n.value]
+
+    def plan(self):
+        out = np.zeros((self.P, 2), np.int32)
+        check(_lib.janus_trainer_plan(self.h, _p(out)))
+        return out
+
+    def stage(self, block: int, force_replica: bool = False) -> Stage:
+        h = c_vp()
+        check(_lib.janus_trainer_stage(self.h, block, 1 if force_replica else 0, ctypes.byref(h)))
+        u0, u1 = self.plan()[block]
+        return _StageView(self.model, h, int(u0), int(u1))
+
+    def schedule_text(self) -> str:
+        n = c_i64()
+        check(_lib.janus_trainer_schedule_text(self.h, None, 0, ctypes.byref(n)))
+        buf = ctypes.create_string_buffer(n.value + 1)
+        check(_lib.janus_trainer_schedule_text(self.h, buf, n.value + 1, ctypes.byref(n)))
+        return buf.value.decode()
+
+    def params(self) -> np.ndarray:
+        """Full parameter vector gathered from the energy copies."""
+        return np.concatenate([self.stage(b).params() for b in range(self.P)])
+
+    def grads(self, which=0) -> np.ndarray:
+        """Per-micro-batch-ledger sums (energy copies; 1F1B force replicas hold the rest)."""
+        return np.concatenate([self.stage(b).grads(which, -1) for b in range(self.P)])

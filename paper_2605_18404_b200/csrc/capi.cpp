@@ -12,6 +12,7 @@
 #include "../../include/janus/schedule_gen.hpp"
 #include "../../include/janus_cuda.h"
 #include "cuda_check.hpp"
+#include "executor.hpp"
 #include "host.hpp"
 #include "stage_api.hpp"
 
@@ -43,6 +44,9 @@ int guard(F&& f) {
   } catch (const janus::cuda_error& e) {
     g_last_error = e.what();
     return janus::kCudaError;
+  } catch (const janus::nccl_error& e) {
+    g_last_error = e.what();
+    return janus::kNcclError;
   } catch (const std::bad_alloc&) {
     g_last_error = "out of host memory";
     return janus::kOutOfMemory;
@@ -208,8 +212,119 @@ int janus_stage_optimizer_step(janus_stage* st, const janus_opt* opt, void* stre
     janus::stage_optimizer(st, *opt, S(stream));
   });
 }
+int janus_stage_time_edge_kernel(janus_stage* st, int which, int mb, int slot, int iters, void* stream,
+                                 float* avg_ms, int64_t* edges, double* flops) {
+  return guard([&] {
+    need(st, "stage");
+    need(avg_ms, "avg_ms");
+    need(edges, "edges");
+    need(flops, "flops");
+    janus::stage_time_edge_kernel(st, which, mb, slot, iters, S(stream), avg_ms, edges, flops);
+  });
+}
 int janus_stage_memory(janus_stage* st, int64_t* static_bytes, int64_t* arena_bytes) {
   return guard([&] { need(st, "stage"); janus::stage_memory(st, static_bytes, arena_bytes); });
+}
+
+// -------------------------------------------------------------- transports
+int janus_nccl_unique_id(void* id_out) {
+  return guard([&] {
+    need(id_out, "id_out");
+    janus::nccl_unique_id(id_out);
+  });
+}
+int janus_comm_init_nccl(const void* id, int nranks, int rank, int device, janus_comm** out) {
+  return guard([&] {
+    need(id, "id");
+    need(out, "out");
+    *out = nullptr;
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw janus::domain_error("bad rank / nranks");
+    *out = janus::comm_init_nccl(id, nranks, rank, device);
+  });
+}
+int janus_comm_destroy(janus_comm* c) {
+  return guard([&] { janus::comm_destroy(c); });
+}
+int janus_comm_send(janus_comm* c, const void* buf, size_t bytes, int peer, void* stream) {
+  return guard([&] { need(c, "comm"); janus::comm_send(c, buf, bytes, peer, S(stream)); });
+}
+int janus_comm_recv(janus_comm* c, void* buf, size_t bytes, int peer, void* stream) {
+  return guard([&] { need(c, "comm"); janus::comm_recv(c, buf, bytes, peer, S(stream)); });
+}
+int janus_comm_group_start(void) {
+  return guard([&] { janus::comm_group_start(); });
+}
+int janus_comm_group_end(void) {
+  return guard([&] { janus::comm_group_end(); });
+}
+int janus_comm_allreduce_sum(janus_comm* c, float* buf, int64_t count, void* stream) {
+  return guard([&] { need(c, "comm"); janus::comm_allreduce_sum(c, buf, count, S(stream)); });
+}
+
+// ---------------------------------------------------------------- trainer
+int janus_trainer_create(const janus_exec_desc* ed, const janus_stage_desc* sd, const float* all_params,
+                         janus_comm* comm, int rank, janus_trainer** out) {
+  return guard([&] {
+    need(ed, "exec desc");
+    need(sd, "stage desc");
+    need(all_params, "all_params");
+    need(out, "out");
+    *out = nullptr;
+    *out = janus::trainer_create(*ed, *sd, all_params, comm, rank);
+  });
+}
+int janus_trainer_destroy(janus_trainer* t) {
+  return guard([&] { janus::trainer_destroy(t); });
+}
+int janus_trainer_load(janus_trainer* t, int mb, const janus_host_batch* hb) {
+  return guard([&] {
+    need(t, "trainer");
+    need(hb, "batch");
+    janus::trainer_load(t, mb, *hb);
+  });
+}
+int janus_trainer_step(janus_trainer* t, const janus_opt* opt, janus_step_stats* stats) {
+  return guard([&] {
+    need(t, "trainer");
+    need(opt, "opt");
+    janus::trainer_step(t, *opt, stats);
+  });
+}
+int janus_trainer_timeline(janus_trainer* t, double* out, int32_t cap, int32_t* n) {
+  return guard([&] {
+    need(t, "trainer");
+    need(n, "n");
+    int nn = 0;
+    janus::trainer_timeline(t, out, out ? cap : 0, &nn);
+    *n = nn;
+  });
+}
+int janus_trainer_stage(janus_trainer* t, int block, int force_replica, janus_stage** out) {
+  return guard([&] {
+    need(t, "trainer");
+    need(out, "out");
+    *out = janus::trainer_stage(t, block, force_replica);
+  });
+}
+int janus_trainer_schedule_text(janus_trainer* t, char* buf, int64_t cap, int64_t* len) {
+  return guard([&] {
+    need(t, "trainer");
+    need(len, "len");
+    const std::string text = janus::trainer_schedule_text(t);
+    *len = static_cast<int64_t>(text.size());
+    if (buf && cap > 0) {
+      const size_t n = std::min<size_t>(text.size(), static_cast<size_t>(cap - 1));
+      std::memcpy(buf, text.data(), n);
+      buf[n] = '\0';
+    }
+  });
+}
+int janus_trainer_plan(janus_trainer* t, int32_t* unit_ranges) {
+  return guard([&] {
+    need(t, "trainer");
+    need(unit_ranges, "unit_ranges");
+    janus::trainer_plan(t, unit_ranges);
+  });
 }
 
 // --------------------------------------------------------------- schedules

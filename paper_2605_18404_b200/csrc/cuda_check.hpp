@@ -12,6 +12,11 @@ struct cuda_error : std::runtime_error {
   explicit cuda_error(const std::string& m) : std::runtime_error(m) {}
 };
 
+/// NCCL failures (executor transports); mapped to janus::kNcclError at the ABI.
+struct nccl_error : std::runtime_error {
+  explicit nccl_error(const std::string& m) : std::runtime_error(m) {}
+};
+
 inline void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw cuda_error(std::string(what) + ": " + cudaGetErrorString(e));
 }

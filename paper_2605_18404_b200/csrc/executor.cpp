@@ -1,0 +1,777 @@
+// executor.cpp — janus_trainer: executes a SymFold / WaveK / 1F1B-2nd
+// schedule (include/janus/schedule_gen.hpp) instruction by instruction.
+//
+// Replaces the reference's "look up a duration" seam (graph.hpp:168 replay,
+// SPEC.md:377-385 instr_duration) with "execute the instruction":
+//   FE/FF/BF/BE -> stage phase kernels on the device's compute stream
+//   S*  -> payload leaves the stage's out-port on a side stream
+//   R*  -> payload lands in the peer stage's in-port; the compute stream waits
+//   OS  -> ledger reduce (+ AR) + Adam;  LM -> geometry is uploaded by load()
+// Channels follow the DepGraph pairing key (graph.hpp:95-97): one transport
+// channel per flow (act / adj / tan / badj / mirror), so per-channel order is
+// the micro-batch order of the device lists on both ends (checked at create).
+//
+// Transports:
+//   local: all P virtual devices in this process on one GPU, each with its own
+//          compute/send streams; a send is an async D2D copy into the peer's
+//          port followed by an event the receiver's compute stream waits on.
+//   NCCL : one process per GPU, ncclSend / ncclRecv on dedicated send / recv
+//          streams per rank, so transfers overlap compute (NVLink/NVSwitch).
+// 1F1B-2nd runs the force half on
+// replicated parameters: FF recomputes FE from the block input (mirror
+// transfer), BF is followed by an injection-only BE whose block-input
+// cotangent is sent back to the energy device, and OS all-reduces the pair.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <numeric>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/janus/errors.hpp"
+#include "../../include/janus/graph.hpp"
+#include "../../include/janus/model.hpp"
+#include "../../include/janus/schedule_gen.hpp"
+#include "../../include/janus_cuda.h"
+#include "cuda_check.hpp"
+#include "stage.cuh"
+#include "stage_api.hpp"
+
+namespace janus {
+namespace {
+
+// One channel per flow.  1F1B-2nd pairs two blocks per device pair, so its
+// mirror flows are split by block parity to keep per-channel order = mb order.
+enum Flow { kFlowAct = 0, kFlowAdj = 1, kFlowTan = 2, kFlowBadj = 3, kFlowMirror = 4, kFlowMirrorBack = 6, kNumFlows = 8 };
+
+inline void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw nccl_error(std::string(what) + ": " + ncclGetErrorString(r));
+}
+#define JANUS_NCCL(x) nccl_check((x), #x)
+
+}  // namespace
+}  // namespace janus
+
+struct janus_comm {
+  int nranks = 1, rank = 0, device = 0;
+  ncclComm_t base = nullptr;
+  ncclComm_t flow[janus::kNumFlows] = {};
+  ncclComm_t pair = nullptr;  // 1F1B-2nd replicated-parameter pairs
+  ncclComm_t dp = nullptr;    // data-parallel replicas of one stage
+};
+
+namespace janus {
+namespace {
+
+struct VDev {
+  int id = 0;                    // schedule device index
+  cudaStream_t compute = nullptr, send = nullptr, recv = nullptr;
+  std::vector<cudaEvent_t> timing;  // start/end pairs
+};
+
+struct Rec {
+  int device, kind, mb;
+  cudaEvent_t a, b;
+};
+
+// A transfer endpoint: which stage object and which port.
+struct End {
+  janus_stage* st = nullptr;
+  int port = -1;
+};
+
+}  // namespace
+}  // namespace janus
+
+struct janus_trainer {
+  janus_exec_desc ed{};
+  janus_stage_desc sd{};
+  janus::Schedule sched;
+  janus::StagePlan plan;
+  int P = 1, method = 0;
+  bool local = true, onef1b = false;
+  janus_comm* comm = nullptr;
+  int rank = 0, replica = 0, my_dev = 0;
+  std::vector<janus::VDev> devs;                 // local virtual devices (local: P, NCCL: 1)
+  std::vector<janus_stage*> E, F;                // per block (nullptr if not on this process)
+  std::vector<int> E_dev, F_dev;                 // schedule device that holds E_b / F_b
+  std::vector<janus_stage*> owned;
+  std::vector<float*> mirror_buf;                // 1F1B: [block*n_mb + mb] cotangent from F_b
+  std::vector<void*> allocs;
+  cudaStream_t root = nullptr;
+  cudaEvent_t anchor = nullptr, finish = nullptr;
+  std::vector<cudaEvent_t> pool;
+  size_t pool_next = 0;
+  std::map<std::tuple<int, int, int, int>, cudaEvent_t> delivered;  // (flow, mb, from_block, to_block)
+  std::vector<int> order;                        // local mode: global issue order (flat indices)
+  janus::DepGraph graph;
+  std::vector<janus::Rec> recs;
+  bool recording = false;
+  int64_t p2p_bytes = 0;
+  int64_t kernel_count = -1;
+  cudaGraphExec_t gexec = nullptr;
+  janus_step_stats last{};
+  std::vector<int> n_atoms;                      // per mb (for port sizes on the receive side)
+};
+
+namespace janus {
+namespace {
+
+cudaEvent_t next_event(janus_trainer* t) {
+  if (t->pool_next == t->pool.size()) {
+    cudaEvent_t e;
+    JANUS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    t->pool.push_back(e);
+  }
+  return t->pool[t->pool_next++];
+}
+
+VDev& vdev(janus_trainer* t, int d) {
+  if (t->local) return t->devs[static_cast<size_t>(d)];
+  if (d != t->my_dev) throw state_error("instruction for a device this process does not own");
+  return t->devs[0];
+}
+
+int peer_rank(const janus_trainer* t, int dev) { return t->replica * t->P + dev; }
+
+int block_of(const janus_trainer* t, int vs) { return vs < t->P ? vs : 2 * t->P - 1 - vs; }
+
+// Map a comm instruction to (flow, sender end, receiver end, from-block, to-block).
+// Returns false for the fold-point pair of 1F1B-2nd (carried by the mirror flow).
+bool route(janus_trainer* t, const Instruction& in, int* flow, End* src, End* dst, int* from_b, int* to_b) {
+  const int P = t->P, vs = in.virtual_stage;
+  const CommClass c = comm_class(in.kind);
+  const bool send = is_send(in.kind);
+  // normalise to the sending stage
+  const int s_vs = send ? vs : comm_peer_stage(in.kind, vs);
+  const int r_vs = send ? comm_peer_stage(in.kind, vs) : vs;
+  const bool act = (c == CommClass::SA || c == CommClass::RA);
+  if (act) {
+    if (s_vs == P - 1 && r_vs == P) return false;  // fold point (1F1B-2nd only)
+    if (r_vs < P) {                                 // FE chain up: SAE
+      *flow = kFlowAct;
+      *src = {t->E[static_cast<size_t>(s_vs)], JANUS_PORT_ACT_OUT};
+      *dst = {t->E[static_cast<size_t>(r_vs)], JANUS_PORT_ACT_IN};
+    } else {  // FF chain: force stage s_vs -> s_vs+1 = block b -> b-1
+      *flow = kFlowAdj;
+      *src = {t->F[static_cast<size_t>(block_of(t, s_vs))], JANUS_PORT_ADJ_OUT};
+      *dst = {t->F[static_cast<size_t>(block_of(t, r_vs))], JANUS_PORT_ADJ_IN};
+    }
+  } else {
+    if (s_vs == P && r_vs == P - 1) return false;  // fold point (1F1B-2nd only)
+    if (r_vs >= P) {                                // BF chain: block b -> b+1
+      *flow = kFlowTan;
+      *src = {t->F[static_cast<size_t>(block_of(t, s_vs))], JANUS_PORT_TAN_OUT};
+      *dst = {t->F[static_cast<size_t>(block_of(t, r_vs))], JANUS_PORT_TAN_IN};
+    } else {  // BE chain down
+      *flow = kFlowBadj;
+      *src = {t->E[static_cast<size_t>(s_vs)], JANUS_PORT_BADJ_OUT};
+      *dst = {t->E[static_cast<size_t>(r_vs)], JANUS_PORT_BADJ_IN};
+    }
+  }
+  *from_b = block_of(t, s_vs);
+  *to_b = block_of(t, r_vs);
+  return true;
+}
+
+void port_ptr(janus_stage* st, int mb, int port, float** p, size_t* bytes) {
+  void* d = nullptr;
+  stage_port(st, mb, mb, port, &d, bytes);
+  *p = static_cast<float*>(d);
+}
+
+size_t port_bytes_for(const janus_trainer* t, int block, int port, int mb) {
+  // both ends of a channel use identical layouts; compute from the model
+  const int H = t->sd.model.H, n = t->n_atoms[static_cast<size_t>(mb)];
+  const bool at_input = (port == JANUS_PORT_ACT_IN || port == JANUS_PORT_ADJ_OUT || port == JANUS_PORT_TAN_IN ||
+                         port == JANUS_PORT_BADJ_OUT);
+  const int u = at_input ? t->plan.blocks[static_cast<size_t>(block)].first : t->plan.blocks[static_cast<size_t>(block)].second;
+  const bool has_m = (u - 1 >= 1) && (u - 1 <= 2 * t->sd.model.L) && ((u - 1) % 2 == 1);
+  const bool has_vec = port >= JANUS_PORT_ADJ_IN && port <= JANUS_PORT_TAN_OUT;
+  return sizeof(float) * (static_cast<size_t>(n) * H * (has_m ? 2 : 1) + (has_vec ? 3 * static_cast<size_t>(n) : 0));
+}
+
+// ------------------------------------------------------------- transfers
+void do_send(janus_trainer* t, VDev& dv, int flow, int mb, janus_stage* src, int sport, janus_stage* dst, int dport,
+             int from_b, int to_b, int peer_dev) {
+  float* sp;
+  size_t sb;
+  port_ptr(src, mb, sport, &sp, &sb);
+  cudaEvent_t ready = next_event(t);
+  JANUS_CUDA(cudaEventRecord(ready, dv.compute));
+  JANUS_CUDA(cudaStreamWaitEvent(dv.send, ready, 0));
+  t->p2p_bytes += static_cast<int64_t>(sb);
+  if (t->local) {
+    float* dp;
+    size_t db;
+    port_ptr(dst, mb, dport, &dp, &db);
+    if (db != sb) throw state_error("port size mismatch between channel ends");
+    JANUS_CUDA(cudaMemcpyAsync(dp, sp, sb, cudaMemcpyDeviceToDevice, dv.send));
+    cudaEvent_t done = next_event(t);
+    JANUS_CUDA(cudaEventRecord(done, dv.send));
+    t->delivered[{flow, mb, from_b, to_b}] = done;
+  } else {
+    JANUS_NCCL(ncclSend(sp, sb, ncclChar, peer_rank(t, peer_dev), t->comm->flow[flow], dv.send));
+  }
+}
+
+void do_recv(janus_trainer* t, VDev& dv, int flow, int mb, janus_stage* dst, int dport, int from_b, int to_b,
+             int peer_dev, size_t bytes) {
+  if (t->local) {
+    const auto it = t->delivered.find({flow, mb, from_b, to_b});
+    if (it == t->delivered.end()) throw deadlock_error("receive issued before its send (issue order)");
+    JANUS_CUDA(cudaStreamWaitEvent(dv.compute, it->second, 0));
+    t->delivered.erase(it);
+  } else {
+    float* dp;
+    size_t db;
+    port_ptr(dst, mb, dport, &dp, &db);
+    if (db != bytes) throw state_error("port size mismatch between channel ends");
+    JANUS_NCCL(ncclRecv(dp, db, ncclChar, peer_rank(t, peer_dev), t->comm->flow[flow], dv.recv));
+    cudaEvent_t done = next_event(t);
+    JANUS_CUDA(cudaEventRecord(done, dv.recv));
+    JANUS_CUDA(cudaStreamWaitEvent(dv.compute, done, 0));
+  }
+}
+
+// 1F1B-2nd mirror transfers (not IR instructions: implied by recompute /
+// replicated parameters).  Act: E_b block input -> F_b.
+void mirror_act_send(janus_trainer* t, VDev& dv, int b, int mb) {
+  if (b == 0) return;  // block 0 starts at the embedding: no input
+  do_send(t, dv, kFlowMirror + (b & 1), mb, t->E[static_cast<size_t>(b)], JANUS_PORT_ACT_IN, t->F[static_cast<size_t>(b)],
+          JANUS_PORT_ACT_IN, b, b, t->F_dev[static_cast<size_t>(b)]);
+}
+void mirror_act_recv(janus_trainer* t, VDev& dv, int b, int mb) {
+  if (b == 0) return;
+  do_recv(t, dv, kFlowMirror + (b & 1), mb, t->F[static_cast<size_t>(b)], JANUS_PORT_ACT_IN, b, b, t->E_dev[static_cast<size_t>(b)],
+          port_bytes_for(t, b, JANUS_PORT_ACT_IN, mb));
+}
+
+// Back: F_b's injection-only block-input cotangent -> E_b (added after its BE).
+void mirror_back_send(janus_trainer* t, VDev& dv, int b, int mb) {
+  if (b == 0) return;
+  janus_stage* f = t->F[static_cast<size_t>(b)];
+  float* sp;
+  size_t sb;
+  port_ptr(f, mb, JANUS_PORT_BADJ_OUT, &sp, &sb);
+  cudaEvent_t ready = next_event(t);
+  JANUS_CUDA(cudaEventRecord(ready, dv.compute));
+  JANUS_CUDA(cudaStreamWaitEvent(dv.send, ready, 0));
+  t->p2p_bytes += static_cast<int64_t>(sb);
+  float* buf = t->mirror_buf[static_cast<size_t>(b) * t->ed.n_micro_batches + mb];
+  if (t->local) {
+    JANUS_CUDA(cudaMemcpyAsync(buf, sp, sb, cudaMemcpyDeviceToDevice, dv.send));
+    cudaEvent_t done = next_event(t);
+    JANUS_CUDA(cudaEventRecord(done, dv.send));
+    t->delivered[{kFlowMirrorBack, mb, b, b}] = done;
+  } else {
+    JANUS_NCCL(ncclSend(sp, sb, ncclChar, peer_rank(t, t->E_dev[static_cast<size_t>(b)]), t->comm->flow[kFlowMirrorBack + (b & 1)], dv.send));
+  }
+}
+void mirror_back_recv_add(janus_trainer* t, VDev& dv, int b, int mb) {
+  if (b == 0) return;
+  janus_stage* e = t->E[static_cast<size_t>(b)];
+  float* dp;
+  size_t db;
+  port_ptr(e, mb, JANUS_PORT_BADJ_OUT, &dp, &db);
+  float* buf = t->mirror_buf[static_cast<size_t>(b) * t->ed.n_micro_batches + mb];
+  if (t->local) {
+    const auto it = t->delivered.find({kFlowMirrorBack, mb, b, b});
+    if (it == t->delivered.end()) throw deadlock_error("mirror cotangent not sent before BE");
+    JANUS_CUDA(cudaStreamWaitEvent(dv.compute, it->second, 0));
+    t->delivered.erase(it);
+  } else {
+    JANUS_NCCL(ncclRecv(buf, db, ncclChar, peer_rank(t, t->F_dev[static_cast<size_t>(b)]), t->comm->flow[kFlowMirrorBack + (b & 1)], dv.recv));
+    cudaEvent_t done = next_event(t);
+    JANUS_CUDA(cudaEventRecord(done, dv.recv));
+    JANUS_CUDA(cudaStreamWaitEvent(dv.compute, done, 0));
+  }
+  add_into(dp, buf, static_cast<int64_t>(db / sizeof(float)), dv.compute);
+}
+
+// ------------------------------------------------------------ one instruction
+void timed(janus_trainer* t, VDev& dv, const Instruction& in, auto&& body) {
+  if (!t->recording) {
+    body();
+    return;
+  }
+  Rec r{in.device, static_cast<int>(in.kind), in.micro_batch, nullptr, nullptr};
+  JANUS_CUDA(cudaEventCreate(&r.a));
+  JANUS_CUDA(cudaEventCreate(&r.b));
+  JANUS_CUDA(cudaEventRecord(r.a, dv.compute));
+  body();
+  JANUS_CUDA(cudaEventRecord(r.b, dv.compute));
+  t->recs.push_back(r);
+}
+
+void execute(janus_trainer* t, const Instruction& in, const janus_opt& opt) {
+  VDev& dv = vdev(t, in.device);
+  const int mb = in.micro_batch;
+  switch (in.kind) {
+    case InstrKind::LM:
+      return;  // geometry is uploaded to every stage by janus_trainer_load
+    case InstrKind::FE: {
+      const int b = block_of(t, in.virtual_stage);
+      timed(t, dv, in, [&] { stage_fe(t->E[static_cast<size_t>(b)], mb, mb, dv.compute); });
+      if (t->onef1b) mirror_act_send(t, dv, b, mb);
+      return;
+    }
+    case InstrKind::FF: {
+      const int b = block_of(t, in.virtual_stage);
+      janus_stage* f = t->F[static_cast<size_t>(b)];
+      if (t->onef1b) mirror_act_recv(t, dv, b, mb);
+      timed(t, dv, in, [&] {
+        if (in.has_flag(kFlagRecompute)) stage_fe(f, mb, mb, dv.compute);  // regenerate FE activations
+        stage_ff(f, mb, mb, dv.compute);
+      });
+      return;
+    }
+    case InstrKind::BF: {
+      const int b = block_of(t, in.virtual_stage);
+      janus_stage* f = t->F[static_cast<size_t>(b)];
+      timed(t, dv, in, [&] {
+        stage_bf(f, mb, mb, dv.compute);
+        if (t->onef1b) stage_be(f, mb, mb, dv.compute, /*inj_only=*/true);
+      });
+      if (t->onef1b) mirror_back_send(t, dv, b, mb);
+      return;
+    }
+    case InstrKind::BE: {
+      const int b = block_of(t, in.virtual_stage);
+      timed(t, dv, in, [&] {
+        stage_be(t->E[static_cast<size_t>(b)], mb, mb, dv.compute);
+        if (t->onef1b) mirror_back_recv_add(t, dv, b, mb);
+      });
+      return;
+    }
+    case InstrKind::OS: {
+      if (t->local) return;  // local mode: optimizer runs after the join (finalize_local)
+      timed(t, dv, in, [&] {
+        std::vector<janus_stage*> mine;  // this rank's objects, block order
+        for (int b = 0; b < t->P; ++b) {
+          if (t->E[static_cast<size_t>(b)]) mine.push_back(t->E[static_cast<size_t>(b)]);
+          if (t->onef1b && t->F[static_cast<size_t>(b)]) mine.push_back(t->F[static_cast<size_t>(b)]);
+        }
+        for (janus_stage* st : mine) stage_reduce_grads(st, dv.compute);
+        if (t->onef1b)  // replicated parameters: energy and force copies sum their grads
+          for (janus_stage* st : mine)
+            JANUS_NCCL(ncclAllReduce(st->grad, st->grad, static_cast<size_t>(st->n_params), ncclFloat, ncclSum, t->comm->pair, dv.compute));
+        if (t->ed.dp_degree > 1)
+          for (janus_stage* st : mine)
+            JANUS_NCCL(ncclAllReduce(st->grad, st->grad, static_cast<size_t>(st->n_params), ncclFloat, ncclSum, t->comm->dp, dv.compute));
+        for (janus_stage* st : mine) stage_optimizer(st, opt, dv.compute);
+      });
+      return;
+    }
+    case InstrKind::AR:
+      return;  // pairwise / DP all-reduce is part of OS (both ends participate)
+    default:
+      break;
+  }
+  // point-to-point
+  int flow, fb, tb;
+  End src, dst;
+  if (!route(t, in, &flow, &src, &dst, &fb, &tb)) return;
+  if (is_send(in.kind)) {
+    do_send(t, dv, flow, mb, src.st, src.port, dst.st, dst.port, fb, tb, in.peer_device);
+  } else {
+    do_recv(t, dv, flow, mb, dst.st, dst.port, fb, tb, in.peer_device, port_bytes_for(t, tb, dst.port, mb));
+  }
+}
+
+// Issue one full step on the streams (no host synchronisation inside).
+void issue_step(janus_trainer* t, const janus_opt& opt) {
+  t->pool_next = 0;
+  t->delivered.clear();
+  t->p2p_bytes = 0;
+  if (t->local) {
+    for (int idx : t->order) execute(t, *t->graph.flat[static_cast<size_t>(idx)], opt);
+  } else {
+    for (const Instruction& in : t->sched.device_lists[static_cast<size_t>(t->my_dev)]) execute(t, in, opt);
+  }
+}
+
+void fork_join_begin(janus_trainer* t) {
+  JANUS_CUDA(cudaEventRecord(t->anchor, t->root));
+  for (auto& d : t->devs) {
+    JANUS_CUDA(cudaStreamWaitEvent(d.compute, t->anchor, 0));
+    JANUS_CUDA(cudaStreamWaitEvent(d.send, t->anchor, 0));
+    JANUS_CUDA(cudaStreamWaitEvent(d.recv, t->anchor, 0));
+  }
+}
+
+void fork_join_end(janus_trainer* t) {
+  for (auto& d : t->devs) {
+    for (cudaStream_t s : {d.send, d.recv, d.compute}) {
+      cudaEvent_t e = next_event(t);
+      JANUS_CUDA(cudaEventRecord(e, s));
+      JANUS_CUDA(cudaStreamWaitEvent(t->root, e, 0));
+    }
+  }
+}
+
+// Local mode OS for every block after all streams joined on root: ledger
+// reduce, 1F1B-2nd pairwise sum of the replicated copies, Adam.
+void finalize_local(janus_trainer* t, const janus_opt& opt) {
+  for (int b = 0; b < t->P; ++b) {
+    janus_stage* e = t->E[static_cast<size_t>(b)];
+    janus_stage* f = t->F[static_cast<size_t>(b)];
+    stage_reduce_grads(e, t->root);
+    if (f != e) {
+      stage_reduce_grads(f, t->root);
+      add_into(e->grad, f->grad, e->n_params, t->root);
+      JANUS_CUDA(cudaMemcpyAsync(f->grad, e->grad, sizeof(float) * e->n_params, cudaMemcpyDeviceToDevice, t->root));
+      stage_optimizer(f, opt, t->root);
+    }
+    stage_optimizer(e, opt, t->root);
+  }
+}
+
+}  // namespace
+
+// ================================================================ create
+janus_trainer* trainer_create(const janus_exec_desc& ed, const janus_stage_desc& sd, const float* all_params,
+                              janus_comm* comm, int rank) {
+  auto t = std::make_unique<janus_trainer>();
+  t->ed = ed;
+  t->sd = sd;
+  t->P = ed.n_stages;
+  t->method = ed.method;
+  t->local = ed.local_stages != 0;
+  t->onef1b = ed.method == 2;
+  if (ed.dp_degree < 1) t->ed.dp_degree = 1;
+  if (ed.n_micro_batches < 1) throw domain_error("n_micro_batches must be >= 1");
+  if (!t->local && !comm) throw config_error("NCCL mode needs a janus_comm");
+  if (t->local && t->ed.dp_degree != 1) throw config_error("data parallelism needs NCCL mode");
+  switch (ed.method) {
+    case 0: t->sched = symfold(t->P, ed.n_micro_batches); break;
+    case 1: t->sched = wavek(t->P, ed.n_micro_batches, ed.wavek_k); break;
+    case 2: t->sched = onef1b_2nd(t->P, ed.n_micro_batches); break;
+    default: throw domain_error("unknown method");
+  }
+  const ValidationReport vr = validate_schedule(t->sched);
+  if (!vr.ok()) throw state_error("generated schedule failed validation");
+  // per-channel order must agree on both ends (NCCL pairs sends/receives in issue order)
+  {
+    std::map<std::tuple<int, char, int, int>, std::vector<int>> snd, rcv;
+    for (const auto& dl : t->sched.device_lists)
+      for (const Instruction& in : dl) {
+        if (!is_comm(in.kind)) continue;
+        const int pay = is_activation_comm(in.kind) ? 0 : 1;
+        const int from = is_send(in.kind) ? in.device : in.peer_device, to = is_send(in.kind) ? in.peer_device : in.device;
+        (is_send(in.kind) ? snd : rcv)[{pay, comm_suffix(in.kind), from, to}].push_back(in.micro_batch);
+      }
+    if (snd != rcv) throw deadlock_error("channel micro-batch order differs between send and receive ends");
+  }
+  ModelConfig mc;
+  mc.L = sd.model.L;
+  mc.H = sd.model.H;
+  mc.R = sd.model.R;
+  mc.n_species = sd.model.n_species;
+  t->plan = partition_units(mc, t->P);
+  t->E.assign(static_cast<size_t>(t->P), nullptr);
+  t->F.assign(static_cast<size_t>(t->P), nullptr);
+  t->E_dev.resize(static_cast<size_t>(t->P));
+  t->F_dev.resize(static_cast<size_t>(t->P));
+  for (int b = 0; b < t->P; ++b) {
+    t->E_dev[static_cast<size_t>(b)] = t->sched.stage_map[static_cast<size_t>(b)];
+    t->F_dev[static_cast<size_t>(b)] = t->sched.stage_map[static_cast<size_t>(2 * t->P - 1 - b)];
+  }
+  if (!t->local) {
+    t->comm = comm;
+    t->rank = rank;
+    t->replica = rank / t->P;
+    t->my_dev = rank % t->P;
+    if (comm->nranks != t->P * t->ed.dp_degree) throw config_error("communicator size != P * dp_degree");
+  }
+  JANUS_CUDA(cudaSetDevice(sd.device));
+  const int nd = t->local ? t->P : 1;
+  t->devs.resize(static_cast<size_t>(nd));
+  for (int d = 0; d < nd; ++d) {
+    VDev& v = t->devs[static_cast<size_t>(d)];
+    v.id = t->local ? d : t->my_dev;
+    JANUS_CUDA(cudaStreamCreateWithFlags(&v.compute, cudaStreamNonBlocking));
+    JANUS_CUDA(cudaStreamCreateWithFlags(&v.send, cudaStreamNonBlocking));
+    JANUS_CUDA(cudaStreamCreateWithFlags(&v.recv, cudaStreamNonBlocking));
+  }
+  JANUS_CUDA(cudaStreamCreateWithFlags(&t->root, cudaStreamNonBlocking));
+  JANUS_CUDA(cudaEventCreate(&t->anchor));
+  JANUS_CUDA(cudaEventCreate(&t->finish));
+  auto make = [&](int b) {
+    janus_stage_desc d = sd;
+    d.unit_begin = t->plan.blocks[static_cast<size_t>(b)].first;
+    d.unit_end = t->plan.blocks[static_cast<size_t>(b)].second;
+    d.n_micro_batches = ed.n_micro_batches;
+    d.n_slots = ed.n_micro_batches;
+    const int64_t off = mc.unit_param_offset(d.unit_begin);
+    janus_stage* st = stage_create(d, all_params + off);
+    t->owned.push_back(st);
+    return st;
+  };
+  for (int b = 0; b < t->P; ++b) {
+    const bool e_here = t->local || t->E_dev[static_cast<size_t>(b)] == t->my_dev;
+    const bool f_here = t->local || t->F_dev[static_cast<size_t>(b)] == t->my_dev;
+    if (e_here) t->E[static_cast<size_t>(b)] = make(b);
+    if (f_here) t->F[static_cast<size_t>(b)] = (t->onef1b ? make(b) : t->E[static_cast<size_t>(b)]);
+  }
+  if (t->onef1b) {
+    t->mirror_buf.assign(static_cast<size_t>(t->P) * ed.n_micro_batches, nullptr);
+    const size_t bytes = sizeof(float) * static_cast<size_t>(sd.max_atoms) * sd.model.H * 2;
+    for (int b = 1; b < t->P; ++b) {
+      if (!(t->local || t->E_dev[static_cast<size_t>(b)] == t->my_dev)) continue;
+      for (int m = 0; m < ed.n_micro_batches; ++m) {
+        void* p;
+        JANUS_CUDA(cudaMalloc(&p, bytes));
+        t->allocs.push_back(p);
+        t->mirror_buf[static_cast<size_t>(b) * ed.n_micro_batches + m] = static_cast<float*>(p);
+      }
+    }
+  }
+  if (!t->local && (t->onef1b || t->ed.dp_degree > 1)) {
+    // split sub-communicators: pairs (d, P-1-d) of one replica; replicas of one stage
+    const int d = t->my_dev;
+    const int pair_color = t->onef1b ? t->replica * t->P + std::min(d, t->P - 1 - d) : NCCL_SPLIT_NOCOLOR;
+    JANUS_NCCL(ncclCommSplit(comm->base, pair_color, rank, &comm->pair, nullptr));
+    const int dp_color = t->ed.dp_degree > 1 ? d : NCCL_SPLIT_NOCOLOR;
+    JANUS_NCCL(ncclCommSplit(comm->base, dp_color, rank, &comm->dp, nullptr));
+  }
+  // local issue order: a topological order of the full DAG (seq + data edges),
+  // so every send is issued before its receive.
+  t->graph = build_dependencies(t->sched);
+  if (t->local) {
+    const int n = t->graph.size();
+    std::vector<int> indeg(static_cast<size_t>(n));
+    std::vector<std::vector<int>> succ(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) {
+      indeg[static_cast<size_t>(i)] = static_cast<int>(t->graph.preds[static_cast<size_t>(i)].size());
+      for (int p : t->graph.preds[static_cast<size_t>(i)]) succ[static_cast<size_t>(p)].push_back(i);
+    }
+    std::vector<int> q;
+    for (int i = 0; i < n; ++i)
+      if (indeg[static_cast<size_t>(i)] == 0) q.push_back(i);
+    for (size_t h = 0; h < q.size(); ++h)
+      for (int x : succ[static_cast<size_t>(q[h])])
+        if (--indeg[static_cast<size_t>(x)] == 0) q.push_back(x);
+    if (static_cast<int>(q.size()) != n) throw deadlock_error("schedule dependency graph has a cycle");
+    t->order = std::move(q);
+  }
+  t->n_atoms.assign(static_cast<size_t>(ed.n_micro_batches), 0);
+  JANUS_CUDA(cudaDeviceSynchronize());
+  return t.release();
+}
+
+void trainer_destroy(janus_trainer* t) {
+  if (!t) return;
+  cudaSetDevice(t->sd.device);
+  cudaDeviceSynchronize();
+  if (t->gexec) cudaGraphExecDestroy(t->gexec);
+  for (janus_stage* s : t->owned) stage_destroy(s);
+  for (void* p : t->allocs) cudaFree(p);
+  for (cudaEvent_t e : t->pool) cudaEventDestroy(e);
+  for (auto& r : t->recs) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (auto& d : t->devs) {
+    cudaStreamDestroy(d.compute);
+    cudaStreamDestroy(d.send);
+    cudaStreamDestroy(d.recv);
+  }
+  if (t->root) cudaStreamDestroy(t->root);
+  if (t->anchor) cudaEventDestroy(t->anchor);
+  if (t->finish) cudaEventDestroy(t->finish);
+  delete t;
+}
+
+void trainer_load(janus_trainer* t, int mb, const janus_host_batch& hb) {
+  if (mb < 0 || mb >= t->ed.n_micro_batches) throw domain_error("micro-batch index out of range");
+  for (janus_stage* s : t->owned) stage_load(s, mb, hb, t->root);
+  t->n_atoms[static_cast<size_t>(mb)] = hb.n_atoms;
+}
+
+// count kernel nodes of one captured step (the gpu_launches evidence)
+int64_t count_kernels(janus_trainer* t, const janus_opt& opt) {
+  cudaGraph_t g;
+  JANUS_CUDA(cudaStreamBeginCapture(t->root, cudaStreamCaptureModeThreadLocal));
+  try {
+    fork_join_begin(t);
+    issue_step(t, opt);
+    fork_join_end(t);
+    if (t->local) finalize_local(t, opt);
+  } catch (...) {
+    cudaStreamEndCapture(t->root, &g);
+    throw;
+  }
+  JANUS_CUDA(cudaStreamEndCapture(t->root, &g));
+  size_t n = 0;
+  JANUS_CUDA(cudaGraphGetNodes(g, nullptr, &n));
+  std::vector<cudaGraphNode_t> nodes(n);
+  JANUS_CUDA(cudaGraphGetNodes(g, nodes.data(), &n));
+  int64_t k = 0;
+  for (auto nd : nodes) {
+    cudaGraphNodeType ty;
+    JANUS_CUDA(cudaGraphNodeGetType(nd, &ty));
+    if (ty == cudaGraphNodeTypeKernel) ++k;
+  }
+  if (t->ed.use_graphs && !t->ed.record_timeline) {
+    JANUS_CUDA(cudaGraphInstantiate(&t->gexec, g, 0));
+  }
+  JANUS_CUDA(cudaGraphDestroy(g));
+  return k;
+}
+
+void trainer_step(janus_trainer* t, const janus_opt& opt, janus_step_stats* stats) {
+  JANUS_CUDA(cudaSetDevice(t->sd.device));
+  for (int m = 0; m < t->ed.n_micro_batches; ++m)
+    if (t->n_atoms[static_cast<size_t>(m)] <= 0) throw state_error("micro-batch " + std::to_string(m) + " not loaded");
+  if (t->local && t->kernel_count < 0) t->kernel_count = count_kernels(t, opt);  // capture only, nothing runs
+  for (auto& r : t->recs) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  t->recs.clear();
+  t->recording = t->ed.record_timeline != 0;
+  if (t->gexec) {
+    JANUS_CUDA(cudaEventRecord(t->anchor, t->root));
+    JANUS_CUDA(cudaGraphLaunch(t->gexec, t->root));
+  } else {
+    fork_join_begin(t);
+    issue_step(t, opt);
+    fork_join_end(t);
+    if (t->local) finalize_local(t, opt);
+  }
+  JANUS_CUDA(cudaEventRecord(t->finish, t->root));
+  JANUS_CUDA(cudaEventSynchronize(t->finish));
+  t->recording = false;
+  float ms = 0.f;
+  JANUS_CUDA(cudaEventElapsedTime(&ms, t->anchor, t->finish));
+  janus_step_stats s{};
+  s.makespan_ms = ms;
+  s.p2p_bytes = t->p2p_bytes;
+  s.kernel_launches = t->kernel_count;
+  if (!t->recs.empty()) {
+    std::vector<double> busy(static_cast<size_t>(t->P), 0.0);
+    for (auto& r : t->recs) {
+      float a = 0.f;
+      JANUS_CUDA(cudaEventElapsedTime(&a, r.a, r.b));
+      busy[static_cast<size_t>(r.device)] += a;
+    }
+    double idle = 0;
+    for (int d = 0; d < t->P && d < 64; ++d) {
+      s.busy_ms[d] = busy[static_cast<size_t>(d)];
+      idle += ms - busy[static_cast<size_t>(d)];
+    }
+    s.bubble_ratio = t->local ? idle / (t->P * static_cast<double>(ms)) : (ms - busy[static_cast<size_t>(t->my_dev)]) / ms;
+  }
+  for (size_t x = 0; x < t->owned.size(); ++x) {
+    janus_stage* st = t->owned[x];
+    int dev = t->local ? 0 : t->my_dev;
+    for (int b = 0; b < t->P; ++b) {
+      if (t->E[static_cast<size_t>(b)] == st) dev = t->E_dev[static_cast<size_t>(b)];
+      else if (t->F[static_cast<size_t>(b)] == st) dev = t->F_dev[static_cast<size_t>(b)];
+    }
+    if (dev < 64) s.peak_bytes[dev] += st->static_bytes + st->arena_bytes;
+  }
+  // losses held here: L_E on the readout stage, L_F on the stage holding block 0's force replica
+  double loss = 0;
+  for (int m = 0; m < t->ed.n_micro_batches; ++m) {
+    float l[2];
+    janus_stage* top = t->E[static_cast<size_t>(t->P - 1)];
+    if (top) {
+      JANUS_CUDA(cudaMemcpy(l, top->slots[static_cast<size_t>(m)].loss, sizeof(float), cudaMemcpyDeviceToHost));
+      loss += l[0];
+    }
+    janus_stage* bot = t->F[0];
+    if (bot) {
+      JANUS_CUDA(cudaMemcpy(l + 1, bot->slots[static_cast<size_t>(m)].loss + 1, sizeof(float), cudaMemcpyDeviceToHost));
+      loss += l[1];
+    }
+  }
+  s.loss = loss;
+  t->last = s;
+  if (stats) *stats = s;
+}
+
+}  // namespace janus
+
+namespace janus {
+
+void trainer_timeline(janus_trainer* t, double* out, int cap, int* n) {
+  *n = static_cast<int>(t->recs.size());
+  for (int x = 0; x < *n && x < cap; ++x) {
+    const Rec& r = t->recs[static_cast<size_t>(x)];
+    float a = 0.f, b = 0.f;
+    JANUS_CUDA(cudaEventElapsedTime(&a, t->anchor, r.a));
+    JANUS_CUDA(cudaEventElapsedTime(&b, t->anchor, r.b));
+    out[5 * x + 0] = r.device;
+    out[5 * x + 1] = r.kind;
+    out[5 * x + 2] = r.mb;
+    out[5 * x + 3] = 1000.0 * a;
+    out[5 * x + 4] = 1000.0 * b;
+  }
+}
+
+janus_stage* trainer_stage(janus_trainer* t, int block, int force_replica) {
+  if (block < 0 || block >= t->P) throw domain_error("block out of range");
+  janus_stage* s = force_replica ? t->F[static_cast<size_t>(block)] : t->E[static_cast<size_t>(block)];
+  if (!s) throw state_error("block is not held by this process");
+  return s;
+}
+
+std::string trainer_schedule_text(janus_trainer* t) { return serialize(t->sched); }
+
+void trainer_plan(janus_trainer* t, int32_t* out) {
+  for (int b = 0; b < t->P; ++b) {
+    out[2 * b] = t->plan.blocks[static_cast<size_t>(b)].first;
+    out[2 * b + 1] = t->plan.blocks[static_cast<size_t>(b)].second;
+  }
+}
+
+// ------------------------------------------------------------------ NCCL
+void nccl_unique_id(void* out) {
+  ncclUniqueId id;
+  JANUS_NCCL(ncclGetUniqueId(&id));
+  std::memcpy(out, &id, sizeof(id));
+}
+
+janus_comm* comm_init_nccl(const void* id, int nranks, int rank, int device) {
+  JANUS_CUDA(cudaSetDevice(device));
+  auto c = std::make_unique<janus_comm>();
+  c->nranks = nranks;
+  c->rank = rank;
+  c->device = device;
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, sizeof(uid));
+  JANUS_NCCL(ncclCommInitRank(&c->base, nranks, uid, rank));
+  for (int f = 0; f < kNumFlows; ++f) JANUS_NCCL(ncclCommSplit(c->base, 0, rank, &c->flow[f], nullptr));
+  return c.release();
+}
+
+void comm_destroy(janus_comm* c) {
+  if (!c) return;
+  for (auto& f : c->flow)
+    if (f) ncclCommDestroy(f);
+  if (c->pair) ncclCommDestroy(c->pair);
+  if (c->dp) ncclCommDestroy(c->dp);
+  if (c->base) ncclCommDestroy(c->base);
+  delete c;
+}
+
+void comm_send(janus_comm* c, const void* buf, size_t bytes, int peer, cudaStream_t s) {
+  JANUS_NCCL(ncclSend(buf, bytes, ncclChar, peer, c->base, s));
+}
+void comm_recv(janus_comm* c, void* buf, size_t bytes, int peer, cudaStream_t s) {
+  JANUS_NCCL(ncclRecv(buf, bytes, ncclChar, peer, c->base, s));
+}
+void comm_group_start() { JANUS_NCCL(ncclGroupStart()); }
+void comm_group_end() { JANUS_NCCL(ncclGroupEnd()); }
+void comm_allreduce_sum(janus_comm* c, float* buf, int64_t count, cudaStream_t s) {
+  JANUS_NCCL(ncclAllReduce(buf, buf, static_cast<size_t>(count), ncclFloat, ncclSum, c->base, s));
+}
+
+}  // namespace janus

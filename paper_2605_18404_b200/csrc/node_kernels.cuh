@@ -255,10 +255,17 @@ __global__ void ledger_reduce_kernel(int64_t n, int n_mb, const float* __restric
   g[x] = s;
 }
 
+__global__ void adam_tick_kernel(int* step) { *step += 1; }
+
+// Bias corrections from the device-side step counter so a captured step
+// (CUDA graph) replays correctly.
 __global__ void adam_kernel(int64_t n, float* __restrict__ p, float* __restrict__ m1, float* __restrict__ m2,
-                            const float* __restrict__ g, float lr, float b1, float b2, float eps, float c1, float c2) {
+                            const float* __restrict__ g, float lr, float b1, float b2, float eps,
+                            const int* __restrict__ step) {
   const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= n) return;
+  const float t = static_cast<float>(*step);
+  const float c1 = 1.0f - powf(b1, t), c2 = 1.0f - powf(b2, t);
   const float gg = g[x];
   const float a = b1 * m1[x] + (1.0f - b1) * gg;
   const float b = b2 * m2[x] + (1.0f - b2) * gg * gg;

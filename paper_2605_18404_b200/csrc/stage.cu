@@ -201,6 +201,7 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
     st->grad = dalloc<float>(st, NP, true);
     st->m1 = dalloc<float>(st, NP, true);
     st->m2 = dalloc<float>(st, NP, true);
+    st->dstep = dalloc<int>(st, 1, true);
     st->g1 = dalloc<float>(st, NP * NMB, true);
     st->g2 = dalloc<float>(st, NP * NMB, true);
     JANUS_CUDA(cudaMemcpy(st->params, unit_params, NP * sizeof(float), cudaMemcpyHostToDevice));
@@ -564,7 +565,7 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s) {
 }
 
 // ================================================================== BE
-void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s) {
+void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only) {
   check_mb_slot(st, mb, slot);
   const DevGeo& g = st->geo[static_cast<size_t>(mb)];
   Slot& sl = st->slots[static_cast<size_t>(slot)];
@@ -574,7 +575,12 @@ void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s) {
   float* bh = st->wh;
   float* bm = st->wm;
   JANUS_CUDA(cudaMemsetAsync(st->g1 + static_cast<size_t>(mb) * st->n_params, 0, sizeof(float) * st->n_params, s));
-  if (!st->has_readout) {
+  if (inj_only) {
+    // 1F1B-2nd force replica: propagate only the BF->BE injections (b_out = 0,
+    // no L_E seed); the energy device adds the result at its block input.
+    JANUS_CUDA(cudaMemsetAsync(bh, 0, sizeof(float) * NH, s));
+    JANUS_CUDA(cudaMemsetAsync(bm, 0, sizeof(float) * NH, s));
+  } else if (!st->has_readout) {
     const Port& in = sl.ports[JANUS_PORT_BADJ_IN];
     copy(s, bh, port_h(in, N), NH);
     if (in.has_m) copy(s, bm, port_m(in, N), NH);
@@ -586,6 +592,10 @@ void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s) {
     float* G1 = ledger(st, st->g1, mb, u);
     switch (unit_kind(u, L)) {
       case kReadout: {
+        if (inj_only) {  // no energy seed: b_h = hbar^F, readout first-order grads are zero
+          copy(s, bh, b.inj, NH);
+          break;
+        }
         const float* om = P + H * H + H;
         float *dO = G1, *dob = G1 + H * H, *dom = G1 + H * H + H, *dbias = G1 + H * H + 2 * H;
         node::ro_be_ew_kernel<kH><<<blocks(NH, 256), 256, 0, s>>>(static_cast<int>(NH), b.p, om, sl.eps, g.struct_id,
@@ -634,6 +644,18 @@ void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s) {
   }
 }
 
+// dst[x] += src[x]
+__global__ void add_kernel(int64_t n, float* __restrict__ dst, const float* __restrict__ src) {
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x < n) dst[x] += src[x];
+}
+
+void add_into(float* dst, const float* src, int64_t n, cudaStream_t s) {
+  if (n <= 0) return;
+  add_kernel<<<blocks(n, 256), 256, 0, s>>>(n, dst, src);
+  JANUS_LAUNCH_CHECK("add");
+}
+
 // ============================================================ grads / OS
 void stage_reduce_grads(janus_stage* st, cudaStream_t s) {
   node::ledger_reduce_kernel<<<blocks(st->n_params, 256), 256, 0, s>>>(st->n_params, st->desc.n_micro_batches, st->g1,
@@ -643,10 +665,9 @@ void stage_reduce_grads(janus_stage* st, cudaStream_t s) {
 
 void stage_optimizer(janus_stage* st, const janus_opt& o, cudaStream_t s) {
   ++st->adam_step;
-  const float c1 = 1.0f - std::pow(o.beta1, static_cast<float>(st->adam_step));
-  const float c2 = 1.0f - std::pow(o.beta2, static_cast<float>(st->adam_step));
+  node::adam_tick_kernel<<<1, 1, 0, s>>>(st->dstep);
   node::adam_kernel<<<blocks(st->n_params, 256), 256, 0, s>>>(st->n_params, st->params, st->m1, st->m2, st->grad, o.lr,
-                                                              o.beta1, o.beta2, o.eps, c1, c2);
+                                                              o.beta1, o.beta2, o.eps, st->dstep);
   JANUS_LAUNCH_CHECK("adam");
   refresh_transposes(st, s);
 }
@@ -663,6 +684,74 @@ void stage_port(janus_stage* st, int mb, int slot, int port, void** dptr, size_t
   }
   *dptr = p.buf;
   *bytes = port_elems(st, port, st->geo[static_cast<size_t>(mb)].n_atoms) * sizeof(float);
+}
+
+// ============================================================ kernel timing
+// Algorithmic FLOPs per edge of each msg-unit edge kernel (multiply-adds x 2),
+// counting the per-edge contractions only:
+//   FE: z=phi A, g=s B                                  -> RH + H^2
+//   FF: z, z', g, g' (+ q dot)                          -> 2RH + 2H^2 + H
+//   BF: z, z', g, g', sbar, sdotbar, dB(2), dA(2)       -> 4RH + 6H^2
+//   BE: z, g, sbar, dB, dA                              -> 2RH + 3H^2
+double edge_kernel_flops_per_edge(int which, int H, int R) {
+  const double RH = static_cast<double>(R) * H, HH = static_cast<double>(H) * H;
+  switch (which) {
+    case 0: return 2.0 * (RH + HH);
+    case 1: return 2.0 * (2 * RH + 2 * HH + H);
+    case 2: return 2.0 * (4 * RH + 6 * HH);
+    default: return 2.0 * (2 * RH + 3 * HH);
+  }
+}
+
+void stage_time_edge_kernel(janus_stage* st, int which, int mb, int slot, int iters, cudaStream_t s, float* avg_ms,
+                            int64_t* edges, double* flops) {
+  check_mb_slot(st, mb, slot);
+  int u = -1;
+  for (int x = st->u0; x < st->u1; ++x)
+    if (unit_kind(x, st->m.L) == kMsg) {
+      u = x;
+      break;
+    }
+  if (u < 0) throw state_error("stage has no msg unit");
+  if (iters < 1 || which < 0 || which > 3) throw domain_error("bad timing request");
+  const DevGeo& g = st->geo[static_cast<size_t>(mb)];
+  Slot& sl = st->slots[static_cast<size_t>(slot)];
+  UnitBufs& b = sl.units[static_cast<size_t>(u - st->u0)];
+  const EdgeGeom eg = edge_geom(g);
+  const MsgParams mp = msg_params(st, u);
+  auto launch = [&] {
+    switch (which) {
+      case 0:
+        edge::msg_fe_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::fe_smem<kH, kR>(), s>>>(eg, mp, st->m.r_c, b.v, st->s3);
+        break;
+      case 1:
+        edge::msg_ff_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::ff_smem<kH, kR>(), s>>>(eg, mp, st->m.r_c, b.v, b.ff_a, st->s3, st->q);
+        break;
+      case 2:
+        edge::msg_bf_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::bf_smem<kH, kR>(), s>>>(eg, mp, st->m.r_c, b.v, st->s1, b.ff_a,
+                                                                                       sl.Fbar, st->s3, st->s4, st->partial);
+        break;
+      default:
+        edge::msg_be_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::be_smem<kH, kR>(), s>>>(eg, mp, st->m.r_c, b.v, st->s2, st->s3, st->partial);
+        break;
+    }
+  };
+  launch();
+  JANUS_LAUNCH_CHECK("time_edge_kernel");
+  cudaEvent_t a, z;
+  JANUS_CUDA(cudaEventCreate(&a));
+  JANUS_CUDA(cudaEventCreate(&z));
+  JANUS_CUDA(cudaEventRecord(a, s));
+  for (int i = 0; i < iters; ++i) launch();
+  JANUS_CUDA(cudaEventRecord(z, s));
+  JANUS_CUDA(cudaEventSynchronize(z));
+  float ms = 0.f;
+  JANUS_CUDA(cudaEventElapsedTime(&ms, a, z));
+  cudaEventDestroy(a);
+  cudaEventDestroy(z);
+  *avg_ms = ms / iters;
+  *edges = g.n_edges;
+  *flops = edge_kernel_flops_per_edge(which, kH, kR) * g.n_edges;
 }
 
 // ============================================================ read-back

@@ -75,6 +75,7 @@ struct janus_stage {
   float *g1 = nullptr, *g2 = nullptr;  // [n_mb][n_params]
   std::vector<float*> tw;              // per unit: transposed weights block
   int adam_step = 0;
+  int* dstep = nullptr;  // device-side Adam step (graph-replayable bias correction)
   std::vector<janus::DevGeo> geo;
   std::vector<janus::Slot> slots;
   // scratch

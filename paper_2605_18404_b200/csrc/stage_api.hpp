@@ -13,7 +13,8 @@ void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_
 void stage_fe(janus_stage* st, int mb, int slot, cudaStream_t s);
 void stage_ff(janus_stage* st, int mb, int slot, cudaStream_t s);
 void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s);
-void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s);
+void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only = false);
+void add_into(float* dst, const float* src, int64_t n, cudaStream_t s);
 void stage_reduce_grads(janus_stage* st, cudaStream_t s);
 void stage_optimizer(janus_stage* st, const janus_opt& o, cudaStream_t s);
 void stage_port(janus_stage* st, int mb, int slot, int port, void** dptr, size_t* bytes);
@@ -27,5 +28,7 @@ int64_t stage_param_count(const janus_stage* st);
 void stage_grad_buffer(janus_stage* st, float** dptr, int64_t* count);
 void stage_memory(const janus_stage* st, int64_t* static_bytes, int64_t* arena_bytes);
 int stage_slot_of_mb(const janus_stage* st, int mb);
+void stage_time_edge_kernel(janus_stage* st, int which, int mb, int slot, int iters, cudaStream_t s, float* avg_ms,
+                            int64_t* edges, double* flops);
 
 }  // namespace janus

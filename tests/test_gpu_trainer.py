@@ -1,0 +1,114 @@
+"""The schedule executor (C++ janus_trainer) on one GPU: P pipeline stages as
+virtual devices with their own streams and a D2D transport.
+
+* SymFold and WaveK at any P produce BIT-IDENTICAL gradients and updated
+  parameters to P=1: per-micro-batch gradient ledgers are reduced in a fixed
+  order, so neither P nor the schedule order changes a single rounding.
+* 1F1B-2nd (recompute + replicated parameters + pairwise sum) matches the
+  oracle within the fp32 tolerance.
+* CUDA-graph replay equals eager issue bit-for-bit.
+"""
+import ctypes
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+TOL_G = 1e-4
+
+
+@pytest.fixture(scope="module")
+def data(janus, oracle, has_gpu):
+    if not has_gpu:
+        pytest.skip("no GPU")
+    m = janus.Model(L=2, H=64, R=64)
+    params = m.synth_params(21)
+    batches = [janus.synth_batch(m, [n], 0.095, 100 + i) for i, n in enumerate([32, 40, 27, 36])]
+    om = oracle.Model(L=m.L, H=m.H, R=m.R, n_species=m.n_species, r_c=m.r_c, w_E=m.w_E, w_F=m.w_F)
+    g = np.zeros(m.param_count())
+    loss = 0.0
+    for b in batches:
+        ob = oracle.Batch(b.pos, b.species, b.struct_id, b.cell, b.E_target.astype(float), b.F_target.astype(float))
+        r = oracle.step(om, ob, oracle.build_nbrlist(om, ob), params.astype(float))
+        g += r.grad
+        loss += r.loss
+    return m, params, batches, g, loss
+
+
+def reduced_grad(janus, stage):
+    ptr, n = ctypes.c_void_p(), ctypes.c_int64()
+    fn = janus.lib().janus_stage_grad_buffer
+    fn.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+    janus.check(fn(stage.h, ctypes.byref(ptr), ctypes.byref(n)))
+    out = np.zeros(n.value, np.float32)
+    rt = janus.cudart()
+    assert rt.cudaDeviceSynchronize() == 0
+    assert rt.cudaMemcpy(out.ctypes.data, ptr.value, out.nbytes, 2) == 0
+    return out
+
+
+def run(janus, m, params, batches, P, method, k=1, graphs=False, timeline=False, steps=1):
+    t = janus.Trainer(m, params, P, method, len(batches), k=k, max_atoms=64, max_edges=64 * 120,
+                      graphs=graphs, timeline=timeline)
+    for i, b in enumerate(batches):
+        t.load(i, b)
+    stats = [t.step(lr=1e-3) for _ in range(steps)]
+    g = np.concatenate([reduced_grad(janus, t.stage(b)) for b in range(P)])
+    p = t.params()
+    return t, g, p, stats
+
+
+def test_symfold_p1_matches_oracle(janus, data):
+    m, params, batches, g_ref, loss_ref = data
+    t, g, p, st = run(janus, m, params, batches, 1, janus.METHOD_SYMFOLD)
+    assert np.abs(g - g_ref).max() / np.abs(g_ref).max() < TOL_G
+    assert abs(st[0].loss - loss_ref) < 1e-5 * abs(loss_ref)
+    assert st[0].makespan_ms > 0 and st[0].kernel_launches > 0
+    t.close()
+
+
+@pytest.mark.parametrize("P,method,k", [(2, 0, 1), (4, 0, 1), (4, 1, 2), (4, 1, 4), (6, 0, 1)])
+def test_pipeline_bit_identical_to_p1(janus, data, P, method, k):
+    m, params, batches, g_ref, _ = data
+    t1, g1, p1, _ = run(janus, m, params, batches, 1, janus.METHOD_SYMFOLD)
+    tp, gp, pp, st = run(janus, m, params, batches, P, method, k)
+    assert np.array_equal(g1, gp) and np.array_equal(p1, pp)
+    assert st[0].p2p_bytes > 0
+    t1.close()
+    tp.close()
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_onef1b_2nd_matches_oracle(janus, data, P):
+    m, params, batches, g_ref, loss_ref = data
+    t, g, p, st = run(janus, m, params, batches, P, janus.METHOD_ONEF1B)
+    assert np.abs(g - g_ref).max() / np.abs(g_ref).max() < TOL_G
+    # the force replicas received the same summed gradient and took the same step
+    for b in range(P):
+        assert np.array_equal(t.stage(b).params(), t.stage(b, force_replica=True).params())
+    t1, _, p1, _ = run(janus, m, params, batches, 1, janus.METHOD_SYMFOLD)
+    assert np.abs(p - p1).max() < 1e-5
+    t.close()
+    t1.close()
+
+
+def test_graph_replay_equals_eager(janus, data):
+    m, params, batches, _, _ = data
+    ta, ga, pa, _ = run(janus, m, params, batches, 4, janus.METHOD_WAVEK, k=2, steps=3)
+    tb, gb, pb, _ = run(janus, m, params, batches, 4, janus.METHOD_WAVEK, k=2, graphs=True, steps=3)
+    assert np.array_equal(ga, gb) and np.array_equal(pa, pb)
+    ta.close()
+    tb.close()
+
+
+def test_timeline_and_bubble(janus, data):
+    m, params, batches, _, _ = data
+    P = 4
+    t, _, _, st = run(janus, m, params, batches, P, janus.METHOD_SYMFOLD, timeline=True)
+    tl = t.timeline()
+    assert len(tl) == 4 * P * len(batches)  # one record per compute instruction
+    assert (tl[:, 4] >= tl[:, 3]).all()
+    s = st[0]
+    assert 0.0 <= s.bubble_ratio < 1.0
+    assert all(s.busy_ms[d] > 0 for d in range(P))
+    t.close()
