@@ -232,7 +232,8 @@ def main():
     k = min(n_mb, 2 * P)
     max_edges = max(b.n_edges for b in batches) + 64
     tr = J.Trainer(model, params, P, method, n_mb, k=k, max_atoms=CONFIG["atoms"], max_edges=max_edges,
-                   max_struct=1, local=(N == 1), graphs=(N == 1), comm=comm, rank=rank, device=local_rank)
+                   max_struct=1, local=(N == 1), graphs=(N == 1), comm=comm, rank=rank, device=local_rank,
+                   lanes=(8 if N == 1 else 1))
     for m, b in enumerate(batches):
         tr.load(m, b)
     for _ in range(args.warmup):
@@ -311,7 +312,8 @@ def main():
                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
                "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
                "config": dict(cfg, parallelism=f"pp{P}" if P > 1 else "single-gpu", schedule=method_name,
-                              wavek_k=k if method == J.METHOD_WAVEK else None, cuda_graph=(N == 1)),
+                              wavek_k=k if method == J.METHOD_WAVEK else None, cuda_graph=(N == 1),
+                              lanes=(8 if N == 1 else 1)),
                "e2e": {"value": e2e_val, "unit": "structures/s", "h2d_bytes_per_step": h2d,
                        "d2h_bytes_per_step": 8 * n_mb},
                "gpu_launches": int(launches), "gpu_launches_per_step": int(stats.kernel_launches),

@@ -46,6 +46,7 @@ typedef struct {
   int32_t n_micro_batches;                  /* geometry + gradient-ledger slots */
   int32_t n_slots;                          /* in-flight activation slots */
   int32_t device;                           /* CUDA ordinal */
+  int32_t n_lanes;                          /* concurrent micro-batch lanes (scratch sets), >= 1 */
 } janus_stage_desc;
 
 /* Host-side micro-batch: the LM payload.  Neighbour list in CSR by receiver
@@ -163,6 +164,9 @@ typedef struct {
   int32_t use_graphs;      /* capture the step once as a CUDA graph, replay it */
   int32_t dp_degree;       /* data-parallel replicas (NCCL mode), >= 1 */
   int32_t record_timeline; /* per-instruction CUDA events (disables graphs) */
+  int32_t lanes;           /* compute streams per device; micro-batch m runs on lane m % lanes.
+                              1 = strict list order (pipeline/bubble studies); >1 overlaps
+                              independent micro-batches (throughput at P=1) */
 } janus_exec_desc;
 
 typedef struct {

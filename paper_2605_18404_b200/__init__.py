@@ -42,7 +42,8 @@ class ModelDesc(ctypes.Structure):
 class StageDesc(ctypes.Structure):
     _fields_ = [("model", ModelDesc), ("unit_begin", ctypes.c_int32), ("unit_end", ctypes.c_int32),
                 ("max_atoms", ctypes.c_int32), ("max_edges", ctypes.c_int32), ("max_struct", ctypes.c_int32),
-                ("n_micro_batches", ctypes.c_int32), ("n_slots", ctypes.c_int32), ("device", ctypes.c_int32)]
+                ("n_micro_batches", ctypes.c_int32), ("n_slots", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("n_lanes", ctypes.c_int32)]
 
 
 class HostBatch(ctypes.Structure):
@@ -226,7 +227,7 @@ class Stage:
         o0, o1 = model.unit_offset(u0), model.unit_offset(u1)
         self.param_slice = slice(o0, o1)
         sl = np.ascontiguousarray(params_all[o0:o1], np.float32)
-        self.desc = StageDesc(model.desc(), u0, u1, max_atoms, max_edges, max_struct, n_mb, n_slots, device)
+        self.desc = StageDesc(model.desc(), u0, u1, max_atoms, max_edges, max_struct, n_mb, n_slots, device, 1)
         h = c_vp()
         check(_lib.janus_stage_create(ctypes.byref(self.desc), _p(sl), ctypes.byref(h)))
         self.h = h
@@ -365,7 +366,7 @@ class StepStats(ctypes.Structure):
 class ExecDesc(ctypes.Structure):
     _fields_ = [("n_stages", ctypes.c_int32), ("method", ctypes.c_int32), ("wavek_k", ctypes.c_int32),
                 ("n_micro_batches", ctypes.c_int32), ("local_stages", ctypes.c_int32), ("use_graphs", ctypes.c_int32),
-                ("dp_degree", ctypes.c_int32), ("record_timeline", ctypes.c_int32)]
+                ("dp_degree", ctypes.c_int32), ("record_timeline", ctypes.c_int32), ("lanes", ctypes.c_int32)]
 
 
 _sig("janus_trainer_create", c_int, c_vp, c_vp, c_vp, c_vp, c_int, c_vp)
@@ -418,10 +419,12 @@ class Trainer:
     def __init__(self, model: Model, params: np.ndarray, P: int, method: int, n_mb: int, k: int = 1,
                  max_atoms: int = 256, max_edges: int = 256 * 120, max_struct: int = 8, local: bool = True,
                  graphs: bool = False, timeline: bool = False, dp: int = 1, comm: "Comm | None" = None,
-                 rank: int = 0, device: int = 0):
+                 rank: int = 0, device: int = 0, lanes: int = 1):
         self.model, self.P, self.n_mb = model, P, n_mb
-        self.ed = ExecDesc(P, method, k, n_mb, 1 if local else 0, 1 if graphs else 0, dp, 1 if timeline else 0)
-        self.sd = StageDesc(model.desc(), 0, model.n_units, max_atoms, max_edges, max_struct, n_mb, n_mb, device)
+        self.ed = ExecDesc(P, method, k, n_mb, 1 if local else 0, 1 if graphs else 0, dp, 1 if timeline else 0,
+                           lanes)
+        self.sd = StageDesc(model.desc(), 0, model.n_units, max_atoms, max_edges, max_struct, n_mb, n_mb, device,
+                            lanes)
         p = np.ascontiguousarray(params, np.float32)
         h = c_vp()
         check(_lib.janus_trainer_create(ctypes.byref(self.ed), ctypes.byref(self.sd), _p(p),

@@ -222,11 +222,14 @@ __global__ void __launch_bounds__(NT) msg_fe_kernel(EdgeGeom g, MsgParams p, flo
 
 // ------------------------------------------------------------------- FF
 // Y_i = sum_{e in row i} w_e * am[col e]     (transposed scatter via symmetry)
-// q_e = < am[i] * v[j], w'_e >,  w' = c' g + c (SiLU'(z) z') B
+// q_e = < am[i] * v[j], w'_e >,  w' = c' g + c (SiLU'(z) z') B, and the force
+// F_i += sum_{e in row i} (q_e + q_rev(e)) u_e where, w' being symmetric,
+// q_rev(e) = < am[j] * v[i], w'_e > is evaluated in the same tile (no q buffer,
+// no separate scatter kernel; the row's warp owns F_i => deterministic).
 template <int H, int R>
 __global__ void __launch_bounds__(NT) msg_ff_kernel(EdgeGeom g, MsgParams p, float rc, const float* __restrict__ v,
                                                     const float* __restrict__ am, float* __restrict__ Y_out,
-                                                    float* __restrict__ q_out) {
+                                                    float* __restrict__ F) {
   using C = Cfg<H, R>;
   extern __shared__ __align__(16) float sm[];
   float* sA = sm;
@@ -251,10 +254,14 @@ __global__ void __launch_bounds__(NT) msg_ff_kernel(EdgeGeom g, MsgParams p, flo
   float acc_y[H / 32];
 #pragma unroll
   for (int q = 0; q < H / 32; ++q) acc_y[q] = 0.f;
-  float am_i[H / 32];
+  float am_i[H / 32], v_i[H / 32];
+  float fx = 0.f, fy = 0.f, fz = 0.f;
   if (has_row) {
 #pragma unroll
-    for (int q = 0; q < H / 32; ++q) am_i[q] = am[(size_t)row * H + lane + 32 * q];
+    for (int q = 0; q < H / 32; ++q) {
+      am_i[q] = am[(size_t)row * H + lane + 32 * q];
+      v_i[q] = v[(size_t)row * H + lane + 32 * q];
+    }
   }
   __syncthreads();
   for (int c0 = t.e0; c0 < t.e1; c0 += TE) {
@@ -295,11 +302,14 @@ __global__ void __launch_bounds__(NT) msg_ff_kernel(EdgeGeom g, MsgParams p, flo
 #pragma unroll
         for (int q = 0; q < H / 32; ++q) {
           const int h = lane + 32 * q;
-          acc_y[q] = fmaf(P0[h * LD + le], am[(size_t)j * H + h], acc_y[q]);
-          part = fmaf(am_i[q] * v[(size_t)j * H + h], P1[h * LD + le], part);
+          const float amj = am[(size_t)j * H + h];
+          acc_y[q] = fmaf(P0[h * LD + le], amj, acc_y[q]);
+          part = fmaf(fmaf(am_i[q], v[(size_t)j * H + h], amj * v_i[q]), P1[h * LD + le], part);
         }
-        part = dev::warp_sum(part);
-        if (lane == 0) q_out[x] = part;
+        part = dev::warp_sum(part);  // q_e + q_rev(e), identical in every lane
+        fx = fmaf(part, g.u[3 * x + 0], fx);
+        fy = fmaf(part, g.u[3 * x + 1], fy);
+        fz = fmaf(part, g.u[3 * x + 2], fz);
       }
     }
     __syncthreads();
@@ -307,23 +317,12 @@ __global__ void __launch_bounds__(NT) msg_ff_kernel(EdgeGeom g, MsgParams p, flo
   if (has_row) {
 #pragma unroll
     for (int q = 0; q < H / 32; ++q) Y_out[(size_t)row * H + lane + 32 * q] = acc_y[q];
+    if (lane == 0) {
+      F[3 * row + 0] += fx;
+      F[3 * row + 1] += fy;
+      F[3 * row + 2] += fz;
+    }
   }
-}
-
-// F_i += sum_{e in row i} (q_e + q_rev(e)) u_e   (one thread per row; order fixed)
-__global__ void msg_force_kernel(EdgeGeom g, const float* __restrict__ q, float* __restrict__ F) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= g.n_atoms) return;
-  float fx = 0.f, fy = 0.f, fz = 0.f;
-  for (int e = g.row_ptr[i]; e < g.row_ptr[i + 1]; ++e) {
-    const float s = q[e] + q[g.rev[e]];
-    fx = fmaf(s, g.u[3 * e + 0], fx);
-    fy = fmaf(s, g.u[3 * e + 1], fy);
-    fz = fmaf(s, g.u[3 * e + 2], fz);
-  }
-  F[3 * i + 0] += fx;
-  F[3 * i + 1] += fy;
-  F[3 * i + 2] += fz;
 }
 
 // ------------------------------------------------------------------- BF
@@ -628,7 +627,8 @@ __global__ void reduce_partials_kernel(const float* __restrict__ partial, int n_
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= PE) return;
   float s = 0.f;
-  for (int t = 0; t < n_tiles; ++t) s += partial[(size_t)t * PE + p];
+#pragma unroll 8
+  for (int t = 0; t < n_tiles; ++t) s += __ldg(partial + (size_t)t * PE + p);
   out[p] = s;
 }
 

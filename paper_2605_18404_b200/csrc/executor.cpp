@@ -69,9 +69,10 @@ namespace janus {
 namespace {
 
 struct VDev {
-  int id = 0;                    // schedule device index
-  cudaStream_t compute = nullptr, send = nullptr, recv = nullptr;
-  std::vector<cudaEvent_t> timing;  // start/end pairs
+  int id = 0;                          // schedule device index
+  cudaStream_t compute = nullptr;      // lane 0; OS runs here after joining the lanes
+  std::vector<cudaStream_t> lane;      // compute streams; micro-batch m -> lane m % size
+  cudaStream_t send = nullptr, recv = nullptr;
 };
 
 struct Rec {
@@ -197,13 +198,19 @@ size_t port_bytes_for(const janus_trainer* t, int block, int port, int mb) {
 }
 
 // ------------------------------------------------------------- transfers
+cudaStream_t lane_stream(const janus_trainer* t, const VDev& dv, int mb) {
+  (void)t;
+  return dv.lane[static_cast<size_t>(mb < 0 ? 0 : mb) % dv.lane.size()];
+}
+int lane_index(const VDev& dv, int mb) { return (mb < 0 ? 0 : mb) % static_cast<int>(dv.lane.size()); }
+
 void do_send(janus_trainer* t, VDev& dv, int flow, int mb, janus_stage* src, int sport, janus_stage* dst, int dport,
              int from_b, int to_b, int peer_dev) {
   float* sp;
   size_t sb;
   port_ptr(src, mb, sport, &sp, &sb);
   cudaEvent_t ready = next_event(t);
-  JANUS_CUDA(cudaEventRecord(ready, dv.compute));
+  JANUS_CUDA(cudaEventRecord(ready, lane_stream(t, dv, mb)));
   JANUS_CUDA(cudaStreamWaitEvent(dv.send, ready, 0));
   t->p2p_bytes += static_cast<int64_t>(sb);
   if (t->local) {
@@ -225,7 +232,7 @@ void do_recv(janus_trainer* t, VDev& dv, int flow, int mb, janus_stage* dst, int
   if (t->local) {
     const auto it = t->delivered.find({flow, mb, from_b, to_b});
     if (it == t->delivered.end()) throw deadlock_error("receive issued before its send (issue order)");
-    JANUS_CUDA(cudaStreamWaitEvent(dv.compute, it->second, 0));
+    JANUS_CUDA(cudaStreamWaitEvent(lane_stream(t, dv, mb), it->second, 0));
     t->delivered.erase(it);
   } else {
     float* dp;
@@ -235,7 +242,7 @@ void do_recv(janus_trainer* t, VDev& dv, int flow, int mb, janus_stage* dst, int
     JANUS_NCCL(ncclRecv(dp, db, ncclChar, peer_rank(t, peer_dev), t->comm->flow[flow], dv.recv));
     cudaEvent_t done = next_event(t);
     JANUS_CUDA(cudaEventRecord(done, dv.recv));
-    JANUS_CUDA(cudaStreamWaitEvent(dv.compute, done, 0));
+    JANUS_CUDA(cudaStreamWaitEvent(lane_stream(t, dv, mb), done, 0));
   }
 }
 
@@ -260,7 +267,7 @@ void mirror_back_send(janus_trainer* t, VDev& dv, int b, int mb) {
   size_t sb;
   port_ptr(f, mb, JANUS_PORT_BADJ_OUT, &sp, &sb);
   cudaEvent_t ready = next_event(t);
-  JANUS_CUDA(cudaEventRecord(ready, dv.compute));
+  JANUS_CUDA(cudaEventRecord(ready, lane_stream(t, dv, mb)));
   JANUS_CUDA(cudaStreamWaitEvent(dv.send, ready, 0));
   t->p2p_bytes += static_cast<int64_t>(sb);
   float* buf = t->mirror_buf[static_cast<size_t>(b) * t->ed.n_micro_batches + mb];
@@ -283,15 +290,47 @@ void mirror_back_recv_add(janus_trainer* t, VDev& dv, int b, int mb) {
   if (t->local) {
     const auto it = t->delivered.find({kFlowMirrorBack, mb, b, b});
     if (it == t->delivered.end()) throw deadlock_error("mirror cotangent not sent before BE");
-    JANUS_CUDA(cudaStreamWaitEvent(dv.compute, it->second, 0));
+    JANUS_CUDA(cudaStreamWaitEvent(lane_stream(t, dv, mb), it->second, 0));
     t->delivered.erase(it);
   } else {
     JANUS_NCCL(ncclRecv(buf, db, ncclChar, peer_rank(t, t->F_dev[static_cast<size_t>(b)]), t->comm->flow[kFlowMirrorBack + (b & 1)], dv.recv));
     cudaEvent_t done = next_event(t);
     JANUS_CUDA(cudaEventRecord(done, dv.recv));
-    JANUS_CUDA(cudaStreamWaitEvent(dv.compute, done, 0));
+    JANUS_CUDA(cudaStreamWaitEvent(lane_stream(t, dv, mb), done, 0));
   }
-  add_into(dp, buf, static_cast<int64_t>(db / sizeof(float)), dv.compute);
+  add_into(dp, buf, static_cast<int64_t>(db / sizeof(float)), lane_stream(t, dv, mb));
+}
+
+// Pass 3 pruned the comm pair between adjacent virtual stages that share a
+// device (transform.hpp:124-136).  When they are different stage objects
+// (1F1B-2nd: two blocks per device) the payload still has to move: a local
+// port copy on the compute stream, in list order.
+void local_handoff(janus_trainer* t, VDev& dv, int mb, int from_vs, int to_vs) {
+  const int P = t->P, S = 2 * P;
+  if (to_vs < 0 || to_vs >= S) return;
+  if (t->sched.stage_map[static_cast<size_t>(from_vs)] != t->sched.stage_map[static_cast<size_t>(to_vs)]) return;
+  if ((from_vs == P - 1 && to_vs == P) || (from_vs == P && to_vs == P - 1)) return;  // fold point: same block
+  const bool fwd = to_vs == from_vs + 1;
+  janus_stage *src, *dst;
+  int sp, dp;
+  if (fwd && to_vs < P) {  // FE chain
+    src = t->E[static_cast<size_t>(from_vs)], dst = t->E[static_cast<size_t>(to_vs)], sp = JANUS_PORT_ACT_OUT, dp = JANUS_PORT_ACT_IN;
+  } else if (fwd) {  // FF chain (blocks descending)
+    src = t->F[static_cast<size_t>(block_of(t, from_vs))], dst = t->F[static_cast<size_t>(block_of(t, to_vs))];
+    sp = JANUS_PORT_ADJ_OUT, dp = JANUS_PORT_ADJ_IN;
+  } else if (to_vs >= P) {  // BF chain (blocks ascending)
+    src = t->F[static_cast<size_t>(block_of(t, from_vs))], dst = t->F[static_cast<size_t>(block_of(t, to_vs))];
+    sp = JANUS_PORT_TAN_OUT, dp = JANUS_PORT_TAN_IN;
+  } else {  // BE chain
+    src = t->E[static_cast<size_t>(from_vs)], dst = t->E[static_cast<size_t>(to_vs)], sp = JANUS_PORT_BADJ_OUT, dp = JANUS_PORT_BADJ_IN;
+  }
+  if (src == dst) return;
+  float *a, *b;
+  size_t na, nb;
+  port_ptr(src, mb, sp, &a, &na);
+  port_ptr(dst, mb, dp, &b, &nb);
+  if (na != nb) throw state_error("local hand-off size mismatch");
+  JANUS_CUDA(cudaMemcpyAsync(b, a, na, cudaMemcpyDeviceToDevice, lane_stream(t, dv, mb)));
 }
 
 // ------------------------------------------------------------ one instruction
@@ -303,21 +342,25 @@ void timed(janus_trainer* t, VDev& dv, const Instruction& in, auto&& body) {
   Rec r{in.device, static_cast<int>(in.kind), in.micro_batch, nullptr, nullptr};
   JANUS_CUDA(cudaEventCreate(&r.a));
   JANUS_CUDA(cudaEventCreate(&r.b));
-  JANUS_CUDA(cudaEventRecord(r.a, dv.compute));
+  cudaStream_t cs = lane_stream(t, dv, in.micro_batch);
+  JANUS_CUDA(cudaEventRecord(r.a, cs));
   body();
-  JANUS_CUDA(cudaEventRecord(r.b, dv.compute));
+  JANUS_CUDA(cudaEventRecord(r.b, cs));
   t->recs.push_back(r);
 }
 
 void execute(janus_trainer* t, const Instruction& in, const janus_opt& opt) {
   VDev& dv = vdev(t, in.device);
   const int mb = in.micro_batch;
+  cudaStream_t cs = lane_stream(t, dv, mb);
+  const int ln = lane_index(dv, mb);
   switch (in.kind) {
     case InstrKind::LM:
       return;  // geometry is uploaded to every stage by janus_trainer_load
     case InstrKind::FE: {
       const int b = block_of(t, in.virtual_stage);
-      timed(t, dv, in, [&] { stage_fe(t->E[static_cast<size_t>(b)], mb, mb, dv.compute); });
+      timed(t, dv, in, [&] { stage_fe(t->E[static_cast<size_t>(b)], mb, mb, cs, ln); });
+      local_handoff(t, dv, mb, in.virtual_stage, in.virtual_stage + 1);
       if (t->onef1b) mirror_act_send(t, dv, b, mb);
       return;
     }
@@ -326,31 +369,39 @@ void execute(janus_trainer* t, const Instruction& in, const janus_opt& opt) {
       janus_stage* f = t->F[static_cast<size_t>(b)];
       if (t->onef1b) mirror_act_recv(t, dv, b, mb);
       timed(t, dv, in, [&] {
-        if (in.has_flag(kFlagRecompute)) stage_fe(f, mb, mb, dv.compute);  // regenerate FE activations
-        stage_ff(f, mb, mb, dv.compute);
+        if (in.has_flag(kFlagRecompute)) stage_fe(f, mb, mb, cs, ln);  // regenerate FE activations
+        stage_ff(f, mb, mb, cs, ln);
       });
+      local_handoff(t, dv, mb, in.virtual_stage, in.virtual_stage + 1);
       return;
     }
     case InstrKind::BF: {
       const int b = block_of(t, in.virtual_stage);
       janus_stage* f = t->F[static_cast<size_t>(b)];
       timed(t, dv, in, [&] {
-        stage_bf(f, mb, mb, dv.compute);
-        if (t->onef1b) stage_be(f, mb, mb, dv.compute, /*inj_only=*/true);
+        stage_bf(f, mb, mb, cs, ln);
+        if (t->onef1b) stage_be(f, mb, mb, cs, /*inj_only=*/true, ln);
       });
       if (t->onef1b) mirror_back_send(t, dv, b, mb);
+      local_handoff(t, dv, mb, in.virtual_stage, in.virtual_stage - 1);
       return;
     }
     case InstrKind::BE: {
       const int b = block_of(t, in.virtual_stage);
       timed(t, dv, in, [&] {
-        stage_be(t->E[static_cast<size_t>(b)], mb, mb, dv.compute);
+        stage_be(t->E[static_cast<size_t>(b)], mb, mb, cs, false, ln);
         if (t->onef1b) mirror_back_recv_add(t, dv, b, mb);
       });
+      local_handoff(t, dv, mb, in.virtual_stage, in.virtual_stage - 1);
       return;
     }
     case InstrKind::OS: {
       if (t->local) return;  // local mode: optimizer runs after the join (finalize_local)
+      for (size_t l = 1; l < dv.lane.size(); ++l) {  // all micro-batch lanes must be done
+        cudaEvent_t e = next_event(t);
+        JANUS_CUDA(cudaEventRecord(e, dv.lane[l]));
+        JANUS_CUDA(cudaStreamWaitEvent(dv.compute, e, 0));
+      }
       timed(t, dv, in, [&] {
         std::vector<janus_stage*> mine;  // this rank's objects, block order
         for (int b = 0; b < t->P; ++b) {
@@ -399,7 +450,7 @@ void issue_step(janus_trainer* t, const janus_opt& opt) {
 void fork_join_begin(janus_trainer* t) {
   JANUS_CUDA(cudaEventRecord(t->anchor, t->root));
   for (auto& d : t->devs) {
-    JANUS_CUDA(cudaStreamWaitEvent(d.compute, t->anchor, 0));
+    for (cudaStream_t l : d.lane) JANUS_CUDA(cudaStreamWaitEvent(l, t->anchor, 0));
     JANUS_CUDA(cudaStreamWaitEvent(d.send, t->anchor, 0));
     JANUS_CUDA(cudaStreamWaitEvent(d.recv, t->anchor, 0));
   }
@@ -407,7 +458,10 @@ void fork_join_begin(janus_trainer* t) {
 
 void fork_join_end(janus_trainer* t) {
   for (auto& d : t->devs) {
-    for (cudaStream_t s : {d.send, d.recv, d.compute}) {
+    std::vector<cudaStream_t> all = d.lane;
+    all.push_back(d.send);
+    all.push_back(d.recv);
+    for (cudaStream_t s : all) {
       cudaEvent_t e = next_event(t);
       JANUS_CUDA(cudaEventRecord(e, s));
       JANUS_CUDA(cudaStreamWaitEvent(t->root, e, 0));
@@ -445,6 +499,7 @@ janus_trainer* trainer_create(const janus_exec_desc& ed, const janus_stage_desc&
   t->local = ed.local_stages != 0;
   t->onef1b = ed.method == 2;
   if (ed.dp_degree < 1) t->ed.dp_degree = 1;
+  if (ed.lanes < 1) t->ed.lanes = 1;
   if (ed.n_micro_batches < 1) throw domain_error("n_micro_batches must be >= 1");
   if (!t->local && !comm) throw config_error("NCCL mode needs a janus_comm");
   if (t->local && t->ed.dp_degree != 1) throw config_error("data parallelism needs NCCL mode");
@@ -495,7 +550,9 @@ janus_trainer* trainer_create(const janus_exec_desc& ed, const janus_stage_desc&
   for (int d = 0; d < nd; ++d) {
     VDev& v = t->devs[static_cast<size_t>(d)];
     v.id = t->local ? d : t->my_dev;
-    JANUS_CUDA(cudaStreamCreateWithFlags(&v.compute, cudaStreamNonBlocking));
+    v.lane.resize(static_cast<size_t>(std::max(1, t->ed.lanes)));
+    for (auto& l : v.lane) JANUS_CUDA(cudaStreamCreateWithFlags(&l, cudaStreamNonBlocking));
+    v.compute = v.lane[0];
     JANUS_CUDA(cudaStreamCreateWithFlags(&v.send, cudaStreamNonBlocking));
     JANUS_CUDA(cudaStreamCreateWithFlags(&v.recv, cudaStreamNonBlocking));
   }
@@ -508,6 +565,7 @@ janus_trainer* trainer_create(const janus_exec_desc& ed, const janus_stage_desc&
     d.unit_end = t->plan.blocks[static_cast<size_t>(b)].second;
     d.n_micro_batches = ed.n_micro_batches;
     d.n_slots = ed.n_micro_batches;
+    d.n_lanes = std::max(1, t->ed.lanes);
     const int64_t off = mc.unit_param_offset(d.unit_begin);
     janus_stage* st = stage_create(d, all_params + off);
     t->owned.push_back(st);
@@ -578,7 +636,7 @@ void trainer_destroy(janus_trainer* t) {
     cudaEventDestroy(r.b);
   }
   for (auto& d : t->devs) {
-    cudaStreamDestroy(d.compute);
+    for (cudaStream_t l : d.lane) cudaStreamDestroy(l);
     cudaStreamDestroy(d.send);
     cudaStreamDestroy(d.recv);
   }

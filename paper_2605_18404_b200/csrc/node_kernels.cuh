@@ -39,71 +39,140 @@ struct InDsiluOmega {
 };
 
 // out[i][n] = sum_k op(X[i][k]) M[k][n] (+ bias[n]) (+ add1[i][n]) (+ add2[i][n])
-// One CTA = 16 rows x all H columns; thread owns H/16 consecutive columns.
+// One CTA = 256/H rows x H columns, one output per thread; the transformed
+// input rows are staged in smem (op applied once per element), M is read
+// through L1 (every CTA reads all of M: 16 KB, L2-resident).
 template <int H, typename InOp>
 __global__ void __launch_bounds__(256) gemm_rows_kernel(int rows, const float* __restrict__ X, const float* __restrict__ M,
                                                         const float* __restrict__ bias, const float* add1, const float* add2,
                                                         float* out, InOp op) {
-  constexpr int CPT = H / 16;
-  __shared__ __align__(16) float sx[16][H];
-  const int r0 = blockIdx.x * 16;
-  for (int x = threadIdx.x; x < 16 * H; x += 256) {
-    const int r = x / H, k = x % H;
-    sx[r][k] = (r0 + r < rows) ? op(r0 + r, k, X[(size_t)(r0 + r) * H + k]) : 0.f;
-  }
+  constexpr int RB = 256 / H;
+  __shared__ __align__(16) float sx[RB][H];
+  const int r0 = blockIdx.x * RB;
+  const int r = threadIdx.x / H, c = threadIdx.x % H;
+  const int i = r0 + r;
+  sx[r][c] = (i < rows) ? op(i, c, X[(size_t)i * H + c]) : 0.f;
   __syncthreads();
-  const int r = threadIdx.x / 16, c0 = (threadIdx.x % 16) * CPT;
-  float acc[CPT];
+  float acc0 = 0.f, acc1 = 0.f;
+#pragma unroll 16
+  for (int k = 0; k < H; k += 2) {
+    acc0 = fmaf(sx[r][k], __ldg(M + (size_t)k * H + c), acc0);
+    acc1 = fmaf(sx[r][k + 1], __ldg(M + (size_t)(k + 1) * H + c), acc1);
+  }
+  if (i >= rows) return;
+  const size_t o = (size_t)i * H + c;
+  float y = acc0 + acc1;
+  if (bias) y += bias[c];
+  if (add1) y += add1[o];
+  if (add2) y += add2[o];
+  out[o] = y;
+}
+
+// Weight gradients over atoms, two deterministic stages:
+//  (1) wgrad_partial: CTA c reduces rows [64c, 64c+64): G_c = sum_i opA(a_i)^T b_i
+//      (+ a2_i^T b2_i), plus up to two column sums cs1 = sum_i x1_i, cs2 = sum_i x2_i;
+//  (2) wgrad_final: out = sum_c G_c in chunk order.
+// Partial layout per chunk: [H*H | H | H].
+constexpr int kWChunk = 64;
+
+template <int H, typename InOp>
+__global__ void __launch_bounds__(256) wgrad_partial_kernel(int rows, const float* __restrict__ a, const float* __restrict__ b,
+                                                            const float* __restrict__ a2, const float* __restrict__ b2,
+                                                            const float* __restrict__ x1, const float* __restrict__ x2,
+                                                            float* __restrict__ part, InOp op) {
+  static_assert(H == 64, "tile mapping assumes H = 64");
+  __shared__ __align__(16) float sa[kWChunk][H + 4];
+  __shared__ __align__(16) float sb[kWChunk][H + 4];
+  const int i0 = blockIdx.x * kWChunk;
+  const int n = min(kWChunk, rows - i0);
+  const int kb = (threadIdx.x >> 4) * 4, hb = (threadIdx.x & 15) * 4;
+  float acc[4][4];
 #pragma unroll
-  for (int j = 0; j < CPT; ++j) acc[j] = 0.f;
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) acc[x][y] = 0.f;
+  for (int pass = 0; pass < (a2 ? 2 : 1); ++pass) {
+    const float* A = pass ? a2 : a;
+    const float* B = pass ? b2 : b;
+    __syncthreads();
+    for (int x = threadIdx.x; x < kWChunk * H; x += 256) {
+      const int r = x / H, c = x % H;
+      const bool ok = r < n;
+      sa[r][c] = ok ? (pass ? A[(size_t)(i0 + r) * H + c] : op(i0 + r, c, A[(size_t)(i0 + r) * H + c])) : 0.f;
+      sb[r][c] = ok ? B[(size_t)(i0 + r) * H + c] : 0.f;
+    }
+    __syncthreads();
 #pragma unroll 4
-  for (int k = 0; k < H; ++k) {
-    const float a = sx[r][k];
+    for (int r = 0; r < n; ++r) {
+      const float4 va = *reinterpret_cast<const float4*>(&sa[r][kb]);
+      const float4 vb = *reinterpret_cast<const float4*>(&sb[r][hb]);
+      const float xa[4] = {va.x, va.y, va.z, va.w}, xb[4] = {vb.x, vb.y, vb.z, vb.w};
 #pragma unroll
-    for (int j = 0; j < CPT; j += 4) {
-      const float4 m = *reinterpret_cast<const float4*>(M + (size_t)k * H + c0 + j);
-      acc[j + 0] = fmaf(a, m.x, acc[j + 0]);
-      acc[j + 1] = fmaf(a, m.y, acc[j + 1]);
-      acc[j + 2] = fmaf(a, m.z, acc[j + 2]);
-      acc[j + 3] = fmaf(a, m.w, acc[j + 3]);
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) acc[x][y] = fmaf(xa[x], xb[y], acc[x][y]);
     }
   }
-  const int i = r0 + r;
-  if (i >= rows) return;
+  float* P = part + (size_t)blockIdx.x * (H * H + 2 * H);
 #pragma unroll
-  for (int j = 0; j < CPT; ++j) {
-    const size_t o = (size_t)i * H + c0 + j;
-    float y = acc[j];
-    if (bias) y += bias[c0 + j];
-    if (add1) y += add1[o];
-    if (add2) y += add2[o];
-    out[o] = y;
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) P[(kb + x) * H + hb + y] = acc[x][y];
+  if (threadIdx.x < 2 * H) {
+    const float* X = threadIdx.x < H ? x1 : x2;
+    const int c = threadIdx.x % H;
+    float s = 0.f;
+    if (X)
+      for (int r = 0; r < n; ++r) s += X[(size_t)(i0 + r) * H + c];
+    P[H * H + threadIdx.x] = s;
   }
 }
 
-// G[k][n] (+)= sum_i opA(a[i][k]) b[i][n]  (+ sum_i a2[i][k] b2[i][n]); thread per output.
-template <int H, typename InOp>
-__global__ void wgrad_kernel(int rows, const float* __restrict__ a, const float* __restrict__ b,
-                             const float* __restrict__ a2, const float* __restrict__ b2, float* __restrict__ G,
-                             int accumulate, InOp op) {
+// out_G (if non-null) = sum_c G_c ; cs_out1/2 = sum_c cs_c (fixed chunk order)
+template <int H>
+__global__ void wgrad_final_kernel(int n_chunks, const float* __restrict__ part, float* __restrict__ G,
+                                   float* __restrict__ cs_out1, float* __restrict__ cs_out2) {
   const int o = blockIdx.x * blockDim.x + threadIdx.x;
-  if (o >= H * H) return;
-  const int k = o / H, n = o % H;
+  constexpr int W = H * H + 2 * H;
+  if (o >= W) return;
+  float* dst = o < H * H ? G : (o < H * H + H ? cs_out1 : cs_out2);
+  if (!dst) return;
   float s = 0.f;
-  for (int i = 0; i < rows; ++i) s = fmaf(op(i, k, a[(size_t)i * H + k]), b[(size_t)i * H + n], s);
-  if (a2)
-    for (int i = 0; i < rows; ++i) s = fmaf(a2[(size_t)i * H + k], b2[(size_t)i * H + n], s);
-  G[o] = accumulate ? G[o] + s : s;
+#pragma unroll 4
+  for (int c = 0; c < n_chunks; ++c) s += part[(size_t)c * W + o];
+  dst[o < H * H ? o : (o - H * H) % H] = s;
 }
 
-// out[n] = sum_i op(x[i][n])
-template <int H, typename InOp>
-__global__ void colsum_kernel(int rows, const float* __restrict__ x, float* __restrict__ out, InOp op) {
-  const int n = threadIdx.x;
-  if (n >= H) return;
+// out[z][k] = sum_{i: Z_i = z} x[i][k]  (chunked; partial [chunk][S*H]).  When
+// x is null the summand is the scalar eps[struct_id[i]] (readout bias grads, k = 0).
+template <int H>
+__global__ void species_sum_partial_kernel(int rows, int S, const int* __restrict__ species, const float* __restrict__ x,
+                                           const float* __restrict__ eps, const int* __restrict__ struct_id,
+                                           float* __restrict__ part) {
+  const int i0 = blockIdx.x * kWChunk;
+  const int n = min(kWChunk, rows - i0);
+  for (int o = threadIdx.x; o < S * H; o += blockDim.x) {
+    const int z = o / H, k = o % H;
+    float s = 0.f;
+    for (int r = 0; r < n; ++r) {
+      const int i = i0 + r;
+      if (species[i] != z) continue;
+      s += x ? x[(size_t)i * H + k] : (k == 0 ? eps[struct_id[i]] : 0.f);
+    }
+    part[(size_t)blockIdx.x * S * H + o] = s;
+  }
+}
+
+template <int H>
+__global__ void species_sum_final_kernel(int n_chunks, int S, int stride_out, const float* __restrict__ part,
+                                         float* __restrict__ out) {
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= S * H) return;
+  const int z = o / H, k = o % H;
+  if (stride_out == 1 && k != 0) return;  // scalar mode: one value per species
   float s = 0.f;
-  for (int i = 0; i < rows; ++i) s += op(i, n, x[(size_t)i * H + n]);
-  out[n] = s;
+  for (int c = 0; c < n_chunks; ++c) s += part[(size_t)c * S * H + o];
+  out[stride_out == 1 ? z : o] = s;
 }
 
 // ------------------------------------------------------------ elementwise
@@ -163,19 +232,6 @@ __global__ void embed_fe_kernel(int n_atoms, const int* __restrict__ species, co
   h[x] = Emb[(size_t)species[i] * H + k];
 }
 
-// dEmb[z][k] = sum_{i: Z_i = z} b[i][k]  (thread per (z,k), atom order)
-template <int H>
-__global__ void embed_be_kernel(int n_atoms, int n_species, const int* __restrict__ species, const float* __restrict__ b,
-                                float* __restrict__ dEmb) {
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  if (x >= n_species * H) return;
-  const int z = x / H, k = x % H;
-  float s = 0.f;
-  for (int i = 0; i < n_atoms; ++i)
-    if (species[i] == z) s += b[(size_t)i * H + k];
-  dEmb[x] = s;
-}
-
 // e_i = <SiLU(t_i), omega> + bias[Z_i]   (warp per atom)
 template <int H>
 __global__ void readout_energy_kernel(int n_atoms, const float* __restrict__ t, const float* __restrict__ omega,
@@ -228,17 +284,6 @@ __global__ void force_loss_kernel(int n3, const float* __restrict__ F, const flo
     __syncthreads();
   }
   if (threadIdx.x == 0) *loss_F = red[0];
-}
-
-// dbias[z] = sum_{i: Z_i = z} eps_{s(i)}
-__global__ void bias_grad_kernel(int n_atoms, int n_species, const int* __restrict__ species,
-                                 const int* __restrict__ struct_id, const float* __restrict__ eps, float* __restrict__ db) {
-  const int z = threadIdx.x;
-  if (z >= n_species) return;
-  float s = 0.f;
-  for (int i = 0; i < n_atoms; ++i)
-    if (species[i] == z) s += eps[struct_id[i]];
-  db[z] = s;
 }
 
 // ----------------------------------------------------------- optimizer

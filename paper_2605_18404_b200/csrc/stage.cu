@@ -62,21 +62,34 @@ template <typename Op = node::InId>
 void gemm(cudaStream_t s, int rows, const float* X, const float* M, const float* bias, const float* add1,
           const float* add2, float* out, Op op = Op{}) {
   if (rows <= 0) return;
-  node::gemm_rows_kernel<kH, Op><<<blocks(rows, 16), 256, 0, s>>>(rows, X, M, bias, add1, add2, out, op);
+  node::gemm_rows_kernel<kH, Op><<<blocks(rows, 256 / kH), 256, 0, s>>>(rows, X, M, bias, add1, add2, out, op);
   JANUS_LAUNCH_CHECK("gemm_rows");
 }
 
+// G = sum_i op(a_i)^T b_i (+ a2_i^T b2_i) over atoms, optional column sums
+// cs_out1 = sum_i x1_i, cs_out2 = sum_i x2_i — two deterministic stages.
+struct Colsums {
+  const float* x1 = nullptr;
+  float* out1 = nullptr;
+  const float* x2 = nullptr;
+  float* out2 = nullptr;
+};
+
 template <typename Op = node::InId>
-void wgrad(cudaStream_t s, int rows, const float* a, const float* b, const float* a2, const float* b2, float* G,
-           Op op = Op{}) {
-  node::wgrad_kernel<kH, Op><<<blocks(kH * kH, 256), 256, 0, s>>>(rows, a, b, a2, b2, G, 0, op);
+void wgrad(Scratch& sc, cudaStream_t s, int rows, const float* a, const float* b, const float* a2, const float* b2,
+           float* G, Op op = Op{}, Colsums cs = {}) {
+  const int chunks = blocks(rows, node::kWChunk);
+  node::wgrad_partial_kernel<kH, Op><<<chunks, 256, 0, s>>>(rows, a, b, a2, b2, cs.x1, cs.x2, sc.wpart, op);
+  node::wgrad_final_kernel<kH><<<blocks(kH * kH + 2 * kH, 256), 256, 0, s>>>(chunks, sc.wpart, G, cs.out1, cs.out2);
   JANUS_LAUNCH_CHECK("wgrad");
 }
 
-template <typename Op = node::InId>
-void colsum(cudaStream_t s, int rows, const float* x, float* out, Op op = Op{}) {
-  node::colsum_kernel<kH, Op><<<1, kH, 0, s>>>(rows, x, out, op);
-  JANUS_LAUNCH_CHECK("colsum");
+// out[z][k] = sum_{Z_i = z} x[i][k]; x == null: out[z] = sum_{Z_i = z} eps[s(i)]
+void species_sum(janus_stage* st, Scratch& sc, cudaStream_t s, const DevGeo& g, const float* x, const float* eps, float* out) {
+  const int chunks = blocks(g.n_atoms, node::kWChunk), S = st->m.n_species;
+  node::species_sum_partial_kernel<kH><<<chunks, 256, 0, s>>>(g.n_atoms, S, g.species, x, eps, g.struct_id, sc.wpart);
+  node::species_sum_final_kernel<kH><<<blocks(S * kH, 256), 256, 0, s>>>(chunks, S, x ? kH : 1, sc.wpart, out);
+  JANUS_LAUNCH_CHECK("species_sum");
 }
 
 void copy(cudaStream_t s, float* dst, const float* src, size_t n) {
@@ -156,6 +169,11 @@ const float* in_m(const janus_stage* st, const Slot& sl, int u, int n) {
 
 float* ledger(janus_stage* st, float* base, int mb, int u) {
   return base + static_cast<size_t>(mb) * st->n_params + st->uoff[static_cast<size_t>(u - st->u0)];
+}
+
+Scratch& lane_of(janus_stage* st, int lane) {
+  if (lane < 0 || lane >= static_cast<int>(st->lanes.size())) throw domain_error("lane index out of range");
+  return st->lanes[static_cast<size_t>(lane)];
 }
 
 void check_mb_slot(const janus_stage* st, int mb, int slot) {
@@ -273,16 +291,19 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
       sl.eps = dalloc<float>(st, static_cast<size_t>(d.max_struct), false);
       sl.loss = dalloc<float>(st, 2, false);
     }
-    st->wh = dalloc<float>(st, NH, false);
-    st->wm = dalloc<float>(st, NH, false);
-    st->s1 = dalloc<float>(st, NH, false);
-    st->s2 = dalloc<float>(st, NH, false);
-    st->s3 = dalloc<float>(st, NH, false);
-    st->s4 = dalloc<float>(st, NH, false);
-    st->s5 = dalloc<float>(st, NH, false);
-    st->q = dalloc<float>(st, NE, false);
-    st->partial = dalloc<float>(st, NA * static_cast<size_t>(EC::PE), false);
-    st->zero = dalloc<float>(st, NH, false);
+    st->lanes.resize(static_cast<size_t>(std::max(1, d.n_lanes)));
+    for (Scratch& sc : st->lanes) {
+      sc.wh = dalloc<float>(st, NH, false);
+      sc.wm = dalloc<float>(st, NH, false);
+      sc.s1 = dalloc<float>(st, NH, false);
+      sc.s2 = dalloc<float>(st, NH, false);
+      sc.s3 = dalloc<float>(st, NH, false);
+      sc.s4 = dalloc<float>(st, NH, false);
+      sc.s5 = dalloc<float>(st, NH, false);
+      sc.partial = dalloc<float>(st, NA * static_cast<size_t>(EC::PE), false);
+      const size_t chunks = (NA + node::kWChunk - 1) / node::kWChunk;
+      sc.wpart = dalloc<float>(st, chunks * std::max<size_t>(kH * kH + 2 * kH, static_cast<size_t>(m.n_species) * kH), false);
+    }
     JANUS_CUDA(cudaFuncSetAttribute(edge::msg_fe_kernel<kH, kR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge::fe_smem<kH, kR>()));
     JANUS_CUDA(cudaFuncSetAttribute(edge::msg_ff_kernel<kH, kR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge::ff_smem<kH, kR>()));
     JANUS_CUDA(cudaFuncSetAttribute(edge::msg_bf_kernel<kH, kR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge::bf_smem<kH, kR>()));
@@ -371,8 +392,9 @@ void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_
 }
 
 // ================================================================== FE
-void stage_fe(janus_stage* st, int mb, int slot, cudaStream_t s) {
+void stage_fe(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
   check_mb_slot(st, mb, slot);
+  Scratch& sc = lane_of(st, lane);
   const DevGeo& g = st->geo[static_cast<size_t>(mb)];
   Slot& sl = st->slots[static_cast<size_t>(slot)];
   sl.mb = mb;
@@ -423,15 +445,16 @@ void stage_fe(janus_stage* st, int mb, int slot, cudaStream_t s) {
 }
 
 // ================================================================== FF
-void stage_ff(janus_stage* st, int mb, int slot, cudaStream_t s) {
+void stage_ff(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
   check_mb_slot(st, mb, slot);
+  Scratch& sc = lane_of(st, lane);
   const DevGeo& g = st->geo[static_cast<size_t>(mb)];
   Slot& sl = st->slots[static_cast<size_t>(slot)];
   const int N = g.n_atoms, H = kH, R = kR, L = st->m.L;
   const size_t NH = static_cast<size_t>(N) * H;
   const EdgeGeom eg = edge_geom(g);
-  float* wh = st->wh;
-  float* wm = st->wm;
+  float* wh = sc.wh;
+  float* wm = sc.wm;
   if (st->has_readout) {
     JANUS_CUDA(cudaMemsetAsync(sl.F, 0, sizeof(float) * 3 * N, s));
   } else {
@@ -452,18 +475,17 @@ void stage_ff(janus_stage* st, int mb, int slot, cudaStream_t s) {
       }
       case kUpd: {  // a_m = ((a' V^T) SiLU'(p)) U^T
         copy(s, b.ff_a, wh, NH);
-        gemm(s, N, wh, T + H * H, nullptr, nullptr, nullptr, st->s1);
-        gemm(s, N, st->s1, T, nullptr, nullptr, nullptr, wm, node::InMulDsilu{b.p, H});
+        gemm(s, N, wh, T + H * H, nullptr, nullptr, nullptr, sc.s1);
+        gemm(s, N, sc.s1, T, nullptr, nullptr, nullptr, wm, node::InMulDsilu{b.p, H});
         break;
       }
       case kMsg: {
         copy(s, b.ff_a, wm, NH);
         if (g.n_tiles > 0)
-          edge::msg_ff_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::ff_smem<kH, kR>(), s>>>(eg, msg_params(st, u), st->m.r_c, b.v, b.ff_a, b.ff_Y, st->q);
+          edge::msg_ff_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::ff_smem<kH, kR>(), s>>>(eg, msg_params(st, u), st->m.r_c, b.v, b.ff_a, b.ff_Y, sl.F);
         else
           JANUS_CUDA(cudaMemsetAsync(b.ff_Y, 0, sizeof(float) * NH, s));
         gemm(s, N, b.ff_Y, T + H * H, nullptr, wh, nullptr, wh);  // a_h += Y W^T
-        edge::msg_force_kernel<<<blocks(N, 128), 128, 0, s>>>(eg, st->q, sl.F);
         break;
       }
       case kEmbed:
@@ -484,15 +506,16 @@ void stage_ff(janus_stage* st, int mb, int slot, cudaStream_t s) {
 }
 
 // ================================================================== BF
-void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s) {
+void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
   check_mb_slot(st, mb, slot);
+  Scratch& sc = lane_of(st, lane);
   const DevGeo& g = st->geo[static_cast<size_t>(mb)];
   Slot& sl = st->slots[static_cast<size_t>(slot)];
   const int N = g.n_atoms, H = kH, R = kR, L = st->m.L;
   const size_t NH = static_cast<size_t>(N) * H;
   const EdgeGeom eg = edge_geom(g);
-  float* ah = st->wh;
-  float* am = st->wm;
+  float* ah = sc.wh;
+  float* am = sc.wm;
   const float* Fbar = sl.Fbar;
   JANUS_CUDA(cudaMemsetAsync(st->g2 + static_cast<size_t>(mb) * st->n_params, 0, sizeof(float) * st->n_params, s));
   if (st->u0 == 0) {
@@ -513,44 +536,43 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s) {
         break;
       case kMsg: {
         const float* W = P + R * H + H + H * H + H;
-        gemm(s, N, ah, W, nullptr, nullptr, nullptr, st->s1);  // vdot
+        gemm(s, N, ah, W, nullptr, nullptr, nullptr, sc.s1);  // vdot
         if (g.n_tiles > 0) {
           edge::msg_bf_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::bf_smem<kH, kR>(), s>>>(
-              eg, msg_params(st, u), st->m.r_c, b.v, st->s1, b.ff_a, Fbar, am, st->s2, st->partial);
+              eg, msg_params(st, u), st->m.r_c, b.v, sc.s1, b.ff_a, Fbar, am, sc.s2, sc.partial);
           JANUS_LAUNCH_CHECK("msg_bf");
-          edge::reduce_partials_kernel<<<blocks(EC::PE, 256), 256, 0, s>>>(st->partial, g.n_tiles, EC::PE, G2);
+          edge::reduce_partials_kernel<<<blocks(EC::PE, 256), 256, 0, s>>>(sc.partial, g.n_tiles, EC::PE, G2);
         } else {
           JANUS_CUDA(cudaMemsetAsync(am, 0, sizeof(float) * NH, s));
-          JANUS_CUDA(cudaMemsetAsync(st->s2, 0, sizeof(float) * NH, s));
+          JANUS_CUDA(cudaMemsetAsync(sc.s2, 0, sizeof(float) * NH, s));
         }
-        gemm(s, N, st->s2, T + H * H, nullptr, nullptr, nullptr, b.inj);                  // hbar^F = X W^T
-        wgrad(s, N, in_h(st, sl, u, N), st->s2, ah, b.ff_Y, G2 + EC::PE);             // dW2 = h^T X + abar^T Y
+        gemm(s, N, sc.s2, T + H * H, nullptr, nullptr, nullptr, b.inj);                  // hbar^F = X W^T
+        wgrad(sc, s, N, in_h(st, sl, u, N), sc.s2, ah, b.ff_Y, G2 + EC::PE);         // dW2 = h^T X + abar^T Y
         break;
       }
       case kUpd: {
         const float *Um = P, *V = P + H * H + H;
         float *dU = G2, *dups = G2 + H * H, *dV = G2 + H * H + H;
-        gemm(s, N, am, Um, nullptr, nullptr, nullptr, st->s1);             // pdot
-        gemm(s, N, b.ff_a, T + H * H, nullptr, nullptr, nullptr, st->s2);  // r = a' V^T
-        node::upd_bf_ew_kernel<<<blocks(NH, 256), 256, 0, s>>>(static_cast<int>(NH), st->s2, st->s1, b.p, st->s3,
-                                                               st->s4, st->s5);
-        gemm(s, N, st->s3, T, nullptr, nullptr, nullptr, b.inj);           // mbar^F = pbar U^T
-        wgrad(s, N, st->s5, b.ff_a, nullptr, nullptr, dV);                 // dV2 = u^T a'
-        wgrad(s, N, in_m(st, sl, u, N), st->s3, am, st->s4, dU);           // dU2 = m^T pbar + abar_m^T pdbar
-        colsum(s, N, st->s3, dups);
-        gemm(s, N, st->s5, V, nullptr, ah, nullptr, ah);                   // abar' = abar_h + u V
+        gemm(s, N, am, Um, nullptr, nullptr, nullptr, sc.s1);             // pdot
+        gemm(s, N, b.ff_a, T + H * H, nullptr, nullptr, nullptr, sc.s2);  // r = a' V^T
+        node::upd_bf_ew_kernel<<<blocks(NH, 256), 256, 0, s>>>(static_cast<int>(NH), sc.s2, sc.s1, b.p, sc.s3,
+                                                               sc.s4, sc.s5);
+        gemm(s, N, sc.s3, T, nullptr, nullptr, nullptr, b.inj);           // mbar^F = pbar U^T
+        wgrad(sc, s, N, sc.s5, b.ff_a, nullptr, nullptr, dV);             // dV2 = u^T a'
+        wgrad(sc, s, N, in_m(st, sl, u, N), sc.s3, am, sc.s4, dU, node::InId{},
+              Colsums{sc.s3, dups});                                        // dU2 = m^T pbar + abar_m^T pdbar
+        gemm(s, N, sc.s5, V, nullptr, ah, nullptr, ah);                   // abar' = abar_h + u V
         break;
       }
       case kReadout: {
         const float *O = P, *om = P + H * H + H;
         float *dO = G2, *dob = G2 + H * H, *dom = G2 + H * H + H;
-        gemm(s, N, ah, O, nullptr, nullptr, nullptr, st->s1);  // tdot
-        node::ro_bf_ew_kernel<kH><<<blocks(NH, 256), 256, 0, s>>>(static_cast<int>(NH), st->s1, b.p, om, st->s2,
-                                                                  st->s3, st->s4);
-        gemm(s, N, st->s2, T, nullptr, nullptr, nullptr, b.inj);  // hbar^F = tau O^T
-        colsum(s, N, st->s3, dom);
-        wgrad(s, N, ah, st->s4, in_h(st, sl, u, N), st->s2, dO);
-        colsum(s, N, st->s2, dob);
+        gemm(s, N, ah, O, nullptr, nullptr, nullptr, sc.s1);  // tdot
+        node::ro_bf_ew_kernel<kH><<<blocks(NH, 256), 256, 0, s>>>(static_cast<int>(NH), sc.s1, b.p, om, sc.s2,
+                                                                  sc.s3, sc.s4);
+        gemm(s, N, sc.s2, T, nullptr, nullptr, nullptr, b.inj);  // hbar^F = tau O^T
+        wgrad(sc, s, N, ah, sc.s4, in_h(st, sl, u, N), sc.s2, dO, node::InId{},
+              Colsums{sc.s3, dom, sc.s2, dob});
         break;
       }
     }
@@ -565,15 +587,16 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s) {
 }
 
 // ================================================================== BE
-void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only) {
+void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only, int lane) {
   check_mb_slot(st, mb, slot);
+  Scratch& sc = lane_of(st, lane);
   const DevGeo& g = st->geo[static_cast<size_t>(mb)];
   Slot& sl = st->slots[static_cast<size_t>(slot)];
   const int N = g.n_atoms, H = kH, R = kR, L = st->m.L;
   const size_t NH = static_cast<size_t>(N) * H;
   const EdgeGeom eg = edge_geom(g);
-  float* bh = st->wh;
-  float* bm = st->wm;
+  float* bh = sc.wh;
+  float* bm = sc.wm;
   JANUS_CUDA(cudaMemsetAsync(st->g1 + static_cast<size_t>(mb) * st->n_params, 0, sizeof(float) * st->n_params, s));
   if (inj_only) {
     // 1F1B-2nd force replica: propagate only the BF->BE injections (b_out = 0,
@@ -599,39 +622,38 @@ void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only) 
         const float* om = P + H * H + H;
         float *dO = G1, *dob = G1 + H * H, *dom = G1 + H * H + H, *dbias = G1 + H * H + 2 * H;
         node::ro_be_ew_kernel<kH><<<blocks(NH, 256), 256, 0, s>>>(static_cast<int>(NH), b.p, om, sl.eps, g.struct_id,
-                                                                  st->s1, st->s2);
-        gemm(s, N, st->s1, T, nullptr, b.inj, nullptr, bh);  // b_h = tbar O^T + hbar^F
-        wgrad(s, N, in_h(st, sl, u, N), st->s1, nullptr, nullptr, dO);
-        colsum(s, N, st->s1, dob);
-        colsum(s, N, st->s2, dom);
-        node::bias_grad_kernel<<<1, 256, 0, s>>>(N, st->m.n_species, g.species, g.struct_id, sl.eps, dbias);
+                                                                  sc.s1, sc.s2);
+        gemm(s, N, sc.s1, T, nullptr, b.inj, nullptr, bh);  // b_h = tbar O^T + hbar^F
+        wgrad(sc, s, N, in_h(st, sl, u, N), sc.s1, nullptr, nullptr, dO, node::InId{},
+              Colsums{sc.s1, dob, sc.s2, dom});
+        species_sum(st, sc, s, g, nullptr, sl.eps, dbias);
         break;
       }
       case kUpd: {
         float *dU = G1, *dups = G1 + H * H, *dV = G1 + H * H + H;
-        gemm(s, N, bh, T + H * H, nullptr, nullptr, nullptr, st->s1);  // r = b' V^T
-        node::upd_be_ew_kernel<<<blocks(NH, 256), 256, 0, s>>>(static_cast<int>(NH), st->s1, b.p, st->s2);
-        gemm(s, N, st->s2, T, nullptr, b.inj, nullptr, bm);             // b_m = pbar U^T + mbar^F
-        wgrad(s, N, b.p, bh, nullptr, nullptr, dV, node::InSilu{});      // dV1 = SiLU(p)^T b'
-        wgrad(s, N, in_m(st, sl, u, N), st->s2, nullptr, nullptr, dU);   // dU1 = m^T pbar
-        colsum(s, N, st->s2, dups);
+        gemm(s, N, bh, T + H * H, nullptr, nullptr, nullptr, sc.s1);  // r = b' V^T
+        node::upd_be_ew_kernel<<<blocks(NH, 256), 256, 0, s>>>(static_cast<int>(NH), sc.s1, b.p, sc.s2);
+        gemm(s, N, sc.s2, T, nullptr, b.inj, nullptr, bm);             // b_m = pbar U^T + mbar^F
+        wgrad(sc, s, N, b.p, bh, nullptr, nullptr, dV, node::InSilu{});  // dV1 = SiLU(p)^T b'
+        wgrad(sc, s, N, in_m(st, sl, u, N), sc.s2, nullptr, nullptr, dU, node::InId{},
+              Colsums{sc.s2, dups});                                     // dU1 = m^T pbar
         break;
       }
       case kMsg: {
         if (g.n_tiles > 0) {
           edge::msg_be_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::be_smem<kH, kR>(), s>>>(
-              eg, msg_params(st, u), st->m.r_c, b.v, bm, st->s1, st->partial);
+              eg, msg_params(st, u), st->m.r_c, b.v, bm, sc.s1, sc.partial);
           JANUS_LAUNCH_CHECK("msg_be");
-          edge::reduce_partials_kernel<<<blocks(EC::PE, 256), 256, 0, s>>>(st->partial, g.n_tiles, EC::PE, G1);
+          edge::reduce_partials_kernel<<<blocks(EC::PE, 256), 256, 0, s>>>(sc.partial, g.n_tiles, EC::PE, G1);
         } else {
-          JANUS_CUDA(cudaMemsetAsync(st->s1, 0, sizeof(float) * NH, s));
+          JANUS_CUDA(cudaMemsetAsync(sc.s1, 0, sizeof(float) * NH, s));
         }
-        wgrad(s, N, in_h(st, sl, u, N), st->s1, nullptr, nullptr, G1 + EC::PE);  // dW1 = h^T Yb
-        gemm(s, N, st->s1, T + H * H, nullptr, bh, b.inj, bh);                 // b_h += Yb W^T + hbar^F
+        wgrad(sc, s, N, in_h(st, sl, u, N), sc.s1, nullptr, nullptr, G1 + EC::PE);  // dW1 = h^T Yb
+        gemm(s, N, sc.s1, T + H * H, nullptr, bh, b.inj, bh);                 // b_h += Yb W^T + hbar^F
         break;
       }
       case kEmbed:
-        node::embed_be_kernel<kH><<<blocks(st->m.n_species * H, 256), 256, 0, s>>>(N, st->m.n_species, g.species, bh, G1);
+        species_sum(st, sc, s, g, bh, nullptr, G1);
         break;
     }
     JANUS_LAUNCH_CHECK("stage_be");
@@ -719,20 +741,21 @@ void stage_time_edge_kernel(janus_stage* st, int which, int mb, int slot, int it
   UnitBufs& b = sl.units[static_cast<size_t>(u - st->u0)];
   const EdgeGeom eg = edge_geom(g);
   const MsgParams mp = msg_params(st, u);
+  Scratch& sc = lane_of(st, 0);
   auto launch = [&] {
     switch (which) {
       case 0:
-        edge::msg_fe_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::fe_smem<kH, kR>(), s>>>(eg, mp, st->m.r_c, b.v, st->s3);
+        edge::msg_fe_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::fe_smem<kH, kR>(), s>>>(eg, mp, st->m.r_c, b.v, sc.s3);
         break;
       case 1:
-        edge::msg_ff_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::ff_smem<kH, kR>(), s>>>(eg, mp, st->m.r_c, b.v, b.ff_a, st->s3, st->q);
+        edge::msg_ff_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::ff_smem<kH, kR>(), s>>>(eg, mp, st->m.r_c, b.v, b.ff_a, sc.s3, sc.s5);
         break;
       case 2:
-        edge::msg_bf_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::bf_smem<kH, kR>(), s>>>(eg, mp, st->m.r_c, b.v, st->s1, b.ff_a,
-                                                                                       sl.Fbar, st->s3, st->s4, st->partial);
+        edge::msg_bf_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::bf_smem<kH, kR>(), s>>>(eg, mp, st->m.r_c, b.v, sc.s1, b.ff_a,
+                                                                                       sl.Fbar, sc.s3, sc.s4, sc.partial);
         break;
       default:
-        edge::msg_be_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::be_smem<kH, kR>(), s>>>(eg, mp, st->m.r_c, b.v, st->s2, st->s3, st->partial);
+        edge::msg_be_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::be_smem<kH, kR>(), s>>>(eg, mp, st->m.r_c, b.v, sc.s2, sc.s3, sc.partial);
         break;
     }
   };

@@ -50,6 +50,13 @@ struct Port {
   bool has_m = false, has_vec = false;
 };
 
+// Per-lane scratch: phases of different micro-batches may run concurrently on
+// different streams ("lanes") of one device; all transient buffers are per lane.
+struct Scratch {
+  float *wh = nullptr, *wm = nullptr, *s1 = nullptr, *s2 = nullptr, *s3 = nullptr, *s4 = nullptr, *s5 = nullptr;
+  float *partial = nullptr, *wpart = nullptr;
+};
+
 struct Slot {
   std::vector<UnitBufs> units;
   Port ports[8];
@@ -78,9 +85,7 @@ struct janus_stage {
   int* dstep = nullptr;  // device-side Adam step (graph-replayable bias correction)
   std::vector<janus::DevGeo> geo;
   std::vector<janus::Slot> slots;
-  // scratch
-  float *wh = nullptr, *wm = nullptr, *s1 = nullptr, *s2 = nullptr, *s3 = nullptr, *s4 = nullptr, *s5 = nullptr;
-  float *q = nullptr, *partial = nullptr, *zero = nullptr;
+  std::vector<janus::Scratch> lanes;
   std::vector<void*> allocs;
   int64_t static_bytes = 0, arena_bytes = 0;
 

@@ -10,10 +10,10 @@ namespace janus {
 janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params);
 void stage_destroy(janus_stage* st);
 void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_t s);
-void stage_fe(janus_stage* st, int mb, int slot, cudaStream_t s);
-void stage_ff(janus_stage* st, int mb, int slot, cudaStream_t s);
-void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s);
-void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only = false);
+void stage_fe(janus_stage* st, int mb, int slot, cudaStream_t s, int lane = 0);
+void stage_ff(janus_stage* st, int mb, int slot, cudaStream_t s, int lane = 0);
+void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane = 0);
+void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only = false, int lane = 0);
 void add_into(float* dst, const float* src, int64_t n, cudaStream_t s);
 void stage_reduce_grads(janus_stage* st, cudaStream_t s);
 void stage_optimizer(janus_stage* st, const janus_opt& o, cudaStream_t s);

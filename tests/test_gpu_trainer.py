@@ -112,3 +112,20 @@ def test_timeline_and_bubble(janus, data):
     assert 0.0 <= s.bubble_ratio < 1.0
     assert all(s.busy_ms[d] > 0 for d in range(P))
     t.close()
+
+
+@pytest.mark.parametrize("P,lanes", [(1, 4), (4, 3)])
+def test_lanes_bit_identical(janus, data, P, lanes):
+    """Overlapping independent micro-batches on several streams of a device
+    changes nothing: gradient ledgers are per micro-batch, reduced in order."""
+    m, params, batches, _, _ = data
+    t1, g1, p1, _ = run(janus, m, params, batches, P, janus.METHOD_SYMFOLD)
+    t = janus.Trainer(m, params, P, janus.METHOD_SYMFOLD, len(batches), max_atoms=64, max_edges=64 * 120,
+                      lanes=lanes, graphs=True)
+    for i, b in enumerate(batches):
+        t.load(i, b)
+    t.step(lr=1e-3)
+    g = np.concatenate([reduced_grad(janus, t.stage(b)) for b in range(P)])
+    assert np.array_equal(g, g1) and np.array_equal(t.params(), p1)
+    t.close()
+    t1.close()
