@@ -118,13 +118,24 @@ __global__ void __launch_bounds__(256) wgrad_partial_kernel(int rows, const floa
   for (int x = 0; x < 4; ++x)
 #pragma unroll
     for (int y = 0; y < 4; ++y) P[(kb + x) * H + hb + y] = acc[x][y];
-  if (threadIdx.x < 2 * H) {
-    const float* X = threadIdx.x < H ? x1 : x2;
-    const int c = threadIdx.x % H;
-    float s = 0.f;
-    if (X)
-      for (int r = 0; r < n; ++r) s += X[(size_t)(i0 + r) * H + c];
-    P[H * H + threadIdx.x] = s;
+  // column sums, staged through smem (coalesced loads, fixed row order)
+  for (int q = 0; q < 2; ++q) {
+    const float* X = q ? x2 : x1;
+    if (!X) {
+      if (threadIdx.x < H) P[H * H + q * H + threadIdx.x] = 0.f;
+      continue;
+    }
+    __syncthreads();
+    for (int x = threadIdx.x; x < kWChunk * H; x += 256) {
+      const int r = x / H, c = x % H;
+      sa[r][c] = r < n ? X[(size_t)(i0 + r) * H + c] : 0.f;
+    }
+    __syncthreads();
+    if (threadIdx.x < H) {
+      float s = 0.f;
+      for (int r = 0; r < n; ++r) s += sa[r][threadIdx.x];
+      P[H * H + q * H + threadIdx.x] = s;
+    }
   }
 }
 
