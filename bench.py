@@ -175,6 +175,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--method", default=None, choices=[None, "symfold", "wavek", "onef1b"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--precision", default="tf32", choices=["tf32", "fp32"],
+                    help="tf32: tcgen05 tensor-core edge kernels (tolerances in tests/test_gpu_tf32.py); "
+                         "fp32: SIMT parity path")
     args = ap.parse_args()
     rank, world, local_rank = dist_env()
     N = args.gpus
@@ -183,7 +186,8 @@ def main():
 
     import paper_2605_18404_b200 as J
 
-    model = J.Model(L=CONFIG["L"], H=CONFIG["H"], R=CONFIG["R"], r_c=CONFIG["r_c"])
+    model = J.Model(L=CONFIG["L"], H=CONFIG["H"], R=CONFIG["R"], r_c=CONFIG["r_c"],
+                    precision=J.PREC_TF32 if args.precision == "tf32" else J.PREC_FP32)
     params = model.synth_params(CONFIG["seed"])
     n_mb = CONFIG["n_mb"]
     batches = [J.synth_batch(model, [CONFIG["atoms"]], CONFIG["rho"], CONFIG["seed"] * 100 + m) for m in range(n_mb)]
@@ -291,7 +295,8 @@ def main():
         try:
             ms_bf, ne, fl = st.time_edge_kernel(2, 0, iters=50)
             achieved = fl / (ms_bf * 1e-3) / 1e12
-            roof = {"kernel": "msg_bf_kernel (SIMT fp32)", "bound": "tensor", "achieved": achieved,
+            roof = {"kernel": "msg_bf_tc (tcgen05 kind::tf32)" if args.precision == "tf32" else "msg_bf_kernel (SIMT fp32)",
+                    "bound": "tensor", "achieved": achieved,
                     "peak": peaks["bf16_tflops"], "unit": "TFLOP/s", "frac": achieved / peaks["bf16_tflops"],
                     "traffic": None, "peak_source": f"{peak_src} bf16 dense (MEASURED_PEAKS.json)",
                     "launch_ms": ms_bf, "edges_per_launch": ne, "flops_per_launch": fl,
@@ -310,8 +315,9 @@ def main():
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": "structures/s", "n_gpus": N, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
-               "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
-               "config": dict(cfg, parallelism=f"pp{P}" if P > 1 else "single-gpu", schedule=method_name,
+               "vs_baseline": None, "dtype": "fp32 (tf32 tensor-core contractions)" if args.precision == "tf32" else "fp32",
+               "data": "synthetic",
+               "config": dict(cfg, precision=args.precision, parallelism=f"pp{P}" if P > 1 else "single-gpu", schedule=method_name,
                               wavek_k=k if method == J.METHOD_WAVEK else None, cuda_graph=(N == 1),
                               lanes=(8 if N == 1 else 1)),
                "e2e": {"value": e2e_val, "unit": "structures/s", "h2d_bytes_per_step": h2d,

@@ -191,6 +191,13 @@ int janus_trainer_stage(janus_trainer* t, int block, int force_replica, janus_st
 int janus_trainer_schedule_text(janus_trainer* t, char* buf, int64_t cap, int64_t* len);
 int janus_trainer_plan(janus_trainer* t, int32_t* unit_ranges /* [P][2] */);
 
+/* ---- diagnostics ---- */
+/* tcgen05 layer self-test (tests/test_gpu_tc.py).  args = {M, N, K, a_mn, b_mn,
+ * a_rows, a_cols, b_rows, b_cols}; tiles are row-major fp32; K-major tiles are
+ * [M|N rows][K cols], MN-major tiles [K rows][M|N cols].  D = raw TMEM image,
+ * 128 lanes x N fp32 columns. */
+int janus_tc_probe(const int32_t* args, const float* A, const float* B, float* D);
+
 /* ---- schedule generation (host only) ---- */
 int janus_schedule_generate(int method, int P, int n_mb, int k, char* buf, int64_t cap, int64_t* len);
 int janus_schedule_validate(const char* text, int32_t* n_errors);

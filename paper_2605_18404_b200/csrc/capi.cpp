@@ -327,6 +327,17 @@ int janus_trainer_plan(janus_trainer* t, int32_t* unit_ranges) {
   });
 }
 
+// ------------------------------------------------------------ diagnostics
+int janus_tc_probe(const int32_t* args, const float* A, const float* B, float* D) {
+  return guard([&] {
+    need(args, "args");
+    need(A, "A");
+    need(B, "B");
+    need(D, "D");
+    janus::tc_probe(args, A, B, D);
+  });
+}
+
 // --------------------------------------------------------------- schedules
 int janus_schedule_generate(int method, int P, int n_mb, int k, char* buf, int64_t cap, int64_t* len) {
   return guard([&] {

@@ -1,0 +1,781 @@
+// edge_tc.cuh — the msg unit's four phases on 5th-gen tensor cores
+// (tcgen05.mma kind::tf32, accumulators in TMEM), the JANUS_PREC_TF32 path.
+// Same math as edge_kernels.cuh (SIMT fp32 parity path).
+//
+// Work decomposition (256 threads; thread t owns edge row e = t % 128 of the
+// tile = TMEM lane e, and feature half t / 128):
+//  * an edge tile = <= 8 CSR rows with <= 128 edges (a long row is chunked);
+//  * every per-edge contraction is an M=128 x N=64 x K=64 MMA from shared
+//    memory: A = the tile's edge-major operand, B = a weight tile;
+//  * the epilogue reads the 128x64 accumulator with tcgen05.ld (thread = edge)
+//    and applies SiLU', SiLU'', cutoff, ... in registers;
+//  * weight gradients sum_e X_e^T Y_e are M=64 x N=64 x K=128 MMAs over
+//    feature-major (transposed) tiles, accumulated in TMEM across all tiles of
+//    the CTA (BF/BE run persistent CTAs with a static tile assignment, so the
+//    per-CTA partials and their ordered reduction are deterministic);
+//  * all operand tiles use the SWIZZLE_128B K-major layout (tc::sw128_off): the
+//    edge-major float4 stores and the feature-major scalar stores are both
+//    bank-conflict-free; the tcgen05 MN-major (transpose) path was measured to
+//    return zeros for kind::tf32 (tests/test_gpu_tc.py) and is not used.
+#pragma once
+
+#include "common.cuh"
+#include "edge_kernels.cuh"
+#include "tc.cuh"
+
+namespace janus {
+namespace edge_tc {
+
+constexpr int TE = 128;
+constexpr int NT = 256;
+constexpr int H = 64, R = 64;
+constexpr int kRowsPerTile = 8;
+constexpr uint32_t kTile = 128 * 64 * 4;  // 32 KB operand tile
+constexpr uint32_t kWTile = 64 * 64 * 4;  // 16 KB weight tile
+constexpr int PE = R * H + H + H * H + H;
+// TMEM columns
+constexpr uint32_t TM_Z = 0, TM_ZP = 64, TM_G = 128, TM_GP = 192, TM_AG = 256, TM_BG = 320;
+
+__device__ __forceinline__ uint32_t off_em(int e, int f) { return tc::sw128_off(e, f, 128); }  // [128 edges][64 feat]
+__device__ __forceinline__ uint32_t off_fm(int f, int e) { return tc::sw128_off(f, e, 64); }   // [64 feat][128 edges]
+
+// D[tmem] (+)= A(rows a_rows, K) . B(rows b_rows, K)^T, K-major SWIZZLE_128B tiles.
+__device__ __forceinline__ void mma_tiles(uint32_t d, uint32_t a, int a_rows, uint32_t b, int b_rows, int K, int M,
+                                          bool accumulate) {
+  const uint32_t id = tc::idesc_tf32(M, 64, false, false);
+  const uint32_t as = static_cast<uint32_t>(a_rows) * 128u, bs = static_cast<uint32_t>(b_rows) * 128u;
+#pragma unroll 1
+  for (int s = 0; s < K / 8; ++s) {
+    const uint64_t da = tc::smem_desc(a + (s >> 2) * as + 32u * (s & 3), 16, 1024, 2);
+    const uint64_t db = tc::smem_desc(b + (s >> 2) * bs + 32u * (s & 3), 16, 1024, 2);
+    tc::mma_tf32(d, da, db, id, (s > 0 || accumulate) ? 1u : 0u);
+  }
+}
+
+struct Ctx {
+  uint8_t* sm;
+  uint64_t* mbar;
+  uint32_t tmem;
+  uint32_t phase;
+  int e, half, warp, lane;
+  __device__ uint32_t lane_base() const { return static_cast<uint32_t>((warp & 3) * 32) << 16; }
+  // all threads: make smem writes visible to the tensor core, order TMEM reads, barrier
+  __device__ void publish() {
+    tc::fence_async_smem();
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+  }
+  __device__ void wait_mma() {
+    tc::mbar_wait(mbar, phase);
+    phase ^= 1u;
+    tc::fence_after();
+  }
+  __device__ void ld(uint32_t col, float (&v)[32]) const { tc::ld32(tmem + lane_base() + col + 32u * half, v); }
+};
+
+// Weight tile for B operands: element (n, k) = src[k*64 + n] (transpose=true)
+// or src[n*64 + k].
+__device__ __forceinline__ void stage_weight(uint8_t* dst, const float* __restrict__ src, bool transpose) {
+  for (int x = threadIdx.x; x < 64 * 64; x += NT) {
+    const int a = x / 64, b = x % 64;
+    const int n = transpose ? b : a, k = transpose ? a : b;
+    *reinterpret_cast<float*>(dst + tc::sw128_off(n, k, 64)) = src[x];
+  }
+}
+
+__device__ __forceinline__ void st_em(uint8_t* t, int e, int f0, const float (&v)[32]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    *reinterpret_cast<float4*>(t + off_em(e, f0 + 4 * j)) = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+}
+__device__ __forceinline__ void st_fm(uint8_t* t, int e, int f0, const float (&v)[32]) {
+#pragma unroll
+  for (int j = 0; j < 32; ++j) *reinterpret_cast<float*>(t + off_fm(f0 + j, e)) = v[j];
+}
+__device__ __forceinline__ float ld_em(const uint8_t* t, int e, int f) {
+  return *reinterpret_cast<const float*>(t + off_em(e, f));
+}
+
+// radial basis (and derivative) of this thread's edge for its 32 features
+__device__ __forceinline__ void basis(float d, float rc, int f0, float (&p)[32], float (&dp)[32]) {
+  const float delta = rc / (R - 1);
+  const float gamma = 1.0f / (2.0f * delta * delta);
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const float x = d - (f0 + j) * delta;
+    p[j] = expf(-gamma * x * x);
+    dp[j] = -2.0f * gamma * x * p[j];
+  }
+}
+
+struct TileRange {
+  int r0, r1, e0, e1;
+};
+__device__ __forceinline__ TileRange tile_range(const EdgeGeom& g, const int* tile_row, int t) {
+  TileRange r;
+  r.r0 = tile_row[t];
+  r.r1 = tile_row[t + 1];
+  r.e0 = g.row_ptr[r.r0];
+  r.e1 = g.row_ptr[r.r1];
+  return r;
+}
+
+__device__ __forceinline__ void setup(Ctx& c, uint32_t* tmem_slot, uint32_t ncols) {
+  c.e = threadIdx.x & 127;
+  c.half = threadIdx.x >> 7;
+  c.warp = threadIdx.x >> 5;
+  c.lane = threadIdx.x & 31;
+  c.phase = 0;
+  if (threadIdx.x == 0) tc::mbar_init(c.mbar, 1);
+  if (c.warp == 0) tc::tmem_alloc(tmem_slot, ncols);
+  c.publish();
+  c.tmem = *tmem_slot;
+}
+
+__device__ __forceinline__ void teardown(Ctx& c, uint32_t ncols) {
+  tc::fence_before();
+  __syncthreads();
+  if (c.warp == 0) tc::tmem_free(c.tmem, ncols);
+}
+
+// per-chunk edge scalars into smem (threads 0..127)
+struct Scal {
+  float *d, *c, *dc, *qb;
+  int *src, *col;
+};
+__device__ __forceinline__ void load_scalars(const EdgeGeom& g, Scal& s, int c0, int ne, const float* Fbar) {
+  const int t = threadIdx.x;
+  if (t < TE) {
+    const bool ok = t < ne;
+    const int x = c0 + t;
+    s.d[t] = ok ? g.d[x] : 0.f;
+    s.c[t] = ok ? g.c[x] : 0.f;
+    if (s.dc) s.dc[t] = ok ? g.dc[x] : 0.f;
+    const int i = ok ? g.src[x] : 0, j = ok ? g.col[x] : 0;
+    s.src[t] = i;
+    s.col[t] = j;
+    if (s.qb) {
+      float q = 0.f;
+      if (ok)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) q = fmaf(Fbar[3 * i + k] - Fbar[3 * j + k], g.u[3 * x + k], q);
+      s.qb[t] = q;
+    }
+  }
+}
+
+// ----------------------------------------------------------------------- FE
+// m_i = sum_{e in row i} w_e * v[col e], w = c (SiLU(phi A + alpha) B + beta)
+__global__ void __launch_bounds__(NT) msg_fe_tc(EdgeGeom g, const int* __restrict__ tiles, int n_tiles, MsgParams p,
+                                               float rc, const float* __restrict__ v, float* __restrict__ m_out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  uint8_t* W0 = sm;               // A^T  (n = h, k = r)
+  uint8_t* W1 = W0 + kWTile;      // B^T  (n = out, k = in)
+  uint8_t* T0 = W1 + kWTile;      // phi -> s
+  uint8_t* T1 = T0 + kTile;       // w (edge-major)
+  float* fsm = reinterpret_cast<float*>(T1 + kTile);
+  float* al = fsm;
+  float* be = al + 64;
+  Scal sc{be + 64, be + 64 + TE, nullptr, nullptr, reinterpret_cast<int*>(be + 64 + 2 * TE), reinterpret_cast<int*>(be + 64 + 3 * TE)};
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tslot;
+  Ctx c;
+  c.sm = sm;
+  c.mbar = &mbar;
+  stage_weight(W0, p.A, true);
+  stage_weight(W1, p.B, true);
+  if (threadIdx.x < 64) {
+    al[threadIdx.x] = p.alpha[threadIdx.x];
+    be[threadIdx.x] = p.beta[threadIdx.x];
+  }
+  setup(c, &tslot, 128);
+  const uint32_t aW0 = tc::smem_u32(W0), aW1 = tc::smem_u32(W1), aT0 = tc::smem_u32(T0);
+  for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    const TileRange tr = tile_range(g, tiles, t);
+    const int row = tr.r0 + c.warp;
+    const bool has_row = row < tr.r1;
+    float acc0 = 0.f, acc1 = 0.f;
+    for (int c0 = tr.e0; c0 < tr.e1; c0 += TE) {
+      const int ne = min(TE, tr.e1 - c0);
+      load_scalars(g, sc, c0, ne, nullptr);
+      __syncthreads();
+      {
+        float ph[32], dph[32];
+        basis(sc.d[c.e], rc, 32 * c.half, ph, dph);
+        st_em(T0, c.e, 32 * c.half, ph);
+      }
+      c.publish();
+      if (threadIdx.x == 0) {
+        mma_tiles(c.tmem + TM_Z, aT0, 128, aW0, 64, 64, 128, false);
+        tc::commit(c.mbar);
+      }
+      c.wait_mma();
+      {
+        float z[32];
+        c.ld(TM_Z, z);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) z[j] = dev::silu(z[j] + al[32 * c.half + j]);
+        st_em(T0, c.e, 32 * c.half, z);
+      }
+      c.publish();
+      if (threadIdx.x == 0) {
+        mma_tiles(c.tmem + TM_G, aT0, 128, aW1, 64, 64, 128, false);
+        tc::commit(c.mbar);
+      }
+      c.wait_mma();
+      {
+        float gg[32];
+        c.ld(TM_G, gg);
+        const float ce = sc.c[c.e];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) gg[j] = ce * (gg[j] + be[32 * c.half + j]);
+        st_em(T1, c.e, 32 * c.half, gg);
+      }
+      tc::fence_before();
+      __syncthreads();
+      if (has_row) {
+        const int eb = max(g.row_ptr[row], c0), ee = min(g.row_ptr[row + 1], c0 + ne);
+        for (int x = eb; x < ee; ++x) {
+          const int j = g.col[x], le = x - c0;
+          acc0 = fmaf(ld_em(T1, le, c.lane), v[(size_t)j * H + c.lane], acc0);
+          acc1 = fmaf(ld_em(T1, le, c.lane + 32), v[(size_t)j * H + c.lane + 32], acc1);
+        }
+      }
+      __syncthreads();
+    }
+    if (has_row) {
+      m_out[(size_t)row * H + c.lane] = acc0;
+      m_out[(size_t)row * H + c.lane + 32] = acc1;
+    }
+  }
+  teardown(c, 128);
+}
+
+// ----------------------------------------------------------------------- FF
+// Y_i = sum w_e * am[col e];  F_i += sum_e (q_e + q_rev(e)) u_e with
+// q_e + q_rev(e) = < am_i v_j + am_j v_i , w'_e >  (w' symmetric in e <-> rev e)
+__global__ void __launch_bounds__(NT) msg_ff_tc(EdgeGeom g, const int* __restrict__ tiles, int n_tiles, MsgParams p,
+                                               float rc, const float* __restrict__ v, const float* __restrict__ am,
+                                               float* __restrict__ Y_out, float* __restrict__ F) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  uint8_t* W0 = sm;
+  uint8_t* W1 = W0 + kWTile;
+  uint8_t* T0 = W1 + kWTile;  // phi -> s -> w
+  uint8_t* T1 = T0 + kTile;   // phi' -> sdot -> w'
+  float* fsm = reinterpret_cast<float*>(T1 + kTile);
+  float* al = fsm;
+  float* be = al + 64;
+  Scal sc{be + 64, be + 64 + TE, be + 64 + 2 * TE, nullptr, reinterpret_cast<int*>(be + 64 + 3 * TE),
+          reinterpret_cast<int*>(be + 64 + 4 * TE)};
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tslot;
+  Ctx c;
+  c.sm = sm;
+  c.mbar = &mbar;
+  stage_weight(W0, p.A, true);
+  stage_weight(W1, p.B, true);
+  if (threadIdx.x < 64) {
+    al[threadIdx.x] = p.alpha[threadIdx.x];
+    be[threadIdx.x] = p.beta[threadIdx.x];
+  }
+  setup(c, &tslot, 256);
+  const uint32_t aW0 = tc::smem_u32(W0), aW1 = tc::smem_u32(W1), aT0 = tc::smem_u32(T0), aT1 = tc::smem_u32(T1);
+  for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    const TileRange tr = tile_range(g, tiles, t);
+    const int row = tr.r0 + c.warp;
+    const bool has_row = row < tr.r1;
+    float y0 = 0.f, y1 = 0.f, fx = 0.f, fy = 0.f, fz = 0.f, ami0 = 0.f, ami1 = 0.f, vi0 = 0.f, vi1 = 0.f;
+    if (has_row) {
+      ami0 = am[(size_t)row * H + c.lane];
+      ami1 = am[(size_t)row * H + c.lane + 32];
+      vi0 = v[(size_t)row * H + c.lane];
+      vi1 = v[(size_t)row * H + c.lane + 32];
+    }
+    for (int c0 = tr.e0; c0 < tr.e1; c0 += TE) {
+      const int ne = min(TE, tr.e1 - c0);
+      load_scalars(g, sc, c0, ne, nullptr);
+      __syncthreads();
+      {
+        float ph[32], dph[32];
+        basis(sc.d[c.e], rc, 32 * c.half, ph, dph);
+        st_em(T0, c.e, 32 * c.half, ph);
+        st_em(T1, c.e, 32 * c.half, dph);
+      }
+      c.publish();
+      if (threadIdx.x == 0) {
+        mma_tiles(c.tmem + TM_Z, aT0, 128, aW0, 64, 64, 128, false);
+        mma_tiles(c.tmem + TM_ZP, aT1, 128, aW0, 64, 64, 128, false);
+        tc::commit(c.mbar);
+      }
+      c.wait_mma();
+      {
+        float z[32], zp[32];
+        c.ld(TM_Z, z);
+        c.ld(TM_ZP, zp);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float zz = z[j] + al[32 * c.half + j];
+          z[j] = dev::silu(zz);
+          zp[j] = dev::dsilu(zz) * zp[j];
+        }
+        st_em(T0, c.e, 32 * c.half, z);
+        st_em(T1, c.e, 32 * c.half, zp);
+      }
+      c.publish();
+      if (threadIdx.x == 0) {
+        mma_tiles(c.tmem + TM_G, aT0, 128, aW1, 64, 64, 128, false);
+        mma_tiles(c.tmem + TM_GP, aT1, 128, aW1, 64, 64, 128, false);
+        tc::commit(c.mbar);
+      }
+      c.wait_mma();
+      {
+        float gg[32], gp[32];
+        c.ld(TM_G, gg);
+        c.ld(TM_GP, gp);
+        const float ce = sc.c[c.e], dce = sc.dc[c.e];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float gb = gg[j] + be[32 * c.half + j];
+          gg[j] = ce * gb;
+          gp[j] = dce * gb + ce * gp[j];
+        }
+        st_em(T0, c.e, 32 * c.half, gg);
+        st_em(T1, c.e, 32 * c.half, gp);
+      }
+      tc::fence_before();
+      __syncthreads();
+      if (has_row) {
+        const int eb = max(g.row_ptr[row], c0), ee = min(g.row_ptr[row + 1], c0 + ne);
+        for (int x = eb; x < ee; ++x) {
+          const int j = g.col[x], le = x - c0;
+          const float amj0 = am[(size_t)j * H + c.lane], amj1 = am[(size_t)j * H + c.lane + 32];
+          const float vj0 = v[(size_t)j * H + c.lane], vj1 = v[(size_t)j * H + c.lane + 32];
+          y0 = fmaf(ld_em(T0, le, c.lane), amj0, y0);
+          y1 = fmaf(ld_em(T0, le, c.lane + 32), amj1, y1);
+          float part = fmaf(fmaf(ami0, vj0, amj0 * vi0), ld_em(T1, le, c.lane),
+                            fmaf(ami1, vj1, amj1 * vi1) * ld_em(T1, le, c.lane + 32));
+          part = dev::warp_sum(part);
+          fx = fmaf(part, g.u[3 * x + 0], fx);
+          fy = fmaf(part, g.u[3 * x + 1], fy);
+          fz = fmaf(part, g.u[3 * x + 2], fz);
+        }
+      }
+      __syncthreads();
+    }
+    if (has_row) {
+      Y_out[(size_t)row * H + c.lane] = y0;
+      Y_out[(size_t)row * H + c.lane + 32] = y1;
+      if (c.lane == 0) {
+        F[3 * row + 0] += fx;
+        F[3 * row + 1] += fy;
+        F[3 * row + 2] += fz;
+      }
+    }
+  }
+  teardown(c, 256);
+}
+
+// Write the CTA's weight-gradient partial [dA | dalpha | dB | dbeta] from the
+// M=64 TMEM accumulators (row r at lane (r/16)*32 + r%16) and the per-thread
+// column sums (reduced over the 128 edge threads in order through smem).
+__device__ __forceinline__ void write_partial(Ctx& c, float* part, uint8_t* scratch, const float (&cs_a)[32],
+                                              const float (&cs_b)[32]) {
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  {
+    const int q = c.warp & 3;
+    float va[32], vb[32];
+    c.ld(TM_AG, va);
+    c.ld(TM_BG, vb);
+    if (c.lane < 16) {
+      const int r = 16 * q + c.lane;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        part[r * H + 32 * c.half + j] = va[j];                  // dA[r][h]
+        part[R * H + H + r * H + 32 * c.half + j] = vb[j];      // dB[k][h]
+      }
+    }
+  }
+  float* red = reinterpret_cast<float*>(scratch);  // [128][64] x 2
+  for (int pass = 0; pass < 2; ++pass) {
+    const float(&cs)[32] = pass ? cs_b : cs_a;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) red[c.e * 64 + 32 * c.half + j] = cs[j];
+    __syncthreads();
+    if (threadIdx.x < 64) {
+      float s = 0.f;
+      for (int e = 0; e < TE; ++e) s += red[e * 64 + threadIdx.x];
+      part[(pass ? R * H + H + H * H : R * H) + threadIdx.x] = s;
+    }
+    __syncthreads();
+  }
+}
+
+// ----------------------------------------------------------------------- BE
+// Yb_i = sum w_e * bm[col e]; gbar = c bm_i v_j; dB = s^T gbar; dbeta = sum gbar;
+// zbar = (gbar B^T) SiLU'(z); dA = phi^T zbar; dalpha = sum zbar.
+__global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int* __restrict__ tiles, int n_tiles, MsgParams p,
+                                                  float rc, const float* __restrict__ v, const float* __restrict__ bm,
+                                                  float* __restrict__ Yb_out, float* __restrict__ partial) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  uint8_t* W0 = sm;               // A^T
+  uint8_t* W1 = W0 + kWTile;      // B^T
+  uint8_t* W2 = W1 + kWTile;      // B
+  uint8_t* T0 = W2 + kWTile;
+  uint8_t* T1 = T0 + kTile;
+  uint8_t* T2 = T1 + kTile;
+  uint8_t* T3 = T2 + kTile;
+  float* fsm = reinterpret_cast<float*>(T3 + kTile);
+  float* al = fsm;
+  float* be = al + 64;
+  Scal sc{be + 64, be + 64 + TE, nullptr, nullptr, reinterpret_cast<int*>(be + 64 + 2 * TE),
+          reinterpret_cast<int*>(be + 64 + 3 * TE)};
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tslot;
+  Ctx c;
+  c.sm = sm;
+  c.mbar = &mbar;
+  stage_weight(W0, p.A, true);
+  stage_weight(W1, p.B, true);
+  stage_weight(W2, p.B, false);
+  if (threadIdx.x < 64) {
+    al[threadIdx.x] = p.alpha[threadIdx.x];
+    be[threadIdx.x] = p.beta[threadIdx.x];
+  }
+  setup(c, &tslot, 512);
+  const uint32_t aW0 = tc::smem_u32(W0), aW1 = tc::smem_u32(W1), aW2 = tc::smem_u32(W2);
+  const uint32_t aT0 = tc::smem_u32(T0), aT1 = tc::smem_u32(T1), aT2 = tc::smem_u32(T2), aT3 = tc::smem_u32(T3);
+  float cs_a[32], cs_b[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) cs_a[j] = cs_b[j] = 0.f;
+  bool first = true;
+  const int f0 = 32 * c.half;
+  for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    const TileRange tr = tile_range(g, tiles, t);
+    const int row = tr.r0 + c.warp;
+    const bool has_row = row < tr.r1;
+    float y0 = 0.f, y1 = 0.f;
+    for (int c0 = tr.e0; c0 < tr.e1; c0 += TE) {
+      const int ne = min(TE, tr.e1 - c0);
+      load_scalars(g, sc, c0, ne, nullptr);
+      __syncthreads();
+      {
+        float ph[32], dph[32];
+        basis(sc.d[c.e], rc, f0, ph, dph);
+        st_em(T0, c.e, f0, ph);
+      }
+      c.publish();
+      if (threadIdx.x == 0) {
+        mma_tiles(c.tmem + TM_Z, aT0, 128, aW0, 64, 64, 128, false);
+        tc::commit(c.mbar);
+      }
+      c.wait_mma();
+      {
+        float z[32];
+        c.ld(TM_Z, z);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) z[j] = dev::silu(z[j] + al[f0 + j]);
+        st_em(T0, c.e, f0, z);   // s, edge-major (A of g = s B)
+        st_fm(T1, c.e, f0, z);   // s^T (A of dB = s^T gbar)
+      }
+      c.publish();
+      if (threadIdx.x == 0) {
+        mma_tiles(c.tmem + TM_G, aT0, 128, aW1, 64, 64, 128, false);
+        tc::commit(c.mbar);
+      }
+      c.wait_mma();
+      {
+        float gg[32];
+        c.ld(TM_G, gg);
+        const float ce = sc.c[c.e];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) gg[j] = ce * (gg[j] + be[f0 + j]);
+        st_em(T0, c.e, f0, gg);  // w
+      }
+      tc::fence_before();
+      __syncthreads();
+      if (has_row) {
+        const int eb = max(g.row_ptr[row], c0), ee = min(g.row_ptr[row + 1], c0 + ne);
+        for (int x = eb; x < ee; ++x) {
+          const int j = g.col[x], le = x - c0;
+          y0 = fmaf(ld_em(T0, le, c.lane), bm[(size_t)j * H + c.lane], y0);
+          y1 = fmaf(ld_em(T0, le, c.lane + 32), bm[(size_t)j * H + c.lane + 32], y1);
+        }
+      }
+      {
+        // gbar = c bm_i v_j  (zero on padding edges: c = 0)
+        const int i = sc.src[c.e], j = sc.col[c.e];
+        const float ce = sc.c[c.e];
+        float gb[32];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float4 b4 = *reinterpret_cast<const float4*>(bm + (size_t)i * H + f0 + 4 * q);
+          const float4 v4 = *reinterpret_cast<const float4*>(v + (size_t)j * H + f0 + 4 * q);
+          gb[4 * q + 0] = ce * b4.x * v4.x;
+          gb[4 * q + 1] = ce * b4.y * v4.y;
+          gb[4 * q + 2] = ce * b4.z * v4.z;
+          gb[4 * q + 3] = ce * b4.w * v4.w;
+        }
+#pragma unroll
+        for (int q = 0; q < 32; ++q) cs_b[q] += gb[q];
+        __syncthreads();  // row sums done reading T0... (T2/T3 are free)
+        st_fm(T2, c.e, f0, gb);  // gbar^T (B of dB)
+        st_em(T3, c.e, f0, gb);  // gbar   (A of sbar = gbar B^T)
+      }
+      c.publish();
+      if (threadIdx.x == 0) {
+        mma_tiles(c.tmem + TM_BG, aT1, 64, aT2, 64, 128, 64, !first);
+        mma_tiles(c.tmem + TM_G, aT3, 128, aW2, 64, 64, 128, false);
+        tc::commit(c.mbar);
+      }
+      c.wait_mma();
+      {
+        float z[32], sb[32];
+        c.ld(TM_Z, z);
+        c.ld(TM_G, sb);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          z[j] = sb[j] * dev::dsilu(z[j] + al[f0 + j]);
+          cs_a[j] += z[j];
+        }
+        st_fm(T2, c.e, f0, z);  // zbar^T
+        float ph[32], dph[32];
+        basis(sc.d[c.e], rc, f0, ph, dph);
+        st_fm(T0, c.e, f0, ph);  // phi^T
+      }
+      c.publish();
+      if (threadIdx.x == 0) {
+        mma_tiles(c.tmem + TM_AG, aT0, 64, aT2, 64, 128, 64, !first);
+        tc::commit(c.mbar);
+      }
+      c.wait_mma();
+      first = false;
+      __syncthreads();
+    }
+    if (has_row) {
+      Yb_out[(size_t)row * H + c.lane] = y0;
+      Yb_out[(size_t)row * H + c.lane + 32] = y1;
+    }
+  }
+  float* part = partial + (size_t)blockIdx.x * PE;
+  if (first) {  // CTA without tiles: zero partial (TMEM accumulators never written)
+    for (int x = threadIdx.x; x < PE; x += NT) part[x] = 0.f;
+    teardown(c, 512);
+    return;
+  }
+  write_partial(c, part, T0, cs_a, cs_b);
+  teardown(c, 512);
+}
+
+// ----------------------------------------------------------------------- BF
+// Second-order term.  Outputs: mdot_i = sum_e qb w'_e v_j + w_e vdot_j,
+// X_i = sum_e qb w'_e am_j, and the partial [dA | dalpha | dB | dbeta].
+__global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __restrict__ tiles, int n_tiles, MsgParams p,
+                                                  float rc, const float* __restrict__ v, const float* __restrict__ vdot,
+                                                  const float* __restrict__ am, const float* __restrict__ Fbar,
+                                                  float* __restrict__ mdot_out, float* __restrict__ X_out,
+                                                  float* __restrict__ partial) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  uint8_t* W0 = sm;
+  uint8_t* W1 = W0 + kWTile;
+  uint8_t* W2 = W1 + kWTile;
+  uint8_t* T0 = W2 + kWTile;
+  uint8_t* T1 = T0 + kTile;
+  uint8_t* T2 = T1 + kTile;
+  uint8_t* T3 = T2 + kTile;
+  float* fsm = reinterpret_cast<float*>(T3 + kTile);
+  float* al = fsm;
+  float* be = al + 64;
+  Scal sc{be + 64, be + 64 + TE, be + 64 + 2 * TE, be + 64 + 3 * TE, reinterpret_cast<int*>(be + 64 + 4 * TE),
+          reinterpret_cast<int*>(be + 64 + 5 * TE)};
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tslot;
+  Ctx c;
+  c.sm = sm;
+  c.mbar = &mbar;
+  stage_weight(W0, p.A, true);
+  stage_weight(W1, p.B, true);
+  stage_weight(W2, p.B, false);
+  if (threadIdx.x < 64) {
+    al[threadIdx.x] = p.alpha[threadIdx.x];
+    be[threadIdx.x] = p.beta[threadIdx.x];
+  }
+  setup(c, &tslot, 512);
+  const uint32_t aW0 = tc::smem_u32(W0), aW1 = tc::smem_u32(W1), aW2 = tc::smem_u32(W2);
+  const uint32_t aT0 = tc::smem_u32(T0), aT1 = tc::smem_u32(T1), aT2 = tc::smem_u32(T2), aT3 = tc::smem_u32(T3);
+  float cs_a[32], cs_b[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) cs_a[j] = cs_b[j] = 0.f;
+  bool first = true;
+  const int f0 = 32 * c.half;
+  for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    const TileRange tr = tile_range(g, tiles, t);
+    const int row = tr.r0 + c.warp;
+    const bool has_row = row < tr.r1;
+    float md0 = 0.f, md1 = 0.f, x0 = 0.f, x1 = 0.f;
+    for (int c0 = tr.e0; c0 < tr.e1; c0 += TE) {
+      const int ne = min(TE, tr.e1 - c0);
+      load_scalars(g, sc, c0, ne, Fbar);
+      __syncthreads();
+      {
+        float ph[32], dph[32];
+        basis(sc.d[c.e], rc, f0, ph, dph);
+        st_em(T0, c.e, f0, ph);
+        st_em(T1, c.e, f0, dph);
+      }
+      c.publish();
+      if (threadIdx.x == 0) {
+        mma_tiles(c.tmem + TM_Z, aT0, 128, aW0, 64, 64, 128, false);
+        mma_tiles(c.tmem + TM_ZP, aT1, 128, aW0, 64, 64, 128, false);
+        tc::commit(c.mbar);
+      }
+      c.wait_mma();
+      {
+        float z[32], zp[32];
+        c.ld(TM_Z, z);
+        c.ld(TM_ZP, zp);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float zz = z[j] + al[f0 + j];
+          z[j] = dev::silu(zz);
+          zp[j] = dev::dsilu(zz) * zp[j];
+        }
+        st_em(T0, c.e, f0, z);   // s
+        st_em(T1, c.e, f0, zp);  // sdot
+        st_fm(T2, c.e, f0, z);   // s^T
+        st_fm(T3, c.e, f0, zp);  // sdot^T
+      }
+      c.publish();
+      if (threadIdx.x == 0) {
+        mma_tiles(c.tmem + TM_G, aT0, 128, aW1, 64, 64, 128, false);
+        mma_tiles(c.tmem + TM_GP, aT1, 128, aW1, 64, 64, 128, false);
+        tc::commit(c.mbar);
+      }
+      c.wait_mma();
+      {
+        float gg[32], gp[32];
+        c.ld(TM_G, gg);
+        c.ld(TM_GP, gp);
+        const float ce = sc.c[c.e], dce = sc.dc[c.e];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float gb = gg[j] + be[f0 + j];
+          gg[j] = ce * gb;
+          gp[j] = dce * gb + ce * gp[j];
+        }
+        st_em(T0, c.e, f0, gg);  // w
+        st_em(T1, c.e, f0, gp);  // w'
+      }
+      tc::fence_before();
+      __syncthreads();
+      if (has_row) {
+        const int eb = max(g.row_ptr[row], c0), ee = min(g.row_ptr[row + 1], c0 + ne);
+        for (int x = eb; x < ee; ++x) {
+          const int j = g.col[x], le = x - c0;
+          const float qb = sc.qb[le];
+          const float wp0 = qb * ld_em(T1, le, c.lane), wp1 = qb * ld_em(T1, le, c.lane + 32);
+          md0 = fmaf(wp0, v[(size_t)j * H + c.lane], fmaf(ld_em(T0, le, c.lane), vdot[(size_t)j * H + c.lane], md0));
+          md1 = fmaf(wp1, v[(size_t)j * H + c.lane + 32],
+                     fmaf(ld_em(T0, le, c.lane + 32), vdot[(size_t)j * H + c.lane + 32], md1));
+          x0 = fmaf(wp0, am[(size_t)j * H + c.lane], x0);
+          x1 = fmaf(wp1, am[(size_t)j * H + c.lane + 32], x1);
+        }
+      }
+      float mu[32], nu[32];
+      {
+        const int i = sc.src[c.e], j = sc.col[c.e];
+        const float qb = sc.qb[c.e], ce = sc.c[c.e], dce = sc.dc[c.e];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float4 a4 = *reinterpret_cast<const float4*>(am + (size_t)i * H + f0 + 4 * q);
+          const float4 v4 = *reinterpret_cast<const float4*>(v + (size_t)j * H + f0 + 4 * q);
+          const float4 d4 = *reinterpret_cast<const float4*>(vdot + (size_t)j * H + f0 + 4 * q);
+          const float av[4] = {a4.x, a4.y, a4.z, a4.w}, vv[4] = {v4.x, v4.y, v4.z, v4.w},
+                      dv[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const float rho = av[r] * vv[r], kap = av[r] * dv[r];
+            mu[4 * q + r] = qb * dce * rho + ce * kap;
+            nu[4 * q + r] = qb * ce * rho;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 32; ++q) cs_b[q] += mu[q];
+      }
+      __syncthreads();         // row sums are done with T0/T1
+      st_fm(T0, c.e, f0, mu);  // mu^T
+      st_fm(T1, c.e, f0, nu);  // nu^T
+      c.publish();
+      if (threadIdx.x == 0) {  // dB += s^T mu + sdot^T nu
+        mma_tiles(c.tmem + TM_BG, aT2, 64, aT0, 64, 128, 64, !first);
+        mma_tiles(c.tmem + TM_BG, aT3, 64, aT1, 64, 128, 64, true);
+        tc::commit(c.mbar);
+      }
+      c.wait_mma();
+      st_em(T2, c.e, f0, mu);  // mu (A of sbar = mu B^T)
+      st_em(T3, c.e, f0, nu);  // nu
+      c.publish();
+      if (threadIdx.x == 0) {
+        mma_tiles(c.tmem + TM_G, aT2, 128, aW2, 64, 64, 128, false);   // sbar
+        mma_tiles(c.tmem + TM_GP, aT3, 128, aW2, 64, 64, 128, false);  // sdotbar
+        tc::commit(c.mbar);
+      }
+      c.wait_mma();
+      {
+        float z[32], zp[32], sb[32], sdb[32];
+        c.ld(TM_Z, z);
+        c.ld(TM_ZP, zp);
+        c.ld(TM_G, sb);
+        c.ld(TM_GP, sdb);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float zz = z[j] + al[f0 + j];
+          const float ds = dev::dsilu(zz);
+          z[j] = sb[j] * ds + sdb[j] * dev::d2silu(zz) * zp[j];  // zbar
+          zp[j] = sdb[j] * ds;                                   // zbar'
+          cs_a[j] += z[j];
+        }
+        st_fm(T2, c.e, f0, z);
+        st_fm(T3, c.e, f0, zp);
+        float ph[32], dph[32];
+        basis(sc.d[c.e], rc, f0, ph, dph);
+        st_fm(T0, c.e, f0, ph);   // phi^T
+        st_fm(T1, c.e, f0, dph);  // phi'^T
+      }
+      c.publish();
+      if (threadIdx.x == 0) {  // dA += phi^T zbar + phi'^T zbar'
+        mma_tiles(c.tmem + TM_AG, aT0, 64, aT2, 64, 128, 64, !first);
+        mma_tiles(c.tmem + TM_AG, aT1, 64, aT3, 64, 128, 64, true);
+        tc::commit(c.mbar);
+      }
+      c.wait_mma();
+      first = false;
+      __syncthreads();
+    }
+    if (has_row) {
+      mdot_out[(size_t)row * H + c.lane] = md0;
+      mdot_out[(size_t)row * H + c.lane + 32] = md1;
+      X_out[(size_t)row * H + c.lane] = x0;
+      X_out[(size_t)row * H + c.lane + 32] = x1;
+    }
+  }
+  float* part = partial + (size_t)blockIdx.x * PE;
+  if (first) {
+    for (int x = threadIdx.x; x < PE; x += NT) part[x] = 0.f;
+    teardown(c, 512);
+    return;
+  }
+  write_partial(c, part, T0, cs_a, cs_b);
+  teardown(c, 512);
+}
+
+constexpr size_t kSmallBytes = sizeof(float) * (128 + 6 * TE);
+constexpr size_t fe_smem() { return 2 * kWTile + 2 * kTile + kSmallBytes; }
+constexpr size_t ff_smem() { return 2 * kWTile + 2 * kTile + kSmallBytes; }
+constexpr size_t be_smem() { return 3 * kWTile + 4 * kTile + kSmallBytes; }
+constexpr size_t bf_smem() { return 3 * kWTile + 4 * kTile + kSmallBytes; }
+
+}  // namespace edge_tc
+}  // namespace janus

@@ -17,6 +17,7 @@
 #include "../../include/janus/errors.hpp"
 
 #include "edge_kernels.cuh"
+#include "edge_tc.cuh"
 #include "node_kernels.cuh"
 #include "stage.cuh"
 #include "stage_api.hpp"
@@ -171,6 +172,9 @@ float* ledger(janus_stage* st, float* base, int mb, int u) {
   return base + static_cast<size_t>(mb) * st->n_params + st->uoff[static_cast<size_t>(u - st->u0)];
 }
 
+bool use_tc(const janus_stage* st) { return st->m.precision == JANUS_PREC_TF32; }
+int tc_grid(const DevGeo& g) { return std::max(1, std::min(g.n_tiles_tc, 148)); }
+
 Scratch& lane_of(janus_stage* st, int lane) {
   if (lane < 0 || lane >= static_cast<int>(st->lanes.size())) throw domain_error("lane index out of range");
   return st->lanes[static_cast<size_t>(lane)];
@@ -236,6 +240,7 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
       g.rev = dalloc<int>(st, NE, false);
       g.shift = dalloc<int>(st, 3 * NE, false);
       g.tile_row = dalloc<int>(st, NA + 1, false);
+      g.tile_row_tc = dalloc<int>(st, NA + 1, false);
       g.species = dalloc<int>(st, NA, false);
       g.struct_id = dalloc<int>(st, NA, false);
       g.struct_ptr = dalloc<int>(st, static_cast<size_t>(d.max_struct) + 1, false);
@@ -308,6 +313,10 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
     JANUS_CUDA(cudaFuncSetAttribute(edge::msg_ff_kernel<kH, kR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge::ff_smem<kH, kR>()));
     JANUS_CUDA(cudaFuncSetAttribute(edge::msg_bf_kernel<kH, kR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge::bf_smem<kH, kR>()));
     JANUS_CUDA(cudaFuncSetAttribute(edge::msg_be_kernel<kH, kR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge::be_smem<kH, kR>()));
+    JANUS_CUDA(cudaFuncSetAttribute(edge_tc::msg_fe_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge_tc::fe_smem()));
+    JANUS_CUDA(cudaFuncSetAttribute(edge_tc::msg_ff_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge_tc::ff_smem()));
+    JANUS_CUDA(cudaFuncSetAttribute(edge_tc::msg_bf_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge_tc::bf_smem()));
+    JANUS_CUDA(cudaFuncSetAttribute(edge_tc::msg_be_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge_tc::be_smem()));
     refresh_transposes(st, nullptr);
     JANUS_CUDA(cudaDeviceSynchronize());
   } catch (...) {
@@ -341,13 +350,13 @@ void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_
   JANUS_CUDA(cudaSetDevice(st->desc.device));
   DevGeo& g = st->geo[static_cast<size_t>(mb)];
   const int N = hb.n_atoms, E = hb.n_edges;
-  // host-side row tiles (<= 8 rows and <= TE edges, or one long row) and struct offsets
-  std::vector<int> tiles{0};
-  {
+  // host-side row tiles (<= 8 rows and <= te edges, or one long row) and struct offsets
+  auto build_tiles = [&](int te) {
+    std::vector<int> tiles{0};
     int rows = 0, edges = 0;
     for (int i = 0; i < N; ++i) {
       const int deg = hb.row_ptr[i + 1] - hb.row_ptr[i];
-      if (rows > 0 && (rows == edge::kRowsPerTile || edges + deg > edge::TE)) {
+      if (rows > 0 && (rows == edge::kRowsPerTile || edges + deg > te)) {
         tiles.push_back(i);
         rows = 0;
         edges = 0;
@@ -356,7 +365,10 @@ void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_
       edges += deg;
     }
     tiles.push_back(N);
-  }
+    return tiles;
+  };
+  const std::vector<int> tiles = build_tiles(edge::TE);
+  const std::vector<int> tiles_tc = build_tiles(edge_tc::TE);
   std::vector<int> sptr(static_cast<size_t>(hb.n_struct) + 1, 0);
   for (int i = 0; i < N; ++i) {
     const int sid = hb.struct_id[i];
@@ -369,6 +381,7 @@ void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_
   g.n_edges = E;
   g.n_struct = hb.n_struct;
   g.n_tiles = static_cast<int>(tiles.size()) - 1;
+  g.n_tiles_tc = static_cast<int>(tiles_tc.size()) - 1;
   auto h2d = [s](void* dst, const void* src, size_t bytes) {
     if (bytes) JANUS_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
   };
@@ -383,6 +396,7 @@ void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_
   h2d(g.E_target, hb.E_target, sizeof(float) * hb.n_struct);
   h2d(g.F_target, hb.F_target, sizeof(float) * 3 * N);
   h2d(g.tile_row, tiles.data(), sizeof(int) * tiles.size());
+  h2d(g.tile_row_tc, tiles_tc.data(), sizeof(int) * tiles_tc.size());
   h2d(g.struct_ptr, sptr.data(), sizeof(int) * sptr.size());
   node::geometry_kernel<<<blocks(N, 128), 128, 0, s>>>(N, g.row_ptr, g.col, g.shift, g.pos, g.struct_id, g.cell,
                                                        static_cast<double>(st->m.r_c), g.src, g.d, g.u, g.c, g.dc);
@@ -413,7 +427,10 @@ void stage_fe(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
       case kMsg: {
         const float* W = P + R * H + H + H * H + H;
         gemm(s, N, cur_h, W, nullptr, nullptr, nullptr, b.v);
-        if (g.n_tiles > 0)
+        if (g.n_tiles > 0 && use_tc(st))
+          edge_tc::msg_fe_tc<<<g.n_tiles_tc, edge_tc::NT, edge_tc::fe_smem(), s>>>(eg, g.tile_row_tc, g.n_tiles_tc, msg_params(st, u),
+                                                                                 st->m.r_c, b.v, b.out_m);
+        else if (g.n_tiles > 0)
           edge::msg_fe_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::fe_smem<kH, kR>(), s>>>(eg, msg_params(st, u), st->m.r_c, b.v, b.out_m);
         cur_m = b.out_m;
         break;
@@ -481,7 +498,10 @@ void stage_ff(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
       }
       case kMsg: {
         copy(s, b.ff_a, wm, NH);
-        if (g.n_tiles > 0)
+        if (g.n_tiles > 0 && use_tc(st))
+          edge_tc::msg_ff_tc<<<g.n_tiles_tc, edge_tc::NT, edge_tc::ff_smem(), s>>>(eg, g.tile_row_tc, g.n_tiles_tc, msg_params(st, u),
+                                                                                 st->m.r_c, b.v, b.ff_a, b.ff_Y, sl.F);
+        else if (g.n_tiles > 0)
           edge::msg_ff_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::ff_smem<kH, kR>(), s>>>(eg, msg_params(st, u), st->m.r_c, b.v, b.ff_a, b.ff_Y, sl.F);
         else
           JANUS_CUDA(cudaMemsetAsync(b.ff_Y, 0, sizeof(float) * NH, s));
@@ -537,7 +557,14 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
       case kMsg: {
         const float* W = P + R * H + H + H * H + H;
         gemm(s, N, ah, W, nullptr, nullptr, nullptr, sc.s1);  // vdot
-        if (g.n_tiles > 0) {
+        if (g.n_tiles > 0 && use_tc(st)) {
+          const int grid = tc_grid(g);
+          edge_tc::msg_bf_tc<<<grid, edge_tc::NT, edge_tc::bf_smem(), s>>>(eg, g.tile_row_tc, g.n_tiles_tc, msg_params(st, u),
+                                                                          st->m.r_c, b.v, sc.s1, b.ff_a, Fbar, am, sc.s2,
+                                                                          sc.partial);
+          JANUS_LAUNCH_CHECK("msg_bf_tc");
+          edge::reduce_partials_kernel<<<blocks(EC::PE, 256), 256, 0, s>>>(sc.partial, grid, EC::PE, G2);
+        } else if (g.n_tiles > 0) {
           edge::msg_bf_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::bf_smem<kH, kR>(), s>>>(
               eg, msg_params(st, u), st->m.r_c, b.v, sc.s1, b.ff_a, Fbar, am, sc.s2, sc.partial);
           JANUS_LAUNCH_CHECK("msg_bf");
@@ -640,7 +667,13 @@ void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only, 
         break;
       }
       case kMsg: {
-        if (g.n_tiles > 0) {
+        if (g.n_tiles > 0 && use_tc(st)) {
+          const int grid = tc_grid(g);
+          edge_tc::msg_be_tc<<<grid, edge_tc::NT, edge_tc::be_smem(), s>>>(eg, g.tile_row_tc, g.n_tiles_tc, msg_params(st, u),
+                                                                          st->m.r_c, b.v, bm, sc.s1, sc.partial);
+          JANUS_LAUNCH_CHECK("msg_be_tc");
+          edge::reduce_partials_kernel<<<blocks(EC::PE, 256), 256, 0, s>>>(sc.partial, grid, EC::PE, G1);
+        } else if (g.n_tiles > 0) {
           edge::msg_be_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::be_smem<kH, kR>(), s>>>(
               eg, msg_params(st, u), st->m.r_c, b.v, bm, sc.s1, sc.partial);
           JANUS_LAUNCH_CHECK("msg_be");
@@ -742,7 +775,27 @@ void stage_time_edge_kernel(janus_stage* st, int which, int mb, int slot, int it
   const EdgeGeom eg = edge_geom(g);
   const MsgParams mp = msg_params(st, u);
   Scratch& sc = lane_of(st, 0);
+  const bool tcm = use_tc(st);
   auto launch = [&] {
+    if (tcm) {
+      const int grid = tc_grid(g);
+      switch (which) {
+        case 0:
+          edge_tc::msg_fe_tc<<<g.n_tiles_tc, edge_tc::NT, edge_tc::fe_smem(), s>>>(eg, g.tile_row_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, sc.s3);
+          break;
+        case 1:
+          edge_tc::msg_ff_tc<<<g.n_tiles_tc, edge_tc::NT, edge_tc::ff_smem(), s>>>(eg, g.tile_row_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, b.ff_a, sc.s3, sc.s5);
+          break;
+        case 2:
+          edge_tc::msg_bf_tc<<<grid, edge_tc::NT, edge_tc::bf_smem(), s>>>(eg, g.tile_row_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, sc.s1, b.ff_a,
+                                                                          sl.Fbar, sc.s3, sc.s4, sc.partial);
+          break;
+        default:
+          edge_tc::msg_be_tc<<<grid, edge_tc::NT, edge_tc::be_smem(), s>>>(eg, g.tile_row_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, sc.s2, sc.s3, sc.partial);
+          break;
+      }
+      return;
+    }
     switch (which) {
       case 0:
         edge::msg_fe_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::fe_smem<kH, kR>(), s>>>(eg, mp, st->m.r_c, b.v, sc.s3);

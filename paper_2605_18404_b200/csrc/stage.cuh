@@ -27,7 +27,9 @@ int64_t unit_param_offset(const janus_model_desc& m, int u);
 
 struct DevGeo {
   int n_atoms = 0, n_edges = 0, n_struct = 0, n_tiles = 0;
+  int n_tiles_tc = 0;
   int *row_ptr = nullptr, *col = nullptr, *src = nullptr, *rev = nullptr, *tile_row = nullptr, *shift = nullptr;
+  int* tile_row_tc = nullptr;  // <= 8 rows, <= 128 edges (tensor-core tiles)
   int *species = nullptr, *struct_id = nullptr, *struct_ptr = nullptr;
   double *pos = nullptr, *cell = nullptr;
   float *d = nullptr, *u = nullptr, *c = nullptr, *dc = nullptr, *E_target = nullptr, *F_target = nullptr;

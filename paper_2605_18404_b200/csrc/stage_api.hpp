@@ -31,4 +31,7 @@ int stage_slot_of_mb(const janus_stage* st, int mb);
 void stage_time_edge_kernel(janus_stage* st, int which, int mb, int slot, int iters, cudaStream_t s, float* avg_ms,
                             int64_t* edges, double* flops);
 
+// tcgen05 layer self-test (tc_probe.cu)
+void tc_probe(const int* args, const float* A, const float* B, float* D);
+
 }  // namespace janus

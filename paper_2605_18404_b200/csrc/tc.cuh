@@ -1,0 +1,130 @@
+// tc.cuh — thin inline-PTX layer for 5th-gen tensor cores (tcgen05), TMEM and
+// mbarriers on sm_100a.  kind::tf32 MMAs with fp32 operands staged in shared
+// memory in the canonical no-swizzle "core matrix" layout:
+//
+//   a [rows][cols] fp32 tile is stored as 8-row x 4-col core matrices of
+//   128 contiguous bytes, core (rg, kc) at byte ((rg * (cols/4)) + kc) * 128,
+//   element (r, c) at core(r/8, c/4) + (r%8)*16 + (c%4)*4.
+//
+// The same physical tile is a valid operand two ways (descriptor strides per
+// the UMMA canonical layouts, CUTLASS mma_sm100_desc.hpp):
+//   * K-major, rows = M or N, cols = K:   LBO = 128 B, SBO = (cols/4)*128 B,
+//     K-step of 8 (tf32) advances the start address by 256 B;
+//   * MN-major, rows = K, cols = M or N:  SBO = 128 B, LBO = (cols/4)*128 B,
+//     K-step of 8 rows advances the start address by (cols/4)*128 B.
+// So an edge-major tile X[edge][feature] feeds both the per-edge GEMM
+// (M = edges, K = features) and the weight-gradient GEMM sum_e X_e^T Y_e
+// (M = features, K = edges) without any transpose.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace janus {
+namespace tc {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// byte offset of element (r, c) in a core-matrix tile with `cols` columns
+__device__ __forceinline__ uint32_t core_off(int r, int c, int cols) {
+  return static_cast<uint32_t>((((r >> 3) * (cols >> 2) + (c >> 2)) << 7) + ((r & 7) << 4) + ((c & 3) << 2));
+}
+
+// SWIZZLE_128B tile: 32-column (128 B) slabs; slab s holds rows [0, rows) at
+// 128 B per row in 8-row / 1024 B atoms; the 16 B chunk index is XORed with
+// the row index inside the atom (Swizzle<3,4,3>).  Needs 1024 B alignment.
+__device__ __forceinline__ uint32_t sw128_off(int r, int c, int rows) {
+  const int slab = c >> 5, cc = c & 31;
+  return static_cast<uint32_t>(slab * rows * 128 + (r >> 3) * 1024 + (r & 7) * 128 + ((((cc >> 2) ^ (r & 7))) << 4) +
+                               ((cc & 3) << 2));
+}
+
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t layout = 0) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((addr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+  d |= 1ull << 46;  // version = 1 (sm100), base offset 0, lbo mode 0
+  d |= static_cast<uint64_t>(layout & 7u) << 61;  // 0 none, 2 SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor, kind::tf32, fp32 accumulate (mma_sm100_desc.hpp InstrDescriptor).
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, bool a_mn_major, bool b_mn_major) {
+  return (1u << 4)                          // c_format = F32
+         | (2u << 7)                        // a_format = TF32
+         | (2u << 10)                       // b_format = TF32
+         | ((a_mn_major ? 1u : 0u) << 15)   // a_major
+         | ((b_mn_major ? 1u : 0u) << 16)   // b_major
+         | ((static_cast<uint32_t>(N) >> 3) << 17)
+         | ((static_cast<uint32_t>(M) >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void commit(uint64_t* mbar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(mbar))
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* mbar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mbar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(mbar)),
+      "r"(phase)
+      : "memory");
+}
+
+// generic-proxy smem writes -> visible to the tensor core (async proxy)
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// Allocation is warp-wide; the TMEM address lands in *dst (shared memory).
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst)), "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_free(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+
+// 32 lanes x 32 consecutive fp32 columns: thread (lane l of warp w) gets row
+// 32*(w%4)+l, columns [col, col+32).  The wait::ld is in the same asm block so
+// no register is observed before the asynchronous load has landed.
+__device__ __forceinline__ void ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+}  // namespace tc
+}  // namespace janus

@@ -1,0 +1,90 @@
+"""tcgen05 layer self-test on the B200: the descriptor encodings in
+csrc/tc.cuh (no-swizzle core-matrix tiles, K-major and MN-major views,
+kind::tf32) against numpy, and the TMEM row->lane map of M=64 accumulators."""
+import ctypes
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def probe(janus, M, N, K, a_mn, b_mn, A, B, swap=0, layout=0):
+    fn = janus.lib().janus_tc_probe
+    fn.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+    A = np.ascontiguousarray(A, np.float32)
+    B = np.ascontiguousarray(B, np.float32)
+    args = np.array([M, N, K, a_mn, b_mn, A.shape[0], A.shape[1], B.shape[0], B.shape[1], swap, layout], np.int32)
+    D = np.zeros((128, N), np.float32)
+    janus.check(fn(args.ctypes.data, A.ctypes.data, B.ctypes.data, D.ctypes.data))
+    return D
+
+
+def tf32(x):
+    b = np.ascontiguousarray(x, np.float32).view(np.uint32) & np.uint32(0xFFFFE000)
+    return b.view(np.float32).astype(np.float64)
+
+
+def lane_map(D, G):
+    lanes, errs = [], []
+    for r in range(G.shape[0]):
+        e = np.abs(D - G[r][None, :]).max(axis=1)
+        lanes.append(int(e.argmin()))
+        errs.append(float(e.min()))
+    return lanes, max(errs) / np.abs(G).max()
+
+
+CASES = {
+    # name: (M, N, K, a_mn, b_mn, A shape, B shape, reference(A, B) -> G[M][N])
+    "kmajor_m128": (128, 64, 64, 0, 0, (128, 64), (64, 64), lambda A, B: A @ B.T),
+    "kmajor_m64": (64, 64, 128, 0, 0, (64, 128), (64, 128), lambda A, B: A @ B.T),
+    "amn_m128": (128, 64, 64, 1, 0, (64, 128), (64, 64), lambda A, B: A.T @ B.T),
+    "bmn_m128": (128, 64, 64, 0, 1, (128, 64), (64, 64), lambda A, B: A @ B),
+    "mn_m64": (64, 64, 128, 1, 1, (128, 64), (128, 64), lambda A, B: A.T @ B),
+}
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_probe(janus, has_gpu, name):
+    if not has_gpu:
+        pytest.skip("no GPU")
+    M, N, K, amn, bmn, sa, sb, ref = CASES[name]
+    rng = np.random.default_rng(hash(name) % 1000)
+    A = rng.normal(size=sa).astype(np.float32)
+    B = rng.normal(size=sb).astype(np.float32)
+    D = probe(janus, M, N, K, amn, bmn, A, B)
+    G = ref(tf32(A), tf32(B))
+    lanes, err = lane_map(D, G)
+    print(f"{name}: rel err {err:.2e}; row->lane {lanes}")
+    assert err < 1e-3
+    if M == 128:
+        assert lanes == list(range(128))
+
+
+@pytest.mark.parametrize("name", ["amn_m128", "bmn_m128", "mn_m64"])
+def test_probe_mn_swapped(janus, has_gpu, name):
+    """Diagnostic: MN-major with LBO/SBO exchanged."""
+    if not has_gpu:
+        pytest.skip("no GPU")
+    M, N, K, amn, bmn, sa, sb, ref = CASES[name]
+    rng = np.random.default_rng(7)
+    A = rng.normal(size=sa).astype(np.float32)
+    B = rng.normal(size=sb).astype(np.float32)
+    D = probe(janus, M, N, K, amn, bmn, A, B, swap=1)
+    lanes, err = lane_map(D, ref(tf32(A), tf32(B)))
+    print(f"{name} swapped: rel err {err:.2e}; |D| max {np.abs(D).max():.3f}")
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_probe_sw128(janus, has_gpu, name):
+    """SWIZZLE_128B tiles: K-major and MN-major views of [row][col] slabs."""
+    if not has_gpu:
+        pytest.skip("no GPU")
+    M, N, K, amn, bmn, sa, sb, ref = CASES[name]
+    rng = np.random.default_rng(11)
+    A = rng.normal(size=sa).astype(np.float32)
+    B = rng.normal(size=sb).astype(np.float32)
+    D = probe(janus, M, N, K, amn, bmn, A, B, layout=2)
+    lanes, err = lane_map(D, ref(tf32(A), tf32(B)))
+    print(f"{name} sw128: rel err {err:.2e}; |D| max {np.abs(D).max():.3f}; lanes[:20] {lanes[:20]}")
+    assert err < 1e-3

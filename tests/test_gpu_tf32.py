@@ -1,0 +1,64 @@
+"""Tensor-core (tcgen05 kind::tf32) path of the msg edge kernels against the
+fp64 oracle.  tf32 keeps 10 mantissa bits, so the tolerances are widened and
+stated here (north star: "widened and documented where tf32/bf16 tensor-core
+paths are used"): E relative 2e-3, F 2e-2 and parameter gradients 2e-2 of the
+max magnitude.  The fp32 SIMT path (test_gpu_stage.py) keeps 1e-5 / 1e-4."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+TOL_E, TOL_F, TOL_G = 2e-3, 2e-2, 2e-2
+
+
+@pytest.fixture(scope="module")
+def case(janus, oracle, has_gpu):
+    if not has_gpu:
+        pytest.skip("no GPU")
+    m = janus.Model(L=2, H=64, R=64, precision=janus.PREC_TF32)
+    params = m.synth_params(11)
+    batches = [janus.synth_batch(m, [24, 30], 0.095, 3), janus.synth_batch(m, [200], 0.19, 4)]  # 2nd: ~100 nbrs, long rows
+    om = oracle.Model(L=m.L, H=m.H, R=m.R, n_species=m.n_species, r_c=m.r_c, w_E=m.w_E, w_F=m.w_F)
+    refs = []
+    for b in batches:
+        ob = oracle.Batch(b.pos, b.species, b.struct_id, b.cell, b.E_target.astype(float), b.F_target.astype(float))
+        refs.append(oracle.step(om, ob, oracle.build_nbrlist(om, ob), params.astype(np.float64)))
+    return m, params, batches, refs
+
+
+def rel(a, b):
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-30))
+
+
+@pytest.mark.parametrize("which", [0, 1])
+def test_tf32_step_matches_oracle(janus, case, which):
+    m, params, batches, refs = case
+    b, r = batches[which], refs[which]
+    st = janus.Stage(m, params, 0, m.n_units, max_atoms=256, max_edges=256 * 120, max_struct=4)
+    st.load(0, b)
+    for ph in ("fe", "ff", "bf", "be"):
+        getattr(st, ph)(0)
+    E, _ = st.energy(0, b.n_struct)
+    F, _ = st.forces(0, b.n_atoms)
+    g1, g2, g = st.grads(1, 0), st.grads(2, 0), st.grads(0, 0)
+    errs = dict(E=rel(E, r.E), F=rel(F, r.F), g1=rel(g1, r.grad1), g2=rel(g2, r.grad2), g=rel(g, r.grad))
+    per_unit = {}
+    for u in range(m.n_units):
+        o0, o1 = m.unit_offset(u), m.unit_offset(u + 1)
+        per_unit[u] = float(np.abs(g[o0:o1] - r.grad[o0:o1]).max() / np.abs(r.grad).max())
+    print(f"tf32 case {which}: {errs}; per-unit grad err {per_unit}")
+    st.close()
+    assert errs["E"] < TOL_E and errs["F"] < TOL_F
+    assert errs["g1"] < TOL_G and errs["g2"] < TOL_G and errs["g"] < TOL_G
+
+
+def test_tf32_edge_kernels_timed(janus, case):
+    m, params, batches, refs = case
+    b = janus.synth_batch(janus.Model(L=2), [256], 0.095, 9)
+    st = janus.Stage(m, params, 0, m.n_units, max_atoms=256, max_edges=256 * 120, max_struct=1)
+    st.load(0, b)
+    for ph in ("fe", "ff", "bf", "be"):
+        getattr(st, ph)(0)
+    for which, name in enumerate(("fe", "ff", "bf", "be")):
+        ms, ne, fl = st.time_edge_kernel(which, 0, iters=20)
+        print(f"tc {name}: {ms * 1e3:.1f} us, {fl / ms / 1e9:.2f} TFLOP/s")
+    st.close()
