@@ -97,6 +97,66 @@ __device__ __forceinline__ float ld_em(const uint8_t* t, int e, int f) {
   return *reinterpret_cast<const float*>(t + off_em(e, f));
 }
 
+// Plain [128 edges][64 features] fp32 tile for the segmented row sums: the
+// 16 B chunk index is XORed with (edge & 15) so both the per-edge float4
+// stores (32 consecutive edges, same feature chunk) and the per-row reads (32
+// consecutive features of one edge) are bank-conflict-free.
+__device__ __forceinline__ uint32_t off_pl(int e, int f) {
+  return static_cast<uint32_t>(e * 256 + ((((f >> 2) ^ (e & 15))) << 4) + ((f & 3) << 2));
+}
+__device__ __forceinline__ void st_pl(uint8_t* t, int e, int f0, const float (&v)[32]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    *reinterpret_cast<float4*>(t + off_pl(e, f0 + 4 * j)) = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+}
+
+// Deterministic segmented row sums of NA plain tiles over this chunk: thread t
+// owns (row, feature) pairs p = t and t + 256 (row = p / 64 within the tile,
+// feature = p % 64) and adds the row's chunk edges in CSR order.
+template <int NA>
+__device__ __forceinline__ void seg_rows(const EdgeGeom& g, int r0, int r1, int c0, int ne, const uint8_t* const (&tiles)[NA],
+                                         float (&acc)[NA][2]) {
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int pidx = threadIdx.x + 256 * k;
+    const int r = r0 + (pidx >> 6), f = pidx & 63;
+    if (r >= r1) continue;
+    const int eb = max(g.row_ptr[r], c0), ee = min(g.row_ptr[r + 1], c0 + ne);
+    for (int x = eb; x < ee; ++x) {
+      const uint32_t o = off_pl(x - c0, f);
+#pragma unroll
+      for (int a = 0; a < NA; ++a) acc[a][k] += *reinterpret_cast<const float*>(tiles[a] + o);
+    }
+  }
+}
+
+template <int NA>
+__device__ __forceinline__ void seg_write(int r0, int r1, float* const (&out)[NA], const float (&acc)[NA][2]) {
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int pidx = threadIdx.x + 256 * k;
+    const int r = r0 + (pidx >> 6), f = pidx & 63;
+    if (r >= r1) continue;
+#pragma unroll
+    for (int a = 0; a < NA; ++a) out[a][(size_t)r * H + f] = acc[a][k];
+  }
+}
+
+// 32 consecutive features of row `row` of an [N][64] array (8 float4 loads in flight)
+__device__ __forceinline__ void gather32(const float* __restrict__ x, int row, int f0, float (&v)[32]) {
+  const float4* p = reinterpret_cast<const float4*>(x + (size_t)row * H + f0);
+  float4 t[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) t[q] = __ldg(p + q);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    v[4 * q] = t[q].x;
+    v[4 * q + 1] = t[q].y;
+    v[4 * q + 2] = t[q].z;
+    v[4 * q + 3] = t[q].w;
+  }
+}
+
 // radial basis (and derivative) of this thread's edge for its 32 features
 __device__ __forceinline__ void basis(float d, float rc, int f0, float (&p)[32], float (&dp)[32]) {
   const float delta = rc / (R - 1);
@@ -193,9 +253,7 @@ __global__ void __launch_bounds__(NT) msg_fe_tc(EdgeGeom g, const int* __restric
   const uint32_t aW0 = tc::smem_u32(W0), aW1 = tc::smem_u32(W1), aT0 = tc::smem_u32(T0);
   for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
     const TileRange tr = tile_range(g, tiles, t);
-    const int row = tr.r0 + c.warp;
-    const bool has_row = row < tr.r1;
-    float acc0 = 0.f, acc1 = 0.f;
+    float acc[1][2] = {{0.f, 0.f}};
     for (int c0 = tr.e0; c0 < tr.e1; c0 += TE) {
       const int ne = min(TE, tr.e1 - c0);
       load_scalars(g, sc, c0, ne, nullptr);
@@ -225,29 +283,24 @@ __global__ void __launch_bounds__(NT) msg_fe_tc(EdgeGeom g, const int* __restric
       }
       c.wait_mma();
       {
-        float gg[32];
+        float gg[32], vj[32];
+        gather32(v, sc.col[c.e], 32 * c.half, vj);
         c.ld(TM_G, gg);
         const float ce = sc.c[c.e];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) gg[j] = ce * (gg[j] + be[32 * c.half + j]);
-        st_em(T1, c.e, 32 * c.half, gg);
+        for (int j = 0; j < 32; ++j) gg[j] = ce * (gg[j] + be[32 * c.half + j]) * vj[j];  // w_e * v_j
+        st_pl(T1, c.e, 32 * c.half, gg);
       }
       tc::fence_before();
       __syncthreads();
-      if (has_row) {
-        const int eb = max(g.row_ptr[row], c0), ee = min(g.row_ptr[row + 1], c0 + ne);
-        for (int x = eb; x < ee; ++x) {
-          const int j = g.col[x], le = x - c0;
-          acc0 = fmaf(ld_em(T1, le, c.lane), v[(size_t)j * H + c.lane], acc0);
-          acc1 = fmaf(ld_em(T1, le, c.lane + 32), v[(size_t)j * H + c.lane + 32], acc1);
-        }
+      {
+        const uint8_t* const tl[1] = {T1};
+        seg_rows<1>(g, tr.r0, tr.r1, c0, ne, tl, acc);
       }
       __syncthreads();
     }
-    if (has_row) {
-      m_out[(size_t)row * H + c.lane] = acc0;
-      m_out[(size_t)row * H + c.lane + 32] = acc1;
-    }
+    float* const outs[1] = {m_out};
+    seg_write<1>(tr.r0, tr.r1, outs, acc);
   }
   teardown(c, 128);
 }
@@ -261,13 +314,14 @@ __global__ void __launch_bounds__(NT) msg_ff_tc(EdgeGeom g, const int* __restric
   extern __shared__ __align__(1024) uint8_t sm[];
   uint8_t* W0 = sm;
   uint8_t* W1 = W0 + kWTile;
-  uint8_t* T0 = W1 + kWTile;  // phi -> s -> w
-  uint8_t* T1 = T0 + kTile;   // phi' -> sdot -> w'
+  uint8_t* T0 = W1 + kWTile;  // phi -> s -> (plain) w * am_j
+  uint8_t* T1 = T0 + kTile;   // phi' -> sdot
   float* fsm = reinterpret_cast<float*>(T1 + kTile);
   float* al = fsm;
   float* be = al + 64;
   Scal sc{be + 64, be + 64 + TE, be + 64 + 2 * TE, nullptr, reinterpret_cast<int*>(be + 64 + 3 * TE),
           reinterpret_cast<int*>(be + 64 + 4 * TE)};
+  float* sq = be + 64 + 5 * TE;  // [2][TE] per-half force scalars
   __shared__ __align__(8) uint64_t mbar;
   __shared__ uint32_t tslot;
   Ctx c;
@@ -281,26 +335,20 @@ __global__ void __launch_bounds__(NT) msg_ff_tc(EdgeGeom g, const int* __restric
   }
   setup(c, &tslot, 256);
   const uint32_t aW0 = tc::smem_u32(W0), aW1 = tc::smem_u32(W1), aT0 = tc::smem_u32(T0), aT1 = tc::smem_u32(T1);
+  const int f0 = 32 * c.half;
   for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
     const TileRange tr = tile_range(g, tiles, t);
-    const int row = tr.r0 + c.warp;
-    const bool has_row = row < tr.r1;
-    float y0 = 0.f, y1 = 0.f, fx = 0.f, fy = 0.f, fz = 0.f, ami0 = 0.f, ami1 = 0.f, vi0 = 0.f, vi1 = 0.f;
-    if (has_row) {
-      ami0 = am[(size_t)row * H + c.lane];
-      ami1 = am[(size_t)row * H + c.lane + 32];
-      vi0 = v[(size_t)row * H + c.lane];
-      vi1 = v[(size_t)row * H + c.lane + 32];
-    }
+    float acc[1][2] = {{0.f, 0.f}};
+    float fsum = 0.f;  // threads < 24: (row t/3, component t%3)
     for (int c0 = tr.e0; c0 < tr.e1; c0 += TE) {
       const int ne = min(TE, tr.e1 - c0);
       load_scalars(g, sc, c0, ne, nullptr);
       __syncthreads();
       {
         float ph[32], dph[32];
-        basis(sc.d[c.e], rc, 32 * c.half, ph, dph);
-        st_em(T0, c.e, 32 * c.half, ph);
-        st_em(T1, c.e, 32 * c.half, dph);
+        basis(sc.d[c.e], rc, f0, ph, dph);
+        st_em(T0, c.e, f0, ph);
+        st_em(T1, c.e, f0, dph);
       }
       c.publish();
       if (threadIdx.x == 0) {
@@ -315,12 +363,12 @@ __global__ void __launch_bounds__(NT) msg_ff_tc(EdgeGeom g, const int* __restric
         c.ld(TM_ZP, zp);
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-          const float zz = z[j] + al[32 * c.half + j];
+          const float zz = z[j] + al[f0 + j];
           z[j] = dev::silu(zz);
           zp[j] = dev::dsilu(zz) * zp[j];
         }
-        st_em(T0, c.e, 32 * c.half, z);
-        st_em(T1, c.e, 32 * c.half, zp);
+        st_em(T0, c.e, f0, z);
+        st_em(T1, c.e, f0, zp);
       }
       c.publish();
       if (threadIdx.x == 0) {
@@ -330,47 +378,50 @@ __global__ void __launch_bounds__(NT) msg_ff_tc(EdgeGeom g, const int* __restric
       }
       c.wait_mma();
       {
+        const int i = sc.src[c.e], j = sc.col[c.e];
+        const float ce = sc.c[c.e], dce = sc.dc[c.e];
         float gg[32], gp[32];
         c.ld(TM_G, gg);
         c.ld(TM_GP, gp);
-        const float ce = sc.c[c.e], dce = sc.dc[c.e];
+        float pq = 0.f;
+        float amj[32];
+        gather32(am, j, f0, amj);
+        {
+          float vj[32], ami[32], vi[32];
+          gather32(v, j, f0, vj);
+          gather32(am, i, f0, ami);
+          gather32(v, i, f0, vi);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float gb = gg[j] + be[32 * c.half + j];
-          gg[j] = ce * gb;
-          gp[j] = dce * gb + ce * gp[j];
+          for (int q = 0; q < 32; ++q) {
+            const float gb = gg[q] + be[f0 + q];
+            const float wp = dce * gb + ce * gp[q];
+            pq = fmaf(fmaf(ami[q], vj[q], amj[q] * vi[q]), wp, pq);
+            gg[q] = ce * gb * amj[q];  // w_e * am_j
+          }
         }
-        st_em(T0, c.e, 32 * c.half, gg);
-        st_em(T1, c.e, 32 * c.half, gp);
+        st_pl(T0, c.e, f0, gg);
+        sq[c.half * TE + c.e] = pq;
       }
       tc::fence_before();
       __syncthreads();
-      if (has_row) {
-        const int eb = max(g.row_ptr[row], c0), ee = min(g.row_ptr[row + 1], c0 + ne);
-        for (int x = eb; x < ee; ++x) {
-          const int j = g.col[x], le = x - c0;
-          const float amj0 = am[(size_t)j * H + c.lane], amj1 = am[(size_t)j * H + c.lane + 32];
-          const float vj0 = v[(size_t)j * H + c.lane], vj1 = v[(size_t)j * H + c.lane + 32];
-          y0 = fmaf(ld_em(T0, le, c.lane), amj0, y0);
-          y1 = fmaf(ld_em(T0, le, c.lane + 32), amj1, y1);
-          float part = fmaf(fmaf(ami0, vj0, amj0 * vi0), ld_em(T1, le, c.lane),
-                            fmaf(ami1, vj1, amj1 * vi1) * ld_em(T1, le, c.lane + 32));
-          part = dev::warp_sum(part);
-          fx = fmaf(part, g.u[3 * x + 0], fx);
-          fy = fmaf(part, g.u[3 * x + 1], fy);
-          fz = fmaf(part, g.u[3 * x + 2], fz);
+      {
+        const uint8_t* const tl[1] = {T0};
+        seg_rows<1>(g, tr.r0, tr.r1, c0, ne, tl, acc);
+        if (threadIdx.x < 3 * kRowsPerTile) {
+          const int r = tr.r0 + threadIdx.x / 3, comp = threadIdx.x % 3;
+          if (r < tr.r1) {
+            const int eb = max(g.row_ptr[r], c0), ee = min(g.row_ptr[r + 1], c0 + ne);
+            for (int x = eb; x < ee; ++x) fsum = fmaf(sq[x - c0] + sq[TE + x - c0], g.u[3 * x + comp], fsum);
+          }
         }
       }
       __syncthreads();
     }
-    if (has_row) {
-      Y_out[(size_t)row * H + c.lane] = y0;
-      Y_out[(size_t)row * H + c.lane + 32] = y1;
-      if (c.lane == 0) {
-        F[3 * row + 0] += fx;
-        F[3 * row + 1] += fy;
-        F[3 * row + 2] += fz;
-      }
+    float* const outs[1] = {Y_out};
+    seg_write<1>(tr.r0, tr.r1, outs, acc);
+    if (threadIdx.x < 3 * kRowsPerTile) {
+      const int r = tr.r0 + threadIdx.x / 3;
+      if (r < tr.r1) F[3 * r + threadIdx.x % 3] += fsum;
     }
   }
   teardown(c, 256);
@@ -393,12 +444,12 @@ __device__ __forceinline__ void write_partial(Ctx& c, float* part, uint8_t* scra
       const int r = 16 * q + c.lane;
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
-        part[r * H + 32 * c.half + j] = va[j];                  // dA[r][h]
-        part[R * H + H + r * H + 32 * c.half + j] = vb[j];      // dB[k][h]
+        part[r * H + 32 * c.half + j] = va[j];              // dA[r][h]
+        part[R * H + H + r * H + 32 * c.half + j] = vb[j];  // dB[k][h]
       }
     }
   }
-  float* red = reinterpret_cast<float*>(scratch);  // [128][64] x 2
+  float* red = reinterpret_cast<float*>(scratch);  // [128][64]
   for (int pass = 0; pass < 2; ++pass) {
     const float(&cs)[32] = pass ? cs_b : cs_a;
 #pragma unroll
@@ -420,9 +471,9 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int* __rest
                                                   float rc, const float* __restrict__ v, const float* __restrict__ bm,
                                                   float* __restrict__ Yb_out, float* __restrict__ partial) {
   extern __shared__ __align__(1024) uint8_t sm[];
-  uint8_t* W0 = sm;               // A^T
-  uint8_t* W1 = W0 + kWTile;      // B^T
-  uint8_t* W2 = W1 + kWTile;      // B
+  uint8_t* W0 = sm;           // A^T
+  uint8_t* W1 = W0 + kWTile;  // B^T
+  uint8_t* W2 = W1 + kWTile;  // B
   uint8_t* T0 = W2 + kWTile;
   uint8_t* T1 = T0 + kTile;
   uint8_t* T2 = T1 + kTile;
@@ -454,9 +505,7 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int* __rest
   const int f0 = 32 * c.half;
   for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
     const TileRange tr = tile_range(g, tiles, t);
-    const int row = tr.r0 + c.warp;
-    const bool has_row = row < tr.r1;
-    float y0 = 0.f, y1 = 0.f;
+    float acc[1][2] = {{0.f, 0.f}};
     for (int c0 = tr.e0; c0 < tr.e1; c0 += TE) {
       const int ne = min(TE, tr.e1 - c0);
       load_scalars(g, sc, c0, ne, nullptr);
@@ -477,8 +526,8 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int* __rest
         c.ld(TM_Z, z);
 #pragma unroll
         for (int j = 0; j < 32; ++j) z[j] = dev::silu(z[j] + al[f0 + j]);
-        st_em(T0, c.e, f0, z);   // s, edge-major (A of g = s B)
-        st_fm(T1, c.e, f0, z);   // s^T (A of dB = s^T gbar)
+        st_em(T0, c.e, f0, z);  // s, edge-major (A of g = s B)
+        st_fm(T1, c.e, f0, z);  // s^T (A of dB = s^T gbar)
       }
       c.publish();
       if (threadIdx.x == 0) {
@@ -486,51 +535,39 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int* __rest
         tc::commit(c.mbar);
       }
       c.wait_mma();
+      float gb[32];
       {
-        float gg[32];
-        c.ld(TM_G, gg);
-        const float ce = sc.c[c.e];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) gg[j] = ce * (gg[j] + be[f0 + j]);
-        st_em(T0, c.e, f0, gg);  // w
-      }
-      tc::fence_before();
-      __syncthreads();
-      if (has_row) {
-        const int eb = max(g.row_ptr[row], c0), ee = min(g.row_ptr[row + 1], c0 + ne);
-        for (int x = eb; x < ee; ++x) {
-          const int j = g.col[x], le = x - c0;
-          y0 = fmaf(ld_em(T0, le, c.lane), bm[(size_t)j * H + c.lane], y0);
-          y1 = fmaf(ld_em(T0, le, c.lane + 32), bm[(size_t)j * H + c.lane + 32], y1);
-        }
-      }
-      {
-        // gbar = c bm_i v_j  (zero on padding edges: c = 0)
         const int i = sc.src[c.e], j = sc.col[c.e];
         const float ce = sc.c[c.e];
-        float gb[32];
+        float gg[32], bj[32];
+        c.ld(TM_G, gg);
+        gather32(bm, j, f0, bj);
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const float4 b4 = *reinterpret_cast<const float4*>(bm + (size_t)i * H + f0 + 4 * q);
-          const float4 v4 = *reinterpret_cast<const float4*>(v + (size_t)j * H + f0 + 4 * q);
-          gb[4 * q + 0] = ce * b4.x * v4.x;
-          gb[4 * q + 1] = ce * b4.y * v4.y;
-          gb[4 * q + 2] = ce * b4.z * v4.z;
-          gb[4 * q + 3] = ce * b4.w * v4.w;
+        for (int q = 0; q < 32; ++q) gg[q] = ce * (gg[q] + be[f0 + q]) * bj[q];  // w_e * bm_j
+        st_pl(T0, c.e, f0, gg);
+        float bi[32], vj[32];
+        gather32(bm, i, f0, bi);
+        gather32(v, j, f0, vj);
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          gb[q] = ce * bi[q] * vj[q];  // gbar (zero on padding edges: c = 0)
+          cs_b[q] += gb[q];
         }
-#pragma unroll
-        for (int q = 0; q < 32; ++q) cs_b[q] += gb[q];
-        __syncthreads();  // row sums done reading T0... (T2/T3 are free)
-        st_fm(T2, c.e, f0, gb);  // gbar^T (B of dB)
-        st_em(T3, c.e, f0, gb);  // gbar   (A of sbar = gbar B^T)
       }
+      st_fm(T2, c.e, f0, gb);  // gbar^T (B of dB)
+      st_em(T3, c.e, f0, gb);  // gbar   (A of sbar = gbar B^T)
       c.publish();
       if (threadIdx.x == 0) {
         mma_tiles(c.tmem + TM_BG, aT1, 64, aT2, 64, 128, 64, !first);
         mma_tiles(c.tmem + TM_G, aT3, 128, aW2, 64, 64, 128, false);
         tc::commit(c.mbar);
       }
+      {  // row sums overlap the MMAs (they read T1..T3, this reads T0)
+        const uint8_t* const tl[1] = {T0};
+        seg_rows<1>(g, tr.r0, tr.r1, c0, ne, tl, acc);
+      }
       c.wait_mma();
+      __syncthreads();  // T0 reads done before it is rewritten
       {
         float z[32], sb[32];
         c.ld(TM_Z, z);
@@ -554,10 +591,8 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int* __rest
       first = false;
       __syncthreads();
     }
-    if (has_row) {
-      Yb_out[(size_t)row * H + c.lane] = y0;
-      Yb_out[(size_t)row * H + c.lane + 32] = y1;
-    }
+    float* const outs[1] = {Yb_out};
+    seg_write<1>(tr.r0, tr.r1, outs, acc);
   }
   float* part = partial + (size_t)blockIdx.x * PE;
   if (first) {  // CTA without tiles: zero partial (TMEM accumulators never written)
@@ -612,9 +647,7 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
   const int f0 = 32 * c.half;
   for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
     const TileRange tr = tile_range(g, tiles, t);
-    const int row = tr.r0 + c.warp;
-    const bool has_row = row < tr.r1;
-    float md0 = 0.f, md1 = 0.f, x0 = 0.f, x1 = 0.f;
+    float acc[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
     for (int c0 = tr.e0; c0 < tr.e1; c0 += TE) {
       const int ne = min(TE, tr.e1 - c0);
       load_scalars(g, sc, c0, ne, Fbar);
@@ -654,57 +687,46 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
         tc::commit(c.mbar);
       }
       c.wait_mma();
-      {
-        float gg[32], gp[32];
-        c.ld(TM_G, gg);
-        c.ld(TM_GP, gp);
-        const float ce = sc.c[c.e], dce = sc.dc[c.e];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float gb = gg[j] + be[f0 + j];
-          gg[j] = ce * gb;
-          gp[j] = dce * gb + ce * gp[j];
-        }
-        st_em(T0, c.e, f0, gg);  // w
-        st_em(T1, c.e, f0, gp);  // w'
-      }
-      tc::fence_before();
-      __syncthreads();
-      if (has_row) {
-        const int eb = max(g.row_ptr[row], c0), ee = min(g.row_ptr[row + 1], c0 + ne);
-        for (int x = eb; x < ee; ++x) {
-          const int j = g.col[x], le = x - c0;
-          const float qb = sc.qb[le];
-          const float wp0 = qb * ld_em(T1, le, c.lane), wp1 = qb * ld_em(T1, le, c.lane + 32);
-          md0 = fmaf(wp0, v[(size_t)j * H + c.lane], fmaf(ld_em(T0, le, c.lane), vdot[(size_t)j * H + c.lane], md0));
-          md1 = fmaf(wp1, v[(size_t)j * H + c.lane + 32],
-                     fmaf(ld_em(T0, le, c.lane + 32), vdot[(size_t)j * H + c.lane + 32], md1));
-          x0 = fmaf(wp0, am[(size_t)j * H + c.lane], x0);
-          x1 = fmaf(wp1, am[(size_t)j * H + c.lane + 32], x1);
-        }
-      }
       float mu[32], nu[32];
       {
         const int i = sc.src[c.e], j = sc.col[c.e];
         const float qb = sc.qb[c.e], ce = sc.c[c.e], dce = sc.dc[c.e];
+        float gg[32], gp[32];
+        c.ld(TM_G, gg);
+        c.ld(TM_GP, gp);
+        float pm[32], px[32];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          const float4 a4 = *reinterpret_cast<const float4*>(am + (size_t)i * H + f0 + 4 * q);
-          const float4 v4 = *reinterpret_cast<const float4*>(v + (size_t)j * H + f0 + 4 * q);
-          const float4 d4 = *reinterpret_cast<const float4*>(vdot + (size_t)j * H + f0 + 4 * q);
-          const float av[4] = {a4.x, a4.y, a4.z, a4.w}, vv[4] = {v4.x, v4.y, v4.z, v4.w},
-                      dv[4] = {d4.x, d4.y, d4.z, d4.w};
+          const float4 a4 = __ldg(reinterpret_cast<const float4*>(am + (size_t)i * H + f0) + q);
+          const float4 aj4 = __ldg(reinterpret_cast<const float4*>(am + (size_t)j * H + f0) + q);
+          const float4 v4 = __ldg(reinterpret_cast<const float4*>(v + (size_t)j * H + f0) + q);
+          const float4 d4 = __ldg(reinterpret_cast<const float4*>(vdot + (size_t)j * H + f0) + q);
+          const float ai[4] = {a4.x, a4.y, a4.z, a4.w}, aj[4] = {aj4.x, aj4.y, aj4.z, aj4.w};
+          const float vv[4] = {v4.x, v4.y, v4.z, v4.w}, dv[4] = {d4.x, d4.y, d4.z, d4.w};
 #pragma unroll
           for (int r = 0; r < 4; ++r) {
-            const float rho = av[r] * vv[r], kap = av[r] * dv[r];
-            mu[4 * q + r] = qb * dce * rho + ce * kap;
-            nu[4 * q + r] = qb * ce * rho;
+            const int k = 4 * q + r;
+            const float gb = gg[k] + be[f0 + k];
+            const float w = ce * gb, wp = qb * (dce * gb + ce * gp[k]);
+            pm[k] = fmaf(wp, vv[r], w * dv[r]);  // qb w' v_j + w vdot_j
+            px[k] = wp * aj[r];                  // qb w' am_j
+            const float rho = ai[r] * vv[r], kap = ai[r] * dv[r];
+            mu[k] = qb * dce * rho + ce * kap;
+            nu[k] = qb * ce * rho;
           }
         }
+        st_pl(T0, c.e, f0, pm);
+        st_pl(T1, c.e, f0, px);
 #pragma unroll
         for (int q = 0; q < 32; ++q) cs_b[q] += mu[q];
       }
-      __syncthreads();         // row sums are done with T0/T1
+      tc::fence_before();
+      __syncthreads();
+      {
+        const uint8_t* const tl[2] = {T0, T1};
+        seg_rows<2>(g, tr.r0, tr.r1, c0, ne, tl, acc);
+      }
+      __syncthreads();         // row sums done with T0/T1
       st_fm(T0, c.e, f0, mu);  // mu^T
       st_fm(T1, c.e, f0, nu);  // nu^T
       c.publish();
@@ -754,12 +776,8 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
       first = false;
       __syncthreads();
     }
-    if (has_row) {
-      mdot_out[(size_t)row * H + c.lane] = md0;
-      mdot_out[(size_t)row * H + c.lane + 32] = md1;
-      X_out[(size_t)row * H + c.lane] = x0;
-      X_out[(size_t)row * H + c.lane + 32] = x1;
-    }
+    float* const outs[2] = {mdot_out, X_out};
+    seg_write<2>(tr.r0, tr.r1, outs, acc);
   }
   float* part = partial + (size_t)blockIdx.x * PE;
   if (first) {
@@ -771,7 +789,7 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
   teardown(c, 512);
 }
 
-constexpr size_t kSmallBytes = sizeof(float) * (128 + 6 * TE);
+constexpr size_t kSmallBytes = sizeof(float) * (128 + 8 * TE);
 constexpr size_t fe_smem() { return 2 * kWTile + 2 * kTile + kSmallBytes; }
 constexpr size_t ff_smem() { return 2 * kWTile + 2 * kTile + kSmallBytes; }
 constexpr size_t be_smem() { return 3 * kWTile + 4 * kTile + kSmallBytes; }

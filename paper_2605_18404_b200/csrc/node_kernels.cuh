@@ -95,11 +95,23 @@ __global__ void __launch_bounds__(256) wgrad_partial_kernel(int rows, const floa
     const float* A = pass ? a2 : a;
     const float* B = pass ? b2 : b;
     __syncthreads();
-    for (int x = threadIdx.x; x < kWChunk * H; x += 256) {
-      const int r = x / H, c = x % H;
-      const bool ok = r < n;
-      sa[r][c] = ok ? (pass ? A[(size_t)(i0 + r) * H + c] : op(i0 + r, c, A[(size_t)(i0 + r) * H + c])) : 0.f;
-      sb[r][c] = ok ? B[(size_t)(i0 + r) * H + c] : 0.f;
+    {
+      // all 2 x 16 loads of this thread in flight before any use (ILP), then the stores
+      constexpr int PER = kWChunk * H / 256;
+      float va[PER], vb[PER];
+#pragma unroll
+      for (int q = 0; q < PER; ++q) {
+        const int x = threadIdx.x + 256 * q, r = x / H, c = x % H;
+        const bool ok = r < n;
+        va[q] = ok ? __ldg(A + (size_t)(i0 + r) * H + c) : 0.f;
+        vb[q] = ok ? __ldg(B + (size_t)(i0 + r) * H + c) : 0.f;
+      }
+#pragma unroll
+      for (int q = 0; q < PER; ++q) {
+        const int x = threadIdx.x + 256 * q, r = x / H, c = x % H;
+        sa[r][c] = (pass || r >= n) ? va[q] : op(i0 + r, c, va[q]);
+        sb[r][c] = vb[q];
+      }
     }
     __syncthreads();
 #pragma unroll 4
