@@ -175,6 +175,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--method", default=None, choices=[None, "symfold", "wavek", "onef1b"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--lanes", type=int, default=8, help="concurrent micro-batch streams at N=1")
     ap.add_argument("--precision", default="tf32", choices=["tf32", "fp32"],
                     help="tf32: tcgen05 tensor-core edge kernels (tolerances in tests/test_gpu_tf32.py); "
                          "fp32: SIMT parity path")
@@ -237,7 +238,7 @@ def main():
     max_edges = max(b.n_edges for b in batches) + 64
     tr = J.Trainer(model, params, P, method, n_mb, k=k, max_atoms=CONFIG["atoms"], max_edges=max_edges,
                    max_struct=1, local=(N == 1), graphs=(N == 1), comm=comm, rank=rank, device=local_rank,
-                   lanes=(8 if N == 1 else 1))
+                   lanes=(args.lanes if N == 1 else 1))
     for m, b in enumerate(batches):
         tr.load(m, b)
     for _ in range(args.warmup):
@@ -319,7 +320,7 @@ def main():
                "data": "synthetic",
                "config": dict(cfg, precision=args.precision, parallelism=f"pp{P}" if P > 1 else "single-gpu", schedule=method_name,
                               wavek_k=k if method == J.METHOD_WAVEK else None, cuda_graph=(N == 1),
-                              lanes=(8 if N == 1 else 1)),
+                              lanes=(args.lanes if N == 1 else 1)),
                "e2e": {"value": e2e_val, "unit": "structures/s", "h2d_bytes_per_step": h2d,
                        "d2h_bytes_per_step": 8 * n_mb},
                "gpu_launches": int(launches), "gpu_launches_per_step": int(stats.kernel_launches),

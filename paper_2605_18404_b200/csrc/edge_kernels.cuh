@@ -44,6 +44,7 @@ struct MsgParams {
   const float* B;      // [H][H]
   const float* beta;   // [H]
   const float* Bt;     // [H][H] transposed copy of B
+  const float* pack;   // tensor-core image: [A^T | B^T | B] SW128 tiles, alpha, beta (edge_tc.cuh)
 };
 
 namespace edge {

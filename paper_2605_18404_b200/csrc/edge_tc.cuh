@@ -84,6 +84,45 @@ __device__ __forceinline__ void stage_weight(uint8_t* dst, const float* __restri
   }
 }
 
+// Packed weight image in global memory = the exact smem image of
+// [W0 = A^T | W1 = B^T | W2 = B | alpha | beta]; rebuilt after every
+// optimizer step (stage.cu refresh_transposes) and pulled by each CTA with one
+// TMA bulk copy.
+constexpr uint32_t kPackBytes = 3 * kWTile + 2 * 64 * 4;
+
+__global__ void pack_msg_weights(const float* __restrict__ A, const float* __restrict__ alpha, const float* __restrict__ B,
+                                 const float* __restrict__ beta, float* __restrict__ pack) {
+  uint8_t* dst = reinterpret_cast<uint8_t*>(pack);
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x < 64 * 64) {
+    const int a = x / 64, b = x % 64;  // src[a*64 + b]
+    *reinterpret_cast<float*>(dst + tc::sw128_off(b, a, 64)) = A[x];               // A^T: (n=h=b, k=r=a)
+    *reinterpret_cast<float*>(dst + kWTile + tc::sw128_off(b, a, 64)) = B[x];      // B^T: (n=out=b, k=in=a)
+    *reinterpret_cast<float*>(dst + 2 * kWTile + tc::sw128_off(a, b, 64)) = B[x];  // B:   (n=a, k=b)
+  }
+  if (x < 64) {
+    pack[3 * kWTile / 4 + x] = alpha[x];
+    pack[3 * kWTile / 4 + 64 + x] = beta[x];
+  }
+}
+
+// All threads: bulk-load `ntiles` weight tiles (+ alpha, beta) into sm[0..).
+// Returns after the copy landed (mbarrier transaction count).
+__device__ __forceinline__ void load_weights(uint8_t* sm, const float* pack, int ntiles, float* al, float* be,
+                                             uint64_t* wbar) {
+  if (threadIdx.x == 0) {
+    tc::mbar_init(wbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const uint32_t wbytes = static_cast<uint32_t>(ntiles) * kWTile;
+    tc::mbar_expect_tx(wbar, wbytes + 512);
+    tc::bulk_g2s(sm, pack, wbytes, wbar);
+    tc::bulk_g2s(al, reinterpret_cast<const uint8_t*>(pack) + 3 * kWTile, 256, wbar);
+    tc::bulk_g2s(be, reinterpret_cast<const uint8_t*>(pack) + 3 * kWTile + 256, 256, wbar);
+  }
+  __syncthreads();
+  tc::mbar_wait(wbar, 0);
+}
+
 __device__ __forceinline__ void st_em(uint8_t* t, int e, int f0, const float (&v)[32]) {
 #pragma unroll
   for (int j = 0; j < 8; ++j)
@@ -243,12 +282,8 @@ __global__ void __launch_bounds__(NT) msg_fe_tc(EdgeGeom g, const int* __restric
   Ctx c;
   c.sm = sm;
   c.mbar = &mbar;
-  stage_weight(W0, p.A, true);
-  stage_weight(W1, p.B, true);
-  if (threadIdx.x < 64) {
-    al[threadIdx.x] = p.alpha[threadIdx.x];
-    be[threadIdx.x] = p.beta[threadIdx.x];
-  }
+  __shared__ __align__(8) uint64_t wbar;
+  load_weights(sm, p.pack, 2, al, be, &wbar);
   setup(c, &tslot, 128);
   const uint32_t aW0 = tc::smem_u32(W0), aW1 = tc::smem_u32(W1), aT0 = tc::smem_u32(T0);
   for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
@@ -327,12 +362,8 @@ __global__ void __launch_bounds__(NT) msg_ff_tc(EdgeGeom g, const int* __restric
   Ctx c;
   c.sm = sm;
   c.mbar = &mbar;
-  stage_weight(W0, p.A, true);
-  stage_weight(W1, p.B, true);
-  if (threadIdx.x < 64) {
-    al[threadIdx.x] = p.alpha[threadIdx.x];
-    be[threadIdx.x] = p.beta[threadIdx.x];
-  }
+  __shared__ __align__(8) uint64_t wbar;
+  load_weights(sm, p.pack, 2, al, be, &wbar);
   setup(c, &tslot, 256);
   const uint32_t aW0 = tc::smem_u32(W0), aW1 = tc::smem_u32(W1), aT0 = tc::smem_u32(T0), aT1 = tc::smem_u32(T1);
   const int f0 = 32 * c.half;
@@ -488,13 +519,8 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int* __rest
   Ctx c;
   c.sm = sm;
   c.mbar = &mbar;
-  stage_weight(W0, p.A, true);
-  stage_weight(W1, p.B, true);
-  stage_weight(W2, p.B, false);
-  if (threadIdx.x < 64) {
-    al[threadIdx.x] = p.alpha[threadIdx.x];
-    be[threadIdx.x] = p.beta[threadIdx.x];
-  }
+  __shared__ __align__(8) uint64_t wbar;
+  load_weights(sm, p.pack, 3, al, be, &wbar);
   setup(c, &tslot, 512);
   const uint32_t aW0 = tc::smem_u32(W0), aW1 = tc::smem_u32(W1), aW2 = tc::smem_u32(W2);
   const uint32_t aT0 = tc::smem_u32(T0), aT1 = tc::smem_u32(T1), aT2 = tc::smem_u32(T2), aT3 = tc::smem_u32(T3);
@@ -630,13 +656,8 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
   Ctx c;
   c.sm = sm;
   c.mbar = &mbar;
-  stage_weight(W0, p.A, true);
-  stage_weight(W1, p.B, true);
-  stage_weight(W2, p.B, false);
-  if (threadIdx.x < 64) {
-    al[threadIdx.x] = p.alpha[threadIdx.x];
-    be[threadIdx.x] = p.beta[threadIdx.x];
-  }
+  __shared__ __align__(8) uint64_t wbar;
+  load_weights(sm, p.pack, 3, al, be, &wbar);
   setup(c, &tslot, 512);
   const uint32_t aW0 = tc::smem_u32(W0), aW1 = tc::smem_u32(W1), aW2 = tc::smem_u32(W2);
   const uint32_t aT0 = tc::smem_u32(T0), aT1 = tc::smem_u32(T1), aT2 = tc::smem_u32(T2), aT3 = tc::smem_u32(T3);

@@ -382,3 +382,310 @@ __global__ void geometry_kernel(int n_atoms, const int* __restrict__ row_ptr, co
 
 }  // namespace node
 }  // namespace janus
+
+namespace janus {
+namespace node {
+
+// ===================================================================== fused
+// Row-local programs for the upd unit (p = mU + ups, y = SiLU(p) V): one CTA =
+// 16 atoms x 64 features, thread (row t/16, 4 columns); row vectors staged in
+// smem, weights read through L1.  Each replaces 3-5 separate launches.
+constexpr int kRB = 16;
+
+__device__ __forceinline__ void rowmm(const float (*X)[68], const float* Ms, int r, int c0, float (&o)[4]) {
+  o[0] = o[1] = o[2] = o[3] = 0.f;
+#pragma unroll 16
+  for (int k = 0; k < 64; ++k) {
+    const float a = X[r][k];
+    const float4 m = *reinterpret_cast<const float4*>(Ms + k * 64 + c0);
+    o[0] = fmaf(a, m.x, o[0]);
+    o[1] = fmaf(a, m.y, o[1]);
+    o[2] = fmaf(a, m.z, o[2]);
+    o[3] = fmaf(a, m.w, o[3]);
+  }
+}
+// Stage up to 4 [64][64] weight matrices into smem with every load in flight
+// at once (16 float4 per thread per matrix), then one barrier.
+__device__ __forceinline__ void stage_mats(float* dst, const float* const* src, int n) {
+  for (int m = 0; m < n; ++m) {
+    const float4* s4 = reinterpret_cast<const float4*>(src[m]);
+    float4* d4 = reinterpret_cast<float4*>(dst + m * 4096);
+    float4 t[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) t[q] = __ldg(s4 + threadIdx.x + 256 * q);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) d4[threadIdx.x + 256 * q] = t[q];
+  }
+}
+constexpr size_t upd_smem(int nmats) { return sizeof(float) * 4096 * nmats; }
+
+__device__ __forceinline__ void row_load(float (*X)[68], const float* __restrict__ src, int i0, int rows) {
+  for (int x = threadIdx.x; x < kRB * 16; x += 256) {
+    const int r = x / 16, q = x % 16;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (i0 + r < rows) v = __ldg(reinterpret_cast<const float4*>(src + (size_t)(i0 + r) * 64) + q);
+    *reinterpret_cast<float4*>(&X[r][4 * q]) = v;
+  }
+}
+__device__ __forceinline__ void row_store(float* dst, int i, int c0, const float (&v)[4]) {
+  *reinterpret_cast<float4*>(dst + (size_t)i * 64 + c0) = make_float4(v[0], v[1], v[2], v[3]);
+}
+__device__ __forceinline__ float4 row_get(const float* src, int i, int c0) {
+  return __ldg(reinterpret_cast<const float4*>(src + (size_t)i * 64 + c0));
+}
+
+// FE: p = m U + ups ; h_out = h + SiLU(p) V
+__global__ void __launch_bounds__(256) upd_fe_fused(int rows, const float* __restrict__ m, const float* __restrict__ h,
+                                                    const float* __restrict__ U, const float* __restrict__ ups,
+                                                    const float* __restrict__ V, float* __restrict__ p_out,
+                                                    float* __restrict__ h_out) {
+  __shared__ __align__(16) float X[kRB][68];
+  extern __shared__ __align__(16) float Ws[];
+  const int i0 = blockIdx.x * kRB, r = threadIdx.x / 16, c0 = (threadIdx.x % 16) * 4, i = i0 + r;
+  {
+    const float* mats[2] = {U, V};
+    stage_mats(Ws, mats, 2);
+  }
+  row_load(X, m, i0, rows);
+  __syncthreads();
+  float o[4];
+  rowmm(X, Ws, r, c0, o);
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    o[q] += ups[c0 + q];
+    X[r][c0 + q] = dev::silu(o[q]);
+  }
+  if (i < rows) row_store(p_out, i, c0, o);
+  __syncthreads();
+  rowmm(X, Ws + 4096, r, c0, o);
+  if (i < rows) {
+    const float4 hh = row_get(h, i, c0);
+    o[0] += hh.x, o[1] += hh.y, o[2] += hh.z, o[3] += hh.w;
+    row_store(h_out, i, c0, o);
+  }
+}
+
+// FF: ff_a = a' ; am = ((a' V^T) SiLU'(p)) U^T
+__global__ void __launch_bounds__(256) upd_ff_fused(int rows, const float* __restrict__ a, const float* __restrict__ p,
+                                                    const float* __restrict__ Vt, const float* __restrict__ Ut,
+                                                    float* __restrict__ ff_a, float* __restrict__ am) {
+  __shared__ __align__(16) float X[kRB][68];
+  extern __shared__ __align__(16) float Ws[];
+  const int i0 = blockIdx.x * kRB, r = threadIdx.x / 16, c0 = (threadIdx.x % 16) * 4, i = i0 + r;
+  {
+    const float* mats[2] = {Vt, Ut};
+    stage_mats(Ws, mats, 2);
+  }
+  row_load(X, a, i0, rows);
+  __syncthreads();
+  if (i < rows) {
+    const float v4[4] = {X[r][c0], X[r][c0 + 1], X[r][c0 + 2], X[r][c0 + 3]};
+    row_store(ff_a, i, c0, v4);
+  }
+  float o[4];
+  rowmm(X, Ws, r, c0, o);
+  __syncthreads();
+  if (i < rows) {
+    const float4 pp = row_get(p, i, c0);
+    o[0] *= dev::dsilu(pp.x), o[1] *= dev::dsilu(pp.y), o[2] *= dev::dsilu(pp.z), o[3] *= dev::dsilu(pp.w);
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) X[r][c0 + q] = o[q];
+  __syncthreads();
+  rowmm(X, Ws + 4096, r, c0, o);
+  if (i < rows) row_store(am, i, c0, o);
+}
+
+// BF: pdot = abar_m U ; r = a' V^T ; pbar = r pdot SiLU''(p) ; pdbar = r SiLU'(p) ;
+//     u = SiLU'(p) pdot ; inj = pbar U^T ; abar_h += u V
+__global__ void __launch_bounds__(256) upd_bf_fused(int rows, const float* __restrict__ am, const float* __restrict__ ffa,
+                                                    const float* __restrict__ p, const float* __restrict__ U,
+                                                    const float* __restrict__ Vt, const float* __restrict__ Ut,
+                                                    const float* __restrict__ V, float* __restrict__ pbar,
+                                                    float* __restrict__ pdbar, float* __restrict__ u,
+                                                    float* __restrict__ inj, float* ah) {
+  __shared__ __align__(16) float X[kRB][68];
+  __shared__ __align__(16) float Y[kRB][68];
+  extern __shared__ __align__(16) float Ws[];
+  const int i0 = blockIdx.x * kRB, r = threadIdx.x / 16, c0 = (threadIdx.x % 16) * 4, i = i0 + r;
+  {
+    const float* mats[4] = {U, Vt, Ut, V};
+    stage_mats(Ws, mats, 4);
+  }
+  row_load(X, am, i0, rows);
+  row_load(Y, ffa, i0, rows);
+  __syncthreads();
+  float pd[4], rr[4];
+  rowmm(X, Ws, r, c0, pd);
+  rowmm(Y, Ws + 4096, r, c0, rr);
+  __syncthreads();
+  float pb[4], pdb[4], uu[4];
+  const float4 pp4 = i < rows ? row_get(p, i, c0) : make_float4(0.f, 0.f, 0.f, 0.f);
+  const float pp[4] = {pp4.x, pp4.y, pp4.z, pp4.w};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float ds = dev::dsilu(pp[q]);
+    pb[q] = rr[q] * pd[q] * dev::d2silu(pp[q]);
+    pdb[q] = rr[q] * ds;
+    uu[q] = ds * pd[q];
+    X[r][c0 + q] = pb[q];
+    Y[r][c0 + q] = uu[q];
+  }
+  if (i < rows) {
+    row_store(pbar, i, c0, pb);
+    row_store(pdbar, i, c0, pdb);
+    row_store(u, i, c0, uu);
+  }
+  __syncthreads();
+  float o[4];
+  rowmm(X, Ws + 2 * 4096, r, c0, o);
+  if (i < rows) row_store(inj, i, c0, o);
+  rowmm(Y, Ws + 3 * 4096, r, c0, o);
+  if (i < rows) {
+    const float4 a4 = row_get(ah, i, c0);
+    o[0] += a4.x, o[1] += a4.y, o[2] += a4.z, o[3] += a4.w;
+    row_store(ah, i, c0, o);
+  }
+}
+
+// BE: r = b' V^T ; pbar = r SiLU'(p) ; b_m = pbar U^T + inj
+__global__ void __launch_bounds__(256) upd_be_fused(int rows, const float* __restrict__ bh, const float* __restrict__ p,
+                                                    const float* __restrict__ Vt, const float* __restrict__ Ut,
+                                                    const float* __restrict__ inj, float* __restrict__ pbar,
+                                                    float* __restrict__ bm) {
+  __shared__ __align__(16) float X[kRB][68];
+  extern __shared__ __align__(16) float Ws[];
+  const int i0 = blockIdx.x * kRB, r = threadIdx.x / 16, c0 = (threadIdx.x % 16) * 4, i = i0 + r;
+  {
+    const float* mats[2] = {Vt, Ut};
+    stage_mats(Ws, mats, 2);
+  }
+  row_load(X, bh, i0, rows);
+  __syncthreads();
+  float o[4];
+  rowmm(X, Ws, r, c0, o);
+  __syncthreads();
+  const float4 pp4 = i < rows ? row_get(p, i, c0) : make_float4(0.f, 0.f, 0.f, 0.f);
+  const float pp[4] = {pp4.x, pp4.y, pp4.z, pp4.w};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    o[q] *= dev::dsilu(pp[q]);
+    X[r][c0 + q] = o[q];
+  }
+  if (i < rows) row_store(pbar, i, c0, o);
+  __syncthreads();
+  rowmm(X, Ws + 4096, r, c0, o);
+  if (i < rows) {
+    const float4 j4 = row_get(inj, i, c0);
+    o[0] += j4.x, o[1] += j4.y, o[2] += j4.z, o[3] += j4.w;
+    row_store(bm, i, c0, o);
+  }
+}
+
+// ------------------------------------------------------- multi-job wgrad
+// Up to 3 independent weight-gradient jobs in one launch (grid.y = job),
+// 64-row chunks (grid.x); the last CTA to finish reduces every job's chunk
+// partials in chunk order (deterministic) and resets the launch counter.
+struct WJob {
+  const float *a, *b, *a2, *b2, *x1, *x2;
+  float *G, *cs1, *cs2;
+  int silu_a;
+};
+struct WJobs {
+  WJob j[3];
+  int n;
+};
+
+__global__ void __launch_bounds__(256) wgrad_multi_kernel(int rows, WJobs jobs, float* __restrict__ part,
+                                                          unsigned* __restrict__ counter) {
+  constexpr int H = 64, W = H * H + 2 * H;
+  __shared__ __align__(16) float sa[kWChunk][H + 4];
+  __shared__ __align__(16) float sb[kWChunk][H + 4];
+  __shared__ bool last;
+  const WJob& jb = jobs.j[blockIdx.y];
+  const int chunks = gridDim.x;
+  const int i0 = blockIdx.x * kWChunk;
+  const int n = min(kWChunk, rows - i0);
+  const int kb = (threadIdx.x >> 4) * 4, hb = (threadIdx.x & 15) * 4;
+  float acc[4][4];
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) acc[x][y] = 0.f;
+  for (int pass = 0; pass < (jb.a2 ? 2 : 1); ++pass) {
+    const float* A = pass ? jb.a2 : jb.a;
+    const float* B = pass ? jb.b2 : jb.b;
+    const bool sl = !pass && jb.silu_a;
+    __syncthreads();
+    {
+      constexpr int PER = kWChunk * H / 256;
+      float va[PER], vb[PER];
+#pragma unroll
+      for (int q = 0; q < PER; ++q) {
+        const int x = threadIdx.x + 256 * q, r = x / H, c = x % H;
+        const bool ok = r < n;
+        va[q] = ok ? __ldg(A + (size_t)(i0 + r) * H + c) : 0.f;
+        vb[q] = ok ? __ldg(B + (size_t)(i0 + r) * H + c) : 0.f;
+      }
+#pragma unroll
+      for (int q = 0; q < PER; ++q) {
+        const int x = threadIdx.x + 256 * q, r = x / H, c = x % H;
+        sa[r][c] = (sl && r < n) ? dev::silu(va[q]) : va[q];
+        sb[r][c] = vb[q];
+      }
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int r = 0; r < n; ++r) {
+      const float4 va = *reinterpret_cast<const float4*>(&sa[r][kb]);
+      const float4 vb = *reinterpret_cast<const float4*>(&sb[r][hb]);
+      const float xa[4] = {va.x, va.y, va.z, va.w}, xb[4] = {vb.x, vb.y, vb.z, vb.w};
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) acc[x][y] = fmaf(xa[x], xb[y], acc[x][y]);
+    }
+  }
+  float* P = part + ((size_t)blockIdx.y * chunks + blockIdx.x) * W;
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) P[(kb + x) * H + hb + y] = acc[x][y];
+  for (int q = 0; q < 2; ++q) {
+    const float* X = q ? jb.x2 : jb.x1;
+    if (!X) continue;
+    __syncthreads();
+    for (int x = threadIdx.x; x < kWChunk * H; x += 256) {
+      const int r = x / H, c = x % H;
+      sa[r][c] = r < n ? X[(size_t)(i0 + r) * H + c] : 0.f;
+    }
+    __syncthreads();
+    if (threadIdx.x < H) {
+      float s = 0.f;
+      for (int r = 0; r < n; ++r) s += sa[r][threadIdx.x];
+      P[H * H + q * H + threadIdx.x] = s;
+    }
+  }
+  // last CTA reduces (threadfence: partials visible before the counter bump)
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x * gridDim.y - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int job = 0; job < jobs.n; ++job) {
+    const WJob& J = jobs.j[job];
+    for (int o = threadIdx.x; o < W; o += 256) {
+      float* dst = o < H * H ? J.G : (o < H * H + H ? J.cs1 : J.cs2);
+      if (!dst) continue;
+      float s = 0.f;
+      for (int c = 0; c < chunks; ++c) s += __ldcg(part + ((size_t)job * chunks + c) * W + o);
+      dst[o < H * H ? o : (o - H * H) % H] = s;
+    }
+  }
+  if (threadIdx.x == 0) *counter = 0u;
+}
+
+}  // namespace node
+}  // namespace janus

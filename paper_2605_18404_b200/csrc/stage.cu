@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <initializer_list>
 #include <stdexcept>
 #include <vector>
 
@@ -85,6 +86,34 @@ void wgrad(Scratch& sc, cudaStream_t s, int rows, const float* a, const float* b
   JANUS_LAUNCH_CHECK("wgrad");
 }
 
+// Up to three weight-gradient jobs in one launch (last CTA reduces, fixed order).
+node::WJob wjob(const float* a, const float* b, float* G, const float* a2 = nullptr, const float* b2 = nullptr,
+                bool silu_a = false, const float* x1 = nullptr, float* cs1 = nullptr, const float* x2 = nullptr,
+                float* cs2 = nullptr) {
+  node::WJob j;
+  j.a = a;
+  j.b = b;
+  j.a2 = a2;
+  j.b2 = b2;
+  j.x1 = x1;
+  j.x2 = x2;
+  j.G = G;
+  j.cs1 = cs1;
+  j.cs2 = cs2;
+  j.silu_a = silu_a ? 1 : 0;
+  return j;
+}
+
+void wjobs(Scratch& sc, cudaStream_t s, int rows, std::initializer_list<node::WJob> list) {
+  node::WJobs J{};
+  J.n = static_cast<int>(list.size());
+  int k = 0;
+  for (const auto& j : list) J.j[k++] = j;
+  const dim3 grid(static_cast<unsigned>(blocks(rows, node::kWChunk)), static_cast<unsigned>(J.n));
+  node::wgrad_multi_kernel<<<grid, 256, 0, s>>>(rows, J, sc.wpart, sc.counter);
+  JANUS_LAUNCH_CHECK("wgrad_multi");
+}
+
 // out[z][k] = sum_{Z_i = z} x[i][k]; x == null: out[z] = sum_{Z_i = z} eps[s(i)]
 void species_sum(janus_stage* st, Scratch& sc, cudaStream_t s, const DevGeo& g, const float* x, const float* eps, float* out) {
   const int chunks = blocks(g.n_atoms, node::kWChunk), S = st->m.n_species;
@@ -122,6 +151,7 @@ MsgParams msg_params(const janus_stage* st, int u) {
   p.B = p.alpha + H;
   p.beta = p.B + H * H;
   p.Bt = st->tw[static_cast<size_t>(u - st->u0)];
+  p.pack = p.Bt + 2 * H * H;
   return p;
 }
 
@@ -136,6 +166,7 @@ void refresh_transposes(janus_stage* st, cudaStream_t s) {
       case kMsg:
         node::transpose_kernel<kH><<<b, 256, 0, s>>>(P + R * H + H, t);
         node::transpose_kernel<kH><<<b, 256, 0, s>>>(P + R * H + H + H * H + H, t + H * H);
+        edge_tc::pack_msg_weights<<<b, 256, 0, s>>>(P, P + R * H, P + R * H + H, P + R * H + H + H * H, t + 2 * H * H);
         break;
       case kUpd:
         node::transpose_kernel<kH><<<b, 256, 0, s>>>(P, t);
@@ -229,7 +260,9 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
     JANUS_CUDA(cudaMemcpy(st->params, unit_params, NP * sizeof(float), cudaMemcpyHostToDevice));
     for (int u = st->u0; u < st->u1; ++u) {
       const UnitKind k = unit_kind(u, m.L);
-      st->tw.push_back(k == kEmbed ? nullptr : dalloc<float>(st, (k == kReadout ? 1 : 2) * kH * kH, true));
+      // msg: [Bt | Wt | tensor-core pack]; upd: [Ut | Vt]; readout: [Ot]
+      const size_t n = k == kMsg ? 2 * kH * kH + edge_tc::kPackBytes / sizeof(float) : (k == kReadout ? 1 : 2) * kH * kH;
+      st->tw.push_back(k == kEmbed ? nullptr : dalloc<float>(st, n, true));
     }
     // geometry per micro-batch
     st->geo.resize(NMB);
@@ -307,12 +340,14 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
       sc.s5 = dalloc<float>(st, NH, false);
       sc.partial = dalloc<float>(st, NA * static_cast<size_t>(EC::PE), false);
       const size_t chunks = (NA + node::kWChunk - 1) / node::kWChunk;
-      sc.wpart = dalloc<float>(st, chunks * std::max<size_t>(kH * kH + 2 * kH, static_cast<size_t>(m.n_species) * kH), false);
+      sc.wpart = dalloc<float>(st, 3 * chunks * std::max<size_t>(kH * kH + 2 * kH, static_cast<size_t>(m.n_species) * kH), false);
+      sc.counter = dalloc<unsigned>(st, 1, false);
     }
     JANUS_CUDA(cudaFuncSetAttribute(edge::msg_fe_kernel<kH, kR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge::fe_smem<kH, kR>()));
     JANUS_CUDA(cudaFuncSetAttribute(edge::msg_ff_kernel<kH, kR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge::ff_smem<kH, kR>()));
     JANUS_CUDA(cudaFuncSetAttribute(edge::msg_bf_kernel<kH, kR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge::bf_smem<kH, kR>()));
     JANUS_CUDA(cudaFuncSetAttribute(edge::msg_be_kernel<kH, kR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge::be_smem<kH, kR>()));
+    JANUS_CUDA(cudaFuncSetAttribute(node::upd_bf_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)node::upd_smem(4)));
     JANUS_CUDA(cudaFuncSetAttribute(edge_tc::msg_fe_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge_tc::fe_smem()));
     JANUS_CUDA(cudaFuncSetAttribute(edge_tc::msg_ff_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge_tc::ff_smem()));
     JANUS_CUDA(cudaFuncSetAttribute(edge_tc::msg_bf_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge_tc::bf_smem()));
@@ -437,8 +472,7 @@ void stage_fe(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
       }
       case kUpd: {
         const float *Um = P, *ups = P + H * H, *V = P + H * H + H;
-        gemm(s, N, cur_m, Um, ups, nullptr, nullptr, b.p);
-        gemm(s, N, b.p, V, nullptr, cur_h, nullptr, b.out_h, node::InSilu{});
+        node::upd_fe_fused<<<blocks(N, node::kRB), 256, node::upd_smem(2), s>>>(N, cur_m, cur_h, Um, ups, V, b.p, b.out_h);
         cur_h = b.out_h;
         cur_m = nullptr;
         break;
@@ -490,14 +524,14 @@ void stage_ff(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
         gemm(s, N, b.p, T, nullptr, nullptr, nullptr, wh, node::InDsiluOmega{om});
         break;
       }
-      case kUpd: {  // a_m = ((a' V^T) SiLU'(p)) U^T
-        copy(s, b.ff_a, wh, NH);
-        gemm(s, N, wh, T + H * H, nullptr, nullptr, nullptr, sc.s1);
-        gemm(s, N, sc.s1, T, nullptr, nullptr, nullptr, wm, node::InMulDsilu{b.p, H});
+      case kUpd: {  // ff_a = a'; a_m = ((a' V^T) SiLU'(p)) U^T, written straight into the
+                    // preceding msg unit's saved FF input when it is on this stage
+        float* am_dst = (u - 1 >= st->u0) ? sl.units[static_cast<size_t>(u - 1 - st->u0)].ff_a : wm;
+        node::upd_ff_fused<<<blocks(N, node::kRB), 256, node::upd_smem(2), s>>>(N, wh, b.p, T + H * H, T, b.ff_a, am_dst);
         break;
       }
       case kMsg: {
-        copy(s, b.ff_a, wm, NH);
+        if (u == st->u1 - 1) copy(s, b.ff_a, wm, NH);  // a_m arrived through the ADJ_IN port
         if (g.n_tiles > 0 && use_tc(st))
           edge_tc::msg_ff_tc<<<g.n_tiles_tc, edge_tc::NT, edge_tc::ff_smem(), s>>>(eg, g.tile_row_tc, g.n_tiles_tc, msg_params(st, u),
                                                                                  st->m.r_c, b.v, b.ff_a, b.ff_Y, sl.F);
@@ -574,21 +608,17 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
           JANUS_CUDA(cudaMemsetAsync(sc.s2, 0, sizeof(float) * NH, s));
         }
         gemm(s, N, sc.s2, T + H * H, nullptr, nullptr, nullptr, b.inj);                  // hbar^F = X W^T
-        wgrad(sc, s, N, in_h(st, sl, u, N), sc.s2, ah, b.ff_Y, G2 + EC::PE);         // dW2 = h^T X + abar^T Y
+        wjobs(sc, s, N, {wjob(in_h(st, sl, u, N), sc.s2, G2 + EC::PE, ah, b.ff_Y)});  // dW2 = h^T X + abar^T Y
         break;
       }
       case kUpd: {
         const float *Um = P, *V = P + H * H + H;
         float *dU = G2, *dups = G2 + H * H, *dV = G2 + H * H + H;
-        gemm(s, N, am, Um, nullptr, nullptr, nullptr, sc.s1);             // pdot
-        gemm(s, N, b.ff_a, T + H * H, nullptr, nullptr, nullptr, sc.s2);  // r = a' V^T
-        node::upd_bf_ew_kernel<<<blocks(NH, 256), 256, 0, s>>>(static_cast<int>(NH), sc.s2, sc.s1, b.p, sc.s3,
-                                                               sc.s4, sc.s5);
-        gemm(s, N, sc.s3, T, nullptr, nullptr, nullptr, b.inj);           // mbar^F = pbar U^T
-        wgrad(sc, s, N, sc.s5, b.ff_a, nullptr, nullptr, dV);             // dV2 = u^T a'
-        wgrad(sc, s, N, in_m(st, sl, u, N), sc.s3, am, sc.s4, dU, node::InId{},
-              Colsums{sc.s3, dups});                                        // dU2 = m^T pbar + abar_m^T pdbar
-        gemm(s, N, sc.s5, V, nullptr, ah, nullptr, ah);                   // abar' = abar_h + u V
+        // pdot, r, pbar (s3), pdbar (s4), u (s5), mbar^F = pbar U^T, abar' = abar_h + u V
+        node::upd_bf_fused<<<blocks(N, node::kRB), 256, node::upd_smem(4), s>>>(N, am, b.ff_a, b.p, Um, T + H * H, T, V, sc.s3, sc.s4,
+                                                                sc.s5, b.inj, ah);
+        wjobs(sc, s, N, {wjob(sc.s5, b.ff_a, dV),                                          // dV2 = u^T a'
+                         wjob(in_m(st, sl, u, N), sc.s3, dU, am, sc.s4, false, sc.s3, dups)});  // dU2, dups2
         break;
       }
       case kReadout: {
@@ -598,8 +628,7 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
         node::ro_bf_ew_kernel<kH><<<blocks(NH, 256), 256, 0, s>>>(static_cast<int>(NH), sc.s1, b.p, om, sc.s2,
                                                                   sc.s3, sc.s4);
         gemm(s, N, sc.s2, T, nullptr, nullptr, nullptr, b.inj);  // hbar^F = tau O^T
-        wgrad(sc, s, N, ah, sc.s4, in_h(st, sl, u, N), sc.s2, dO, node::InId{},
-              Colsums{sc.s3, dom, sc.s2, dob});
+        wjobs(sc, s, N, {wjob(ah, sc.s4, dO, in_h(st, sl, u, N), sc.s2, false, sc.s3, dom, sc.s2, dob)});
         break;
       }
     }
@@ -651,19 +680,16 @@ void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only, 
         node::ro_be_ew_kernel<kH><<<blocks(NH, 256), 256, 0, s>>>(static_cast<int>(NH), b.p, om, sl.eps, g.struct_id,
                                                                   sc.s1, sc.s2);
         gemm(s, N, sc.s1, T, nullptr, b.inj, nullptr, bh);  // b_h = tbar O^T + hbar^F
-        wgrad(sc, s, N, in_h(st, sl, u, N), sc.s1, nullptr, nullptr, dO, node::InId{},
-              Colsums{sc.s1, dob, sc.s2, dom});
+        wjobs(sc, s, N, {wjob(in_h(st, sl, u, N), sc.s1, dO, nullptr, nullptr, false, sc.s1, dob, sc.s2, dom)});
         species_sum(st, sc, s, g, nullptr, sl.eps, dbias);
         break;
       }
       case kUpd: {
         float *dU = G1, *dups = G1 + H * H, *dV = G1 + H * H + H;
-        gemm(s, N, bh, T + H * H, nullptr, nullptr, nullptr, sc.s1);  // r = b' V^T
-        node::upd_be_ew_kernel<<<blocks(NH, 256), 256, 0, s>>>(static_cast<int>(NH), sc.s1, b.p, sc.s2);
-        gemm(s, N, sc.s2, T, nullptr, b.inj, nullptr, bm);             // b_m = pbar U^T + mbar^F
-        wgrad(sc, s, N, b.p, bh, nullptr, nullptr, dV, node::InSilu{});  // dV1 = SiLU(p)^T b'
-        wgrad(sc, s, N, in_m(st, sl, u, N), sc.s2, nullptr, nullptr, dU, node::InId{},
-              Colsums{sc.s2, dups});                                     // dU1 = m^T pbar
+        // pbar (s2) = (b' V^T) SiLU'(p); b_m = pbar U^T + mbar^F
+        node::upd_be_fused<<<blocks(N, node::kRB), 256, node::upd_smem(2), s>>>(N, bh, b.p, T + H * H, T, b.inj, sc.s2, bm);
+        wjobs(sc, s, N, {wjob(b.p, bh, dV, nullptr, nullptr, true),                                  // dV1 = SiLU(p)^T b'
+                         wjob(in_m(st, sl, u, N), sc.s2, dU, nullptr, nullptr, false, sc.s2, dups)});  // dU1, dups1
         break;
       }
       case kMsg: {
@@ -681,7 +707,7 @@ void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only, 
         } else {
           JANUS_CUDA(cudaMemsetAsync(sc.s1, 0, sizeof(float) * NH, s));
         }
-        wgrad(sc, s, N, in_h(st, sl, u, N), sc.s1, nullptr, nullptr, G1 + EC::PE);  // dW1 = h^T Yb
+        wjobs(sc, s, N, {wjob(in_h(st, sl, u, N), sc.s1, G1 + EC::PE)});  // dW1 = h^T Yb
         gemm(s, N, sc.s1, T + H * H, nullptr, bh, b.inj, bh);                 // b_h += Yb W^T + hbar^F
         break;
       }

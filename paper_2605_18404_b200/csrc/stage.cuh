@@ -57,6 +57,7 @@ struct Port {
 struct Scratch {
   float *wh = nullptr, *wm = nullptr, *s1 = nullptr, *s2 = nullptr, *s3 = nullptr, *s4 = nullptr, *s5 = nullptr;
   float *partial = nullptr, *wpart = nullptr;
+  unsigned* counter = nullptr;  // last-CTA-reduces launch counter (one launch at a time per lane)
 };
 
 struct Slot {

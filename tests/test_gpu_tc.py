@@ -44,7 +44,10 @@ CASES = {
 }
 
 
-@pytest.mark.parametrize("name", list(CASES))
+MN = {"amn_m128", "bmn_m128", "mn_m64"}  # tcgen05 transpose bit with kind::tf32: measured to return zeros
+
+
+@pytest.mark.parametrize("name", [n for n in CASES if n not in MN])
 def test_probe(janus, has_gpu, name):
     if not has_gpu:
         pytest.skip("no GPU")
@@ -73,9 +76,11 @@ def test_probe_mn_swapped(janus, has_gpu, name):
     D = probe(janus, M, N, K, amn, bmn, A, B, swap=1)
     lanes, err = lane_map(D, ref(tf32(A), tf32(B)))
     print(f"{name} swapped: rel err {err:.2e}; |D| max {np.abs(D).max():.3f}")
+    # documents the finding that drives edge_tc.cuh's transposed tiles
+    assert np.abs(D).max() == 0.0
 
 
-@pytest.mark.parametrize("name", list(CASES))
+@pytest.mark.parametrize("name", [n for n in CASES if n not in MN])
 def test_probe_sw128(janus, has_gpu, name):
     """SWIZZLE_128B tiles: K-major and MN-major views of [row][col] slabs."""
     if not has_gpu:
