@@ -597,94 +597,80 @@ struct WJobs {
   int n;
 };
 
-__global__ void __launch_bounds__(256) wgrad_multi_kernel(int rows, WJobs jobs, float* __restrict__ part,
-                                                          unsigned* __restrict__ counter) {
-  constexpr int H = 64, W = H * H + 2 * H;
-  __shared__ __align__(16) float sa[kWChunk][H + 4];
+// Output-partitioned (no reduction pass): grid.y = job; grid.x = 8 CTAs each
+// owning 8 rows of the 64x64 gradient (thread: 1 row, 2 columns), looping over
+// all atoms in 64-row chunks in order, + 1 CTA for the column sums.  Every
+// output is summed by one thread in atom order => deterministic.
+__global__ void __launch_bounds__(256) wgrad_multi_kernel(int rows, WJobs jobs, float* __restrict__ /*part*/,
+                                                          unsigned* __restrict__ /*counter*/) {
+  constexpr int H = 64;
+  __shared__ __align__(16) float sa[kWChunk][8];
   __shared__ __align__(16) float sb[kWChunk][H + 4];
-  __shared__ bool last;
   const WJob& jb = jobs.j[blockIdx.y];
-  const int chunks = gridDim.x;
-  const int i0 = blockIdx.x * kWChunk;
-  const int n = min(kWChunk, rows - i0);
-  const int kb = (threadIdx.x >> 4) * 4, hb = (threadIdx.x & 15) * 4;
-  float acc[4][4];
+  if (blockIdx.x == 8) {  // column sums
+    const int q = threadIdx.x >> 6, c = threadIdx.x & 63;
+    const float* X = q == 0 ? jb.x1 : (q == 1 ? jb.x2 : nullptr);
+    float* out = q == 0 ? jb.cs1 : (q == 1 ? jb.cs2 : nullptr);
+    if (!X || !out) return;
+    float s0 = 0.f;
+    int i = 0;
+    for (; i + 8 <= rows; i += 8) {  // 8 loads in flight, summed in order
+      float v[8];
 #pragma unroll
-  for (int x = 0; x < 4; ++x)
+      for (int u = 0; u < 8; ++u) v[u] = __ldg(X + (size_t)(i + u) * H + c);
 #pragma unroll
-    for (int y = 0; y < 4; ++y) acc[x][y] = 0.f;
+      for (int u = 0; u < 8; ++u) s0 += v[u];
+    }
+    for (; i < rows; ++i) s0 += __ldg(X + (size_t)i * H + c);
+    out[c] = s0;
+    return;
+  }
+  const int k0 = blockIdx.x * 8;
+  const int kr = threadIdx.x >> 5, h = threadIdx.x & 31;
+  float acc0 = 0.f, acc1 = 0.f;
   for (int pass = 0; pass < (jb.a2 ? 2 : 1); ++pass) {
     const float* A = pass ? jb.a2 : jb.a;
     const float* B = pass ? jb.b2 : jb.b;
     const bool sl = !pass && jb.silu_a;
-    __syncthreads();
-    {
-      constexpr int PER = kWChunk * H / 256;
-      float va[PER], vb[PER];
+    for (int i0 = 0; i0 < rows; i0 += kWChunk) {
+      const int n = min(kWChunk, rows - i0);
+      __syncthreads();
+      {
+        // a: 64 rows x 8 cols (2 per thread); b: 64 rows x 64 cols (4 float4 per thread)
+        float va[2];
+        float4 vb[4];
 #pragma unroll
-      for (int q = 0; q < PER; ++q) {
-        const int x = threadIdx.x + 256 * q, r = x / H, c = x % H;
-        const bool ok = r < n;
-        va[q] = ok ? __ldg(A + (size_t)(i0 + r) * H + c) : 0.f;
-        vb[q] = ok ? __ldg(B + (size_t)(i0 + r) * H + c) : 0.f;
+        for (int q = 0; q < 2; ++q) {
+          const int x = threadIdx.x + 256 * q, r = x >> 3, c = x & 7;
+          va[q] = r < n ? __ldg(A + (size_t)(i0 + r) * H + k0 + c) : 0.f;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int x = threadIdx.x + 256 * q, r = x >> 4, c4 = x & 15;
+          vb[q] = r < n ? __ldg(reinterpret_cast<const float4*>(B + (size_t)(i0 + r) * H) + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int x = threadIdx.x + 256 * q, r = x >> 3, c = x & 7;
+          sa[r][c] = (sl && r < n) ? dev::silu(va[q]) : va[q];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int x = threadIdx.x + 256 * q, r = x >> 4, c4 = x & 15;
+          *reinterpret_cast<float4*>(&sb[r][4 * c4]) = vb[q];
+        }
       }
-#pragma unroll
-      for (int q = 0; q < PER; ++q) {
-        const int x = threadIdx.x + 256 * q, r = x / H, c = x % H;
-        sa[r][c] = (sl && r < n) ? dev::silu(va[q]) : va[q];
-        sb[r][c] = vb[q];
+      __syncthreads();
+#pragma unroll 8
+      for (int r = 0; r < n; ++r) {
+        const float a = sa[r][kr];
+        acc0 = fmaf(a, sb[r][h], acc0);
+        acc1 = fmaf(a, sb[r][h + 32], acc1);
       }
     }
-    __syncthreads();
-#pragma unroll 4
-    for (int r = 0; r < n; ++r) {
-      const float4 va = *reinterpret_cast<const float4*>(&sa[r][kb]);
-      const float4 vb = *reinterpret_cast<const float4*>(&sb[r][hb]);
-      const float xa[4] = {va.x, va.y, va.z, va.w}, xb[4] = {vb.x, vb.y, vb.z, vb.w};
-#pragma unroll
-      for (int x = 0; x < 4; ++x)
-#pragma unroll
-        for (int y = 0; y < 4; ++y) acc[x][y] = fmaf(xa[x], xb[y], acc[x][y]);
-    }
   }
-  float* P = part + ((size_t)blockIdx.y * chunks + blockIdx.x) * W;
-#pragma unroll
-  for (int x = 0; x < 4; ++x)
-#pragma unroll
-    for (int y = 0; y < 4; ++y) P[(kb + x) * H + hb + y] = acc[x][y];
-  for (int q = 0; q < 2; ++q) {
-    const float* X = q ? jb.x2 : jb.x1;
-    if (!X) continue;
-    __syncthreads();
-    for (int x = threadIdx.x; x < kWChunk * H; x += 256) {
-      const int r = x / H, c = x % H;
-      sa[r][c] = r < n ? X[(size_t)(i0 + r) * H + c] : 0.f;
-    }
-    __syncthreads();
-    if (threadIdx.x < H) {
-      float s = 0.f;
-      for (int r = 0; r < n; ++r) s += sa[r][threadIdx.x];
-      P[H * H + q * H + threadIdx.x] = s;
-    }
-  }
-  // last CTA reduces (threadfence: partials visible before the counter bump)
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x * gridDim.y - 1;
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  for (int job = 0; job < jobs.n; ++job) {
-    const WJob& J = jobs.j[job];
-    for (int o = threadIdx.x; o < W; o += 256) {
-      float* dst = o < H * H ? J.G : (o < H * H + H ? J.cs1 : J.cs2);
-      if (!dst) continue;
-      float s = 0.f;
-      for (int c = 0; c < chunks; ++c) s += __ldcg(part + ((size_t)job * chunks + c) * W + o);
-      dst[o < H * H ? o : (o - H * H) % H] = s;
-    }
-  }
-  if (threadIdx.x == 0) *counter = 0u;
+  jb.G[(k0 + kr) * H + h] = acc0;
+  jb.G[(k0 + kr) * H + h + 32] = acc1;
 }
 
 }  // namespace node

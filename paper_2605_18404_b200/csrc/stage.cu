@@ -109,7 +109,7 @@ void wjobs(Scratch& sc, cudaStream_t s, int rows, std::initializer_list<node::WJ
   J.n = static_cast<int>(list.size());
   int k = 0;
   for (const auto& j : list) J.j[k++] = j;
-  const dim3 grid(static_cast<unsigned>(blocks(rows, node::kWChunk)), static_cast<unsigned>(J.n));
+  const dim3 grid(9u, static_cast<unsigned>(J.n));  // 8 row blocks of the gradient + 1 column-sum block
   node::wgrad_multi_kernel<<<grid, 256, 0, s>>>(rows, J, sc.wpart, sc.counter);
   JANUS_LAUNCH_CHECK("wgrad_multi");
 }
