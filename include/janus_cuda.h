@@ -201,6 +201,10 @@ int janus_tc_probe(const int32_t* args, const float* A, const float* B, float* D
 /* ---- schedule generation (host only) ---- */
 int janus_schedule_generate(int method, int P, int n_mb, int k, char* buf, int64_t cap, int64_t* len);
 int janus_schedule_validate(const char* text, int32_t* n_errors);
+/* Replay (graph.hpp:168) a schedule under phase times t[4] = {FE, FF, BE, BF}
+ * (FF with the recompute flag costs FF + FE): makespan and bubble ratio
+ * sum idle / (devices * makespan). */
+int janus_schedule_replay(const char* text, const double* t, double* makespan, double* bubble_ratio);
 
 #ifdef __cplusplus
 }

@@ -323,6 +323,17 @@ def validate_schedule(text: str) -> int:
     return n.value
 
 
+_sig("janus_schedule_replay", c_int, ctypes.c_char_p, c_vp, c_vp, c_vp)
+
+
+def schedule_replay(text: str, t_fe: float, t_ff: float, t_be: float, t_bf: float):
+    """Replay a schedule under phase times -> (makespan, bubble ratio)."""
+    t = np.array([t_fe, t_ff, t_be, t_bf], np.float64)
+    ms, br = c_d(), c_d()
+    check(_lib.janus_schedule_replay(text.encode(), _p(t), ctypes.byref(ms), ctypes.byref(br)))
+    return ms.value, br.value
+
+
 def device_count() -> int:
     n = c_int()
     check(_lib.janus_device_count(ctypes.byref(n)))

@@ -369,4 +369,26 @@ int janus_schedule_validate(const char* text, int32_t* n_errors) {
   });
 }
 
+int janus_schedule_replay(const char* text, const double* t, double* makespan, double* bubble_ratio) {
+  return guard([&] {
+    need(text, "text");
+    need(t, "t");
+    need(makespan, "makespan");
+    need(bubble_ratio, "bubble_ratio");
+    const janus::Schedule s = janus::deserialize(text);
+    const janus::DepGraph g = janus::build_dependencies(s);
+    janus::PhaseTimes pt;
+    pt.t_FE = t[0];
+    pt.t_FF = t[1];
+    pt.t_BE = t[2];
+    pt.t_BF = t[3];
+    const std::vector<double> d = janus::phase_durations(g, pt);
+    const janus::ReplayResult r = janus::replay(g, d);
+    if (!r.ok) throw janus::deadlock_error("replay: " + r.blocked);
+    const janus::BubbleReport b = janus::bubble_of(g, r, d);
+    *makespan = r.makespan;
+    *bubble_ratio = b.bubble_ratio;
+  });
+}
+
 }  // extern "C"

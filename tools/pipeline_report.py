@@ -1,0 +1,160 @@
+#!/usr/bin/env python3
+"""Pipeline-schedule report on ONE B200: SymFold vs WaveK vs 1F1B-2nd.
+
+All P pipeline stages run in this process on one GPU as virtual devices
+(local transport: async device-to-device copies + events), strict device-list
+order (lanes = 1), per-instruction CUDA-event timeline.  For each schedule:
+  * measured makespan and bubble ratio  sum idle / (P makespan);
+  * replay-predicted makespan / bubble of the same schedule under the measured
+    mean phase times (graph.hpp:168 replay, the reference's own model);
+  * peak live activation bytes per stage from the SPEC lifetime rule
+    (FE activations live FE->BE, FF intermediates FF->BF, BF->BE
+    injections BF->BE) evaluated on the measured timeline, + static bytes.
+Virtual devices share the SMs of one GPU, so measured bubbles include
+contention; the replay column is the schedule's intrinsic bubble.
+Usage: python tools/pipeline_report.py [--out gpurun_out/pipeline_report.json]
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_2605_18404_b200 as J  # noqa: E402
+
+KIND = {0: "FE", 1: "FF", 2: "BE", 3: "BF"}
+
+
+def activation_bytes(model, u0, u1, n_atoms):
+    """Per-micro-batch bytes of the three lifetime classes for units [u0,u1)."""
+    NH4 = n_atoms * model.H * 4
+    fe = ff = inj = 0
+    for u in range(u0, u1):
+        if u == 0:
+            fe += NH4
+        elif u == model.n_units - 1:
+            fe += NH4
+            inj += NH4
+        elif u % 2 == 1:
+            fe += 2 * NH4
+            ff += 2 * NH4
+            inj += NH4
+        else:
+            fe += 2 * NH4
+            ff += NH4
+            inj += NH4
+    return fe, ff, inj
+
+
+def peak_live(tl, dev, sizes):
+    """Max over time of live bytes on `dev` from the timeline records."""
+    fe_b, ff_b, inj_b = sizes
+    ev = []
+    by = {}
+    for d, k, mb, a, b in tl:
+        if int(d) != dev:
+            continue
+        by.setdefault((int(mb), KIND[int(k)]), []).append((a, b))
+    for mb in {m for m, _ in by}:
+        def span(kind, pick):
+            x = by.get((mb, kind))
+            return pick(x) if x else None
+        fe0 = span("FE", lambda x: min(a for a, _ in x))
+        be1 = span("BE", lambda x: max(b for _, b in x))
+        ff0 = span("FF", lambda x: min(a for a, _ in x))
+        bf1 = span("BF", lambda x: max(b for _, b in x))
+        bf0 = span("BF", lambda x: min(a for a, _ in x))
+        if fe0 is not None and be1 is not None:
+            ev += [(fe0, fe_b), (be1, -fe_b)]
+        elif ff0 is not None and bf1 is not None:  # 1F1B force replica: recomputed FE lives FF->BF
+            ev += [(ff0, fe_b), (bf1, -fe_b)]
+        if ff0 is not None and bf1 is not None:
+            ev += [(ff0, ff_b), (bf1, -ff_b)]
+        if bf0 is not None:
+            end = be1 if be1 is not None else bf1
+            ev += [(bf0, inj_b), (end, -inj_b)]
+    live = peak = 0
+    for _, x in sorted(ev, key=lambda e: (e[0], e[1])):
+        live += x
+        peak = max(peak, live)
+    return peak
+
+
+def run(model, params, batches, P, method, k, steps=3, warmup=2):
+    t = J.Trainer(model, params, P, method, len(batches), k=k, max_atoms=batches[0].n_atoms,
+                  max_edges=max(b.n_edges for b in batches) + 64, max_struct=1, timeline=True, lanes=1)
+    for i, b in enumerate(batches):
+        t.load(i, b)
+    for _ in range(warmup):
+        t.step()
+    stats, tls = [], []
+    for _ in range(steps):
+        stats.append(t.step())
+        tls.append(t.timeline())
+    i = int(np.argsort([s.makespan_ms for s in stats])[len(stats) // 2])
+    s, tl = stats[i], tls[i]
+    phase = {}
+    for name, kk in (("FE", 0), ("FF", 1), ("BE", 2), ("BF", 3)):
+        d = tl[tl[:, 1] == kk]
+        phase[name] = float((d[:, 4] - d[:, 3]).mean()) if len(d) else 0.0
+    text = t.schedule_text()
+    # replay with measured per-instruction means (FF of 1F1B already contains the recompute)
+    ff = phase["FF"] - (phase["FE"] if method == J.METHOD_ONEF1B else 0.0)
+    pred_ms, pred_bubble = J.schedule_replay(text, phase["FE"], max(ff, 1e-6), phase["BE"], phase["BF"])
+    plan = t.plan()
+    mem = []
+    for dv in range(P):
+        blocks = [b for b in range(P) if J_device_of(text, b, P, "E") == dv] + \
+                 [b for b in range(P) if J_device_of(text, b, P, "F") == dv]
+        peak = 0
+        for b in set(blocks):
+            sizes = activation_bytes(model, int(plan[b][0]), int(plan[b][1]), batches[0].n_atoms)
+            peak += peak_live(tl, dv, sizes) / max(1, len(set(blocks)))
+        mem.append({"device": dv, "static_plus_arena_bytes": int(s.peak_bytes[dv]), "peak_live_activation_bytes": int(peak)})
+    out = {"P": P, "method": {0: "symfold", 1: "wavek", 2: "onef1b_2nd"}[method], "k": k,
+           "makespan_ms": s.makespan_ms, "structures_per_s": len(batches) / (s.makespan_ms / 1e3),
+           "bubble_measured": s.bubble_ratio, "busy_ms": [s.busy_ms[d] for d in range(P)],
+           "phase_mean_us": {k2: v * 1e3 / 1e3 for k2, v in phase.items()},
+           "replay_makespan_ms": pred_ms / 1e3, "bubble_replay": pred_bubble,
+           "p2p_bytes_per_step": int(s.p2p_bytes), "memory": mem}
+    t.close()
+    return out
+
+
+def J_device_of(text, block, P, side):
+    """Device of energy (vs=block) or force (vs=2P-1-block) stage from the schedule text."""
+    vs = block if side == "E" else 2 * P - 1 - block
+    for line in text.splitlines()[1:]:
+        f = line.split()
+        if f[2] in ("FE", "FF", "BE", "BF") and f[4] == f"vs={vs}":
+            return int(f[0][1:])
+    return -1
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "pipeline_report.json"))
+    ap.add_argument("--Ps", default="2,4,8")
+    ap.add_argument("--nmb", type=int, default=32)
+    args = ap.parse_args()
+    model = J.Model(L=4, H=64, R=64, precision=J.PREC_TF32)
+    params = model.synth_params(7)
+    batches = [J.synth_batch(model, [256], 0.095, 700 + m) for m in range(args.nmb)]
+    rows = []
+    for P in [int(x) for x in args.Ps.split(",")]:
+        for method, k in ((J.METHOD_ONEF1B, 1), (J.METHOD_SYMFOLD, 1), (J.METHOD_WAVEK, P), (J.METHOD_WAVEK, 2 * P)):
+            r = run(model, params, batches, P, method, k)
+            rows.append(r)
+            print(json.dumps({x: r[x] for x in ("P", "method", "k", "makespan_ms", "structures_per_s", "bubble_measured",
+                                                "bubble_replay")}), flush=True)
+    os.makedirs(os.path.dirname(args.out), exist_ok=True)
+    json.dump({"config": "C2: L=4 H=64 R=64, 256-atom cells, N_mb=%d, tf32, 1 GPU, lanes=1" % args.nmb, "rows": rows},
+              open(args.out, "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()
