@@ -110,10 +110,11 @@ def run(model, params, batches, P, method, k, steps=3, warmup=2):
     for dv in range(P):
         blocks = [b for b in range(P) if J_device_of(text, b, P, "E") == dv] + \
                  [b for b in range(P) if J_device_of(text, b, P, "F") == dv]
-        peak = 0
-        for b in set(blocks):
-            sizes = activation_bytes(model, int(plan[b][0]), int(plan[b][1]), batches[0].n_atoms)
-            peak += peak_live(tl, dv, sizes) / max(1, len(set(blocks)))
+        sizes = [0, 0, 0]
+        for b in sorted(set(blocks)):  # every block whose stage object lives on this device
+            for q, x in enumerate(activation_bytes(model, int(plan[b][0]), int(plan[b][1]), batches[0].n_atoms)):
+                sizes[q] += x
+        peak = peak_live(tl, dv, sizes)
         mem.append({"device": dv, "static_plus_arena_bytes": int(s.peak_bytes[dv]), "peak_live_activation_bytes": int(peak)})
     out = {"P": P, "method": {0: "symfold", 1: "wavek", 2: "onef1b_2nd"}[method], "k": k,
            "makespan_ms": s.makespan_ms, "structures_per_s": len(batches) / (s.makespan_ms / 1e3),
