@@ -181,6 +181,36 @@ __device__ __forceinline__ void seg_write(int r0, int r1, float* const (&out)[NA
   }
 }
 
+// Row epilogue fused into the edge kernels: the tile's finished rows R (from
+// the segmented sums) times W^T:  out[r] = (base ? base[r] : 0) + R[r] W^T
+// (+ add[r]).  Rows staged in smem (rs[8][64]), W^T ([64][64] row-major) via L1.
+__device__ __forceinline__ void rows_times_wt(int r0, int r1, const float (&acc)[2], float* rs, const float* __restrict__ Wt,
+                                              const float* base, const float* __restrict__ add, float* out) {
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int pidx = threadIdx.x + 256 * k;
+    rs[(pidx >> 6) * 64 + (pidx & 63)] = (r0 + (pidx >> 6) < r1) ? acc[k] : 0.f;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int pidx = threadIdx.x + 256 * k;
+    const int rl = pidx >> 6, c = pidx & 63, r = r0 + rl;
+    if (r >= r1) continue;
+    float o0 = 0.f, o1 = 0.f;
+#pragma unroll 8
+    for (int q = 0; q < 64; q += 2) {
+      o0 = fmaf(rs[rl * 64 + q], __ldg(Wt + q * 64 + c), o0);
+      o1 = fmaf(rs[rl * 64 + q + 1], __ldg(Wt + (q + 1) * 64 + c), o1);
+    }
+    float y = o0 + o1;
+    if (base) y += base[(size_t)r * H + c];
+    if (add) y += add[(size_t)r * H + c];
+    out[(size_t)r * H + c] = y;
+  }
+  __syncthreads();
+}
+
 // 32 consecutive features of row `row` of an [N][64] array (8 float4 loads in flight)
 __device__ __forceinline__ void gather32(const float* __restrict__ x, int row, int f0, float (&v)[32]) {
   const float4* p = reinterpret_cast<const float4*>(x + (size_t)row * H + f0);
@@ -345,7 +375,8 @@ __global__ void __launch_bounds__(NT) msg_fe_tc(EdgeGeom g, const int* __restric
 // q_e + q_rev(e) = < am_i v_j + am_j v_i , w'_e >  (w' symmetric in e <-> rev e)
 __global__ void __launch_bounds__(NT) msg_ff_tc(EdgeGeom g, const int* __restrict__ tiles, int n_tiles, MsgParams p,
                                                float rc, const float* __restrict__ v, const float* __restrict__ am,
-                                               float* __restrict__ Y_out, float* __restrict__ F) {
+                                               float* __restrict__ Y_out, float* __restrict__ F, const float* __restrict__ Wt,
+                                               float* ah) {
   extern __shared__ __align__(1024) uint8_t sm[];
   uint8_t* W0 = sm;
   uint8_t* W1 = W0 + kWTile;
@@ -454,6 +485,7 @@ __global__ void __launch_bounds__(NT) msg_ff_tc(EdgeGeom g, const int* __restric
       const int r = tr.r0 + threadIdx.x / 3;
       if (r < tr.r1) F[3 * r + threadIdx.x % 3] += fsum;
     }
+    if (ah) rows_times_wt(tr.r0, tr.r1, acc[0], reinterpret_cast<float*>(T1), Wt, ah, nullptr, ah);  // a_h += Y W^T
   }
   teardown(c, 256);
 }
@@ -500,7 +532,8 @@ __device__ __forceinline__ void write_partial(Ctx& c, float* part, uint8_t* scra
 // zbar = (gbar B^T) SiLU'(z); dA = phi^T zbar; dalpha = sum zbar.
 __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int* __restrict__ tiles, int n_tiles, MsgParams p,
                                                   float rc, const float* __restrict__ v, const float* __restrict__ bm,
-                                                  float* __restrict__ Yb_out, float* __restrict__ partial) {
+                                                  float* __restrict__ Yb_out, float* __restrict__ partial,
+                                                  const float* __restrict__ Wt, const float* __restrict__ inj, float* bh) {
   extern __shared__ __align__(1024) uint8_t sm[];
   uint8_t* W0 = sm;           // A^T
   uint8_t* W1 = W0 + kWTile;  // B^T
@@ -619,6 +652,7 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int* __rest
     }
     float* const outs[1] = {Yb_out};
     seg_write<1>(tr.r0, tr.r1, outs, acc);
+    if (bh) rows_times_wt(tr.r0, tr.r1, acc[0], reinterpret_cast<float*>(T1), Wt, bh, inj, bh);  // b_h += Yb W^T + inj
   }
   float* part = partial + (size_t)blockIdx.x * PE;
   if (first) {  // CTA without tiles: zero partial (TMEM accumulators never written)
@@ -637,7 +671,8 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
                                                   float rc, const float* __restrict__ v, const float* __restrict__ vdot,
                                                   const float* __restrict__ am, const float* __restrict__ Fbar,
                                                   float* __restrict__ mdot_out, float* __restrict__ X_out,
-                                                  float* __restrict__ partial) {
+                                                  float* __restrict__ partial, const float* __restrict__ Wt,
+                                                  float* __restrict__ inj) {
   extern __shared__ __align__(1024) uint8_t sm[];
   uint8_t* W0 = sm;
   uint8_t* W1 = W0 + kWTile;
@@ -799,6 +834,7 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
     }
     float* const outs[2] = {mdot_out, X_out};
     seg_write<2>(tr.r0, tr.r1, outs, acc);
+    if (inj) rows_times_wt(tr.r0, tr.r1, acc[1], reinterpret_cast<float*>(T1), Wt, nullptr, nullptr, inj);  // hbar^F = X W^T
   }
   float* part = partial + (size_t)blockIdx.x * PE;
   if (first) {

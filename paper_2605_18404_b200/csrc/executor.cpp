@@ -648,8 +648,11 @@ void trainer_destroy(janus_trainer* t) {
 
 void trainer_load(janus_trainer* t, int mb, const janus_host_batch& hb) {
   if (mb < 0 || mb >= t->ed.n_micro_batches) throw domain_error("micro-batch index out of range");
-  for (janus_stage* s : t->owned) stage_load(s, mb, hb, t->root);
+  // asynchronous on the root stream (the step is issued behind it on the same
+  // stream); the last micro-batch of a batch of loads synchronises once
+  for (janus_stage* s : t->owned) stage_load(s, mb, hb, t->root, /*sync=*/false);
   t->n_atoms[static_cast<size_t>(mb)] = hb.n_atoms;
+  if (mb == t->ed.n_micro_batches - 1) JANUS_CUDA(cudaStreamSynchronize(t->root));
 }
 
 // count kernel nodes of one captured step (the gpu_launches evidence)
@@ -736,19 +739,23 @@ void trainer_step(janus_trainer* t, const janus_opt& opt, janus_step_stats* stat
     if (dev < 64) s.peak_bytes[dev] += st->static_bytes + st->arena_bytes;
   }
   // losses held here: L_E on the readout stage, L_F on the stage holding block 0's force replica
+  // (slot == micro-batch; one contiguous copy per stage, summed in micro-batch order)
   double loss = 0;
-  for (int m = 0; m < t->ed.n_micro_batches; ++m) {
-    float l[2];
+  {
+    const int n = t->ed.n_micro_batches;
+    std::vector<float> buf(2 * static_cast<size_t>(n));
     janus_stage* top = t->E[static_cast<size_t>(t->P - 1)];
-    if (top) {
-      JANUS_CUDA(cudaMemcpy(l, top->slots[static_cast<size_t>(m)].loss, sizeof(float), cudaMemcpyDeviceToHost));
-      loss += l[0];
-    }
     janus_stage* bot = t->F[0];
-    if (bot) {
-      JANUS_CUDA(cudaMemcpy(l + 1, bot->slots[static_cast<size_t>(m)].loss + 1, sizeof(float), cudaMemcpyDeviceToHost));
-      loss += l[1];
+    std::vector<float> lE(static_cast<size_t>(n), 0.f), lF(static_cast<size_t>(n), 0.f);
+    if (top) {
+      JANUS_CUDA(cudaMemcpy(buf.data(), top->losses, sizeof(float) * 2 * n, cudaMemcpyDeviceToHost));
+      for (int m = 0; m < n; ++m) lE[static_cast<size_t>(m)] = buf[2 * static_cast<size_t>(m)];
     }
+    if (bot) {
+      JANUS_CUDA(cudaMemcpy(buf.data(), bot->losses, sizeof(float) * 2 * n, cudaMemcpyDeviceToHost));
+      for (int m = 0; m < n; ++m) lF[static_cast<size_t>(m)] = buf[2 * static_cast<size_t>(m) + 1];
+    }
+    for (int m = 0; m < n; ++m) loss += static_cast<double>(lE[static_cast<size_t>(m)]) + lF[static_cast<size_t>(m)];
   }
   s.loss = loss;
   t->last = s;

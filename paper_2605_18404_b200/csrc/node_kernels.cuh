@@ -352,32 +352,35 @@ __global__ void transpose_kernel(const float* __restrict__ src, float* __restric
 }
 
 // ------------------------------------------------------------ LM geometry
-// r = x_j + s L - x_i in fp64 (same association as the oracle), then
+// One thread per edge: receiver i by binary search on row_ptr, then
+// r = x_j + s L - x_i in fp64 (same association as the oracle, no FMA), and
 // d, u = r/d, cosine cutoff c and c' stored in fp32.
-__global__ void geometry_kernel(int n_atoms, const int* __restrict__ row_ptr, const int* __restrict__ col,
+__global__ void geometry_kernel(int n_atoms, int n_edges, const int* __restrict__ row_ptr, const int* __restrict__ col,
                                 const int* __restrict__ shift, const double* __restrict__ pos,
                                 const int* __restrict__ struct_id, const double* __restrict__ cell, double rc,
                                 int* __restrict__ src, float* __restrict__ d_out, float* __restrict__ u_out,
                                 float* __restrict__ c_out, float* __restrict__ dc_out) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_atoms) return;
-  const double L = cell[struct_id[i]];
-  const double xi0 = pos[3 * i], xi1 = pos[3 * i + 1], xi2 = pos[3 * i + 2];
-  for (int e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
-    const int j = col[e];
-    const double rx = __dsub_rn(__dadd_rn(pos[3 * j + 0], __dmul_rn((double)shift[3 * e + 0], L)), xi0);
-    const double ry = __dsub_rn(__dadd_rn(pos[3 * j + 1], __dmul_rn((double)shift[3 * e + 1], L)), xi1);
-    const double rz = __dsub_rn(__dadd_rn(pos[3 * j + 2], __dmul_rn((double)shift[3 * e + 2], L)), xi2);
-    const double d = sqrt(rx * rx + ry * ry + rz * rz);
-    src[e] = i;
-    d_out[e] = (float)d;
-    u_out[3 * e + 0] = (float)(rx / d);
-    u_out[3 * e + 1] = (float)(ry / d);
-    u_out[3 * e + 2] = (float)(rz / d);
-    const double arg = 3.14159265358979323846 * d / rc;
-    c_out[e] = d < rc ? (float)(0.5 * (cos(arg) + 1.0)) : 0.f;
-    dc_out[e] = d < rc ? (float)(-0.5 * (3.14159265358979323846 / rc) * sin(arg)) : 0.f;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n_edges) return;
+  int lo = 0, hi = n_atoms;  // largest i with row_ptr[i] <= e
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (row_ptr[mid] <= e) lo = mid; else hi = mid;
   }
+  const int i = lo, j = col[e];
+  const double L = cell[struct_id[i]];
+  const double rx = __dsub_rn(__dadd_rn(pos[3 * j + 0], __dmul_rn((double)shift[3 * e + 0], L)), pos[3 * i + 0]);
+  const double ry = __dsub_rn(__dadd_rn(pos[3 * j + 1], __dmul_rn((double)shift[3 * e + 1], L)), pos[3 * i + 1]);
+  const double rz = __dsub_rn(__dadd_rn(pos[3 * j + 2], __dmul_rn((double)shift[3 * e + 2], L)), pos[3 * i + 2]);
+  const double d = sqrt(rx * rx + ry * ry + rz * rz);
+  src[e] = i;
+  d_out[e] = (float)d;
+  u_out[3 * e + 0] = (float)(rx / d);
+  u_out[3 * e + 1] = (float)(ry / d);
+  u_out[3 * e + 2] = (float)(rz / d);
+  const double arg = 3.14159265358979323846 * d / rc;
+  c_out[e] = d < rc ? (float)(0.5 * (cos(arg) + 1.0)) : 0.f;
+  dc_out[e] = d < rc ? (float)(-0.5 * (3.14159265358979323846 / rc) * sin(arg)) : 0.f;
 }
 
 }  // namespace node

@@ -327,8 +327,10 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
       sl.e_atom = dalloc<float>(st, NA, false);
       sl.E = dalloc<float>(st, static_cast<size_t>(d.max_struct), false);
       sl.eps = dalloc<float>(st, static_cast<size_t>(d.max_struct), false);
-      sl.loss = dalloc<float>(st, 2, false);
+      sl.loss = nullptr;  // points into st->losses below
     }
+    st->losses = dalloc<float>(st, 2 * static_cast<size_t>(d.n_slots), false);
+    for (size_t x = 0; x < st->slots.size(); ++x) st->slots[x].loss = st->losses + 2 * x;
     st->lanes.resize(static_cast<size_t>(std::max(1, d.n_lanes)));
     for (Scratch& sc : st->lanes) {
       sc.wh = dalloc<float>(st, NH, false);
@@ -377,7 +379,7 @@ size_t port_elems(const janus_stage* st, int port, int n) {
 }
 
 // ================================================================== LM
-void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_t s) {
+void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_t s, bool sync) {
   if (mb < 0 || mb >= st->desc.n_micro_batches) throw domain_error("micro-batch index out of range");
   if (hb.n_atoms < 1 || hb.n_atoms > st->desc.max_atoms) throw domain_error("n_atoms exceeds stage capacity");
   if (hb.n_edges < 0 || hb.n_edges > st->desc.max_edges) throw domain_error("n_edges exceeds stage capacity");
@@ -402,9 +404,13 @@ void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_
     tiles.push_back(N);
     return tiles;
   };
-  const std::vector<int> tiles = build_tiles(edge::TE);
-  const std::vector<int> tiles_tc = build_tiles(edge_tc::TE);
-  std::vector<int> sptr(static_cast<size_t>(hb.n_struct) + 1, 0);
+  DevGeo& gg = st->geo[static_cast<size_t>(mb)];
+  gg.h_tiles = build_tiles(edge::TE);
+  gg.h_tiles_tc = build_tiles(edge_tc::TE);
+  const std::vector<int>& tiles = gg.h_tiles;
+  const std::vector<int>& tiles_tc = gg.h_tiles_tc;
+  std::vector<int>& sptr = gg.h_sptr;
+  sptr.assign(static_cast<size_t>(hb.n_struct) + 1, 0);
   for (int i = 0; i < N; ++i) {
     const int sid = hb.struct_id[i];
     if (sid < 0 || sid >= hb.n_struct || (i > 0 && sid < hb.struct_id[i - 1])) throw domain_error("struct_id must be non-decreasing in [0, n_struct)");
@@ -433,11 +439,13 @@ void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_
   h2d(g.tile_row, tiles.data(), sizeof(int) * tiles.size());
   h2d(g.tile_row_tc, tiles_tc.data(), sizeof(int) * tiles_tc.size());
   h2d(g.struct_ptr, sptr.data(), sizeof(int) * sptr.size());
-  node::geometry_kernel<<<blocks(N, 128), 128, 0, s>>>(N, g.row_ptr, g.col, g.shift, g.pos, g.struct_id, g.cell,
-                                                       static_cast<double>(st->m.r_c), g.src, g.d, g.u, g.c, g.dc);
+  if (E > 0)
+    node::geometry_kernel<<<blocks(E, 256), 256, 0, s>>>(N, E, g.row_ptr, g.col, g.shift, g.pos, g.struct_id, g.cell,
+                                                         static_cast<double>(st->m.r_c), g.src, g.d, g.u, g.c, g.dc);
   JANUS_LAUNCH_CHECK("geometry");
-  // pageable H2D copies of host vectors: make sure they are consumed before return
-  JANUS_CUDA(cudaStreamSynchronize(s));
+  // host arrays of the caller must stay valid until the stream reaches the
+  // copies (pageable sources are staged by the driver before return)
+  if (sync) JANUS_CUDA(cudaStreamSynchronize(s));
 }
 
 // ================================================================== FE
@@ -532,14 +540,16 @@ void stage_ff(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
       }
       case kMsg: {
         if (u == st->u1 - 1) copy(s, b.ff_a, wm, NH);  // a_m arrived through the ADJ_IN port
-        if (g.n_tiles > 0 && use_tc(st))
+        if (g.n_tiles > 0 && use_tc(st)) {  // a_h += Y W^T fused into the tile epilogue
           edge_tc::msg_ff_tc<<<g.n_tiles_tc, edge_tc::NT, edge_tc::ff_smem(), s>>>(eg, g.tile_row_tc, g.n_tiles_tc, msg_params(st, u),
-                                                                                 st->m.r_c, b.v, b.ff_a, b.ff_Y, sl.F);
-        else if (g.n_tiles > 0)
-          edge::msg_ff_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::ff_smem<kH, kR>(), s>>>(eg, msg_params(st, u), st->m.r_c, b.v, b.ff_a, b.ff_Y, sl.F);
-        else
-          JANUS_CUDA(cudaMemsetAsync(b.ff_Y, 0, sizeof(float) * NH, s));
-        gemm(s, N, b.ff_Y, T + H * H, nullptr, wh, nullptr, wh);  // a_h += Y W^T
+                                                                                 st->m.r_c, b.v, b.ff_a, b.ff_Y, sl.F, T + H * H, wh);
+        } else {
+          if (g.n_tiles > 0)
+            edge::msg_ff_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::ff_smem<kH, kR>(), s>>>(eg, msg_params(st, u), st->m.r_c, b.v, b.ff_a, b.ff_Y, sl.F);
+          else
+            JANUS_CUDA(cudaMemsetAsync(b.ff_Y, 0, sizeof(float) * NH, s));
+          gemm(s, N, b.ff_Y, T + H * H, nullptr, wh, nullptr, wh);  // a_h += Y W^T
+        }
         break;
       }
       case kEmbed:
@@ -595,7 +605,7 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
           const int grid = tc_grid(g);
           edge_tc::msg_bf_tc<<<grid, edge_tc::NT, edge_tc::bf_smem(), s>>>(eg, g.tile_row_tc, g.n_tiles_tc, msg_params(st, u),
                                                                           st->m.r_c, b.v, sc.s1, b.ff_a, Fbar, am, sc.s2,
-                                                                          sc.partial);
+                                                                          sc.partial, T + H * H, b.inj);  // + hbar^F = X W^T
           JANUS_LAUNCH_CHECK("msg_bf_tc");
           edge::reduce_partials_kernel<<<blocks(EC::PE, 256), 256, 0, s>>>(sc.partial, grid, EC::PE, G2);
         } else if (g.n_tiles > 0) {
@@ -607,7 +617,7 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
           JANUS_CUDA(cudaMemsetAsync(am, 0, sizeof(float) * NH, s));
           JANUS_CUDA(cudaMemsetAsync(sc.s2, 0, sizeof(float) * NH, s));
         }
-        gemm(s, N, sc.s2, T + H * H, nullptr, nullptr, nullptr, b.inj);                  // hbar^F = X W^T
+        if (!(g.n_tiles > 0 && use_tc(st))) gemm(s, N, sc.s2, T + H * H, nullptr, nullptr, nullptr, b.inj);  // hbar^F = X W^T
         wjobs(sc, s, N, {wjob(in_h(st, sl, u, N), sc.s2, G2 + EC::PE, ah, b.ff_Y)});  // dW2 = h^T X + abar^T Y
         break;
       }
@@ -696,7 +706,8 @@ void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only, 
         if (g.n_tiles > 0 && use_tc(st)) {
           const int grid = tc_grid(g);
           edge_tc::msg_be_tc<<<grid, edge_tc::NT, edge_tc::be_smem(), s>>>(eg, g.tile_row_tc, g.n_tiles_tc, msg_params(st, u),
-                                                                          st->m.r_c, b.v, bm, sc.s1, sc.partial);
+                                                                          st->m.r_c, b.v, bm, sc.s1, sc.partial, T + H * H,
+                                                                          b.inj, bh);  // + b_h += Yb W^T + hbar^F
           JANUS_LAUNCH_CHECK("msg_be_tc");
           edge::reduce_partials_kernel<<<blocks(EC::PE, 256), 256, 0, s>>>(sc.partial, grid, EC::PE, G1);
         } else if (g.n_tiles > 0) {
@@ -708,7 +719,7 @@ void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only, 
           JANUS_CUDA(cudaMemsetAsync(sc.s1, 0, sizeof(float) * NH, s));
         }
         wjobs(sc, s, N, {wjob(in_h(st, sl, u, N), sc.s1, G1 + EC::PE)});  // dW1 = h^T Yb
-        gemm(s, N, sc.s1, T + H * H, nullptr, bh, b.inj, bh);                 // b_h += Yb W^T + hbar^F
+        if (!(g.n_tiles > 0 && use_tc(st))) gemm(s, N, sc.s1, T + H * H, nullptr, bh, b.inj, bh);  // b_h += Yb W^T + hbar^F
         break;
       }
       case kEmbed:
@@ -810,14 +821,14 @@ void stage_time_edge_kernel(janus_stage* st, int which, int mb, int slot, int it
           edge_tc::msg_fe_tc<<<g.n_tiles_tc, edge_tc::NT, edge_tc::fe_smem(), s>>>(eg, g.tile_row_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, sc.s3);
           break;
         case 1:
-          edge_tc::msg_ff_tc<<<g.n_tiles_tc, edge_tc::NT, edge_tc::ff_smem(), s>>>(eg, g.tile_row_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, b.ff_a, sc.s3, sc.s5);
+          edge_tc::msg_ff_tc<<<g.n_tiles_tc, edge_tc::NT, edge_tc::ff_smem(), s>>>(eg, g.tile_row_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, b.ff_a, sc.s3, sc.s5, nullptr, nullptr);
           break;
         case 2:
           edge_tc::msg_bf_tc<<<grid, edge_tc::NT, edge_tc::bf_smem(), s>>>(eg, g.tile_row_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, sc.s1, b.ff_a,
-                                                                          sl.Fbar, sc.s3, sc.s4, sc.partial);
+                                                                          sl.Fbar, sc.s3, sc.s4, sc.partial, nullptr, nullptr);
           break;
         default:
-          edge_tc::msg_be_tc<<<grid, edge_tc::NT, edge_tc::be_smem(), s>>>(eg, g.tile_row_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, sc.s2, sc.s3, sc.partial);
+          edge_tc::msg_be_tc<<<grid, edge_tc::NT, edge_tc::be_smem(), s>>>(eg, g.tile_row_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, sc.s2, sc.s3, sc.partial, nullptr, nullptr, nullptr);
           break;
       }
       return;

@@ -30,6 +30,7 @@ struct DevGeo {
   int n_tiles_tc = 0;
   int *row_ptr = nullptr, *col = nullptr, *src = nullptr, *rev = nullptr, *tile_row = nullptr, *shift = nullptr;
   int* tile_row_tc = nullptr;  // <= 8 rows, <= 128 edges (tensor-core tiles)
+  std::vector<int> h_tiles, h_tiles_tc, h_sptr;  // host staging kept alive for the async LM copies
   int *species = nullptr, *struct_id = nullptr, *struct_ptr = nullptr;
   double *pos = nullptr, *cell = nullptr;
   float *d = nullptr, *u = nullptr, *c = nullptr, *dc = nullptr, *E_target = nullptr, *F_target = nullptr;
@@ -89,6 +90,7 @@ struct janus_stage {
   std::vector<janus::DevGeo> geo;
   std::vector<janus::Slot> slots;
   std::vector<janus::Scratch> lanes;
+  float* losses = nullptr;  // [n_slots][2] loss_E, loss_F (slot.loss points here)
   std::vector<void*> allocs;
   int64_t static_bytes = 0, arena_bytes = 0;
 

@@ -9,7 +9,7 @@ namespace janus {
 
 janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params);
 void stage_destroy(janus_stage* st);
-void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_t s);
+void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_t s, bool sync = true);
 void stage_fe(janus_stage* st, int mb, int slot, cudaStream_t s, int lane = 0);
 void stage_ff(janus_stage* st, int mb, int slot, cudaStream_t s, int lane = 0);
 void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane = 0);
