@@ -2,8 +2,8 @@
 // (tcgen05.mma kind::tf32, accumulators in TMEM), the JANUS_PREC_TF32 path.
 // Same math as edge_kernels.cuh (SIMT fp32 parity path).
 //
-// Work decomposition (256 threads; thread t owns edge row e = t % 128 of the
-// tile = TMEM lane e, and feature half t / 128):
+// Work decomposition (512 threads; thread t owns edge row e = t % 128 of the
+// tile = TMEM lane e, and feature quarter t / 128, i.e. 16 features):
 //  * an edge tile = <= 8 CSR rows with <= 128 edges (a long row is chunked);
 //  * every per-edge contraction is an M=128 x N=64 x K=64 MMA from shared
 //    memory: A = the tile's edge-major operand, B = a weight tile;
@@ -27,7 +27,10 @@ namespace janus {
 namespace edge_tc {
 
 constexpr int TE = 128;
-constexpr int NT = 256;
+constexpr int NT = 512;            // 16 warps: 4 threads per edge row
+constexpr int NQ = NT / TE;        // feature quarters per edge
+constexpr int FPT = 64 / NQ;       // features per thread (16)
+constexpr int PAIRS = 8 * 64 / NT; // (row, feature) pairs per thread in the segmented sums
 constexpr int H = 64, R = 64;
 constexpr int kRowsPerTile = 8;
 constexpr uint32_t kTile = 128 * 64 * 4;  // 32 KB operand tile
@@ -57,7 +60,7 @@ struct Ctx {
   uint64_t* mbar;
   uint32_t tmem;
   uint32_t phase;
-  int e, half, warp, lane;
+  int e, q, warp, lane;
   __device__ uint32_t lane_base() const { return static_cast<uint32_t>((warp & 3) * 32) << 16; }
   // all threads: make smem writes visible to the tensor core, order TMEM reads, barrier
   __device__ void publish() {
@@ -71,7 +74,7 @@ struct Ctx {
     phase ^= 1u;
     tc::fence_after();
   }
-  __device__ void ld(uint32_t col, float (&v)[32]) const { tc::ld32(tmem + lane_base() + col + 32u * half, v); }
+  __device__ void ld(uint32_t col, float (&v)[FPT]) const { tc::ld16(tmem + lane_base() + col + static_cast<uint32_t>(FPT * q), v); }
 };
 
 // Weight tile for B operands: element (n, k) = src[k*64 + n] (transpose=true)
@@ -123,14 +126,14 @@ __device__ __forceinline__ void load_weights(uint8_t* sm, const float* pack, int
   tc::mbar_wait(wbar, 0);
 }
 
-__device__ __forceinline__ void st_em(uint8_t* t, int e, int f0, const float (&v)[32]) {
+__device__ __forceinline__ void st_em(uint8_t* t, int e, int f0, const float (&v)[FPT]) {
 #pragma unroll
-  for (int j = 0; j < 8; ++j)
+  for (int j = 0; j < FPT / 4; ++j)
     *reinterpret_cast<float4*>(t + off_em(e, f0 + 4 * j)) = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
 }
-__device__ __forceinline__ void st_fm(uint8_t* t, int e, int f0, const float (&v)[32]) {
+__device__ __forceinline__ void st_fm(uint8_t* t, int e, int f0, const float (&v)[FPT]) {
 #pragma unroll
-  for (int j = 0; j < 32; ++j) *reinterpret_cast<float*>(t + off_fm(f0 + j, e)) = v[j];
+  for (int j = 0; j < FPT; ++j) *reinterpret_cast<float*>(t + off_fm(f0 + j, e)) = v[j];
 }
 __device__ __forceinline__ float ld_em(const uint8_t* t, int e, int f) {
   return *reinterpret_cast<const float*>(t + off_em(e, f));
@@ -143,9 +146,9 @@ __device__ __forceinline__ float ld_em(const uint8_t* t, int e, int f) {
 __device__ __forceinline__ uint32_t off_pl(int e, int f) {
   return static_cast<uint32_t>(e * 256 + ((((f >> 2) ^ (e & 15))) << 4) + ((f & 3) << 2));
 }
-__device__ __forceinline__ void st_pl(uint8_t* t, int e, int f0, const float (&v)[32]) {
+__device__ __forceinline__ void st_pl(uint8_t* t, int e, int f0, const float (&v)[FPT]) {
 #pragma unroll
-  for (int j = 0; j < 8; ++j)
+  for (int j = 0; j < FPT / 4; ++j)
     *reinterpret_cast<float4*>(t + off_pl(e, f0 + 4 * j)) = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
 }
 
@@ -154,10 +157,10 @@ __device__ __forceinline__ void st_pl(uint8_t* t, int e, int f0, const float (&v
 // feature = p % 64) and adds the row's chunk edges in CSR order.
 template <int NA>
 __device__ __forceinline__ void seg_rows(const EdgeGeom& g, int r0, int r1, int c0, int ne, const uint8_t* const (&tiles)[NA],
-                                         float (&acc)[NA][2]) {
+                                         float (&acc)[NA][PAIRS]) {
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const int pidx = threadIdx.x + 256 * k;
+  for (int k = 0; k < PAIRS; ++k) {
+    const int pidx = threadIdx.x + NT * k;
     const int r = r0 + (pidx >> 6), f = pidx & 63;
     if (r >= r1) continue;
     const int eb = max(g.row_ptr[r], c0), ee = min(g.row_ptr[r + 1], c0 + ne);
@@ -170,10 +173,10 @@ __device__ __forceinline__ void seg_rows(const EdgeGeom& g, int r0, int r1, int 
 }
 
 template <int NA>
-__device__ __forceinline__ void seg_write(int r0, int r1, float* const (&out)[NA], const float (&acc)[NA][2]) {
+__device__ __forceinline__ void seg_write(int r0, int r1, float* const (&out)[NA], const float (&acc)[NA][PAIRS]) {
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const int pidx = threadIdx.x + 256 * k;
+  for (int k = 0; k < PAIRS; ++k) {
+    const int pidx = threadIdx.x + NT * k;
     const int r = r0 + (pidx >> 6), f = pidx & 63;
     if (r >= r1) continue;
 #pragma unroll
@@ -184,17 +187,17 @@ __device__ __forceinline__ void seg_write(int r0, int r1, float* const (&out)[NA
 // Row epilogue fused into the edge kernels: the tile's finished rows R (from
 // the segmented sums) times W^T:  out[r] = (base ? base[r] : 0) + R[r] W^T
 // (+ add[r]).  Rows staged in smem (rs[8][64]), W^T ([64][64] row-major) via L1.
-__device__ __forceinline__ void rows_times_wt(int r0, int r1, const float (&acc)[2], float* rs, const float* __restrict__ Wt,
+__device__ __forceinline__ void rows_times_wt(int r0, int r1, const float (&acc)[PAIRS], float* rs, const float* __restrict__ Wt,
                                               const float* base, const float* __restrict__ add, float* out) {
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const int pidx = threadIdx.x + 256 * k;
+  for (int k = 0; k < PAIRS; ++k) {
+    const int pidx = threadIdx.x + NT * k;
     rs[(pidx >> 6) * 64 + (pidx & 63)] = (r0 + (pidx >> 6) < r1) ? acc[k] : 0.f;
   }
   __syncthreads();
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const int pidx = threadIdx.x + 256 * k;
+  for (int k = 0; k < PAIRS; ++k) {
+    const int pidx = threadIdx.x + NT * k;
     const int rl = pidx >> 6, c = pidx & 63, r = r0 + rl;
     if (r >= r1) continue;
     float o0 = 0.f, o1 = 0.f;
@@ -212,13 +215,13 @@ __device__ __forceinline__ void rows_times_wt(int r0, int r1, const float (&acc)
 }
 
 // 32 consecutive features of row `row` of an [N][64] array (8 float4 loads in flight)
-__device__ __forceinline__ void gather32(const float* __restrict__ x, int row, int f0, float (&v)[32]) {
+__device__ __forceinline__ void gather32(const float* __restrict__ x, int row, int f0, float (&v)[FPT]) {
   const float4* p = reinterpret_cast<const float4*>(x + (size_t)row * H + f0);
-  float4 t[8];
+  float4 t[FPT / 4];
 #pragma unroll
-  for (int q = 0; q < 8; ++q) t[q] = __ldg(p + q);
+  for (int q = 0; q < FPT / 4; ++q) t[q] = __ldg(p + q);
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
+  for (int q = 0; q < FPT / 4; ++q) {
     v[4 * q] = t[q].x;
     v[4 * q + 1] = t[q].y;
     v[4 * q + 2] = t[q].z;
@@ -227,11 +230,11 @@ __device__ __forceinline__ void gather32(const float* __restrict__ x, int row, i
 }
 
 // radial basis (and derivative) of this thread's edge for its 32 features
-__device__ __forceinline__ void basis(float d, float rc, int f0, float (&p)[32], float (&dp)[32]) {
+__device__ __forceinline__ void basis(float d, float rc, int f0, float (&p)[FPT], float (&dp)[FPT]) {
   const float delta = rc / (R - 1);
   const float gamma = 1.0f / (2.0f * delta * delta);
 #pragma unroll
-  for (int j = 0; j < 32; ++j) {
+  for (int j = 0; j < FPT; ++j) {
     const float x = d - (f0 + j) * delta;
     p[j] = expf(-gamma * x * x);
     dp[j] = -2.0f * gamma * x * p[j];
@@ -252,7 +255,7 @@ __device__ __forceinline__ TileRange tile_range(const EdgeGeom& g, const int* ti
 
 __device__ __forceinline__ void setup(Ctx& c, uint32_t* tmem_slot, uint32_t ncols) {
   c.e = threadIdx.x & 127;
-  c.half = threadIdx.x >> 7;
+  c.q = threadIdx.x >> 7;
   c.warp = threadIdx.x >> 5;
   c.lane = threadIdx.x & 31;
   c.phase = 0;
@@ -318,15 +321,15 @@ __global__ void __launch_bounds__(NT) msg_fe_tc(EdgeGeom g, const int* __restric
   const uint32_t aW0 = tc::smem_u32(W0), aW1 = tc::smem_u32(W1), aT0 = tc::smem_u32(T0);
   for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
     const TileRange tr = tile_range(g, tiles, t);
-    float acc[1][2] = {{0.f, 0.f}};
+    float acc[1][PAIRS] = {};
     for (int c0 = tr.e0; c0 < tr.e1; c0 += TE) {
       const int ne = min(TE, tr.e1 - c0);
       load_scalars(g, sc, c0, ne, nullptr);
       __syncthreads();
       {
-        float ph[32], dph[32];
-        basis(sc.d[c.e], rc, 32 * c.half, ph, dph);
-        st_em(T0, c.e, 32 * c.half, ph);
+        float ph[FPT], dph[FPT];
+        basis(sc.d[c.e], rc, FPT * c.q, ph, dph);
+        st_em(T0, c.e, FPT * c.q, ph);
       }
       c.publish();
       if (threadIdx.x == 0) {
@@ -335,11 +338,11 @@ __global__ void __launch_bounds__(NT) msg_fe_tc(EdgeGeom g, const int* __restric
       }
       c.wait_mma();
       {
-        float z[32];
+        float z[FPT];
         c.ld(TM_Z, z);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) z[j] = dev::silu(z[j] + al[32 * c.half + j]);
-        st_em(T0, c.e, 32 * c.half, z);
+        for (int j = 0; j < FPT; ++j) z[j] = dev::silu(z[j] + al[FPT * c.q + j]);
+        st_em(T0, c.e, FPT * c.q, z);
       }
       c.publish();
       if (threadIdx.x == 0) {
@@ -348,13 +351,13 @@ __global__ void __launch_bounds__(NT) msg_fe_tc(EdgeGeom g, const int* __restric
       }
       c.wait_mma();
       {
-        float gg[32], vj[32];
-        gather32(v, sc.col[c.e], 32 * c.half, vj);
+        float gg[FPT], vj[FPT];
+        gather32(v, sc.col[c.e], FPT * c.q, vj);
         c.ld(TM_G, gg);
         const float ce = sc.c[c.e];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) gg[j] = ce * (gg[j] + be[32 * c.half + j]) * vj[j];  // w_e * v_j
-        st_pl(T1, c.e, 32 * c.half, gg);
+        for (int j = 0; j < FPT; ++j) gg[j] = ce * (gg[j] + be[FPT * c.q + j]) * vj[j];  // w_e * v_j
+        st_pl(T1, c.e, FPT * c.q, gg);
       }
       tc::fence_before();
       __syncthreads();
@@ -387,7 +390,7 @@ __global__ void __launch_bounds__(NT) msg_ff_tc(EdgeGeom g, const int* __restric
   float* be = al + 64;
   Scal sc{be + 64, be + 64 + TE, be + 64 + 2 * TE, nullptr, reinterpret_cast<int*>(be + 64 + 3 * TE),
           reinterpret_cast<int*>(be + 64 + 4 * TE)};
-  float* sq = be + 64 + 5 * TE;  // [2][TE] per-half force scalars
+  float* sq = be + 64 + 5 * TE;  // [NQ][TE] per-quarter force scalars
   __shared__ __align__(8) uint64_t mbar;
   __shared__ uint32_t tslot;
   Ctx c;
@@ -397,17 +400,17 @@ __global__ void __launch_bounds__(NT) msg_ff_tc(EdgeGeom g, const int* __restric
   load_weights(sm, p.pack, 2, al, be, &wbar);
   setup(c, &tslot, 256);
   const uint32_t aW0 = tc::smem_u32(W0), aW1 = tc::smem_u32(W1), aT0 = tc::smem_u32(T0), aT1 = tc::smem_u32(T1);
-  const int f0 = 32 * c.half;
+  const int f0 = FPT * c.q;
   for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
     const TileRange tr = tile_range(g, tiles, t);
-    float acc[1][2] = {{0.f, 0.f}};
+    float acc[1][PAIRS] = {};
     float fsum = 0.f;  // threads < 24: (row t/3, component t%3)
     for (int c0 = tr.e0; c0 < tr.e1; c0 += TE) {
       const int ne = min(TE, tr.e1 - c0);
       load_scalars(g, sc, c0, ne, nullptr);
       __syncthreads();
       {
-        float ph[32], dph[32];
+        float ph[FPT], dph[FPT];
         basis(sc.d[c.e], rc, f0, ph, dph);
         st_em(T0, c.e, f0, ph);
         st_em(T1, c.e, f0, dph);
@@ -420,11 +423,11 @@ __global__ void __launch_bounds__(NT) msg_ff_tc(EdgeGeom g, const int* __restric
       }
       c.wait_mma();
       {
-        float z[32], zp[32];
+        float z[FPT], zp[FPT];
         c.ld(TM_Z, z);
         c.ld(TM_ZP, zp);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
+        for (int j = 0; j < FPT; ++j) {
           const float zz = z[j] + al[f0 + j];
           z[j] = dev::silu(zz);
           zp[j] = dev::dsilu(zz) * zp[j];
@@ -442,19 +445,19 @@ __global__ void __launch_bounds__(NT) msg_ff_tc(EdgeGeom g, const int* __restric
       {
         const int i = sc.src[c.e], j = sc.col[c.e];
         const float ce = sc.c[c.e], dce = sc.dc[c.e];
-        float gg[32], gp[32];
+        float gg[FPT], gp[FPT];
         c.ld(TM_G, gg);
         c.ld(TM_GP, gp);
         float pq = 0.f;
-        float amj[32];
+        float amj[FPT];
         gather32(am, j, f0, amj);
         {
-          float vj[32], ami[32], vi[32];
+          float vj[FPT], ami[FPT], vi[FPT];
           gather32(v, j, f0, vj);
           gather32(am, i, f0, ami);
           gather32(v, i, f0, vi);
 #pragma unroll
-          for (int q = 0; q < 32; ++q) {
+          for (int q = 0; q < FPT; ++q) {
             const float gb = gg[q] + be[f0 + q];
             const float wp = dce * gb + ce * gp[q];
             pq = fmaf(fmaf(ami[q], vj[q], amj[q] * vi[q]), wp, pq);
@@ -462,7 +465,7 @@ __global__ void __launch_bounds__(NT) msg_ff_tc(EdgeGeom g, const int* __restric
           }
         }
         st_pl(T0, c.e, f0, gg);
-        sq[c.half * TE + c.e] = pq;
+        sq[c.q * TE + c.e] = pq;
       }
       tc::fence_before();
       __syncthreads();
@@ -473,7 +476,8 @@ __global__ void __launch_bounds__(NT) msg_ff_tc(EdgeGeom g, const int* __restric
           const int r = tr.r0 + threadIdx.x / 3, comp = threadIdx.x % 3;
           if (r < tr.r1) {
             const int eb = max(g.row_ptr[r], c0), ee = min(g.row_ptr[r + 1], c0 + ne);
-            for (int x = eb; x < ee; ++x) fsum = fmaf(sq[x - c0] + sq[TE + x - c0], g.u[3 * x + comp], fsum);
+            for (int x = eb; x < ee; ++x)
+              fsum = fmaf((sq[x - c0] + sq[TE + x - c0]) + (sq[2 * TE + x - c0] + sq[3 * TE + x - c0]), g.u[3 * x + comp], fsum);
           }
         }
       }
@@ -493,30 +497,30 @@ __global__ void __launch_bounds__(NT) msg_ff_tc(EdgeGeom g, const int* __restric
 // Write the CTA's weight-gradient partial [dA | dalpha | dB | dbeta] from the
 // M=64 TMEM accumulators (row r at lane (r/16)*32 + r%16) and the per-thread
 // column sums (reduced over the 128 edge threads in order through smem).
-__device__ __forceinline__ void write_partial(Ctx& c, float* part, uint8_t* scratch, const float (&cs_a)[32],
-                                              const float (&cs_b)[32]) {
+__device__ __forceinline__ void write_partial(Ctx& c, float* part, uint8_t* scratch, const float (&cs_a)[FPT],
+                                              const float (&cs_b)[FPT]) {
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   {
     const int q = c.warp & 3;
-    float va[32], vb[32];
+    float va[FPT], vb[FPT];
     c.ld(TM_AG, va);
     c.ld(TM_BG, vb);
     if (c.lane < 16) {
       const int r = 16 * q + c.lane;
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        part[r * H + 32 * c.half + j] = va[j];              // dA[r][h]
-        part[R * H + H + r * H + 32 * c.half + j] = vb[j];  // dB[k][h]
+      for (int j = 0; j < FPT; ++j) {
+        part[r * H + FPT * c.q + j] = va[j];              // dA[r][h]
+        part[R * H + H + r * H + FPT * c.q + j] = vb[j];  // dB[k][h]
       }
     }
   }
   float* red = reinterpret_cast<float*>(scratch);  // [128][64]
   for (int pass = 0; pass < 2; ++pass) {
-    const float(&cs)[32] = pass ? cs_b : cs_a;
+    const float(&cs)[FPT] = pass ? cs_b : cs_a;
 #pragma unroll
-    for (int j = 0; j < 32; ++j) red[c.e * 64 + 32 * c.half + j] = cs[j];
+    for (int j = 0; j < FPT; ++j) red[c.e * 64 + FPT * c.q + j] = cs[j];
     __syncthreads();
     if (threadIdx.x < 64) {
       float s = 0.f;
@@ -557,20 +561,20 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int* __rest
   setup(c, &tslot, 512);
   const uint32_t aW0 = tc::smem_u32(W0), aW1 = tc::smem_u32(W1), aW2 = tc::smem_u32(W2);
   const uint32_t aT0 = tc::smem_u32(T0), aT1 = tc::smem_u32(T1), aT2 = tc::smem_u32(T2), aT3 = tc::smem_u32(T3);
-  float cs_a[32], cs_b[32];
+  float cs_a[FPT], cs_b[FPT];
 #pragma unroll
-  for (int j = 0; j < 32; ++j) cs_a[j] = cs_b[j] = 0.f;
+  for (int j = 0; j < FPT; ++j) cs_a[j] = cs_b[j] = 0.f;
   bool first = true;
-  const int f0 = 32 * c.half;
+  const int f0 = FPT * c.q;
   for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
     const TileRange tr = tile_range(g, tiles, t);
-    float acc[1][2] = {{0.f, 0.f}};
+    float acc[1][PAIRS] = {};
     for (int c0 = tr.e0; c0 < tr.e1; c0 += TE) {
       const int ne = min(TE, tr.e1 - c0);
       load_scalars(g, sc, c0, ne, nullptr);
       __syncthreads();
       {
-        float ph[32], dph[32];
+        float ph[FPT], dph[FPT];
         basis(sc.d[c.e], rc, f0, ph, dph);
         st_em(T0, c.e, f0, ph);
       }
@@ -581,10 +585,10 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int* __rest
       }
       c.wait_mma();
       {
-        float z[32];
+        float z[FPT];
         c.ld(TM_Z, z);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) z[j] = dev::silu(z[j] + al[f0 + j]);
+        for (int j = 0; j < FPT; ++j) z[j] = dev::silu(z[j] + al[f0 + j]);
         st_em(T0, c.e, f0, z);  // s, edge-major (A of g = s B)
         st_fm(T1, c.e, f0, z);  // s^T (A of dB = s^T gbar)
       }
@@ -594,21 +598,21 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int* __rest
         tc::commit(c.mbar);
       }
       c.wait_mma();
-      float gb[32];
+      float gb[FPT];
       {
         const int i = sc.src[c.e], j = sc.col[c.e];
         const float ce = sc.c[c.e];
-        float gg[32], bj[32];
+        float gg[FPT], bj[FPT];
         c.ld(TM_G, gg);
         gather32(bm, j, f0, bj);
 #pragma unroll
-        for (int q = 0; q < 32; ++q) gg[q] = ce * (gg[q] + be[f0 + q]) * bj[q];  // w_e * bm_j
+        for (int q = 0; q < FPT; ++q) gg[q] = ce * (gg[q] + be[f0 + q]) * bj[q];  // w_e * bm_j
         st_pl(T0, c.e, f0, gg);
-        float bi[32], vj[32];
+        float bi[FPT], vj[FPT];
         gather32(bm, i, f0, bi);
         gather32(v, j, f0, vj);
 #pragma unroll
-        for (int q = 0; q < 32; ++q) {
+        for (int q = 0; q < FPT; ++q) {
           gb[q] = ce * bi[q] * vj[q];  // gbar (zero on padding edges: c = 0)
           cs_b[q] += gb[q];
         }
@@ -628,16 +632,16 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int* __rest
       c.wait_mma();
       __syncthreads();  // T0 reads done before it is rewritten
       {
-        float z[32], sb[32];
+        float z[FPT], sb[FPT];
         c.ld(TM_Z, z);
         c.ld(TM_G, sb);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
+        for (int j = 0; j < FPT; ++j) {
           z[j] = sb[j] * dev::dsilu(z[j] + al[f0 + j]);
           cs_a[j] += z[j];
         }
         st_fm(T2, c.e, f0, z);  // zbar^T
-        float ph[32], dph[32];
+        float ph[FPT], dph[FPT];
         basis(sc.d[c.e], rc, f0, ph, dph);
         st_fm(T0, c.e, f0, ph);  // phi^T
       }
@@ -696,20 +700,20 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
   setup(c, &tslot, 512);
   const uint32_t aW0 = tc::smem_u32(W0), aW1 = tc::smem_u32(W1), aW2 = tc::smem_u32(W2);
   const uint32_t aT0 = tc::smem_u32(T0), aT1 = tc::smem_u32(T1), aT2 = tc::smem_u32(T2), aT3 = tc::smem_u32(T3);
-  float cs_a[32], cs_b[32];
+  float cs_a[FPT], cs_b[FPT];
 #pragma unroll
-  for (int j = 0; j < 32; ++j) cs_a[j] = cs_b[j] = 0.f;
+  for (int j = 0; j < FPT; ++j) cs_a[j] = cs_b[j] = 0.f;
   bool first = true;
-  const int f0 = 32 * c.half;
+  const int f0 = FPT * c.q;
   for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
     const TileRange tr = tile_range(g, tiles, t);
-    float acc[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+    float acc[2][PAIRS] = {};
     for (int c0 = tr.e0; c0 < tr.e1; c0 += TE) {
       const int ne = min(TE, tr.e1 - c0);
       load_scalars(g, sc, c0, ne, Fbar);
       __syncthreads();
       {
-        float ph[32], dph[32];
+        float ph[FPT], dph[FPT];
         basis(sc.d[c.e], rc, f0, ph, dph);
         st_em(T0, c.e, f0, ph);
         st_em(T1, c.e, f0, dph);
@@ -722,11 +726,11 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
       }
       c.wait_mma();
       {
-        float z[32], zp[32];
+        float z[FPT], zp[FPT];
         c.ld(TM_Z, z);
         c.ld(TM_ZP, zp);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
+        for (int j = 0; j < FPT; ++j) {
           const float zz = z[j] + al[f0 + j];
           z[j] = dev::silu(zz);
           zp[j] = dev::dsilu(zz) * zp[j];
@@ -743,16 +747,16 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
         tc::commit(c.mbar);
       }
       c.wait_mma();
-      float mu[32], nu[32];
+      float mu[FPT], nu[FPT];
       {
         const int i = sc.src[c.e], j = sc.col[c.e];
         const float qb = sc.qb[c.e], ce = sc.c[c.e], dce = sc.dc[c.e];
-        float gg[32], gp[32];
+        float gg[FPT], gp[FPT];
         c.ld(TM_G, gg);
         c.ld(TM_GP, gp);
-        float pm[32], px[32];
+        float pm[FPT], px[FPT];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int q = 0; q < FPT / 4; ++q) {
           const float4 a4 = __ldg(reinterpret_cast<const float4*>(am + (size_t)i * H + f0) + q);
           const float4 aj4 = __ldg(reinterpret_cast<const float4*>(am + (size_t)j * H + f0) + q);
           const float4 v4 = __ldg(reinterpret_cast<const float4*>(v + (size_t)j * H + f0) + q);
@@ -774,7 +778,7 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
         st_pl(T0, c.e, f0, pm);
         st_pl(T1, c.e, f0, px);
 #pragma unroll
-        for (int q = 0; q < 32; ++q) cs_b[q] += mu[q];
+        for (int q = 0; q < FPT; ++q) cs_b[q] += mu[q];
       }
       tc::fence_before();
       __syncthreads();
@@ -802,13 +806,13 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
       }
       c.wait_mma();
       {
-        float z[32], zp[32], sb[32], sdb[32];
+        float z[FPT], zp[FPT], sb[FPT], sdb[FPT];
         c.ld(TM_Z, z);
         c.ld(TM_ZP, zp);
         c.ld(TM_G, sb);
         c.ld(TM_GP, sdb);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
+        for (int j = 0; j < FPT; ++j) {
           const float zz = z[j] + al[f0 + j];
           const float ds = dev::dsilu(zz);
           z[j] = sb[j] * ds + sdb[j] * dev::d2silu(zz) * zp[j];  // zbar
@@ -817,7 +821,7 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
         }
         st_fm(T2, c.e, f0, z);
         st_fm(T3, c.e, f0, zp);
-        float ph[32], dph[32];
+        float ph[FPT], dph[FPT];
         basis(sc.d[c.e], rc, f0, ph, dph);
         st_fm(T0, c.e, f0, ph);   // phi^T
         st_fm(T1, c.e, f0, dph);  // phi'^T
@@ -846,7 +850,7 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
   teardown(c, 512);
 }
 
-constexpr size_t kSmallBytes = sizeof(float) * (128 + 8 * TE);
+constexpr size_t kSmallBytes = sizeof(float) * (128 + 10 * TE);
 constexpr size_t fe_smem() { return 2 * kWTile + 2 * kTile + kSmallBytes; }
 constexpr size_t ff_smem() { return 2 * kWTile + 2 * kTile + kSmallBytes; }
 constexpr size_t be_smem() { return 3 * kWTile + 4 * kTile + kSmallBytes; }
