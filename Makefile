@@ -9,6 +9,11 @@ OBJ := build/obj
 LIB := $(PKG)/libjanus_b200.so
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := -Iinclude -std=c++20 -O3 $(ARCH) -lineinfo -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
+ifeq ($(TRACE),1)  # phase-traced profiling build (edge_tc.cuh TC_MARK), loaded via JANUS_LIB
+OBJ := build/trace_obj
+LIB := build/trace/libjanus_b200.so
+NVFLAGS += -DJANUS_TC_TRACE
+endif
 CXXFLAGS := -Iinclude -std=c++20 -O2 -fPIC -ffp-contract=off -Wall -Wextra -I/usr/local/cuda/include
 CU_SRCS := $(wildcard $(SRC)/*.cu)
 CPP_SRCS := $(wildcard $(SRC)/*.cpp)
@@ -30,6 +35,7 @@ $(OBJ)/%.cpp.o: $(SRC)/%.cpp $(HDRS) | $(OBJ)
 	$(CXX) $(CXXFLAGS) -c $< -o $@
 
 $(LIB): $(OBJS)
+	mkdir -p $(dir $@)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -L/usr/lib/x86_64-linux-gnu -lnccl -lcudart
 
 oracle:

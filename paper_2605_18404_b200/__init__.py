@@ -17,7 +17,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libjanus_b200.so")
+LIB_PATH = os.environ.get("JANUS_LIB") or os.path.join(_HERE, "libjanus_b200.so")  # JANUS_LIB: profiling builds only
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} not built — run `make` (or __graft_entry__.build()) first; "

@@ -30,12 +30,34 @@ constexpr int TE = 128;
 constexpr int NT = 512;            // 16 warps: 4 threads per edge row
 constexpr int NQ = NT / TE;        // feature quarters per edge
 constexpr int FPT = 64 / NQ;       // features per thread (16)
-constexpr int PAIRS = 8 * 64 / NT; // (row, feature) pairs per thread in the segmented sums
 constexpr int H = 64, R = 64;
 constexpr int kRowsPerTile = 8;
 constexpr uint32_t kTile = 128 * 64 * 4;  // 32 KB operand tile
 constexpr uint32_t kWTile = 64 * 64 * 4;  // 16 KB weight tile
 constexpr int PE = R * H + H + H * H + H;
+
+// Phase tracing (profiling builds only: make TRACE=1): thread 0 of CTAs 0 and
+// gridDim/2 prints clock64 deltas between the marks of one kernel.
+#ifdef JANUS_TC_TRACE
+#define TC_DECL long long trc[24] = {}; int ntr = 0
+#define TC_M()                                                   \
+  do {                                                           \
+    if (threadIdx.x == 0 && ntr < 24) trc[ntr] = clock64();      \
+    ++ntr;                                                       \
+  } while (0)
+#define TC_DUMP(name)                                                                                          \
+  if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x / 2)) {                                   \
+    long long d[20] = {};                                                                                      \
+    for (int k = 1; k < ntr && k < 21; ++k) d[k - 1] = trc[k] - trc[k - 1];                                    \
+    printf("TRACE %s cta %d marks %d total %lld: %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld\n", \
+           name, blockIdx.x, ntr, trc[min(ntr, 24) - 1] - trc[0], d[0], d[1], d[2], d[3], d[4], d[5], d[6], d[7], d[8], \
+           d[9], d[10], d[11], d[12], d[13], d[14], d[15], d[16], d[17], d[18], d[19]);                        \
+  }
+#else
+#define TC_DECL
+#define TC_M()
+#define TC_DUMP(name)
+#endif
 // TMEM columns
 constexpr uint32_t TM_Z = 0, TM_ZP = 64, TM_G = 128, TM_GP = 192, TM_AG = 256, TM_BG = 320;
 
@@ -53,6 +75,13 @@ __device__ __forceinline__ void mma_tiles(uint32_t d, uint32_t a, int a_rows, ui
     const uint64_t db = tc::smem_desc(b + (s >> 2) * bs + 32u * (s & 3), 16, 1024, 2);
     tc::mma_tf32(d, da, db, id, (s > 0 || accumulate) ? 1u : 0u);
   }
+}
+
+// SWIZZLE_128B tiles need a 1024 B-aligned base; a second co-resident CTA's
+// dynamic window is not guaranteed to start on one (smem sizes carry +1 KB).
+__device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
+  const uint32_t a = tc::smem_u32(p);
+  return p + ((1024u - (a & 1023u)) & 1023u);
 }
 
 struct Ctx {
@@ -152,54 +181,67 @@ __device__ __forceinline__ void st_pl(uint8_t* t, int e, int f0, const float (&v
     *reinterpret_cast<float4*>(t + off_pl(e, f0 + 4 * j)) = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
 }
 
-// Deterministic segmented row sums of NA plain tiles over this chunk: thread t
-// owns (row, feature) pairs p = t and t + 256 (row = p / 64 within the tile,
-// feature = p % 64) and adds the row's chunk edges in CSR order.
-template <int NA>
-__device__ __forceinline__ void seg_rows(const EdgeGeom& g, int r0, int r1, int c0, int ne, const uint8_t* const (&tiles)[NA],
-                                         float (&acc)[NA][PAIRS]) {
-#pragma unroll
-  for (int k = 0; k < PAIRS; ++k) {
-    const int pidx = threadIdx.x + NT * k;
-    const int r = r0 + (pidx >> 6), f = pidx & 63;
-    if (r >= r1) continue;
-    const int eb = max(g.row_ptr[r], c0), ee = min(g.row_ptr[r + 1], c0 + ne);
-    for (int x = eb; x < ee; ++x) {
-      const uint32_t o = off_pl(x - c0, f);
-#pragma unroll
-      for (int a = 0; a < NA; ++a) acc[a][k] += *reinterpret_cast<const float*>(tiles[a] + o);
-    }
-  }
+// Deterministic segmented row sums of NA plain tiles over one chunk.  The
+// tile's nr rows x 64 features are spread over the CTA with `split` threads
+// per (row, feature) pair (split = 8 / nr rounded down to a power of two):
+// consecutive lanes share a pair and take interleaved edges of the row, so
+// each partial is a short dependent chain; the partials stay per-thread across
+// the tile's chunks and are combined once by an xor butterfly (seg_finish),
+// which leaves the bit-identical total in every lane of the group.
+struct SegMap {
+  int split, span, pair, part;
+  bool active;
+};
+__device__ __forceinline__ SegMap seg_map(int nr) {
+  SegMap m;
+  m.split = nr <= 1 ? 8 : nr <= 2 ? 4 : nr <= 4 ? 2 : 1;
+  m.span = nr * 64;
+  m.part = static_cast<int>(threadIdx.x) & (m.split - 1);
+  m.pair = static_cast<int>(threadIdx.x) / m.split;
+  m.active = m.pair < m.span;
+  return m;
 }
 
 template <int NA>
-__device__ __forceinline__ void seg_write(int r0, int r1, float* const (&out)[NA], const float (&acc)[NA][PAIRS]) {
+__device__ __forceinline__ void seg_rows(const EdgeGeom& g, int r0, int c0, int ne, const uint8_t* const (&tiles)[NA],
+                                         const SegMap& m, float (&acc)[NA]) {
+  if (!m.active) return;
+  const int r = r0 + (m.pair >> 6), f = m.pair & 63;
+  const int eb = max(g.row_ptr[r], c0), ee = min(g.row_ptr[r + 1], c0 + ne);
+  for (int x = eb + m.part; x < ee; x += m.split) {
+    const uint32_t o = off_pl(x - c0, f);
 #pragma unroll
-  for (int k = 0; k < PAIRS; ++k) {
-    const int pidx = threadIdx.x + NT * k;
-    const int r = r0 + (pidx >> 6), f = pidx & 63;
-    if (r >= r1) continue;
-#pragma unroll
-    for (int a = 0; a < NA; ++a) out[a][(size_t)r * H + f] = acc[a][k];
+    for (int a = 0; a < NA; ++a) acc[a] += *reinterpret_cast<const float*>(tiles[a] + o);
   }
+}
+
+// all threads (warp-uniform split): combine the interleaved partials
+template <int NA>
+__device__ __forceinline__ void seg_finish(const SegMap& m, float (&acc)[NA]) {
+  for (int o = 1; o < m.split; o <<= 1)
+#pragma unroll
+    for (int a = 0; a < NA; ++a) acc[a] += __shfl_xor_sync(0xffffffffu, acc[a], o);
+}
+
+template <int NA>
+__device__ __forceinline__ void seg_write(int r0, const SegMap& m, float* const (&out)[NA], const float (&acc)[NA]) {
+  if (!m.active || m.part != 0) return;
+  const int r = r0 + (m.pair >> 6), f = m.pair & 63;
+#pragma unroll
+  for (int a = 0; a < NA; ++a) out[a][(size_t)r * H + f] = acc[a];
 }
 
 // Row epilogue fused into the edge kernels: the tile's finished rows R (from
 // the segmented sums) times W^T:  out[r] = (base ? base[r] : 0) + R[r] W^T
 // (+ add[r]).  Rows staged in smem (rs[8][64]), W^T ([64][64] row-major) via L1.
-__device__ __forceinline__ void rows_times_wt(int r0, int r1, const float (&acc)[PAIRS], float* rs, const float* __restrict__ Wt,
-                                              const float* base, const float* __restrict__ add, float* out) {
-#pragma unroll
-  for (int k = 0; k < PAIRS; ++k) {
-    const int pidx = threadIdx.x + NT * k;
-    rs[(pidx >> 6) * 64 + (pidx & 63)] = (r0 + (pidx >> 6) < r1) ? acc[k] : 0.f;
-  }
+__device__ __forceinline__ void rows_times_wt(int r0, int r1, const SegMap& m, float accv, float* rs,
+                                              const float* __restrict__ Wt, const float* base, const float* __restrict__ add,
+                                              float* out) {
+  if (m.active && m.part == 0) rs[m.pair] = accv;
   __syncthreads();
-#pragma unroll
-  for (int k = 0; k < PAIRS; ++k) {
-    const int pidx = threadIdx.x + NT * k;
-    const int rl = pidx >> 6, c = pidx & 63, r = r0 + rl;
-    if (r >= r1) continue;
+  const int pidx = threadIdx.x;
+  const int rl = pidx >> 6, c = pidx & 63, r = r0 + rl;
+  if (r < r1) {
     float o0 = 0.f, o1 = 0.f;
 #pragma unroll 8
     for (int q = 0; q < 64; q += 2) {
@@ -236,7 +278,7 @@ __device__ __forceinline__ void basis(float d, float rc, int f0, float (&p)[FPT]
 #pragma unroll
   for (int j = 0; j < FPT; ++j) {
     const float x = d - (f0 + j) * delta;
-    p[j] = expf(-gamma * x * x);
+    p[j] = __expf(-gamma * x * x);
     dp[j] = -2.0f * gamma * x * p[j];
   }
 }
@@ -271,45 +313,48 @@ __device__ __forceinline__ void teardown(Ctx& c, uint32_t ncols) {
   if (c.warp == 0) tc::tmem_free(c.tmem, ncols);
 }
 
-// per-chunk edge scalars into smem (threads 0..127)
-struct Scal {
-  float *d, *c, *dc, *qb;
-  int *src, *col;
+// This thread's edge scalars (the 4 threads of an edge read the same values
+// through L1; padding edges get c = dc = 0, which zeroes all their terms).
+struct ES {
+  float d, c, dc;
+  int i, j, x;
+  bool ok;
 };
-__device__ __forceinline__ void load_scalars(const EdgeGeom& g, Scal& s, int c0, int ne, const float* Fbar) {
-  const int t = threadIdx.x;
-  if (t < TE) {
-    const bool ok = t < ne;
-    const int x = c0 + t;
-    s.d[t] = ok ? g.d[x] : 0.f;
-    s.c[t] = ok ? g.c[x] : 0.f;
-    if (s.dc) s.dc[t] = ok ? g.dc[x] : 0.f;
-    const int i = ok ? g.src[x] : 0, j = ok ? g.col[x] : 0;
-    s.src[t] = i;
-    s.col[t] = j;
-    if (s.qb) {
-      float q = 0.f;
-      if (ok)
-#pragma unroll
-        for (int k = 0; k < 3; ++k) q = fmaf(Fbar[3 * i + k] - Fbar[3 * j + k], g.u[3 * x + k], q);
-      s.qb[t] = q;
-    }
-  }
+__device__ __forceinline__ ES edge_sc(const EdgeGeom& g, int c0, int ne, int e) {
+  ES s;
+  s.ok = e < ne;
+  s.x = c0 + (s.ok ? e : 0);
+  s.d = s.ok ? __ldg(g.d + s.x) : 0.f;
+  s.c = s.ok ? __ldg(g.c + s.x) : 0.f;
+  s.dc = s.ok ? __ldg(g.dc + s.x) : 0.f;
+  s.i = s.ok ? __ldg(g.src + s.x) : 0;
+  s.j = s.ok ? __ldg(g.col + s.x) : 0;
+  return s;
 }
+// qbar_e = < Fbar_i - Fbar_j, u_e >
+__device__ __forceinline__ float edge_qbar(const EdgeGeom& g, const ES& s, const float* __restrict__ Fbar) {
+  float q = 0.f;
+  if (s.ok)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) q = fmaf(__ldg(Fbar + 3 * s.i + k) - __ldg(Fbar + 3 * s.j + k), __ldg(g.u + 3 * s.x + k), q);
+  return q;
+}
+
+// fast sigmoid for the tf32 path; SiLU and its derivatives derive from one s
+__device__ __forceinline__ float fsig(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
 
 // ----------------------------------------------------------------------- FE
 // m_i = sum_{e in row i} w_e * v[col e], w = c (SiLU(phi A + alpha) B + beta)
 __global__ void __launch_bounds__(NT) msg_fe_tc(EdgeGeom g, const int* __restrict__ tiles, int n_tiles, MsgParams p,
                                                float rc, const float* __restrict__ v, float* __restrict__ m_out) {
-  extern __shared__ __align__(1024) uint8_t sm[];
+  extern __shared__ __align__(1024) uint8_t sm_raw[];
+  uint8_t* sm = align1024(sm_raw);
   uint8_t* W0 = sm;               // A^T  (n = h, k = r)
   uint8_t* W1 = W0 + kWTile;      // B^T  (n = out, k = in)
   uint8_t* T0 = W1 + kWTile;      // phi -> s
   uint8_t* T1 = T0 + kTile;       // w (edge-major)
-  float* fsm = reinterpret_cast<float*>(T1 + kTile);
-  float* al = fsm;
+  float* al = reinterpret_cast<float*>(T1 + kTile);
   float* be = al + 64;
-  Scal sc{be + 64, be + 64 + TE, nullptr, nullptr, reinterpret_cast<int*>(be + 64 + 2 * TE), reinterpret_cast<int*>(be + 64 + 3 * TE)};
   __shared__ __align__(8) uint64_t mbar;
   __shared__ uint32_t tslot;
   Ctx c;
@@ -319,17 +364,18 @@ __global__ void __launch_bounds__(NT) msg_fe_tc(EdgeGeom g, const int* __restric
   load_weights(sm, p.pack, 2, al, be, &wbar);
   setup(c, &tslot, 128);
   const uint32_t aW0 = tc::smem_u32(W0), aW1 = tc::smem_u32(W1), aT0 = tc::smem_u32(T0);
+  const int f0 = FPT * c.q;
   for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
     const TileRange tr = tile_range(g, tiles, t);
-    float acc[1][PAIRS] = {};
+    const SegMap sg = seg_map(tr.r1 - tr.r0);
+    float acc[1] = {};
     for (int c0 = tr.e0; c0 < tr.e1; c0 += TE) {
       const int ne = min(TE, tr.e1 - c0);
-      load_scalars(g, sc, c0, ne, nullptr);
-      __syncthreads();
+      const ES es = edge_sc(g, c0, ne, c.e);
       {
         float ph[FPT], dph[FPT];
-        basis(sc.d[c.e], rc, FPT * c.q, ph, dph);
-        st_em(T0, c.e, FPT * c.q, ph);
+        basis(es.d, rc, f0, ph, dph);
+        st_em(T0, c.e, f0, ph);
       }
       c.publish();
       if (threadIdx.x == 0) {
@@ -341,34 +387,37 @@ __global__ void __launch_bounds__(NT) msg_fe_tc(EdgeGeom g, const int* __restric
         float z[FPT];
         c.ld(TM_Z, z);
 #pragma unroll
-        for (int j = 0; j < FPT; ++j) z[j] = dev::silu(z[j] + al[FPT * c.q + j]);
-        st_em(T0, c.e, FPT * c.q, z);
+        for (int j = 0; j < FPT; ++j) {
+          const float zz = z[j] + al[f0 + j];
+          z[j] = zz * fsig(zz);
+        }
+        st_em(T0, c.e, f0, z);
       }
       c.publish();
       if (threadIdx.x == 0) {
-        mma_tiles(c.tmem + TM_G, aT0, 128, aW1, 64, 64, 128, false);
+        mma_tiles(c.tmem + TM_ZP, aT0, 128, aW1, 64, 64, 128, false);
         tc::commit(c.mbar);
       }
       c.wait_mma();
       {
         float gg[FPT], vj[FPT];
-        gather32(v, sc.col[c.e], FPT * c.q, vj);
-        c.ld(TM_G, gg);
-        const float ce = sc.c[c.e];
+        gather32(v, es.j, f0, vj);
+        c.ld(TM_ZP, gg);
 #pragma unroll
-        for (int j = 0; j < FPT; ++j) gg[j] = ce * (gg[j] + be[FPT * c.q + j]) * vj[j];  // w_e * v_j
-        st_pl(T1, c.e, FPT * c.q, gg);
+        for (int j = 0; j < FPT; ++j) gg[j] = es.c * (gg[j] + be[f0 + j]) * vj[j];  // w_e * v_j
+        st_pl(T1, c.e, f0, gg);
       }
       tc::fence_before();
       __syncthreads();
       {
         const uint8_t* const tl[1] = {T1};
-        seg_rows<1>(g, tr.r0, tr.r1, c0, ne, tl, acc);
+        seg_rows<1>(g, tr.r0, c0, ne, tl, sg, acc);
       }
       __syncthreads();
     }
+    seg_finish<1>(sg, acc);
     float* const outs[1] = {m_out};
-    seg_write<1>(tr.r0, tr.r1, outs, acc);
+    seg_write<1>(tr.r0, sg, outs, acc);
   }
   teardown(c, 128);
 }
@@ -380,17 +429,15 @@ __global__ void __launch_bounds__(NT) msg_ff_tc(EdgeGeom g, const int* __restric
                                                float rc, const float* __restrict__ v, const float* __restrict__ am,
                                                float* __restrict__ Y_out, float* __restrict__ F, const float* __restrict__ Wt,
                                                float* ah) {
-  extern __shared__ __align__(1024) uint8_t sm[];
+  extern __shared__ __align__(1024) uint8_t sm_raw[];
+  uint8_t* sm = align1024(sm_raw);
   uint8_t* W0 = sm;
   uint8_t* W1 = W0 + kWTile;
   uint8_t* T0 = W1 + kWTile;  // phi -> s -> (plain) w * am_j
   uint8_t* T1 = T0 + kTile;   // phi' -> sdot
-  float* fsm = reinterpret_cast<float*>(T1 + kTile);
-  float* al = fsm;
+  float* al = reinterpret_cast<float*>(T1 + kTile);
   float* be = al + 64;
-  Scal sc{be + 64, be + 64 + TE, be + 64 + 2 * TE, nullptr, reinterpret_cast<int*>(be + 64 + 3 * TE),
-          reinterpret_cast<int*>(be + 64 + 4 * TE)};
-  float* sq = be + 64 + 5 * TE;  // [NQ][TE] per-quarter force scalars
+  float* sq = be + 64;  // [NQ][TE] per-quarter force scalars
   __shared__ __align__(8) uint64_t mbar;
   __shared__ uint32_t tslot;
   Ctx c;
@@ -401,17 +448,19 @@ __global__ void __launch_bounds__(NT) msg_ff_tc(EdgeGeom g, const int* __restric
   setup(c, &tslot, 256);
   const uint32_t aW0 = tc::smem_u32(W0), aW1 = tc::smem_u32(W1), aT0 = tc::smem_u32(T0), aT1 = tc::smem_u32(T1);
   const int f0 = FPT * c.q;
+  // force sums: 8 lanes per (row, component), interleaved edges
+  const int fr = threadIdx.x >> 3, fpart = threadIdx.x & 7;
   for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
     const TileRange tr = tile_range(g, tiles, t);
-    float acc[1][PAIRS] = {};
-    float fsum = 0.f;  // threads < 24: (row t/3, component t%3)
+    const SegMap sg = seg_map(tr.r1 - tr.r0);
+    float acc[1] = {};
+    float fsum = 0.f;
     for (int c0 = tr.e0; c0 < tr.e1; c0 += TE) {
       const int ne = min(TE, tr.e1 - c0);
-      load_scalars(g, sc, c0, ne, nullptr);
-      __syncthreads();
+      const ES es = edge_sc(g, c0, ne, c.e);
       {
         float ph[FPT], dph[FPT];
-        basis(sc.d[c.e], rc, f0, ph, dph);
+        basis(es.d, rc, f0, ph, dph);
         st_em(T0, c.e, f0, ph);
         st_em(T1, c.e, f0, dph);
       }
@@ -428,9 +477,9 @@ __global__ void __launch_bounds__(NT) msg_ff_tc(EdgeGeom g, const int* __restric
         c.ld(TM_ZP, zp);
 #pragma unroll
         for (int j = 0; j < FPT; ++j) {
-          const float zz = z[j] + al[f0 + j];
-          z[j] = dev::silu(zz);
-          zp[j] = dev::dsilu(zz) * zp[j];
+          const float zz = z[j] + al[f0 + j], sg1 = fsig(zz);
+          z[j] = zz * sg1;
+          zp[j] = sg1 * (1.0f + zz * (1.0f - sg1)) * zp[j];
         }
         st_em(T0, c.e, f0, z);
         st_em(T1, c.e, f0, zp);
@@ -443,26 +492,21 @@ __global__ void __launch_bounds__(NT) msg_ff_tc(EdgeGeom g, const int* __restric
       }
       c.wait_mma();
       {
-        const int i = sc.src[c.e], j = sc.col[c.e];
-        const float ce = sc.c[c.e], dce = sc.dc[c.e];
         float gg[FPT], gp[FPT];
+        float pq = 0.f;
+        float amj[FPT], vj[FPT], ami[FPT], vi[FPT];
+        gather32(am, es.j, f0, amj);
+        gather32(v, es.j, f0, vj);
+        gather32(am, es.i, f0, ami);
+        gather32(v, es.i, f0, vi);
         c.ld(TM_G, gg);
         c.ld(TM_GP, gp);
-        float pq = 0.f;
-        float amj[FPT];
-        gather32(am, j, f0, amj);
-        {
-          float vj[FPT], ami[FPT], vi[FPT];
-          gather32(v, j, f0, vj);
-          gather32(am, i, f0, ami);
-          gather32(v, i, f0, vi);
 #pragma unroll
-          for (int q = 0; q < FPT; ++q) {
-            const float gb = gg[q] + be[f0 + q];
-            const float wp = dce * gb + ce * gp[q];
-            pq = fmaf(fmaf(ami[q], vj[q], amj[q] * vi[q]), wp, pq);
-            gg[q] = ce * gb * amj[q];  // w_e * am_j
-          }
+        for (int q = 0; q < FPT; ++q) {
+          const float gb = gg[q] + be[f0 + q];
+          const float wp = es.dc * gb + es.c * gp[q];
+          pq = fmaf(fmaf(ami[q], vj[q], amj[q] * vi[q]), wp, pq);
+          gg[q] = es.c * gb * amj[q];  // w_e * am_j
         }
         st_pl(T0, c.e, f0, gg);
         sq[c.q * TE + c.e] = pq;
@@ -471,32 +515,31 @@ __global__ void __launch_bounds__(NT) msg_ff_tc(EdgeGeom g, const int* __restric
       __syncthreads();
       {
         const uint8_t* const tl[1] = {T0};
-        seg_rows<1>(g, tr.r0, tr.r1, c0, ne, tl, acc);
-        if (threadIdx.x < 3 * kRowsPerTile) {
-          const int r = tr.r0 + threadIdx.x / 3, comp = threadIdx.x % 3;
-          if (r < tr.r1) {
-            const int eb = max(g.row_ptr[r], c0), ee = min(g.row_ptr[r + 1], c0 + ne);
-            for (int x = eb; x < ee; ++x)
-              fsum = fmaf((sq[x - c0] + sq[TE + x - c0]) + (sq[2 * TE + x - c0] + sq[3 * TE + x - c0]), g.u[3 * x + comp], fsum);
-          }
+        seg_rows<1>(g, tr.r0, c0, ne, tl, sg, acc);
+        if (fr < 3 * (tr.r1 - tr.r0)) {
+          const int r = tr.r0 + fr / 3, comp = fr % 3;
+          const int eb = max(g.row_ptr[r], c0), ee = min(g.row_ptr[r + 1], c0 + ne);
+          for (int x = eb + fpart; x < ee; x += 8)
+            fsum = fmaf((sq[x - c0] + sq[TE + x - c0]) + (sq[2 * TE + x - c0] + sq[3 * TE + x - c0]), g.u[3 * x + comp], fsum);
         }
       }
       __syncthreads();
     }
+    seg_finish<1>(sg, acc);
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) fsum += __shfl_xor_sync(0xffffffffu, fsum, o);
     float* const outs[1] = {Y_out};
-    seg_write<1>(tr.r0, tr.r1, outs, acc);
-    if (threadIdx.x < 3 * kRowsPerTile) {
-      const int r = tr.r0 + threadIdx.x / 3;
-      if (r < tr.r1) F[3 * r + threadIdx.x % 3] += fsum;
-    }
-    if (ah) rows_times_wt(tr.r0, tr.r1, acc[0], reinterpret_cast<float*>(T1), Wt, ah, nullptr, ah);  // a_h += Y W^T
+    seg_write<1>(tr.r0, sg, outs, acc);
+    if (fpart == 0 && fr < 3 * (tr.r1 - tr.r0)) F[3 * tr.r0 + fr] += fsum;
+    if (ah) rows_times_wt(tr.r0, tr.r1, sg, acc[0], reinterpret_cast<float*>(T1), Wt, ah, nullptr, ah);  // a_h += Y W^T
   }
   teardown(c, 256);
 }
 
 // Write the CTA's weight-gradient partial [dA | dalpha | dB | dbeta] from the
 // M=64 TMEM accumulators (row r at lane (r/16)*32 + r%16) and the per-thread
-// column sums (reduced over the 128 edge threads in order through smem).
+// column sums (xor-butterfly over the warp's 32 edges, then the 4 edge warps
+// of each feature quarter in fixed order through smem).
 __device__ __forceinline__ void write_partial(Ctx& c, float* part, uint8_t* scratch, const float (&cs_a)[FPT],
                                               const float (&cs_b)[FPT]) {
   tc::fence_before();
@@ -509,25 +552,44 @@ __device__ __forceinline__ void write_partial(Ctx& c, float* part, uint8_t* scra
     c.ld(TM_BG, vb);
     if (c.lane < 16) {
       const int r = 16 * q + c.lane;
+      float4* pa = reinterpret_cast<float4*>(part + r * H + FPT * c.q);
+      float4* pb = reinterpret_cast<float4*>(part + R * H + H + r * H + FPT * c.q);
 #pragma unroll
-      for (int j = 0; j < FPT; ++j) {
-        part[r * H + FPT * c.q + j] = va[j];              // dA[r][h]
-        part[R * H + H + r * H + FPT * c.q + j] = vb[j];  // dB[k][h]
+      for (int j = 0; j < FPT / 4; ++j) {
+        pa[j] = make_float4(va[4 * j], va[4 * j + 1], va[4 * j + 2], va[4 * j + 3]);  // dA[r][h]
+        pb[j] = make_float4(vb[4 * j], vb[4 * j + 1], vb[4 * j + 2], vb[4 * j + 3]);  // dB[k][h]
       }
     }
   }
-  float* red = reinterpret_cast<float*>(scratch);  // [128][64]
-  for (int pass = 0; pass < 2; ++pass) {
-    const float(&cs)[FPT] = pass ? cs_b : cs_a;
+  // column sums: [feature][edge] staging (conflict-free: consecutive edges),
+  // then 8 threads per feature sum 16 contiguous edges each and combine by an
+  // xor butterfly — a fixed order, so the partial is deterministic.
+  float* red = reinterpret_cast<float*>(scratch);  // [2][64][TE]
 #pragma unroll
-    for (int j = 0; j < FPT; ++j) red[c.e * 64 + FPT * c.q + j] = cs[j];
-    __syncthreads();
-    if (threadIdx.x < 64) {
-      float s = 0.f;
-      for (int e = 0; e < TE; ++e) s += red[e * 64 + threadIdx.x];
-      part[(pass ? R * H + H + H * H : R * H) + threadIdx.x] = s;
+  for (int j = 0; j < FPT; ++j) {
+    red[(FPT * c.q + j) * TE + c.e] = cs_a[j];
+    red[64 * TE + (FPT * c.q + j) * TE + c.e] = cs_b[j];
+  }
+  __syncthreads();
+  {
+    const int f = threadIdx.x >> 3, prt = threadIdx.x & 7;
+    float sa = 0.f, sb = 0.f;
+#pragma unroll
+    for (int k = 0; k < TE / 32; ++k) {
+      const float4 x = *reinterpret_cast<const float4*>(red + f * TE + 16 * prt + 4 * k);
+      const float4 y = *reinterpret_cast<const float4*>(red + 64 * TE + f * TE + 16 * prt + 4 * k);
+      sa += (x.x + x.y) + (x.z + x.w);
+      sb += (y.x + y.y) + (y.z + y.w);
     }
-    __syncthreads();
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      sa += __shfl_xor_sync(0xffffffffu, sa, o);
+      sb += __shfl_xor_sync(0xffffffffu, sb, o);
+    }
+    if (prt == 0) {
+      part[R * H + f] = sa;
+      part[R * H + H + H * H + f] = sb;
+    }
   }
 }
 
@@ -538,7 +600,10 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int* __rest
                                                   float rc, const float* __restrict__ v, const float* __restrict__ bm,
                                                   float* __restrict__ Yb_out, float* __restrict__ partial,
                                                   const float* __restrict__ Wt, const float* __restrict__ inj, float* bh) {
-  extern __shared__ __align__(1024) uint8_t sm[];
+  extern __shared__ __align__(1024) uint8_t sm_raw[];
+  uint8_t* sm = align1024(sm_raw);
+  TC_DECL;
+  TC_M();
   uint8_t* W0 = sm;           // A^T
   uint8_t* W1 = W0 + kWTile;  // B^T
   uint8_t* W2 = W1 + kWTile;  // B
@@ -546,11 +611,8 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int* __rest
   uint8_t* T1 = T0 + kTile;
   uint8_t* T2 = T1 + kTile;
   uint8_t* T3 = T2 + kTile;
-  float* fsm = reinterpret_cast<float*>(T3 + kTile);
-  float* al = fsm;
+  float* al = reinterpret_cast<float*>(T3 + kTile);
   float* be = al + 64;
-  Scal sc{be + 64, be + 64 + TE, nullptr, nullptr, reinterpret_cast<int*>(be + 64 + 2 * TE),
-          reinterpret_cast<int*>(be + 64 + 3 * TE)};
   __shared__ __align__(8) uint64_t mbar;
   __shared__ uint32_t tslot;
   Ctx c;
@@ -558,7 +620,9 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int* __rest
   c.mbar = &mbar;
   __shared__ __align__(8) uint64_t wbar;
   load_weights(sm, p.pack, 3, al, be, &wbar);
+  TC_M();
   setup(c, &tslot, 512);
+  TC_M();
   const uint32_t aW0 = tc::smem_u32(W0), aW1 = tc::smem_u32(W1), aW2 = tc::smem_u32(W2);
   const uint32_t aT0 = tc::smem_u32(T0), aT1 = tc::smem_u32(T1), aT2 = tc::smem_u32(T2), aT3 = tc::smem_u32(T3);
   float cs_a[FPT], cs_b[FPT];
@@ -568,14 +632,14 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int* __rest
   const int f0 = FPT * c.q;
   for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
     const TileRange tr = tile_range(g, tiles, t);
-    float acc[1][PAIRS] = {};
+    const SegMap sg = seg_map(tr.r1 - tr.r0);
+    float acc[1] = {};
     for (int c0 = tr.e0; c0 < tr.e1; c0 += TE) {
       const int ne = min(TE, tr.e1 - c0);
-      load_scalars(g, sc, c0, ne, nullptr);
-      __syncthreads();
+      const ES es = edge_sc(g, c0, ne, c.e);
       {
         float ph[FPT], dph[FPT];
-        basis(sc.d[c.e], rc, f0, ph, dph);
+        basis(es.d, rc, f0, ph, dph);
         st_em(T0, c.e, f0, ph);
       }
       c.publish();
@@ -583,12 +647,17 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int* __rest
         mma_tiles(c.tmem + TM_Z, aT0, 128, aW0, 64, 64, 128, false);
         tc::commit(c.mbar);
       }
+      TC_M();
       c.wait_mma();
+      TC_M();
       {
         float z[FPT];
         c.ld(TM_Z, z);
 #pragma unroll
-        for (int j = 0; j < FPT; ++j) z[j] = dev::silu(z[j] + al[f0 + j]);
+        for (int j = 0; j < FPT; ++j) {
+          const float zz = z[j] + al[f0 + j];
+          z[j] = zz * fsig(zz);
+        }
         st_em(T0, c.e, f0, z);  // s, edge-major (A of g = s B)
         st_fm(T1, c.e, f0, z);  // s^T (A of dB = s^T gbar)
       }
@@ -597,52 +666,58 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int* __rest
         mma_tiles(c.tmem + TM_G, aT0, 128, aW1, 64, 64, 128, false);
         tc::commit(c.mbar);
       }
+      TC_M();
       c.wait_mma();
+      TC_M();
       float gb[FPT];
       {
-        const int i = sc.src[c.e], j = sc.col[c.e];
-        const float ce = sc.c[c.e];
-        float gg[FPT], bj[FPT];
+        float gg[FPT], bj[FPT], bi[FPT], vj[FPT];
+        gather32(bm, es.j, f0, bj);
+        gather32(bm, es.i, f0, bi);
+        gather32(v, es.j, f0, vj);
         c.ld(TM_G, gg);
-        gather32(bm, j, f0, bj);
-#pragma unroll
-        for (int q = 0; q < FPT; ++q) gg[q] = ce * (gg[q] + be[f0 + q]) * bj[q];  // w_e * bm_j
-        st_pl(T0, c.e, f0, gg);
-        float bi[FPT], vj[FPT];
-        gather32(bm, i, f0, bi);
-        gather32(v, j, f0, vj);
+        TC_M();
 #pragma unroll
         for (int q = 0; q < FPT; ++q) {
-          gb[q] = ce * bi[q] * vj[q];  // gbar (zero on padding edges: c = 0)
+          gg[q] = es.c * (gg[q] + be[f0 + q]) * bj[q];  // w_e * bm_j
+          gb[q] = es.c * bi[q] * vj[q];                 // gbar (zero on padding edges: c = 0)
           cs_b[q] += gb[q];
         }
+        TC_M();
+        st_pl(T0, c.e, f0, gg);
       }
       st_fm(T2, c.e, f0, gb);  // gbar^T (B of dB)
       st_em(T3, c.e, f0, gb);  // gbar   (A of sbar = gbar B^T)
+      TC_M();
       c.publish();
+      TC_M();
       if (threadIdx.x == 0) {
         mma_tiles(c.tmem + TM_BG, aT1, 64, aT2, 64, 128, 64, !first);
         mma_tiles(c.tmem + TM_G, aT3, 128, aW2, 64, 64, 128, false);
         tc::commit(c.mbar);
       }
+      TC_M();
       {  // row sums overlap the MMAs (they read T1..T3, this reads T0)
         const uint8_t* const tl[1] = {T0};
-        seg_rows<1>(g, tr.r0, tr.r1, c0, ne, tl, acc);
+        seg_rows<1>(g, tr.r0, c0, ne, tl, sg, acc);
       }
+      TC_M();
       c.wait_mma();
       __syncthreads();  // T0 reads done before it is rewritten
+      TC_M();
       {
         float z[FPT], sb[FPT];
         c.ld(TM_Z, z);
         c.ld(TM_G, sb);
 #pragma unroll
         for (int j = 0; j < FPT; ++j) {
-          z[j] = sb[j] * dev::dsilu(z[j] + al[f0 + j]);
+          const float zz = z[j] + al[f0 + j], s1 = fsig(zz);
+          z[j] = sb[j] * (s1 * (1.0f + zz * (1.0f - s1)));
           cs_a[j] += z[j];
         }
         st_fm(T2, c.e, f0, z);  // zbar^T
         float ph[FPT], dph[FPT];
-        basis(sc.d[c.e], rc, f0, ph, dph);
+        basis(es.d, rc, f0, ph, dph);
         st_fm(T0, c.e, f0, ph);  // phi^T
       }
       c.publish();
@@ -650,13 +725,18 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int* __rest
         mma_tiles(c.tmem + TM_AG, aT0, 64, aT2, 64, 128, 64, !first);
         tc::commit(c.mbar);
       }
+      TC_M();
       c.wait_mma();
+      TC_M();
       first = false;
       __syncthreads();
     }
+    seg_finish<1>(sg, acc);
     float* const outs[1] = {Yb_out};
-    seg_write<1>(tr.r0, tr.r1, outs, acc);
-    if (bh) rows_times_wt(tr.r0, tr.r1, acc[0], reinterpret_cast<float*>(T1), Wt, bh, inj, bh);  // b_h += Yb W^T + inj
+    seg_write<1>(tr.r0, sg, outs, acc);
+    TC_M();
+    if (bh) rows_times_wt(tr.r0, tr.r1, sg, acc[0], reinterpret_cast<float*>(T1), Wt, bh, inj, bh);  // b_h += Yb W^T + inj
+    TC_M();
   }
   float* part = partial + (size_t)blockIdx.x * PE;
   if (first) {  // CTA without tiles: zero partial (TMEM accumulators never written)
@@ -665,7 +745,10 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int* __rest
     return;
   }
   write_partial(c, part, T0, cs_a, cs_b);
+  TC_M();
   teardown(c, 512);
+  TC_M();
+  TC_DUMP("be");
 }
 
 // ----------------------------------------------------------------------- BF
@@ -677,7 +760,10 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
                                                   float* __restrict__ mdot_out, float* __restrict__ X_out,
                                                   float* __restrict__ partial, const float* __restrict__ Wt,
                                                   float* __restrict__ inj) {
-  extern __shared__ __align__(1024) uint8_t sm[];
+  extern __shared__ __align__(1024) uint8_t sm_raw[];
+  uint8_t* sm = align1024(sm_raw);
+  TC_DECL;
+  TC_M();
   uint8_t* W0 = sm;
   uint8_t* W1 = W0 + kWTile;
   uint8_t* W2 = W1 + kWTile;
@@ -685,11 +771,8 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
   uint8_t* T1 = T0 + kTile;
   uint8_t* T2 = T1 + kTile;
   uint8_t* T3 = T2 + kTile;
-  float* fsm = reinterpret_cast<float*>(T3 + kTile);
-  float* al = fsm;
+  float* al = reinterpret_cast<float*>(T3 + kTile);
   float* be = al + 64;
-  Scal sc{be + 64, be + 64 + TE, be + 64 + 2 * TE, be + 64 + 3 * TE, reinterpret_cast<int*>(be + 64 + 4 * TE),
-          reinterpret_cast<int*>(be + 64 + 5 * TE)};
   __shared__ __align__(8) uint64_t mbar;
   __shared__ uint32_t tslot;
   Ctx c;
@@ -697,7 +780,9 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
   c.mbar = &mbar;
   __shared__ __align__(8) uint64_t wbar;
   load_weights(sm, p.pack, 3, al, be, &wbar);
+  TC_M();
   setup(c, &tslot, 512);
+  TC_M();
   const uint32_t aW0 = tc::smem_u32(W0), aW1 = tc::smem_u32(W1), aW2 = tc::smem_u32(W2);
   const uint32_t aT0 = tc::smem_u32(T0), aT1 = tc::smem_u32(T1), aT2 = tc::smem_u32(T2), aT3 = tc::smem_u32(T3);
   float cs_a[FPT], cs_b[FPT];
@@ -707,14 +792,14 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
   const int f0 = FPT * c.q;
   for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
     const TileRange tr = tile_range(g, tiles, t);
-    float acc[2][PAIRS] = {};
+    const SegMap sg = seg_map(tr.r1 - tr.r0);
+    float acc[2] = {};
     for (int c0 = tr.e0; c0 < tr.e1; c0 += TE) {
       const int ne = min(TE, tr.e1 - c0);
-      load_scalars(g, sc, c0, ne, Fbar);
-      __syncthreads();
+      const ES es = edge_sc(g, c0, ne, c.e);
       {
         float ph[FPT], dph[FPT];
-        basis(sc.d[c.e], rc, f0, ph, dph);
+        basis(es.d, rc, f0, ph, dph);
         st_em(T0, c.e, f0, ph);
         st_em(T1, c.e, f0, dph);
       }
@@ -724,16 +809,18 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
         mma_tiles(c.tmem + TM_ZP, aT1, 128, aW0, 64, 64, 128, false);
         tc::commit(c.mbar);
       }
+      TC_M();
       c.wait_mma();
+      TC_M();
       {
         float z[FPT], zp[FPT];
         c.ld(TM_Z, z);
         c.ld(TM_ZP, zp);
 #pragma unroll
         for (int j = 0; j < FPT; ++j) {
-          const float zz = z[j] + al[f0 + j];
-          z[j] = dev::silu(zz);
-          zp[j] = dev::dsilu(zz) * zp[j];
+          const float zz = z[j] + al[f0 + j], s1 = fsig(zz);
+          z[j] = zz * s1;
+          zp[j] = s1 * (1.0f + zz * (1.0f - s1)) * zp[j];
         }
         st_em(T0, c.e, f0, z);   // s
         st_em(T1, c.e, f0, zp);  // sdot
@@ -746,33 +833,38 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
         mma_tiles(c.tmem + TM_GP, aT1, 128, aW1, 64, 64, 128, false);
         tc::commit(c.mbar);
       }
+      TC_M();
       c.wait_mma();
+      TC_M();
       float mu[FPT], nu[FPT];
       {
-        const int i = sc.src[c.e], j = sc.col[c.e];
-        const float qb = sc.qb[c.e], ce = sc.c[c.e], dce = sc.dc[c.e];
+        const float qb = edge_qbar(g, es, Fbar);
         float gg[FPT], gp[FPT];
-        c.ld(TM_G, gg);
-        c.ld(TM_GP, gp);
         float pm[FPT], px[FPT];
+        float4 a4[FPT / 4], aj4[FPT / 4], v4[FPT / 4], d4[FPT / 4];
 #pragma unroll
         for (int q = 0; q < FPT / 4; ++q) {
-          const float4 a4 = __ldg(reinterpret_cast<const float4*>(am + (size_t)i * H + f0) + q);
-          const float4 aj4 = __ldg(reinterpret_cast<const float4*>(am + (size_t)j * H + f0) + q);
-          const float4 v4 = __ldg(reinterpret_cast<const float4*>(v + (size_t)j * H + f0) + q);
-          const float4 d4 = __ldg(reinterpret_cast<const float4*>(vdot + (size_t)j * H + f0) + q);
-          const float ai[4] = {a4.x, a4.y, a4.z, a4.w}, aj[4] = {aj4.x, aj4.y, aj4.z, aj4.w};
-          const float vv[4] = {v4.x, v4.y, v4.z, v4.w}, dv[4] = {d4.x, d4.y, d4.z, d4.w};
+          a4[q] = __ldg(reinterpret_cast<const float4*>(am + (size_t)es.i * H + f0) + q);
+          aj4[q] = __ldg(reinterpret_cast<const float4*>(am + (size_t)es.j * H + f0) + q);
+          v4[q] = __ldg(reinterpret_cast<const float4*>(v + (size_t)es.j * H + f0) + q);
+          d4[q] = __ldg(reinterpret_cast<const float4*>(vdot + (size_t)es.j * H + f0) + q);
+        }
+        c.ld(TM_G, gg);
+        c.ld(TM_GP, gp);
+#pragma unroll
+        for (int q = 0; q < FPT / 4; ++q) {
+          const float ai[4] = {a4[q].x, a4[q].y, a4[q].z, a4[q].w}, aj[4] = {aj4[q].x, aj4[q].y, aj4[q].z, aj4[q].w};
+          const float vv[4] = {v4[q].x, v4[q].y, v4[q].z, v4[q].w}, dv[4] = {d4[q].x, d4[q].y, d4[q].z, d4[q].w};
 #pragma unroll
           for (int r = 0; r < 4; ++r) {
             const int k = 4 * q + r;
             const float gb = gg[k] + be[f0 + k];
-            const float w = ce * gb, wp = qb * (dce * gb + ce * gp[k]);
+            const float w = es.c * gb, wp = qb * (es.dc * gb + es.c * gp[k]);
             pm[k] = fmaf(wp, vv[r], w * dv[r]);  // qb w' v_j + w vdot_j
             px[k] = wp * aj[r];                  // qb w' am_j
             const float rho = ai[r] * vv[r], kap = ai[r] * dv[r];
-            mu[k] = qb * dce * rho + ce * kap;
-            nu[k] = qb * ce * rho;
+            mu[k] = qb * es.dc * rho + es.c * kap;
+            nu[k] = qb * es.c * rho;
           }
         }
         st_pl(T0, c.e, f0, pm);
@@ -784,8 +876,9 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
       __syncthreads();
       {
         const uint8_t* const tl[2] = {T0, T1};
-        seg_rows<2>(g, tr.r0, tr.r1, c0, ne, tl, acc);
+        seg_rows<2>(g, tr.r0, c0, ne, tl, sg, acc);
       }
+      TC_M();
       __syncthreads();         // row sums done with T0/T1
       st_fm(T0, c.e, f0, mu);  // mu^T
       st_fm(T1, c.e, f0, nu);  // nu^T
@@ -795,7 +888,9 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
         mma_tiles(c.tmem + TM_BG, aT3, 64, aT1, 64, 128, 64, true);
         tc::commit(c.mbar);
       }
+      TC_M();
       c.wait_mma();
+      TC_M();
       st_em(T2, c.e, f0, mu);  // mu (A of sbar = mu B^T)
       st_em(T3, c.e, f0, nu);  // nu
       c.publish();
@@ -804,7 +899,9 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
         mma_tiles(c.tmem + TM_GP, aT3, 128, aW2, 64, 64, 128, false);  // sdotbar
         tc::commit(c.mbar);
       }
+      TC_M();
       c.wait_mma();
+      TC_M();
       {
         float z[FPT], zp[FPT], sb[FPT], sdb[FPT];
         c.ld(TM_Z, z);
@@ -813,16 +910,17 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
         c.ld(TM_GP, sdb);
 #pragma unroll
         for (int j = 0; j < FPT; ++j) {
-          const float zz = z[j] + al[f0 + j];
-          const float ds = dev::dsilu(zz);
-          z[j] = sb[j] * ds + sdb[j] * dev::d2silu(zz) * zp[j];  // zbar
-          zp[j] = sdb[j] * ds;                                   // zbar'
+          const float zz = z[j] + al[f0 + j], s1 = fsig(zz);
+          const float ds = s1 * (1.0f + zz * (1.0f - s1));
+          const float d2s = s1 * (1.0f - s1) * (2.0f + zz * (1.0f - 2.0f * s1));
+          z[j] = sb[j] * ds + sdb[j] * d2s * zp[j];  // zbar
+          zp[j] = sdb[j] * ds;                       // zbar'
           cs_a[j] += z[j];
         }
         st_fm(T2, c.e, f0, z);
         st_fm(T3, c.e, f0, zp);
         float ph[FPT], dph[FPT];
-        basis(sc.d[c.e], rc, f0, ph, dph);
+        basis(es.d, rc, f0, ph, dph);
         st_fm(T0, c.e, f0, ph);   // phi^T
         st_fm(T1, c.e, f0, dph);  // phi'^T
       }
@@ -832,13 +930,18 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
         mma_tiles(c.tmem + TM_AG, aT1, 64, aT3, 64, 128, 64, true);
         tc::commit(c.mbar);
       }
+      TC_M();
       c.wait_mma();
+      TC_M();
       first = false;
       __syncthreads();
     }
+    seg_finish<2>(sg, acc);
     float* const outs[2] = {mdot_out, X_out};
-    seg_write<2>(tr.r0, tr.r1, outs, acc);
-    if (inj) rows_times_wt(tr.r0, tr.r1, acc[1], reinterpret_cast<float*>(T1), Wt, nullptr, nullptr, inj);  // hbar^F = X W^T
+    seg_write<2>(tr.r0, sg, outs, acc);
+    TC_M();
+    if (inj) rows_times_wt(tr.r0, tr.r1, sg, acc[1], reinterpret_cast<float*>(T1), Wt, nullptr, nullptr, inj);  // hbar^F = X W^T
+    TC_M();
   }
   float* part = partial + (size_t)blockIdx.x * PE;
   if (first) {
@@ -847,10 +950,13 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
     return;
   }
   write_partial(c, part, T0, cs_a, cs_b);
+  TC_M();
   teardown(c, 512);
+  TC_M();
+  TC_DUMP("bf");
 }
 
-constexpr size_t kSmallBytes = sizeof(float) * (128 + 10 * TE);
+constexpr size_t kSmallBytes = sizeof(float) * (128 + NQ * TE) + 1024;  // alpha, beta, FF force scalars
 constexpr size_t fe_smem() { return 2 * kWTile + 2 * kTile + kSmallBytes; }
 constexpr size_t ff_smem() { return 2 * kWTile + 2 * kTile + kSmallBytes; }
 constexpr size_t be_smem() { return 3 * kWTile + 4 * kTile + kSmallBytes; }
