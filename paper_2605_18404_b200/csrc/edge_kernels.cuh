@@ -623,14 +623,31 @@ __global__ void __launch_bounds__(NT) msg_be_kernel(EdgeGeom g, MsgParams p, flo
   }
 }
 
-// out[p] = sum_t partial[t][p]  (tile order => deterministic)
-__global__ void reduce_partials_kernel(const float* __restrict__ partial, int n_tiles, int PE, float* __restrict__ out) {
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= PE) return;
+// out[p] = sum_t partial[t][p]: each CTA owns 32 columns; its 8 warps sum
+// contiguous eighths of the partial list in order (coalesced 128 B rows, loads
+// in flight) and warp 0 adds the eight results in order => deterministic.
+constexpr int kReduceCols = 32;
+inline int reduce_grid(int PE) { return (PE + kReduceCols - 1) / kReduceCols; }
+__global__ void __launch_bounds__(256) reduce_partials_kernel(const float* __restrict__ partial, int n_tiles, int PE,
+                                                              float* __restrict__ out) {
+  __shared__ float red[8][kReduceCols + 1];
+  const int c = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const int p = blockIdx.x * kReduceCols + c;
+  const int per = (n_tiles + 7) / 8;
+  const int t0 = grp * per, t1 = min(n_tiles, t0 + per);
   float s = 0.f;
+  if (p < PE) {
 #pragma unroll 8
-  for (int t = 0; t < n_tiles; ++t) s += __ldg(partial + (size_t)t * PE + p);
-  out[p] = s;
+    for (int t = t0; t < t1; ++t) s += __ldg(partial + (size_t)t * PE + p);
+  }
+  red[grp][c] = s;
+  __syncthreads();
+  if (grp == 0 && p < PE) {
+    float r = 0.f;
+#pragma unroll
+    for (int g = 0; g < 8; ++g) r += red[g][c];
+    out[p] = r;
+  }
 }
 
 template <int H, int R>

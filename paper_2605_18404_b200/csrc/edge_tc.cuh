@@ -35,25 +35,41 @@ constexpr int kRowsPerTile = 8;
 constexpr uint32_t kTile = 128 * 64 * 4;  // 32 KB operand tile
 constexpr uint32_t kWTile = 64 * 64 * 4;  // 16 KB weight tile
 constexpr int PE = R * H + H + H * H + H;
+static_assert(PE == 4 * 2080, "write_partial copy-out assumes H = R = 64");
 
 // Phase tracing (profiling builds only: make TRACE=1): thread 0 of CTAs 0 and
 // gridDim/2 prints clock64 deltas between the marks of one kernel.
 #ifdef JANUS_TC_TRACE
-#define TC_DECL long long trc[24] = {}; int ntr = 0
+#define TC_DECL long long trc[32] = {}; int ntr = 0
 #define TC_M()                                                   \
   do {                                                           \
-    if (threadIdx.x == 0 && ntr < 24) trc[ntr] = clock64();      \
+    if (threadIdx.x == 0 && ntr < 32) trc[ntr] = clock64();      \
     ++ntr;                                                       \
   } while (0)
 #define TC_DUMP(name)                                                                                          \
   if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x / 2)) {                                   \
-    long long d[20] = {};                                                                                      \
-    for (int k = 1; k < ntr && k < 21; ++k) d[k - 1] = trc[k] - trc[k - 1];                                    \
-    printf("TRACE %s cta %d marks %d total %lld: %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld\n", \
-           name, blockIdx.x, ntr, trc[min(ntr, 24) - 1] - trc[0], d[0], d[1], d[2], d[3], d[4], d[5], d[6], d[7], d[8], \
-           d[9], d[10], d[11], d[12], d[13], d[14], d[15], d[16], d[17], d[18], d[19]);                        \
+    long long d[30] = {};                                                                                      \
+    for (int k = 1; k < ntr && k < 31; ++k) d[k - 1] = trc[k] - trc[k - 1];                                    \
+    printf("TRACE %s cta %d marks %d total %lld: %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld\n", \
+           name, blockIdx.x, ntr, trc[min(ntr, 32) - 1] - trc[0], d[0], d[1], d[2], d[3], d[4], d[5], d[6], d[7], d[8], \
+           d[9], d[10], d[11], d[12], d[13], d[14]);                                                           \
+    printf("TRACE+ %s cta %d: %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld\n", name, blockIdx.x, \
+           d[15], d[16], d[17], d[18], d[19], d[20], d[21], d[22], d[23], d[24], d[25], d[26], d[27], d[28], d[29]); \
   }
+#define TC_ARGS , long long *trc, int &ntr
+#define TC_GT(v) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v))
+#define TC_SPAN_BEGIN unsigned long long gt0 = 0; if (threadIdx.x == 0) TC_GT(gt0)
+#define TC_SPAN_END(name)                                                                          \
+  if (threadIdx.x == 0) {                                                                          \
+    unsigned long long gt1; TC_GT(gt1); unsigned smid; asm volatile("mov.u32 %0, %%smid;" : "=r"(smid)); \
+    printf("SPAN %s cta %d sm %u t0 %llu t1 %llu\n", name, blockIdx.x, smid, gt0, gt1);              \
+  }
+#define TC_PASS , trc, ntr
 #else
+#define TC_ARGS
+#define TC_PASS
+#define TC_SPAN_BEGIN
+#define TC_SPAN_END(name)
 #define TC_DECL
 #define TC_M()
 #define TC_DUMP(name)
@@ -64,16 +80,20 @@ constexpr uint32_t TM_Z = 0, TM_ZP = 64, TM_G = 128, TM_GP = 192, TM_AG = 256, T
 __device__ __forceinline__ uint32_t off_em(int e, int f) { return tc::sw128_off(e, f, 128); }  // [128 edges][64 feat]
 __device__ __forceinline__ uint32_t off_fm(int f, int e) { return tc::sw128_off(f, e, 64); }   // [64 feat][128 edges]
 
-// D[tmem] (+)= A(rows a_rows, K) . B(rows b_rows, K)^T, K-major SWIZZLE_128B tiles.
-__device__ __forceinline__ void mma_tiles(uint32_t d, uint32_t a, int a_rows, uint32_t b, int b_rows, int K, int M,
-                                          bool accumulate) {
-  const uint32_t id = tc::idesc_tf32(M, 64, false, false);
-  const uint32_t as = static_cast<uint32_t>(a_rows) * 128u, bs = static_cast<uint32_t>(b_rows) * 128u;
-#pragma unroll 1
+// D[tmem] (+)= A(rows A_ROWS, K) . B(rows B_ROWS, K)^T, K-major SWIZZLE_128B
+// tiles.  Fully unrolled: the base descriptors are built once and each K-step
+// of 8 adds a compile-time offset to the 14-bit start-address field (32 B
+// inside a 128 B slab row, A_ROWS * 128 B between slabs), so the issuing
+// thread emits the UTCHMMAs back to back.
+template <int A_ROWS, int B_ROWS, int K, int M>
+__device__ __forceinline__ void mma_tiles(uint32_t d, uint32_t a, uint32_t b, bool accumulate) {
+  constexpr uint32_t id = tc::idesc_tf32(M, 64, false, false);
+  const uint64_t da0 = tc::smem_desc(a, 16, 1024, 2), db0 = tc::smem_desc(b, 16, 1024, 2);
+#pragma unroll
   for (int s = 0; s < K / 8; ++s) {
-    const uint64_t da = tc::smem_desc(a + (s >> 2) * as + 32u * (s & 3), 16, 1024, 2);
-    const uint64_t db = tc::smem_desc(b + (s >> 2) * bs + 32u * (s & 3), 16, 1024, 2);
-    tc::mma_tf32(d, da, db, id, (s > 0 || accumulate) ? 1u : 0u);
+    const uint64_t oa = static_cast<uint64_t>(((s >> 2) * A_ROWS * 128 + 32 * (s & 3)) >> 4);
+    const uint64_t ob = static_cast<uint64_t>(((s >> 2) * B_ROWS * 128 + 32 * (s & 3)) >> 4);
+    tc::mma_tf32(d, da0 + oa, db0 + ob, id, (s > 0 || accumulate) ? 1u : 0u);
   }
 }
 
@@ -117,13 +137,14 @@ __device__ __forceinline__ void stage_weight(uint8_t* dst, const float* __restri
 }
 
 // Packed weight image in global memory = the exact smem image of
-// [W0 = A^T | W1 = B^T | W2 = B | alpha | beta]; rebuilt after every
-// optimizer step (stage.cu refresh_transposes) and pulled by each CTA with one
-// TMA bulk copy.
-constexpr uint32_t kPackBytes = 3 * kWTile + 2 * 64 * 4;
+// [W0 = A^T | W1 = B^T | W2 = B | alpha | beta | W^T (plain row-major, for
+// the fused row epilogue)]; rebuilt after every optimizer step (stage.cu
+// refresh_transposes) and pulled by each CTA with TMA bulk copies.
+constexpr uint32_t kWtOff = 3 * kWTile + 2 * 64 * 4;
+constexpr uint32_t kPackBytes = kWtOff + kWTile;
 
 __global__ void pack_msg_weights(const float* __restrict__ A, const float* __restrict__ alpha, const float* __restrict__ B,
-                                 const float* __restrict__ beta, float* __restrict__ pack) {
+                                 const float* __restrict__ beta, const float* __restrict__ W, float* __restrict__ pack) {
   uint8_t* dst = reinterpret_cast<uint8_t*>(pack);
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x < 64 * 64) {
@@ -131,6 +152,7 @@ __global__ void pack_msg_weights(const float* __restrict__ A, const float* __res
     *reinterpret_cast<float*>(dst + tc::sw128_off(b, a, 64)) = A[x];               // A^T: (n=h=b, k=r=a)
     *reinterpret_cast<float*>(dst + kWTile + tc::sw128_off(b, a, 64)) = B[x];      // B^T: (n=out=b, k=in=a)
     *reinterpret_cast<float*>(dst + 2 * kWTile + tc::sw128_off(a, b, 64)) = B[x];  // B:   (n=a, k=b)
+    pack[kWtOff / 4 + b * 64 + a] = W[x];                                           // W^T[b][a] = W[a][b]
   }
   if (x < 64) {
     pack[3 * kWTile / 4 + x] = alpha[x];
@@ -138,21 +160,24 @@ __global__ void pack_msg_weights(const float* __restrict__ A, const float* __res
   }
 }
 
-// All threads: bulk-load `ntiles` weight tiles (+ alpha, beta) into sm[0..).
-// Returns after the copy landed (mbarrier transaction count).
-__device__ __forceinline__ void load_weights(uint8_t* sm, const float* pack, int ntiles, float* al, float* be,
+// Thread 0 arms `wbar` and bulk-loads `ntiles` weight tiles (+ alpha, beta,
+// and W^T when wts != nullptr); ends with a CTA barrier so every thread may
+// wait on `wbar` (tc::mbar_wait(wbar, 0)) — done just before the first MMA so
+// the copy overlaps the TMEM allocation and the first chunk's basis.
+__device__ __forceinline__ void load_weights(uint8_t* sm, const float* pack, int ntiles, float* al, float* be, float* wts,
                                              uint64_t* wbar) {
   if (threadIdx.x == 0) {
     tc::mbar_init(wbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     const uint32_t wbytes = static_cast<uint32_t>(ntiles) * kWTile;
-    tc::mbar_expect_tx(wbar, wbytes + 512);
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(pack);
+    tc::mbar_expect_tx(wbar, wbytes + 512 + (wts ? kWTile : 0u));
     tc::bulk_g2s(sm, pack, wbytes, wbar);
-    tc::bulk_g2s(al, reinterpret_cast<const uint8_t*>(pack) + 3 * kWTile, 256, wbar);
-    tc::bulk_g2s(be, reinterpret_cast<const uint8_t*>(pack) + 3 * kWTile + 256, 256, wbar);
+    tc::bulk_g2s(al, src + 3 * kWTile, 256, wbar);
+    tc::bulk_g2s(be, src + 3 * kWTile + 256, 256, wbar);
+    if (wts) tc::bulk_g2s(wts, src + kWtOff, kWTile, wbar);
   }
   __syncthreads();
-  tc::mbar_wait(wbar, 0);
 }
 
 __device__ __forceinline__ void st_em(uint8_t* t, int e, int f0, const float (&v)[FPT]) {
@@ -233,22 +258,26 @@ __device__ __forceinline__ void seg_write(int r0, const SegMap& m, float* const 
 
 // Row epilogue fused into the edge kernels: the tile's finished rows R (from
 // the segmented sums) times W^T:  out[r] = (base ? base[r] : 0) + R[r] W^T
-// (+ add[r]).  Rows staged in smem (rs[8][64]), W^T ([64][64] row-major) via L1.
+// (+ add[r]).  Rows staged in smem (rs[8][64]); W^T ([64][64] row-major) was
+// bulk-loaded into smem with the weight image.
 __device__ __forceinline__ void rows_times_wt(int r0, int r1, const SegMap& m, float accv, float* rs,
-                                              const float* __restrict__ Wt, const float* base, const float* __restrict__ add,
+                                              const float* Wts, const float* base, const float* __restrict__ add,
                                               float* out) {
   if (m.active && m.part == 0) rs[m.pair] = accv;
   __syncthreads();
   const int pidx = threadIdx.x;
   const int rl = pidx >> 6, c = pidx & 63, r = r0 + rl;
   if (r < r1) {
-    float o0 = 0.f, o1 = 0.f;
-#pragma unroll 8
-    for (int q = 0; q < 64; q += 2) {
-      o0 = fmaf(rs[rl * 64 + q], __ldg(Wt + q * 64 + c), o0);
-      o1 = fmaf(rs[rl * 64 + q + 1], __ldg(Wt + (q + 1) * 64 + c), o1);
+    float o[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int q = 0; q < 64; q += 4) {
+      const float4 x = *reinterpret_cast<const float4*>(rs + rl * 64 + q);
+      o[0] = fmaf(x.x, Wts[q * 64 + c], o[0]);
+      o[1] = fmaf(x.y, Wts[(q + 1) * 64 + c], o[1]);
+      o[2] = fmaf(x.z, Wts[(q + 2) * 64 + c], o[2]);
+      o[3] = fmaf(x.w, Wts[(q + 3) * 64 + c], o[3]);
     }
-    float y = o0 + o1;
+    float y = (o[0] + o[1]) + (o[2] + o[3]);
     if (base) y += base[(size_t)r * H + c];
     if (add) y += add[(size_t)r * H + c];
     out[(size_t)r * H + c] = y;
@@ -361,7 +390,7 @@ __global__ void __launch_bounds__(NT) msg_fe_tc(EdgeGeom g, const int* __restric
   c.sm = sm;
   c.mbar = &mbar;
   __shared__ __align__(8) uint64_t wbar;
-  load_weights(sm, p.pack, 2, al, be, &wbar);
+  load_weights(sm, p.pack, 2, al, be, nullptr, &wbar);
   setup(c, &tslot, 128);
   const uint32_t aW0 = tc::smem_u32(W0), aW1 = tc::smem_u32(W1), aT0 = tc::smem_u32(T0);
   const int f0 = FPT * c.q;
@@ -377,9 +406,10 @@ __global__ void __launch_bounds__(NT) msg_fe_tc(EdgeGeom g, const int* __restric
         basis(es.d, rc, f0, ph, dph);
         st_em(T0, c.e, f0, ph);
       }
+      tc::mbar_wait(&wbar, 0);  // weights landed (immediate after the first chunk)
       c.publish();
       if (threadIdx.x == 0) {
-        mma_tiles(c.tmem + TM_Z, aT0, 128, aW0, 64, 64, 128, false);
+        mma_tiles<128, 64, 64, 128>(c.tmem + TM_Z, aT0, aW0, false);
         tc::commit(c.mbar);
       }
       c.wait_mma();
@@ -395,7 +425,7 @@ __global__ void __launch_bounds__(NT) msg_fe_tc(EdgeGeom g, const int* __restric
       }
       c.publish();
       if (threadIdx.x == 0) {
-        mma_tiles(c.tmem + TM_ZP, aT0, 128, aW1, 64, 64, 128, false);
+        mma_tiles<128, 64, 64, 128>(c.tmem + TM_ZP, aT0, aW1, false);
         tc::commit(c.mbar);
       }
       c.wait_mma();
@@ -427,7 +457,7 @@ __global__ void __launch_bounds__(NT) msg_fe_tc(EdgeGeom g, const int* __restric
 // q_e + q_rev(e) = < am_i v_j + am_j v_i , w'_e >  (w' symmetric in e <-> rev e)
 __global__ void __launch_bounds__(NT) msg_ff_tc(EdgeGeom g, const int* __restrict__ tiles, int n_tiles, MsgParams p,
                                                float rc, const float* __restrict__ v, const float* __restrict__ am,
-                                               float* __restrict__ Y_out, float* __restrict__ F, const float* __restrict__ Wt,
+                                               float* __restrict__ Y_out, float* __restrict__ F,
                                                float* ah) {
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = align1024(sm_raw);
@@ -437,14 +467,15 @@ __global__ void __launch_bounds__(NT) msg_ff_tc(EdgeGeom g, const int* __restric
   uint8_t* T1 = T0 + kTile;   // phi' -> sdot
   float* al = reinterpret_cast<float*>(T1 + kTile);
   float* be = al + 64;
-  float* sq = be + 64;  // [NQ][TE] per-quarter force scalars
+  float* wts = be + 64;  // W^T [64][64] (fused row epilogue)
+  float* sq = wts + 64 * 64;  // [NQ][TE] per-quarter force scalars
   __shared__ __align__(8) uint64_t mbar;
   __shared__ uint32_t tslot;
   Ctx c;
   c.sm = sm;
   c.mbar = &mbar;
   __shared__ __align__(8) uint64_t wbar;
-  load_weights(sm, p.pack, 2, al, be, &wbar);
+  load_weights(sm, p.pack, 2, al, be, wts, &wbar);
   setup(c, &tslot, 256);
   const uint32_t aW0 = tc::smem_u32(W0), aW1 = tc::smem_u32(W1), aT0 = tc::smem_u32(T0), aT1 = tc::smem_u32(T1);
   const int f0 = FPT * c.q;
@@ -464,10 +495,11 @@ __global__ void __launch_bounds__(NT) msg_ff_tc(EdgeGeom g, const int* __restric
         st_em(T0, c.e, f0, ph);
         st_em(T1, c.e, f0, dph);
       }
+      tc::mbar_wait(&wbar, 0);  // weights landed (immediate after the first chunk)
       c.publish();
       if (threadIdx.x == 0) {
-        mma_tiles(c.tmem + TM_Z, aT0, 128, aW0, 64, 64, 128, false);
-        mma_tiles(c.tmem + TM_ZP, aT1, 128, aW0, 64, 64, 128, false);
+        mma_tiles<128, 64, 64, 128>(c.tmem + TM_Z, aT0, aW0, false);
+        mma_tiles<128, 64, 64, 128>(c.tmem + TM_ZP, aT1, aW0, false);
         tc::commit(c.mbar);
       }
       c.wait_mma();
@@ -486,8 +518,8 @@ __global__ void __launch_bounds__(NT) msg_ff_tc(EdgeGeom g, const int* __restric
       }
       c.publish();
       if (threadIdx.x == 0) {
-        mma_tiles(c.tmem + TM_G, aT0, 128, aW1, 64, 64, 128, false);
-        mma_tiles(c.tmem + TM_GP, aT1, 128, aW1, 64, 64, 128, false);
+        mma_tiles<128, 64, 64, 128>(c.tmem + TM_G, aT0, aW1, false);
+        mma_tiles<128, 64, 64, 128>(c.tmem + TM_GP, aT1, aW1, false);
         tc::commit(c.mbar);
       }
       c.wait_mma();
@@ -531,53 +563,58 @@ __global__ void __launch_bounds__(NT) msg_ff_tc(EdgeGeom g, const int* __restric
     float* const outs[1] = {Y_out};
     seg_write<1>(tr.r0, sg, outs, acc);
     if (fpart == 0 && fr < 3 * (tr.r1 - tr.r0)) F[3 * tr.r0 + fr] += fsum;
-    if (ah) rows_times_wt(tr.r0, tr.r1, sg, acc[0], reinterpret_cast<float*>(T1), Wt, ah, nullptr, ah);  // a_h += Y W^T
+    if (ah) rows_times_wt(tr.r0, tr.r1, sg, acc[0], reinterpret_cast<float*>(T1), wts, ah, nullptr, ah);  // a_h += Y W^T
   }
   teardown(c, 256);
 }
 
 // Write the CTA's weight-gradient partial [dA | dalpha | dB | dbeta] from the
 // M=64 TMEM accumulators (row r at lane (r/16)*32 + r%16) and the per-thread
-// column sums (xor-butterfly over the warp's 32 edges, then the 4 edge warps
-// of each feature quarter in fixed order through smem).
+// column sums.  Everything is staged in smem (`scratch` = the four operand
+// tiles, free by now) and leaves with coalesced float4 stores.
 __device__ __forceinline__ void write_partial(Ctx& c, float* part, uint8_t* scratch, const float (&cs_a)[FPT],
-                                              const float (&cs_b)[FPT]) {
+                                              const float (&cs_b)[FPT] TC_ARGS) {
+  constexpr int LDP = 68;  // padded row: the 8 rows of an STS.128 phase hit distinct banks
+  float* red = reinterpret_cast<float*>(scratch);  // [2][64][TE] column-sum staging (64 KB)
+  float* stg = red + 2 * 64 * TE;                  // [2][64][LDP] dA, dB rows
+  float* col = stg + 2 * 64 * LDP;                 // [2][64] dalpha, dbeta
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
+  TC_M();
   {
-    const int q = c.warp & 3;
     float va[FPT], vb[FPT];
     c.ld(TM_AG, va);
     c.ld(TM_BG, vb);
     if (c.lane < 16) {
-      const int r = 16 * q + c.lane;
-      float4* pa = reinterpret_cast<float4*>(part + r * H + FPT * c.q);
-      float4* pb = reinterpret_cast<float4*>(part + R * H + H + r * H + FPT * c.q);
+      const int r = 16 * (c.warp & 3) + c.lane;
+      float4* pa = reinterpret_cast<float4*>(stg + r * LDP + FPT * c.q);
+      float4* pb = reinterpret_cast<float4*>(stg + 64 * LDP + r * LDP + FPT * c.q);
 #pragma unroll
       for (int j = 0; j < FPT / 4; ++j) {
-        pa[j] = make_float4(va[4 * j], va[4 * j + 1], va[4 * j + 2], va[4 * j + 3]);  // dA[r][h]
-        pb[j] = make_float4(vb[4 * j], vb[4 * j + 1], vb[4 * j + 2], vb[4 * j + 3]);  // dB[k][h]
+        pa[j] = make_float4(va[4 * j], va[4 * j + 1], va[4 * j + 2], va[4 * j + 3]);
+        pb[j] = make_float4(vb[4 * j], vb[4 * j + 1], vb[4 * j + 2], vb[4 * j + 3]);
       }
     }
   }
+  TC_M();
   // column sums: [feature][edge] staging (conflict-free: consecutive edges),
-  // then 8 threads per feature sum 16 contiguous edges each and combine by an
-  // xor butterfly — a fixed order, so the partial is deterministic.
-  float* red = reinterpret_cast<float*>(scratch);  // [2][64][TE]
+  // then 8 threads per feature sum 16 edges each (4 float4, conflict-free) and
+  // combine by an xor butterfly — a fixed order, so the partial is deterministic.
 #pragma unroll
   for (int j = 0; j < FPT; ++j) {
     red[(FPT * c.q + j) * TE + c.e] = cs_a[j];
     red[64 * TE + (FPT * c.q + j) * TE + c.e] = cs_b[j];
   }
   __syncthreads();
+  TC_M();
   {
     const int f = threadIdx.x >> 3, prt = threadIdx.x & 7;
     float sa = 0.f, sb = 0.f;
 #pragma unroll
     for (int k = 0; k < TE / 32; ++k) {
-      const float4 x = *reinterpret_cast<const float4*>(red + f * TE + 16 * prt + 4 * k);
-      const float4 y = *reinterpret_cast<const float4*>(red + 64 * TE + f * TE + 16 * prt + 4 * k);
+      const float4 x = *reinterpret_cast<const float4*>(red + f * TE + 32 * k + 4 * prt);
+      const float4 y = *reinterpret_cast<const float4*>(red + 64 * TE + f * TE + 32 * k + 4 * prt);
       sa += (x.x + x.y) + (x.z + x.w);
       sb += (y.x + y.y) + (y.z + y.w);
     }
@@ -587,9 +624,27 @@ __device__ __forceinline__ void write_partial(Ctx& c, float* part, uint8_t* scra
       sb += __shfl_xor_sync(0xffffffffu, sb, o);
     }
     if (prt == 0) {
-      part[R * H + f] = sa;
-      part[R * H + H + H * H + f] = sb;
+      col[f] = sa;
+      col[64 + f] = sb;
     }
+  }
+  __syncthreads();
+  TC_M();
+  // coalesced copy-out: PE / 4 = 2080 float4 in global order
+  float4* out = reinterpret_cast<float4*>(part);
+  for (int k = threadIdx.x; k < PE / 4; k += NT) {
+    float4 v;
+    if (k < 1024) {
+      v = *reinterpret_cast<const float4*>(stg + (k >> 4) * LDP + 4 * (k & 15));
+    } else if (k < 1040) {
+      v = *reinterpret_cast<const float4*>(col + 4 * (k - 1024));
+    } else if (k < 2064) {
+      const int kk = k - 1040;
+      v = *reinterpret_cast<const float4*>(stg + 64 * LDP + (kk >> 4) * LDP + 4 * (kk & 15));
+    } else {
+      v = *reinterpret_cast<const float4*>(col + 64 + 4 * (k - 2064));
+    }
+    out[k] = v;
   }
 }
 
@@ -599,7 +654,7 @@ __device__ __forceinline__ void write_partial(Ctx& c, float* part, uint8_t* scra
 __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int* __restrict__ tiles, int n_tiles, MsgParams p,
                                                   float rc, const float* __restrict__ v, const float* __restrict__ bm,
                                                   float* __restrict__ Yb_out, float* __restrict__ partial,
-                                                  const float* __restrict__ Wt, const float* __restrict__ inj, float* bh) {
+                                                  const float* __restrict__ inj, float* bh) {
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = align1024(sm_raw);
   TC_DECL;
@@ -613,13 +668,14 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int* __rest
   uint8_t* T3 = T2 + kTile;
   float* al = reinterpret_cast<float*>(T3 + kTile);
   float* be = al + 64;
+  float* wts = be + 64;  // W^T [64][64] (fused row epilogue)
   __shared__ __align__(8) uint64_t mbar;
   __shared__ uint32_t tslot;
   Ctx c;
   c.sm = sm;
   c.mbar = &mbar;
   __shared__ __align__(8) uint64_t wbar;
-  load_weights(sm, p.pack, 3, al, be, &wbar);
+  load_weights(sm, p.pack, 3, al, be, wts, &wbar);
   TC_M();
   setup(c, &tslot, 512);
   TC_M();
@@ -642,9 +698,10 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int* __rest
         basis(es.d, rc, f0, ph, dph);
         st_em(T0, c.e, f0, ph);
       }
+      tc::mbar_wait(&wbar, 0);  // weights landed (immediate after the first chunk)
       c.publish();
       if (threadIdx.x == 0) {
-        mma_tiles(c.tmem + TM_Z, aT0, 128, aW0, 64, 64, 128, false);
+        mma_tiles<128, 64, 64, 128>(c.tmem + TM_Z, aT0, aW0, false);
         tc::commit(c.mbar);
       }
       TC_M();
@@ -663,7 +720,7 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int* __rest
       }
       c.publish();
       if (threadIdx.x == 0) {
-        mma_tiles(c.tmem + TM_G, aT0, 128, aW1, 64, 64, 128, false);
+        mma_tiles<128, 64, 64, 128>(c.tmem + TM_G, aT0, aW1, false);
         tc::commit(c.mbar);
       }
       TC_M();
@@ -692,8 +749,8 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int* __rest
       c.publish();
       TC_M();
       if (threadIdx.x == 0) {
-        mma_tiles(c.tmem + TM_BG, aT1, 64, aT2, 64, 128, 64, !first);
-        mma_tiles(c.tmem + TM_G, aT3, 128, aW2, 64, 64, 128, false);
+        mma_tiles<64, 64, 128, 64>(c.tmem + TM_BG, aT1, aT2, !first);
+        mma_tiles<128, 64, 64, 128>(c.tmem + TM_G, aT3, aW2, false);
         tc::commit(c.mbar);
       }
       TC_M();
@@ -722,7 +779,7 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int* __rest
       }
       c.publish();
       if (threadIdx.x == 0) {
-        mma_tiles(c.tmem + TM_AG, aT0, 64, aT2, 64, 128, 64, !first);
+        mma_tiles<64, 64, 128, 64>(c.tmem + TM_AG, aT0, aT2, !first);
         tc::commit(c.mbar);
       }
       TC_M();
@@ -735,7 +792,7 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int* __rest
     float* const outs[1] = {Yb_out};
     seg_write<1>(tr.r0, sg, outs, acc);
     TC_M();
-    if (bh) rows_times_wt(tr.r0, tr.r1, sg, acc[0], reinterpret_cast<float*>(T1), Wt, bh, inj, bh);  // b_h += Yb W^T + inj
+    if (bh) rows_times_wt(tr.r0, tr.r1, sg, acc[0], reinterpret_cast<float*>(T1), wts, bh, inj, bh);  // b_h += Yb W^T + inj
     TC_M();
   }
   float* part = partial + (size_t)blockIdx.x * PE;
@@ -744,7 +801,7 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int* __rest
     teardown(c, 512);
     return;
   }
-  write_partial(c, part, T0, cs_a, cs_b);
+  write_partial(c, part, T0, cs_a, cs_b TC_PASS);
   TC_M();
   teardown(c, 512);
   TC_M();
@@ -758,11 +815,12 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
                                                   float rc, const float* __restrict__ v, const float* __restrict__ vdot,
                                                   const float* __restrict__ am, const float* __restrict__ Fbar,
                                                   float* __restrict__ mdot_out, float* __restrict__ X_out,
-                                                  float* __restrict__ partial, const float* __restrict__ Wt,
+                                                  float* __restrict__ partial,
                                                   float* __restrict__ inj) {
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = align1024(sm_raw);
   TC_DECL;
+  TC_SPAN_BEGIN;
   TC_M();
   uint8_t* W0 = sm;
   uint8_t* W1 = W0 + kWTile;
@@ -773,13 +831,16 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
   uint8_t* T3 = T2 + kTile;
   float* al = reinterpret_cast<float*>(T3 + kTile);
   float* be = al + 64;
+  float* wts = be + 64;  // W^T [64][64] (fused row epilogue)
   __shared__ __align__(8) uint64_t mbar;
   __shared__ uint32_t tslot;
   Ctx c;
   c.sm = sm;
   c.mbar = &mbar;
   __shared__ __align__(8) uint64_t wbar;
-  load_weights(sm, p.pack, 3, al, be, &wbar);
+#ifndef JANUS_TC_LATEW
+  load_weights(sm, p.pack, 3, al, be, wts, &wbar);
+#endif
   TC_M();
   setup(c, &tslot, 512);
   TC_M();
@@ -797,16 +858,30 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
     for (int c0 = tr.e0; c0 < tr.e1; c0 += TE) {
       const int ne = min(TE, tr.e1 - c0);
       const ES es = edge_sc(g, c0, ne, c.e);
+#ifdef JANUS_TC_TRACE
+      {
+        float dmy;
+        asm volatile("mov.b32 %0, %1;" : "=f"(dmy) : "f"(es.d));
+        TC_M();
+      }
+#ifdef JANUS_TC_LATEW
+      if (first) load_weights(sm, p.pack, 3, al, be, wts, &wbar);
+#endif
+#endif
       {
         float ph[FPT], dph[FPT];
         basis(es.d, rc, f0, ph, dph);
+        TC_M();
         st_em(T0, c.e, f0, ph);
         st_em(T1, c.e, f0, dph);
       }
+      TC_M();
+      tc::mbar_wait(&wbar, 0);
+      TC_M();  // weights landed (immediate after the first chunk)
       c.publish();
       if (threadIdx.x == 0) {
-        mma_tiles(c.tmem + TM_Z, aT0, 128, aW0, 64, 64, 128, false);
-        mma_tiles(c.tmem + TM_ZP, aT1, 128, aW0, 64, 64, 128, false);
+        mma_tiles<128, 64, 64, 128>(c.tmem + TM_Z, aT0, aW0, false);
+        mma_tiles<128, 64, 64, 128>(c.tmem + TM_ZP, aT1, aW0, false);
         tc::commit(c.mbar);
       }
       TC_M();
@@ -829,8 +904,8 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
       }
       c.publish();
       if (threadIdx.x == 0) {
-        mma_tiles(c.tmem + TM_G, aT0, 128, aW1, 64, 64, 128, false);
-        mma_tiles(c.tmem + TM_GP, aT1, 128, aW1, 64, 64, 128, false);
+        mma_tiles<128, 64, 64, 128>(c.tmem + TM_G, aT0, aW1, false);
+        mma_tiles<128, 64, 64, 128>(c.tmem + TM_GP, aT1, aW1, false);
         tc::commit(c.mbar);
       }
       TC_M();
@@ -839,6 +914,13 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
       float mu[FPT], nu[FPT];
       {
         const float qb = edge_qbar(g, es, Fbar);
+#ifdef JANUS_TC_TRACE
+        {
+          float dmy;
+          asm volatile("mov.b32 %0, %1;" : "=f"(dmy) : "f"(qb));
+          TC_M();
+        }
+#endif
         float gg[FPT], gp[FPT];
         float pm[FPT], px[FPT];
         float4 a4[FPT / 4], aj4[FPT / 4], v4[FPT / 4], d4[FPT / 4];
@@ -851,6 +933,7 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
         }
         c.ld(TM_G, gg);
         c.ld(TM_GP, gp);
+        TC_M();
 #pragma unroll
         for (int q = 0; q < FPT / 4; ++q) {
           const float ai[4] = {a4[q].x, a4[q].y, a4[q].z, a4[q].w}, aj[4] = {aj4[q].x, aj4[q].y, aj4[q].z, aj4[q].w};
@@ -867,13 +950,16 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
             nu[k] = qb * es.c * rho;
           }
         }
+        TC_M();
         st_pl(T0, c.e, f0, pm);
         st_pl(T1, c.e, f0, px);
 #pragma unroll
         for (int q = 0; q < FPT; ++q) cs_b[q] += mu[q];
       }
+      TC_M();
       tc::fence_before();
       __syncthreads();
+      TC_M();
       {
         const uint8_t* const tl[2] = {T0, T1};
         seg_rows<2>(g, tr.r0, c0, ne, tl, sg, acc);
@@ -884,8 +970,8 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
       st_fm(T1, c.e, f0, nu);  // nu^T
       c.publish();
       if (threadIdx.x == 0) {  // dB += s^T mu + sdot^T nu
-        mma_tiles(c.tmem + TM_BG, aT2, 64, aT0, 64, 128, 64, !first);
-        mma_tiles(c.tmem + TM_BG, aT3, 64, aT1, 64, 128, 64, true);
+        mma_tiles<64, 64, 128, 64>(c.tmem + TM_BG, aT2, aT0, !first);
+        mma_tiles<64, 64, 128, 64>(c.tmem + TM_BG, aT3, aT1, true);
         tc::commit(c.mbar);
       }
       TC_M();
@@ -895,8 +981,8 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
       st_em(T3, c.e, f0, nu);  // nu
       c.publish();
       if (threadIdx.x == 0) {
-        mma_tiles(c.tmem + TM_G, aT2, 128, aW2, 64, 64, 128, false);   // sbar
-        mma_tiles(c.tmem + TM_GP, aT3, 128, aW2, 64, 64, 128, false);  // sdotbar
+        mma_tiles<128, 64, 64, 128>(c.tmem + TM_G, aT2, aW2, false);   // sbar
+        mma_tiles<128, 64, 64, 128>(c.tmem + TM_GP, aT3, aW2, false);  // sdotbar
         tc::commit(c.mbar);
       }
       TC_M();
@@ -926,8 +1012,8 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
       }
       c.publish();
       if (threadIdx.x == 0) {  // dA += phi^T zbar + phi'^T zbar'
-        mma_tiles(c.tmem + TM_AG, aT0, 64, aT2, 64, 128, 64, !first);
-        mma_tiles(c.tmem + TM_AG, aT1, 64, aT3, 64, 128, 64, true);
+        mma_tiles<64, 64, 128, 64>(c.tmem + TM_AG, aT0, aT2, !first);
+        mma_tiles<64, 64, 128, 64>(c.tmem + TM_AG, aT1, aT3, true);
         tc::commit(c.mbar);
       }
       TC_M();
@@ -940,7 +1026,7 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
     float* const outs[2] = {mdot_out, X_out};
     seg_write<2>(tr.r0, sg, outs, acc);
     TC_M();
-    if (inj) rows_times_wt(tr.r0, tr.r1, sg, acc[1], reinterpret_cast<float*>(T1), Wt, nullptr, nullptr, inj);  // hbar^F = X W^T
+    if (inj) rows_times_wt(tr.r0, tr.r1, sg, acc[1], reinterpret_cast<float*>(T1), wts, nullptr, nullptr, inj);  // hbar^F = X W^T
     TC_M();
   }
   float* part = partial + (size_t)blockIdx.x * PE;
@@ -949,18 +1035,19 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
     teardown(c, 512);
     return;
   }
-  write_partial(c, part, T0, cs_a, cs_b);
+  write_partial(c, part, T0, cs_a, cs_b TC_PASS);
   TC_M();
   teardown(c, 512);
   TC_M();
+  TC_SPAN_END("bf");
   TC_DUMP("bf");
 }
 
-constexpr size_t kSmallBytes = sizeof(float) * (128 + NQ * TE) + 1024;  // alpha, beta, FF force scalars
+constexpr size_t kSmallBytes = sizeof(float) * (128 + NQ * TE) + 1024;  // alpha, beta, FF force scalars, 1 KB alignment slack
 constexpr size_t fe_smem() { return 2 * kWTile + 2 * kTile + kSmallBytes; }
-constexpr size_t ff_smem() { return 2 * kWTile + 2 * kTile + kSmallBytes; }
-constexpr size_t be_smem() { return 3 * kWTile + 4 * kTile + kSmallBytes; }
-constexpr size_t bf_smem() { return 3 * kWTile + 4 * kTile + kSmallBytes; }
+constexpr size_t ff_smem() { return 3 * kWTile + 2 * kTile + kSmallBytes; }  // + W^T
+constexpr size_t be_smem() { return 4 * kWTile + 4 * kTile + kSmallBytes; }
+constexpr size_t bf_smem() { return 4 * kWTile + 4 * kTile + kSmallBytes; }
 
 }  // namespace edge_tc
 }  // namespace janus

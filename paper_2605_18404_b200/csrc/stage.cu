@@ -166,7 +166,8 @@ void refresh_transposes(janus_stage* st, cudaStream_t s) {
       case kMsg:
         node::transpose_kernel<kH><<<b, 256, 0, s>>>(P + R * H + H, t);
         node::transpose_kernel<kH><<<b, 256, 0, s>>>(P + R * H + H + H * H + H, t + H * H);
-        edge_tc::pack_msg_weights<<<b, 256, 0, s>>>(P, P + R * H, P + R * H + H, P + R * H + H + H * H, t + 2 * H * H);
+        edge_tc::pack_msg_weights<<<b, 256, 0, s>>>(P, P + R * H, P + R * H + H, P + R * H + H + H * H,
+                                                     P + R * H + H + H * H + H, t + 2 * H * H);
         break;
       case kUpd:
         node::transpose_kernel<kH><<<b, 256, 0, s>>>(P, t);
@@ -542,7 +543,7 @@ void stage_ff(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
         if (u == st->u1 - 1) copy(s, b.ff_a, wm, NH);  // a_m arrived through the ADJ_IN port
         if (g.n_tiles > 0 && use_tc(st)) {  // a_h += Y W^T fused into the tile epilogue
           edge_tc::msg_ff_tc<<<g.n_tiles_tc, edge_tc::NT, edge_tc::ff_smem(), s>>>(eg, g.tile_row_tc, g.n_tiles_tc, msg_params(st, u),
-                                                                                 st->m.r_c, b.v, b.ff_a, b.ff_Y, sl.F, T + H * H, wh);
+                                                                                 st->m.r_c, b.v, b.ff_a, b.ff_Y, sl.F, wh);
         } else {
           if (g.n_tiles > 0)
             edge::msg_ff_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::ff_smem<kH, kR>(), s>>>(eg, msg_params(st, u), st->m.r_c, b.v, b.ff_a, b.ff_Y, sl.F);
@@ -605,14 +606,14 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
           const int grid = tc_grid(g);
           edge_tc::msg_bf_tc<<<grid, edge_tc::NT, edge_tc::bf_smem(), s>>>(eg, g.tile_row_tc, g.n_tiles_tc, msg_params(st, u),
                                                                           st->m.r_c, b.v, sc.s1, b.ff_a, Fbar, am, sc.s2,
-                                                                          sc.partial, T + H * H, b.inj);  // + hbar^F = X W^T
+                                                                          sc.partial, b.inj);  // + hbar^F = X W^T
           JANUS_LAUNCH_CHECK("msg_bf_tc");
-          edge::reduce_partials_kernel<<<blocks(EC::PE, 256), 256, 0, s>>>(sc.partial, grid, EC::PE, G2);
+          edge::reduce_partials_kernel<<<edge::reduce_grid(EC::PE), 256, 0, s>>>(sc.partial, grid, EC::PE, G2);
         } else if (g.n_tiles > 0) {
           edge::msg_bf_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::bf_smem<kH, kR>(), s>>>(
               eg, msg_params(st, u), st->m.r_c, b.v, sc.s1, b.ff_a, Fbar, am, sc.s2, sc.partial);
           JANUS_LAUNCH_CHECK("msg_bf");
-          edge::reduce_partials_kernel<<<blocks(EC::PE, 256), 256, 0, s>>>(sc.partial, g.n_tiles, EC::PE, G2);
+          edge::reduce_partials_kernel<<<edge::reduce_grid(EC::PE), 256, 0, s>>>(sc.partial, g.n_tiles, EC::PE, G2);
         } else {
           JANUS_CUDA(cudaMemsetAsync(am, 0, sizeof(float) * NH, s));
           JANUS_CUDA(cudaMemsetAsync(sc.s2, 0, sizeof(float) * NH, s));
@@ -706,15 +707,15 @@ void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only, 
         if (g.n_tiles > 0 && use_tc(st)) {
           const int grid = tc_grid(g);
           edge_tc::msg_be_tc<<<grid, edge_tc::NT, edge_tc::be_smem(), s>>>(eg, g.tile_row_tc, g.n_tiles_tc, msg_params(st, u),
-                                                                          st->m.r_c, b.v, bm, sc.s1, sc.partial, T + H * H,
+                                                                          st->m.r_c, b.v, bm, sc.s1, sc.partial,
                                                                           b.inj, bh);  // + b_h += Yb W^T + hbar^F
           JANUS_LAUNCH_CHECK("msg_be_tc");
-          edge::reduce_partials_kernel<<<blocks(EC::PE, 256), 256, 0, s>>>(sc.partial, grid, EC::PE, G1);
+          edge::reduce_partials_kernel<<<edge::reduce_grid(EC::PE), 256, 0, s>>>(sc.partial, grid, EC::PE, G1);
         } else if (g.n_tiles > 0) {
           edge::msg_be_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::be_smem<kH, kR>(), s>>>(
               eg, msg_params(st, u), st->m.r_c, b.v, bm, sc.s1, sc.partial);
           JANUS_LAUNCH_CHECK("msg_be");
-          edge::reduce_partials_kernel<<<blocks(EC::PE, 256), 256, 0, s>>>(sc.partial, g.n_tiles, EC::PE, G1);
+          edge::reduce_partials_kernel<<<edge::reduce_grid(EC::PE), 256, 0, s>>>(sc.partial, g.n_tiles, EC::PE, G1);
         } else {
           JANUS_CUDA(cudaMemsetAsync(sc.s1, 0, sizeof(float) * NH, s));
         }
@@ -821,14 +822,14 @@ void stage_time_edge_kernel(janus_stage* st, int which, int mb, int slot, int it
           edge_tc::msg_fe_tc<<<g.n_tiles_tc, edge_tc::NT, edge_tc::fe_smem(), s>>>(eg, g.tile_row_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, sc.s3);
           break;
         case 1:
-          edge_tc::msg_ff_tc<<<g.n_tiles_tc, edge_tc::NT, edge_tc::ff_smem(), s>>>(eg, g.tile_row_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, b.ff_a, sc.s3, sc.s5, nullptr, nullptr);
+          edge_tc::msg_ff_tc<<<g.n_tiles_tc, edge_tc::NT, edge_tc::ff_smem(), s>>>(eg, g.tile_row_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, b.ff_a, sc.s3, sc.s5, nullptr);
           break;
         case 2:
           edge_tc::msg_bf_tc<<<grid, edge_tc::NT, edge_tc::bf_smem(), s>>>(eg, g.tile_row_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, sc.s1, b.ff_a,
-                                                                          sl.Fbar, sc.s3, sc.s4, sc.partial, nullptr, nullptr);
+                                                                          sl.Fbar, sc.s3, sc.s4, sc.partial, nullptr);
           break;
         default:
-          edge_tc::msg_be_tc<<<grid, edge_tc::NT, edge_tc::be_smem(), s>>>(eg, g.tile_row_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, sc.s2, sc.s3, sc.partial, nullptr, nullptr, nullptr);
+          edge_tc::msg_be_tc<<<grid, edge_tc::NT, edge_tc::be_smem(), s>>>(eg, g.tile_row_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, sc.s2, sc.s3, sc.partial, nullptr, nullptr);
           break;
       }
       return;
