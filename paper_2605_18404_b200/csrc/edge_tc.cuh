@@ -206,6 +206,14 @@ __device__ __forceinline__ void st_pl(uint8_t* t, int e, int f0, const float (&v
     *reinterpret_cast<float4*>(t + off_pl(e, f0 + 4 * j)) = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
 }
 
+struct TileRange {
+  int r0, r1, e0, e1;
+};
+__device__ __forceinline__ TileRange tile_range(const int4* __restrict__ tiles, int t) {
+  const int4 v = __ldg(tiles + t);
+  return TileRange{v.x, v.y, v.z, v.w};
+}
+
 // Deterministic segmented row sums of NA plain tiles over one chunk.  The
 // tile's nr rows x 64 features are spread over the CTA with `split` threads
 // per (row, feature) pair (split = 8 / nr rounded down to a power of two):
@@ -215,15 +223,20 @@ __device__ __forceinline__ void st_pl(uint8_t* t, int e, int f0, const float (&v
 // which leaves the bit-identical total in every lane of the group.
 struct SegMap {
   int split, span, pair, part;
+  int rb, re;  // this pair's row: CSR edge range (loaded once per tile, off the chunk's critical path)
   bool active;
 };
-__device__ __forceinline__ SegMap seg_map(int nr) {
+__device__ __forceinline__ SegMap seg_map(const EdgeGeom& g, const TileRange& tr) {
   SegMap m;
+  const int nr = tr.r1 - tr.r0;
   m.split = nr <= 1 ? 8 : nr <= 2 ? 4 : nr <= 4 ? 2 : 1;
   m.span = nr * 64;
   m.part = static_cast<int>(threadIdx.x) & (m.split - 1);
   m.pair = static_cast<int>(threadIdx.x) / m.split;
   m.active = m.pair < m.span;
+  const int r = tr.r0 + (m.active ? (m.pair >> 6) : 0);
+  m.rb = __ldg(g.row_ptr + r);
+  m.re = __ldg(g.row_ptr + r + 1);
   return m;
 }
 
@@ -231,8 +244,8 @@ template <int NA>
 __device__ __forceinline__ void seg_rows(const EdgeGeom& g, int r0, int c0, int ne, const uint8_t* const (&tiles)[NA],
                                          const SegMap& m, float (&acc)[NA]) {
   if (!m.active) return;
-  const int r = r0 + (m.pair >> 6), f = m.pair & 63;
-  const int eb = max(g.row_ptr[r], c0), ee = min(g.row_ptr[r + 1], c0 + ne);
+  const int f = m.pair & 63;
+  const int eb = max(m.rb, c0), ee = min(m.re, c0 + ne);
   for (int x = eb + m.part; x < ee; x += m.split) {
     const uint32_t o = off_pl(x - c0, f);
 #pragma unroll
@@ -312,18 +325,6 @@ __device__ __forceinline__ void basis(float d, float rc, int f0, float (&p)[FPT]
   }
 }
 
-struct TileRange {
-  int r0, r1, e0, e1;
-};
-__device__ __forceinline__ TileRange tile_range(const EdgeGeom& g, const int* tile_row, int t) {
-  TileRange r;
-  r.r0 = tile_row[t];
-  r.r1 = tile_row[t + 1];
-  r.e0 = g.row_ptr[r.r0];
-  r.e1 = g.row_ptr[r.r1];
-  return r;
-}
-
 __device__ __forceinline__ void setup(Ctx& c, uint32_t* tmem_slot, uint32_t ncols) {
   c.e = threadIdx.x & 127;
   c.q = threadIdx.x >> 7;
@@ -374,10 +375,13 @@ __device__ __forceinline__ float fsig(float x) { return __fdividef(1.0f, 1.0f + 
 
 // ----------------------------------------------------------------------- FE
 // m_i = sum_{e in row i} w_e * v[col e], w = c (SiLU(phi A + alpha) B + beta)
-__global__ void __launch_bounds__(NT) msg_fe_tc(EdgeGeom g, const int* __restrict__ tiles, int n_tiles, MsgParams p,
+__global__ void __launch_bounds__(NT) msg_fe_tc(EdgeGeom g, const int4* __restrict__ tiles, int n_tiles, MsgParams p,
                                                float rc, const float* __restrict__ v, float* __restrict__ m_out) {
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = align1024(sm_raw);
+  TC_DECL;
+  TC_SPAN_BEGIN;
+  TC_M();
   uint8_t* W0 = sm;               // A^T  (n = h, k = r)
   uint8_t* W1 = W0 + kWTile;      // B^T  (n = out, k = in)
   uint8_t* T0 = W1 + kWTile;      // phi -> s
@@ -391,16 +395,25 @@ __global__ void __launch_bounds__(NT) msg_fe_tc(EdgeGeom g, const int* __restric
   c.mbar = &mbar;
   __shared__ __align__(8) uint64_t wbar;
   load_weights(sm, p.pack, 2, al, be, nullptr, &wbar);
+  TC_M();
   setup(c, &tslot, 128);
+  TC_M();
   const uint32_t aW0 = tc::smem_u32(W0), aW1 = tc::smem_u32(W1), aT0 = tc::smem_u32(T0);
   const int f0 = FPT * c.q;
   for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-    const TileRange tr = tile_range(g, tiles, t);
-    const SegMap sg = seg_map(tr.r1 - tr.r0);
+    const TileRange tr = tile_range(tiles, t);
+    const SegMap sg = seg_map(g, tr);
     float acc[1] = {};
     for (int c0 = tr.e0; c0 < tr.e1; c0 += TE) {
       const int ne = min(TE, tr.e1 - c0);
       const ES es = edge_sc(g, c0, ne, c.e);
+#ifdef JANUS_TC_TRACE
+      {
+        float dmy;
+        asm volatile("mov.b32 %0, %1;" : "=f"(dmy) : "f"(es.d));
+        TC_M();
+      }
+#endif
       {
         float ph[FPT], dph[FPT];
         basis(es.d, rc, f0, ph, dph);
@@ -412,7 +425,9 @@ __global__ void __launch_bounds__(NT) msg_fe_tc(EdgeGeom g, const int* __restric
         mma_tiles<128, 64, 64, 128>(c.tmem + TM_Z, aT0, aW0, false);
         tc::commit(c.mbar);
       }
+      TC_M();
       c.wait_mma();
+      TC_M();
       {
         float z[FPT];
         c.ld(TM_Z, z);
@@ -428,7 +443,9 @@ __global__ void __launch_bounds__(NT) msg_fe_tc(EdgeGeom g, const int* __restric
         mma_tiles<128, 64, 64, 128>(c.tmem + TM_ZP, aT0, aW1, false);
         tc::commit(c.mbar);
       }
+      TC_M();
       c.wait_mma();
+      TC_M();
       {
         float gg[FPT], vj[FPT];
         gather32(v, es.j, f0, vj);
@@ -441,21 +458,27 @@ __global__ void __launch_bounds__(NT) msg_fe_tc(EdgeGeom g, const int* __restric
       __syncthreads();
       {
         const uint8_t* const tl[1] = {T1};
+        TC_M();
         seg_rows<1>(g, tr.r0, c0, ne, tl, sg, acc);
       }
+      TC_M();
       __syncthreads();
     }
     seg_finish<1>(sg, acc);
     float* const outs[1] = {m_out};
     seg_write<1>(tr.r0, sg, outs, acc);
   }
+  TC_M();
   teardown(c, 128);
+  TC_M();
+  TC_SPAN_END("fe");
+  TC_DUMP("fe");
 }
 
 // ----------------------------------------------------------------------- FF
 // Y_i = sum w_e * am[col e];  F_i += sum_e (q_e + q_rev(e)) u_e with
 // q_e + q_rev(e) = < am_i v_j + am_j v_i , w'_e >  (w' symmetric in e <-> rev e)
-__global__ void __launch_bounds__(NT) msg_ff_tc(EdgeGeom g, const int* __restrict__ tiles, int n_tiles, MsgParams p,
+__global__ void __launch_bounds__(NT) msg_ff_tc(EdgeGeom g, const int4* __restrict__ tiles, int n_tiles, MsgParams p,
                                                float rc, const float* __restrict__ v, const float* __restrict__ am,
                                                float* __restrict__ Y_out, float* __restrict__ F,
                                                float* ah) {
@@ -482,10 +505,12 @@ __global__ void __launch_bounds__(NT) msg_ff_tc(EdgeGeom g, const int* __restric
   // force sums: 8 lanes per (row, component), interleaved edges
   const int fr = threadIdx.x >> 3, fpart = threadIdx.x & 7;
   for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-    const TileRange tr = tile_range(g, tiles, t);
-    const SegMap sg = seg_map(tr.r1 - tr.r0);
+    const TileRange tr = tile_range(tiles, t);
+    const SegMap sg = seg_map(g, tr);
     float acc[1] = {};
     float fsum = 0.f;
+    const bool frow = fr < 3 * (tr.r1 - tr.r0);
+    const int fb = frow ? __ldg(g.row_ptr + tr.r0 + fr / 3) : 0, fe = frow ? __ldg(g.row_ptr + tr.r0 + fr / 3 + 1) : 0;
     for (int c0 = tr.e0; c0 < tr.e1; c0 += TE) {
       const int ne = min(TE, tr.e1 - c0);
       const ES es = edge_sc(g, c0, ne, c.e);
@@ -548,9 +573,9 @@ __global__ void __launch_bounds__(NT) msg_ff_tc(EdgeGeom g, const int* __restric
       {
         const uint8_t* const tl[1] = {T0};
         seg_rows<1>(g, tr.r0, c0, ne, tl, sg, acc);
-        if (fr < 3 * (tr.r1 - tr.r0)) {
-          const int r = tr.r0 + fr / 3, comp = fr % 3;
-          const int eb = max(g.row_ptr[r], c0), ee = min(g.row_ptr[r + 1], c0 + ne);
+        if (frow) {
+          const int comp = fr % 3;
+          const int eb = max(fb, c0), ee = min(fe, c0 + ne);
           for (int x = eb + fpart; x < ee; x += 8)
             fsum = fmaf((sq[x - c0] + sq[TE + x - c0]) + (sq[2 * TE + x - c0] + sq[3 * TE + x - c0]), g.u[3 * x + comp], fsum);
         }
@@ -562,7 +587,7 @@ __global__ void __launch_bounds__(NT) msg_ff_tc(EdgeGeom g, const int* __restric
     for (int o = 1; o < 8; o <<= 1) fsum += __shfl_xor_sync(0xffffffffu, fsum, o);
     float* const outs[1] = {Y_out};
     seg_write<1>(tr.r0, sg, outs, acc);
-    if (fpart == 0 && fr < 3 * (tr.r1 - tr.r0)) F[3 * tr.r0 + fr] += fsum;
+    if (fpart == 0 && frow) F[3 * tr.r0 + fr] += fsum;
     if (ah) rows_times_wt(tr.r0, tr.r1, sg, acc[0], reinterpret_cast<float*>(T1), wts, ah, nullptr, ah);  // a_h += Y W^T
   }
   teardown(c, 256);
@@ -651,7 +676,7 @@ __device__ __forceinline__ void write_partial(Ctx& c, float* part, uint8_t* scra
 // ----------------------------------------------------------------------- BE
 // Yb_i = sum w_e * bm[col e]; gbar = c bm_i v_j; dB = s^T gbar; dbeta = sum gbar;
 // zbar = (gbar B^T) SiLU'(z); dA = phi^T zbar; dalpha = sum zbar.
-__global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int* __restrict__ tiles, int n_tiles, MsgParams p,
+__global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int4* __restrict__ tiles, int n_tiles, MsgParams p,
                                                   float rc, const float* __restrict__ v, const float* __restrict__ bm,
                                                   float* __restrict__ Yb_out, float* __restrict__ partial,
                                                   const float* __restrict__ inj, float* bh) {
@@ -687,8 +712,8 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int* __rest
   bool first = true;
   const int f0 = FPT * c.q;
   for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-    const TileRange tr = tile_range(g, tiles, t);
-    const SegMap sg = seg_map(tr.r1 - tr.r0);
+    const TileRange tr = tile_range(tiles, t);
+    const SegMap sg = seg_map(g, tr);
     float acc[1] = {};
     for (int c0 = tr.e0; c0 < tr.e1; c0 += TE) {
       const int ne = min(TE, tr.e1 - c0);
@@ -811,7 +836,7 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int* __rest
 // ----------------------------------------------------------------------- BF
 // Second-order term.  Outputs: mdot_i = sum_e qb w'_e v_j + w_e vdot_j,
 // X_i = sum_e qb w'_e am_j, and the partial [dA | dalpha | dB | dbeta].
-__global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __restrict__ tiles, int n_tiles, MsgParams p,
+__global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int4* __restrict__ tiles, int n_tiles, MsgParams p,
                                                   float rc, const float* __restrict__ v, const float* __restrict__ vdot,
                                                   const float* __restrict__ am, const float* __restrict__ Fbar,
                                                   float* __restrict__ mdot_out, float* __restrict__ X_out,
@@ -852,8 +877,8 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
   bool first = true;
   const int f0 = FPT * c.q;
   for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-    const TileRange tr = tile_range(g, tiles, t);
-    const SegMap sg = seg_map(tr.r1 - tr.r0);
+    const TileRange tr = tile_range(tiles, t);
+    const SegMap sg = seg_map(g, tr);
     float acc[2] = {};
     for (int c0 = tr.e0; c0 < tr.e1; c0 += TE) {
       const int ne = min(TE, tr.e1 - c0);
@@ -885,6 +910,7 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
         tc::commit(c.mbar);
       }
       TC_M();
+      const float qb = edge_qbar(g, es, Fbar);  // its loads overlap the MMAs
       c.wait_mma();
       TC_M();
       {
@@ -913,14 +939,6 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int* __rest
       TC_M();
       float mu[FPT], nu[FPT];
       {
-        const float qb = edge_qbar(g, es, Fbar);
-#ifdef JANUS_TC_TRACE
-        {
-          float dmy;
-          asm volatile("mov.b32 %0, %1;" : "=f"(dmy) : "f"(qb));
-          TC_M();
-        }
-#endif
         float gg[FPT], gp[FPT];
         float pm[FPT], px[FPT];
         float4 a4[FPT / 4], aj4[FPT / 4], v4[FPT / 4], d4[FPT / 4];

@@ -274,7 +274,7 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
       g.rev = dalloc<int>(st, NE, false);
       g.shift = dalloc<int>(st, 3 * NE, false);
       g.tile_row = dalloc<int>(st, NA + 1, false);
-      g.tile_row_tc = dalloc<int>(st, NA + 1, false);
+      g.tile_tc = reinterpret_cast<int4*>(dalloc<int>(st, 4 * static_cast<size_t>(NA), false));
       g.species = dalloc<int>(st, NA, false);
       g.struct_id = dalloc<int>(st, NA, false);
       g.struct_ptr = dalloc<int>(st, static_cast<size_t>(d.max_struct) + 1, false);
@@ -438,7 +438,17 @@ void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_
   h2d(g.E_target, hb.E_target, sizeof(float) * hb.n_struct);
   h2d(g.F_target, hb.F_target, sizeof(float) * 3 * N);
   h2d(g.tile_row, tiles.data(), sizeof(int) * tiles.size());
-  h2d(g.tile_row_tc, tiles_tc.data(), sizeof(int) * tiles_tc.size());
+  {
+    std::vector<int>& t4 = gg.h_tiles_tc4;  // edge ranges resolved on the host: one dependent load less per CTA
+    t4.resize(4 * static_cast<size_t>(g.n_tiles_tc));
+    for (int t = 0; t < g.n_tiles_tc; ++t) {
+      t4[4 * t] = tiles_tc[t];
+      t4[4 * t + 1] = tiles_tc[t + 1];
+      t4[4 * t + 2] = hb.row_ptr[tiles_tc[t]];
+      t4[4 * t + 3] = hb.row_ptr[tiles_tc[t + 1]];
+    }
+    h2d(g.tile_tc, t4.data(), sizeof(int) * t4.size());
+  }
   h2d(g.struct_ptr, sptr.data(), sizeof(int) * sptr.size());
   if (E > 0)
     node::geometry_kernel<<<blocks(E, 256), 256, 0, s>>>(N, E, g.row_ptr, g.col, g.shift, g.pos, g.struct_id, g.cell,
@@ -472,7 +482,7 @@ void stage_fe(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
         const float* W = P + R * H + H + H * H + H;
         gemm(s, N, cur_h, W, nullptr, nullptr, nullptr, b.v);
         if (g.n_tiles > 0 && use_tc(st))
-          edge_tc::msg_fe_tc<<<g.n_tiles_tc, edge_tc::NT, edge_tc::fe_smem(), s>>>(eg, g.tile_row_tc, g.n_tiles_tc, msg_params(st, u),
+          edge_tc::msg_fe_tc<<<g.n_tiles_tc, edge_tc::NT, edge_tc::fe_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, msg_params(st, u),
                                                                                  st->m.r_c, b.v, b.out_m);
         else if (g.n_tiles > 0)
           edge::msg_fe_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::fe_smem<kH, kR>(), s>>>(eg, msg_params(st, u), st->m.r_c, b.v, b.out_m);
@@ -542,7 +552,7 @@ void stage_ff(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
       case kMsg: {
         if (u == st->u1 - 1) copy(s, b.ff_a, wm, NH);  // a_m arrived through the ADJ_IN port
         if (g.n_tiles > 0 && use_tc(st)) {  // a_h += Y W^T fused into the tile epilogue
-          edge_tc::msg_ff_tc<<<g.n_tiles_tc, edge_tc::NT, edge_tc::ff_smem(), s>>>(eg, g.tile_row_tc, g.n_tiles_tc, msg_params(st, u),
+          edge_tc::msg_ff_tc<<<g.n_tiles_tc, edge_tc::NT, edge_tc::ff_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, msg_params(st, u),
                                                                                  st->m.r_c, b.v, b.ff_a, b.ff_Y, sl.F, wh);
         } else {
           if (g.n_tiles > 0)
@@ -604,7 +614,7 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
         gemm(s, N, ah, W, nullptr, nullptr, nullptr, sc.s1);  // vdot
         if (g.n_tiles > 0 && use_tc(st)) {
           const int grid = tc_grid(g);
-          edge_tc::msg_bf_tc<<<grid, edge_tc::NT, edge_tc::bf_smem(), s>>>(eg, g.tile_row_tc, g.n_tiles_tc, msg_params(st, u),
+          edge_tc::msg_bf_tc<<<grid, edge_tc::NT, edge_tc::bf_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, msg_params(st, u),
                                                                           st->m.r_c, b.v, sc.s1, b.ff_a, Fbar, am, sc.s2,
                                                                           sc.partial, b.inj);  // + hbar^F = X W^T
           JANUS_LAUNCH_CHECK("msg_bf_tc");
@@ -706,7 +716,7 @@ void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only, 
       case kMsg: {
         if (g.n_tiles > 0 && use_tc(st)) {
           const int grid = tc_grid(g);
-          edge_tc::msg_be_tc<<<grid, edge_tc::NT, edge_tc::be_smem(), s>>>(eg, g.tile_row_tc, g.n_tiles_tc, msg_params(st, u),
+          edge_tc::msg_be_tc<<<grid, edge_tc::NT, edge_tc::be_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, msg_params(st, u),
                                                                           st->m.r_c, b.v, bm, sc.s1, sc.partial,
                                                                           b.inj, bh);  // + b_h += Yb W^T + hbar^F
           JANUS_LAUNCH_CHECK("msg_be_tc");
@@ -819,17 +829,17 @@ void stage_time_edge_kernel(janus_stage* st, int which, int mb, int slot, int it
       const int grid = tc_grid(g);
       switch (which) {
         case 0:
-          edge_tc::msg_fe_tc<<<g.n_tiles_tc, edge_tc::NT, edge_tc::fe_smem(), s>>>(eg, g.tile_row_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, sc.s3);
+          edge_tc::msg_fe_tc<<<g.n_tiles_tc, edge_tc::NT, edge_tc::fe_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, sc.s3);
           break;
         case 1:
-          edge_tc::msg_ff_tc<<<g.n_tiles_tc, edge_tc::NT, edge_tc::ff_smem(), s>>>(eg, g.tile_row_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, b.ff_a, sc.s3, sc.s5, nullptr);
+          edge_tc::msg_ff_tc<<<g.n_tiles_tc, edge_tc::NT, edge_tc::ff_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, b.ff_a, sc.s3, sc.s5, nullptr);
           break;
         case 2:
-          edge_tc::msg_bf_tc<<<grid, edge_tc::NT, edge_tc::bf_smem(), s>>>(eg, g.tile_row_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, sc.s1, b.ff_a,
+          edge_tc::msg_bf_tc<<<grid, edge_tc::NT, edge_tc::bf_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, sc.s1, b.ff_a,
                                                                           sl.Fbar, sc.s3, sc.s4, sc.partial, nullptr);
           break;
         default:
-          edge_tc::msg_be_tc<<<grid, edge_tc::NT, edge_tc::be_smem(), s>>>(eg, g.tile_row_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, sc.s2, sc.s3, sc.partial, nullptr, nullptr);
+          edge_tc::msg_be_tc<<<grid, edge_tc::NT, edge_tc::be_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, sc.s2, sc.s3, sc.partial, nullptr, nullptr);
           break;
       }
       return;

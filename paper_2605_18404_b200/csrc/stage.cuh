@@ -29,8 +29,8 @@ struct DevGeo {
   int n_atoms = 0, n_edges = 0, n_struct = 0, n_tiles = 0;
   int n_tiles_tc = 0;
   int *row_ptr = nullptr, *col = nullptr, *src = nullptr, *rev = nullptr, *tile_row = nullptr, *shift = nullptr;
-  int* tile_row_tc = nullptr;  // <= 8 rows, <= 128 edges (tensor-core tiles)
-  std::vector<int> h_tiles, h_tiles_tc, h_sptr;  // host staging kept alive for the async LM copies
+  int4* tile_tc = nullptr;  // tensor-core tiles (<= 8 rows, <= 128 edges): {row0, row1, edge0, edge1}
+  std::vector<int> h_tiles, h_tiles_tc, h_tiles_tc4, h_sptr;  // host staging kept alive for the async LM copies
   int *species = nullptr, *struct_id = nullptr, *struct_ptr = nullptr;
   double *pos = nullptr, *cell = nullptr;
   float *d = nullptr, *u = nullptr, *c = nullptr, *dc = nullptr, *E_target = nullptr, *F_target = nullptr;
