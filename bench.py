@@ -39,6 +39,17 @@ CONFIG = dict(L=4, H=64, R=64, r_c=5.0, atoms=256, rho=0.095, n_mb=32, seed=7)
 METRIC = "structures/sec"
 
 
+def load_traffic(precision):
+    """DRAM bytes per launch of the roofline kernel from the committed ncu --set full
+    capture (profiles/r01_roofline_traffic.json); None when absent or for another kernel."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_roofline_traffic.json")) as f:
+            t = json.load(f)
+        return t["dram_bytes_per_launch"] if precision == "tf32" and t.get("kernel", "").endswith("msg_bf_tc") else None
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
@@ -299,7 +310,7 @@ def main():
             roof = {"kernel": "msg_bf_tc (tcgen05 kind::tf32)" if args.precision == "tf32" else "msg_bf_kernel (SIMT fp32)",
                     "bound": "tensor", "achieved": achieved,
                     "peak": peaks["bf16_tflops"], "unit": "TFLOP/s", "frac": achieved / peaks["bf16_tflops"],
-                    "traffic": None, "peak_source": f"{peak_src} bf16 dense (MEASURED_PEAKS.json)",
+                    "traffic": load_traffic(args.precision), "peak_source": f"{peak_src} bf16 dense (MEASURED_PEAKS.json)",
                     "launch_ms": ms_bf, "edges_per_launch": ne, "flops_per_launch": fl,
                     "fp32_simt_nominal_tflops": 74.4}
             fe = st.time_edge_kernel(0, 0, iters=50)
