@@ -185,6 +185,12 @@ int janus_trainer_create(const janus_exec_desc* ed, const janus_stage_desc* sd, 
 int janus_trainer_destroy(janus_trainer* t);
 int janus_trainer_load(janus_trainer* t, int mb, const janus_host_batch* hb);
 int janus_trainer_step(janus_trainer* t, const janus_opt* opt, janus_step_stats* stats);
+/* janus_trainer_step split in two: issue the step and return; then wait for it
+ * and fill stats (loss read back).  Loads issued in between are queued behind
+ * the step in flight, so the next step's uploads overlap this step's device
+ * time (input pipelining).  janus_trainer_step == step_async + wait. */
+int janus_trainer_step_async(janus_trainer* t, const janus_opt* opt);
+int janus_trainer_wait(janus_trainer* t, janus_step_stats* stats);
 /* per compute instruction of the last timed step: [n][5] = device, kind, mb, start_us, end_us */
 int janus_trainer_timeline(janus_trainer* t, double* out, int32_t cap, int32_t* n);
 int janus_trainer_stage(janus_trainer* t, int block, int force_replica, janus_stage** out);

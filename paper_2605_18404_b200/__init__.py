@@ -384,6 +384,8 @@ _sig("janus_trainer_create", c_int, c_vp, c_vp, c_vp, c_vp, c_int, c_vp)
 _sig("janus_trainer_destroy", c_int, c_vp)
 _sig("janus_trainer_load", c_int, c_vp, c_int, c_vp)
 _sig("janus_trainer_step", c_int, c_vp, c_vp, c_vp)
+_sig("janus_trainer_step_async", c_int, c_vp, c_vp)
+_sig("janus_trainer_wait", c_int, c_vp, c_vp)
 _sig("janus_trainer_timeline", c_int, c_vp, c_vp, ctypes.c_int32, c_vp)
 _sig("janus_trainer_stage", c_int, c_vp, c_int, c_int, c_vp)
 _sig("janus_trainer_schedule_text", c_int, c_vp, c_vp, c_i64, c_vp)
@@ -461,6 +463,16 @@ class Trainer:
         o = Opt(lr, beta1, beta2, eps)
         s = StepStats()
         check(_lib.janus_trainer_step(self.h, ctypes.byref(o), ctypes.byref(s)))
+        return s
+
+    def step_async(self, lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8) -> None:
+        """Issue a step and return; loads issued before wait() queue behind it."""
+        o = Opt(lr, beta1, beta2, eps)
+        check(_lib.janus_trainer_step_async(self.h, ctypes.byref(o)))
+
+    def wait(self) -> StepStats:
+        s = StepStats()
+        check(_lib.janus_trainer_wait(self.h, ctypes.byref(s)))
         return s
 
     def timeline(self):

@@ -290,6 +290,19 @@ int janus_trainer_step(janus_trainer* t, const janus_opt* opt, janus_step_stats*
     janus::trainer_step(t, *opt, stats);
   });
 }
+int janus_trainer_step_async(janus_trainer* t, const janus_opt* opt) {
+  return guard([&] {
+    need(t, "trainer");
+    need(opt, "opt");
+    janus::trainer_step_async(t, *opt);
+  });
+}
+int janus_trainer_wait(janus_trainer* t, janus_step_stats* stats) {
+  return guard([&] {
+    need(t, "trainer");
+    janus::trainer_wait(t, stats);
+  });
+}
 int janus_trainer_timeline(janus_trainer* t, double* out, int32_t cap, int32_t* n) {
   return guard([&] {
     need(t, "trainer");

@@ -31,6 +31,7 @@
 #include <numeric>
 #include <string>
 #include <tuple>
+#include <array>
 #include <vector>
 
 #include "../../include/janus/errors.hpp"
@@ -113,11 +114,13 @@ struct janus_trainer {
   janus::DepGraph graph;
   std::vector<janus::Rec> recs;
   bool recording = false;
+  bool pending = false;  // a step issued by trainer_step_async not yet waited for
   int64_t p2p_bytes = 0;
   int64_t kernel_count = -1;
   cudaGraphExec_t gexec = nullptr;
   janus_step_stats last{};
   std::vector<int> n_atoms;                      // per mb (for port sizes on the receive side)
+  std::vector<std::array<int, 5>> shape;         // per mb: atoms, edges, structs, tiles, TC tiles (graph validity)
 };
 
 namespace janus {
@@ -648,11 +651,26 @@ void trainer_destroy(janus_trainer* t) {
 
 void trainer_load(janus_trainer* t, int mb, const janus_host_batch& hb) {
   if (mb < 0 || mb >= t->ed.n_micro_batches) throw domain_error("micro-batch index out of range");
-  // asynchronous on the root stream (the step is issued behind it on the same
-  // stream); the last micro-batch of a batch of loads synchronises once
+  // asynchronous on the root stream: queued behind a step in flight and ahead
+  // of the next step.  The caller's arrays must stay valid until the copies
+  // run (pinned memory) or are staged by the driver (pageable memory); the
+  // host-built tile tables go through the stage's double-buffered pinned staging
   for (janus_stage* s : t->owned) stage_load(s, mb, hb, t->root, /*sync=*/false);
   t->n_atoms[static_cast<size_t>(mb)] = hb.n_atoms;
-  if (mb == t->ed.n_micro_batches - 1) JANUS_CUDA(cudaStreamSynchronize(t->root));
+  // a captured step graph bakes in grid sizes and copy lengths: a batch of a
+  // different shape in this slot forces a re-capture at the next step
+  if (t->shape.size() != t->n_atoms.size()) t->shape.assign(t->n_atoms.size(), {-1, -1, -1, -1, -1});
+  const DevGeo& g = t->owned.front()->geo[static_cast<size_t>(mb)];
+  const std::array<int, 5> sh{hb.n_atoms, hb.n_edges, hb.n_struct, g.n_tiles, g.n_tiles_tc};
+  if (t->shape[static_cast<size_t>(mb)] != sh) {
+    t->shape[static_cast<size_t>(mb)] = sh;
+    if (t->gexec) {
+      if (t->pending) JANUS_CUDA(cudaEventSynchronize(t->finish));  // the old graph may still be running
+      JANUS_CUDA(cudaGraphExecDestroy(t->gexec));
+      t->gexec = nullptr;
+      t->kernel_count = -1;
+    }
+  }
 }
 
 // count kernel nodes of one captured step (the gpu_launches evidence)
@@ -686,8 +704,12 @@ int64_t count_kernels(janus_trainer* t, const janus_opt& opt) {
   return k;
 }
 
-void trainer_step(janus_trainer* t, const janus_opt& opt, janus_step_stats* stats) {
+// Issue one step on the root stream and return without waiting: the caller may
+// queue the next step's uploads (janus_trainer_load) behind it, which overlaps
+// their host-side cost with this step's device time.
+void trainer_step_async(janus_trainer* t, const janus_opt& opt) {
   JANUS_CUDA(cudaSetDevice(t->sd.device));
+  if (t->pending) throw state_error("a step is already in flight (call janus_trainer_wait)");
   for (int m = 0; m < t->ed.n_micro_batches; ++m)
     if (t->n_atoms[static_cast<size_t>(m)] <= 0) throw state_error("micro-batch " + std::to_string(m) + " not loaded");
   if (t->local && t->kernel_count < 0) t->kernel_count = count_kernels(t, opt);  // capture only, nothing runs
@@ -707,6 +729,15 @@ void trainer_step(janus_trainer* t, const janus_opt& opt, janus_step_stats* stat
     if (t->local) finalize_local(t, opt);
   }
   JANUS_CUDA(cudaEventRecord(t->finish, t->root));
+  t->pending = true;
+}
+
+// Wait for the step in flight and report it (device time, bubbles, loss: the
+// per-micro-batch loss terms are read back here).
+void trainer_wait(janus_trainer* t, janus_step_stats* stats) {
+  JANUS_CUDA(cudaSetDevice(t->sd.device));
+  if (!t->pending) throw state_error("no step in flight");
+  t->pending = false;
   JANUS_CUDA(cudaEventSynchronize(t->finish));
   t->recording = false;
   float ms = 0.f;
@@ -760,6 +791,11 @@ void trainer_step(janus_trainer* t, const janus_opt& opt, janus_step_stats* stat
   s.loss = loss;
   t->last = s;
   if (stats) *stats = s;
+}
+
+void trainer_step(janus_trainer* t, const janus_opt& opt, janus_step_stats* stats) {
+  trainer_step_async(t, opt);
+  trainer_wait(t, stats);
 }
 
 }  // namespace janus

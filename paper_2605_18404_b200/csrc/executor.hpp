@@ -14,6 +14,8 @@ janus_trainer* trainer_create(const janus_exec_desc& ed, const janus_stage_desc&
 void trainer_destroy(janus_trainer* t);
 void trainer_load(janus_trainer* t, int mb, const janus_host_batch& hb);
 void trainer_step(janus_trainer* t, const janus_opt& opt, janus_step_stats* stats);
+void trainer_step_async(janus_trainer* t, const janus_opt& opt);
+void trainer_wait(janus_trainer* t, janus_step_stats* stats);
 void trainer_timeline(janus_trainer* t, double* out, int cap, int* n);
 janus_stage* trainer_stage(janus_trainer* t, int block, int force_replica);
 std::string trainer_schedule_text(janus_trainer* t);

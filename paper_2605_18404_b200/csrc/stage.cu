@@ -221,6 +221,23 @@ void check_mb_slot(const janus_stage* st, int mb, int slot) {
 }  // namespace
 
 // ============================================================= creation
+// upload block layout: capacity-sized fields, 256 B aligned
+LoadLayout load_layout(const janus_stage_desc& d) {
+  const size_t NA = static_cast<size_t>(d.max_atoms), NE = static_cast<size_t>(std::max(d.max_edges, 1));
+  const size_t MS = static_cast<size_t>(d.max_struct);
+  const size_t sz[LoadLayout::kN] = {
+      4 * (NA + 1), 4 * NE,     4 * NE, 4 * 3 * NE, 4 * NA, 4 * NA,    4 * (MS + 1),
+      4 * (NA + 1), 16 * NA,    8 * 3 * NA,  8 * MS, 4 * MS, 4 * 3 * NA};
+  LoadLayout L;
+  size_t o = 0;
+  for (int k = 0; k < LoadLayout::kN; ++k) {
+    L.off[k] = o;
+    o += (sz[k] + 255) & ~static_cast<size_t>(255);
+  }
+  L.bytes = o;
+  return L;
+}
+
 janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
   const janus_model_desc& m = d.model;
   if (m.H != kH || m.R != kR) throw config_error("this build supports H=64, R=64 (got H=" + std::to_string(m.H) + ", R=" + std::to_string(m.R) + ")");
@@ -268,24 +285,35 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
     // geometry per micro-batch
     st->geo.resize(NMB);
     for (auto& g : st->geo) {
-      g.row_ptr = dalloc<int>(st, NA + 1, false);
-      g.col = dalloc<int>(st, NE, false);
+      st->lay = load_layout(d);
+      const LoadLayout& L = st->lay;
+      g.d_block = dalloc<uint8_t>(st, L.bytes, false);
+      auto at = [&](int k) { return g.d_block + L.off[k]; };
+      g.row_ptr = reinterpret_cast<int*>(at(LoadLayout::kRowPtr));
+      g.col = reinterpret_cast<int*>(at(LoadLayout::kCol));
+      g.rev = reinterpret_cast<int*>(at(LoadLayout::kRev));
+      g.shift = reinterpret_cast<int*>(at(LoadLayout::kShift));
+      g.species = reinterpret_cast<int*>(at(LoadLayout::kSpecies));
+      g.struct_id = reinterpret_cast<int*>(at(LoadLayout::kStructId));
+      g.struct_ptr = reinterpret_cast<int*>(at(LoadLayout::kStructPtr));
+      g.tile_row = reinterpret_cast<int*>(at(LoadLayout::kTileRow));
+      g.tile_tc = reinterpret_cast<int4*>(at(LoadLayout::kTileTc));
+      g.pos = reinterpret_cast<double*>(at(LoadLayout::kPos));
+      g.cell = reinterpret_cast<double*>(at(LoadLayout::kCell));
+      g.E_target = reinterpret_cast<float*>(at(LoadLayout::kETarget));
+      g.F_target = reinterpret_cast<float*>(at(LoadLayout::kFTarget));
+      for (int par = 0; par < 2; ++par) {
+        void* hp = nullptr;
+        JANUS_CUDA(cudaHostAlloc(&hp, L.bytes, cudaHostAllocDefault));
+        std::memset(hp, 0, L.bytes);
+        st->host_allocs.push_back(hp);
+        g.h_pin[par] = static_cast<uint8_t*>(hp);
+      }
       g.src = dalloc<int>(st, NE, false);
-      g.rev = dalloc<int>(st, NE, false);
-      g.shift = dalloc<int>(st, 3 * NE, false);
-      g.tile_row = dalloc<int>(st, NA + 1, false);
-      g.tile_tc = reinterpret_cast<int4*>(dalloc<int>(st, 4 * static_cast<size_t>(NA), false));
-      g.species = dalloc<int>(st, NA, false);
-      g.struct_id = dalloc<int>(st, NA, false);
-      g.struct_ptr = dalloc<int>(st, static_cast<size_t>(d.max_struct) + 1, false);
-      g.pos = dalloc<double>(st, 3 * NA, false);
-      g.cell = dalloc<double>(st, static_cast<size_t>(d.max_struct), false);
       g.d = dalloc<float>(st, NE, false);
       g.u = dalloc<float>(st, 3 * NE, false);
       g.c = dalloc<float>(st, NE, false);
       g.dc = dalloc<float>(st, NE, false);
-      g.E_target = dalloc<float>(st, static_cast<size_t>(d.max_struct), false);
-      g.F_target = dalloc<float>(st, 3 * NA, false);
     }
     // slots
     st->slots.resize(static_cast<size_t>(d.n_slots));
@@ -359,6 +387,7 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
     JANUS_CUDA(cudaDeviceSynchronize());
   } catch (...) {
     for (void* p : st->allocs) cudaFree(p);
+    for (void* p : st->host_allocs) cudaFreeHost(p);
     delete st;
     throw;
   }
@@ -370,6 +399,7 @@ void stage_destroy(janus_stage* st) {
   cudaSetDevice(st->desc.device);
   cudaDeviceSynchronize();
   for (void* p : st->allocs) cudaFree(p);
+  for (void* p : st->host_allocs) cudaFreeHost(p);
   delete st;
 }
 
@@ -424,32 +454,37 @@ void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_
   g.n_struct = hb.n_struct;
   g.n_tiles = static_cast<int>(tiles.size()) - 1;
   g.n_tiles_tc = static_cast<int>(tiles_tc.size()) - 1;
-  auto h2d = [s](void* dst, const void* src, size_t bytes) {
-    if (bytes) JANUS_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+  // one pinned image per load (alternating halves: the other may still feed
+  // a queued copy), one host->device copy
+  const LoadLayout& L = st->lay;
+  uint8_t* hp = g.h_pin[g.h_par];
+  g.h_par ^= 1;
+  auto put = [&](int k, const void* src, size_t bytes) {
+    if (bytes) std::memcpy(hp + L.off[k], src, bytes);
   };
-  h2d(g.row_ptr, hb.row_ptr, sizeof(int) * (N + 1));
-  h2d(g.col, hb.col, sizeof(int) * E);
-  h2d(g.rev, hb.rev, sizeof(int) * E);
-  h2d(g.shift, hb.shift, sizeof(int) * 3 * E);
-  h2d(g.species, hb.species, sizeof(int) * N);
-  h2d(g.struct_id, hb.struct_id, sizeof(int) * N);
-  h2d(g.pos, hb.pos, sizeof(double) * 3 * N);
-  h2d(g.cell, hb.cell, sizeof(double) * hb.n_struct);
-  h2d(g.E_target, hb.E_target, sizeof(float) * hb.n_struct);
-  h2d(g.F_target, hb.F_target, sizeof(float) * 3 * N);
-  h2d(g.tile_row, tiles.data(), sizeof(int) * tiles.size());
+  put(LoadLayout::kRowPtr, hb.row_ptr, sizeof(int) * (N + 1));
+  put(LoadLayout::kCol, hb.col, sizeof(int) * E);
+  put(LoadLayout::kRev, hb.rev, sizeof(int) * E);
+  put(LoadLayout::kShift, hb.shift, sizeof(int) * 3 * E);
+  put(LoadLayout::kSpecies, hb.species, sizeof(int) * N);
+  put(LoadLayout::kStructId, hb.struct_id, sizeof(int) * N);
+  put(LoadLayout::kStructPtr, sptr.data(), sizeof(int) * sptr.size());
+  put(LoadLayout::kTileRow, tiles.data(), sizeof(int) * tiles.size());
   {
-    std::vector<int>& t4 = gg.h_tiles_tc4;  // edge ranges resolved on the host: one dependent load less per CTA
-    t4.resize(4 * static_cast<size_t>(g.n_tiles_tc));
+    int* t4 = reinterpret_cast<int*>(hp + L.off[LoadLayout::kTileTc]);  // edge ranges resolved on the host
     for (int t = 0; t < g.n_tiles_tc; ++t) {
       t4[4 * t] = tiles_tc[t];
       t4[4 * t + 1] = tiles_tc[t + 1];
       t4[4 * t + 2] = hb.row_ptr[tiles_tc[t]];
       t4[4 * t + 3] = hb.row_ptr[tiles_tc[t + 1]];
     }
-    h2d(g.tile_tc, t4.data(), sizeof(int) * t4.size());
   }
-  h2d(g.struct_ptr, sptr.data(), sizeof(int) * sptr.size());
+  put(LoadLayout::kPos, hb.pos, sizeof(double) * 3 * N);
+  put(LoadLayout::kCell, hb.cell, sizeof(double) * hb.n_struct);
+  put(LoadLayout::kETarget, hb.E_target, sizeof(float) * hb.n_struct);
+  put(LoadLayout::kFTarget, hb.F_target, sizeof(float) * 3 * N);
+  const size_t extent = L.off[LoadLayout::kFTarget] + sizeof(float) * 3 * N;
+  JANUS_CUDA(cudaMemcpyAsync(g.d_block, hp, extent, cudaMemcpyHostToDevice, s));
   if (E > 0)
     node::geometry_kernel<<<blocks(E, 256), 256, 0, s>>>(N, E, g.row_ptr, g.col, g.shift, g.pos, g.struct_id, g.cell,
                                                          static_cast<double>(st->m.r_c), g.src, g.d, g.u, g.c, g.dc);

@@ -25,12 +25,27 @@ inline UnitKind unit_kind(int u, int L) {
 int64_t unit_param_count(const janus_model_desc& m, int u);
 int64_t unit_param_offset(const janus_model_desc& m, int u);
 
+// Upload block of one micro-batch: the caller's arrays and the host-built
+// tables at fixed capacity offsets, so one LM is ONE host->device copy into a
+// device block with the same layout (the device pointers below point into it).
+struct LoadLayout {
+  enum { kRowPtr, kCol, kRev, kShift, kSpecies, kStructId, kStructPtr, kTileRow, kTileTc, kPos, kCell, kETarget, kFTarget, kN };
+  size_t off[kN] = {};
+  size_t bytes = 0;
+};
+
 struct DevGeo {
   int n_atoms = 0, n_edges = 0, n_struct = 0, n_tiles = 0;
   int n_tiles_tc = 0;
   int *row_ptr = nullptr, *col = nullptr, *src = nullptr, *rev = nullptr, *tile_row = nullptr, *shift = nullptr;
   int4* tile_tc = nullptr;  // tensor-core tiles (<= 8 rows, <= 128 edges): {row0, row1, edge0, edge1}
-  std::vector<int> h_tiles, h_tiles_tc, h_tiles_tc4, h_sptr;  // host staging kept alive for the async LM copies
+  std::vector<int> h_tiles, h_tiles_tc, h_sptr;  // host-side tile / struct tables (built at LM)
+  // pinned host image of the upload block, double-buffered: a load may be
+  // issued while the previous load's copy of this micro-batch is still queued
+  // (the trainer pipelines step k+1's uploads behind step k)
+  uint8_t* h_pin[2] = {nullptr, nullptr};
+  uint8_t* d_block = nullptr;
+  int h_par = 0;
   int *species = nullptr, *struct_id = nullptr, *struct_ptr = nullptr;
   double *pos = nullptr, *cell = nullptr;
   float *d = nullptr, *u = nullptr, *c = nullptr, *dc = nullptr, *E_target = nullptr, *F_target = nullptr;
@@ -92,6 +107,8 @@ struct janus_stage {
   std::vector<janus::Scratch> lanes;
   float* losses = nullptr;  // [n_slots][2] loss_E, loss_F (slot.loss points here)
   std::vector<void*> allocs;
+  std::vector<void*> host_allocs;  // pinned (cudaHostAlloc)
+  janus::LoadLayout lay;           // upload block layout (capacity offsets)
   int64_t static_bytes = 0, arena_bytes = 0;
 
   float* P(int u) const { return params + uoff[static_cast<size_t>(u - u0)]; }

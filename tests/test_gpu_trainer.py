@@ -129,3 +129,45 @@ def test_lanes_bit_identical(janus, data, P, lanes):
     assert np.array_equal(g, g1) and np.array_equal(t.params(), p1)
     t.close()
     t1.close()
+
+
+@pytest.mark.parametrize("graphs", [False, True])
+def test_pipelined_loads_bit_identical(janus, data, graphs):
+    """Input pipelining (loads of step k+1 queued behind step k via
+    step_async/wait, as bench.py's e2e loop does) changes nothing: every step
+    sees its own freshly uploaded batches; losses and parameters match the
+    synchronous load+step loop bit for bit.  Step k+1 uses different batches
+    (reversed order) so a stale geometry or tile table would show."""
+    m, params, batches, _, _ = data
+    order = [batches, batches[::-1], batches]
+
+    def make():
+        return janus.Trainer(m, params, 2, janus.METHOD_SYMFOLD, len(batches), k=1, max_atoms=64,
+                             max_edges=64 * 120, graphs=graphs, lanes=2)
+
+    ta = make()
+    la = []
+    for bs in order:
+        for i, b in enumerate(bs):
+            ta.load(i, b)
+        la.append(ta.step().loss)
+    pa = ta.params()
+
+    tb = make()
+    lb = []
+    for i, b in enumerate(order[0]):
+        tb.load(i, b)
+    tb.step_async()
+    for bs in order[1:]:
+        for i, b in enumerate(bs):
+            tb.load(i, b)
+        lb.append(tb.wait().loss)
+        tb.step_async()
+    lb.append(tb.wait().loss)
+    pb = tb.params()
+    assert la == lb
+    assert np.array_equal(pa, pb)
+    with pytest.raises(janus.JanusError):
+        tb.wait()  # nothing in flight
+    ta.close()
+    tb.close()
