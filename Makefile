@@ -8,13 +8,24 @@ SRC := $(PKG)/csrc
 OBJ := build/obj
 LIB := $(PKG)/libjanus_b200.so
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := -Iinclude -std=c++20 -O3 $(ARCH) -lineinfo -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
+# NCCL: the torch-bundled 2.28 (same image on the GPU boxes).  Linking the
+# system 2.27 would make a later `import torch` bind its libnccl.so.2 SONAME to
+# 2.27 and fail (ncclDevCommCreate), which breaks torchrun launches.
+NCCL_HOME ?= $(shell python -c "import nvidia.nccl as n; print(n.__path__[0])" 2>/dev/null)
+ifneq ($(NCCL_HOME),)
+NCCL_INC := -I$(NCCL_HOME)/include
+NCCL_LINK := -L$(NCCL_HOME)/lib -l:libnccl.so.2 -Xlinker -rpath -Xlinker $(NCCL_HOME)/lib
+else
+NCCL_INC :=
+NCCL_LINK := -L/usr/lib/x86_64-linux-gnu -lnccl
+endif
+NVFLAGS := $(NCCL_INC) -Iinclude -std=c++20 -O3 $(ARCH) -lineinfo -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
 ifeq ($(TRACE),1)  # phase-traced profiling build (edge_tc.cuh TC_MARK), loaded via JANUS_LIB
 OBJ := build/trace_obj
 LIB := build/trace/libjanus_b200.so
 NVFLAGS += -DJANUS_TC_TRACE
 endif
-CXXFLAGS := -Iinclude -std=c++20 -O2 -fPIC -ffp-contract=off -Wall -Wextra -I/usr/local/cuda/include
+CXXFLAGS := $(NCCL_INC) -Iinclude -std=c++20 -O2 -fPIC -ffp-contract=off -Wall -Wextra -I/usr/local/cuda/include
 CU_SRCS := $(wildcard $(SRC)/*.cu)
 CPP_SRCS := $(wildcard $(SRC)/*.cpp)
 OBJS := $(patsubst $(SRC)/%.cu,$(OBJ)/%.cu.o,$(CU_SRCS)) $(patsubst $(SRC)/%.cpp,$(OBJ)/%.cpp.o,$(CPP_SRCS))
@@ -36,7 +47,7 @@ $(OBJ)/%.cpp.o: $(SRC)/%.cpp $(HDRS) | $(OBJ)
 
 $(LIB): $(OBJS)
 	mkdir -p $(dir $@)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -L/usr/lib/x86_64-linux-gnu -lnccl -lcudart
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) $(NCCL_LINK) -lcudart
 
 oracle:
 	$(MAKE) -s -C oracle

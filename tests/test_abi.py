@@ -100,3 +100,16 @@ def test_schedule_entry_points(janus):
     assert janus.validate_schedule(janus.schedule_text(janus.METHOD_ONEF1B, 4, 8)) == 0
     with pytest.raises(janus.JanusError):
         janus.schedule_text(janus.METHOD_ONEF1B, 3, 8)  # odd P -> config error
+
+
+def test_torch_imports_after_library():
+    """The library links the torch-bundled NCCL (Makefile NCCL_HOME): loading it
+    first must not break a later `import torch.distributed` (bench.py under
+    torchrun does exactly that); a system libnccl.so.2 would shadow torch's."""
+    import subprocess
+    import sys
+
+    code = ("import paper_2605_18404_b200 as J; import torch, torch.distributed as d; "
+            "assert d.is_nccl_available(); print(J.lib().janus_abi_version())")
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-1500:]
