@@ -93,6 +93,26 @@ int janus_nbrlist_build(int32_t n_atoms, const double* pos, const int32_t* struc
                         double r_c, int32_t max_edges, int32_t* row_ptr, int32_t* col, int32_t* shift,
                         int32_t* rev, int32_t* n_edges);
 
+/* Device neighbour list (LM on the GPU).  A cell-list
+ * build whose CSR (row_ptr, col, shift, rev) is bit-identical to
+ * janus_nbrlist_build.  pos [n_atoms*3] and struct_id are DEVICE pointers,
+ * cell [n_struct] (box lengths, which size the cell grid) is HOST; the outputs
+ * are device buffers with room for max_edges edges.  Runs on `stream` and
+ * synchronizes it once to return *n_edges; kDomainError if max_edges is
+ * exceeded (same message as the host build).  Replaces the reference's LM
+ * duration slot (ir.hpp:25, graph.hpp:124).
+ *
+ * The stage and trainer loads use it when a batch carries no neighbour list:
+ * janus_stage_load / janus_trainer_load with hb->row_ptr == NULL build the CSR
+ * on the device from hb->pos (col / shift / rev / n_edges are ignored). */
+typedef struct janus_nbrlist janus_nbrlist;
+int janus_nbrlist_create(int32_t max_atoms, int32_t max_struct, int32_t max_edges, int32_t device,
+                         janus_nbrlist** out);
+int janus_nbrlist_destroy(janus_nbrlist* nl);
+int janus_nbrlist_build_device(janus_nbrlist* nl, int32_t n_atoms, int32_t n_struct, const double* pos,
+                               const int32_t* struct_id, const double* cell, double r_c, int32_t* row_ptr,
+                               int32_t* col, int32_t* shift, int32_t* rev, int32_t* n_edges, void* stream);
+
 /* ---- stages ---- */
 int janus_stage_create(const janus_stage_desc* desc, const float* unit_params, janus_stage** out);
 int janus_stage_destroy(janus_stage* st);
@@ -184,6 +204,11 @@ int janus_trainer_create(const janus_exec_desc* ed, const janus_stage_desc* sd, 
                          janus_comm* comm, int rank, janus_trainer** out);
 int janus_trainer_destroy(janus_trainer* t);
 int janus_trainer_load(janus_trainer* t, int mb, const janus_host_batch* hb);
+/* LM of n micro-batches (mbs[k] <- hbs[k]).  Batches without a neighbour list
+ * (row_ptr == NULL) get ONE device cell-list build over all of them (their
+ * structures side by side), run on a side stream beside a step in flight, and
+ * one host sync for the row-tile tables.  janus_trainer_load == n = 1. */
+int janus_trainer_load_many(janus_trainer* t, int n, const int32_t* mbs, const janus_host_batch* hbs);
 int janus_trainer_step(janus_trainer* t, const janus_opt* opt, janus_step_stats* stats);
 /* janus_trainer_step split in two: issue the step and return; then wait for it
  * and fill stats (loss read back).  Loads issued in between are queued behind

@@ -74,6 +74,10 @@ _sig("janus_synth_params", c_int, c_vp, c_u64, c_vp)
 _sig("janus_synth_cell", c_int, ctypes.c_int32, c_d, ctypes.c_int32, c_u64, c_vp, c_vp, c_vp, c_vp, c_vp)
 _sig("janus_nbrlist_build", c_int, ctypes.c_int32, c_vp, c_vp, c_vp, c_d, ctypes.c_int32, c_vp, c_vp, c_vp, c_vp,
      c_vp)
+_sig("janus_nbrlist_create", c_int, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, c_vp)
+_sig("janus_nbrlist_destroy", c_int, c_vp)
+_sig("janus_nbrlist_build_device", c_int, c_vp, ctypes.c_int32, ctypes.c_int32, c_vp, c_vp, c_vp, c_d, c_vp, c_vp,
+     c_vp, c_vp, c_vp, c_vp)
 _sig("janus_stage_create", c_int, c_vp, c_vp, c_vp)
 _sig("janus_stage_destroy", c_int, c_vp)
 _sig("janus_stage_load", c_int, c_vp, c_int, c_vp, c_vp)
@@ -146,7 +150,10 @@ class Model:
 
 
 class Batch:
-    """One micro-batch: concatenated cubic cells + neighbour list (host arrays)."""
+    """One micro-batch: concatenated cubic cells + neighbour list (host arrays).
+
+    nl="device": no host neighbour list; the load builds it on the GPU
+    (janus_stage_load / janus_trainer_load with row_ptr == NULL)."""
 
     def __init__(self, pos, species, struct_id, cell, E_target, F_target, nl=None, r_c: float | None = None,
                  max_edges: int | None = None):
@@ -156,9 +163,15 @@ class Batch:
         self.cell = np.ascontiguousarray(cell, np.float64)
         self.E_target = np.ascontiguousarray(E_target, np.float32)
         self.F_target = np.ascontiguousarray(F_target, np.float32).reshape(-1, 3)
-        if nl is None:
+        if isinstance(nl, str) and nl == "device":
+            nl = (None, None, None, None)
+        elif nl is None:
             nl = nbrlist(self.pos, self.struct_id, self.cell, r_c, max_edges)
         self.row_ptr, self.col, self.shift, self.rev = nl
+
+    @property
+    def device_nbrlist(self) -> bool:
+        return self.row_ptr is None
 
     @property
     def n_atoms(self):
@@ -170,12 +183,13 @@ class Batch:
 
     @property
     def n_edges(self):
-        return int(self.col.shape[0])
+        return 0 if self.row_ptr is None else int(self.col.shape[0])
 
     def c(self) -> HostBatch:
+        q = (lambda a: None if a is None else _p(a))
         return HostBatch(self.n_atoms, self.n_struct, self.n_edges, _p(self.pos), _p(self.species),
-                         _p(self.struct_id), _p(self.cell), _p(self.E_target), _p(self.F_target), _p(self.row_ptr),
-                         _p(self.col), _p(self.shift), _p(self.rev))
+                         _p(self.struct_id), _p(self.cell), _p(self.E_target), _p(self.F_target), q(self.row_ptr),
+                         q(self.col), q(self.shift), q(self.rev))
 
 
 def nbrlist(pos, struct_id, cell, r_c, max_edges=None):
@@ -195,6 +209,47 @@ def nbrlist(pos, struct_id, cell, r_c, max_edges=None):
     return row_ptr, col[:E].copy(), shift[:3 * E].copy(), rev[:E].copy()
 
 
+def nbrlist_device(pos, struct_id, cell, r_c, max_edges=None, device: int = 0):
+    """janus_nbrlist_build_device on device memory (cudart), CSR copied back."""
+    pos = np.ascontiguousarray(pos, np.float64).reshape(-1, 3)
+    n = pos.shape[0]
+    sid = np.ascontiguousarray(struct_id, np.int32)
+    cl = np.ascontiguousarray(cell, np.float64)
+    max_edges = max_edges or n * 400
+    rt = cudart()
+    sizes = [pos.nbytes, sid.nbytes, 4 * (n + 1), 4 * max_edges, 12 * max_edges, 4 * max_edges]
+    ptrs = []
+    h = c_vp()
+    try:
+        for b in sizes:
+            p = c_vp()
+            if rt.cudaMalloc(ctypes.byref(p), max(b, 4)) != 0:
+                raise RuntimeError("cudaMalloc failed")
+            ptrs.append(p.value)
+        dpos, dsid, drow, dcol, dsh, drev = ptrs
+        if rt.cudaMemcpy(dpos, _p(pos), pos.nbytes, 1) or rt.cudaMemcpy(dsid, _p(sid), sid.nbytes, 1):
+            raise RuntimeError("cudaMemcpy H2D failed")
+        check(_lib.janus_nbrlist_create(n, len(cl), max_edges, device, ctypes.byref(h)))
+        ne = ctypes.c_int32(0)
+        check(_lib.janus_nbrlist_build_device(h, n, len(cl), dpos, dsid, _p(cl), r_c, drow, dcol, dsh, drev,
+                                              ctypes.byref(ne), None))
+        E = ne.value
+        row_ptr = np.zeros(n + 1, np.int32)
+        col = np.zeros(max(E, 1), np.int32)
+        shift = np.zeros(max(3 * E, 1), np.int32)
+        rev = np.zeros(max(E, 1), np.int32)
+        for host, dev, nb in ((row_ptr, drow, 4 * (n + 1)), (col, dcol, 4 * E), (shift, dsh, 12 * E),
+                              (rev, drev, 4 * E)):
+            if nb and rt.cudaMemcpy(_p(host), dev, nb, 2):
+                raise RuntimeError("cudaMemcpy D2H failed")
+        return row_ptr, col[:E].copy(), shift[:3 * E].copy(), rev[:E].copy()
+    finally:
+        if h.value:
+            _lib.janus_nbrlist_destroy(h)
+        for p in ptrs:
+            rt.cudaFree(p)
+
+
 def synth_cell(n_atoms: int, rho: float, n_species: int, seed: int):
     pos = np.zeros((n_atoms, 3))
     sp = np.zeros(n_atoms, np.int32)
@@ -205,8 +260,9 @@ def synth_cell(n_atoms: int, rho: float, n_species: int, seed: int):
     return pos, sp, cell.value, float(Et[0]), Ft
 
 
-def synth_batch(model: Model, atoms_per_cell, rho: float, seed: int) -> Batch:
-    """A micro-batch of one or more synthetic cells (sizes in atoms_per_cell)."""
+def synth_batch(model: Model, atoms_per_cell, rho: float, seed: int, device_nl: bool = False) -> Batch:
+    """A micro-batch of one or more synthetic cells (sizes in atoms_per_cell).
+    device_nl: leave the neighbour list to the GPU load (no host CSR)."""
     if isinstance(atoms_per_cell, int):
         atoms_per_cell = [atoms_per_cell]
     P, S, SID, C, E, F = [], [], [], [], [], []
@@ -214,7 +270,7 @@ def synth_batch(model: Model, atoms_per_cell, rho: float, seed: int) -> Batch:
         pos, sp, L, Et, Ft = synth_cell(n, rho, model.n_species, seed * 1000003 + s)
         P.append(pos); S.append(sp); SID.append(np.full(n, s, np.int32)); C.append(L); E.append(Et); F.append(Ft)
     return Batch(np.concatenate(P), np.concatenate(S), np.concatenate(SID), np.array(C), np.array(E),
-                 np.concatenate(F), r_c=model.r_c)
+                 np.concatenate(F), r_c=model.r_c, nl="device" if device_nl else None)
 
 
 class Stage:
@@ -358,6 +414,10 @@ def cudart():
             raise ImportError("libcudart not found")
         _cudart.cudaMemcpy.argtypes = [c_vp, c_vp, c_sz, c_int]
         _cudart.cudaMemcpy.restype = c_int
+        _cudart.cudaMalloc.argtypes = [c_vp, c_sz]
+        _cudart.cudaMalloc.restype = c_int
+        _cudart.cudaFree.argtypes = [c_vp]
+        _cudart.cudaFree.restype = c_int
         _cudart.cudaDeviceSynchronize.restype = c_int
     return _cudart
 
@@ -458,6 +518,13 @@ class Trainer:
     def load(self, mb: int, batch: Batch):
         hb = batch.c()
         check(_lib.janus_trainer_load(self.h, mb, ctypes.byref(hb)))
+
+    def load_many(self, batches, mbs=None):
+        """LM of several micro-batches; device-LM batches share one GPU build."""
+        mbs = list(range(len(batches))) if mbs is None else list(mbs)
+        arr = (HostBatch * len(batches))(*[b.c() for b in batches])
+        ids = np.ascontiguousarray(mbs, np.int32)
+        check(_lib.janus_trainer_load_many(self.h, len(batches), _p(ids), arr))
 
     def step(self, lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8) -> StepStats:
         o = Opt(lr, beta1, beta2, eps)

@@ -14,6 +14,7 @@
 #include "cuda_check.hpp"
 #include "executor.hpp"
 #include "host.hpp"
+#include "nbrlist.hpp"
 #include "stage_api.hpp"
 
 namespace {
@@ -130,6 +131,35 @@ int janus_nbrlist_build(int32_t n_atoms, const double* pos, const int32_t* struc
     if (n_atoms < 1) throw janus::domain_error("n_atoms must be >= 1");
     if (!(r_c > 0)) throw janus::domain_error("r_c must be > 0");
     *n_edges = janus::nbrlist_build(n_atoms, pos, struct_id, cell, r_c, max_edges, row_ptr, col, shift, rev);
+  });
+}
+
+int janus_nbrlist_create(int32_t max_atoms, int32_t max_struct, int32_t max_edges, int32_t device,
+                         janus_nbrlist** out) {
+  return guard([&] {
+    need(out, "out");
+    *out = nullptr;
+    *out = janus::nbrlist_create(max_atoms, max_struct, max_edges, device);
+  });
+}
+int janus_nbrlist_destroy(janus_nbrlist* nl) {
+  return guard([&] { janus::nbrlist_destroy(nl); });
+}
+int janus_nbrlist_build_device(janus_nbrlist* nl, int32_t n_atoms, int32_t n_struct, const double* pos,
+                               const int32_t* struct_id, const double* cell, double r_c, int32_t* row_ptr,
+                               int32_t* col, int32_t* shift, int32_t* rev, int32_t* n_edges, void* stream) {
+  return guard([&] {
+    need(nl, "nbrlist");
+    need(pos, "pos");
+    need(struct_id, "struct_id");
+    need(cell, "cell");
+    need(row_ptr, "row_ptr");
+    need(col, "col");
+    need(shift, "shift");
+    need(rev, "rev");
+    need(n_edges, "n_edges");
+    janus::nbrlist_enqueue(nl, n_atoms, n_struct, pos, struct_id, cell, r_c, row_ptr, col, shift, rev, S(stream));
+    *n_edges = janus::nbrlist_finish(nl, S(stream));
   });
 }
 
@@ -281,6 +311,17 @@ int janus_trainer_load(janus_trainer* t, int mb, const janus_host_batch* hb) {
     need(t, "trainer");
     need(hb, "batch");
     janus::trainer_load(t, mb, *hb);
+  });
+}
+int janus_trainer_load_many(janus_trainer* t, int n, const int32_t* mbs, const janus_host_batch* hbs) {
+  return guard([&] {
+    need(t, "trainer");
+    if (n < 0) throw janus::domain_error("n must be >= 0");
+    if (n > 0) {
+      need(mbs, "mbs");
+      need(hbs, "hbs");
+      janus::trainer_load_many(t, n, mbs, hbs);
+    }
   });
 }
 int janus_trainer_step(janus_trainer* t, const janus_opt* opt, janus_step_stats* stats) {

@@ -42,6 +42,7 @@
 #include "cuda_check.hpp"
 #include "stage.cuh"
 #include "stage_api.hpp"
+#include "nbrlist.hpp"
 
 namespace janus {
 namespace {
@@ -121,6 +122,9 @@ struct janus_trainer {
   janus_step_stats last{};
   std::vector<int> n_atoms;                      // per mb (for port sizes on the receive side)
   std::vector<std::array<int, 5>> shape;         // per mb: atoms, edges, structs, tiles, TC tiles (graph validity)
+  janus::LmBuilder* lm = nullptr;                // device neighbour lists (loads without a CSR)
+  cudaStream_t lm_stream = nullptr;              // their builds run here, beside a step in flight
+  int lm_par = 0;                                 // CSR buffer of the next device LM build
 };
 
 namespace janus {
@@ -643,19 +647,73 @@ void trainer_destroy(janus_trainer* t) {
     cudaStreamDestroy(d.send);
     cudaStreamDestroy(d.recv);
   }
+  delete t->lm;
+  if (t->lm_stream) cudaStreamDestroy(t->lm_stream);
   if (t->root) cudaStreamDestroy(t->root);
   if (t->anchor) cudaEventDestroy(t->anchor);
   if (t->finish) cudaEventDestroy(t->finish);
   delete t;
 }
 
-void trainer_load(janus_trainer* t, int mb, const janus_host_batch& hb) {
-  if (mb < 0 || mb >= t->ed.n_micro_batches) throw domain_error("micro-batch index out of range");
+void trainer_note_shape(janus_trainer* t, int mb, const janus_host_batch& hb);
+void trainer_load_many(janus_trainer* t, int n, const int* mbs, const janus_host_batch* hbs);
+
+void trainer_load(janus_trainer* t, int mb, const janus_host_batch& hb) { trainer_load_many(t, 1, &mb, &hb); }
+
+void trainer_load_many(janus_trainer* t, int n, const int* mbs, const janus_host_batch* hbs) {
+  for (int k = 0; k < n; ++k)
+    if (mbs[k] < 0 || mbs[k] >= t->ed.n_micro_batches) throw domain_error("micro-batch index out of range");
   // asynchronous on the root stream: queued behind a step in flight and ahead
   // of the next step.  The caller's arrays must stay valid until the copies
   // run (pinned memory) or are staged by the driver (pageable memory); the
   // host-built tile tables go through the stage's double-buffered pinned staging
-  for (janus_stage* s : t->owned) stage_load(s, mb, hb, t->root, /*sync=*/false);
+  std::vector<janus_host_batch> dev;
+  std::vector<int> dev_mb;
+  for (int k = 0; k < n; ++k) {
+    if (hbs[k].row_ptr) {
+      for (janus_stage* s : t->owned) stage_load(s, mbs[k], hbs[k], t->root, /*sync=*/false);
+      trainer_note_shape(t, mbs[k], hbs[k]);
+    } else {
+      dev.push_back(hbs[k]);
+      dev_mb.push_back(mbs[k]);
+    }
+  }
+  if (dev.empty()) return;
+  // LM with the neighbour lists built on the device: ONE cell-list build over
+  // all these micro-batches (their structures side by side) on a side stream,
+  // while a step may still run on root; each stage copies its batch's slice
+  // on root (queued behind that step).  Builds alternate between two buffers
+  // and the build after next into a buffer waits for those copies on the device.
+  if (!t->lm) {
+    const int nm = t->ed.n_micro_batches;
+    t->lm = new LmBuilder(nm * t->sd.max_atoms, nm * t->sd.max_struct, nm * t->sd.max_edges, t->sd.device, 2);
+    // highest priority: the build's CTAs take SMs ahead of the step in flight,
+    // so the host's one sync for the tile tables stays short
+    int lo = 0, hi = 0;
+    JANUS_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    JANUS_CUDA(cudaStreamCreateWithPriority(&t->lm_stream, cudaStreamNonBlocking, hi));
+  }
+  const int b = t->lm_par;
+  t->lm_par ^= 1;
+  t->lm->build(dev.data(), static_cast<int>(dev.size()), static_cast<double>(t->sd.model.r_c), b, t->lm_stream);
+  const int* hrow = t->lm->host_row_ptr();
+  std::vector<int> rp;
+  for (size_t k = 0; k < dev.size(); ++k) {
+    const int a0 = t->lm->atom0(static_cast<int>(k)), N = dev[k].n_atoms;
+    rp.resize(static_cast<size_t>(N) + 1);
+    for (int i = 0; i <= N; ++i) rp[static_cast<size_t>(i)] = hrow[a0 + i] - hrow[a0];
+    janus_host_batch hb2 = dev[k];
+    hb2.row_ptr = rp.data();
+    hb2.n_edges = rp[static_cast<size_t>(N)];
+    hb2.col = hb2.shift = hb2.rev = nullptr;
+    const DevCsrSlice sl{&t->lm->buf(b), a0, hrow[a0]};
+    for (janus_stage* s : t->owned) stage_load(s, dev_mb[k], hb2, t->root, /*sync=*/false, &sl);
+    trainer_note_shape(t, dev_mb[k], hb2);
+  }
+  t->lm->release(b, t->root);
+}
+
+void trainer_note_shape(janus_trainer* t, int mb, const janus_host_batch& hb) {
   t->n_atoms[static_cast<size_t>(mb)] = hb.n_atoms;
   // a captured step graph bakes in grid sizes and copy lengths: a batch of a
   // different shape in this slot forces a re-capture at the next step

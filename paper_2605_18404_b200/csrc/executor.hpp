@@ -13,6 +13,7 @@ janus_trainer* trainer_create(const janus_exec_desc& ed, const janus_stage_desc&
                               janus_comm* comm, int rank);
 void trainer_destroy(janus_trainer* t);
 void trainer_load(janus_trainer* t, int mb, const janus_host_batch& hb);
+void trainer_load_many(janus_trainer* t, int n, const int* mbs, const janus_host_batch* hbs);
 void trainer_step(janus_trainer* t, const janus_opt& opt, janus_step_stats* stats);
 void trainer_step_async(janus_trainer* t, const janus_opt& opt);
 void trainer_wait(janus_trainer* t, janus_step_stats* stats);

@@ -22,6 +22,7 @@
 #include "node_kernels.cuh"
 #include "stage.cuh"
 #include "stage_api.hpp"
+#include "nbrlist.hpp"
 
 namespace janus {
 
@@ -398,6 +399,7 @@ void stage_destroy(janus_stage* st) {
   if (!st) return;
   cudaSetDevice(st->desc.device);
   cudaDeviceSynchronize();
+  delete st->lm;
   for (void* p : st->allocs) cudaFree(p);
   for (void* p : st->host_allocs) cudaFreeHost(p);
   delete st;
@@ -410,8 +412,19 @@ size_t port_elems(const janus_stage* st, int port, int n) {
 }
 
 // ================================================================== LM
-void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_t s, bool sync) {
+void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_t s, bool sync,
+                const DevCsrSlice* dcsr) {
   if (mb < 0 || mb >= st->desc.n_micro_batches) throw domain_error("micro-batch index out of range");
+  if (!hb.row_ptr && !dcsr) {  // no neighbour list in the batch: build it on the device (nbrlist.cu)
+    if (!st->lm) st->lm = new LmBuilder(st->desc.max_atoms, st->desc.max_struct, st->desc.max_edges, st->desc.device, 1);
+    janus_host_batch hb2 = hb;
+    hb2.n_edges = st->lm->build(&hb, 1, static_cast<double>(st->m.r_c), 0, s);
+    hb2.row_ptr = st->lm->host_row_ptr();
+    const DevCsrSlice sl{&st->lm->buf(0), 0, 0};
+    stage_load(st, mb, hb2, s, sync, &sl);
+    st->lm->release(0, s);
+    return;
+  }
   if (hb.n_atoms < 1 || hb.n_atoms > st->desc.max_atoms) throw domain_error("n_atoms exceeds stage capacity");
   if (hb.n_edges < 0 || hb.n_edges > st->desc.max_edges) throw domain_error("n_edges exceeds stage capacity");
   if (hb.n_struct < 1 || hb.n_struct > st->desc.max_struct) throw domain_error("n_struct exceeds stage capacity");
@@ -463,9 +476,11 @@ void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_
     if (bytes) std::memcpy(hp + L.off[k], src, bytes);
   };
   put(LoadLayout::kRowPtr, hb.row_ptr, sizeof(int) * (N + 1));
-  put(LoadLayout::kCol, hb.col, sizeof(int) * E);
-  put(LoadLayout::kRev, hb.rev, sizeof(int) * E);
-  put(LoadLayout::kShift, hb.shift, sizeof(int) * 3 * E);
+  if (!dcsr) {
+    put(LoadLayout::kCol, hb.col, sizeof(int) * E);
+    put(LoadLayout::kRev, hb.rev, sizeof(int) * E);
+    put(LoadLayout::kShift, hb.shift, sizeof(int) * 3 * E);
+  }
   put(LoadLayout::kSpecies, hb.species, sizeof(int) * N);
   put(LoadLayout::kStructId, hb.struct_id, sizeof(int) * N);
   put(LoadLayout::kStructPtr, sptr.data(), sizeof(int) * sptr.size());
@@ -485,6 +500,8 @@ void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_
   put(LoadLayout::kFTarget, hb.F_target, sizeof(float) * 3 * N);
   const size_t extent = L.off[LoadLayout::kFTarget] + sizeof(float) * 3 * N;
   JANUS_CUDA(cudaMemcpyAsync(g.d_block, hp, extent, cudaMemcpyHostToDevice, s));
+  if (dcsr)  // the device-built CSR replaces the (unused) host regions of the block
+    csr_slice_copy(*dcsr->csr, dcsr->atom0, dcsr->edge0, E, g.col, g.rev, g.shift, s);
   if (E > 0)
     node::geometry_kernel<<<blocks(E, 256), 256, 0, s>>>(N, E, g.row_ptr, g.col, g.shift, g.pos, g.struct_id, g.cell,
                                                          static_cast<double>(st->m.r_c), g.src, g.d, g.u, g.c, g.dc);

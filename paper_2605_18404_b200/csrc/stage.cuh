@@ -14,6 +14,8 @@
 
 namespace janus {
 
+class LmBuilder;
+
 enum UnitKind { kEmbed = 0, kMsg = 1, kUpd = 2, kReadout = 3 };
 
 inline UnitKind unit_kind(int u, int L) {
@@ -110,6 +112,7 @@ struct janus_stage {
   std::vector<void*> host_allocs;  // pinned (cudaHostAlloc)
   janus::LoadLayout lay;           // upload block layout (capacity offsets)
   int64_t static_bytes = 0, arena_bytes = 0;
+  janus::LmBuilder* lm = nullptr;  // device neighbour-list builder (lazy, janus_stage_load without a CSR)
 
   float* P(int u) const { return params + uoff[static_cast<size_t>(u - u0)]; }
 

@@ -9,7 +9,13 @@ namespace janus {
 
 janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params);
 void stage_destroy(janus_stage* st);
-void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_t s, bool sync = true);
+struct DevCsrSlice;
+// LM.  hb.row_ptr == nullptr: the neighbour list is built on the device
+// (nbrlist.cu).  dcsr: col / shift / rev already on the device, as a slice of
+// a batched build (hb.row_ptr is then the host mirror of this batch's row_ptr
+// and hb.col/shift/rev are ignored).
+void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_t s, bool sync = true,
+                const DevCsrSlice* dcsr = nullptr);
 void stage_fe(janus_stage* st, int mb, int slot, cudaStream_t s, int lane = 0);
 void stage_ff(janus_stage* st, int mb, int slot, cudaStream_t s, int lane = 0);
 void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane = 0);
