@@ -229,6 +229,22 @@ int janus_trainer_plan(janus_trainer* t, int32_t* unit_ranges /* [P][2] */);
  * 128 lanes x N fp32 columns. */
 int janus_tc_probe(const int32_t* args, const float* A, const float* B, float* D);
 
+/* ---- GARS micro-batch packing (host only; include/janus/gars.hpp) ----
+ * SPEC.md:496-562, Algorithm 1.  Graph i has atoms[i] atoms and id i.
+ * order[M]: graph ids grouped by micro-batch (in shuffled order), mb_ptr[n_mb+1]
+ * the group offsets, tags[n_mb]: 0 comm_free / 1 dist (max size * d_gp <= total). */
+int janus_gars_pack(const int32_t* atoms, int32_t M, int32_t n_mb, int32_t d_gp, uint64_t seed, int32_t* order,
+                    int32_t* mb_ptr, int32_t* tags);
+/* Baseline: greedy sequential fixed-atom packing in dataset order. */
+int janus_gars_greedy(const int32_t* atoms, int32_t M, int32_t n_mb, int32_t d_gp, int32_t* order,
+                      int32_t* mb_ptr, int32_t* tags);
+/* Second-level GP bins of one comm_free micro-batch (atoms in its order): bin_of[n];
+ * kStateError for a dist micro-batch. */
+int janus_gars_assign_bins(const int32_t* atoms, int32_t n, int32_t d_gp, int32_t* bin_of);
+/* Synthetic long-tailed sizes: stats = {mean, P50, P90, P99, max} or NULL for
+ * the mixed preset (85, 53, 213, 427, 905); edges = 20 * atoms^1.3. */
+int janus_gars_synth_sizes(const double* stats, int32_t n, uint64_t seed, int32_t* atoms, int64_t* edges);
+
 /* ---- schedule generation (host only) ---- */
 int janus_schedule_generate(int method, int P, int n_mb, int k, char* buf, int64_t cap, int64_t* len);
 int janus_schedule_validate(const char* text, int32_t* n_errors);

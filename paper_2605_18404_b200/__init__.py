@@ -78,6 +78,10 @@ _sig("janus_nbrlist_create", c_int, ctypes.c_int32, ctypes.c_int32, ctypes.c_int
 _sig("janus_nbrlist_destroy", c_int, c_vp)
 _sig("janus_nbrlist_build_device", c_int, c_vp, ctypes.c_int32, ctypes.c_int32, c_vp, c_vp, c_vp, c_d, c_vp, c_vp,
      c_vp, c_vp, c_vp, c_vp)
+_sig("janus_gars_pack", c_int, c_vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, c_u64, c_vp, c_vp, c_vp)
+_sig("janus_gars_greedy", c_int, c_vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, c_vp, c_vp, c_vp)
+_sig("janus_gars_assign_bins", c_int, c_vp, ctypes.c_int32, ctypes.c_int32, c_vp)
+_sig("janus_gars_synth_sizes", c_int, c_vp, ctypes.c_int32, c_u64, c_vp, c_vp)
 _sig("janus_stage_create", c_int, c_vp, c_vp, c_vp)
 _sig("janus_stage_destroy", c_int, c_vp)
 _sig("janus_stage_load", c_int, c_vp, c_int, c_vp, c_vp)
@@ -248,6 +252,36 @@ def nbrlist_device(pos, struct_id, cell, r_c, max_edges=None, device: int = 0):
             _lib.janus_nbrlist_destroy(h)
         for p in ptrs:
             rt.cudaFree(p)
+
+
+# ------------------------------------------------------------------ GARS
+def gars_pack(atoms, n_mb: int, d_gp: int = 1, seed: int = 0, greedy: bool = False):
+    """janus_gars_pack (or the greedy sequential baseline): list of
+    (graph ids in micro-batch order, tag) per micro-batch; tag 0 comm_free, 1 dist."""
+    a = np.ascontiguousarray(atoms, np.int32)
+    order = np.zeros(len(a), np.int32)
+    ptr = np.zeros(n_mb + 1, np.int32)
+    tags = np.zeros(n_mb, np.int32)
+    if greedy:
+        check(_lib.janus_gars_greedy(_p(a), len(a), n_mb, d_gp, _p(order), _p(ptr), _p(tags)))
+    else:
+        check(_lib.janus_gars_pack(_p(a), len(a), n_mb, d_gp, seed, _p(order), _p(ptr), _p(tags)))
+    return [(order[ptr[j]:ptr[j + 1]].tolist(), int(tags[j])) for j in range(n_mb)]
+
+
+def gars_assign_bins(sizes, d_gp: int):
+    a = np.ascontiguousarray(sizes, np.int32)
+    out = np.zeros(len(a), np.int32)
+    check(_lib.janus_gars_assign_bins(_p(a), len(a), d_gp, _p(out)))
+    return out.tolist()
+
+
+def gars_synth_sizes(n: int, seed: int, stats=None):
+    a = np.zeros(n, np.int32)
+    e = np.zeros(n, np.int64)
+    st = None if stats is None else np.ascontiguousarray(stats, np.float64)
+    check(_lib.janus_gars_synth_sizes(None if st is None else _p(st), n, seed, _p(a), _p(e)))
+    return a, e
 
 
 def synth_cell(n_atoms: int, rho: float, n_species: int, seed: int):

@@ -9,6 +9,7 @@
 #include <string>
 
 #include "../../include/janus/errors.hpp"
+#include "../../include/janus/gars.hpp"
 #include "../../include/janus/schedule_gen.hpp"
 #include "../../include/janus_cuda.h"
 #include "cuda_check.hpp"
@@ -442,6 +443,69 @@ int janus_schedule_replay(const char* text, const double* t, double* makespan, d
     const janus::BubbleReport b = janus::bubble_of(g, r, d);
     *makespan = r.makespan;
     *bubble_ratio = b.bubble_ratio;
+  });
+}
+
+// ------------------------------------------------------------------ GARS
+namespace {
+std::vector<janus::gars::AtomGraph> graphs_of(const int32_t* atoms, int32_t M) {
+  need(atoms, "atoms");
+  if (M < 1) throw janus::domain_error("GARS: empty batch");
+  std::vector<janus::gars::AtomGraph> g(static_cast<size_t>(M));
+  for (int32_t i = 0; i < M; ++i) g[static_cast<size_t>(i)] = janus::gars::AtomGraph{i, atoms[i], 0};
+  return g;
+}
+void write_packing(const std::vector<janus::gars::PackedMicroBatch>& mbs, int d_gp, int32_t* order, int32_t* mb_ptr,
+                   int32_t* tags) {
+  need(order, "order");
+  need(mb_ptr, "mb_ptr");
+  int32_t k = 0;
+  mb_ptr[0] = 0;
+  for (size_t j = 0; j < mbs.size(); ++j) {
+    for (const auto& g : mbs[j].graphs) order[k++] = static_cast<int32_t>(g.id);
+    mb_ptr[j + 1] = k;
+    if (tags) tags[j] = static_cast<int32_t>(mbs[j].graphs.empty() ? janus::gars::MbTag::comm_free
+                                                                    : janus::gars::tag_of(mbs[j].graphs, d_gp));
+  }
+}
+}  // namespace
+
+int janus_gars_pack(const int32_t* atoms, int32_t M, int32_t n_mb, int32_t d_gp, uint64_t seed, int32_t* order,
+                    int32_t* mb_ptr, int32_t* tags) {
+  return guard([&] {
+    const auto mbs = janus::gars::pack_and_shuffle(graphs_of(atoms, M), n_mb, d_gp, seed);
+    write_packing(mbs, d_gp, order, mb_ptr, tags);
+  });
+}
+int janus_gars_greedy(const int32_t* atoms, int32_t M, int32_t n_mb, int32_t d_gp, int32_t* order,
+                      int32_t* mb_ptr, int32_t* tags) {
+  return guard([&] {
+    if (d_gp < 1) throw janus::domain_error("d_gp must be >= 1");
+    const auto mbs = janus::gars::greedy_sequential(graphs_of(atoms, M), n_mb);
+    write_packing(mbs, d_gp, order, mb_ptr, tags);
+  });
+}
+int janus_gars_assign_bins(const int32_t* atoms, int32_t n, int32_t d_gp, int32_t* bin_of) {
+  return guard([&] {
+    need(bin_of, "bin_of");
+    janus::gars::PackedMicroBatch mb;
+    mb.graphs = graphs_of(atoms, n);
+    mb.tag = janus::gars::tag_of(mb.graphs, d_gp);
+    const auto r = janus::gars::assign_gp_bins(mb, d_gp);
+    for (size_t b = 0; b < r.gp_bins.size(); ++b)
+      for (auto id : r.gp_bins[b]) bin_of[id] = static_cast<int32_t>(b);
+  });
+}
+int janus_gars_synth_sizes(const double* stats, int32_t n, uint64_t seed, int32_t* atoms, int64_t* edges) {
+  return guard([&] {
+    need(atoms, "atoms");
+    janus::gars::SizeStats s = janus::gars::mixed_preset();
+    if (stats) s = janus::gars::SizeStats{stats[0], stats[1], stats[2], stats[3], stats[4]};
+    const auto g = janus::gars::synth_dataset(s, n, seed);
+    for (int32_t i = 0; i < n; ++i) {
+      atoms[i] = g[static_cast<size_t>(i)].atoms;
+      if (edges) edges[i] = g[static_cast<size_t>(i)].edges;
+    }
   });
 }
 
