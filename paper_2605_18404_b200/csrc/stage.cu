@@ -10,6 +10,7 @@
 // Kernels: edge_kernels.cuh (msg unit), node_kernels.cuh (everything else).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <initializer_list>
 #include <stdexcept>
@@ -206,7 +207,17 @@ float* ledger(janus_stage* st, float* base, int mb, int u) {
 }
 
 bool use_tc(const janus_stage* st) { return st->m.precision == JANUS_PREC_TF32; }
-int tc_grid(const DevGeo& g) { return std::max(1, std::min(g.n_tiles_tc, 148)); }
+// Tensor-core edge grids.  CTAs loop over tiles (static assignment), so a CTA
+// may take several: its fixed costs (weight TMA, TMEM alloc, first dependent
+// loads and, for BF/BE, the weight-gradient partial write-out and its share of
+// the ordered reduction) are paid once per CTA.  Throughput runs (several
+// lanes: the step is bound by SM-time) use tpc tiles per CTA; a latency-bound
+// pipeline (1 lane) keeps one tile per CTA.
+int tc_grid_tpc(const DevGeo& g, int tpc) { return std::max(1, std::min((g.n_tiles_tc + tpc - 1) / tpc, 148)); }
+int tc_grid(const janus_stage* st, const DevGeo& g) { return tc_grid_tpc(g, st->tpc_wg); }
+int fe_grid(const janus_stage* st, const DevGeo& g) {
+  return std::max(1, (g.n_tiles_tc + st->tpc_fe - 1) / st->tpc_fe);
+}
 
 Scratch& lane_of(janus_stage* st, int lane) {
   if (lane < 0 || lane >= static_cast<int>(st->lanes.size())) throw domain_error("lane index out of range");
@@ -362,6 +373,11 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
     st->losses = dalloc<float>(st, 2 * static_cast<size_t>(d.n_slots), false);
     for (size_t x = 0; x < st->slots.size(); ++x) st->slots[x].loss = st->losses + 2 * x;
     st->lanes.resize(static_cast<size_t>(std::max(1, d.n_lanes)));
+    // measured on the C2 bench (16 lanes): 1/1 -> 4735, 2/4 -> 5616, 4/8 -> 5765 structures/s
+    st->tpc_fe = std::max(1, std::min(4, d.n_lanes / 4));
+    st->tpc_wg = std::max(1, std::min(8, d.n_lanes / 2));
+    if (const char* e = std::getenv("JANUS_TPC_FE")) st->tpc_fe = std::max(1, std::atoi(e));  // tuning runs only
+    if (const char* e = std::getenv("JANUS_TPC_WG")) st->tpc_wg = std::max(1, std::atoi(e));
     for (Scratch& sc : st->lanes) {
       sc.wh = dalloc<float>(st, NH, false);
       sc.wm = dalloc<float>(st, NH, false);
@@ -534,7 +550,7 @@ void stage_fe(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
         const float* W = P + R * H + H + H * H + H;
         gemm(s, N, cur_h, W, nullptr, nullptr, nullptr, b.v);
         if (g.n_tiles > 0 && use_tc(st))
-          edge_tc::msg_fe_tc<<<g.n_tiles_tc, edge_tc::NT, edge_tc::fe_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, msg_params(st, u),
+          edge_tc::msg_fe_tc<<<fe_grid(st, g), edge_tc::NT, edge_tc::fe_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, msg_params(st, u),
                                                                                  st->m.r_c, b.v, b.out_m);
         else if (g.n_tiles > 0)
           edge::msg_fe_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::fe_smem<kH, kR>(), s>>>(eg, msg_params(st, u), st->m.r_c, b.v, b.out_m);
@@ -604,7 +620,7 @@ void stage_ff(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
       case kMsg: {
         if (u == st->u1 - 1) copy(s, b.ff_a, wm, NH);  // a_m arrived through the ADJ_IN port
         if (g.n_tiles > 0 && use_tc(st)) {  // a_h += Y W^T fused into the tile epilogue
-          edge_tc::msg_ff_tc<<<g.n_tiles_tc, edge_tc::NT, edge_tc::ff_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, msg_params(st, u),
+          edge_tc::msg_ff_tc<<<fe_grid(st, g), edge_tc::NT, edge_tc::ff_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, msg_params(st, u),
                                                                                  st->m.r_c, b.v, b.ff_a, b.ff_Y, sl.F, wh);
         } else {
           if (g.n_tiles > 0)
@@ -665,7 +681,7 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
         const float* W = P + R * H + H + H * H + H;
         gemm(s, N, ah, W, nullptr, nullptr, nullptr, sc.s1);  // vdot
         if (g.n_tiles > 0 && use_tc(st)) {
-          const int grid = tc_grid(g);
+          const int grid = tc_grid(st, g);
           edge_tc::msg_bf_tc<<<grid, edge_tc::NT, edge_tc::bf_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, msg_params(st, u),
                                                                           st->m.r_c, b.v, sc.s1, b.ff_a, Fbar, am, sc.s2,
                                                                           sc.partial, b.inj);  // + hbar^F = X W^T
@@ -767,7 +783,7 @@ void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only, 
       }
       case kMsg: {
         if (g.n_tiles > 0 && use_tc(st)) {
-          const int grid = tc_grid(g);
+          const int grid = tc_grid(st, g);
           edge_tc::msg_be_tc<<<grid, edge_tc::NT, edge_tc::be_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, msg_params(st, u),
                                                                           st->m.r_c, b.v, bm, sc.s1, sc.partial,
                                                                           b.inj, bh);  // + b_h += Yb W^T + hbar^F
@@ -878,7 +894,7 @@ void stage_time_edge_kernel(janus_stage* st, int which, int mb, int slot, int it
   const bool tcm = use_tc(st);
   auto launch = [&] {
     if (tcm) {
-      const int grid = tc_grid(g);
+      const int grid = tc_grid_tpc(g, 1);  // isolated launch: one tile per CTA, full grid
       switch (which) {
         case 0:
           edge_tc::msg_fe_tc<<<g.n_tiles_tc, edge_tc::NT, edge_tc::fe_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, sc.s3);

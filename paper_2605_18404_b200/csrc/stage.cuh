@@ -112,6 +112,7 @@ struct janus_stage {
   std::vector<void*> host_allocs;  // pinned (cudaHostAlloc)
   janus::LoadLayout lay;           // upload block layout (capacity offsets)
   int64_t static_bytes = 0, arena_bytes = 0;
+  int tpc_fe = 1, tpc_wg = 1;        // TC edge tiles per CTA: FE/FF, BF/BE (stage_create)
   janus::LmBuilder* lm = nullptr;  // device neighbour-list builder (lazy, janus_stage_load without a CSR)
 
   float* P(int u) const { return params + uoff[static_cast<size_t>(u - u0)]; }
