@@ -245,6 +245,15 @@ int janus_gars_assign_bins(const int32_t* atoms, int32_t n, int32_t d_gp, int32_
  * the mixed preset (85, 53, 213, 427, 905); edges = 20 * atoms^1.3. */
 int janus_gars_synth_sizes(const double* stats, int32_t n, uint64_t seed, int32_t* atoms, int64_t* edges);
 
+/* ---- cost model + WaveK tuner (host only; include/janus/tuner.hpp) ----
+ * SPEC.md:387-395 (lifetime-rule peak memory), 578-637 (tuner).  t[4] =
+ * measured per-stage phase times {FE, FF, BE, BF}; mem[6] = {M_GPU,
+ * M_reserve, M_static, fe_bytes, ff_bytes, stage0_mult} in bytes (fe/ff =
+ * activation bytes one micro-batch keeps live FE->BE / FF->BF per device).
+ * table[n][5] = {k, makespan, bubble_ratio, peak_max_bytes, feasible}. */
+int janus_tune_wavek(int32_t P, int32_t n_mb, const double* t, const double* mem, int32_t divisors_only,
+                     int32_t* k_star, int32_t* tuned, double* table, int32_t cap, int32_t* n);
+
 /* ---- schedule generation (host only) ---- */
 int janus_schedule_generate(int method, int P, int n_mb, int k, char* buf, int64_t cap, int64_t* len);
 int janus_schedule_validate(const char* text, int32_t* n_errors);

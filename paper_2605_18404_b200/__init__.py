@@ -82,6 +82,8 @@ _sig("janus_gars_pack", c_int, c_vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_in
 _sig("janus_gars_greedy", c_int, c_vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, c_vp, c_vp, c_vp)
 _sig("janus_gars_assign_bins", c_int, c_vp, ctypes.c_int32, ctypes.c_int32, c_vp)
 _sig("janus_gars_synth_sizes", c_int, c_vp, ctypes.c_int32, c_u64, c_vp, c_vp)
+_sig("janus_tune_wavek", c_int, ctypes.c_int32, ctypes.c_int32, c_vp, c_vp, ctypes.c_int32, c_vp, c_vp, c_vp,
+     ctypes.c_int32, c_vp)
 _sig("janus_stage_create", c_int, c_vp, c_vp, c_vp)
 _sig("janus_stage_destroy", c_int, c_vp)
 _sig("janus_stage_load", c_int, c_vp, c_int, c_vp, c_vp)
@@ -252,6 +254,21 @@ def nbrlist_device(pos, struct_id, cell, r_c, max_edges=None, device: int = 0):
             _lib.janus_nbrlist_destroy(h)
         for p in ptrs:
             rt.cudaFree(p)
+
+
+# ------------------------------------------------------------------ tuner
+def tune_wavek(P: int, n_mb: int, t, m_gpu: float, m_reserve: float, m_static: float, fe_bytes: float,
+               ff_bytes: float, stage0_mult: float = 1.0, divisors_only: bool = True):
+    """janus_tune_wavek: (k_star, tuned, rows of {k, makespan, bubble_ratio, peak_max, feasible})."""
+    tt = np.ascontiguousarray(t, np.float64)
+    mem = np.array([m_gpu, m_reserve, m_static, fe_bytes, ff_bytes, stage0_mult], np.float64)
+    ks, tu, n = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    table = np.zeros((max(n_mb, 1), 5))
+    check(_lib.janus_tune_wavek(P, n_mb, _p(tt), _p(mem), 1 if divisors_only else 0, ctypes.byref(ks),
+                                ctypes.byref(tu), _p(table), table.shape[0], ctypes.byref(n)))
+    rows = [dict(k=int(r[0]), makespan=float(r[1]), bubble_ratio=float(r[2]), peak_max=float(r[3]),
+                 feasible=bool(r[4])) for r in table[:n.value]]
+    return ks.value, bool(tu.value), rows
 
 
 # ------------------------------------------------------------------ GARS

@@ -11,6 +11,7 @@
 #include "../../include/janus/errors.hpp"
 #include "../../include/janus/gars.hpp"
 #include "../../include/janus/schedule_gen.hpp"
+#include "../../include/janus/tuner.hpp"
 #include "../../include/janus_cuda.h"
 #include "cuda_check.hpp"
 #include "executor.hpp"
@@ -506,6 +507,38 @@ int janus_gars_synth_sizes(const double* stats, int32_t n, uint64_t seed, int32_
       atoms[i] = g[static_cast<size_t>(i)].atoms;
       if (edges) edges[i] = g[static_cast<size_t>(i)].edges;
     }
+  });
+}
+
+// ------------------------------------------------------------------ tuner
+int janus_tune_wavek(int32_t P, int32_t n_mb, const double* t, const double* mem, int32_t divisors_only,
+                     int32_t* k_star, int32_t* tuned, double* table, int32_t cap, int32_t* n) {
+  return guard([&] {
+    need(t, "t");
+    need(mem, "mem");
+    need(k_star, "k_star");
+    need(n, "n");
+    janus::PhaseTimes pt{t[0], t[1], t[2], t[3]};
+    janus::tuner::MemoryParams mp;
+    mp.m_gpu = mem[0];
+    mp.m_reserve = mem[1];
+    mp.static_bytes = {mem[2]};
+    mp.fe_bytes = mem[3];
+    mp.ff_bytes = mem[4];
+    mp.stage0_mult = mem[5];
+    const janus::tuner::TuneResult r = janus::tuner::tune(P, n_mb, pt, mp, divisors_only != 0);
+    *k_star = r.k_star;
+    if (tuned) *tuned = r.tuned ? 1 : 0;
+    *n = static_cast<int32_t>(r.table.size());
+    if (table)
+      for (int32_t i = 0; i < std::min(cap, *n); ++i) {
+        const auto& c = r.table[static_cast<size_t>(i)];
+        table[5 * i + 0] = c.k;
+        table[5 * i + 1] = c.makespan;
+        table[5 * i + 2] = c.bubble_ratio;
+        table[5 * i + 3] = c.peak_max;
+        table[5 * i + 4] = c.feasible ? 1.0 : 0.0;
+      }
   });
 }
 
