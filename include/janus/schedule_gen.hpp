@@ -123,6 +123,33 @@ inline Schedule onef1b_2nd(int P, int N_mb) {
   return out;
 }
 
+/// Hanayo-2nd baseline (§5.1 "single wave
+/// (W=1, S=2P)"): the V-shape placement of fold_map (virtual stage s_v on
+/// device fold_map(s_v), intra-device hand-offs pruned) with wave-style
+/// ordering instead of SymFold's folded 1F1B: every instruction of micro-batch
+/// m belongs to the synchronous wave step at which m reaches its virtual stage
+/// (forward s_v: m + s_v; backward s_v: m + 4P - 1 - s_v), and each device
+/// issues in (step, backward first, micro-batch) order — the projection of one
+/// global topological order, so deadlock-free.  Every FF carries the
+/// recompute flag: the baseline lacks SymFold's FE-activation reuse, so the
+/// executor re-runs the block's FE before its FF.
+inline Schedule hanayo_2nd(int P, int N_mb) {
+  if (P < 1) throw domain_error("hanayo_2nd: P must be >= 1");
+  const Schedule v = symfold(P, N_mb);
+  Schedule out = transform::priority_topo_order(v, [P](const Instruction& in) {
+    if (in.micro_batch < 0) return std::tuple<int, int, int>{std::numeric_limits<int>::max(), 0, 0};  // OS / AR last
+    const bool fwd = is_forward_flow(in.kind);
+    const int vs = in.virtual_stage < 0 ? 0 : in.virtual_stage;
+    const int step = fwd ? in.micro_batch + vs : in.micro_batch + 4 * P - 1 - vs;
+    return std::tuple<int, int, int>{step, fwd ? 1 : 0, in.micro_batch};
+  });
+  for (auto& dl : out.device_lists)
+    for (auto& in : dl)
+      if (in.kind == InstrKind::FF) in.flags |= kFlagRecompute;
+  renumber_seq(out);
+  return out;
+}
+
 // ---------------------------------------------------------------------------
 // Phase times (costmodel PhaseTimes).
 // ---------------------------------------------------------------------------

@@ -177,7 +177,7 @@ int janus_comm_allreduce_sum(janus_comm* c, float* buf, int64_t count, void* str
  * the stage(s) of rank r over janus_comm (P2P per flow + allreduce). */
 typedef struct {
   int32_t n_stages;        /* P */
-  int32_t method;          /* 0 SymFold, 1 WaveK, 2 1F1B-2nd */
+  int32_t method;          /* 0 SymFold, 1 WaveK, 2 1F1B-2nd, 4 Hanayo-2nd */
   int32_t wavek_k;
   int32_t n_micro_batches; /* per replica */
   int32_t local_stages;    /* 1 = all P stages in this process on one GPU */
@@ -254,7 +254,16 @@ int janus_gars_synth_sizes(const double* stats, int32_t n, uint64_t seed, int32_
 int janus_tune_wavek(int32_t P, int32_t n_mb, const double* t, const double* mem, int32_t divisors_only,
                      int32_t* k_star, int32_t* tuned, double* table, int32_t cap, int32_t* n);
 
+/* ---- timeline rendering (host only; include/janus/render.hpp) ----
+ * recs[n][5] = {device, phase (0 FE 1 FF 2 BE 3 BF), mb, start, end}, e.g. the
+ * executor timeline (janus_trainer_timeline) or a replay (text != NULL: the
+ * schedule is replayed under t[4] and recs is ignored).  fmt 0 = ASCII (one
+ * column per `quantum`), 1 = SVG (`quantum` = pixels per time unit). */
+int janus_render_timeline(const double* recs, int32_t n, const char* text, const double* t, int32_t fmt,
+                          double quantum, char* buf, int64_t cap, int64_t* len);
+
 /* ---- schedule generation (host only) ---- */
+/* method: 0 SymFold, 1 WaveK(k), 2 1F1B-2nd, 3 first-order Pass 0, 4 Hanayo-2nd */
 int janus_schedule_generate(int method, int P, int n_mb, int k, char* buf, int64_t cap, int64_t* len);
 int janus_schedule_validate(const char* text, int32_t* n_errors);
 /* Replay (graph.hpp:168) a schedule under phase times t[4] = {FE, FF, BE, BF}

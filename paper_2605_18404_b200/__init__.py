@@ -31,7 +31,7 @@ c_int, c_i64, c_u64, c_f, c_d, c_vp, c_sz = (ctypes.c_int, ctypes.c_int64, ctype
 PREC_FP32, PREC_TF32 = 0, 1
 (PORT_ACT_IN, PORT_ACT_OUT, PORT_ADJ_IN, PORT_ADJ_OUT, PORT_TAN_IN, PORT_TAN_OUT, PORT_BADJ_IN,
  PORT_BADJ_OUT) = range(8)
-METHOD_SYMFOLD, METHOD_WAVEK, METHOD_ONEF1B, METHOD_FIRST = 0, 1, 2, 3
+METHOD_SYMFOLD, METHOD_WAVEK, METHOD_ONEF1B, METHOD_FIRST, METHOD_HANAYO = 0, 1, 2, 3, 4
 
 
 class ModelDesc(ctypes.Structure):
@@ -84,6 +84,8 @@ _sig("janus_gars_assign_bins", c_int, c_vp, ctypes.c_int32, ctypes.c_int32, c_vp
 _sig("janus_gars_synth_sizes", c_int, c_vp, ctypes.c_int32, c_u64, c_vp, c_vp)
 _sig("janus_tune_wavek", c_int, ctypes.c_int32, ctypes.c_int32, c_vp, c_vp, ctypes.c_int32, c_vp, c_vp, c_vp,
      ctypes.c_int32, c_vp)
+_sig("janus_render_timeline", c_int, c_vp, ctypes.c_int32, ctypes.c_char_p, c_vp, ctypes.c_int32, c_d, c_vp, c_i64,
+     c_vp)
 _sig("janus_stage_create", c_int, c_vp, c_vp, c_vp)
 _sig("janus_stage_destroy", c_int, c_vp)
 _sig("janus_stage_load", c_int, c_vp, c_int, c_vp, c_vp)
@@ -254,6 +256,21 @@ def nbrlist_device(pos, struct_id, cell, r_c, max_edges=None, device: int = 0):
             _lib.janus_nbrlist_destroy(h)
         for p in ptrs:
             rt.cudaFree(p)
+
+
+# ------------------------------------------------------------------ render
+def render_timeline(recs=None, text=None, t=None, svg=False, quantum=1.0) -> str:
+    """ASCII / SVG timeline of executor records ([n][5]: device, phase, mb, start, end)
+    or of a schedule text replayed under phase times t = (FE, FF, BE, BF)."""
+    r = None if recs is None else np.ascontiguousarray(recs, np.float64)
+    tt = None if t is None else np.ascontiguousarray(t, np.float64)
+    args = (None if r is None else _p(r), 0 if r is None else r.shape[0], None if text is None else text.encode(),
+            None if tt is None else _p(tt), 1 if svg else 0, quantum)
+    n = c_i64()
+    check(_lib.janus_render_timeline(*args, None, 0, ctypes.byref(n)))
+    buf = ctypes.create_string_buffer(n.value + 1)
+    check(_lib.janus_render_timeline(*args, buf, n.value + 1, ctypes.byref(n)))
+    return buf.value.decode()
 
 
 # ------------------------------------------------------------------ tuner

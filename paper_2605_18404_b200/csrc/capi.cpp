@@ -10,6 +10,7 @@
 
 #include "../../include/janus/errors.hpp"
 #include "../../include/janus/gars.hpp"
+#include "../../include/janus/render.hpp"
 #include "../../include/janus/schedule_gen.hpp"
 #include "../../include/janus/tuner.hpp"
 #include "../../include/janus_cuda.h"
@@ -404,6 +405,7 @@ int janus_schedule_generate(int method, int P, int n_mb, int k, char* buf, int64
       case 1: s = janus::wavek(P, n_mb, k); break;
       case 2: s = janus::onef1b_2nd(P, n_mb); break;
       case 3: s = janus::gen_first_order(P, n_mb); break;
+      case 4: s = janus::hanayo_2nd(P, n_mb); break;
       default: throw janus::domain_error("unknown schedule method");
     }
     const std::string text = janus::serialize(s);
@@ -539,6 +541,36 @@ int janus_tune_wavek(int32_t P, int32_t n_mb, const double* t, const double* mem
         table[5 * i + 3] = c.peak_max;
         table[5 * i + 4] = c.feasible ? 1.0 : 0.0;
       }
+  });
+}
+
+// ------------------------------------------------------------------ render
+int janus_render_timeline(const double* recs, int32_t n, const char* text, const double* t, int32_t fmt,
+                          double quantum, char* buf, int64_t cap, int64_t* len) {
+  return guard([&] {
+    need(len, "len");
+    std::vector<janus::render::Span> spans;
+    if (text) {
+      need(t, "t");
+      const janus::Schedule s = janus::deserialize(text);
+      const janus::DepGraph g = janus::build_dependencies(s);
+      const janus::PhaseTimes pt{t[0], t[1], t[2], t[3]};
+      const janus::ReplayResult r = janus::replay(g, janus::phase_durations(g, pt));
+      if (!r.ok) throw janus::deadlock_error("render: replay stalled: " + r.blocked);
+      spans = janus::render::spans_of(g, r);
+    } else {
+      if (n > 0) need(recs, "recs");
+      for (int32_t i = 0; i < n; ++i)
+        spans.push_back(janus::render::Span{static_cast<int>(recs[5 * i]), static_cast<int>(recs[5 * i + 1]),
+                                            static_cast<int>(recs[5 * i + 2]), recs[5 * i + 3], recs[5 * i + 4]});
+    }
+    const std::string out = fmt == 1 ? janus::render::svg(spans, quantum) : janus::render::ascii(spans, quantum);
+    *len = static_cast<int64_t>(out.size());
+    if (buf && cap > 0) {
+      const size_t k = std::min<size_t>(out.size(), static_cast<size_t>(cap - 1));
+      std::memcpy(buf, out.data(), k);
+      buf[k] = '\0';
+    }
   });
 }
 

@@ -514,6 +514,7 @@ janus_trainer* trainer_create(const janus_exec_desc& ed, const janus_stage_desc&
     case 0: t->sched = symfold(t->P, ed.n_micro_batches); break;
     case 1: t->sched = wavek(t->P, ed.n_micro_batches, ed.wavek_k); break;
     case 2: t->sched = onef1b_2nd(t->P, ed.n_micro_batches); break;
+    case 4: t->sched = hanayo_2nd(t->P, ed.n_micro_batches); break;  // V-shape + wave order, FF recompute
     default: throw domain_error("unknown method");
   }
   const ValidationReport vr = validate_schedule(t->sched);

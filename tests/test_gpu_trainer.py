@@ -67,7 +67,7 @@ def test_symfold_p1_matches_oracle(janus, data):
     t.close()
 
 
-@pytest.mark.parametrize("P,method,k", [(2, 0, 1), (4, 0, 1), (4, 1, 2), (4, 1, 4), (6, 0, 1)])
+@pytest.mark.parametrize("P,method,k", [(2, 0, 1), (4, 0, 1), (4, 1, 2), (4, 1, 4), (6, 0, 1), (2, 4, 1), (4, 4, 1)])
 def test_pipeline_bit_identical_to_p1(janus, data, P, method, k):
     m, params, batches, g_ref, _ = data
     t1, g1, p1, _ = run(janus, m, params, batches, 1, janus.METHOD_SYMFOLD)

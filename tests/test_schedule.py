@@ -144,3 +144,46 @@ def test_wavek_beats_symfold_and_1f1b_in_replay():
     best = min(v for k, v in ms.items() if k.startswith("wavek"))
     assert best <= ms["symfold"] < ms["onef1b_2nd"]
     assert all(l.endswith("valid 1") for l in _lines(out))
+
+
+def test_hanayo_2nd_baseline(janus):
+    """Hanayo-2nd: V-shape = fold_map placement,
+    valid for P 1..8 x N 4..12, FF carries the recompute flag, hanayo_2nd(1,1)
+    keeps both virtual stages on D0; under Table 4 times it is slower than
+    SymFold (it recomputes FE inside FF)."""
+    for P in (1, 2, 3, 4, 8):
+        for N in (1, 4, 8, 12):
+            text = janus.schedule_text(janus.METHOD_HANAYO, P, N)
+            assert janus.validate_schedule(text) == 0, (P, N)
+            sym = janus.schedule_text(janus.METHOD_SYMFOLD, P, N)
+            # same instructions per device as SymFold (V placement), wave order, FF recompute
+            body = lambda t: sorted(" ".join(l.replace(" flags=recompute", "").split()[:1] +  # noqa: E731
+                                             l.replace(" flags=recompute", "").split()[2:])
+                                    for l in t.splitlines()[1:])
+            assert body(text) == body(sym), (P, N)
+            ff = [l for l in text.splitlines()[1:] if l.split()[2] == "FF"]
+            assert ff and all(l.endswith("flags=recompute") for l in ff), ff[:2]
+    t1 = janus.schedule_text(janus.METHOD_HANAYO, 1, 1)
+    assert {l.split()[0] for l in t1.splitlines()[1:]} == {"D0"}
+    uma = (26.25, 37.51, 43.59, 82.03)
+    for P in (4, 8):
+        mh, _ = janus.schedule_replay(janus.schedule_text(janus.METHOD_HANAYO, P, 2 * P), *uma)
+        ms, _ = janus.schedule_replay(janus.schedule_text(janus.METHOD_SYMFOLD, P, 2 * P), *uma)
+        assert ms < mh
+
+
+def test_render_timeline(janus):
+    """render: symfold(1,1) lane reads FE FF BF BE; byte-identical reruns; SVG well-formed."""
+    txt = janus.schedule_text(janus.METHOD_SYMFOLD, 1, 1)
+    a = janus.render_timeline(text=txt, t=(1, 2, 3, 4), quantum=0)
+    lane = a.splitlines()[0]
+    assert [lane.index(x) for x in ("FE", "FF", "BF", "BE")] == sorted(lane.index(x) for x in ("FE", "FF", "BF", "BE"))
+    assert a == janus.render_timeline(text=txt, t=(1, 2, 3, 4), quantum=0)
+    w = janus.schedule_text(janus.METHOD_WAVEK, 4, 12, 4)
+    r4 = janus.render_timeline(text=w, t=(26.25, 37.51, 43.59, 82.03), quantum=10)
+    assert len(r4.splitlines()) == 4 and r4 == janus.render_timeline(text=w, t=(26.25, 37.51, 43.59, 82.03), quantum=10)
+    svg = janus.render_timeline(text=w, t=(26.25, 37.51, 43.59, 82.03), svg=True, quantum=0.5)
+    assert svg.startswith("<svg") and svg.rstrip().endswith("</svg>") and svg.count("<rect") == 4 * 4 * 12
+    recs = [[0, 0, 0, 0.0, 1.0], [0, 1, 0, 1.0, 3.0], [1, 3, 0, 3.0, 7.0]]
+    out = janus.render_timeline(recs=recs, quantum=0.5)
+    assert out.splitlines()[0].startswith("D0 |FEFF==") and out.splitlines()[1].startswith("D1 |......BF")

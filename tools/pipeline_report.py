@@ -103,7 +103,7 @@ def run(model, params, batches, P, method, k, steps=3, warmup=2):
         phase[name] = float((d[:, 4] - d[:, 3]).mean()) if len(d) else 0.0
     text = t.schedule_text()
     # replay with measured per-instruction means (FF of 1F1B already contains the recompute)
-    ff = phase["FF"] - (phase["FE"] if method == J.METHOD_ONEF1B else 0.0)
+    ff = phase["FF"] - (phase["FE"] if method in (J.METHOD_ONEF1B, J.METHOD_HANAYO) else 0.0)
     pred_ms, pred_bubble = J.schedule_replay(text, phase["FE"], max(ff, 1e-6), phase["BE"], phase["BF"])
     plan = t.plan()
     mem = []
@@ -116,12 +116,13 @@ def run(model, params, batches, P, method, k, steps=3, warmup=2):
                 sizes[q] += x
         peak = peak_live(tl, dv, sizes)
         mem.append({"device": dv, "static_plus_arena_bytes": int(s.peak_bytes[dv]), "peak_live_activation_bytes": int(peak)})
-    out = {"P": P, "method": {0: "symfold", 1: "wavek", 2: "onef1b_2nd"}[method], "k": k,
+    out = {"P": P, "method": {0: "symfold", 1: "wavek", 2: "onef1b_2nd", 4: "hanayo_2nd"}[method], "k": k,
            "makespan_ms": s.makespan_ms, "structures_per_s": len(batches) / (s.makespan_ms / 1e3),
            "bubble_measured": s.bubble_ratio, "busy_ms": [s.busy_ms[d] for d in range(P)],
            "phase_mean_us": {k2: v * 1e3 / 1e3 for k2, v in phase.items()},
            "replay_makespan_ms": pred_ms / 1e3, "bubble_replay": pred_bubble,
-           "p2p_bytes_per_step": int(s.p2p_bytes), "memory": mem}
+           "p2p_bytes_per_step": int(s.p2p_bytes), "memory": mem,
+           "timeline_ascii": J.render_timeline(recs=tl, quantum=max(s.makespan_ms * 1e3 / 160, 1e-3))}
     t.close()
     return out
 
@@ -147,7 +148,8 @@ def main():
     batches = [J.synth_batch(model, [256], 0.095, 700 + m) for m in range(args.nmb)]
     rows = []
     for P in [int(x) for x in args.Ps.split(",")]:
-        for method, k in ((J.METHOD_ONEF1B, 1), (J.METHOD_SYMFOLD, 1), (J.METHOD_WAVEK, P), (J.METHOD_WAVEK, 2 * P)):
+        for method, k in ((J.METHOD_ONEF1B, 1), (J.METHOD_HANAYO, 1), (J.METHOD_SYMFOLD, 1), (J.METHOD_WAVEK, P),
+                          (J.METHOD_WAVEK, 2 * P)):
             r = run(model, params, batches, P, method, k)
             rows.append(r)
             print(json.dumps({x: r[x] for x in ("P", "method", "k", "makespan_ms", "structures_per_s", "bubble_measured",
