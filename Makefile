@@ -20,6 +20,11 @@ NCCL_INC :=
 NCCL_LINK := -L/usr/lib/x86_64-linux-gnu -lnccl
 endif
 NVFLAGS := $(NCCL_INC) -Iinclude -std=c++20 -O3 $(ARCH) -lineinfo -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
+ifneq ($(TC_NT),)  # tensor-core edge kernel CTA size experiment (512 default / 1024)
+OBJ := build/nt$(TC_NT)_obj
+LIB := build/nt$(TC_NT)/libjanus_b200.so
+NVFLAGS += -DJANUS_TC_NT=$(TC_NT)
+endif
 ifeq ($(TRACE),1)  # phase-traced profiling build (edge_tc.cuh TC_MARK), loaded via JANUS_LIB
 OBJ := build/trace_obj
 LIB := build/trace/libjanus_b200.so

@@ -39,6 +39,7 @@ struct MemoryParams {
   std::vector<double> static_bytes{0.0};
   double fe_bytes = 0, ff_bytes = 0;
   double stage0_mult = 1.0;
+  bool replicate_static = true;  // SPEC rule: replicated-parameter devices count static twice
   double m_mem() const { return m_gpu - m_reserve; }
   double static_of(int d) const {
     return static_bytes.size() == 1 ? static_bytes[0] : static_bytes.at(static_cast<std::size_t>(d));
@@ -53,6 +54,8 @@ inline std::vector<double> peak_memory(const DepGraph& g, const ReplayResult& r,
   const Schedule& s = *g.schedule;
   const int D = s.num_devices();
   std::vector<std::vector<std::pair<double, double>>> ev(static_cast<std::size_t>(D));
+  std::vector<std::vector<std::pair<int, double>>> recomputed(static_cast<std::size_t>(D));  // (mb, FF start)
+  std::vector<bool> replicated(static_cast<std::size_t>(D), false);
   for (int i = 0; i < g.size(); ++i) {
     const Instruction& in = *g.flat[static_cast<std::size_t>(i)];
     const int d = in.device;
@@ -62,10 +65,28 @@ inline std::vector<double> peak_memory(const DepGraph& g, const ReplayResult& r,
     switch (in.kind) {
       case InstrKind::FE: e.push_back({a, mult * mp.fe_bytes}); break;
       case InstrKind::BE: e.push_back({z, -mult * mp.fe_bytes}); break;
-      case InstrKind::FF: e.push_back({a, mult * mp.ff_bytes}); break;
+      case InstrKind::FF:
+        e.push_back({a, mult * mp.ff_bytes});
+        if (in.has_flag(kFlagRecompute)) recomputed[static_cast<std::size_t>(d)].push_back({in.micro_batch, a});
+        break;
       case InstrKind::BF: e.push_back({z, -mult * mp.ff_bytes}); break;
       default: break;
     }
+    if (in.kind == InstrKind::AR && in.has_flag(kFlagReplicatedParams)) replicated[static_cast<std::size_t>(d)] = true;
+  }
+  // baselines: an FF that recomputes FE holds those activations until the
+  // block's BF on that device ends; replicated parameters add the static
+  // bytes once more
+  for (int i = 0; i < g.size(); ++i) {
+    const Instruction& in = *g.flat[static_cast<std::size_t>(i)];
+    if (in.kind != InstrKind::BF) continue;
+    const int d = in.device;
+    for (const auto& [mb, t0] : recomputed[static_cast<std::size_t>(d)])
+      if (mb == in.micro_batch) {
+        const double mult = d == 0 ? mp.stage0_mult : 1.0;
+        ev[static_cast<std::size_t>(d)].push_back({t0, mult * mp.fe_bytes});
+        ev[static_cast<std::size_t>(d)].push_back({r.end[static_cast<std::size_t>(i)], -mult * mp.fe_bytes});
+      }
   }
   std::vector<double> peak(static_cast<std::size_t>(D), 0.0);
   for (int d = 0; d < D; ++d) {
@@ -76,7 +97,8 @@ inline std::vector<double> peak_memory(const DepGraph& g, const ReplayResult& r,
       live += x.second;
       best = std::max(best, live);
     }
-    peak[static_cast<std::size_t>(d)] = mp.static_of(d) + best;
+    const bool twice = mp.replicate_static && replicated[static_cast<std::size_t>(d)];
+    peak[static_cast<std::size_t>(d)] = mp.static_of(d) * (twice ? 2.0 : 1.0) + best;
   }
   return peak;
 }

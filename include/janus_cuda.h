@@ -113,6 +113,11 @@ int janus_nbrlist_build_device(janus_nbrlist* nl, int32_t n_atoms, int32_t n_str
                                const int32_t* struct_id, const double* cell, double r_c, int32_t* row_ptr,
                                int32_t* col, int32_t* shift, int32_t* rev, int32_t* n_edges, void* stream);
 
+/* Stage plan without a device: the trainer's min-max contiguous partition of
+ * the 2L+2 units into P blocks (include/janus/model.hpp partition_units).
+ * unit_ranges[P][2] = [begin, end). */
+int janus_plan_stages(const janus_model_desc* m, int32_t P, int32_t* unit_ranges);
+
 /* ---- stages ---- */
 int janus_stage_create(const janus_stage_desc* desc, const float* unit_params, janus_stage** out);
 int janus_stage_destroy(janus_stage* st);
@@ -253,6 +258,15 @@ int janus_gars_synth_sizes(const double* stats, int32_t n, uint64_t seed, int32_
  * table[n][5] = {k, makespan, bubble_ratio, peak_max_bytes, feasible}. */
 int janus_tune_wavek(int32_t P, int32_t n_mb, const double* t, const double* mem, int32_t divisors_only,
                      int32_t* k_star, int32_t* tuned, double* table, int32_t cap, int32_t* n);
+/* Lifetime-rule peak bytes per device of any schedule text replayed under
+ * t[4]; static_bytes[n_static] per device (n_static = 1: all devices),
+ * act[4] = {fe_bytes, ff_bytes, stage0_mult, replicate}.  FF with the
+ * recompute flag holds fe_bytes until its BF; with replicate != 0,
+ * replicated-parameter devices (AR flag) count static twice (the SPEC's
+ * uniform-static rule); 0 = static_bytes are exact per device.
+ * peaks[num devices]. */
+int janus_schedule_memory(const char* text, const double* t, const double* static_bytes, int32_t n_static,
+                          const double* act, double* peaks, int32_t cap, int32_t* n_devices);
 
 /* ---- timeline rendering (host only; include/janus/render.hpp) ----
  * recs[n][5] = {device, phase (0 FE 1 FF 2 BE 3 BF), mb, start, end}, e.g. the

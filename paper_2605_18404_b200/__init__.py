@@ -86,6 +86,8 @@ _sig("janus_tune_wavek", c_int, ctypes.c_int32, ctypes.c_int32, c_vp, c_vp, ctyp
      ctypes.c_int32, c_vp)
 _sig("janus_render_timeline", c_int, c_vp, ctypes.c_int32, ctypes.c_char_p, c_vp, ctypes.c_int32, c_d, c_vp, c_i64,
      c_vp)
+_sig("janus_schedule_memory", c_int, ctypes.c_char_p, c_vp, c_vp, ctypes.c_int32, c_vp, c_vp, ctypes.c_int32, c_vp)
+_sig("janus_plan_stages", c_int, c_vp, ctypes.c_int32, c_vp)
 _sig("janus_stage_create", c_int, c_vp, c_vp, c_vp)
 _sig("janus_stage_destroy", c_int, c_vp)
 _sig("janus_stage_load", c_int, c_vp, c_int, c_vp, c_vp)
@@ -286,6 +288,26 @@ def tune_wavek(P: int, n_mb: int, t, m_gpu: float, m_reserve: float, m_static: f
     rows = [dict(k=int(r[0]), makespan=float(r[1]), bubble_ratio=float(r[2]), peak_max=float(r[3]),
                  feasible=bool(r[4])) for r in table[:n.value]]
     return ks.value, bool(tu.value), rows
+
+
+def plan_stages(model: "Model", P: int) -> np.ndarray:
+    """Unit ranges [P][2] of the trainer's stage partition (no device needed)."""
+    out = np.zeros((P, 2), np.int32)
+    d = model.desc()
+    check(_lib.janus_plan_stages(ctypes.byref(d), P, _p(out)))
+    return out
+
+
+def schedule_memory(text: str, t, static_bytes, fe_bytes: float, ff_bytes: float, stage0_mult: float = 1.0,
+                    replicate: bool = True):
+    """Lifetime-rule peak bytes per device of a schedule replayed under t (janus_schedule_memory)."""
+    tt = np.ascontiguousarray(t, np.float64)
+    st = np.ascontiguousarray(np.atleast_1d(static_bytes), np.float64)
+    act = np.array([fe_bytes, ff_bytes, stage0_mult, 1.0 if replicate else 0.0], np.float64)
+    out = np.zeros(256)
+    n = ctypes.c_int32()
+    check(_lib.janus_schedule_memory(text.encode(), _p(tt), _p(st), len(st), _p(act), _p(out), 256, ctypes.byref(n)))
+    return out[:n.value].copy()
 
 
 # ------------------------------------------------------------------ GARS

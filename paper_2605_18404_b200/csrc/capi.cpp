@@ -10,6 +10,7 @@
 
 #include "../../include/janus/errors.hpp"
 #include "../../include/janus/gars.hpp"
+#include "../../include/janus/model.hpp"
 #include "../../include/janus/render.hpp"
 #include "../../include/janus/schedule_gen.hpp"
 #include "../../include/janus/tuner.hpp"
@@ -163,6 +164,24 @@ int janus_nbrlist_build_device(janus_nbrlist* nl, int32_t n_atoms, int32_t n_str
     need(n_edges, "n_edges");
     janus::nbrlist_enqueue(nl, n_atoms, n_struct, pos, struct_id, cell, r_c, row_ptr, col, shift, rev, S(stream));
     *n_edges = janus::nbrlist_finish(nl, S(stream));
+  });
+}
+
+int janus_plan_stages(const janus_model_desc* m, int32_t P, int32_t* unit_ranges) {
+  return guard([&] {
+    check_model(m);
+    need(unit_ranges, "unit_ranges");
+    janus::ModelConfig mc;
+    mc.L = m->L;
+    mc.H = m->H;
+    mc.R = m->R;
+    mc.n_species = m->n_species;
+    mc.r_c = m->r_c;
+    const janus::StagePlan plan = janus::partition_units(mc, P);
+    for (int b = 0; b < P; ++b) {
+      unit_ranges[2 * b] = plan.blocks[static_cast<size_t>(b)].first;
+      unit_ranges[2 * b + 1] = plan.blocks[static_cast<size_t>(b)].second;
+    }
   });
 }
 
@@ -571,6 +590,34 @@ int janus_render_timeline(const double* recs, int32_t n, const char* text, const
       std::memcpy(buf, out.data(), k);
       buf[k] = '\0';
     }
+  });
+}
+
+int janus_schedule_memory(const char* text, const double* t, const double* static_bytes, int32_t n_static,
+                          const double* act, double* peaks, int32_t cap, int32_t* n_devices) {
+  return guard([&] {
+    need(text, "text");
+    need(t, "t");
+    need(static_bytes, "static_bytes");
+    need(act, "act");
+    need(n_devices, "n_devices");
+    const janus::Schedule s = janus::deserialize(text);
+    const janus::DepGraph g = janus::build_dependencies(s);
+    const janus::PhaseTimes pt{t[0], t[1], t[2], t[3]};
+    const janus::ReplayResult r = janus::replay(g, janus::phase_durations(g, pt));
+    if (!r.ok) throw janus::deadlock_error("memory: replay stalled: " + r.blocked);
+    janus::tuner::MemoryParams mp;
+    if (n_static < 1) throw janus::domain_error("n_static must be >= 1");
+    mp.static_bytes.assign(static_bytes, static_bytes + n_static);
+    if (n_static != 1 && n_static != s.num_devices()) throw janus::domain_error("static_bytes: 1 or one per device");
+    mp.fe_bytes = act[0];
+    mp.ff_bytes = act[1];
+    mp.stage0_mult = act[2];
+    mp.replicate_static = act[3] != 0.0;
+    const std::vector<double> p = janus::tuner::peak_memory(g, r, mp);
+    *n_devices = static_cast<int32_t>(p.size());
+    if (peaks)
+      for (int32_t i = 0; i < std::min<int32_t>(cap, *n_devices); ++i) peaks[i] = p[static_cast<size_t>(i)];
   });
 }
 

@@ -27,7 +27,10 @@ namespace janus {
 namespace edge_tc {
 
 constexpr int TE = 128;
-constexpr int NT = 512;            // 16 warps: 4 threads per edge row
+#ifndef JANUS_TC_NT
+#define JANUS_TC_NT 512
+#endif
+constexpr int NT = JANUS_TC_NT;    // 512: 16 warps, 4 threads per edge row (1024: 8 per row)
 constexpr int NQ = NT / TE;        // feature quarters per edge
 constexpr int FPT = 64 / NQ;       // features per thread (16)
 constexpr int H = 64, R = 64;
@@ -123,7 +126,7 @@ struct Ctx {
     phase ^= 1u;
     tc::fence_after();
   }
-  __device__ void ld(uint32_t col, float (&v)[FPT]) const { tc::ld16(tmem + lane_base() + col + static_cast<uint32_t>(FPT * q), v); }
+  __device__ void ld(uint32_t col, float (&v)[FPT]) const { tc::ldv(tmem + lane_base() + col + static_cast<uint32_t>(FPT * q), v); }
 };
 
 // Weight tile for B operands: element (n, k) = src[k*64 + n] (transpose=true)
@@ -229,7 +232,8 @@ struct SegMap {
 __device__ __forceinline__ SegMap seg_map(const EdgeGeom& g, const TileRange& tr) {
   SegMap m;
   const int nr = tr.r1 - tr.r0;
-  m.split = nr <= 1 ? 8 : nr <= 2 ? 4 : nr <= 4 ? 2 : 1;
+  constexpr int S1 = NT / 64;  // threads per (row, feature) pair for a one-row tile
+  m.split = nr <= 1 ? S1 : nr <= 2 ? S1 / 2 : nr <= 4 ? S1 / 4 : S1 / 8;
   m.span = nr * 64;
   m.part = static_cast<int>(threadIdx.x) & (m.split - 1);
   m.pair = static_cast<int>(threadIdx.x) / m.split;
@@ -577,7 +581,12 @@ __global__ void __launch_bounds__(NT) msg_ff_tc(EdgeGeom g, const int4* __restri
           const int comp = fr % 3;
           const int eb = max(fb, c0), ee = min(fe, c0 + ne);
           for (int x = eb + fpart; x < ee; x += 8)
-            fsum = fmaf((sq[x - c0] + sq[TE + x - c0]) + (sq[2 * TE + x - c0] + sq[3 * TE + x - c0]), g.u[3 * x + comp], fsum);
+          {
+            float qs = 0.f;
+#pragma unroll
+            for (int k = 0; k < NQ; ++k) qs += sq[k * TE + x - c0];
+            fsum = fmaf(qs, g.u[3 * x + comp], fsum);
+          }
         }
       }
       __syncthreads();
@@ -633,7 +642,7 @@ __device__ __forceinline__ void write_partial(Ctx& c, float* part, uint8_t* scra
   }
   __syncthreads();
   TC_M();
-  {
+  if (threadIdx.x < 512) {
     const int f = threadIdx.x >> 3, prt = threadIdx.x & 7;
     float sa = 0.f, sb = 0.f;
 #pragma unroll

@@ -25,6 +25,8 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -751,10 +753,20 @@ int64_t count_kernels(janus_trainer* t, const janus_opt& opt) {
   std::vector<cudaGraphNode_t> nodes(n);
   JANUS_CUDA(cudaGraphGetNodes(g, nodes.data(), &n));
   int64_t k = 0;
+  int by_type[16] = {};
   for (auto nd : nodes) {
     cudaGraphNodeType ty;
     JANUS_CUDA(cudaGraphNodeGetType(nd, &ty));
     if (ty == cudaGraphNodeTypeKernel) ++k;
+    by_type[static_cast<int>(ty) & 15]++;
+  }
+  if (std::getenv("JANUS_GRAPH_STATS")) {  // profiling: node census of the captured step
+    size_t ne = 0;
+    JANUS_CUDA(cudaGraphGetEdges(g, nullptr, nullptr, &ne));
+    std::fprintf(stderr, "graph nodes %zu edges %zu: kernel %d memcpy %d memset %d host %d empty %d event_wait %d event_record %d\n",
+                 n, ne, by_type[cudaGraphNodeTypeKernel], by_type[cudaGraphNodeTypeMemcpy],
+                 by_type[cudaGraphNodeTypeMemset], by_type[cudaGraphNodeTypeHost], by_type[cudaGraphNodeTypeEmpty],
+                 by_type[cudaGraphNodeTypeWaitEvent & 15], by_type[cudaGraphNodeTypeEventRecord & 15]);
   }
   if (t->ed.use_graphs && !t->ed.record_timeline) {
     JANUS_CUDA(cudaGraphInstantiate(&t->gexec, g, 0));

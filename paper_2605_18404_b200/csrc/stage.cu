@@ -62,10 +62,23 @@ T* dalloc(janus_stage* st, size_t n, bool count_static) {
 
 inline int blocks(int64_t n, int t) { return static_cast<int>((n + t - 1) / t); }
 
+// Attribution switch for profiling runs ONLY (numerically invalid when set):
+// JANUS_PROF_SKIP bitmask drops launches — 1 FE, 2 FF, 4 BF, 8 BE tensor-core
+// edge kernels, 16 wgrad_multi, 32 fused upd kernels, 64 gemm_rows, 128
+// reduce_partials — so the step-time drop
+// measures each family's share of the concurrent step (tools/dbg).
+int prof_skip() {
+  static const int v = [] {
+    const char* e = std::getenv("JANUS_PROF_SKIP");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+
 template <typename Op = node::InId>
 void gemm(cudaStream_t s, int rows, const float* X, const float* M, const float* bias, const float* add1,
           const float* add2, float* out, Op op = Op{}) {
-  if (rows <= 0) return;
+  if (rows <= 0 || (prof_skip() & 64)) return;
   node::gemm_rows_kernel<kH, Op><<<blocks(rows, 256 / kH), 256, 0, s>>>(rows, X, M, bias, add1, add2, out, op);
   JANUS_LAUNCH_CHECK("gemm_rows");
 }
@@ -107,6 +120,7 @@ node::WJob wjob(const float* a, const float* b, float* G, const float* a2 = null
 }
 
 void wjobs(Scratch& sc, cudaStream_t s, int rows, std::initializer_list<node::WJob> list) {
+  if (prof_skip() & 16) return;
   node::WJobs J{};
   J.n = static_cast<int>(list.size());
   int k = 0;
@@ -549,17 +563,17 @@ void stage_fe(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
       case kMsg: {
         const float* W = P + R * H + H + H * H + H;
         gemm(s, N, cur_h, W, nullptr, nullptr, nullptr, b.v);
-        if (g.n_tiles > 0 && use_tc(st))
-          edge_tc::msg_fe_tc<<<fe_grid(st, g), edge_tc::NT, edge_tc::fe_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, msg_params(st, u),
+        if (g.n_tiles > 0 && use_tc(st)) {
+          if (!(prof_skip() & 1)) edge_tc::msg_fe_tc<<<fe_grid(st, g), edge_tc::NT, edge_tc::fe_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, msg_params(st, u),
                                                                                  st->m.r_c, b.v, b.out_m);
-        else if (g.n_tiles > 0)
+        } else if (g.n_tiles > 0)
           edge::msg_fe_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::fe_smem<kH, kR>(), s>>>(eg, msg_params(st, u), st->m.r_c, b.v, b.out_m);
         cur_m = b.out_m;
         break;
       }
       case kUpd: {
         const float *Um = P, *ups = P + H * H, *V = P + H * H + H;
-        node::upd_fe_fused<<<blocks(N, node::kRB), 256, node::upd_smem(2), s>>>(N, cur_m, cur_h, Um, ups, V, b.p, b.out_h);
+        if (!(prof_skip() & 32)) node::upd_fe_fused<<<blocks(N, node::kRB), 256, node::upd_smem(2), s>>>(N, cur_m, cur_h, Um, ups, V, b.p, b.out_h);
         cur_h = b.out_h;
         cur_m = nullptr;
         break;
@@ -614,13 +628,13 @@ void stage_ff(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
       case kUpd: {  // ff_a = a'; a_m = ((a' V^T) SiLU'(p)) U^T, written straight into the
                     // preceding msg unit's saved FF input when it is on this stage
         float* am_dst = (u - 1 >= st->u0) ? sl.units[static_cast<size_t>(u - 1 - st->u0)].ff_a : wm;
-        node::upd_ff_fused<<<blocks(N, node::kRB), 256, node::upd_smem(2), s>>>(N, wh, b.p, T + H * H, T, b.ff_a, am_dst);
+        if (!(prof_skip() & 32)) node::upd_ff_fused<<<blocks(N, node::kRB), 256, node::upd_smem(2), s>>>(N, wh, b.p, T + H * H, T, b.ff_a, am_dst);
         break;
       }
       case kMsg: {
         if (u == st->u1 - 1) copy(s, b.ff_a, wm, NH);  // a_m arrived through the ADJ_IN port
         if (g.n_tiles > 0 && use_tc(st)) {  // a_h += Y W^T fused into the tile epilogue
-          edge_tc::msg_ff_tc<<<fe_grid(st, g), edge_tc::NT, edge_tc::ff_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, msg_params(st, u),
+          if (!(prof_skip() & 2)) edge_tc::msg_ff_tc<<<fe_grid(st, g), edge_tc::NT, edge_tc::ff_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, msg_params(st, u),
                                                                                  st->m.r_c, b.v, b.ff_a, b.ff_Y, sl.F, wh);
         } else {
           if (g.n_tiles > 0)
@@ -682,11 +696,11 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
         gemm(s, N, ah, W, nullptr, nullptr, nullptr, sc.s1);  // vdot
         if (g.n_tiles > 0 && use_tc(st)) {
           const int grid = tc_grid(st, g);
-          edge_tc::msg_bf_tc<<<grid, edge_tc::NT, edge_tc::bf_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, msg_params(st, u),
+          if (!(prof_skip() & 4)) edge_tc::msg_bf_tc<<<grid, edge_tc::NT, edge_tc::bf_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, msg_params(st, u),
                                                                           st->m.r_c, b.v, sc.s1, b.ff_a, Fbar, am, sc.s2,
                                                                           sc.partial, b.inj);  // + hbar^F = X W^T
           JANUS_LAUNCH_CHECK("msg_bf_tc");
-          edge::reduce_partials_kernel<<<edge::reduce_grid(EC::PE), 256, 0, s>>>(sc.partial, grid, EC::PE, G2);
+          if (!(prof_skip() & 128)) edge::reduce_partials_kernel<<<edge::reduce_grid(EC::PE), 256, 0, s>>>(sc.partial, grid, EC::PE, G2);
         } else if (g.n_tiles > 0) {
           edge::msg_bf_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::bf_smem<kH, kR>(), s>>>(
               eg, msg_params(st, u), st->m.r_c, b.v, sc.s1, b.ff_a, Fbar, am, sc.s2, sc.partial);
@@ -704,7 +718,7 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
         const float *Um = P, *V = P + H * H + H;
         float *dU = G2, *dups = G2 + H * H, *dV = G2 + H * H + H;
         // pdot, r, pbar (s3), pdbar (s4), u (s5), mbar^F = pbar U^T, abar' = abar_h + u V
-        node::upd_bf_fused<<<blocks(N, node::kRB), 256, node::upd_smem(4), s>>>(N, am, b.ff_a, b.p, Um, T + H * H, T, V, sc.s3, sc.s4,
+        if (!(prof_skip() & 32)) node::upd_bf_fused<<<blocks(N, node::kRB), 256, node::upd_smem(4), s>>>(N, am, b.ff_a, b.p, Um, T + H * H, T, V, sc.s3, sc.s4,
                                                                 sc.s5, b.inj, ah);
         wjobs(sc, s, N, {wjob(sc.s5, b.ff_a, dV),                                          // dV2 = u^T a'
                          wjob(in_m(st, sl, u, N), sc.s3, dU, am, sc.s4, false, sc.s3, dups)});  // dU2, dups2
@@ -776,7 +790,7 @@ void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only, 
       case kUpd: {
         float *dU = G1, *dups = G1 + H * H, *dV = G1 + H * H + H;
         // pbar (s2) = (b' V^T) SiLU'(p); b_m = pbar U^T + mbar^F
-        node::upd_be_fused<<<blocks(N, node::kRB), 256, node::upd_smem(2), s>>>(N, bh, b.p, T + H * H, T, b.inj, sc.s2, bm);
+        if (!(prof_skip() & 32)) node::upd_be_fused<<<blocks(N, node::kRB), 256, node::upd_smem(2), s>>>(N, bh, b.p, T + H * H, T, b.inj, sc.s2, bm);
         wjobs(sc, s, N, {wjob(b.p, bh, dV, nullptr, nullptr, true),                                  // dV1 = SiLU(p)^T b'
                          wjob(in_m(st, sl, u, N), sc.s2, dU, nullptr, nullptr, false, sc.s2, dups)});  // dU1, dups1
         break;
@@ -784,11 +798,11 @@ void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only, 
       case kMsg: {
         if (g.n_tiles > 0 && use_tc(st)) {
           const int grid = tc_grid(st, g);
-          edge_tc::msg_be_tc<<<grid, edge_tc::NT, edge_tc::be_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, msg_params(st, u),
+          if (!(prof_skip() & 8)) edge_tc::msg_be_tc<<<grid, edge_tc::NT, edge_tc::be_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, msg_params(st, u),
                                                                           st->m.r_c, b.v, bm, sc.s1, sc.partial,
                                                                           b.inj, bh);  // + b_h += Yb W^T + hbar^F
           JANUS_LAUNCH_CHECK("msg_be_tc");
-          edge::reduce_partials_kernel<<<edge::reduce_grid(EC::PE), 256, 0, s>>>(sc.partial, grid, EC::PE, G1);
+          if (!(prof_skip() & 128)) edge::reduce_partials_kernel<<<edge::reduce_grid(EC::PE), 256, 0, s>>>(sc.partial, grid, EC::PE, G1);
         } else if (g.n_tiles > 0) {
           edge::msg_be_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::be_smem<kH, kR>(), s>>>(
               eg, msg_params(st, u), st->m.r_c, b.v, bm, sc.s1, sc.partial);

@@ -44,3 +44,19 @@ def test_non_divisor_candidates(janus):
     assert ks == list(range(4, ks[-1] + 1)) and tuned
     with pytest.raises(janus.JanusError):  # partial order t_FE < t_FF < t_BE < t_BF
         janus.tune_wavek(4, 32, (2, 1, 3, 4), 1000 * GB, 0, GB, GB, GB)
+
+
+def test_schedule_memory_lifetime_rule(janus):
+    """zero activation bytes -> peak = static; SymFold peak <=
+    1F1B-2nd peak (no replication, no recompute) under the SPEC uniform-static
+    rule; the plan partition covers every unit once."""
+    P, N = 4, 8
+    sym = janus.schedule_text(janus.METHOD_SYMFOLD, P, N)
+    one = janus.schedule_text(janus.METHOD_ONEF1B, P, N)
+    assert (janus.schedule_memory(sym, UMA, 5.0, 0, 0) == 5.0).all()
+    ps = janus.schedule_memory(sym, UMA, 10.0, 3.0, 2.0)
+    po = janus.schedule_memory(one, UMA, 10.0, 3.0, 2.0)
+    assert ps.max() <= po.max()
+    m = janus.Model(L=32, H=256)
+    plan = janus.plan_stages(m, 8)
+    assert plan[0][0] == 0 and plan[-1][1] == m.n_units and all(plan[i][1] == plan[i + 1][0] for i in range(7))
