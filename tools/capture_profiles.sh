@@ -17,3 +17,6 @@ if [ -f build/trace/libjanus_b200.so ]; then
   JANUS_LIB=build/trace/libjanus_b200.so timeout 200 python tools/tc_trace.py > $out/${tag}_trace.txt 2>&1
 fi
 ls -la $out | grep $tag
+# device LM (nbrlist.cu): full capture of the fill kernel on the batched C2 x 32 build
+timeout 300 ncu --set full --clock-control none -k regex:fill_kernel -s 20 -c 1 \
+  -o $out/${tag}_nbr_fill python tools/nbrlist_bench.py > $out/${tag}_ncu_nbr.log 2>&1
