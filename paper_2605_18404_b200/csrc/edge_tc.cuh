@@ -127,6 +127,11 @@ struct Ctx {
     tc::fence_after();
   }
   __device__ void ld(uint32_t col, float (&v)[FPT]) const { tc::ldv(tmem + lane_base() + col + static_cast<uint32_t>(FPT * q), v); }
+  // two accumulators, both loads in flight before one wait
+  __device__ void ld2(uint32_t ca, uint32_t cb, float (&a)[FPT], float (&b)[FPT]) const {
+    const uint32_t base = tmem + lane_base() + static_cast<uint32_t>(FPT * q);
+    tc::ldv2(base + ca, base + cb, a, b);
+  }
 };
 
 // Weight tile for B operands: element (n, k) = src[k*64 + n] (transpose=true)
@@ -534,8 +539,7 @@ __global__ void __launch_bounds__(NT) msg_ff_tc(EdgeGeom g, const int4* __restri
       c.wait_mma();
       {
         float z[FPT], zp[FPT];
-        c.ld(TM_Z, z);
-        c.ld(TM_ZP, zp);
+        c.ld2(TM_Z, TM_ZP, z, zp);
 #pragma unroll
         for (int j = 0; j < FPT; ++j) {
           const float zz = z[j] + al[f0 + j], sg1 = fsig(zz);
@@ -560,8 +564,7 @@ __global__ void __launch_bounds__(NT) msg_ff_tc(EdgeGeom g, const int4* __restri
         gather32(v, es.j, f0, vj);
         gather32(am, es.i, f0, ami);
         gather32(v, es.i, f0, vi);
-        c.ld(TM_G, gg);
-        c.ld(TM_GP, gp);
+        c.ld2(TM_G, TM_GP, gg, gp);
 #pragma unroll
         for (int q = 0; q < FPT; ++q) {
           const float gb = gg[q] + be[f0 + q];
@@ -602,24 +605,48 @@ __global__ void __launch_bounds__(NT) msg_ff_tc(EdgeGeom g, const int4* __restri
   teardown(c, 256);
 }
 
+// Column sums (over the chunk's edges) of a feature-major SWIZZLE_128B tile
+// [64 features][128 edges], added to the CTA accumulator acc[64] in shared
+// memory: 8 threads per feature read 16 edges each (4 conflict-free LDS.128),
+// an xor butterfly combines them and one thread adds — a fixed order per
+// feature, so the sums are deterministic.  Runs while the tensor core reads
+// the same tile (both are reads).  Padding edges hold zeros.
+__device__ __forceinline__ void fm_colsum_add(const uint8_t* t, float* acc) {
+  if (threadIdx.x < 512) {
+    const int f = static_cast<int>(threadIdx.x) >> 3, p = static_cast<int>(threadIdx.x) & 7;
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float4 v = *reinterpret_cast<const float4*>(t + off_fm(f, 16 * p + 4 * k));
+      s += (v.x + v.y) + (v.z + v.w);
+    }
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s += __shfl_xor_sync(0xffffffffu, s, 4);
+    if (p == 0) acc[f] += s;
+  }
+}
+
 // Write the CTA's weight-gradient partial [dA | dalpha | dB | dbeta] from the
 // M=64 TMEM accumulators (row r at lane (r/16)*32 + r%16) and the per-thread
 // column sums.  Everything is staged in smem (`scratch` = the four operand
 // tiles, free by now) and leaves with coalesced float4 stores.
-__device__ __forceinline__ void write_partial(Ctx& c, float* part, uint8_t* scratch, const float (&cs_a)[FPT],
-                                              const float (&cs_b)[FPT] TC_ARGS) {
+// Write the CTA's weight-gradient partial [dA | dalpha | dB | dbeta] from the
+// M=64 TMEM accumulators (row r at lane (r/16)*32 + r%16) and the CTA's
+// column-sum accumulators csa/csb (shared memory).  The rows are staged in
+// smem (`scratch` = the operand tiles, free by now) and leave with coalesced
+// float4 stores.
+__device__ __forceinline__ void write_partial(Ctx& c, float* part, uint8_t* scratch, const float* csa,
+                                              const float* csb TC_ARGS) {
   constexpr int LDP = 68;  // padded row: the 8 rows of an STS.128 phase hit distinct banks
-  float* red = reinterpret_cast<float*>(scratch);  // [2][64][TE] column-sum staging (64 KB)
-  float* stg = red + 2 * 64 * TE;                  // [2][64][LDP] dA, dB rows
-  float* col = stg + 2 * 64 * LDP;                 // [2][64] dalpha, dbeta
+  float* stg = reinterpret_cast<float*>(scratch);  // [2][64][LDP] dA, dB rows
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   TC_M();
   {
     float va[FPT], vb[FPT];
-    c.ld(TM_AG, va);
-    c.ld(TM_BG, vb);
+    c.ld2(TM_AG, TM_BG, va, vb);
     if (c.lane < 16) {
       const int r = 16 * (c.warp & 3) + c.lane;
       float4* pa = reinterpret_cast<float4*>(stg + r * LDP + FPT * c.q);
@@ -631,37 +658,6 @@ __device__ __forceinline__ void write_partial(Ctx& c, float* part, uint8_t* scra
       }
     }
   }
-  TC_M();
-  // column sums: [feature][edge] staging (conflict-free: consecutive edges),
-  // then 8 threads per feature sum 16 edges each (4 float4, conflict-free) and
-  // combine by an xor butterfly — a fixed order, so the partial is deterministic.
-#pragma unroll
-  for (int j = 0; j < FPT; ++j) {
-    red[(FPT * c.q + j) * TE + c.e] = cs_a[j];
-    red[64 * TE + (FPT * c.q + j) * TE + c.e] = cs_b[j];
-  }
-  __syncthreads();
-  TC_M();
-  if (threadIdx.x < 512) {
-    const int f = threadIdx.x >> 3, prt = threadIdx.x & 7;
-    float sa = 0.f, sb = 0.f;
-#pragma unroll
-    for (int k = 0; k < TE / 32; ++k) {
-      const float4 x = *reinterpret_cast<const float4*>(red + f * TE + 32 * k + 4 * prt);
-      const float4 y = *reinterpret_cast<const float4*>(red + 64 * TE + f * TE + 32 * k + 4 * prt);
-      sa += (x.x + x.y) + (x.z + x.w);
-      sb += (y.x + y.y) + (y.z + y.w);
-    }
-#pragma unroll
-    for (int o = 1; o < 8; o <<= 1) {
-      sa += __shfl_xor_sync(0xffffffffu, sa, o);
-      sb += __shfl_xor_sync(0xffffffffu, sb, o);
-    }
-    if (prt == 0) {
-      col[f] = sa;
-      col[64 + f] = sb;
-    }
-  }
   __syncthreads();
   TC_M();
   // coalesced copy-out: PE / 4 = 2080 float4 in global order
@@ -671,12 +667,12 @@ __device__ __forceinline__ void write_partial(Ctx& c, float* part, uint8_t* scra
     if (k < 1024) {
       v = *reinterpret_cast<const float4*>(stg + (k >> 4) * LDP + 4 * (k & 15));
     } else if (k < 1040) {
-      v = *reinterpret_cast<const float4*>(col + 4 * (k - 1024));
+      v = *reinterpret_cast<const float4*>(csa + 4 * (k - 1024));
     } else if (k < 2064) {
       const int kk = k - 1040;
       v = *reinterpret_cast<const float4*>(stg + 64 * LDP + (kk >> 4) * LDP + 4 * (kk & 15));
     } else {
-      v = *reinterpret_cast<const float4*>(col + 64 + 4 * (k - 2064));
+      v = *reinterpret_cast<const float4*>(csb + 4 * (k - 2064));
     }
     out[k] = v;
   }
@@ -703,6 +699,8 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int4* __res
   float* al = reinterpret_cast<float*>(T3 + kTile);
   float* be = al + 64;
   float* wts = be + 64;  // W^T [64][64] (fused row epilogue)
+  float* csa = wts + 64 * 64;  // CTA column sums: dalpha, dbeta
+  float* csb = csa + 64;
   __shared__ __align__(8) uint64_t mbar;
   __shared__ uint32_t tslot;
   Ctx c;
@@ -710,14 +708,12 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int4* __res
   c.mbar = &mbar;
   __shared__ __align__(8) uint64_t wbar;
   load_weights(sm, p.pack, 3, al, be, wts, &wbar);
+  if (threadIdx.x < 128) csa[threadIdx.x] = 0.f;  // csa, csb (published by setup's barrier)
   TC_M();
   setup(c, &tslot, 512);
   TC_M();
   const uint32_t aW0 = tc::smem_u32(W0), aW1 = tc::smem_u32(W1), aW2 = tc::smem_u32(W2);
   const uint32_t aT0 = tc::smem_u32(T0), aT1 = tc::smem_u32(T1), aT2 = tc::smem_u32(T2), aT3 = tc::smem_u32(T3);
-  float cs_a[FPT], cs_b[FPT];
-#pragma unroll
-  for (int j = 0; j < FPT; ++j) cs_a[j] = cs_b[j] = 0.f;
   bool first = true;
   const int f0 = FPT * c.q;
   for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
@@ -772,7 +768,6 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int4* __res
         for (int q = 0; q < FPT; ++q) {
           gg[q] = es.c * (gg[q] + be[f0 + q]) * bj[q];  // w_e * bm_j
           gb[q] = es.c * bi[q] * vj[q];                 // gbar (zero on padding edges: c = 0)
-          cs_b[q] += gb[q];
         }
         TC_M();
         st_pl(T0, c.e, f0, gg);
@@ -792,19 +787,18 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int4* __res
         const uint8_t* const tl[1] = {T0};
         seg_rows<1>(g, tr.r0, c0, ne, tl, sg, acc);
       }
+      fm_colsum_add(T2, csb);  // dbeta += sum_e gbar_e (reads gbar^T beside the dB MMA)
       TC_M();
       c.wait_mma();
       __syncthreads();  // T0 reads done before it is rewritten
       TC_M();
       {
         float z[FPT], sb[FPT];
-        c.ld(TM_Z, z);
-        c.ld(TM_G, sb);
+        c.ld2(TM_Z, TM_G, z, sb);
 #pragma unroll
         for (int j = 0; j < FPT; ++j) {
           const float zz = z[j] + al[f0 + j], s1 = fsig(zz);
           z[j] = sb[j] * (s1 * (1.0f + zz * (1.0f - s1)));
-          cs_a[j] += z[j];
         }
         st_fm(T2, c.e, f0, z);  // zbar^T
         float ph[FPT], dph[FPT];
@@ -816,6 +810,7 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int4* __res
         mma_tiles<64, 64, 128, 64>(c.tmem + TM_AG, aT0, aT2, !first);
         tc::commit(c.mbar);
       }
+      fm_colsum_add(T2, csa);  // dalpha += sum_e zbar_e (beside the dA MMA)
       TC_M();
       c.wait_mma();
       TC_M();
@@ -835,7 +830,7 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int4* __res
     teardown(c, 512);
     return;
   }
-  write_partial(c, part, T0, cs_a, cs_b TC_PASS);
+  write_partial(c, part, T0, csa, csb TC_PASS);
   TC_M();
   teardown(c, 512);
   TC_M();
@@ -866,6 +861,8 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int4* __res
   float* al = reinterpret_cast<float*>(T3 + kTile);
   float* be = al + 64;
   float* wts = be + 64;  // W^T [64][64] (fused row epilogue)
+  float* csa = wts + 64 * 64;  // CTA column sums: dalpha, dbeta
+  float* csb = csa + 64;
   __shared__ __align__(8) uint64_t mbar;
   __shared__ uint32_t tslot;
   Ctx c;
@@ -875,14 +872,12 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int4* __res
 #ifndef JANUS_TC_LATEW
   load_weights(sm, p.pack, 3, al, be, wts, &wbar);
 #endif
+  if (threadIdx.x < 128) csa[threadIdx.x] = 0.f;  // csa, csb (published by setup's barrier)
   TC_M();
   setup(c, &tslot, 512);
   TC_M();
   const uint32_t aW0 = tc::smem_u32(W0), aW1 = tc::smem_u32(W1), aW2 = tc::smem_u32(W2);
   const uint32_t aT0 = tc::smem_u32(T0), aT1 = tc::smem_u32(T1), aT2 = tc::smem_u32(T2), aT3 = tc::smem_u32(T3);
-  float cs_a[FPT], cs_b[FPT];
-#pragma unroll
-  for (int j = 0; j < FPT; ++j) cs_a[j] = cs_b[j] = 0.f;
   bool first = true;
   const int f0 = FPT * c.q;
   for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
@@ -924,8 +919,7 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int4* __res
       TC_M();
       {
         float z[FPT], zp[FPT];
-        c.ld(TM_Z, z);
-        c.ld(TM_ZP, zp);
+        c.ld2(TM_Z, TM_ZP, z, zp);
 #pragma unroll
         for (int j = 0; j < FPT; ++j) {
           const float zz = z[j] + al[f0 + j], s1 = fsig(zz);
@@ -958,8 +952,7 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int4* __res
           v4[q] = __ldg(reinterpret_cast<const float4*>(v + (size_t)es.j * H + f0) + q);
           d4[q] = __ldg(reinterpret_cast<const float4*>(vdot + (size_t)es.j * H + f0) + q);
         }
-        c.ld(TM_G, gg);
-        c.ld(TM_GP, gp);
+        c.ld2(TM_G, TM_GP, gg, gp);
         TC_M();
 #pragma unroll
         for (int q = 0; q < FPT / 4; ++q) {
@@ -980,8 +973,6 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int4* __res
         TC_M();
         st_pl(T0, c.e, f0, pm);
         st_pl(T1, c.e, f0, px);
-#pragma unroll
-        for (int q = 0; q < FPT; ++q) cs_b[q] += mu[q];
       }
       TC_M();
       tc::fence_before();
@@ -1001,6 +992,7 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int4* __res
         mma_tiles<64, 64, 128, 64>(c.tmem + TM_BG, aT3, aT1, true);
         tc::commit(c.mbar);
       }
+      fm_colsum_add(T0, csb);  // dbeta += sum_e mu_e (reads mu^T beside the dB MMA)
       TC_M();
       c.wait_mma();
       TC_M();
@@ -1017,10 +1009,8 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int4* __res
       TC_M();
       {
         float z[FPT], zp[FPT], sb[FPT], sdb[FPT];
-        c.ld(TM_Z, z);
-        c.ld(TM_ZP, zp);
-        c.ld(TM_G, sb);
-        c.ld(TM_GP, sdb);
+        c.ld2(TM_Z, TM_ZP, z, zp);
+        c.ld2(TM_G, TM_GP, sb, sdb);
 #pragma unroll
         for (int j = 0; j < FPT; ++j) {
           const float zz = z[j] + al[f0 + j], s1 = fsig(zz);
@@ -1028,7 +1018,6 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int4* __res
           const float d2s = s1 * (1.0f - s1) * (2.0f + zz * (1.0f - 2.0f * s1));
           z[j] = sb[j] * ds + sdb[j] * d2s * zp[j];  // zbar
           zp[j] = sdb[j] * ds;                       // zbar'
-          cs_a[j] += z[j];
         }
         st_fm(T2, c.e, f0, z);
         st_fm(T3, c.e, f0, zp);
@@ -1043,6 +1032,7 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int4* __res
         mma_tiles<64, 64, 128, 64>(c.tmem + TM_AG, aT1, aT3, true);
         tc::commit(c.mbar);
       }
+      fm_colsum_add(T2, csa);  // dalpha += sum_e zbar_e (beside the dA MMA)
       TC_M();
       c.wait_mma();
       TC_M();
@@ -1062,7 +1052,7 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int4* __res
     teardown(c, 512);
     return;
   }
-  write_partial(c, part, T0, cs_a, cs_b TC_PASS);
+  write_partial(c, part, T0, csa, csb TC_PASS);
   TC_M();
   teardown(c, 512);
   TC_M();
