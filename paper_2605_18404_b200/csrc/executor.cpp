@@ -672,16 +672,21 @@ void trainer_load_many(janus_trainer* t, int n, const int* mbs, const janus_host
   // host-built tile tables go through the stage's double-buffered pinned staging
   std::vector<janus_host_batch> dev;
   std::vector<int> dev_mb;
+  std::vector<std::vector<node::GeoJob>> jobs(t->owned.size());  // per stage: one batched geometry launch
   for (int k = 0; k < n; ++k) {
     if (hbs[k].row_ptr) {
-      for (janus_stage* s : t->owned) stage_load(s, mbs[k], hbs[k], t->root, /*sync=*/false);
+      for (size_t x = 0; x < t->owned.size(); ++x)
+        stage_load(t->owned[x], mbs[k], hbs[k], t->root, /*sync=*/false, nullptr, &jobs[x]);
       trainer_note_shape(t, mbs[k], hbs[k]);
     } else {
       dev.push_back(hbs[k]);
       dev_mb.push_back(mbs[k]);
     }
   }
-  if (dev.empty()) return;
+  if (dev.empty()) {
+    for (size_t x = 0; x < t->owned.size(); ++x) stage_geometry_flush(t->owned[x], jobs[x], t->root);
+    return;
+  }
   // LM with the neighbour lists built on the device: ONE cell-list build over
   // all these micro-batches (their structures side by side) on a side stream,
   // while a step may still run on root; each stage copies its batch's slice
@@ -710,9 +715,11 @@ void trainer_load_many(janus_trainer* t, int n, const int* mbs, const janus_host
     hb2.n_edges = rp[static_cast<size_t>(N)];
     hb2.col = hb2.shift = hb2.rev = nullptr;
     const DevCsrSlice sl{&t->lm->buf(b), a0, hrow[a0]};
-    for (janus_stage* s : t->owned) stage_load(s, dev_mb[k], hb2, t->root, /*sync=*/false, &sl);
+    for (size_t x = 0; x < t->owned.size(); ++x)
+      stage_load(t->owned[x], dev_mb[k], hb2, t->root, /*sync=*/false, &sl, &jobs[x]);
     trainer_note_shape(t, dev_mb[k], hb2);
   }
+  for (size_t x = 0; x < t->owned.size(); ++x) stage_geometry_flush(t->owned[x], jobs[x], t->root);
   t->lm->release(b, t->root);
 }
 

@@ -5,6 +5,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "geo_job.hpp"
 
 namespace janus {
 namespace node {
@@ -381,6 +382,57 @@ __global__ void geometry_kernel(int n_atoms, int n_edges, const int* __restrict_
   const double arg = 3.14159265358979323846 * d / rc;
   c_out[e] = d < rc ? (float)(0.5 * (cos(arg) + 1.0)) : 0.f;
   dc_out[e] = d < rc ? (float)(-0.5 * (3.14159265358979323846 / rc) * sin(arg)) : 0.f;
+}
+
+// Batched LM geometry: one launch for the micro-batches of one load.  Per
+// edge: (optionally) the device-built CSR slice is copied in with col / rev
+// rebased, then the same per-edge geometry as geometry_kernel.  The job table
+// travels as a kernel parameter.
+__global__ void geometry_batched_kernel(const __grid_constant__ GeoJobs J) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= J.total_edges) return;
+  int k = 0;
+  while (k + 1 < J.n && J.j[k + 1].edge_base <= t) ++k;
+  const GeoJob& jb = J.j[k];
+  const int e = t - jb.edge_base;
+  int j, sx, sy, sz;
+  if (jb.scol) {
+    j = jb.scol[jb.edge0 + e] - jb.atom0;
+    jb.col[e] = j;
+    jb.rev[e] = jb.srev[jb.edge0 + e] - jb.edge0;
+    sx = jb.sshift[3 * (jb.edge0 + e) + 0];
+    sy = jb.sshift[3 * (jb.edge0 + e) + 1];
+    sz = jb.sshift[3 * (jb.edge0 + e) + 2];
+    jb.shift[3 * e + 0] = sx;
+    jb.shift[3 * e + 1] = sy;
+    jb.shift[3 * e + 2] = sz;
+  } else {
+    j = jb.col[e];
+    sx = jb.shift[3 * e + 0];
+    sy = jb.shift[3 * e + 1];
+    sz = jb.shift[3 * e + 2];
+  }
+  int lo = 0, hi = jb.n_atoms;  // largest i with row_ptr[i] <= e
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (jb.row_ptr[mid] <= e) lo = mid; else hi = mid;
+  }
+  const int i = lo;
+  const double L = jb.cell[jb.struct_id[i]];
+  const double* pj = jb.pos + 3 * j;
+  const double* pi = jb.pos + 3 * i;
+  const double rx = __dsub_rn(__dadd_rn(pj[0], __dmul_rn((double)sx, L)), pi[0]);
+  const double ry = __dsub_rn(__dadd_rn(pj[1], __dmul_rn((double)sy, L)), pi[1]);
+  const double rz = __dsub_rn(__dadd_rn(pj[2], __dmul_rn((double)sz, L)), pi[2]);
+  const double d = sqrt(rx * rx + ry * ry + rz * rz);
+  jb.src[e] = i;
+  jb.d[e] = (float)d;
+  jb.u[3 * e + 0] = (float)(rx / d);
+  jb.u[3 * e + 1] = (float)(ry / d);
+  jb.u[3 * e + 2] = (float)(rz / d);
+  const double arg = 3.14159265358979323846 * d / J.rc;
+  jb.c[e] = d < J.rc ? (float)(0.5 * (cos(arg) + 1.0)) : 0.f;
+  jb.dc[e] = d < J.rc ? (float)(-0.5 * (3.14159265358979323846 / J.rc) * sin(arg)) : 0.f;
 }
 
 }  // namespace node

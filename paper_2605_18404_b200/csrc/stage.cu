@@ -252,8 +252,8 @@ LoadLayout load_layout(const janus_stage_desc& d) {
   const size_t NA = static_cast<size_t>(d.max_atoms), NE = static_cast<size_t>(std::max(d.max_edges, 1));
   const size_t MS = static_cast<size_t>(d.max_struct);
   const size_t sz[LoadLayout::kN] = {
-      4 * (NA + 1), 4 * NE,     4 * NE, 4 * 3 * NE, 4 * NA, 4 * NA,    4 * (MS + 1),
-      4 * (NA + 1), 16 * NA,    8 * 3 * NA,  8 * MS, 4 * MS, 4 * 3 * NA};
+      4 * (NA + 1), 4 * NA, 4 * NA, 4 * (MS + 1), 4 * (NA + 1), 16 * NA, 8 * 3 * NA, 8 * MS, 4 * MS, 4 * 3 * NA,
+      4 * NE,       4 * NE, 4 * 3 * NE};
   LoadLayout L;
   size_t o = 0;
   for (int k = 0; k < LoadLayout::kN; ++k) {
@@ -443,7 +443,7 @@ size_t port_elems(const janus_stage* st, int port, int n) {
 
 // ================================================================== LM
 void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_t s, bool sync,
-                const DevCsrSlice* dcsr) {
+                const DevCsrSlice* dcsr, std::vector<node::GeoJob>* defer) {
   if (mb < 0 || mb >= st->desc.n_micro_batches) throw domain_error("micro-batch index out of range");
   if (!hb.row_ptr && !dcsr) {  // no neighbour list in the batch: build it on the device (nbrlist.cu)
     if (!st->lm) st->lm = new LmBuilder(st->desc.max_atoms, st->desc.max_struct, st->desc.max_edges, st->desc.device, 1);
@@ -530,6 +530,38 @@ void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_
   put(LoadLayout::kFTarget, hb.F_target, sizeof(float) * 3 * N);
   const size_t extent = L.off[LoadLayout::kFTarget] + sizeof(float) * 3 * N;
   JANUS_CUDA(cudaMemcpyAsync(g.d_block, hp, extent, cudaMemcpyHostToDevice, s));
+  if (!dcsr && E > 0) {  // host-built CSR: col | rev | shift (capacity gaps between them included)
+    const size_t a = L.off[LoadLayout::kCol], b = L.off[LoadLayout::kShift] + sizeof(int) * 3 * E;
+    JANUS_CUDA(cudaMemcpyAsync(g.d_block + a, hp + a, b - a, cudaMemcpyHostToDevice, s));
+  }
+  if (defer) {  // batched load: slice + geometry of all its micro-batches in one launch (stage_geometry_flush)
+    if (E > 0) {
+      node::GeoJob j{};
+      j.n_atoms = N;
+      j.n_edges = E;
+      j.row_ptr = g.row_ptr;
+      j.col = g.col;
+      j.rev = g.rev;
+      j.shift = g.shift;
+      if (dcsr) {
+        j.scol = dcsr->csr->col;
+        j.srev = dcsr->csr->rev;
+        j.sshift = dcsr->csr->shift;
+        j.atom0 = dcsr->atom0;
+        j.edge0 = dcsr->edge0;
+      }
+      j.pos = g.pos;
+      j.struct_id = g.struct_id;
+      j.cell = g.cell;
+      j.src = g.src;
+      j.d = g.d;
+      j.u = g.u;
+      j.c = g.c;
+      j.dc = g.dc;
+      defer->push_back(j);
+    }
+    return;
+  }
   if (dcsr)  // the device-built CSR replaces the (unused) host regions of the block
     csr_slice_copy(*dcsr->csr, dcsr->atom0, dcsr->edge0, E, g.col, g.rev, g.shift, s);
   if (E > 0)
@@ -539,6 +571,24 @@ void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_
   // host arrays of the caller must stay valid until the stream reaches the
   // copies (pageable sources are staged by the driver before return)
   if (sync) JANUS_CUDA(cudaStreamSynchronize(s));
+}
+
+void stage_geometry_flush(janus_stage* st, std::vector<node::GeoJob>& jobs, cudaStream_t s) {
+  for (size_t b = 0; b < jobs.size(); b += node::kMaxGeoJobs) {
+    node::GeoJobs J{};
+    J.n = static_cast<int>(std::min<size_t>(node::kMaxGeoJobs, jobs.size() - b));
+    J.rc = static_cast<double>(st->m.r_c);
+    int base = 0;
+    for (int k = 0; k < J.n; ++k) {
+      J.j[k] = jobs[b + static_cast<size_t>(k)];
+      J.j[k].edge_base = base;
+      base += J.j[k].n_edges;
+    }
+    J.total_edges = base;
+    if (base > 0) node::geometry_batched_kernel<<<blocks(base, 256), 256, 0, s>>>(J);
+    JANUS_LAUNCH_CHECK("geometry_batched");
+  }
+  jobs.clear();
 }
 
 // ================================================================== FE

@@ -31,7 +31,9 @@ int64_t unit_param_offset(const janus_model_desc& m, int u);
 // tables at fixed capacity offsets, so one LM is ONE host->device copy into a
 // device block with the same layout (the device pointers below point into it).
 struct LoadLayout {
-  enum { kRowPtr, kCol, kRev, kShift, kSpecies, kStructId, kStructPtr, kTileRow, kTileTc, kPos, kCell, kETarget, kFTarget, kN };
+  // the per-edge CSR arrays come last: a device-LM load (CSR built on the GPU)
+  // uploads only the prefix up to the force targets
+  enum { kRowPtr, kSpecies, kStructId, kStructPtr, kTileRow, kTileTc, kPos, kCell, kETarget, kFTarget, kCol, kRev, kShift, kN };
   size_t off[kN] = {};
   size_t bytes = 0;
 };

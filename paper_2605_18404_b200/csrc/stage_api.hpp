@@ -3,7 +3,10 @@
 
 #include <cuda_runtime.h>
 
+#include <vector>
+
 #include "../../include/janus_cuda.h"
+#include "geo_job.hpp"
 
 namespace janus {
 
@@ -14,8 +17,11 @@ struct DevCsrSlice;
 // (nbrlist.cu).  dcsr: col / shift / rev already on the device, as a slice of
 // a batched build (hb.row_ptr is then the host mirror of this batch's row_ptr
 // and hb.col/shift/rev are ignored).
+// defer: queue the slice + geometry launch into `defer` (run by
+// stage_geometry_flush as one batched kernel) instead of launching per batch.
 void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_t s, bool sync = true,
-                const DevCsrSlice* dcsr = nullptr);
+                const DevCsrSlice* dcsr = nullptr, std::vector<node::GeoJob>* defer = nullptr);
+void stage_geometry_flush(janus_stage* st, std::vector<node::GeoJob>& jobs, cudaStream_t s);
 void stage_fe(janus_stage* st, int mb, int slot, cudaStream_t s, int lane = 0);
 void stage_ff(janus_stage* st, int mb, int slot, cudaStream_t s, int lane = 0);
 void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane = 0);
