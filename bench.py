@@ -332,20 +332,29 @@ def main():
     if rank == 0:
         st = tr.stage(0 if P == 1 else min(1, P - 1))
         try:
-            ms_bf, ne, fl = st.time_edge_kernel(2, 0, iters=50)
+            # dominant kernel = msg BF (33% of the step, profiles/r01_step_attribution.txt), timed
+            # with the step's concurrency: all 32 micro-batches launched on the 16 lanes with the
+            # step's grid (tiles per CTA), CUDA events around whole rounds (P == 1; else isolated)
+            if P == 1:
+                ms_bf, ne, fl = st.time_edge_kernel(2, -1, iters=20)
+                how = "all micro-batches per round on the step's lanes and grids (CUDA events per round)"
+            else:
+                ms_bf, ne, fl = st.time_edge_kernel(2, 0, iters=50)
+                how = "one micro-batch, back-to-back launches"
             achieved = fl / (ms_bf * 1e-3) / 1e12
+            iso_ms, iso_e, iso_fl = st.time_edge_kernel(2, 0, iters=50)
             roof = {"kernel": "msg_bf_tc (tcgen05 kind::tf32)" if args.precision == "tf32" else "msg_bf_kernel (SIMT fp32)",
                     "bound": "tensor", "achieved": achieved,
                     "peak": peaks["bf16_tflops"], "unit": "TFLOP/s", "frac": achieved / peaks["bf16_tflops"],
                     "traffic": load_traffic(args.precision), "peak_source": f"{peak_src} bf16 dense (MEASURED_PEAKS.json)",
-                    "launch_ms": ms_bf, "edges_per_launch": ne, "flops_per_launch": fl,
+                    "timing": how, "round_ms": ms_bf, "edges_per_round": ne, "flops_per_round": fl,
+                    "isolated_launch_ms": iso_ms, "isolated_tflops": iso_fl / (iso_ms * 1e-3) / 1e12,
                     "fp32_simt_nominal_tflops": 74.4}
             fe = st.time_edge_kernel(0, 0, iters=50)
             roof["fe_kernel_tflops"] = fe[2] / (fe[0] * 1e-3) / 1e12
             # step level: algorithmic edge-contraction FLOPs of all four phases,
-            # every layer and micro-batch, over the device-timed step (the edge
-            # kernels run concurrently on the lanes, several tiles per CTA)
-            fl_all = fl + fe[2] + sum(st.time_edge_kernel(w, 0, iters=5)[2] for w in (1, 3))
+            # every layer and micro-batch, over the device-timed step
+            fl_all = iso_fl + fe[2] + sum(st.time_edge_kernel(w, 0, iters=5)[2] for w in (1, 3))
             if P == 1:
                 roof["step_edge_flops"] = fl_all * CONFIG["L"] * n_mb
                 roof["step_edge_tflops"] = roof["step_edge_flops"] / (ms_per_step * 1e-3) / 1e12

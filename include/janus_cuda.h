@@ -157,7 +157,10 @@ int janus_stage_optimizer_step(janus_stage* st, const janus_opt* opt, void* stre
  * events on `stream`, back-to-back launches after one warm-up): which = 0 FE,
  * 1 FF, 2 BF, 3 BE.  Requires the phase's inputs to exist (run the step once
  * first).  Returns the mean launch time, the launch's edge count and
- * algorithmic FLOPs (DESIGN.md §4 per-edge counts). */
+ * algorithmic FLOPs (DESIGN.md §4 per-edge counts).  mb < 0: the step's
+ * concurrency instead — every micro-batch (slot = mb) launched on lane
+ * mb % n_lanes with the step's grid (tiles per CTA); *avg_ms is then the time
+ * of one round of all of them and edges / flops their totals. */
 int janus_stage_time_edge_kernel(janus_stage* st, int which, int mb, int slot, int iters, void* stream,
                                  float* avg_ms, int64_t* edges, double* flops);
 /* Peak device bytes held by the stage (static + activation arena). */

@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <initializer_list>
+#include <limits>
 #include <stdexcept>
 #include <vector>
 
@@ -387,9 +388,17 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
     st->losses = dalloc<float>(st, 2 * static_cast<size_t>(d.n_slots), false);
     for (size_t x = 0; x < st->slots.size(); ++x) st->slots[x].loss = st->losses + 2 * x;
     st->lanes.resize(static_cast<size_t>(std::max(1, d.n_lanes)));
-    // measured on the C2 bench (16 lanes): 1/1 -> 4735, 2/4 -> 5616, 4/8 -> 5765 structures/s
-    st->tpc_fe = std::max(1, std::min(4, d.n_lanes / 4));
-    st->tpc_wg = std::max(1, std::min(8, d.n_lanes / 2));
+    // measured on the C2 bench (16 lanes): 128-edge tiles 1/1 -> 4735, 4/8 -> 5765;
+    // multi-chunk tiles (~2 chunks) 2/4 -> 6363, 2/3 -> 6467 structures/s
+    st->tpc_fe = std::max(1, std::min(2, d.n_lanes / 8));
+    st->tpc_wg = std::max(1, std::min(3, d.n_lanes / 5));
+    // tensor-core tiles: runs of <= 8 rows with <= tc_tile_edges edges, cut into
+    // 128-edge chunks (rows may straddle chunk boundaries: the segmented sums
+    // and force sums carry across the chunks of a tile)
+    st->tc_tile_edges = 0;  // 0: best-fill tiles (stage_load); > 0: greedy runs of <= that many edges (tuning)
+    if (const char* e = std::getenv("JANUS_TC_TILE_EDGES")) st->tc_tile_edges = std::max(0, std::atoi(e));
+    if (const char* e = std::getenv("JANUS_TC_TILE_MAXCH")) st->tc_tile_max_chunks = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("JANUS_TC_TILE_OVH")) st->tc_tile_ovh = std::atof(e);
     if (const char* e = std::getenv("JANUS_TPC_FE")) st->tpc_fe = std::max(1, std::atoi(e));  // tuning runs only
     if (const char* e = std::getenv("JANUS_TPC_WG")) st->tpc_wg = std::max(1, std::atoi(e));
     for (Scratch& sc : st->lanes) {
@@ -478,9 +487,38 @@ void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_
     tiles.push_back(N);
     return tiles;
   };
+  // Tensor-core tiles: runs of <= 8 rows cut into 128-edge chunks (rows may
+  // straddle chunk boundaries; the segmented and force sums carry across a
+  // tile's chunks).  A chunk costs the same whatever its fill (a thread per
+  // edge row) and a tile adds a fixed epilogue (row sums, row GEMM), so each
+  // tile takes the run of 1..8 rows (<= max_chunks chunks; a longer single
+  // row alone) minimising (chunks + ovh) / edges, ties to the longer run.
+  auto build_tiles_cost = [&](int max_chunks, double ovh) {
+    std::vector<int> tiles{0};
+    for (int i = 0; i < N;) {
+      int best_k = 1, e = 0;
+      double best = std::numeric_limits<double>::infinity();
+      for (int k = 1; k <= edge_tc::kRowsPerTile && i + k <= N; ++k) {
+        e += hb.row_ptr[i + k] - hb.row_ptr[i + k - 1];
+        const int chunks = (e + edge_tc::TE - 1) / edge_tc::TE;
+        if (k > 1 && chunks > max_chunks) break;
+        const double cost = e > 0 ? (chunks + ovh) / e : std::numeric_limits<double>::max();
+        if (cost <= best * (1.0 + 1e-12)) {
+          best = cost;
+          best_k = k;
+        }
+      }
+      i += best_k;
+      tiles.push_back(i);
+    }
+    return tiles;
+  };
   DevGeo& gg = st->geo[static_cast<size_t>(mb)];
   gg.h_tiles = build_tiles(edge::TE);
-  gg.h_tiles_tc = build_tiles(edge_tc::TE);
+  // up to 2 chunks per tile at ~50 neighbours, 4 in dense cells (measured:
+  // C2 2 -> 6456 vs 3 -> 6070 structures/s; C5 2 -> 204 vs 4 -> 240)
+  const int max_chunks = st->tc_tile_max_chunks > 0 ? st->tc_tile_max_chunks : (E >= 80 * N ? 4 : 2);
+  gg.h_tiles_tc = st->tc_tile_edges > 0 ? build_tiles(st->tc_tile_edges) : build_tiles_cost(max_chunks, st->tc_tile_ovh);
   const std::vector<int>& tiles = gg.h_tiles;
   const std::vector<int>& tiles_tc = gg.h_tiles_tc;
   std::vector<int>& sptr = gg.h_sptr;
@@ -938,76 +976,115 @@ double edge_kernel_flops_per_edge(int which, int H, int R) {
   }
 }
 
-void stage_time_edge_kernel(janus_stage* st, int which, int mb, int slot, int iters, cudaStream_t s, float* avg_ms,
-                            int64_t* edges, double* flops) {
-  check_mb_slot(st, mb, slot);
-  int u = -1;
-  for (int x = st->u0; x < st->u1; ++x)
-    if (unit_kind(x, st->m.L) == kMsg) {
-      u = x;
-      break;
-    }
-  if (u < 0) throw state_error("stage has no msg unit");
-  if (iters < 1 || which < 0 || which > 3) throw domain_error("bad timing request");
+// One launch of a msg unit's edge kernel for (mb, slot) on `s` with scratch
+// lane `lane`: step_grid = the grid the step uses (tiles per CTA), else one
+// tile per CTA on the full grid.  Inputs must exist (run the step first).
+void launch_edge_kernel(janus_stage* st, int u, int which, int mb, int slot, int lane, cudaStream_t s, bool step_grid) {
   const DevGeo& g = st->geo[static_cast<size_t>(mb)];
   Slot& sl = st->slots[static_cast<size_t>(slot)];
   UnitBufs& b = sl.units[static_cast<size_t>(u - st->u0)];
   const EdgeGeom eg = edge_geom(g);
   const MsgParams mp = msg_params(st, u);
-  Scratch& sc = lane_of(st, 0);
-  const bool tcm = use_tc(st);
-  auto launch = [&] {
-    if (tcm) {
-      const int grid = tc_grid_tpc(g, 1);  // isolated launch: one tile per CTA, full grid
-      switch (which) {
-        case 0:
-          edge_tc::msg_fe_tc<<<g.n_tiles_tc, edge_tc::NT, edge_tc::fe_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, sc.s3);
-          break;
-        case 1:
-          edge_tc::msg_ff_tc<<<g.n_tiles_tc, edge_tc::NT, edge_tc::ff_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, b.ff_a, sc.s3, sc.s5, nullptr);
-          break;
-        case 2:
-          edge_tc::msg_bf_tc<<<grid, edge_tc::NT, edge_tc::bf_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, sc.s1, b.ff_a,
-                                                                          sl.Fbar, sc.s3, sc.s4, sc.partial, nullptr);
-          break;
-        default:
-          edge_tc::msg_be_tc<<<grid, edge_tc::NT, edge_tc::be_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, sc.s2, sc.s3, sc.partial, nullptr, nullptr);
-          break;
-      }
-      return;
-    }
+  Scratch& sc = lane_of(st, lane);
+  if (use_tc(st)) {
+    const int grid = step_grid ? tc_grid(st, g) : tc_grid_tpc(g, 1);
+    const int fgrid = step_grid ? fe_grid(st, g) : g.n_tiles_tc;
     switch (which) {
       case 0:
-        edge::msg_fe_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::fe_smem<kH, kR>(), s>>>(eg, mp, st->m.r_c, b.v, sc.s3);
+        edge_tc::msg_fe_tc<<<fgrid, edge_tc::NT, edge_tc::fe_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, sc.s3);
         break;
       case 1:
-        edge::msg_ff_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::ff_smem<kH, kR>(), s>>>(eg, mp, st->m.r_c, b.v, b.ff_a, sc.s3, sc.s5);
+        edge_tc::msg_ff_tc<<<fgrid, edge_tc::NT, edge_tc::ff_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, b.ff_a, sc.s3, sc.s5, nullptr);
         break;
       case 2:
-        edge::msg_bf_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::bf_smem<kH, kR>(), s>>>(eg, mp, st->m.r_c, b.v, sc.s1, b.ff_a,
-                                                                                       sl.Fbar, sc.s3, sc.s4, sc.partial);
+        edge_tc::msg_bf_tc<<<grid, edge_tc::NT, edge_tc::bf_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, sc.s1, b.ff_a,
+                                                                        sl.Fbar, sc.s3, sc.s4, sc.partial, nullptr);
         break;
       default:
-        edge::msg_be_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::be_smem<kH, kR>(), s>>>(eg, mp, st->m.r_c, b.v, sc.s2, sc.s3, sc.partial);
+        edge_tc::msg_be_tc<<<grid, edge_tc::NT, edge_tc::be_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, sc.s2, sc.s3, sc.partial, nullptr, nullptr);
         break;
     }
-  };
-  launch();
-  JANUS_LAUNCH_CHECK("time_edge_kernel");
+    return;
+  }
+  switch (which) {
+    case 0:
+      edge::msg_fe_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::fe_smem<kH, kR>(), s>>>(eg, mp, st->m.r_c, b.v, sc.s3);
+      break;
+    case 1:
+      edge::msg_ff_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::ff_smem<kH, kR>(), s>>>(eg, mp, st->m.r_c, b.v, b.ff_a, sc.s3, sc.s5);
+      break;
+    case 2:
+      edge::msg_bf_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::bf_smem<kH, kR>(), s>>>(eg, mp, st->m.r_c, b.v, sc.s1, b.ff_a,
+                                                                                     sl.Fbar, sc.s3, sc.s4, sc.partial);
+      break;
+    default:
+      edge::msg_be_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::be_smem<kH, kR>(), s>>>(eg, mp, st->m.r_c, b.v, sc.s2, sc.s3, sc.partial);
+      break;
+  }
+}
+
+int first_msg_unit(const janus_stage* st) {
+  for (int x = st->u0; x < st->u1; ++x)
+    if (unit_kind(x, st->m.L) == kMsg) return x;
+  throw state_error("stage has no msg unit");
+}
+
+void stage_time_edge_kernel(janus_stage* st, int which, int mb, int slot, int iters, cudaStream_t s, float* avg_ms,
+                            int64_t* edges, double* flops) {
+  if (iters < 1 || which < 0 || which > 3) throw domain_error("bad timing request");
+  const int u = first_msg_unit(st);
   cudaEvent_t a, z;
   JANUS_CUDA(cudaEventCreate(&a));
   JANUS_CUDA(cudaEventCreate(&z));
-  JANUS_CUDA(cudaEventRecord(a, s));
-  for (int i = 0; i < iters; ++i) launch();
-  JANUS_CUDA(cudaEventRecord(z, s));
-  JANUS_CUDA(cudaEventSynchronize(z));
-  float ms = 0.f;
-  JANUS_CUDA(cudaEventElapsedTime(&ms, a, z));
+  if (mb >= 0) {  // one micro-batch, back-to-back launches, full grid
+    check_mb_slot(st, mb, slot);
+    const DevGeo& g = st->geo[static_cast<size_t>(mb)];
+    launch_edge_kernel(st, u, which, mb, slot, 0, s, false);
+    JANUS_LAUNCH_CHECK("time_edge_kernel");
+    JANUS_CUDA(cudaEventRecord(a, s));
+    for (int i = 0; i < iters; ++i) launch_edge_kernel(st, u, which, mb, slot, 0, s, false);
+    JANUS_CUDA(cudaEventRecord(z, s));
+    JANUS_CUDA(cudaEventSynchronize(z));
+    float ms = 0.f;
+    JANUS_CUDA(cudaEventElapsedTime(&ms, a, z));
+    *avg_ms = ms / iters;
+    *edges = g.n_edges;
+    *flops = edge_kernel_flops_per_edge(which, kH, kR) * g.n_edges;
+  } else {
+    // the step's concurrency: every micro-batch (slot = mb) on lane mb % lanes,
+    // each launch with the step grid (tiles per CTA); time per round of all of them
+    const int L = static_cast<int>(st->lanes.size()), n_mb = st->desc.n_micro_batches;
+    std::vector<cudaStream_t> ls(static_cast<size_t>(L));
+    std::vector<cudaEvent_t> ev(static_cast<size_t>(L) + 1);
+    for (auto& x : ls) JANUS_CUDA(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+    for (auto& x : ev) JANUS_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+    int64_t E = 0;
+    for (int m = 0; m < n_mb; ++m) E += st->geo[static_cast<size_t>(m)].n_edges;
+    auto round = [&] {
+      JANUS_CUDA(cudaEventRecord(ev[0], s));
+      for (int l = 0; l < L; ++l) JANUS_CUDA(cudaStreamWaitEvent(ls[static_cast<size_t>(l)], ev[0], 0));
+      for (int m = 0; m < n_mb; ++m) launch_edge_kernel(st, u, which, m, m, m % L, ls[static_cast<size_t>(m % L)], true);
+      for (int l = 0; l < L; ++l) {
+        JANUS_CUDA(cudaEventRecord(ev[static_cast<size_t>(l) + 1], ls[static_cast<size_t>(l)]));
+        JANUS_CUDA(cudaStreamWaitEvent(s, ev[static_cast<size_t>(l) + 1], 0));
+      }
+    };
+    round();
+    JANUS_LAUNCH_CHECK("time_edge_kernel");
+    JANUS_CUDA(cudaEventRecord(a, s));
+    for (int i = 0; i < iters; ++i) round();
+    JANUS_CUDA(cudaEventRecord(z, s));
+    JANUS_CUDA(cudaEventSynchronize(z));
+    float ms = 0.f;
+    JANUS_CUDA(cudaEventElapsedTime(&ms, a, z));
+    for (auto& x : ls) cudaStreamDestroy(x);
+    for (auto& x : ev) cudaEventDestroy(x);
+    *avg_ms = ms / iters;  // one round: all micro-batches
+    *edges = E;
+    *flops = edge_kernel_flops_per_edge(which, kH, kR) * static_cast<double>(E);
+  }
   cudaEventDestroy(a);
   cudaEventDestroy(z);
-  *avg_ms = ms / iters;
-  *edges = g.n_edges;
-  *flops = edge_kernel_flops_per_edge(which, kH, kR) * g.n_edges;
 }
 
 // ============================================================ read-back

@@ -115,6 +115,9 @@ struct janus_stage {
   janus::LoadLayout lay;           // upload block layout (capacity offsets)
   int64_t static_bytes = 0, arena_bytes = 0;
   int tpc_fe = 1, tpc_wg = 1;        // TC edge tiles per CTA: FE/FF, BF/BE (stage_create)
+  int tc_tile_edges = 0;             // TC tiles: 0 cost-chosen runs, > 0 greedy edge budget (tuning)
+  int tc_tile_max_chunks = 0;        // cost-chosen tiles: max 128-edge chunks (0: by mean degree)
+  double tc_tile_ovh = 0.3;          // per-tile epilogue cost in chunk units
   janus::LmBuilder* lm = nullptr;  // device neighbour-list builder (lazy, janus_stage_load without a CSR)
 
   float* P(int u) const { return params + uoff[static_cast<size_t>(u - u0)]; }
