@@ -18,5 +18,5 @@ if [ -f build/trace/libjanus_b200.so ]; then
 fi
 ls -la $out | grep $tag
 # device LM (nbrlist.cu): full capture of the fill kernel on the batched C2 x 32 build
-timeout 300 ncu --set full --clock-control none -k regex:fill_kernel -s 20 -c 1 \
+timeout 300 ncu --set full --clock-control none -k regex:fill_kernel -s 280 -c 1 \
   -o $out/${tag}_nbr_fill python tools/nbrlist_bench.py > $out/${tag}_ncu_nbr.log 2>&1
