@@ -187,7 +187,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--method", default=None, choices=[None, "symfold", "wavek", "onef1b"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--lanes", type=int, default=16, help="concurrent micro-batch streams at N=1")
+    ap.add_argument("--lanes", type=int, default=32, help="concurrent micro-batch streams at N=1 (one per micro-batch)")
     ap.add_argument("--precision", default="tf32", choices=["tf32", "fp32"],
                     help="tf32: tcgen05 tensor-core edge kernels (tolerances in tests/test_gpu_tf32.py); "
                          "fp32: SIMT parity path")
