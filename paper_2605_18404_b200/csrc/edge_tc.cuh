@@ -384,7 +384,7 @@ __device__ __forceinline__ float fsig(float x) { return __fdividef(1.0f, 1.0f + 
 
 // ----------------------------------------------------------------------- FE
 // m_i = sum_{e in row i} w_e * v[col e], w = c (SiLU(phi A + alpha) B + beta)
-__global__ void __launch_bounds__(NT) msg_fe_tc(EdgeGeom g, const int4* __restrict__ tiles, int n_tiles, MsgParams p,
+__global__ void __launch_bounds__(NT, 2) msg_fe_tc(EdgeGeom g, const int4* __restrict__ tiles, int n_tiles, MsgParams p,
                                                float rc, const float* __restrict__ v, float* __restrict__ m_out) {
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = align1024(sm_raw);
