@@ -487,7 +487,7 @@ __global__ void __launch_bounds__(NT, 2) msg_fe_tc(EdgeGeom g, const int4* __res
 // ----------------------------------------------------------------------- FF
 // Y_i = sum w_e * am[col e];  F_i += sum_e (q_e + q_rev(e)) u_e with
 // q_e + q_rev(e) = < am_i v_j + am_j v_i , w'_e >  (w' symmetric in e <-> rev e)
-__global__ void __launch_bounds__(NT) msg_ff_tc(EdgeGeom g, const int4* __restrict__ tiles, int n_tiles, MsgParams p,
+__global__ void __launch_bounds__(NT, 2) msg_ff_tc(EdgeGeom g, const int4* __restrict__ tiles, int n_tiles, MsgParams p,
                                                float rc, const float* __restrict__ v, const float* __restrict__ am,
                                                float* __restrict__ Y_out, float* __restrict__ F,
                                                float* ah) {
@@ -499,15 +499,17 @@ __global__ void __launch_bounds__(NT) msg_ff_tc(EdgeGeom g, const int4* __restri
   uint8_t* T1 = T0 + kTile;   // phi' -> sdot
   float* al = reinterpret_cast<float*>(T1 + kTile);
   float* be = al + 64;
-  float* wts = be + 64;  // W^T [64][64] (fused row epilogue)
-  float* sq = wts + 64 * 64;  // [NQ][TE] per-quarter force scalars
+  // W^T for the fused row epilogue is read through L1 from the packed image in
+  // global memory (not staged): without its 16 KB two FF CTAs fit an SM
+  const float* wts = p.pack + kWtOff / sizeof(float);
+  float* sq = be + 64;  // [NQ][TE] per-quarter force scalars
   __shared__ __align__(8) uint64_t mbar;
   __shared__ uint32_t tslot;
   Ctx c;
   c.sm = sm;
   c.mbar = &mbar;
   __shared__ __align__(8) uint64_t wbar;
-  load_weights(sm, p.pack, 2, al, be, wts, &wbar);
+  load_weights(sm, p.pack, 2, al, be, nullptr, &wbar);
   setup(c, &tslot, 256);
   const uint32_t aW0 = tc::smem_u32(W0), aW1 = tc::smem_u32(W1), aT0 = tc::smem_u32(T0), aT1 = tc::smem_u32(T1);
   const int f0 = FPT * c.q;
@@ -1062,7 +1064,7 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int4* __res
 
 constexpr size_t kSmallBytes = sizeof(float) * (128 + NQ * TE) + 1024;  // alpha, beta, FF force scalars, 1 KB alignment slack
 constexpr size_t fe_smem() { return 2 * kWTile + 2 * kTile + kSmallBytes; }
-constexpr size_t ff_smem() { return 3 * kWTile + 2 * kTile + kSmallBytes; }  // + W^T
+constexpr size_t ff_smem() { return 2 * kWTile + 2 * kTile + kSmallBytes; }
 constexpr size_t be_smem() { return 4 * kWTile + 4 * kTile + kSmallBytes; }
 constexpr size_t bf_smem() { return 4 * kWTile + 4 * kTile + kSmallBytes; }
 
