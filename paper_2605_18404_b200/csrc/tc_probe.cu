@@ -5,6 +5,7 @@
 // fp32 in global) are staged into core-matrix smem tiles, K/8 kind::tf32 MMAs
 // run with K-major (rows = M|N, cols = K) or MN-major (rows = K, cols = M|N)
 // descriptors, and the raw TMEM image (128 lanes x N columns) is returned.
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include "../../include/janus/errors.hpp"
@@ -29,11 +30,21 @@ __global__ void __launch_bounds__(128) tc_probe_kernel(ProbeArgs p, const float*
   char* pa = reinterpret_cast<char*>(sa);
   char* pb = reinterpret_cast<char*>(sb);
   const bool sw = p.layout == 2;
-  for (int x = t; x < p.a_rows * p.a_cols; x += 128) {
+  if (p.layout == 3) {  // bf16 SWIZZLE_128B tiles, kind::f16 (K-step 16)
+    for (int x = t; x < p.a_rows * p.a_cols; x += 128) {
+      const int r = x / p.a_cols, c = x % p.a_cols;
+      *reinterpret_cast<__nv_bfloat16*>(pa + tc::sw128_off_b16(r, c, p.a_rows)) = __float2bfloat16_rn(A[x]);
+    }
+    for (int x = t; x < p.b_rows * p.b_cols; x += 128) {
+      const int r = x / p.b_cols, c = x % p.b_cols;
+      *reinterpret_cast<__nv_bfloat16*>(pb + tc::sw128_off_b16(r, c, p.b_rows)) = __float2bfloat16_rn(B[x]);
+    }
+  }
+  for (int x = t; x < p.a_rows * p.a_cols && p.layout != 3; x += 128) {
     const int r = x / p.a_cols, c = x % p.a_cols;
     *reinterpret_cast<float*>(pa + (sw ? tc::sw128_off(r, c, p.a_rows) : tc::core_off(r, c, p.a_cols))) = A[x];
   }
-  for (int x = t; x < p.b_rows * p.b_cols; x += 128) {
+  for (int x = t; x < p.b_rows * p.b_cols && p.layout != 3; x += 128) {
     const int r = x / p.b_cols, c = x % p.b_cols;
     *reinterpret_cast<float*>(pb + (sw ? tc::sw128_off(r, c, p.b_rows) : tc::core_off(r, c, p.b_cols))) = B[x];
   }
@@ -46,9 +57,23 @@ __global__ void __launch_bounds__(128) tc_probe_kernel(ProbeArgs p, const float*
   const uint32_t tmem = tmem_base;
   if (t == 0) {
     const uint32_t a0 = tc::smem_u32(sa), b0 = tc::smem_u32(sb);
+    if (p.layout == 3) {
+      // K-major: rows = M|N, K along 64-col slabs: k-step s (16) -> slab s/4, +32 B inside the row
+      // MN-major: rows = K: k-step of 16 rows -> +2048 B; one 64-wide MN slab (LBO unused: rows*128)
+      const uint32_t id16 = tc::idesc_bf16(p.M, p.N, p.a_mn, p.b_mn);
+      const uint32_t a_slab = p.a_rows * 128, b_slab = p.b_rows * 128;
+      for (int s = 0; s < p.K / 16; ++s) {
+        const uint64_t da = p.a_mn ? tc::smem_desc(a0 + 2048 * s, a_slab, 1024, 2)
+                                   : tc::smem_desc(a0 + (s >> 2) * a_slab + 32 * (s & 3), 16, 1024, 2);
+        const uint64_t db = p.b_mn ? tc::smem_desc(b0 + 2048 * s, b_slab, 1024, 2)
+                                   : tc::smem_desc(b0 + (s >> 2) * b_slab + 32 * (s & 3), 16, 1024, 2);
+        tc::mma_bf16(tmem, da, db, id16, s > 0);
+      }
+      tc::commit(&mbar);
+    }
     const uint32_t id = tc::idesc_tf32(p.M, p.N, p.a_mn, p.b_mn);
     const uint32_t a_grp = (p.a_cols / 4) * 128, b_grp = (p.b_cols / 4) * 128;
-    for (int s = 0; s < p.K / 8; ++s) {
+    for (int s = 0; s < p.K / 8 && p.layout != 3; ++s) {
       if (sw) {
         // K-major: rows = M|N, K along the 32-col slabs: k-step s -> slab s/4, +32 B inside the row
         // MN-major: rows = K: k-step of 8 rows -> +1024 B; MN slabs of 32 at LBO = rows*128
@@ -66,7 +91,7 @@ __global__ void __launch_bounds__(128) tc_probe_kernel(ProbeArgs p, const float*
       const uint64_t db = p.b_mn ? tc::smem_desc(b0 + b_grp * s, bl, bs) : tc::smem_desc(b0 + 256 * s, 128, b_grp);
       tc::mma_tf32(tmem, da, db, id, s > 0);
     }
-    tc::commit(&mbar);
+    if (p.layout != 3) tc::commit(&mbar);
   }
   tc::mbar_wait(&mbar, 0);
   tc::fence_after();
