@@ -19,6 +19,8 @@
 //    return zeros for kind::tf32 (tests/test_gpu_tc.py) and is not used.
 #pragma once
 
+#include <cuda_bf16.h>
+
 #include "common.cuh"
 #include "edge_kernels.cuh"
 #include "tc.cuh"
@@ -607,6 +609,54 @@ __global__ void __launch_bounds__(NT, 2) msg_ff_tc(EdgeGeom g, const int4* __res
   teardown(c, 256);
 }
 
+// Weight-gradient operands in bf16 (kind::f16): an edge-major [128 edges][64
+// features] bf16 tile (one 128 B SWIZZLE_128B row per edge, 16 KB) is an
+// MN-major operand of sum_e X_e^T Y_e (M|N = features, K = edges), so no
+// transposed copy is written (tcgen05 MN-major returns zeros for kind::tf32,
+// tests/test_gpu_tc.py).  Per-edge contractions stay tf32.
+constexpr uint32_t kBTile = 128 * 64 * 2;
+__device__ __forceinline__ uint32_t off_b16(int e, int f) { return tc::sw128_off_b16(e, f, 128); }
+__device__ __forceinline__ void st_b16(uint8_t* t, int e, int f0, const float (&v)[FPT]) {
+#pragma unroll
+  for (int j = 0; j < FPT / 8; ++j) {
+    const __nv_bfloat162 a = __floats2bfloat162_rn(v[8 * j], v[8 * j + 1]), b = __floats2bfloat162_rn(v[8 * j + 2], v[8 * j + 3]);
+    const __nv_bfloat162 c = __floats2bfloat162_rn(v[8 * j + 4], v[8 * j + 5]), d = __floats2bfloat162_rn(v[8 * j + 6], v[8 * j + 7]);
+    uint4 w;
+    w.x = *reinterpret_cast<const uint32_t*>(&a);
+    w.y = *reinterpret_cast<const uint32_t*>(&b);
+    w.z = *reinterpret_cast<const uint32_t*>(&c);
+    w.w = *reinterpret_cast<const uint32_t*>(&d);
+    *reinterpret_cast<uint4*>(t + off_b16(e, f0 + 8 * j)) = w;
+  }
+}
+// D[64][64] (+)= sum_e A[e][m] B[e][n] over the 128 edges of two bf16 tiles
+// (MN-major SWIZZLE_128B: K-step of 16 edges = 2048 B; one 64-wide MN slab).
+__device__ __forceinline__ void mma_wg_b16(uint32_t d, uint32_t a, uint32_t b, bool accumulate) {
+  constexpr uint32_t id = tc::idesc_bf16(64, 64, true, true);
+  const uint64_t da0 = tc::smem_desc(a, kBTile, 1024, 2), db0 = tc::smem_desc(b, kBTile, 1024, 2);
+#pragma unroll
+  for (int s = 0; s < TE / 16; ++s) {
+    const uint64_t o = static_cast<uint64_t>((2048 * s) >> 4);
+    tc::mma_bf16(d, da0 + o, db0 + o, id, (s > 0 || accumulate) ? 1u : 0u);
+  }
+}
+// Column sums (over the chunk's edges) of an edge-major fp32 SWIZZLE_128B tile
+// [128 edges][64 features], added to acc[64] (shared memory): 8 threads per
+// feature take edges p, p+8, ... (conflict-free scalar loads), an xor
+// butterfly combines them, one thread adds — a fixed order, deterministic.
+__device__ __forceinline__ void em_colsum_add(const uint8_t* t, float* acc) {
+  if (threadIdx.x < 512) {
+    const int f = static_cast<int>(threadIdx.x) >> 3, p = static_cast<int>(threadIdx.x) & 7;
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < TE / 8; ++k) s += *reinterpret_cast<const float*>(t + off_em(p + 8 * k, f));
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s += __shfl_xor_sync(0xffffffffu, s, 4);
+    if (p == 0) acc[f] += s;
+  }
+}
+
 // Column sums (over the chunk's edges) of a feature-major SWIZZLE_128B tile
 // [64 features][128 edges], added to the CTA accumulator acc[64] in shared
 // memory: 8 threads per feature read 16 edges each (4 conflict-free LDS.128),
@@ -683,6 +733,8 @@ __device__ __forceinline__ void write_partial(Ctx& c, float* part, uint8_t* scra
 // ----------------------------------------------------------------------- BE
 // Yb_i = sum w_e * bm[col e]; gbar = c bm_i v_j; dB = s^T gbar; dbeta = sum gbar;
 // zbar = (gbar B^T) SiLU'(z); dA = phi^T zbar; dalpha = sum zbar.
+// Per chunk: fp32 tiles T0 (phi -> s -> w bm_j rows -> zbar) and T1 (gbar,
+// A of sbar); bf16 tiles B0..B3 = phi, s, gbar, zbar for the weight gradients.
 __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int4* __restrict__ tiles, int n_tiles, MsgParams p,
                                                   float rc, const float* __restrict__ v, const float* __restrict__ bm,
                                                   float* __restrict__ Yb_out, float* __restrict__ partial,
@@ -696,26 +748,29 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int4* __res
   uint8_t* W2 = W1 + kWTile;  // B
   uint8_t* T0 = W2 + kWTile;
   uint8_t* T1 = T0 + kTile;
-  uint8_t* T2 = T1 + kTile;
-  uint8_t* T3 = T2 + kTile;
-  float* al = reinterpret_cast<float*>(T3 + kTile);
+  uint8_t* B0 = T1 + kTile;   // bf16: phi
+  uint8_t* B1 = B0 + kBTile;  //       s
+  uint8_t* B2 = B1 + kBTile;  //       gbar
+  uint8_t* B3 = B2 + kBTile;  //       zbar
+  float* al = reinterpret_cast<float*>(B3 + kBTile);
   float* be = al + 64;
-  float* wts = be + 64;  // W^T [64][64] (fused row epilogue)
-  float* csa = wts + 64 * 64;  // CTA column sums: dalpha, dbeta
+  float* csa = be + 64;  // CTA column sums: dalpha, dbeta
   float* csb = csa + 64;
+  const float* wts = p.pack + kWtOff / sizeof(float);  // W^T (row epilogue) through L1
   __shared__ __align__(8) uint64_t mbar;
   __shared__ uint32_t tslot;
   Ctx c;
   c.sm = sm;
   c.mbar = &mbar;
   __shared__ __align__(8) uint64_t wbar;
-  load_weights(sm, p.pack, 3, al, be, wts, &wbar);
+  load_weights(sm, p.pack, 3, al, be, nullptr, &wbar);
   if (threadIdx.x < 128) csa[threadIdx.x] = 0.f;  // csa, csb (published by setup's barrier)
   TC_M();
   setup(c, &tslot, 512);
   TC_M();
   const uint32_t aW0 = tc::smem_u32(W0), aW1 = tc::smem_u32(W1), aW2 = tc::smem_u32(W2);
-  const uint32_t aT0 = tc::smem_u32(T0), aT1 = tc::smem_u32(T1), aT2 = tc::smem_u32(T2), aT3 = tc::smem_u32(T3);
+  const uint32_t aT0 = tc::smem_u32(T0), aT1 = tc::smem_u32(T1);
+  const uint32_t aB0 = tc::smem_u32(B0), aB1 = tc::smem_u32(B1), aB2 = tc::smem_u32(B2), aB3 = tc::smem_u32(B3);
   bool first = true;
   const int f0 = FPT * c.q;
   for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
@@ -729,6 +784,7 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int4* __res
         float ph[FPT], dph[FPT];
         basis(es.d, rc, f0, ph, dph);
         st_em(T0, c.e, f0, ph);
+        st_b16(B0, c.e, f0, ph);  // phi (A of dA)
       }
       tc::mbar_wait(&wbar, 0);  // weights landed (immediate after the first chunk)
       c.publish();
@@ -747,8 +803,8 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int4* __res
           const float zz = z[j] + al[f0 + j];
           z[j] = zz * fsig(zz);
         }
-        st_em(T0, c.e, f0, z);  // s, edge-major (A of g = s B)
-        st_fm(T1, c.e, f0, z);  // s^T (A of dB = s^T gbar)
+        st_em(T0, c.e, f0, z);   // s, edge-major (A of g = s B)
+        st_b16(B1, c.e, f0, z);  // s (A of dB = s^T gbar)
       }
       c.publish();
       if (threadIdx.x == 0) {
@@ -758,41 +814,43 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int4* __res
       TC_M();
       c.wait_mma();
       TC_M();
-      float gb[FPT];
       {
-        float gg[FPT], bj[FPT], bi[FPT], vj[FPT];
-        gather32(bm, es.j, f0, bj);
-        gather32(bm, es.i, f0, bi);
-        gather32(v, es.j, f0, vj);
-        c.ld(TM_G, gg);
-        TC_M();
+        float gb[FPT];
+        {
+          float gg[FPT], bj[FPT], bi[FPT], vj[FPT];
+          gather32(bm, es.j, f0, bj);
+          gather32(bm, es.i, f0, bi);
+          gather32(v, es.j, f0, vj);
+          c.ld(TM_G, gg);
+          TC_M();
 #pragma unroll
-        for (int q = 0; q < FPT; ++q) {
-          gg[q] = es.c * (gg[q] + be[f0 + q]) * bj[q];  // w_e * bm_j
-          gb[q] = es.c * bi[q] * vj[q];                 // gbar (zero on padding edges: c = 0)
+          for (int q = 0; q < FPT; ++q) {
+            gg[q] = es.c * (gg[q] + be[f0 + q]) * bj[q];  // w_e * bm_j
+            gb[q] = es.c * bi[q] * vj[q];                 // gbar (zero on padding edges: c = 0)
+          }
+          TC_M();
+          st_pl(T0, c.e, f0, gg);
         }
-        TC_M();
-        st_pl(T0, c.e, f0, gg);
+        st_em(T1, c.e, f0, gb);   // gbar (A of sbar = gbar B^T; its column sums)
+        st_b16(B2, c.e, f0, gb);  // gbar (B of dB)
       }
-      st_fm(T2, c.e, f0, gb);  // gbar^T (B of dB)
-      st_em(T3, c.e, f0, gb);  // gbar   (A of sbar = gbar B^T)
       TC_M();
       c.publish();
       TC_M();
       if (threadIdx.x == 0) {
-        mma_tiles<64, 64, 128, 64>(c.tmem + TM_BG, aT1, aT2, !first);
-        mma_tiles<128, 64, 64, 128>(c.tmem + TM_G, aT3, aW2, false);
+        mma_wg_b16(c.tmem + TM_BG, aB1, aB2, !first);                // dB += s^T gbar
+        mma_tiles<128, 64, 64, 128>(c.tmem + TM_G, aT1, aW2, false);  // sbar
         tc::commit(c.mbar);
       }
       TC_M();
-      {  // row sums overlap the MMAs (they read T1..T3, this reads T0)
+      {  // row sums and dbeta overlap the MMAs (reads of T0 / T1)
         const uint8_t* const tl[1] = {T0};
         seg_rows<1>(g, tr.r0, c0, ne, tl, sg, acc);
       }
-      fm_colsum_add(T2, csb);  // dbeta += sum_e gbar_e (reads gbar^T beside the dB MMA)
+      em_colsum_add(T1, csb);  // dbeta += sum_e gbar_e
       TC_M();
       c.wait_mma();
-      __syncthreads();  // T0 reads done before it is rewritten
+      __syncthreads();  // T0 / T1 reads done before T0 is rewritten
       TC_M();
       {
         float z[FPT], sb[FPT];
@@ -802,17 +860,15 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int4* __res
           const float zz = z[j] + al[f0 + j], s1 = fsig(zz);
           z[j] = sb[j] * (s1 * (1.0f + zz * (1.0f - s1)));
         }
-        st_fm(T2, c.e, f0, z);  // zbar^T
-        float ph[FPT], dph[FPT];
-        basis(es.d, rc, f0, ph, dph);
-        st_fm(T0, c.e, f0, ph);  // phi^T
+        st_b16(B3, c.e, f0, z);  // zbar (B of dA)
+        st_em(T0, c.e, f0, z);   // zbar (column sums)
       }
       c.publish();
       if (threadIdx.x == 0) {
-        mma_tiles<64, 64, 128, 64>(c.tmem + TM_AG, aT0, aT2, !first);
+        mma_wg_b16(c.tmem + TM_AG, aB0, aB3, !first);  // dA += phi^T zbar
         tc::commit(c.mbar);
       }
-      fm_colsum_add(T2, csa);  // dalpha += sum_e zbar_e (beside the dA MMA)
+      em_colsum_add(T0, csa);  // dalpha += sum_e zbar_e (beside the dA MMA)
       TC_M();
       c.wait_mma();
       TC_M();
@@ -842,6 +898,9 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int4* __res
 // ----------------------------------------------------------------------- BF
 // Second-order term.  Outputs: mdot_i = sum_e qb w'_e v_j + w_e vdot_j,
 // X_i = sum_e qb w'_e am_j, and the partial [dA | dalpha | dB | dbeta].
+// Per chunk: fp32 tiles T0/T1 (phi, phi' -> s, sdot -> row terms -> mu, nu;
+// zbar for its column sums) and bf16 tiles B0..B5 = s, sdot, mu|zbar,
+// nu|zbar', phi, phi' for the weight gradients (phi kept: no second basis).
 __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int4* __restrict__ tiles, int n_tiles, MsgParams p,
                                                   float rc, const float* __restrict__ v, const float* __restrict__ vdot,
                                                   const float* __restrict__ am, const float* __restrict__ Fbar,
@@ -858,28 +917,32 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int4* __res
   uint8_t* W2 = W1 + kWTile;
   uint8_t* T0 = W2 + kWTile;
   uint8_t* T1 = T0 + kTile;
-  uint8_t* T2 = T1 + kTile;
-  uint8_t* T3 = T2 + kTile;
-  float* al = reinterpret_cast<float*>(T3 + kTile);
+  uint8_t* B0 = T1 + kTile;   // bf16: s
+  uint8_t* B1 = B0 + kBTile;  //       sdot
+  uint8_t* B2 = B1 + kBTile;  //       mu, then zbar
+  uint8_t* B3 = B2 + kBTile;  //       nu, then zbar'
+  uint8_t* B4 = B3 + kBTile;  //       phi
+  uint8_t* B5 = B4 + kBTile;  //       phi'
+  float* al = reinterpret_cast<float*>(B5 + kBTile);
   float* be = al + 64;
-  float* wts = be + 64;  // W^T [64][64] (fused row epilogue)
-  float* csa = wts + 64 * 64;  // CTA column sums: dalpha, dbeta
+  float* csa = be + 64;  // CTA column sums: dalpha, dbeta
   float* csb = csa + 64;
+  const float* wts = p.pack + kWtOff / sizeof(float);  // W^T (row epilogue) through L1
   __shared__ __align__(8) uint64_t mbar;
   __shared__ uint32_t tslot;
   Ctx c;
   c.sm = sm;
   c.mbar = &mbar;
   __shared__ __align__(8) uint64_t wbar;
-#ifndef JANUS_TC_LATEW
-  load_weights(sm, p.pack, 3, al, be, wts, &wbar);
-#endif
+  load_weights(sm, p.pack, 3, al, be, nullptr, &wbar);
   if (threadIdx.x < 128) csa[threadIdx.x] = 0.f;  // csa, csb (published by setup's barrier)
   TC_M();
   setup(c, &tslot, 512);
   TC_M();
   const uint32_t aW0 = tc::smem_u32(W0), aW1 = tc::smem_u32(W1), aW2 = tc::smem_u32(W2);
-  const uint32_t aT0 = tc::smem_u32(T0), aT1 = tc::smem_u32(T1), aT2 = tc::smem_u32(T2), aT3 = tc::smem_u32(T3);
+  const uint32_t aT0 = tc::smem_u32(T0), aT1 = tc::smem_u32(T1);
+  const uint32_t aB0 = tc::smem_u32(B0), aB1 = tc::smem_u32(B1), aB2 = tc::smem_u32(B2), aB3 = tc::smem_u32(B3);
+  const uint32_t aB4 = tc::smem_u32(B4), aB5 = tc::smem_u32(B5);
   bool first = true;
   const int f0 = FPT * c.q;
   for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
@@ -895,9 +958,6 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int4* __res
         asm volatile("mov.b32 %0, %1;" : "=f"(dmy) : "f"(es.d));
         TC_M();
       }
-#ifdef JANUS_TC_LATEW
-      if (first) load_weights(sm, p.pack, 3, al, be, wts, &wbar);
-#endif
 #endif
       {
         float ph[FPT], dph[FPT];
@@ -905,6 +965,8 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int4* __res
         TC_M();
         st_em(T0, c.e, f0, ph);
         st_em(T1, c.e, f0, dph);
+        st_b16(B4, c.e, f0, ph);   // phi  (A of dA)
+        st_b16(B5, c.e, f0, dph);  // phi' (A of dA)
       }
       TC_M();
       tc::mbar_wait(&wbar, 0);
@@ -930,8 +992,8 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int4* __res
         }
         st_em(T0, c.e, f0, z);   // s
         st_em(T1, c.e, f0, zp);  // sdot
-        st_fm(T2, c.e, f0, z);   // s^T
-        st_fm(T3, c.e, f0, zp);  // sdot^T
+        st_b16(B0, c.e, f0, z);  // s    (A of dB)
+        st_b16(B1, c.e, f0, zp); // sdot (A of dB)
       }
       c.publish();
       if (threadIdx.x == 0) {
@@ -975,10 +1037,15 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int4* __res
         TC_M();
         st_pl(T0, c.e, f0, pm);
         st_pl(T1, c.e, f0, px);
+        st_b16(B2, c.e, f0, mu);  // mu (B of dB)
+        st_b16(B3, c.e, f0, nu);  // nu (B of dB)
       }
       TC_M();
-      tc::fence_before();
-      __syncthreads();
+      c.publish();
+      if (threadIdx.x == 0) {  // dB += s^T mu + sdot^T nu, under the row sums (committed with sbar)
+        mma_wg_b16(c.tmem + TM_BG, aB0, aB2, !first);
+        mma_wg_b16(c.tmem + TM_BG, aB1, aB3, true);
+      }
       TC_M();
       {
         const uint8_t* const tl[2] = {T0, T1};
@@ -986,28 +1053,17 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int4* __res
       }
       TC_M();
       __syncthreads();         // row sums done with T0/T1
-      st_fm(T0, c.e, f0, mu);  // mu^T
-      st_fm(T1, c.e, f0, nu);  // nu^T
-      c.publish();
-      if (threadIdx.x == 0) {  // dB += s^T mu + sdot^T nu
-        mma_tiles<64, 64, 128, 64>(c.tmem + TM_BG, aT2, aT0, !first);
-        mma_tiles<64, 64, 128, 64>(c.tmem + TM_BG, aT3, aT1, true);
-        tc::commit(c.mbar);
-      }
-      fm_colsum_add(T0, csb);  // dbeta += sum_e mu_e (reads mu^T beside the dB MMA)
-      TC_M();
-      c.wait_mma();
-      TC_M();
-      st_em(T2, c.e, f0, mu);  // mu (A of sbar = mu B^T)
-      st_em(T3, c.e, f0, nu);  // nu
+      st_em(T0, c.e, f0, mu);  // mu (A of sbar = mu B^T; its column sums)
+      st_em(T1, c.e, f0, nu);  // nu
       c.publish();
       if (threadIdx.x == 0) {
-        mma_tiles<128, 64, 64, 128>(c.tmem + TM_G, aT2, aW2, false);   // sbar
-        mma_tiles<128, 64, 64, 128>(c.tmem + TM_GP, aT3, aW2, false);  // sdotbar
-        tc::commit(c.mbar);
+        mma_tiles<128, 64, 64, 128>(c.tmem + TM_G, aT0, aW2, false);   // sbar
+        mma_tiles<128, 64, 64, 128>(c.tmem + TM_GP, aT1, aW2, false);  // sdotbar
+        tc::commit(c.mbar);  // completes with every earlier MMA of this thread (dB too)
       }
+      em_colsum_add(T0, csb);  // dbeta += sum_e mu_e (beside the MMAs)
       TC_M();
-      c.wait_mma();
+      c.wait_mma();  // dB and sbar done: B2/B3 and T1 are free
       TC_M();
       {
         float z[FPT], zp[FPT], sb[FPT], sdb[FPT];
@@ -1021,20 +1077,17 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int4* __res
           z[j] = sb[j] * ds + sdb[j] * d2s * zp[j];  // zbar
           zp[j] = sdb[j] * ds;                       // zbar'
         }
-        st_fm(T2, c.e, f0, z);
-        st_fm(T3, c.e, f0, zp);
-        float ph[FPT], dph[FPT];
-        basis(es.d, rc, f0, ph, dph);
-        st_fm(T0, c.e, f0, ph);   // phi^T
-        st_fm(T1, c.e, f0, dph);  // phi'^T
+        st_b16(B2, c.e, f0, z);   // zbar  (B of dA)
+        st_b16(B3, c.e, f0, zp);  // zbar' (B of dA)
+        st_em(T1, c.e, f0, z);    // zbar (column sums; T0 is still being summed)
       }
       c.publish();
       if (threadIdx.x == 0) {  // dA += phi^T zbar + phi'^T zbar'
-        mma_tiles<64, 64, 128, 64>(c.tmem + TM_AG, aT0, aT2, !first);
-        mma_tiles<64, 64, 128, 64>(c.tmem + TM_AG, aT1, aT3, true);
+        mma_wg_b16(c.tmem + TM_AG, aB4, aB2, !first);
+        mma_wg_b16(c.tmem + TM_AG, aB5, aB3, true);
         tc::commit(c.mbar);
       }
-      fm_colsum_add(T2, csa);  // dalpha += sum_e zbar_e (beside the dA MMA)
+      em_colsum_add(T1, csa);  // dalpha += sum_e zbar_e (beside the dA MMA)
       TC_M();
       c.wait_mma();
       TC_M();
@@ -1065,8 +1118,8 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int4* __res
 constexpr size_t kSmallBytes = sizeof(float) * (128 + NQ * TE) + 1024;  // alpha, beta, FF force scalars, 1 KB alignment slack
 constexpr size_t fe_smem() { return 2 * kWTile + 2 * kTile + kSmallBytes; }
 constexpr size_t ff_smem() { return 2 * kWTile + 2 * kTile + kSmallBytes; }
-constexpr size_t be_smem() { return 4 * kWTile + 4 * kTile + kSmallBytes; }
-constexpr size_t bf_smem() { return 4 * kWTile + 4 * kTile + kSmallBytes; }
+constexpr size_t be_smem() { return 3 * kWTile + 2 * kTile + 4 * kBTile + kSmallBytes; }
+constexpr size_t bf_smem() { return 3 * kWTile + 2 * kTile + 6 * kBTile + kSmallBytes; }
 
 }  // namespace edge_tc
 }  // namespace janus
