@@ -1,5 +1,7 @@
-"""Tensor-core (tcgen05 kind::tf32) path of the msg edge kernels against the
-fp64 oracle.  tf32 keeps 10 mantissa bits, so the tolerances are widened and
+"""Tensor-core path of the msg edge kernels against the fp64 oracle: per-edge
+contractions on tcgen05 kind::tf32 (10 mantissa bits), the BF/BE
+edge-parameter weight gradients sum_e X_e^T Y_e on kind::f16 with bf16
+operands (8 bits) and fp32 accumulation.  The tolerances are widened and
 stated here (north star: "widened and documented where tf32/bf16 tensor-core
 paths are used"): E relative 2e-3, F 2e-2 and parameter gradients 2e-2 of the
 max magnitude.  The fp32 SIMT path (test_gpu_stage.py) keeps 1e-5 / 1e-4."""
