@@ -22,6 +22,7 @@
 #include "edge_kernels.cuh"
 #include "edge_tc.cuh"
 #include "node_kernels.cuh"
+#include "wgrad_tc.cuh"
 #include "stage.cuh"
 #include "stage_api.hpp"
 #include "nbrlist.hpp"
@@ -120,15 +121,24 @@ node::WJob wjob(const float* a, const float* b, float* G, const float* a2 = null
   return j;
 }
 
-void wjobs(Scratch& sc, cudaStream_t s, int rows, std::initializer_list<node::WJob> list) {
+bool use_tc(const janus_stage* st);
+
+// Node weight gradients of one phase (up to 3 jobs per launch): tcgen05 in
+// the tensor-core mode (wgrad_tc.cuh, one CTA per job), the output-partitioned
+// SIMT kernel in the fp32 parity mode.
+void wjobs(const janus_stage* st, Scratch& sc, cudaStream_t s, int rows, std::initializer_list<node::WJob> list) {
   if (prof_skip() & 16) return;
   node::WJobs J{};
   J.n = static_cast<int>(list.size());
   int k = 0;
   for (const auto& j : list) J.j[k++] = j;
-  const dim3 grid(9u, static_cast<unsigned>(J.n));  // 8 row blocks of the gradient + 1 column-sum block
-  node::wgrad_multi_kernel<<<grid, 256, 0, s>>>(rows, J, sc.wpart, sc.counter);
-  JANUS_LAUNCH_CHECK("wgrad_multi");
+  if (use_tc(st)) {
+    edge_tc::wgrad_tc_kernel<<<J.n, 256, edge_tc::wgrad_tc_smem(), s>>>(rows, J);
+  } else {
+    const dim3 grid(9u, static_cast<unsigned>(J.n));  // 8 row blocks of the gradient + 1 column-sum block
+    node::wgrad_multi_kernel<<<grid, 256, 0, s>>>(rows, J, sc.wpart, sc.counter);
+  }
+  JANUS_LAUNCH_CHECK("wgrad");
 }
 
 // out[z][k] = sum_{Z_i = z} x[i][k]; x == null: out[z] = sum_{Z_i = z} eps[s(i)]
@@ -414,6 +424,7 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
       sc.wpart = dalloc<float>(st, 3 * chunks * std::max<size_t>(kH * kH + 2 * kH, static_cast<size_t>(m.n_species) * kH), false);
       sc.counter = dalloc<unsigned>(st, 1, false);
     }
+    JANUS_CUDA(cudaFuncSetAttribute(edge_tc::wgrad_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge_tc::wgrad_tc_smem()));
     JANUS_CUDA(cudaFuncSetAttribute(edge::msg_fe_kernel<kH, kR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge::fe_smem<kH, kR>()));
     JANUS_CUDA(cudaFuncSetAttribute(edge::msg_ff_kernel<kH, kR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge::ff_smem<kH, kR>()));
     JANUS_CUDA(cudaFuncSetAttribute(edge::msg_bf_kernel<kH, kR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge::bf_smem<kH, kR>()));
@@ -799,7 +810,7 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
           JANUS_CUDA(cudaMemsetAsync(sc.s2, 0, sizeof(float) * NH, s));
         }
         if (!(g.n_tiles > 0 && use_tc(st))) gemm(s, N, sc.s2, T + H * H, nullptr, nullptr, nullptr, b.inj);  // hbar^F = X W^T
-        wjobs(sc, s, N, {wjob(in_h(st, sl, u, N), sc.s2, G2 + EC::PE, ah, b.ff_Y)});  // dW2 = h^T X + abar^T Y
+        wjobs(st, sc, s, N, {wjob(in_h(st, sl, u, N), sc.s2, G2 + EC::PE, ah, b.ff_Y)});  // dW2 = h^T X + abar^T Y
         break;
       }
       case kUpd: {
@@ -808,7 +819,7 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
         // pdot, r, pbar (s3), pdbar (s4), u (s5), mbar^F = pbar U^T, abar' = abar_h + u V
         if (!(prof_skip() & 32)) node::upd_bf_fused<<<blocks(N, node::kRB), 256, node::upd_smem(4), s>>>(N, am, b.ff_a, b.p, Um, T + H * H, T, V, sc.s3, sc.s4,
                                                                 sc.s5, b.inj, ah);
-        wjobs(sc, s, N, {wjob(sc.s5, b.ff_a, dV),                                          // dV2 = u^T a'
+        wjobs(st, sc, s, N, {wjob(sc.s5, b.ff_a, dV),                                          // dV2 = u^T a'
                          wjob(in_m(st, sl, u, N), sc.s3, dU, am, sc.s4, false, sc.s3, dups)});  // dU2, dups2
         break;
       }
@@ -819,7 +830,7 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
         node::ro_bf_ew_kernel<kH><<<blocks(NH, 256), 256, 0, s>>>(static_cast<int>(NH), sc.s1, b.p, om, sc.s2,
                                                                   sc.s3, sc.s4);
         gemm(s, N, sc.s2, T, nullptr, nullptr, nullptr, b.inj);  // hbar^F = tau O^T
-        wjobs(sc, s, N, {wjob(ah, sc.s4, dO, in_h(st, sl, u, N), sc.s2, false, sc.s3, dom, sc.s2, dob)});
+        wjobs(st, sc, s, N, {wjob(ah, sc.s4, dO, in_h(st, sl, u, N), sc.s2, false, sc.s3, dom, sc.s2, dob)});
         break;
       }
     }
@@ -871,7 +882,7 @@ void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only, 
         node::ro_be_ew_kernel<kH><<<blocks(NH, 256), 256, 0, s>>>(static_cast<int>(NH), b.p, om, sl.eps, g.struct_id,
                                                                   sc.s1, sc.s2);
         gemm(s, N, sc.s1, T, nullptr, b.inj, nullptr, bh);  // b_h = tbar O^T + hbar^F
-        wjobs(sc, s, N, {wjob(in_h(st, sl, u, N), sc.s1, dO, nullptr, nullptr, false, sc.s1, dob, sc.s2, dom)});
+        wjobs(st, sc, s, N, {wjob(in_h(st, sl, u, N), sc.s1, dO, nullptr, nullptr, false, sc.s1, dob, sc.s2, dom)});
         species_sum(st, sc, s, g, nullptr, sl.eps, dbias);
         break;
       }
@@ -879,7 +890,7 @@ void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only, 
         float *dU = G1, *dups = G1 + H * H, *dV = G1 + H * H + H;
         // pbar (s2) = (b' V^T) SiLU'(p); b_m = pbar U^T + mbar^F
         if (!(prof_skip() & 32)) node::upd_be_fused<<<blocks(N, node::kRB), 256, node::upd_smem(2), s>>>(N, bh, b.p, T + H * H, T, b.inj, sc.s2, bm);
-        wjobs(sc, s, N, {wjob(b.p, bh, dV, nullptr, nullptr, true),                                  // dV1 = SiLU(p)^T b'
+        wjobs(st, sc, s, N, {wjob(b.p, bh, dV, nullptr, nullptr, true),                                  // dV1 = SiLU(p)^T b'
                          wjob(in_m(st, sl, u, N), sc.s2, dU, nullptr, nullptr, false, sc.s2, dups)});  // dU1, dups1
         break;
       }
@@ -899,7 +910,7 @@ void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only, 
         } else {
           JANUS_CUDA(cudaMemsetAsync(sc.s1, 0, sizeof(float) * NH, s));
         }
-        wjobs(sc, s, N, {wjob(in_h(st, sl, u, N), sc.s1, G1 + EC::PE)});  // dW1 = h^T Yb
+        wjobs(st, sc, s, N, {wjob(in_h(st, sl, u, N), sc.s1, G1 + EC::PE)});  // dW1 = h^T Yb
         if (!(g.n_tiles > 0 && use_tc(st))) gemm(s, N, sc.s1, T + H * H, nullptr, bh, b.inj, bh);  // b_h += Yb W^T + hbar^F
         break;
       }

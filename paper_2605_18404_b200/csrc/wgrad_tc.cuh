@@ -1,0 +1,123 @@
+// wgrad_tc.cuh — node-side weight gradients G = sum_i op(a_i)^T b_i
+// (+ a2_i^T b2_i) of the upd / msg / readout units on 5th-gen tensor cores
+// (the JANUS_PREC_TF32 path; the fp32 parity path keeps
+// node_kernels.cuh wgrad_multi_kernel).  One CTA per job: 128-atom blocks of
+// a and b are staged transposed ([64 features][128 atoms], SWIZZLE_128B
+// K-major, the same layout as edge_tc.cuh's feature-major tiles) and
+// contracted by M=64 x N=64 x K=128 kind::tf32 MMAs accumulating in TMEM in
+// atom-block order — deterministic, one launch CTA instead of nine.
+#pragma once
+
+#include "edge_tc.cuh"
+#include "geo_job.hpp"
+#include "node_kernels.cuh"
+
+namespace janus {
+namespace edge_tc {
+
+constexpr size_t wgrad_tc_smem() { return 2 * kTile + 1024; }
+
+__global__ void __launch_bounds__(256, 1) wgrad_tc_kernel(int rows, node::WJobs jobs) {
+  extern __shared__ __align__(1024) uint8_t sm_raw[];
+  uint8_t* sm = align1024(sm_raw);
+  uint8_t* TA = sm;          // a^T [64 features][128 atoms]
+  uint8_t* TB = TA + kTile;  // b^T
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tslot;
+  __shared__ float csp[4][2][64];
+  const node::WJob& jb = jobs.j[blockIdx.x];
+  const int tid = static_cast<int>(threadIdx.x), warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) tc::mbar_init(&mbar, 1);
+  if (warp == 0) tc::tmem_alloc(&tslot, 64);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tslot, aA = tc::smem_u32(TA), aB = tc::smem_u32(TB);
+  uint32_t phase = 0;
+  bool first = true;
+  for (int pass = 0; pass < (jb.a2 ? 2 : 1); ++pass) {
+    const float* A = pass ? jb.a2 : jb.a;
+    const float* B = pass ? jb.b2 : jb.b;
+    const bool sl = !pass && jb.silu_a;
+    for (int i0 = 0; i0 < rows; i0 += TE) {
+      // thread -> (feature quad c4, atom r): a warp writes 32 consecutive atoms
+      // of one feature row (conflict-free), 8 float4 per operand per thread
+#pragma unroll 2
+      for (int q = 0; q < 8; ++q) {
+        const int x = tid + 256 * q, c4 = x >> 7, r = x & 127;
+        const bool ok = i0 + r < rows;
+        float4 va = ok ? __ldg(reinterpret_cast<const float4*>(A + (size_t)(i0 + r) * 64) + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 vb = ok ? __ldg(reinterpret_cast<const float4*>(B + (size_t)(i0 + r) * 64) + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (sl && ok) va = make_float4(dev::silu(va.x), dev::silu(va.y), dev::silu(va.z), dev::silu(va.w));
+        *reinterpret_cast<float*>(TA + off_fm(4 * c4 + 0, r)) = va.x;
+        *reinterpret_cast<float*>(TA + off_fm(4 * c4 + 1, r)) = va.y;
+        *reinterpret_cast<float*>(TA + off_fm(4 * c4 + 2, r)) = va.z;
+        *reinterpret_cast<float*>(TA + off_fm(4 * c4 + 3, r)) = va.w;
+        *reinterpret_cast<float*>(TB + off_fm(4 * c4 + 0, r)) = vb.x;
+        *reinterpret_cast<float*>(TB + off_fm(4 * c4 + 1, r)) = vb.y;
+        *reinterpret_cast<float*>(TB + off_fm(4 * c4 + 2, r)) = vb.z;
+        *reinterpret_cast<float*>(TB + off_fm(4 * c4 + 3, r)) = vb.w;
+      }
+      tc::fence_async_smem();
+      tc::fence_before();
+      __syncthreads();
+      tc::fence_after();
+      if (tid == 0) {
+        mma_tiles<64, 64, 128, 64>(tmem, aA, aB, !first);
+        tc::commit(&mbar);
+      }
+      tc::mbar_wait(&mbar, phase);  // the MMA has read TA / TB: they may be restaged
+      phase ^= 1u;
+      tc::fence_after();
+      first = false;
+    }
+  }
+  // M=64 accumulator: row r at lane (r/16)*32 + r%16; warp w reads lanes 32w..
+  if (first) {  // rows == 0
+    for (int x = tid; x < 64 * 64; x += 256) jb.G[x] = 0.f;
+  } else if (warp < 4) {
+#pragma unroll
+    for (int cb = 0; cb < 4; ++cb) {
+      float v[16];
+      tc::ld16(tmem + (static_cast<uint32_t>(32 * warp) << 16) + static_cast<uint32_t>(16 * cb), v);
+      if (lane < 16) {
+        float4* o = reinterpret_cast<float4*>(jb.G + (16 * warp + lane) * 64 + 16 * cb);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) o[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+      }
+    }
+  }
+  // column sums of x1 / x2: 4 row quarters per column, combined in a fixed order
+  if (jb.x1 || jb.x2) {
+    const int qr = tid >> 6, c = tid & 63;
+    const int r0 = (rows * qr) >> 2, r1 = (rows * (qr + 1)) >> 2;
+    for (int w = 0; w < 2; ++w) {
+      const float* X = w ? jb.x2 : jb.x1;
+      float s = 0.f;
+      if (X) {
+        int i = r0;
+        for (; i + 8 <= r1; i += 8) {
+          float v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = __ldg(X + (size_t)(i + u) * 64 + c);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) s += v[u];
+        }
+        for (; i < r1; ++i) s += __ldg(X + (size_t)i * 64 + c);
+      }
+      csp[qr][w][c] = s;
+    }
+    __syncthreads();
+    if (tid < 128) {
+      const int w = tid >> 6, c = tid & 63;
+      float* out = w ? jb.cs2 : jb.cs1;
+      if ((w ? jb.x2 : jb.x1) && out) out[c] = (csp[0][w][c] + csp[1][w][c]) + (csp[2][w][c] + csp[3][w][c]);
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_free(tmem, 64);
+}
+
+}  // namespace edge_tc
+}  // namespace janus
