@@ -400,7 +400,9 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
     st->lanes.resize(static_cast<size_t>(std::max(1, d.n_lanes)));
     // measured on the C2 bench (16 lanes): 128-edge tiles 1/1 -> 4735, 4/8 -> 5765;
     // multi-chunk tiles (~2 chunks) 2/4 -> 6363, 2/3 -> 6467 structures/s
-    st->tpc_fe = std::max(1, std::min(2, d.n_lanes / 8));
+    // FE / FF run two CTAs per SM: one tile per CTA once every micro-batch has
+    // its own lane (32 lanes: 1 -> 7760 vs 2 -> 7648; 16 lanes: 2 -> 7089 vs 1 -> 7066)
+    st->tpc_fe = d.n_lanes >= 32 ? 1 : std::max(1, std::min(2, d.n_lanes / 8));
     st->tpc_wg = std::max(1, std::min(3, d.n_lanes / 5));
     // tensor-core tiles: runs of <= 8 rows with <= tc_tile_edges edges, cut into
     // 128-edge chunks (rows may straddle chunk boundaries: the segmented sums
