@@ -151,7 +151,11 @@ __device__ __forceinline__ void stage_weight(uint8_t* dst, const float* __restri
 // the fused row epilogue)]; rebuilt after every optimizer step (stage.cu
 // refresh_transposes) and pulled by each CTA with TMA bulk copies.
 constexpr uint32_t kWtOff = 3 * kWTile + 2 * 64 * 4;
-constexpr uint32_t kPackBytes = kWtOff + kWTile;
+// + B as a bf16 K-major SWIZZLE_128B tile (n = out, k = in; 8 KB): the B operand
+// of BF / BE's sbar = mu B^T MMAs, which feed only the parameter gradients
+constexpr uint32_t kW2bOff = kWtOff + kWTile;
+constexpr uint32_t kW2bBytes = 64 * 64 * 2;
+constexpr uint32_t kPackBytes = kW2bOff + kW2bBytes;
 
 __global__ void pack_msg_weights(const float* __restrict__ A, const float* __restrict__ alpha, const float* __restrict__ B,
                                  const float* __restrict__ beta, const float* __restrict__ W, float* __restrict__ pack) {
@@ -163,6 +167,7 @@ __global__ void pack_msg_weights(const float* __restrict__ A, const float* __res
     *reinterpret_cast<float*>(dst + kWTile + tc::sw128_off(b, a, 64)) = B[x];      // B^T: (n=out=b, k=in=a)
     *reinterpret_cast<float*>(dst + 2 * kWTile + tc::sw128_off(a, b, 64)) = B[x];  // B:   (n=a, k=b)
     pack[kWtOff / 4 + b * 64 + a] = W[x];                                           // W^T[b][a] = W[a][b]
+    *reinterpret_cast<__nv_bfloat16*>(dst + kW2bOff + tc::sw128_off_b16(a, b, 64)) = __float2bfloat16_rn(B[x]);  // B bf16: (n=a, k=b)
   }
   if (x < 64) {
     pack[3 * kWTile / 4 + x] = alpha[x];
@@ -175,17 +180,18 @@ __global__ void pack_msg_weights(const float* __restrict__ A, const float* __res
 // wait on `wbar` (tc::mbar_wait(wbar, 0)) — done just before the first MMA so
 // the copy overlaps the TMEM allocation and the first chunk's basis.
 __device__ __forceinline__ void load_weights(uint8_t* sm, const float* pack, int ntiles, float* al, float* be, float* wts,
-                                             uint64_t* wbar) {
+                                             uint64_t* wbar, uint8_t* w2b = nullptr) {
   if (threadIdx.x == 0) {
     tc::mbar_init(wbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     const uint32_t wbytes = static_cast<uint32_t>(ntiles) * kWTile;
     const uint8_t* src = reinterpret_cast<const uint8_t*>(pack);
-    tc::mbar_expect_tx(wbar, wbytes + 512 + (wts ? kWTile : 0u));
+    tc::mbar_expect_tx(wbar, wbytes + 512 + (wts ? kWTile : 0u) + (w2b ? kW2bBytes : 0u));
     tc::bulk_g2s(sm, pack, wbytes, wbar);
     tc::bulk_g2s(al, src + 3 * kWTile, 256, wbar);
     tc::bulk_g2s(be, src + 3 * kWTile + 256, 256, wbar);
     if (wts) tc::bulk_g2s(wts, src + kWtOff, kWTile, wbar);
+    if (w2b) tc::bulk_g2s(w2b, src + kW2bOff, kW2bBytes, wbar);
   }
   __syncthreads();
 }
@@ -640,6 +646,31 @@ __device__ __forceinline__ void mma_wg_b16(uint32_t d, uint32_t a, uint32_t b, b
     tc::mma_bf16(d, da0 + o, db0 + o, id, (s > 0 || accumulate) ? 1u : 0u);
   }
 }
+// D[128 edges][64] = A[128][64] . B[64][64]^T on bf16 K-major SWIZZLE_128B
+// tiles (one 128 B row per edge / output; K-step of 16 = +32 B in the row).
+__device__ __forceinline__ void mma_kb16(uint32_t d, uint32_t a, uint32_t b) {
+  constexpr uint32_t id = tc::idesc_bf16(128, 64, false, false);
+  const uint64_t da0 = tc::smem_desc(a, 16, 1024, 2), db0 = tc::smem_desc(b, 16, 1024, 2);
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    const uint64_t o = static_cast<uint64_t>((32 * s) >> 4);
+    tc::mma_bf16(d, da0 + o, db0 + o, id, s > 0 ? 1u : 0u);
+  }
+}
+// Column sums of an edge-major bf16 tile (same mapping as em_colsum_add; the
+// four features of a warp share a 16 B chunk, so the loads broadcast).
+__device__ __forceinline__ void b16_colsum_add(const uint8_t* t, float* acc) {
+  if (threadIdx.x < 512) {
+    const int f = static_cast<int>(threadIdx.x) >> 3, p = static_cast<int>(threadIdx.x) & 7;
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < TE / 8; ++k) s += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(t + off_b16(p + 8 * k, f)));
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s += __shfl_xor_sync(0xffffffffu, s, 4);
+    if (p == 0) acc[f] += s;
+  }
+}
 // Column sums (over the chunk's edges) of an edge-major fp32 SWIZZLE_128B tile
 // [128 edges][64 features], added to acc[64] (shared memory): 8 threads per
 // feature take edges p, p+8, ... (conflict-free scalar loads), an xor
@@ -745,9 +776,9 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int4* __res
   TC_M();
   uint8_t* W0 = sm;           // A^T
   uint8_t* W1 = W0 + kWTile;  // B^T
-  uint8_t* W2 = W1 + kWTile;  // B
-  uint8_t* T0 = W2 + kWTile;
-  uint8_t* T1 = T0 + kTile;
+  uint8_t* W2b = W1 + kWTile; // B (bf16)
+  uint8_t* T0 = W2b + kWTile;
+  uint8_t* T1 = T0 + kTile;   // write_partial / row-epilogue scratch
   uint8_t* B0 = T1 + kTile;   // bf16: phi
   uint8_t* B1 = B0 + kBTile;  //       s
   uint8_t* B2 = B1 + kBTile;  //       gbar
@@ -763,13 +794,13 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int4* __res
   c.sm = sm;
   c.mbar = &mbar;
   __shared__ __align__(8) uint64_t wbar;
-  load_weights(sm, p.pack, 3, al, be, nullptr, &wbar);
+  load_weights(sm, p.pack, 2, al, be, nullptr, &wbar, W2b);
   if (threadIdx.x < 128) csa[threadIdx.x] = 0.f;  // csa, csb (published by setup's barrier)
   TC_M();
   setup(c, &tslot, 512);
   TC_M();
-  const uint32_t aW0 = tc::smem_u32(W0), aW1 = tc::smem_u32(W1), aW2 = tc::smem_u32(W2);
-  const uint32_t aT0 = tc::smem_u32(T0), aT1 = tc::smem_u32(T1);
+  const uint32_t aW0 = tc::smem_u32(W0), aW1 = tc::smem_u32(W1), aW2b = tc::smem_u32(W2b);
+  const uint32_t aT0 = tc::smem_u32(T0);
   const uint32_t aB0 = tc::smem_u32(B0), aB1 = tc::smem_u32(B1), aB2 = tc::smem_u32(B2), aB3 = tc::smem_u32(B3);
   bool first = true;
   const int f0 = FPT * c.q;
@@ -831,15 +862,14 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int4* __res
           TC_M();
           st_pl(T0, c.e, f0, gg);
         }
-        st_em(T1, c.e, f0, gb);   // gbar (A of sbar = gbar B^T; its column sums)
-        st_b16(B2, c.e, f0, gb);  // gbar (B of dB)
+        st_b16(B2, c.e, f0, gb);  // gbar: B of dB, A of sbar = gbar B^T (bf16: feeds dA only)
       }
       TC_M();
       c.publish();
       TC_M();
       if (threadIdx.x == 0) {
-        mma_wg_b16(c.tmem + TM_BG, aB1, aB2, !first);                // dB += s^T gbar
-        mma_tiles<128, 64, 64, 128>(c.tmem + TM_G, aT1, aW2, false);  // sbar
+        mma_wg_b16(c.tmem + TM_BG, aB1, aB2, !first);  // dB += s^T gbar
+        mma_kb16(c.tmem + TM_G, aB2, aW2b);            // sbar
         tc::commit(c.mbar);
       }
       TC_M();
@@ -847,7 +877,7 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int4* __res
         const uint8_t* const tl[1] = {T0};
         seg_rows<1>(g, tr.r0, c0, ne, tl, sg, acc);
       }
-      em_colsum_add(T1, csb);  // dbeta += sum_e gbar_e
+      b16_colsum_add(B2, csb);  // dbeta += sum_e gbar_e
       TC_M();
       c.wait_mma();
       __syncthreads();  // T0 / T1 reads done before T0 is rewritten
@@ -914,8 +944,8 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int4* __res
   TC_M();
   uint8_t* W0 = sm;
   uint8_t* W1 = W0 + kWTile;
-  uint8_t* W2 = W1 + kWTile;
-  uint8_t* T0 = W2 + kWTile;
+  uint8_t* W2b = W1 + kWTile;  // B (bf16)
+  uint8_t* T0 = W2b + kWTile;
   uint8_t* T1 = T0 + kTile;
   uint8_t* B0 = T1 + kTile;   // bf16: s
   uint8_t* B1 = B0 + kBTile;  //       sdot
@@ -934,12 +964,12 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int4* __res
   c.sm = sm;
   c.mbar = &mbar;
   __shared__ __align__(8) uint64_t wbar;
-  load_weights(sm, p.pack, 3, al, be, nullptr, &wbar);
+  load_weights(sm, p.pack, 2, al, be, nullptr, &wbar, W2b);
   if (threadIdx.x < 128) csa[threadIdx.x] = 0.f;  // csa, csb (published by setup's barrier)
   TC_M();
   setup(c, &tslot, 512);
   TC_M();
-  const uint32_t aW0 = tc::smem_u32(W0), aW1 = tc::smem_u32(W1), aW2 = tc::smem_u32(W2);
+  const uint32_t aW0 = tc::smem_u32(W0), aW1 = tc::smem_u32(W1), aW2b = tc::smem_u32(W2b);
   const uint32_t aT0 = tc::smem_u32(T0), aT1 = tc::smem_u32(T1);
   const uint32_t aB0 = tc::smem_u32(B0), aB1 = tc::smem_u32(B1), aB2 = tc::smem_u32(B2), aB3 = tc::smem_u32(B3);
   const uint32_t aB4 = tc::smem_u32(B4), aB5 = tc::smem_u32(B5);
@@ -1004,8 +1034,8 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int4* __res
       TC_M();
       c.wait_mma();
       TC_M();
-      float mu[FPT], nu[FPT];
       {
+        float mu[FPT], nu[FPT];
         float gg[FPT], gp[FPT];
         float pm[FPT], px[FPT];
         float4 a4[FPT / 4], aj4[FPT / 4], v4[FPT / 4], d4[FPT / 4];
@@ -1042,28 +1072,22 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int4* __res
       }
       TC_M();
       c.publish();
-      if (threadIdx.x == 0) {  // dB += s^T mu + sdot^T nu, under the row sums (committed with sbar)
+      if (threadIdx.x == 0) {  // dB += s^T mu + sdot^T nu; sbar = mu B^T, sdotbar = nu B^T (bf16: feed dA only)
         mma_wg_b16(c.tmem + TM_BG, aB0, aB2, !first);
         mma_wg_b16(c.tmem + TM_BG, aB1, aB3, true);
+        mma_kb16(c.tmem + TM_G, aB2, aW2b);
+        mma_kb16(c.tmem + TM_GP, aB3, aW2b);
+        tc::commit(c.mbar);
       }
       TC_M();
-      {
+      {  // row sums and dbeta under the MMAs
         const uint8_t* const tl[2] = {T0, T1};
         seg_rows<2>(g, tr.r0, c0, ne, tl, sg, acc);
       }
+      b16_colsum_add(B2, csb);  // dbeta += sum_e mu_e
       TC_M();
-      __syncthreads();         // row sums done with T0/T1
-      st_em(T0, c.e, f0, mu);  // mu (A of sbar = mu B^T; its column sums)
-      st_em(T1, c.e, f0, nu);  // nu
-      c.publish();
-      if (threadIdx.x == 0) {
-        mma_tiles<128, 64, 64, 128>(c.tmem + TM_G, aT0, aW2, false);   // sbar
-        mma_tiles<128, 64, 64, 128>(c.tmem + TM_GP, aT1, aW2, false);  // sdotbar
-        tc::commit(c.mbar);  // completes with every earlier MMA of this thread (dB too)
-      }
-      em_colsum_add(T0, csb);  // dbeta += sum_e mu_e (beside the MMAs)
-      TC_M();
-      c.wait_mma();  // dB and sbar done: B2/B3 and T1 are free
+      c.wait_mma();  // dB and sbar done
+      __syncthreads();  // row sums and column sums done: T1, B2, B3 may be rewritten
       TC_M();
       {
         float z[FPT], zp[FPT], sb[FPT], sdb[FPT];
@@ -1118,7 +1142,7 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int4* __res
 constexpr size_t kSmallBytes = sizeof(float) * (128 + NQ * TE) + 1024;  // alpha, beta, FF force scalars, 1 KB alignment slack
 constexpr size_t fe_smem() { return 2 * kWTile + 2 * kTile + kSmallBytes; }
 constexpr size_t ff_smem() { return 2 * kWTile + 2 * kTile + kSmallBytes; }
-constexpr size_t be_smem() { return 3 * kWTile + 2 * kTile + 4 * kBTile + kSmallBytes; }
+constexpr size_t be_smem() { return 3 * kWTile + 2 * kTile + 4 * kBTile + kSmallBytes; }  // W0, W1, W2b (8 of 16 KB)
 constexpr size_t bf_smem() { return 3 * kWTile + 2 * kTile + 6 * kBTile + kSmallBytes; }
 
 }  // namespace edge_tc
