@@ -155,7 +155,11 @@ constexpr uint32_t kWtOff = 3 * kWTile + 2 * 64 * 4;
 // of BF / BE's sbar = mu B^T MMAs, which feed only the parameter gradients
 constexpr uint32_t kW2bOff = kWtOff + kWTile;
 constexpr uint32_t kW2bBytes = 64 * 64 * 2;
-constexpr uint32_t kPackBytes = kW2bOff + kW2bBytes;
+// + A^T and B^T as bf16 K-major tiles (8 KB each): BF and BE compute only
+// parameter gradients, so all their per-edge contractions run on bf16
+constexpr uint32_t kW0bOff = kW2bOff + kW2bBytes;
+constexpr uint32_t kW1bOff = kW0bOff + kW2bBytes;
+constexpr uint32_t kPackBytes = kW1bOff + kW2bBytes;
 
 __global__ void pack_msg_weights(const float* __restrict__ A, const float* __restrict__ alpha, const float* __restrict__ B,
                                  const float* __restrict__ beta, const float* __restrict__ W, float* __restrict__ pack) {
@@ -168,11 +172,28 @@ __global__ void pack_msg_weights(const float* __restrict__ A, const float* __res
     *reinterpret_cast<float*>(dst + 2 * kWTile + tc::sw128_off(a, b, 64)) = B[x];  // B:   (n=a, k=b)
     pack[kWtOff / 4 + b * 64 + a] = W[x];                                           // W^T[b][a] = W[a][b]
     *reinterpret_cast<__nv_bfloat16*>(dst + kW2bOff + tc::sw128_off_b16(a, b, 64)) = __float2bfloat16_rn(B[x]);  // B bf16: (n=a, k=b)
+    *reinterpret_cast<__nv_bfloat16*>(dst + kW0bOff + tc::sw128_off_b16(b, a, 64)) = __float2bfloat16_rn(A[x]);  // A^T bf16
+    *reinterpret_cast<__nv_bfloat16*>(dst + kW1bOff + tc::sw128_off_b16(b, a, 64)) = __float2bfloat16_rn(B[x]);  // B^T bf16
   }
   if (x < 64) {
     pack[3 * kWTile / 4 + x] = alpha[x];
     pack[3 * kWTile / 4 + 64 + x] = beta[x];
   }
+}
+
+// BF / BE: the three bf16 weight tiles [A^T | B^T | B] (contiguous in the
+// pack, 24 KB) + alpha, beta with one TMA bulk copy each.
+__device__ __forceinline__ void load_weights_b16(uint8_t* w0b, const float* pack, float* al, float* be, uint64_t* wbar) {
+  if (threadIdx.x == 0) {
+    tc::mbar_init(wbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(pack);
+    tc::mbar_expect_tx(wbar, 3 * kW2bBytes + 512);
+    tc::bulk_g2s(w0b, src + kW2bOff, 3 * kW2bBytes, wbar);  // order in the pack: B, A^T, B^T
+    tc::bulk_g2s(al, src + 3 * kWTile, 256, wbar);
+    tc::bulk_g2s(be, src + 3 * kWTile + 256, 256, wbar);
+  }
+  __syncthreads();
 }
 
 // Thread 0 arms `wbar` and bulk-loads `ntiles` weight tiles (+ alpha, beta,
@@ -774,10 +795,10 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int4* __res
   uint8_t* sm = align1024(sm_raw);
   TC_DECL;
   TC_M();
-  uint8_t* W0 = sm;           // A^T
-  uint8_t* W1 = W0 + kWTile;  // B^T
-  uint8_t* W2b = W1 + kWTile; // B (bf16)
-  uint8_t* T0 = W2b + kWTile;
+  uint8_t* W2b = sm;                // bf16 weights in pack order: B | A^T | B^T
+  uint8_t* W0b = W2b + kW2bBytes;
+  uint8_t* W1b = W0b + kW2bBytes;
+  uint8_t* T0 = sm + 2 * kWTile;    // 1024 B aligned after the 24 KB of weights
   uint8_t* T1 = T0 + kTile;   // write_partial / row-epilogue scratch
   uint8_t* B0 = T1 + kTile;   // bf16: phi
   uint8_t* B1 = B0 + kBTile;  //       s
@@ -794,13 +815,12 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int4* __res
   c.sm = sm;
   c.mbar = &mbar;
   __shared__ __align__(8) uint64_t wbar;
-  load_weights(sm, p.pack, 2, al, be, nullptr, &wbar, W2b);
+  load_weights_b16(W2b, p.pack, al, be, &wbar);
   if (threadIdx.x < 128) csa[threadIdx.x] = 0.f;  // csa, csb (published by setup's barrier)
   TC_M();
   setup(c, &tslot, 512);
   TC_M();
-  const uint32_t aW0 = tc::smem_u32(W0), aW1 = tc::smem_u32(W1), aW2b = tc::smem_u32(W2b);
-  const uint32_t aT0 = tc::smem_u32(T0);
+  const uint32_t aW0b = tc::smem_u32(W0b), aW1b = tc::smem_u32(W1b), aW2b = tc::smem_u32(W2b);
   const uint32_t aB0 = tc::smem_u32(B0), aB1 = tc::smem_u32(B1), aB2 = tc::smem_u32(B2), aB3 = tc::smem_u32(B3);
   bool first = true;
   const int f0 = FPT * c.q;
@@ -814,13 +834,12 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int4* __res
       {
         float ph[FPT], dph[FPT];
         basis(es.d, rc, f0, ph, dph);
-        st_em(T0, c.e, f0, ph);
-        st_b16(B0, c.e, f0, ph);  // phi (A of dA)
+        st_b16(B0, c.e, f0, ph);  // phi (A of z = phi A and of dA)
       }
       tc::mbar_wait(&wbar, 0);  // weights landed (immediate after the first chunk)
       c.publish();
       if (threadIdx.x == 0) {
-        mma_tiles<128, 64, 64, 128>(c.tmem + TM_Z, aT0, aW0, false);
+        mma_kb16(c.tmem + TM_Z, aB0, aW0b);
         tc::commit(c.mbar);
       }
       TC_M();
@@ -834,12 +853,11 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int4* __res
           const float zz = z[j] + al[f0 + j];
           z[j] = zz * fsig(zz);
         }
-        st_em(T0, c.e, f0, z);   // s, edge-major (A of g = s B)
-        st_b16(B1, c.e, f0, z);  // s (A of dB = s^T gbar)
+        st_b16(B1, c.e, f0, z);  // s (A of g = s B and of dB = s^T gbar)
       }
       c.publish();
       if (threadIdx.x == 0) {
-        mma_tiles<128, 64, 64, 128>(c.tmem + TM_G, aT0, aW1, false);
+        mma_kb16(c.tmem + TM_G, aB1, aW1b);
         tc::commit(c.mbar);
       }
       TC_M();
@@ -890,15 +908,14 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int4* __res
           const float zz = z[j] + al[f0 + j], s1 = fsig(zz);
           z[j] = sb[j] * (s1 * (1.0f + zz * (1.0f - s1)));
         }
-        st_b16(B3, c.e, f0, z);  // zbar (B of dA)
-        st_em(T0, c.e, f0, z);   // zbar (column sums)
+        st_b16(B3, c.e, f0, z);  // zbar (B of dA; its column sums)
       }
       c.publish();
       if (threadIdx.x == 0) {
         mma_wg_b16(c.tmem + TM_AG, aB0, aB3, !first);  // dA += phi^T zbar
         tc::commit(c.mbar);
       }
-      em_colsum_add(T0, csa);  // dalpha += sum_e zbar_e (beside the dA MMA)
+      b16_colsum_add(B3, csa);  // dalpha += sum_e zbar_e (beside the dA MMA)
       TC_M();
       c.wait_mma();
       TC_M();
@@ -942,10 +959,10 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int4* __res
   TC_DECL;
   TC_SPAN_BEGIN;
   TC_M();
-  uint8_t* W0 = sm;
-  uint8_t* W1 = W0 + kWTile;
-  uint8_t* W2b = W1 + kWTile;  // B (bf16)
-  uint8_t* T0 = W2b + kWTile;
+  uint8_t* W2b = sm;                // bf16 weights in pack order: B | A^T | B^T
+  uint8_t* W0b = W2b + kW2bBytes;
+  uint8_t* W1b = W0b + kW2bBytes;
+  uint8_t* T0 = sm + 2 * kWTile;    // 1024 B aligned after the 24 KB of weights
   uint8_t* T1 = T0 + kTile;
   uint8_t* B0 = T1 + kTile;   // bf16: s
   uint8_t* B1 = B0 + kBTile;  //       sdot
@@ -964,13 +981,12 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int4* __res
   c.sm = sm;
   c.mbar = &mbar;
   __shared__ __align__(8) uint64_t wbar;
-  load_weights(sm, p.pack, 2, al, be, nullptr, &wbar, W2b);
+  load_weights_b16(W2b, p.pack, al, be, &wbar);
   if (threadIdx.x < 128) csa[threadIdx.x] = 0.f;  // csa, csb (published by setup's barrier)
   TC_M();
   setup(c, &tslot, 512);
   TC_M();
-  const uint32_t aW0 = tc::smem_u32(W0), aW1 = tc::smem_u32(W1), aW2b = tc::smem_u32(W2b);
-  const uint32_t aT0 = tc::smem_u32(T0), aT1 = tc::smem_u32(T1);
+  const uint32_t aW0b = tc::smem_u32(W0b), aW1b = tc::smem_u32(W1b), aW2b = tc::smem_u32(W2b);
   const uint32_t aB0 = tc::smem_u32(B0), aB1 = tc::smem_u32(B1), aB2 = tc::smem_u32(B2), aB3 = tc::smem_u32(B3);
   const uint32_t aB4 = tc::smem_u32(B4), aB5 = tc::smem_u32(B5);
   bool first = true;
@@ -993,18 +1009,16 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int4* __res
         float ph[FPT], dph[FPT];
         basis(es.d, rc, f0, ph, dph);
         TC_M();
-        st_em(T0, c.e, f0, ph);
-        st_em(T1, c.e, f0, dph);
-        st_b16(B4, c.e, f0, ph);   // phi  (A of dA)
-        st_b16(B5, c.e, f0, dph);  // phi' (A of dA)
+        st_b16(B4, c.e, f0, ph);   // phi  (A of z = phi A and of dA)
+        st_b16(B5, c.e, f0, dph);  // phi' (A of z' = phi' A and of dA)
       }
       TC_M();
       tc::mbar_wait(&wbar, 0);
       TC_M();  // weights landed (immediate after the first chunk)
       c.publish();
       if (threadIdx.x == 0) {
-        mma_tiles<128, 64, 64, 128>(c.tmem + TM_Z, aT0, aW0, false);
-        mma_tiles<128, 64, 64, 128>(c.tmem + TM_ZP, aT1, aW0, false);
+        mma_kb16(c.tmem + TM_Z, aB4, aW0b);
+        mma_kb16(c.tmem + TM_ZP, aB5, aW0b);
         tc::commit(c.mbar);
       }
       TC_M();
@@ -1020,15 +1034,13 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int4* __res
           z[j] = zz * s1;
           zp[j] = s1 * (1.0f + zz * (1.0f - s1)) * zp[j];
         }
-        st_em(T0, c.e, f0, z);   // s
-        st_em(T1, c.e, f0, zp);  // sdot
-        st_b16(B0, c.e, f0, z);  // s    (A of dB)
-        st_b16(B1, c.e, f0, zp); // sdot (A of dB)
+        st_b16(B0, c.e, f0, z);  // s    (A of g = s B and of dB)
+        st_b16(B1, c.e, f0, zp); // sdot (A of g' = sdot B and of dB)
       }
       c.publish();
       if (threadIdx.x == 0) {
-        mma_tiles<128, 64, 64, 128>(c.tmem + TM_G, aT0, aW1, false);
-        mma_tiles<128, 64, 64, 128>(c.tmem + TM_GP, aT1, aW1, false);
+        mma_kb16(c.tmem + TM_G, aB0, aW1b);
+        mma_kb16(c.tmem + TM_GP, aB1, aW1b);
         tc::commit(c.mbar);
       }
       TC_M();
@@ -1101,9 +1113,8 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int4* __res
           z[j] = sb[j] * ds + sdb[j] * d2s * zp[j];  // zbar
           zp[j] = sdb[j] * ds;                       // zbar'
         }
-        st_b16(B2, c.e, f0, z);   // zbar  (B of dA)
+        st_b16(B2, c.e, f0, z);   // zbar  (B of dA; its column sums)
         st_b16(B3, c.e, f0, zp);  // zbar' (B of dA)
-        st_em(T1, c.e, f0, z);    // zbar (column sums; T0 is still being summed)
       }
       c.publish();
       if (threadIdx.x == 0) {  // dA += phi^T zbar + phi'^T zbar'
@@ -1111,7 +1122,7 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int4* __res
         mma_wg_b16(c.tmem + TM_AG, aB5, aB3, true);
         tc::commit(c.mbar);
       }
-      em_colsum_add(T1, csa);  // dalpha += sum_e zbar_e (beside the dA MMA)
+      b16_colsum_add(B2, csa);  // dalpha += sum_e zbar_e (beside the dA MMA)
       TC_M();
       c.wait_mma();
       TC_M();
@@ -1142,8 +1153,8 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int4* __res
 constexpr size_t kSmallBytes = sizeof(float) * (128 + NQ * TE) + 1024;  // alpha, beta, FF force scalars, 1 KB alignment slack
 constexpr size_t fe_smem() { return 2 * kWTile + 2 * kTile + kSmallBytes; }
 constexpr size_t ff_smem() { return 2 * kWTile + 2 * kTile + kSmallBytes; }
-constexpr size_t be_smem() { return 3 * kWTile + 2 * kTile + 4 * kBTile + kSmallBytes; }  // W0, W1, W2b (8 of 16 KB)
-constexpr size_t bf_smem() { return 3 * kWTile + 2 * kTile + 6 * kBTile + kSmallBytes; }
+constexpr size_t be_smem() { return 2 * kWTile + 2 * kTile + 4 * kBTile + kSmallBytes; }  // 24 KB bf16 weights in 32
+constexpr size_t bf_smem() { return 2 * kWTile + 2 * kTile + 6 * kBTile + kSmallBytes; }
 
 }  // namespace edge_tc
 }  // namespace janus
