@@ -29,7 +29,8 @@ FLOP_PER_EDGE = 2.0 * ((64 * 64 + 64 * 64) + (2 * 64 * 64 + 2 * 64 * 64 + 64) + 
                        (2 * 64 * 64 + 3 * 64 * 64))  # FE + FF + BF + BE per layer (stage.cu edge_kernel_flops_per_edge)
 
 
-def measure(name, model, params, batches, lanes=16, steps=10, warmup=3):
+def measure(name, model, params, batches, lanes=None, steps=10, warmup=3):
+    lanes = lanes or len(batches)  # one lane per micro-batch, as bench.py
     na = max(b.n_atoms for b in batches)
     t = J.Trainer(model, params, 1, J.METHOD_SYMFOLD, len(batches), max_atoms=na, max_edges=na * 140,
                   max_struct=max(b.n_struct for b in batches), graphs=True, lanes=lanes)
@@ -58,7 +59,7 @@ def main():
     model = J.Model(L=4, H=64, R=64, r_c=5.0, precision=J.PREC_TF32)
     params = model.synth_params(7)
     measure("C1: 64-atom cells, N_mb=4", model, params,
-            [J.synth_batch(model, [64], 0.095, 10 + i, device_nl=True) for i in range(4)], lanes=4)
+            [J.synth_batch(model, [64], 0.095, 10 + i, device_nl=True) for i in range(4)])
     measure("C2: 256-atom cells, N_mb=32", model, params,
             [J.synth_batch(model, [256], 0.095, 700 + i, device_nl=True) for i in range(32)])
     rng = np.random.default_rng(11)
@@ -67,7 +68,7 @@ def main():
     groups = [g for g, _ in J.gars_pack(sizes, 16, 1, seed=11)]
     measure("C4: 64 mixed 128..1024-atom cells, GARS -> N_mb=16", model, params, build_batches(model, cells, groups))
     measure("C5: 4096-atom cells rho=0.19, N_mb=8", model, params,
-            [J.synth_batch(model, [4096], 0.19, 4000 + i, device_nl=True) for i in range(8)], lanes=8)
+            [J.synth_batch(model, [4096], 0.19, 4000 + i, device_nl=True) for i in range(8)])
 
 
 if __name__ == "__main__":
