@@ -17,7 +17,9 @@ namespace edge_tc {
 
 constexpr size_t wgrad_tc_smem() { return 2 * kTile + 1024; }
 
-__global__ void __launch_bounds__(256, 1) wgrad_tc_kernel(int rows, node::WJobs jobs) {
+constexpr int kWgT = 512;  // threads: 4 float4 of a and of b per thread per 128-atom block
+
+__global__ void __launch_bounds__(kWgT, 1) wgrad_tc_kernel(int rows, node::WJobs jobs) {
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = align1024(sm_raw);
   uint8_t* TA = sm;          // a^T [64 features][128 atoms]
@@ -35,46 +37,59 @@ __global__ void __launch_bounds__(256, 1) wgrad_tc_kernel(int rows, node::WJobs 
   const uint32_t tmem = tslot, aA = tc::smem_u32(TA), aB = tc::smem_u32(TB);
   uint32_t phase = 0;
   bool first = true;
-  for (int pass = 0; pass < (jb.a2 ? 2 : 1); ++pass) {
+  // work items: (pass, 128-atom block); the next item's loads are in flight
+  // while the current block is staged and contracted
+  const int nblk = (rows + TE - 1) / TE, npass = jb.a2 ? 2 : 1, nit = nblk * npass;
+  float4 ra[4], rb[4];
+  auto fetch = [&](int it) {
+    const int pass = it / nblk, i0 = (it % nblk) * TE;
     const float* A = pass ? jb.a2 : jb.a;
     const float* B = pass ? jb.b2 : jb.b;
-    const bool sl = !pass && jb.silu_a;
-    for (int i0 = 0; i0 < rows; i0 += TE) {
-      // thread -> (feature quad c4, atom r): a warp writes 32 consecutive atoms
-      // of one feature row (conflict-free), 8 float4 per operand per thread
-#pragma unroll 2
-      for (int q = 0; q < 8; ++q) {
-        const int x = tid + 256 * q, c4 = x >> 7, r = x & 127;
-        const bool ok = i0 + r < rows;
-        float4 va = ok ? __ldg(reinterpret_cast<const float4*>(A + (size_t)(i0 + r) * 64) + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
-        const float4 vb = ok ? __ldg(reinterpret_cast<const float4*>(B + (size_t)(i0 + r) * 64) + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
-        if (sl && ok) va = make_float4(dev::silu(va.x), dev::silu(va.y), dev::silu(va.z), dev::silu(va.w));
-        *reinterpret_cast<float*>(TA + off_fm(4 * c4 + 0, r)) = va.x;
-        *reinterpret_cast<float*>(TA + off_fm(4 * c4 + 1, r)) = va.y;
-        *reinterpret_cast<float*>(TA + off_fm(4 * c4 + 2, r)) = va.z;
-        *reinterpret_cast<float*>(TA + off_fm(4 * c4 + 3, r)) = va.w;
-        *reinterpret_cast<float*>(TB + off_fm(4 * c4 + 0, r)) = vb.x;
-        *reinterpret_cast<float*>(TB + off_fm(4 * c4 + 1, r)) = vb.y;
-        *reinterpret_cast<float*>(TB + off_fm(4 * c4 + 2, r)) = vb.z;
-        *reinterpret_cast<float*>(TB + off_fm(4 * c4 + 3, r)) = vb.w;
-      }
-      tc::fence_async_smem();
-      tc::fence_before();
-      __syncthreads();
-      tc::fence_after();
-      if (tid == 0) {
-        mma_tiles<64, 64, 128, 64>(tmem, aA, aB, !first);
-        tc::commit(&mbar);
-      }
-      tc::mbar_wait(&mbar, phase);  // the MMA has read TA / TB: they may be restaged
-      phase ^= 1u;
-      tc::fence_after();
-      first = false;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int x = tid + kWgT * q, c4 = x >> 7, r = x & 127;
+      const bool ok = i0 + r < rows;
+      ra[q] = ok ? __ldg(reinterpret_cast<const float4*>(A + (size_t)(i0 + r) * 64) + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+      rb[q] = ok ? __ldg(reinterpret_cast<const float4*>(B + (size_t)(i0 + r) * 64) + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
+  };
+  if (nit > 0) fetch(0);
+  for (int it = 0; it < nit; ++it) {
+    const bool sl = it < nblk && jb.silu_a;
+    const int i0 = (it % nblk) * TE;
+    // thread -> (feature quad c4, atom r): a warp writes 32 consecutive atoms of one feature row
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int x = tid + kWgT * q, c4 = x >> 7, r = x & 127;
+      float4 va = ra[q];
+      const float4 vb = rb[q];
+      if (sl && i0 + r < rows) va = make_float4(dev::silu(va.x), dev::silu(va.y), dev::silu(va.z), dev::silu(va.w));
+      *reinterpret_cast<float*>(TA + off_fm(4 * c4 + 0, r)) = va.x;
+      *reinterpret_cast<float*>(TA + off_fm(4 * c4 + 1, r)) = va.y;
+      *reinterpret_cast<float*>(TA + off_fm(4 * c4 + 2, r)) = va.z;
+      *reinterpret_cast<float*>(TA + off_fm(4 * c4 + 3, r)) = va.w;
+      *reinterpret_cast<float*>(TB + off_fm(4 * c4 + 0, r)) = vb.x;
+      *reinterpret_cast<float*>(TB + off_fm(4 * c4 + 1, r)) = vb.y;
+      *reinterpret_cast<float*>(TB + off_fm(4 * c4 + 2, r)) = vb.z;
+      *reinterpret_cast<float*>(TB + off_fm(4 * c4 + 3, r)) = vb.w;
+    }
+    if (it + 1 < nit) fetch(it + 1);
+    tc::fence_async_smem();
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    if (tid == 0) {
+      mma_tiles<64, 64, 128, 64>(tmem, aA, aB, !first);
+      tc::commit(&mbar);
+    }
+    tc::mbar_wait(&mbar, phase);  // the MMA has read TA / TB: they may be restaged
+    phase ^= 1u;
+    tc::fence_after();
+    first = false;
   }
   // M=64 accumulator: row r at lane (r/16)*32 + r%16; warp w reads lanes 32w..
   if (first) {  // rows == 0
-    for (int x = tid; x < 64 * 64; x += 256) jb.G[x] = 0.f;
+    for (int x = tid; x < 64 * 64; x += kWgT) jb.G[x] = 0.f;
   } else if (warp < 4) {
 #pragma unroll
     for (int cb = 0; cb < 4; ++cb) {
@@ -89,9 +104,9 @@ __global__ void __launch_bounds__(256, 1) wgrad_tc_kernel(int rows, node::WJobs 
   }
   // column sums of x1 / x2: 4 row quarters per column, combined in a fixed order
   if (jb.x1 || jb.x2) {
-    const int qr = tid >> 6, c = tid & 63;
+    const int qr = (tid >> 6) & 3, c = tid & 63;
     const int r0 = (rows * qr) >> 2, r1 = (rows * (qr + 1)) >> 2;
-    for (int w = 0; w < 2; ++w) {
+    for (int w = 0; w < 2 && tid < 256; ++w) {
       const float* X = w ? jb.x2 : jb.x1;
       float s = 0.f;
       if (X) {
