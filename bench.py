@@ -279,17 +279,18 @@ def main():
         # its own inputs H2D and reads its own loss back D2H (wait()).
         n_e2e = max(5, args.steps)
 
-        def e2e_loop(bs):
+        def e2e_loop(bs, n=None):
+            n = n or n_e2e
             barrier()
             t0 = time.perf_counter()
             tr.load_many(bs)
             tr.step_async()
-            for _ in range(n_e2e - 1):
+            for _ in range(n - 1):
                 tr.load_many(bs)
                 tr.wait()
                 tr.step_async()
             tr.wait()
-            return (time.perf_counter() - t0) / n_e2e
+            return (time.perf_counter() - t0) / n
 
         # (1) host-built CSR uploaded with the batch (neighbour lists prebuilt
         # once, outside the timed region); (2) device LM: only positions,
@@ -297,6 +298,9 @@ def main():
         # micro-batch's neighbour list on the GPU (janus_trainer_load with
         # row_ptr == NULL, nbrlist.cu) — the headline e2e, since a training
         # loop over a dataset must build them per structure
+        # untimed: loads alternate between two geometry copies, so the step graph
+        # for each parity is captured and instantiated here, outside the timing
+        e2e_loop(batches, n=3)
         e2e_host_csr = e2e_loop(batches)
         dev_batches = [J.Batch(b.pos, b.species, b.struct_id, b.cell, b.E_target, b.F_target, nl="device")
                        for b in batches]

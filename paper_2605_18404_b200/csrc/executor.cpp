@@ -120,12 +120,23 @@ struct janus_trainer {
   bool pending = false;  // a step issued by trainer_step_async not yet waited for
   int64_t p2p_bytes = 0;
   int64_t kernel_count = -1;
-  cudaGraphExec_t gexec = nullptr;
+  cudaGraphExec_t gexec = nullptr;               // instantiated step graph for key gkey (geometry parities)
+  std::vector<int> gkey;
+  cudaGraphExec_t gexec_alt = nullptr;           // the other cached graph (loads alternate the parities)
+  std::vector<int> gkey_alt;
+  int64_t kernel_count_alt = -1;
   janus_step_stats last{};
   std::vector<int> n_atoms;                      // per mb (for port sizes on the receive side)
-  std::vector<std::array<int, 5>> shape;         // per mb: atoms, edges, structs, tiles, TC tiles (graph validity)
+  std::vector<std::array<int, 5>> shape;         // per (parity, mb): atoms, edges, structs, tiles, TC tiles (graph validity)
+  // double-buffered geometry: a load fills the copy the step in flight does not
+  // read, on the load stream, so uploads / neighbour lists / geometry overlap it
+  std::vector<int> step_par;                     // per mb: copy the last issued step read (-1: none)
+  std::vector<int> load_par;                     // per mb: copy filled by a load not yet used by a step (-1: none)
+  cudaStream_t load_stream = nullptr;
+  cudaEvent_t load_done = nullptr;               // end of the latest loads on load_stream
+  cudaEvent_t step_end[2] = {nullptr, nullptr};  // end of steps with even / odd index
+  int64_t nsteps = 0;
   janus::LmBuilder* lm = nullptr;                // device neighbour lists (loads without a CSR)
-  cudaStream_t lm_stream = nullptr;              // their builds run here, beside a step in flight
   int lm_par = 0;                                 // CSR buffer of the next device LM build
 };
 
@@ -638,6 +649,11 @@ void trainer_destroy(janus_trainer* t) {
   cudaSetDevice(t->sd.device);
   cudaDeviceSynchronize();
   if (t->gexec) cudaGraphExecDestroy(t->gexec);
+  if (t->gexec_alt) cudaGraphExecDestroy(t->gexec_alt);
+  if (t->load_stream) cudaStreamDestroy(t->load_stream);
+  if (t->load_done) cudaEventDestroy(t->load_done);
+  for (cudaEvent_t e : t->step_end)
+    if (e) cudaEventDestroy(e);
   for (janus_stage* s : t->owned) stage_destroy(s);
   for (void* p : t->allocs) cudaFree(p);
   for (cudaEvent_t e : t->pool) cudaEventDestroy(e);
@@ -651,14 +667,13 @@ void trainer_destroy(janus_trainer* t) {
     cudaStreamDestroy(d.recv);
   }
   delete t->lm;
-  if (t->lm_stream) cudaStreamDestroy(t->lm_stream);
   if (t->root) cudaStreamDestroy(t->root);
   if (t->anchor) cudaEventDestroy(t->anchor);
   if (t->finish) cudaEventDestroy(t->finish);
   delete t;
 }
 
-void trainer_note_shape(janus_trainer* t, int mb, const janus_host_batch& hb);
+void trainer_note_shape(janus_trainer* t, int mb, const janus_host_batch& hb, int par);
 void trainer_load_many(janus_trainer* t, int n, const int* mbs, const janus_host_batch* hbs);
 
 void trainer_load(janus_trainer* t, int mb, const janus_host_batch& hb) { trainer_load_many(t, 1, &mb, &hb); }
@@ -666,8 +681,32 @@ void trainer_load(janus_trainer* t, int mb, const janus_host_batch& hb) { traine
 void trainer_load_many(janus_trainer* t, int n, const int* mbs, const janus_host_batch* hbs) {
   for (int k = 0; k < n; ++k)
     if (mbs[k] < 0 || mbs[k] >= t->ed.n_micro_batches) throw domain_error("micro-batch index out of range");
-  // asynchronous on the root stream: queued behind a step in flight and ahead
-  // of the next step.  The caller's arrays must stay valid until the copies
+  const size_t NMB = static_cast<size_t>(t->ed.n_micro_batches);
+  if (t->step_par.size() != NMB) {
+    t->step_par.assign(NMB, -1);
+    t->load_par.assign(NMB, -1);
+  }
+  if (!t->load_stream) {
+    // highest priority: the neighbour-list build and geometry take SMs ahead of
+    // the step in flight, so the host's one sync for the tile tables stays short
+    int lo = 0, hi = 0;
+    JANUS_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    JANUS_CUDA(cudaStreamCreateWithPriority(&t->load_stream, cudaStreamNonBlocking, hi));
+    JANUS_CUDA(cudaEventCreateWithFlags(&t->load_done, cudaEventDisableTiming));
+    for (cudaEvent_t& e : t->step_end) JANUS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  // Loads fill the geometry copy the latest step did NOT read.  Its last reader
+  // is at most the step before that one, which must be done first (steps
+  // complete in order on root).
+  if (t->nsteps >= 2) JANUS_CUDA(cudaStreamWaitEvent(t->load_stream, t->step_end[(t->nsteps - 2) & 1], 0));
+  auto par_of = [&](int mb) {
+    const int sp = t->step_par[static_cast<size_t>(mb)];
+    return sp < 0 ? 0 : sp ^ 1;
+  };
+  cudaStream_t ls = t->load_stream;
+  // asynchronous on the load stream, into the geometry copies the step in
+  // flight does not read (the next step_async switches to them and makes root
+  // wait for the loads).  The caller's arrays must stay valid until the copies
   // run (pinned memory) or are staged by the driver (pageable memory); the
   // host-built tile tables go through the stage's double-buffered pinned staging
   std::vector<janus_host_batch> dev;
@@ -675,35 +714,32 @@ void trainer_load_many(janus_trainer* t, int n, const int* mbs, const janus_host
   std::vector<std::vector<node::GeoJob>> jobs(t->owned.size());  // per stage: one batched geometry launch
   for (int k = 0; k < n; ++k) {
     if (hbs[k].row_ptr) {
+      const int q = par_of(mbs[k]);
       for (size_t x = 0; x < t->owned.size(); ++x)
-        stage_load(t->owned[x], mbs[k], hbs[k], t->root, /*sync=*/false, nullptr, &jobs[x]);
-      trainer_note_shape(t, mbs[k], hbs[k]);
+        stage_load(t->owned[x], mbs[k], hbs[k], ls, /*sync=*/false, nullptr, &jobs[x], q);
+      t->load_par[static_cast<size_t>(mbs[k])] = q;
+      trainer_note_shape(t, mbs[k], hbs[k], q);
     } else {
       dev.push_back(hbs[k]);
       dev_mb.push_back(mbs[k]);
     }
   }
   if (dev.empty()) {
-    for (size_t x = 0; x < t->owned.size(); ++x) stage_geometry_flush(t->owned[x], jobs[x], t->root);
+    for (size_t x = 0; x < t->owned.size(); ++x) stage_geometry_flush(t->owned[x], jobs[x], ls);
+    JANUS_CUDA(cudaEventRecord(t->load_done, ls));
     return;
   }
   // LM with the neighbour lists built on the device: ONE cell-list build over
-  // all these micro-batches (their structures side by side) on a side stream,
-  // while a step may still run on root; each stage copies its batch's slice
-  // on root (queued behind that step).  Builds alternate between two buffers
-  // and the build after next into a buffer waits for those copies on the device.
+  // all these micro-batches (their structures side by side) on the load
+  // stream, beside a step in flight; each stage then cuts its batch's slice
+  // into the free geometry copy on the same stream.
   if (!t->lm) {
     const int nm = t->ed.n_micro_batches;
     t->lm = new LmBuilder(nm * t->sd.max_atoms, nm * t->sd.max_struct, nm * t->sd.max_edges, t->sd.device, 2);
-    // highest priority: the build's CTAs take SMs ahead of the step in flight,
-    // so the host's one sync for the tile tables stays short
-    int lo = 0, hi = 0;
-    JANUS_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    JANUS_CUDA(cudaStreamCreateWithPriority(&t->lm_stream, cudaStreamNonBlocking, hi));
   }
   const int b = t->lm_par;
   t->lm_par ^= 1;
-  t->lm->build(dev.data(), static_cast<int>(dev.size()), static_cast<double>(t->sd.model.r_c), b, t->lm_stream);
+  t->lm->build(dev.data(), static_cast<int>(dev.size()), static_cast<double>(t->sd.model.r_c), b, ls);
   const int* hrow = t->lm->host_row_ptr();
   std::vector<int> rp;
   for (size_t k = 0; k < dev.size(); ++k) {
@@ -715,34 +751,44 @@ void trainer_load_many(janus_trainer* t, int n, const int* mbs, const janus_host
     hb2.n_edges = rp[static_cast<size_t>(N)];
     hb2.col = hb2.shift = hb2.rev = nullptr;
     const DevCsrSlice sl{&t->lm->buf(b), a0, hrow[a0]};
+    const int q = par_of(dev_mb[k]);
     for (size_t x = 0; x < t->owned.size(); ++x)
-      stage_load(t->owned[x], dev_mb[k], hb2, t->root, /*sync=*/false, &sl, &jobs[x]);
-    trainer_note_shape(t, dev_mb[k], hb2);
+      stage_load(t->owned[x], dev_mb[k], hb2, ls, /*sync=*/false, &sl, &jobs[x], q);
+    t->load_par[static_cast<size_t>(dev_mb[k])] = q;
+    trainer_note_shape(t, dev_mb[k], hb2, q);
   }
-  for (size_t x = 0; x < t->owned.size(); ++x) stage_geometry_flush(t->owned[x], jobs[x], t->root);
-  t->lm->release(b, t->root);
+  for (size_t x = 0; x < t->owned.size(); ++x) stage_geometry_flush(t->owned[x], jobs[x], ls);
+  t->lm->release(b, ls);
+  JANUS_CUDA(cudaEventRecord(t->load_done, ls));
 }
 
-void trainer_note_shape(janus_trainer* t, int mb, const janus_host_batch& hb) {
+void trainer_note_shape(janus_trainer* t, int mb, const janus_host_batch& hb, int par) {
   t->n_atoms[static_cast<size_t>(mb)] = hb.n_atoms;
   // a captured step graph bakes in grid sizes and copy lengths: a batch of a
-  // different shape in this slot forces a re-capture at the next step
-  if (t->shape.size() != t->n_atoms.size()) t->shape.assign(t->n_atoms.size(), {-1, -1, -1, -1, -1});
-  const DevGeo& g = t->owned.front()->geo[static_cast<size_t>(mb)];
+  // different shape in this geometry copy drops the cached graphs
+  const size_t NMB = t->n_atoms.size();
+  if (t->shape.size() != 2 * NMB) t->shape.assign(2 * NMB, {-1, -1, -1, -1, -1});
+  const DevGeo& g = stage_geo(t->owned.front(), mb, par);
   const std::array<int, 5> sh{hb.n_atoms, hb.n_edges, hb.n_struct, g.n_tiles, g.n_tiles_tc};
-  if (t->shape[static_cast<size_t>(mb)] != sh) {
-    t->shape[static_cast<size_t>(mb)] = sh;
-    if (t->gexec) {
+  std::array<int, 5>& cur = t->shape[static_cast<size_t>(par) * NMB + static_cast<size_t>(mb)];
+  if (cur != sh) {
+    cur = sh;
+    if (t->gexec || t->gexec_alt) {
       if (t->pending) JANUS_CUDA(cudaEventSynchronize(t->finish));  // the old graph may still be running
-      JANUS_CUDA(cudaGraphExecDestroy(t->gexec));
-      t->gexec = nullptr;
-      t->kernel_count = -1;
+      if (t->gexec) JANUS_CUDA(cudaGraphExecDestroy(t->gexec));
+      if (t->gexec_alt) JANUS_CUDA(cudaGraphExecDestroy(t->gexec_alt));
+      t->gexec = t->gexec_alt = nullptr;
+      t->gkey.clear();
+      t->gkey_alt.clear();
+      t->kernel_count = t->kernel_count_alt = -1;
     }
   }
 }
 
 // count kernel nodes of one captured step (the gpu_launches evidence)
-int64_t count_kernels(janus_trainer* t, const janus_opt& opt) {
+// Capture one step (nothing runs); instantiate it when graphs are on.  *nk =
+// kernel nodes (the gpu_launches evidence).
+cudaGraphExec_t capture_step(janus_trainer* t, const janus_opt& opt, int64_t* nk) {
   cudaGraph_t g;
   JANUS_CUDA(cudaStreamBeginCapture(t->root, cudaStreamCaptureModeThreadLocal));
   try {
@@ -775,11 +821,11 @@ int64_t count_kernels(janus_trainer* t, const janus_opt& opt) {
                  by_type[cudaGraphNodeTypeMemset], by_type[cudaGraphNodeTypeHost], by_type[cudaGraphNodeTypeEmpty],
                  by_type[cudaGraphNodeTypeWaitEvent & 15], by_type[cudaGraphNodeTypeEventRecord & 15]);
   }
-  if (t->ed.use_graphs && !t->ed.record_timeline) {
-    JANUS_CUDA(cudaGraphInstantiate(&t->gexec, g, 0));
-  }
+  cudaGraphExec_t exec = nullptr;
+  if (t->ed.use_graphs && !t->ed.record_timeline) JANUS_CUDA(cudaGraphInstantiate(&exec, g, 0));
   JANUS_CUDA(cudaGraphDestroy(g));
-  return k;
+  *nk = k;
+  return exec;
 }
 
 // Issue one step on the root stream and return without waiting: the caller may
@@ -790,16 +836,55 @@ void trainer_step_async(janus_trainer* t, const janus_opt& opt) {
   if (t->pending) throw state_error("a step is already in flight (call janus_trainer_wait)");
   for (int m = 0; m < t->ed.n_micro_batches; ++m)
     if (t->n_atoms[static_cast<size_t>(m)] <= 0) throw state_error("micro-batch " + std::to_string(m) + " not loaded");
-  if (t->local && t->kernel_count < 0) t->kernel_count = count_kernels(t, opt);  // capture only, nothing runs
+  // loads since the last step: the phases switch to the geometry copies they
+  // filled, and root waits for the load stream
+  bool loaded = false;
+  for (size_t m = 0; m < t->load_par.size(); ++m) {
+    const int q = t->load_par[m];
+    if (q < 0) continue;
+    for (janus_stage* st : t->owned) stage_set_parity(st, static_cast<int>(m), q);
+    t->step_par[m] = q;
+    t->load_par[m] = -1;
+    loaded = true;
+  }
+  if (loaded) JANUS_CUDA(cudaStreamWaitEvent(t->root, t->load_done, 0));
+  t->recording = false;  // a capture below must not record timeline events
+  cudaGraphExec_t exec = nullptr;
+  const bool graphs = t->ed.use_graphs && !t->ed.record_timeline;
+  if (t->local && !graphs) {
+    if (t->kernel_count < 0) capture_step(t, opt, &t->kernel_count);  // count only, nothing runs
+  } else if (t->local) {
+    // one instantiated graph per geometry-parity vector (two alternate in steady state)
+    std::vector<int> key(t->step_par.begin(), t->step_par.end());
+    if (t->gexec && key == t->gkey) {
+      exec = t->gexec;
+    } else if (t->gexec_alt && key == t->gkey_alt) {
+      std::swap(t->gexec, t->gexec_alt);
+      std::swap(t->gkey, t->gkey_alt);
+      std::swap(t->kernel_count, t->kernel_count_alt);
+      exec = t->gexec;
+    } else {
+      int64_t nk = 0;
+      cudaGraphExec_t e = capture_step(t, opt, &nk);  // capture only, nothing runs
+      if (t->gexec_alt) JANUS_CUDA(cudaGraphExecDestroy(t->gexec_alt));
+      t->gexec_alt = t->gexec;
+      t->gkey_alt = t->gkey;
+      t->kernel_count_alt = t->kernel_count;
+      t->gexec = e;
+      t->gkey = key;
+      t->kernel_count = nk;
+      exec = e;
+    }
+  }
   for (auto& r : t->recs) {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
   }
   t->recs.clear();
   t->recording = t->ed.record_timeline != 0;
-  if (t->gexec) {
+  if (exec) {
     JANUS_CUDA(cudaEventRecord(t->anchor, t->root));
-    JANUS_CUDA(cudaGraphLaunch(t->gexec, t->root));
+    JANUS_CUDA(cudaGraphLaunch(exec, t->root));
   } else {
     fork_join_begin(t);
     issue_step(t, opt);
@@ -807,6 +892,8 @@ void trainer_step_async(janus_trainer* t, const janus_opt& opt) {
     if (t->local) finalize_local(t, opt);
   }
   JANUS_CUDA(cudaEventRecord(t->finish, t->root));
+  if (t->step_end[0]) JANUS_CUDA(cudaEventRecord(t->step_end[t->nsteps & 1], t->root));
+  ++t->nsteps;
   t->pending = true;
 }
 

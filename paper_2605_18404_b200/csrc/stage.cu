@@ -64,6 +64,12 @@ T* dalloc(janus_stage* st, size_t n, bool count_static) {
 
 inline int blocks(int64_t n, int t) { return static_cast<int>((n + t - 1) / t); }
 
+size_t geo_index(const janus_stage* st, int mb, int par) {
+  return static_cast<size_t>(par) * static_cast<size_t>(st->desc.n_micro_batches) + static_cast<size_t>(mb);
+}
+DevGeo& geo_of(janus_stage* st, int mb) { return st->geo[geo_index(st, mb, st->gpar[static_cast<size_t>(mb)])]; }
+const DevGeo& geo_of(const janus_stage* st, int mb) { return st->geo[geo_index(st, mb, st->gpar[static_cast<size_t>(mb)])]; }
+
 // Attribution switch for profiling runs ONLY (numerically invalid when set):
 // JANUS_PROF_SKIP bitmask drops launches — 1 FE, 2 FF, 4 BF, 8 BE tensor-core
 // edge kernels, 16 wgrad_multi, 32 fused upd kernels, 64 gemm_rows, 128
@@ -253,7 +259,7 @@ Scratch& lane_of(janus_stage* st, int lane) {
 void check_mb_slot(const janus_stage* st, int mb, int slot) {
   if (mb < 0 || mb >= st->desc.n_micro_batches) throw domain_error("micro-batch index out of range");
   if (slot < 0 || slot >= st->desc.n_slots) throw domain_error("slot index out of range");
-  if (st->geo[static_cast<size_t>(mb)].n_atoms <= 0) throw state_error("micro-batch not loaded (LM missing)");
+  if (geo_of(st, mb).n_atoms <= 0) throw state_error("micro-batch not loaded (LM missing)");
 }
 
 }  // namespace
@@ -321,7 +327,8 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
       st->tw.push_back(k == kEmbed ? nullptr : dalloc<float>(st, n, true));
     }
     // geometry per micro-batch
-    st->geo.resize(NMB);
+    st->geo.resize(2 * NMB);
+    st->gpar.assign(NMB, 0);
     for (auto& g : st->geo) {
       st->lay = load_layout(d);
       const LoadLayout& L = st->lay;
@@ -466,7 +473,7 @@ size_t port_elems(const janus_stage* st, int port, int n) {
 
 // ================================================================== LM
 void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_t s, bool sync,
-                const DevCsrSlice* dcsr, std::vector<node::GeoJob>* defer) {
+                const DevCsrSlice* dcsr, std::vector<node::GeoJob>* defer, int par) {
   if (mb < 0 || mb >= st->desc.n_micro_batches) throw domain_error("micro-batch index out of range");
   if (!hb.row_ptr && !dcsr) {  // no neighbour list in the batch: build it on the device (nbrlist.cu)
     if (!st->lm) st->lm = new LmBuilder(st->desc.max_atoms, st->desc.max_struct, st->desc.max_edges, st->desc.device, 1);
@@ -474,15 +481,16 @@ void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_
     hb2.n_edges = st->lm->build(&hb, 1, static_cast<double>(st->m.r_c), 0, s);
     hb2.row_ptr = st->lm->host_row_ptr();
     const DevCsrSlice sl{&st->lm->buf(0), 0, 0};
-    stage_load(st, mb, hb2, s, sync, &sl);
+    stage_load(st, mb, hb2, s, sync, &sl, nullptr, par);
     st->lm->release(0, s);
     return;
   }
+  if (par < 0) par = st->gpar[static_cast<size_t>(mb)];
   if (hb.n_atoms < 1 || hb.n_atoms > st->desc.max_atoms) throw domain_error("n_atoms exceeds stage capacity");
   if (hb.n_edges < 0 || hb.n_edges > st->desc.max_edges) throw domain_error("n_edges exceeds stage capacity");
   if (hb.n_struct < 1 || hb.n_struct > st->desc.max_struct) throw domain_error("n_struct exceeds stage capacity");
   JANUS_CUDA(cudaSetDevice(st->desc.device));
-  DevGeo& g = st->geo[static_cast<size_t>(mb)];
+  DevGeo& g = st->geo[geo_index(st, mb, par)];
   const int N = hb.n_atoms, E = hb.n_edges;
   // host-side row tiles (<= 8 rows and <= te edges, or one long row) and struct offsets
   auto build_tiles = [&](int te) {
@@ -527,7 +535,7 @@ void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_
     }
     return tiles;
   };
-  DevGeo& gg = st->geo[static_cast<size_t>(mb)];
+  DevGeo& gg = g;
   gg.h_tiles = build_tiles(edge::TE);
   // up to 2 chunks per tile at ~50 neighbours, 4 in dense cells (measured:
   // C2 2 -> 6456 vs 3 -> 6070 structures/s; C5 2 -> 204 vs 4 -> 240)
@@ -625,6 +633,12 @@ void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_
   if (sync) JANUS_CUDA(cudaStreamSynchronize(s));
 }
 
+void stage_set_parity(janus_stage* st, int mb, int par) {
+  if (mb < 0 || mb >= st->desc.n_micro_batches || par < 0 || par > 1) throw domain_error("bad geometry parity");
+  st->gpar[static_cast<size_t>(mb)] = par;
+}
+const DevGeo& stage_geo(const janus_stage* st, int mb, int par) { return st->geo[geo_index(st, mb, par)]; }
+
 void stage_geometry_flush(janus_stage* st, std::vector<node::GeoJob>& jobs, cudaStream_t s) {
   for (size_t b = 0; b < jobs.size(); b += node::kMaxGeoJobs) {
     node::GeoJobs J{};
@@ -647,7 +661,7 @@ void stage_geometry_flush(janus_stage* st, std::vector<node::GeoJob>& jobs, cuda
 void stage_fe(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
   check_mb_slot(st, mb, slot);
   Scratch& sc = lane_of(st, lane);
-  const DevGeo& g = st->geo[static_cast<size_t>(mb)];
+  const DevGeo& g = geo_of(st, mb);
   Slot& sl = st->slots[static_cast<size_t>(slot)];
   sl.mb = mb;
   const int N = g.n_atoms, H = kH, R = kR, L = st->m.L;
@@ -702,7 +716,7 @@ void stage_fe(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
 void stage_ff(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
   check_mb_slot(st, mb, slot);
   Scratch& sc = lane_of(st, lane);
-  const DevGeo& g = st->geo[static_cast<size_t>(mb)];
+  const DevGeo& g = geo_of(st, mb);
   Slot& sl = st->slots[static_cast<size_t>(slot)];
   const int N = g.n_atoms, H = kH, R = kR, L = st->m.L;
   const size_t NH = static_cast<size_t>(N) * H;
@@ -768,7 +782,7 @@ void stage_ff(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
 void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
   check_mb_slot(st, mb, slot);
   Scratch& sc = lane_of(st, lane);
-  const DevGeo& g = st->geo[static_cast<size_t>(mb)];
+  const DevGeo& g = geo_of(st, mb);
   Slot& sl = st->slots[static_cast<size_t>(slot)];
   const int N = g.n_atoms, H = kH, R = kR, L = st->m.L;
   const size_t NH = static_cast<size_t>(N) * H;
@@ -851,7 +865,7 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
 void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only, int lane) {
   check_mb_slot(st, mb, slot);
   Scratch& sc = lane_of(st, lane);
-  const DevGeo& g = st->geo[static_cast<size_t>(mb)];
+  const DevGeo& g = geo_of(st, mb);
   Slot& sl = st->slots[static_cast<size_t>(slot)];
   const int N = g.n_atoms, H = kH, R = kR, L = st->m.L;
   const size_t NH = static_cast<size_t>(N) * H;
@@ -970,7 +984,7 @@ void stage_port(janus_stage* st, int mb, int slot, int port, void** dptr, size_t
     return;
   }
   *dptr = p.buf;
-  *bytes = port_elems(st, port, st->geo[static_cast<size_t>(mb)].n_atoms) * sizeof(float);
+  *bytes = port_elems(st, port, geo_of(st, mb).n_atoms) * sizeof(float);
 }
 
 // ============================================================ kernel timing
@@ -994,7 +1008,7 @@ double edge_kernel_flops_per_edge(int which, int H, int R) {
 // lane `lane`: step_grid = the grid the step uses (tiles per CTA), else one
 // tile per CTA on the full grid.  Inputs must exist (run the step first).
 void launch_edge_kernel(janus_stage* st, int u, int which, int mb, int slot, int lane, cudaStream_t s, bool step_grid) {
-  const DevGeo& g = st->geo[static_cast<size_t>(mb)];
+  const DevGeo& g = geo_of(st, mb);
   Slot& sl = st->slots[static_cast<size_t>(slot)];
   UnitBufs& b = sl.units[static_cast<size_t>(u - st->u0)];
   const EdgeGeom eg = edge_geom(g);
@@ -1052,7 +1066,7 @@ void stage_time_edge_kernel(janus_stage* st, int which, int mb, int slot, int it
   JANUS_CUDA(cudaEventCreate(&z));
   if (mb >= 0) {  // one micro-batch, back-to-back launches, full grid
     check_mb_slot(st, mb, slot);
-    const DevGeo& g = st->geo[static_cast<size_t>(mb)];
+    const DevGeo& g = geo_of(st, mb);
     launch_edge_kernel(st, u, which, mb, slot, 0, s, false);
     JANUS_LAUNCH_CHECK("time_edge_kernel");
     JANUS_CUDA(cudaEventRecord(a, s));
@@ -1073,7 +1087,7 @@ void stage_time_edge_kernel(janus_stage* st, int which, int mb, int slot, int it
     for (auto& x : ls) JANUS_CUDA(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
     for (auto& x : ev) JANUS_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
     int64_t E = 0;
-    for (int m = 0; m < n_mb; ++m) E += st->geo[static_cast<size_t>(m)].n_edges;
+    for (int m = 0; m < n_mb; ++m) E += geo_of(st, m).n_edges;
     auto round = [&] {
       JANUS_CUDA(cudaEventRecord(ev[0], s));
       for (int l = 0; l < L; ++l) JANUS_CUDA(cudaStreamWaitEvent(ls[static_cast<size_t>(l)], ev[0], 0));
@@ -1111,7 +1125,7 @@ int stage_slot_of_mb(const janus_stage* st, int mb) {
 void stage_energy(janus_stage* st, int mb, float* E_host, float* loss_E, cudaStream_t s) {
   if (!st->has_readout) throw state_error("energies live on the stage holding the readout unit");
   const Slot& sl = st->slots[static_cast<size_t>(stage_slot_of_mb(st, mb))];
-  const int ns = st->geo[static_cast<size_t>(mb)].n_struct;
+  const int ns = geo_of(st, mb).n_struct;
   if (E_host) JANUS_CUDA(cudaMemcpyAsync(E_host, sl.E, sizeof(float) * ns, cudaMemcpyDeviceToHost, s));
   if (loss_E) JANUS_CUDA(cudaMemcpyAsync(loss_E, sl.loss, sizeof(float), cudaMemcpyDeviceToHost, s));
   JANUS_CUDA(cudaStreamSynchronize(s));
@@ -1120,7 +1134,7 @@ void stage_energy(janus_stage* st, int mb, float* E_host, float* loss_E, cudaStr
 void stage_forces(janus_stage* st, int mb, float* F_host, float* loss_F, cudaStream_t s) {
   if (!st->has_embed) throw state_error("complete forces live on stage 0");
   const Slot& sl = st->slots[static_cast<size_t>(stage_slot_of_mb(st, mb))];
-  const int n = st->geo[static_cast<size_t>(mb)].n_atoms;
+  const int n = geo_of(st, mb).n_atoms;
   if (F_host) JANUS_CUDA(cudaMemcpyAsync(F_host, sl.F, sizeof(float) * 3 * n, cudaMemcpyDeviceToHost, s));
   if (loss_F) JANUS_CUDA(cudaMemcpyAsync(loss_F, sl.loss + 1, sizeof(float), cudaMemcpyDeviceToHost, s));
   JANUS_CUDA(cudaStreamSynchronize(s));

@@ -106,7 +106,11 @@ struct janus_stage {
   std::vector<float*> tw;              // per unit: transposed weights block
   int adam_step = 0;
   int* dstep = nullptr;  // device-side Adam step (graph-replayable bias correction)
+  // geometry per micro-batch, double-buffered: geo[par * n_mb + mb]; the
+  // phases read parity gpar[mb] while a trainer load may fill the other one
+  // (a step in flight keeps reading its own copy)
   std::vector<janus::DevGeo> geo;
+  std::vector<int> gpar;
   std::vector<janus::Slot> slots;
   std::vector<janus::Scratch> lanes;
   float* losses = nullptr;  // [n_slots][2] loss_E, loss_F (slot.loss points here)

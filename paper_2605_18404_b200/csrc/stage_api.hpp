@@ -19,8 +19,13 @@ struct DevCsrSlice;
 // and hb.col/shift/rev are ignored).
 // defer: queue the slice + geometry launch into `defer` (run by
 // stage_geometry_flush as one batched kernel) instead of launching per batch.
+// par: which of the micro-batch's two geometry copies to fill (< 0: the one
+// the phases currently read; the trainer fills the other one beside a step).
 void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_t s, bool sync = true,
-                const DevCsrSlice* dcsr = nullptr, std::vector<node::GeoJob>* defer = nullptr);
+                const DevCsrSlice* dcsr = nullptr, std::vector<node::GeoJob>* defer = nullptr, int par = -1);
+void stage_set_parity(janus_stage* st, int mb, int par);  // the copy the phases read from now on
+struct DevGeo;
+const DevGeo& stage_geo(const janus_stage* st, int mb, int par);
 void stage_geometry_flush(janus_stage* st, std::vector<node::GeoJob>& jobs, cudaStream_t s);
 void stage_fe(janus_stage* st, int mb, int slot, cudaStream_t s, int lane = 0);
 void stage_ff(janus_stage* st, int mb, int slot, cudaStream_t s, int lane = 0);
