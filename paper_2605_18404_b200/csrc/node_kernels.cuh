@@ -461,17 +461,22 @@ __device__ __forceinline__ void rowmm(const float (*X)[68], const float* Ms, int
 }
 // Stage up to 4 [64][64] weight matrices into smem with every load in flight
 // at once (16 float4 per thread per matrix), then one barrier.
+// (cp.async: every 16 B copy of every matrix in flight at once, no registers;
+// the caller's barrier follows cp.async.wait_group 0 in stage_mats_wait)
 __device__ __forceinline__ void stage_mats(float* dst, const float* const* src, int n) {
   for (int m = 0; m < n; ++m) {
     const float4* s4 = reinterpret_cast<const float4*>(src[m]);
     float4* d4 = reinterpret_cast<float4*>(dst + m * 4096);
-    float4 t[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) t[q] = __ldg(s4 + threadIdx.x + 256 * q);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) d4[threadIdx.x + 256 * q] = t[q];
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t da = static_cast<uint32_t>(__cvta_generic_to_shared(d4 + threadIdx.x + 256 * q));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(da), "l"(s4 + threadIdx.x + 256 * q) : "memory");
+    }
   }
+  asm volatile("cp.async.commit_group;" ::: "memory");
 }
+// the matrices landed (this thread's copies); a barrier then publishes them
+__device__ __forceinline__ void stage_mats_wait() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 constexpr size_t upd_smem(int nmats) { return sizeof(float) * 4096 * nmats; }
 
 __device__ __forceinline__ void row_load(float (*X)[68], const float* __restrict__ src, int i0, int rows) {
@@ -502,6 +507,7 @@ __global__ void __launch_bounds__(256) upd_fe_fused(int rows, const float* __res
     stage_mats(Ws, mats, 2);
   }
   row_load(X, m, i0, rows);
+  stage_mats_wait();
   __syncthreads();
   float o[4];
   rowmm(X, Ws, r, c0, o);
@@ -533,6 +539,7 @@ __global__ void __launch_bounds__(256) upd_ff_fused(int rows, const float* __res
     stage_mats(Ws, mats, 2);
   }
   row_load(X, a, i0, rows);
+  stage_mats_wait();
   __syncthreads();
   if (i < rows) {
     const float v4[4] = {X[r][c0], X[r][c0 + 1], X[r][c0 + 2], X[r][c0 + 3]};
@@ -569,6 +576,7 @@ __global__ void __launch_bounds__(256) upd_bf_fused(int rows, const float* __res
     stage_mats(Ws, mats, 4);
   }
   row_load(X, am, i0, rows);
+  stage_mats_wait();
   row_load(Y, ffa, i0, rows);
   __syncthreads();
   float pd[4], rr[4];
@@ -617,6 +625,7 @@ __global__ void __launch_bounds__(256) upd_be_fused(int rows, const float* __res
     stage_mats(Ws, mats, 2);
   }
   row_load(X, bh, i0, rows);
+  stage_mats_wait();
   __syncthreads();
   float o[4];
   rowmm(X, Ws, r, c0, o);
