@@ -212,16 +212,20 @@ int janus_trainer_create(const janus_exec_desc* ed, const janus_stage_desc* sd, 
                          janus_comm* comm, int rank, janus_trainer** out);
 int janus_trainer_destroy(janus_trainer* t);
 int janus_trainer_load(janus_trainer* t, int mb, const janus_host_batch* hb);
-/* LM of n micro-batches (mbs[k] <- hbs[k]).  Batches without a neighbour list
+/* LM of n micro-batches (mbs[k] <- hbs[k]).  Each micro-batch's geometry is
+ * double-buffered: a load fills the copy the step in flight does not read, on
+ * the trainer's load stream, and the next janus_trainer_step[_async] switches
+ * to it (root waits for the loads).  Batches without a neighbour list
  * (row_ptr == NULL) get ONE device cell-list build over all of them (their
- * structures side by side), run on a side stream beside a step in flight, and
- * one host sync for the row-tile tables.  janus_trainer_load == n = 1. */
+ * structures side by side) and one host sync for the row-tile tables.
+ * janus_trainer_load == n = 1. */
 int janus_trainer_load_many(janus_trainer* t, int n, const int32_t* mbs, const janus_host_batch* hbs);
 int janus_trainer_step(janus_trainer* t, const janus_opt* opt, janus_step_stats* stats);
 /* janus_trainer_step split in two: issue the step and return; then wait for it
- * and fill stats (loss read back).  Loads issued in between are queued behind
- * the step in flight, so the next step's uploads overlap this step's device
- * time (input pipelining).  janus_trainer_step == step_async + wait. */
+ * and fill stats (loss read back).  Loads issued in between run beside the
+ * step in flight (into the other geometry copy), so the next step's uploads,
+ * neighbour lists and geometry overlap this step's device time (input
+ * pipelining).  janus_trainer_step == step_async + wait. */
 int janus_trainer_step_async(janus_trainer* t, const janus_opt* opt);
 int janus_trainer_wait(janus_trainer* t, janus_step_stats* stats);
 /* per compute instruction of the last timed step: [n][5] = device, kind, mb, start_us, end_us */
