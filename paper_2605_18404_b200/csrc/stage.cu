@@ -539,7 +539,11 @@ void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_
   gg.h_tiles = build_tiles(edge::TE);
   // up to 2 chunks per tile at ~50 neighbours, 4 in dense cells (measured:
   // C2 2 -> 6456 vs 3 -> 6070 structures/s; C5 2 -> 204 vs 4 -> 240)
-  const int max_chunks = st->tc_tile_max_chunks > 0 ? st->tc_tile_max_chunks : (E >= 80 * N ? 4 : 2);
+  // one lane (a latency-bound pipeline stage issuing one kernel at a time):
+  // single-chunk tiles, the most CTAs per launch
+  const int max_chunks = st->tc_tile_max_chunks > 0 ? st->tc_tile_max_chunks
+                         : st->desc.n_lanes <= 1   ? 1
+                                                   : (E >= 80 * N ? 4 : 2);
   gg.h_tiles_tc = st->tc_tile_edges > 0 ? build_tiles(st->tc_tile_edges) : build_tiles_cost(max_chunks, st->tc_tile_ovh);
   const std::vector<int>& tiles = gg.h_tiles;
   const std::vector<int>& tiles_tc = gg.h_tiles_tc;

@@ -36,7 +36,7 @@ def batch(janus, cell, shift=None):
 
 def run(janus, m, params, batches, P, method, k=1):
     t = janus.Trainer(m, params, P, method, len(batches), k=k, max_atoms=N_ATOMS, max_edges=N_ATOMS * 130,
-                      max_struct=1, lanes=1 if P > 1 else 2)
+                      max_struct=1, lanes=1)  # same lanes: same tiles and tiles per CTA
     t.load_many(batches)
     st = t.step(lr=1e-3)
     E = [t.stage(P - 1).energy(i, 1)[0][0] for i in range(len(batches))]
