@@ -25,6 +25,11 @@ OBJ := build/nt$(TC_NT)_obj
 LIB := build/nt$(TC_NT)/libjanus_b200.so
 NVFLAGS += -DJANUS_TC_NT=$(TC_NT)
 endif
+ifneq ($(FEFF_CTAS),)  # FE / FF CTAs per SM experiment
+OBJ := build/feff$(FEFF_CTAS)_obj
+LIB := build/feff$(FEFF_CTAS)/libjanus_b200.so
+NVFLAGS += -DJANUS_FEFF_CTAS=$(FEFF_CTAS)
+endif
 ifeq ($(TRACE),1)  # phase-traced profiling build (edge_tc.cuh TC_MARK), loaded via JANUS_LIB
 OBJ := build/trace_obj
 LIB := build/trace/libjanus_b200.so

@@ -32,7 +32,10 @@ constexpr int TE = 128;
 #ifndef JANUS_TC_NT
 #define JANUS_TC_NT 512
 #endif
-constexpr int NT = JANUS_TC_NT;    // 512: 16 warps, 4 threads per edge row (1024: 8 per row)
+constexpr int NT = JANUS_TC_NT;
+#ifndef JANUS_FEFF_CTAS
+#define JANUS_FEFF_CTAS 2  // FE / FF CTAs per SM (64 registers per thread at 2)
+#endif    // 512: 16 warps, 4 threads per edge row (1024: 8 per row)
 constexpr int NQ = NT / TE;        // feature quarters per edge
 constexpr int FPT = 64 / NQ;       // features per thread (16)
 constexpr int H = 64, R = 64;
@@ -413,7 +416,7 @@ __device__ __forceinline__ float fsig(float x) { return __fdividef(1.0f, 1.0f + 
 
 // ----------------------------------------------------------------------- FE
 // m_i = sum_{e in row i} w_e * v[col e], w = c (SiLU(phi A + alpha) B + beta)
-__global__ void __launch_bounds__(NT, 2) msg_fe_tc(EdgeGeom g, const int4* __restrict__ tiles, int n_tiles, MsgParams p,
+__global__ void __launch_bounds__(NT, JANUS_FEFF_CTAS) msg_fe_tc(EdgeGeom g, const int4* __restrict__ tiles, int n_tiles, MsgParams p,
                                                float rc, const float* __restrict__ v, float* __restrict__ m_out) {
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = align1024(sm_raw);
@@ -516,7 +519,7 @@ __global__ void __launch_bounds__(NT, 2) msg_fe_tc(EdgeGeom g, const int4* __res
 // ----------------------------------------------------------------------- FF
 // Y_i = sum w_e * am[col e];  F_i += sum_e (q_e + q_rev(e)) u_e with
 // q_e + q_rev(e) = < am_i v_j + am_j v_i , w'_e >  (w' symmetric in e <-> rev e)
-__global__ void __launch_bounds__(NT, 2) msg_ff_tc(EdgeGeom g, const int4* __restrict__ tiles, int n_tiles, MsgParams p,
+__global__ void __launch_bounds__(NT, JANUS_FEFF_CTAS) msg_ff_tc(EdgeGeom g, const int4* __restrict__ tiles, int n_tiles, MsgParams p,
                                                float rc, const float* __restrict__ v, const float* __restrict__ am,
                                                float* __restrict__ Y_out, float* __restrict__ F,
                                                float* ah) {
