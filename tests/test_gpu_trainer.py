@@ -171,3 +171,29 @@ def test_pipelined_loads_bit_identical(janus, data, graphs):
         tb.wait()  # nothing in flight
     ta.close()
     tb.close()
+
+
+@pytest.mark.parametrize("P,method,k", [(4, 1, 8), (2, 0, 1)])
+def test_tensor_core_pipeline_lanes_bit_identical(janus, P, method, k):
+    """The N>1 bench configuration on one GPU: tensor-core kernels, device-built
+    neighbour lists, P pipeline stages with 8 compute lanes per stage and
+    double-buffered loads — bit-identical to one stage with the same lanes."""
+    if not janus.device_count():
+        pytest.skip("no GPU")
+    m = janus.Model(L=2, H=64, R=64, precision=janus.PREC_TF32)
+    params = m.synth_params(8)
+    bs = [janus.synth_batch(m, [64 + 8 * (i % 3)], 0.095, 300 + i, device_nl=True) for i in range(16)]
+    out = []
+    for PP, meth, kk in ((1, janus.METHOD_SYMFOLD, 1), (P, method, k)):
+        t = janus.Trainer(m, params, PP, meth, len(bs), k=kk, max_atoms=96, max_edges=96 * 80, lanes=8,
+                          graphs=True)
+        t.load_many(bs)
+        losses = []
+        for _ in range(2):
+            t.step_async(lr=1e-3)
+            t.load_many(bs)  # next step's loads beside the step in flight
+            losses.append(t.wait().loss)
+        out.append((losses, t.params(), t.grads()))
+        t.close()
+    assert out[0][0] == out[1][0]
+    assert np.array_equal(out[0][1], out[1][1]) and np.array_equal(out[0][2], out[1][2])
