@@ -390,7 +390,11 @@ def main():
                                 "neighbour_lists": "host-built once, uploaded every step"},
                "gpu_launches": int(launches), "gpu_launches_per_step": int(stats.kernel_launches),
                "roofline": roof, "cpu_baseline": cpu, "clocks": clocks,
-               "p2p_bytes_per_step": int(stats.p2p_bytes), "loss": stats.loss,
+               "p2p_bytes_per_step": int(stats.p2p_bytes),
+               "p2p": ({"GBps_per_gpu": stats.p2p_bytes / (ms_per_step * 1e-3) / 1e9,
+                        "nvlink_GBps_per_direction": 900.0,
+                        "frac": stats.p2p_bytes / (ms_per_step * 1e-3) / 1e9 / 900.0} if N > 1 else None),
+               "loss": stats.loss,
                "peak_hbm_bytes_per_stage": [int(stats.peak_bytes[d]) for d in range(P)]}
         print(json.dumps(out), flush=True)
     tr.close()
