@@ -15,6 +15,7 @@ struct GeoJob {
   const double* cell;
   int* src;
   float *d, *u, *c, *dc;
+  int *pcanon, *pidx;                         // pair tables (pair_tc.cuh pairs_kernel)
 };
 constexpr int kMaxGeoJobs = 48;
 struct GeoJobs {

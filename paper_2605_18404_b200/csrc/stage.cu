@@ -21,6 +21,7 @@
 
 #include "edge_kernels.cuh"
 #include "edge_tc.cuh"
+#include "pair_tc.cuh"
 #include "node_kernels.cuh"
 #include "wgrad_tc.cuh"
 #include "stage.cuh"
@@ -359,6 +360,8 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
       g.u = dalloc<float>(st, 3 * NE, false);
       g.c = dalloc<float>(st, NE, false);
       g.dc = dalloc<float>(st, NE, false);
+      g.pidx = dalloc<int>(st, NE, false);
+      g.pcanon = dalloc<int>(st, NE / 2 + 1, false);
     }
     // slots
     st->slots.resize(static_cast<size_t>(d.n_slots));
@@ -374,6 +377,10 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
             b.ff_a = dalloc<float>(st, NH, false);
             b.ff_Y = dalloc<float>(st, NH, false);
             b.inj = dalloc<float>(st, NH, false);
+            if (m.precision == JANUS_PREC_TF32) {
+              b.wf = dalloc<float>(st, (NE / 2 + 1) * kH, false);
+              b.wfp = dalloc<float>(st, (NE / 2 + 1) * kH, false);
+            }
             break;
           case kUpd:
             b.out_h = dalloc<float>(st, NH, false);
@@ -421,6 +428,7 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
     if (const char* e = std::getenv("JANUS_TC_TILE_OVH")) st->tc_tile_ovh = std::atof(e);
     if (const char* e = std::getenv("JANUS_TPC_FE")) st->tpc_fe = std::max(1, std::atoi(e));  // tuning runs only
     if (const char* e = std::getenv("JANUS_TPC_WG")) st->tpc_wg = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("JANUS_FEFF_PAIR")) st->pair_feff = std::atoi(e) != 0;  // A/B runs only
     for (Scratch& sc : st->lanes) {
       sc.wh = dalloc<float>(st, NH, false);
       sc.wm = dalloc<float>(st, NH, false);
@@ -442,6 +450,7 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
     JANUS_CUDA(cudaFuncSetAttribute(node::upd_bf_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)node::upd_smem(4)));
     JANUS_CUDA(cudaFuncSetAttribute(edge_tc::msg_fe_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge_tc::fe_smem()));
     JANUS_CUDA(cudaFuncSetAttribute(edge_tc::msg_ff_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge_tc::ff_smem()));
+    JANUS_CUDA(cudaFuncSetAttribute(edge_tc::msg_filter_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge_tc::filter_smem()));
     JANUS_CUDA(cudaFuncSetAttribute(edge_tc::msg_bf_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge_tc::bf_smem()));
     JANUS_CUDA(cudaFuncSetAttribute(edge_tc::msg_be_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge_tc::be_smem()));
     refresh_transposes(st, nullptr);
@@ -561,6 +570,8 @@ void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_
   g.n_struct = hb.n_struct;
   g.n_tiles = static_cast<int>(tiles.size()) - 1;
   g.n_tiles_tc = static_cast<int>(tiles_tc.size()) - 1;
+  if (use_tc(st) && E % 2) throw domain_error("odd edge count: every edge needs a distinct reverse edge");
+  g.n_pairs = E / 2;
   // one pinned image per load (alternating halves: the other may still feed
   // a queued copy), one host->device copy
   const LoadLayout& L = st->lay;
@@ -622,6 +633,8 @@ void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_
       j.u = g.u;
       j.c = g.c;
       j.dc = g.dc;
+      j.pcanon = g.pcanon;
+      j.pidx = g.pidx;
       defer->push_back(j);
     }
     return;
@@ -631,6 +644,15 @@ void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_
   if (E > 0)
     node::geometry_kernel<<<blocks(E, 256), 256, 0, s>>>(N, E, g.row_ptr, g.col, g.shift, g.pos, g.struct_id, g.cell,
                                                          static_cast<double>(st->m.r_c), g.src, g.d, g.u, g.c, g.dc);
+  if (E > 0 && use_tc(st)) {
+    node::GeoJobs J{};
+    J.n = 1;
+    J.j[0].n_edges = E;
+    J.j[0].rev = g.rev;
+    J.j[0].pcanon = g.pcanon;
+    J.j[0].pidx = g.pidx;
+    edge_tc::pairs_kernel<<<1, 1024, 0, s>>>(J);
+  }
   JANUS_LAUNCH_CHECK("geometry");
   // host arrays of the caller must stay valid until the stream reaches the
   // copies (pageable sources are staged by the driver before return)
@@ -656,9 +678,31 @@ void stage_geometry_flush(janus_stage* st, std::vector<node::GeoJob>& jobs, cuda
     }
     J.total_edges = base;
     if (base > 0) node::geometry_batched_kernel<<<blocks(base, 256), 256, 0, s>>>(J);
+    if (base > 0 && use_tc(st)) edge_tc::pairs_kernel<<<J.n, 1024, 0, s>>>(J);
     JANUS_LAUNCH_CHECK("geometry_batched");
   }
   jobs.clear();
+}
+
+// Filters w, w' of the stage's msg units (u_only < 0: all of them) for the
+// slot's micro-batch, one launch (pair_tc.cuh msg_filter_tc).
+void launch_filter(janus_stage* st, const DevGeo& g, Slot& sl, int u_only, cudaStream_t s, int grid_x = 0) {
+  edge_tc::FilterJobs J{};
+  for (int u = st->u0; u < st->u1; ++u) {
+    if (unit_kind(u, st->m.L) != kMsg || (u_only >= 0 && u != u_only)) continue;
+    if (J.n == edge_tc::kMaxFilterUnits) throw config_error("too many msg units on one stage for the filter launch");
+    UnitBufs& b = sl.units[static_cast<size_t>(u - st->u0)];
+    J.pack[J.n] = msg_params(st, u).pack;
+    J.w[J.n] = b.wf;
+    J.wp[J.n] = b.wfp;
+    ++J.n;
+  }
+  if (J.n == 0 || g.n_pairs == 0) return;
+  const int chunks = (g.n_pairs + edge_tc::TE - 1) / edge_tc::TE;
+  const int gx = grid_x > 0 ? std::min(grid_x, chunks) : std::max(1, std::min(chunks, (chunks + st->tpc_fe - 1) / st->tpc_fe));
+  edge_tc::msg_filter_tc<<<dim3(gx, J.n), edge_tc::NT, edge_tc::filter_smem(), s>>>(edge_geom(g), g.pcanon, g.n_pairs, J,
+                                                                                     st->m.r_c);
+  JANUS_LAUNCH_CHECK("msg_filter_tc");
 }
 
 // ================================================================== FE
@@ -672,6 +716,8 @@ void stage_fe(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
   const EdgeGeom eg = edge_geom(g);
   const float* cur_h = st->u0 > 0 ? port_h(sl.ports[JANUS_PORT_ACT_IN], N) : nullptr;
   const float* cur_m = st->in_has_m ? port_m(sl.ports[JANUS_PORT_ACT_IN], N) : nullptr;
+  const bool pairs = use_tc(st) && st->pair_feff;
+  if (pairs && g.n_pairs > 0 && !(prof_skip() & 1)) launch_filter(st, g, sl, -1, s);  // w, w' of every msg unit
   for (int u = st->u0; u < st->u1; ++u) {
     UnitBufs& b = sl.units[static_cast<size_t>(u - st->u0)];
     const float* P = st->P(u);
@@ -683,7 +729,10 @@ void stage_fe(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
       case kMsg: {
         const float* W = P + R * H + H + H * H + H;
         gemm(s, N, cur_h, W, nullptr, nullptr, nullptr, b.v);
-        if (g.n_tiles > 0 && use_tc(st)) {
+        if (pairs) {
+          if (!(prof_skip() & 1))
+            edge_tc::msg_fe_rows<<<blocks(N, 8), 256, 0, s>>>(N, g.row_ptr, g.col, g.pidx, b.wf, b.v, b.out_m);
+        } else if (g.n_tiles > 0 && use_tc(st)) {
           if (!(prof_skip() & 1)) edge_tc::msg_fe_tc<<<fe_grid(st, g), edge_tc::NT, edge_tc::fe_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, msg_params(st, u),
                                                                                  st->m.r_c, b.v, b.out_m);
         } else if (g.n_tiles > 0)
@@ -753,7 +802,12 @@ void stage_ff(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
       }
       case kMsg: {
         if (u == st->u1 - 1) copy(s, b.ff_a, wm, NH);  // a_m arrived through the ADJ_IN port
-        if (g.n_tiles > 0 && use_tc(st)) {  // a_h += Y W^T fused into the tile epilogue
+        if (use_tc(st) && st->pair_feff) {  // a_h += Y W^T fused into the row kernel
+          if (!(prof_skip() & 2))
+            edge_tc::msg_ff_rows<<<blocks(N, 8), 256, 0, s>>>(N, g.row_ptr, g.col, g.pidx, g.u, b.wf, b.wfp, b.v, b.ff_a,
+                                                               msg_params(st, u).pack + edge_tc::kWtOff / sizeof(float),
+                                                               b.ff_Y, sl.F, wh);
+        } else if (g.n_tiles > 0 && use_tc(st)) {  // a_h += Y W^T fused into the tile epilogue
           if (!(prof_skip() & 2)) edge_tc::msg_ff_tc<<<fe_grid(st, g), edge_tc::NT, edge_tc::ff_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, msg_params(st, u),
                                                                                  st->m.r_c, b.v, b.ff_a, b.ff_Y, sl.F, wh);
         } else {
@@ -998,6 +1052,15 @@ void stage_port(janus_stage* st, int mb, int slot, int port, void** dptr, size_t
 //   FF: z, z', g, g' (+ q dot)                          -> 2RH + 2H^2 + H
 //   BF: z, z', g, g', sbar, sdotbar, dB(2), dA(2)       -> 4RH + 6H^2
 //   BE: z, g, sbar, dB, dA                              -> 2RH + 3H^2
+// Pair mode (tensor-core FE / FF, pair_tc.cuh): "FE" = the filter launch (FE's
+// and FF's per-edge MMAs once per pair, i.e. half of FF's per-edge flops per
+// directed edge) + FE's row sums; "FF" = the row kernel (Y, force scalar, and
+// the a_h += Y W^T row GEMM counted per edge at ~50 edges per row is < 3%: omitted).
+double pair_flops_per_edge(int which, int H, int R) {
+  const double RH = static_cast<double>(R) * H, HH = static_cast<double>(H) * H;
+  return which == 0 ? 0.5 * 2.0 * (2 * RH + 2 * HH + H) + 2.0 * H : 2.0 * (3 * H);
+}
+
 double edge_kernel_flops_per_edge(int which, int H, int R) {
   const double RH = static_cast<double>(R) * H, HH = static_cast<double>(H) * H;
   switch (which) {
@@ -1018,6 +1081,17 @@ void launch_edge_kernel(janus_stage* st, int u, int which, int mb, int slot, int
   const EdgeGeom eg = edge_geom(g);
   const MsgParams mp = msg_params(st, u);
   Scratch& sc = lane_of(st, lane);
+  if (use_tc(st) && st->pair_feff && which < 2) {
+    const int N = g.n_atoms;
+    if (which == 0) {  // the filters of this unit (pair MMAs of FE and FF) + FE's row sums
+      launch_filter(st, g, sl, u, s, step_grid ? 0 : (g.n_pairs + edge_tc::TE - 1) / edge_tc::TE);
+      edge_tc::msg_fe_rows<<<blocks(N, 8), 256, 0, s>>>(N, g.row_ptr, g.col, g.pidx, b.wf, b.v, sc.s3);
+    } else {
+      edge_tc::msg_ff_rows<<<blocks(N, 8), 256, 0, s>>>(N, g.row_ptr, g.col, g.pidx, g.u, b.wf, b.wfp, b.v, b.ff_a,
+                                                         mp.pack + edge_tc::kWtOff / sizeof(float), sc.s3, sc.s5, sc.s4);
+    }
+    return;
+  }
   if (use_tc(st)) {
     const int grid = step_grid ? tc_grid(st, g) : tc_grid_tpc(g, 1);
     const int fgrid = step_grid ? fe_grid(st, g) : g.n_tiles_tc;
@@ -1055,6 +1129,10 @@ void launch_edge_kernel(janus_stage* st, int u, int which, int mb, int slot, int
   }
 }
 
+double kernel_flops_per_edge(const janus_stage* st, int which) {
+  return use_tc(st) && st->pair_feff && which < 2 ? pair_flops_per_edge(which, kH, kR) : edge_kernel_flops_per_edge(which, kH, kR);
+}
+
 int first_msg_unit(const janus_stage* st) {
   for (int x = st->u0; x < st->u1; ++x)
     if (unit_kind(x, st->m.L) == kMsg) return x;
@@ -1081,7 +1159,7 @@ void stage_time_edge_kernel(janus_stage* st, int which, int mb, int slot, int it
     JANUS_CUDA(cudaEventElapsedTime(&ms, a, z));
     *avg_ms = ms / iters;
     *edges = g.n_edges;
-    *flops = edge_kernel_flops_per_edge(which, kH, kR) * g.n_edges;
+    *flops = kernel_flops_per_edge(st, which) * g.n_edges;
   } else {
     // the step's concurrency: every micro-batch (slot = mb) on lane mb % lanes,
     // each launch with the step grid (tiles per CTA); time per round of all of them
@@ -1113,7 +1191,7 @@ void stage_time_edge_kernel(janus_stage* st, int which, int mb, int slot, int it
     for (auto& x : ev) cudaEventDestroy(x);
     *avg_ms = ms / iters;  // one round: all micro-batches
     *edges = E;
-    *flops = edge_kernel_flops_per_edge(which, kH, kR) * static_cast<double>(E);
+    *flops = kernel_flops_per_edge(st, which) * static_cast<double>(E);
   }
   cudaEventDestroy(a);
   cudaEventDestroy(z);

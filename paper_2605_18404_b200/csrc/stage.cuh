@@ -53,6 +53,10 @@ struct DevGeo {
   int *species = nullptr, *struct_id = nullptr, *struct_ptr = nullptr;
   double *pos = nullptr, *cell = nullptr;
   float *d = nullptr, *u = nullptr, *c = nullptr, *dc = nullptr, *E_target = nullptr, *F_target = nullptr;
+  // undirected edge pairs (tensor-core FE / FF, pair_tc.cuh): canonical edge of
+  // pair p, and pair of every directed edge
+  int *pcanon = nullptr, *pidx = nullptr;
+  int n_pairs = 0;
 };
 
 struct UnitBufs {  // per slot, per unit
@@ -62,6 +66,7 @@ struct UnitBufs {  // per slot, per unit
   float* p = nullptr;      // upd: m U + ups ; readout: t
   float* ff_a = nullptr;   // upd: FF input a' ; msg: FF input a_m
   float* ff_Y = nullptr;   // msg: Y
+  float *wf = nullptr, *wfp = nullptr;  // msg, tensor-core path: per-pair filter w and w' [pairs][64] (FE -> FF)
   float* inj = nullptr;    // BF -> BE injection at the unit input (h for msg/readout, m for upd)
   const float* in_h = nullptr;  // where this unit's input h lives (static)
   const float* in_m = nullptr;  // upd: input m
@@ -122,6 +127,7 @@ struct janus_stage {
   int tc_tile_edges = 0;             // TC tiles: 0 cost-chosen runs, > 0 greedy edge budget (tuning)
   int tc_tile_max_chunks = 0;        // cost-chosen tiles: max 128-edge chunks (0: by mean degree)
   double tc_tile_ovh = 0.3;          // per-tile epilogue cost in chunk units
+  bool pair_feff = true;             // TC FE / FF: filters once per edge pair (pair_tc.cuh); JANUS_FEFF_PAIR=0 -> directed-edge kernels
   janus::LmBuilder* lm = nullptr;  // device neighbour-list builder (lazy, janus_stage_load without a CSR)
 
   float* P(int u) const { return params + uoff[static_cast<size_t>(u - u0)]; }
