@@ -154,6 +154,23 @@ __global__ void __launch_bounds__(1024) pairs_kernel(const __grid_constant__ nod
   }
 }
 
+// (Y W^T) of one row held by a warp as float2 per lane (features 2 lane, 2 lane + 1);
+// wt = W^T row-major [64][64] (the pack's plain copy, read through L1)
+__device__ __forceinline__ float2 row_times_wt(float2 Y, const float* __restrict__ wt, int lane) {
+  float2 o0 = make_float2(0.f, 0.f), o1 = make_float2(0.f, 0.f);
+#pragma unroll 8
+  for (int q2 = 0; q2 < 32; ++q2) {
+    const float ya = __shfl_sync(0xffffffffu, Y.x, q2), yb = __shfl_sync(0xffffffffu, Y.y, q2);
+    const float2 ta = __ldg(reinterpret_cast<const float2*>(wt + (size_t)(2 * q2) * H) + lane);
+    const float2 tb = __ldg(reinterpret_cast<const float2*>(wt + (size_t)(2 * q2 + 1) * H) + lane);
+    o0.x = fmaf(ya, ta.x, o0.x);
+    o0.y = fmaf(ya, ta.y, o0.y);
+    o1.x = fmaf(yb, tb.x, o1.x);
+    o1.y = fmaf(yb, tb.y, o1.y);
+  }
+  return make_float2(o0.x + o1.x, o0.y + o1.y);
+}
+
 // m_i = sum_e w_p(e) * v_j   (warp per row, 2 features per lane)
 __global__ void __launch_bounds__(256) msg_fe_rows(int n_atoms, const int* __restrict__ row_ptr, const int* __restrict__ col,
                                                    const int* __restrict__ pidx, const float* __restrict__ w,
@@ -265,26 +282,369 @@ __global__ void __launch_bounds__(256) msg_ff_rows(int n_atoms, const int* __res
     F[3 * (size_t)i + 1] += fy;
     F[3 * (size_t)i + 2] += fz;
   }
-  if (ah) {  // a_h[i][c] += sum_q Y[q] W^T[q][c], c = 2 lane, 2 lane + 1
-    float2 o0 = make_float2(0.f, 0.f), o1 = make_float2(0.f, 0.f);
-#pragma unroll 8
-    for (int q2 = 0; q2 < 32; ++q2) {
-      const float ya = __shfl_sync(0xffffffffu, Y.x, q2), yb = __shfl_sync(0xffffffffu, Y.y, q2);
-      const float2 ta = __ldg(reinterpret_cast<const float2*>(wt + (size_t)(2 * q2) * H) + lane);
-      const float2 tb = __ldg(reinterpret_cast<const float2*>(wt + (size_t)(2 * q2 + 1) * H) + lane);
-      o0.x = fmaf(ya, ta.x, o0.x);
-      o0.y = fmaf(ya, ta.y, o0.y);
-      o1.x = fmaf(yb, tb.x, o1.x);
-      o1.y = fmaf(yb, tb.y, o1.y);
-    }
+  if (ah) {  // a_h[i] += Y W^T
+    const float2 o = row_times_wt(Y, wt, lane);
     float2* dst = reinterpret_cast<float2*>(ah + (size_t)i * H) + lane;
     float2 x = *dst;
-    x.x += o0.x + o1.x;
-    x.y += o0.y + o1.y;
+    x.x += o.x;
+    x.y += o.y;
     *dst = x;
   }
 }
 
+// ------------------------------------------------------------ BF / BE per pair
+// The weight gradients are linear in the per-edge adjoints (mu, nu of BF;
+// gbar of BE) with pair-symmetric left factors (phi, phi', s, sdot, z, z'), so
+// they are accumulated once per pair on the SUMS of both directions:
+//   BF  rho = am_i v_j + am_j v_i,  kappa = am_i vdot_j + am_j vdot_i,
+//       mu = qb c' rho + c kappa,  nu = qb c rho   (qb_rev = qb: u_rev = -u)
+//   BE  gbar = c (bm_i v_j + bm_j v_i)
+// then dB = s^T mu + sdot^T nu, sbar = mu B^T, ..., exactly as the directed
+// kernels (edge_tc.cuh msg_bf_tc / msg_be_tc) but with no w / w' MMAs: the
+// per-row sums use the stored filters (msg_bf_rows / msg_be_rows).
+// Persistent CTAs, static chunk assignment => deterministic partials.
+__global__ void __launch_bounds__(NT, 1) msg_bf_pair_tc(EdgeGeom g, const int* __restrict__ pcanon, int n_pairs, MsgParams p,
+                                                       float rc, const float* __restrict__ v, const float* __restrict__ vdot,
+                                                       const float* __restrict__ am, const float* __restrict__ Fbar,
+                                                       float* __restrict__ partial) {
+  extern __shared__ __align__(1024) uint8_t sm_raw[];
+  uint8_t* sm = align1024(sm_raw);
+  uint8_t* W2b = sm;  // bf16 weights in pack order: B | A^T | B^T
+  uint8_t* W0b = W2b + kW2bBytes;
+  uint8_t* W1b = W0b + kW2bBytes;
+  (void)W1b;
+  uint8_t* B0 = sm + 2 * kWTile;  // bf16: s          (write_partial scratch: B0..B2)
+  uint8_t* B1 = B0 + kBTile;      //       sdot
+  uint8_t* B2 = B1 + kBTile;      //       mu, then zbar
+  uint8_t* B3 = B2 + kBTile;      //       nu, then zbar'
+  uint8_t* B4 = B3 + kBTile;      //       phi
+  uint8_t* B5 = B4 + kBTile;      //       phi'
+  float* al = reinterpret_cast<float*>(B5 + kBTile);
+  float* be = al + 64;
+  float* csa = be + 64;
+  float* csb = csa + 64;
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tslot;
+  __shared__ __align__(8) uint64_t wbar;
+  Ctx c;
+  c.sm = sm;
+  c.mbar = &mbar;
+  load_weights_b16(W2b, p.pack, al, be, &wbar);
+  if (threadIdx.x < 128) csa[threadIdx.x] = 0.f;
+  setup(c, &tslot, 512);
+  const uint32_t aW0b = tc::smem_u32(W0b), aW2b = tc::smem_u32(W2b);
+  const uint32_t aB0 = tc::smem_u32(B0), aB1 = tc::smem_u32(B1), aB2 = tc::smem_u32(B2), aB3 = tc::smem_u32(B3);
+  const uint32_t aB4 = tc::smem_u32(B4), aB5 = tc::smem_u32(B5);
+  bool first = true;
+  const int f0 = FPT * c.q;
+  for (int ch = blockIdx.x; ch * TE < n_pairs; ch += gridDim.x) {
+    const int pp = ch * TE + c.e;
+    const bool ok = pp < n_pairs;
+    const int x = ok ? __ldg(pcanon + pp) : 0;
+    const float d = ok ? __ldg(g.d + x) : 0.f, cc = ok ? __ldg(g.c + x) : 0.f, dc = ok ? __ldg(g.dc + x) : 0.f;
+    const int i = ok ? __ldg(g.src + x) : 0, j = ok ? __ldg(g.col + x) : 0;
+    {
+      float ph[FPT], dph[FPT];
+      basis(d, rc, f0, ph, dph);
+      st_b16(B4, c.e, f0, ph);
+      st_b16(B5, c.e, f0, dph);
+    }
+    tc::mbar_wait(&wbar, 0);
+    c.publish();
+    if (threadIdx.x == 0) {
+      mma_kb16(c.tmem + TM_Z, aB4, aW0b);
+      mma_kb16(c.tmem + TM_ZP, aB5, aW0b);
+      tc::commit(c.mbar);
+    }
+    float qb = 0.f;  // <Fbar_i - Fbar_j, u_x>; its loads and the gathers overlap the MMAs
+    if (ok)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) qb = fmaf(__ldg(Fbar + 3 * i + k) - __ldg(Fbar + 3 * j + k), __ldg(g.u + 3 * x + k), qb);
+    float rho[FPT], kap[FPT];
+    {
+      float ai[FPT], aj[FPT], vi[FPT], vj[FPT];
+      gather32(am, i, f0, ai);
+      gather32(am, j, f0, aj);
+      gather32(v, i, f0, vi);
+      gather32(v, j, f0, vj);
+#pragma unroll
+      for (int k = 0; k < FPT; ++k) rho[k] = fmaf(ai[k], vj[k], aj[k] * vi[k]);
+      gather32(vdot, i, f0, vi);
+      gather32(vdot, j, f0, vj);
+#pragma unroll
+      for (int k = 0; k < FPT; ++k) kap[k] = fmaf(ai[k], vj[k], aj[k] * vi[k]);
+    }
+    c.wait_mma();
+    {
+      float z[FPT], zp[FPT];
+      c.ld2(TM_Z, TM_ZP, z, zp);
+#pragma unroll
+      for (int k = 0; k < FPT; ++k) {
+        const float zz = z[k] + al[f0 + k], s1 = fsig(zz);
+        z[k] = zz * s1;
+        zp[k] = s1 * (1.0f + zz * (1.0f - s1)) * zp[k];
+      }
+      st_b16(B0, c.e, f0, z);   // s
+      st_b16(B1, c.e, f0, zp);  // sdot
+#pragma unroll
+      for (int k = 0; k < FPT; ++k) {
+        const float r = rho[k];
+        rho[k] = qb * dc * r + cc * kap[k];  // mu
+        kap[k] = qb * cc * r;                // nu
+      }
+      st_b16(B2, c.e, f0, rho);
+      st_b16(B3, c.e, f0, kap);
+    }
+    c.publish();
+    if (threadIdx.x == 0) {  // dB += s^T mu + sdot^T nu; sbar = mu B^T, sdotbar = nu B^T
+      mma_wg_b16(c.tmem + TM_BG, aB0, aB2, !first);
+      mma_wg_b16(c.tmem + TM_BG, aB1, aB3, true);
+      mma_kb16(c.tmem + TM_G, aB2, aW2b);
+      mma_kb16(c.tmem + TM_GP, aB3, aW2b);
+      tc::commit(c.mbar);
+    }
+    b16_colsum_add(B2, csb);  // dbeta += sum mu
+    c.wait_mma();
+    __syncthreads();  // column sums done: B2, B3 may be rewritten
+    {
+      float z[FPT], zp[FPT], sb[FPT], sdb[FPT];
+      c.ld2(TM_Z, TM_ZP, z, zp);
+      c.ld2(TM_G, TM_GP, sb, sdb);
+#pragma unroll
+      for (int k = 0; k < FPT; ++k) {
+        const float zz = z[k] + al[f0 + k], s1 = fsig(zz);
+        const float ds = s1 * (1.0f + zz * (1.0f - s1));
+        const float d2s = s1 * (1.0f - s1) * (2.0f + zz * (1.0f - 2.0f * s1));
+        z[k] = sb[k] * ds + sdb[k] * d2s * zp[k];  // zbar
+        zp[k] = sdb[k] * ds;                       // zbar'
+      }
+      st_b16(B2, c.e, f0, z);
+      st_b16(B3, c.e, f0, zp);
+    }
+    c.publish();
+    if (threadIdx.x == 0) {  // dA += phi^T zbar + phi'^T zbar'
+      mma_wg_b16(c.tmem + TM_AG, aB4, aB2, !first);
+      mma_wg_b16(c.tmem + TM_AG, aB5, aB3, true);
+      tc::commit(c.mbar);
+    }
+    b16_colsum_add(B2, csa);  // dalpha += sum zbar
+    c.wait_mma();
+    first = false;
+    __syncthreads();
+  }
+  float* part = partial + (size_t)blockIdx.x * PE;
+  if (first) {
+    for (int x = threadIdx.x; x < PE; x += NT) part[x] = 0.f;
+    teardown(c, 512);
+    return;
+  }
+  write_partial(c, part, B0, csa, csb);
+  teardown(c, 512);
+}
+
+__global__ void __launch_bounds__(NT, 1) msg_be_pair_tc(EdgeGeom g, const int* __restrict__ pcanon, int n_pairs, MsgParams p,
+                                                       float rc, const float* __restrict__ v, const float* __restrict__ bm,
+                                                       float* __restrict__ partial) {
+  extern __shared__ __align__(1024) uint8_t sm_raw[];
+  uint8_t* sm = align1024(sm_raw);
+  uint8_t* W2b = sm;
+  uint8_t* W0b = W2b + kW2bBytes;
+  uint8_t* B0 = sm + 2 * kWTile;  // bf16: phi     (write_partial scratch: B0..B2)
+  uint8_t* B1 = B0 + kBTile;      //       s
+  uint8_t* B2 = B1 + kBTile;      //       gbar
+  uint8_t* B3 = B2 + kBTile;      //       zbar
+  float* al = reinterpret_cast<float*>(B3 + kBTile);
+  float* be = al + 64;
+  float* csa = be + 64;
+  float* csb = csa + 64;
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tslot;
+  __shared__ __align__(8) uint64_t wbar;
+  Ctx c;
+  c.sm = sm;
+  c.mbar = &mbar;
+  load_weights_b16(W2b, p.pack, al, be, &wbar);
+  if (threadIdx.x < 128) csa[threadIdx.x] = 0.f;
+  setup(c, &tslot, 512);
+  const uint32_t aW0b = tc::smem_u32(W0b), aW2b = tc::smem_u32(W2b);
+  const uint32_t aB0 = tc::smem_u32(B0), aB1 = tc::smem_u32(B1), aB2 = tc::smem_u32(B2), aB3 = tc::smem_u32(B3);
+  bool first = true;
+  const int f0 = FPT * c.q;
+  for (int ch = blockIdx.x; ch * TE < n_pairs; ch += gridDim.x) {
+    const int pp = ch * TE + c.e;
+    const bool ok = pp < n_pairs;
+    const int x = ok ? __ldg(pcanon + pp) : 0;
+    const float d = ok ? __ldg(g.d + x) : 0.f, cc = ok ? __ldg(g.c + x) : 0.f;
+    const int i = ok ? __ldg(g.src + x) : 0, j = ok ? __ldg(g.col + x) : 0;
+    {
+      float ph[FPT], dph[FPT];
+      basis(d, rc, f0, ph, dph);
+      st_b16(B0, c.e, f0, ph);
+    }
+    tc::mbar_wait(&wbar, 0);
+    c.publish();
+    if (threadIdx.x == 0) {
+      mma_kb16(c.tmem + TM_Z, aB0, aW0b);
+      tc::commit(c.mbar);
+    }
+    float gb[FPT];
+    {
+      float bi[FPT], bj[FPT], vi[FPT], vj[FPT];
+      gather32(bm, i, f0, bi);
+      gather32(bm, j, f0, bj);
+      gather32(v, i, f0, vi);
+      gather32(v, j, f0, vj);
+#pragma unroll
+      for (int k = 0; k < FPT; ++k) gb[k] = cc * fmaf(bi[k], vj[k], bj[k] * vi[k]);  // zero on padding (c = 0)
+    }
+    c.wait_mma();
+    {
+      float z[FPT];
+      c.ld(TM_Z, z);
+#pragma unroll
+      for (int k = 0; k < FPT; ++k) {
+        const float zz = z[k] + al[f0 + k];
+        z[k] = zz * fsig(zz);
+      }
+      st_b16(B1, c.e, f0, z);  // s
+      st_b16(B2, c.e, f0, gb);
+    }
+    c.publish();
+    if (threadIdx.x == 0) {
+      mma_wg_b16(c.tmem + TM_BG, aB1, aB2, !first);  // dB += s^T gbar
+      mma_kb16(c.tmem + TM_G, aB2, aW2b);            // sbar = gbar B^T
+      tc::commit(c.mbar);
+    }
+    b16_colsum_add(B2, csb);  // dbeta += sum gbar
+    c.wait_mma();
+    {
+      float z[FPT], sb[FPT];
+      c.ld2(TM_Z, TM_G, z, sb);
+#pragma unroll
+      for (int k = 0; k < FPT; ++k) {
+        const float zz = z[k] + al[f0 + k], s1 = fsig(zz);
+        z[k] = sb[k] * (s1 * (1.0f + zz * (1.0f - s1)));
+      }
+      st_b16(B3, c.e, f0, z);  // zbar
+    }
+    c.publish();
+    if (threadIdx.x == 0) {
+      mma_wg_b16(c.tmem + TM_AG, aB0, aB3, !first);  // dA += phi^T zbar
+      tc::commit(c.mbar);
+    }
+    b16_colsum_add(B3, csa);  // dalpha += sum zbar
+    c.wait_mma();
+    first = false;
+    __syncthreads();
+  }
+  float* part = partial + (size_t)blockIdx.x * PE;
+  if (first) {
+    for (int x = threadIdx.x; x < PE; x += NT) part[x] = 0.f;
+    teardown(c, 512);
+    return;
+  }
+  write_partial(c, part, B0, csa, csb);
+  teardown(c, 512);
+}
+
+// BF rows: mdot_i = sum_e qb_e w'_p v_j + w_p vdot_j ; X_i = sum_e qb_e w'_p am_j ;
+// inj = X W^T (hbar^F of the unit input), qb_e = <Fbar_i - Fbar_j, u_e>
+__global__ void __launch_bounds__(256) msg_bf_rows(int n_atoms, const int* __restrict__ row_ptr, const int* __restrict__ col,
+                                                   const int* __restrict__ pidx, const float* __restrict__ uvec,
+                                                   const float* __restrict__ Fbar, const float* __restrict__ w,
+                                                   const float* __restrict__ wp, const float* __restrict__ v,
+                                                   const float* __restrict__ vdot, const float* __restrict__ am,
+                                                   const float* __restrict__ wt, float* __restrict__ mdot_out,
+                                                   float* __restrict__ X_out, float* __restrict__ inj) {
+  const int i = blockIdx.x * 8 + static_cast<int>(threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (i >= n_atoms) return;
+  const int eb = __ldg(row_ptr + i), ee = __ldg(row_ptr + i + 1);
+  const float fi0 = __ldg(Fbar + 3 * i), fi1 = __ldg(Fbar + 3 * i + 1), fi2 = __ldg(Fbar + 3 * i + 2);
+  float2 md = make_float2(0.f, 0.f), X = make_float2(0.f, 0.f);
+  for (int e0 = eb; e0 < ee; e0 += 32) {
+    const int n = min(32, ee - e0);
+    int mp = 0, mj = 0;
+    float mq = 0.f;
+    if (lane < n) {
+      const int e = e0 + lane;
+      mp = __ldg(pidx + e);
+      mj = __ldg(col + e);
+      mq = fmaf(fi0 - __ldg(Fbar + 3 * mj), __ldg(uvec + 3 * e), 0.f);
+      mq = fmaf(fi1 - __ldg(Fbar + 3 * mj + 1), __ldg(uvec + 3 * e + 1), mq);
+      mq = fmaf(fi2 - __ldg(Fbar + 3 * mj + 2), __ldg(uvec + 3 * e + 2), mq);
+    }
+    for (int k0 = 0; k0 < n; k0 += 8) {
+      float2 a[8], b[8], vv[8], dv[8], aj[8];
+      float q[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int pk = __shfl_sync(0xffffffffu, mp, k0 + k), jk = __shfl_sync(0xffffffffu, mj, k0 + k);
+        q[k] = __shfl_sync(0xffffffffu, mq, k0 + k);
+        a[k] = __ldg(reinterpret_cast<const float2*>(w + (size_t)pk * H) + lane);
+        b[k] = __ldg(reinterpret_cast<const float2*>(wp + (size_t)pk * H) + lane);
+        vv[k] = __ldg(reinterpret_cast<const float2*>(v + (size_t)jk * H) + lane);
+        dv[k] = __ldg(reinterpret_cast<const float2*>(vdot + (size_t)jk * H) + lane);
+        aj[k] = __ldg(reinterpret_cast<const float2*>(am + (size_t)jk * H) + lane);
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (k0 + k < n) {
+          const float px = q[k] * b[k].x, py = q[k] * b[k].y;
+          md.x = fmaf(px, vv[k].x, fmaf(a[k].x, dv[k].x, md.x));
+          md.y = fmaf(py, vv[k].y, fmaf(a[k].y, dv[k].y, md.y));
+          X.x = fmaf(px, aj[k].x, X.x);
+          X.y = fmaf(py, aj[k].y, X.y);
+        }
+    }
+  }
+  reinterpret_cast<float2*>(mdot_out + (size_t)i * H)[lane] = md;
+  reinterpret_cast<float2*>(X_out + (size_t)i * H)[lane] = X;
+  if (inj) reinterpret_cast<float2*>(inj + (size_t)i * H)[lane] = row_times_wt(X, wt, lane);
+}
+
+// BE rows: Yb_i = sum_e w_p bm_j ; b_h += Yb W^T + inj
+__global__ void __launch_bounds__(256) msg_be_rows(int n_atoms, const int* __restrict__ row_ptr, const int* __restrict__ col,
+                                                   const int* __restrict__ pidx, const float* __restrict__ w,
+                                                   const float* __restrict__ bm, const float* __restrict__ wt,
+                                                   float* __restrict__ Yb_out, const float* __restrict__ inj, float* bh) {
+  const int i = blockIdx.x * 8 + static_cast<int>(threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (i >= n_atoms) return;
+  const int eb = __ldg(row_ptr + i), ee = __ldg(row_ptr + i + 1);
+  float2 acc = make_float2(0.f, 0.f);
+  for (int e0 = eb; e0 < ee; e0 += 32) {
+    const int n = min(32, ee - e0);
+    const int mp = lane < n ? __ldg(pidx + e0 + lane) : 0;
+    const int mj = lane < n ? __ldg(col + e0 + lane) : 0;
+    for (int k0 = 0; k0 < n; k0 += 8) {
+      float2 a[8], b[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int pk = __shfl_sync(0xffffffffu, mp, k0 + k), jk = __shfl_sync(0xffffffffu, mj, k0 + k);
+        a[k] = __ldg(reinterpret_cast<const float2*>(w + (size_t)pk * H) + lane);
+        b[k] = __ldg(reinterpret_cast<const float2*>(bm + (size_t)jk * H) + lane);
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (k0 + k < n) {
+          acc.x = fmaf(a[k].x, b[k].x, acc.x);
+          acc.y = fmaf(a[k].y, b[k].y, acc.y);
+        }
+    }
+  }
+  reinterpret_cast<float2*>(Yb_out + (size_t)i * H)[lane] = acc;
+  if (bh) {
+    const float2 o = row_times_wt(acc, wt, lane);
+    const float2 in = inj ? __ldg(reinterpret_cast<const float2*>(inj + (size_t)i * H) + lane) : make_float2(0.f, 0.f);
+    float2* dst = reinterpret_cast<float2*>(bh + (size_t)i * H) + lane;
+    float2 x = *dst;
+    x.x += o.x + in.x;
+    x.y += o.y + in.y;
+    *dst = x;
+  }
+}
+
+constexpr size_t bf_pair_smem() { return 2 * kWTile + 6 * kBTile + kSmallBytes; }
+constexpr size_t be_pair_smem() { return 2 * kWTile + 4 * kBTile + kSmallBytes; }
 constexpr size_t filter_smem() { return 2 * kWTile + 2 * kTile + kSmallBytes; }
 
 }  // namespace edge_tc

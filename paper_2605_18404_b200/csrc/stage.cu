@@ -248,6 +248,11 @@ bool use_tc(const janus_stage* st) { return st->m.precision == JANUS_PREC_TF32; 
 // pipeline (1 lane) keeps one tile per CTA.
 int tc_grid_tpc(const DevGeo& g, int tpc) { return std::max(1, std::min((g.n_tiles_tc + tpc - 1) / tpc, 148)); }
 int tc_grid(const janus_stage* st, const DevGeo& g) { return tc_grid_tpc(g, st->tpc_wg); }
+// BF / BE per pair: persistent CTAs, tpc_wg 128-pair chunks each
+int pair_grid(const janus_stage* st, const DevGeo& g) {
+  const int chunks = (g.n_pairs + edge_tc::TE - 1) / edge_tc::TE;
+  return std::max(1, std::min((chunks + st->tpc_wg - 1) / st->tpc_wg, 148));
+}
 int fe_grid(const janus_stage* st, const DevGeo& g) {
   return std::max(1, (g.n_tiles_tc + st->tpc_fe - 1) / st->tpc_fe);
 }
@@ -429,6 +434,8 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
     if (const char* e = std::getenv("JANUS_TPC_FE")) st->tpc_fe = std::max(1, std::atoi(e));  // tuning runs only
     if (const char* e = std::getenv("JANUS_TPC_WG")) st->tpc_wg = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("JANUS_FEFF_PAIR")) st->pair_feff = std::atoi(e) != 0;  // A/B runs only
+    st->pair_bfbe = st->pair_feff;
+    if (const char* e = std::getenv("JANUS_BFBE_PAIR")) st->pair_bfbe = st->pair_feff && std::atoi(e) != 0;
     for (Scratch& sc : st->lanes) {
       sc.wh = dalloc<float>(st, NH, false);
       sc.wm = dalloc<float>(st, NH, false);
@@ -451,6 +458,8 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
     JANUS_CUDA(cudaFuncSetAttribute(edge_tc::msg_fe_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge_tc::fe_smem()));
     JANUS_CUDA(cudaFuncSetAttribute(edge_tc::msg_ff_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge_tc::ff_smem()));
     JANUS_CUDA(cudaFuncSetAttribute(edge_tc::msg_filter_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge_tc::filter_smem()));
+    JANUS_CUDA(cudaFuncSetAttribute(edge_tc::msg_bf_pair_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge_tc::bf_pair_smem()));
+    JANUS_CUDA(cudaFuncSetAttribute(edge_tc::msg_be_pair_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge_tc::be_pair_smem()));
     JANUS_CUDA(cudaFuncSetAttribute(edge_tc::msg_bf_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge_tc::bf_smem()));
     JANUS_CUDA(cudaFuncSetAttribute(edge_tc::msg_be_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge_tc::be_smem()));
     refresh_transposes(st, nullptr);
@@ -868,7 +877,20 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
       case kMsg: {
         const float* W = P + R * H + H + H * H + H;
         gemm(s, N, ah, W, nullptr, nullptr, nullptr, sc.s1);  // vdot
-        if (g.n_tiles > 0 && use_tc(st)) {
+        const bool pairs = use_tc(st) && st->pair_bfbe;
+        if (pairs) {  // weight gradients once per pair + row sums from the stored filters (+ hbar^F = X W^T)
+          const int grid = pair_grid(st, g);
+          const MsgParams mp = msg_params(st, u);
+          if (g.n_pairs > 0 && !(prof_skip() & 4)) {
+            edge_tc::msg_bf_pair_tc<<<grid, edge_tc::NT, edge_tc::bf_pair_smem(), s>>>(eg, g.pcanon, g.n_pairs, mp, st->m.r_c, b.v,
+                                                                                       sc.s1, b.ff_a, Fbar, sc.partial);
+            JANUS_LAUNCH_CHECK("msg_bf_pair_tc");
+          }
+          if (g.n_pairs > 0 && !(prof_skip() & 128)) edge::reduce_partials_kernel<<<edge::reduce_grid(EC::PE), 256, 0, s>>>(sc.partial, grid, EC::PE, G2);
+          if (!(prof_skip() & 4))
+            edge_tc::msg_bf_rows<<<blocks(N, 8), 256, 0, s>>>(N, g.row_ptr, g.col, g.pidx, g.u, Fbar, b.wf, b.wfp, b.v, sc.s1, b.ff_a,
+                                                               mp.pack + edge_tc::kWtOff / sizeof(float), am, sc.s2, b.inj);
+        } else if (g.n_tiles > 0 && use_tc(st)) {
           const int grid = tc_grid(st, g);
           if (!(prof_skip() & 4)) edge_tc::msg_bf_tc<<<grid, edge_tc::NT, edge_tc::bf_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, msg_params(st, u),
                                                                           st->m.r_c, b.v, sc.s1, b.ff_a, Fbar, am, sc.s2,
@@ -884,7 +906,7 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
           JANUS_CUDA(cudaMemsetAsync(am, 0, sizeof(float) * NH, s));
           JANUS_CUDA(cudaMemsetAsync(sc.s2, 0, sizeof(float) * NH, s));
         }
-        if (!(g.n_tiles > 0 && use_tc(st))) gemm(s, N, sc.s2, T + H * H, nullptr, nullptr, nullptr, b.inj);  // hbar^F = X W^T
+        if (!pairs && !(g.n_tiles > 0 && use_tc(st))) gemm(s, N, sc.s2, T + H * H, nullptr, nullptr, nullptr, b.inj);  // hbar^F = X W^T
         wjobs(st, sc, s, N, {wjob(in_h(st, sl, u, N), sc.s2, G2 + EC::PE, ah, b.ff_Y)});  // dW2 = h^T X + abar^T Y
         break;
       }
@@ -970,7 +992,20 @@ void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only, 
         break;
       }
       case kMsg: {
-        if (g.n_tiles > 0 && use_tc(st)) {
+        const bool pairs = use_tc(st) && st->pair_bfbe;
+        if (pairs) {
+          const int grid = pair_grid(st, g);
+          const MsgParams mp = msg_params(st, u);
+          if (g.n_pairs > 0 && !(prof_skip() & 8)) {
+            edge_tc::msg_be_pair_tc<<<grid, edge_tc::NT, edge_tc::be_pair_smem(), s>>>(eg, g.pcanon, g.n_pairs, mp, st->m.r_c, b.v, bm,
+                                                                                       sc.partial);
+            JANUS_LAUNCH_CHECK("msg_be_pair_tc");
+          }
+          if (g.n_pairs > 0 && !(prof_skip() & 128)) edge::reduce_partials_kernel<<<edge::reduce_grid(EC::PE), 256, 0, s>>>(sc.partial, grid, EC::PE, G1);
+          if (!(prof_skip() & 8))  // Yb; b_h += Yb W^T + hbar^F
+            edge_tc::msg_be_rows<<<blocks(N, 8), 256, 0, s>>>(N, g.row_ptr, g.col, g.pidx, b.wf, bm,
+                                                               mp.pack + edge_tc::kWtOff / sizeof(float), sc.s1, b.inj, bh);
+        } else if (g.n_tiles > 0 && use_tc(st)) {
           const int grid = tc_grid(st, g);
           if (!(prof_skip() & 8)) edge_tc::msg_be_tc<<<grid, edge_tc::NT, edge_tc::be_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, msg_params(st, u),
                                                                           st->m.r_c, b.v, bm, sc.s1, sc.partial,
@@ -986,7 +1021,7 @@ void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only, 
           JANUS_CUDA(cudaMemsetAsync(sc.s1, 0, sizeof(float) * NH, s));
         }
         wjobs(st, sc, s, N, {wjob(in_h(st, sl, u, N), sc.s1, G1 + EC::PE)});  // dW1 = h^T Yb
-        if (!(g.n_tiles > 0 && use_tc(st))) gemm(s, N, sc.s1, T + H * H, nullptr, bh, b.inj, bh);  // b_h += Yb W^T + hbar^F
+        if (!pairs && !(g.n_tiles > 0 && use_tc(st))) gemm(s, N, sc.s1, T + H * H, nullptr, bh, b.inj, bh);  // b_h += Yb W^T + hbar^F
         break;
       }
       case kEmbed:
@@ -1056,9 +1091,16 @@ void stage_port(janus_stage* st, int mb, int slot, int port, void** dptr, size_t
 // and FF's per-edge MMAs once per pair, i.e. half of FF's per-edge flops per
 // directed edge) + FE's row sums; "FF" = the row kernel (Y, force scalar, and
 // the a_h += Y W^T row GEMM counted per edge at ~50 edges per row is < 3%: omitted).
+// BF / BE per pair: z, z', dB(2), sbar, sdotbar, dA(2) = 4RH + 4H^2 and
+// z, dB, sbar, dA = 2RH + 2H^2 per PAIR (half per directed edge) + row sums.
 double pair_flops_per_edge(int which, int H, int R) {
   const double RH = static_cast<double>(R) * H, HH = static_cast<double>(H) * H;
-  return which == 0 ? 0.5 * 2.0 * (2 * RH + 2 * HH + H) + 2.0 * H : 2.0 * (3 * H);
+  switch (which) {
+    case 0: return 0.5 * 2.0 * (2 * RH + 2 * HH + H) + 2.0 * H;
+    case 1: return 2.0 * (3 * H);
+    case 2: return 0.5 * 2.0 * (4 * RH + 4 * HH) + 2.0 * (3 * H);
+    default: return 0.5 * 2.0 * (2 * RH + 2 * HH) + 2.0 * H;
+  }
 }
 
 double edge_kernel_flops_per_edge(int which, int H, int R) {
@@ -1089,6 +1131,24 @@ void launch_edge_kernel(janus_stage* st, int u, int which, int mb, int slot, int
     } else {
       edge_tc::msg_ff_rows<<<blocks(N, 8), 256, 0, s>>>(N, g.row_ptr, g.col, g.pidx, g.u, b.wf, b.wfp, b.v, b.ff_a,
                                                          mp.pack + edge_tc::kWtOff / sizeof(float), sc.s3, sc.s5, sc.s4);
+    }
+    return;
+  }
+  if (use_tc(st) && st->pair_bfbe) {  // which 2 / 3: pair kernel (weight gradients) + row kernel
+    const int N = g.n_atoms;
+    const int grid = step_grid ? pair_grid(st, g) : std::max(1, std::min((g.n_pairs + edge_tc::TE - 1) / edge_tc::TE, 148));
+    const float* wt = mp.pack + edge_tc::kWtOff / sizeof(float);
+    if (which == 2) {
+      if (g.n_pairs > 0)
+        edge_tc::msg_bf_pair_tc<<<grid, edge_tc::NT, edge_tc::bf_pair_smem(), s>>>(eg, g.pcanon, g.n_pairs, mp, st->m.r_c, b.v, sc.s1,
+                                                                                   b.ff_a, sl.Fbar, sc.partial);
+      edge_tc::msg_bf_rows<<<blocks(N, 8), 256, 0, s>>>(N, g.row_ptr, g.col, g.pidx, g.u, sl.Fbar, b.wf, b.wfp, b.v, sc.s1, b.ff_a, wt,
+                                                         sc.s3, sc.s4, nullptr);
+    } else {
+      if (g.n_pairs > 0)
+        edge_tc::msg_be_pair_tc<<<grid, edge_tc::NT, edge_tc::be_pair_smem(), s>>>(eg, g.pcanon, g.n_pairs, mp, st->m.r_c, b.v, sc.s2,
+                                                                                   sc.partial);
+      edge_tc::msg_be_rows<<<blocks(N, 8), 256, 0, s>>>(N, g.row_ptr, g.col, g.pidx, b.wf, sc.s2, wt, sc.s3, nullptr, nullptr);
     }
     return;
   }
@@ -1130,7 +1190,8 @@ void launch_edge_kernel(janus_stage* st, int u, int which, int mb, int slot, int
 }
 
 double kernel_flops_per_edge(const janus_stage* st, int which) {
-  return use_tc(st) && st->pair_feff && which < 2 ? pair_flops_per_edge(which, kH, kR) : edge_kernel_flops_per_edge(which, kH, kR);
+  const bool pairs = use_tc(st) && (which < 2 ? st->pair_feff : st->pair_bfbe);
+  return pairs ? pair_flops_per_edge(which, kH, kR) : edge_kernel_flops_per_edge(which, kH, kR);
 }
 
 int first_msg_unit(const janus_stage* st) {
