@@ -39,6 +39,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CONFIG = dict(L=4, H=64, R=64, r_c=5.0, atoms=256, rho=0.095, n_mb=32, seed=7)
+# per-layer edge-contraction FLOPs of the directed-edge algorithm, FE + FF + BF + BE
+# (stage.cu edge_kernel_flops_per_edge)
+DIRECTED_FLOP_PER_EDGE = 2.0 * ((64 * 64 + 64 * 64) + (2 * 64 * 64 + 2 * 64 * 64 + 64) + (4 * 64 * 64 + 6 * 64 * 64)
+                                + (2 * 64 * 64 + 3 * 64 * 64))
 METRIC = "structures/sec"
 
 
@@ -48,7 +52,7 @@ def load_traffic(precision):
     try:
         with open(os.path.join(ROOT, "profiles", "r01_roofline_traffic.json")) as f:
             t = json.load(f)
-        return t["dram_bytes_per_launch"] if precision == "tf32" and t.get("kernel", "").endswith("msg_bf_tc") else None
+        return t["dram_bytes_per_launch"] if precision == "tf32" and t.get("kernel", "").endswith("msg_bf_pair_tc") else None
     except (OSError, ValueError, KeyError):
         return None
 
@@ -332,39 +336,49 @@ def main():
               + b.F_target.nbytes + 4 * (b.n_atoms + 1) for b in batches)
     d2h_lm = sum(4 * (b.n_atoms + 1) + 8 for b in batches)  # row_ptr mirror + edge count / status
 
-    # roofline of the dominant kernel (msg BF edge kernel) on the first stage holding a msg unit
+    # roofline of the dominant edge kernel on the first stage holding a msg unit
     peaks, peak_src = load_peaks()
     roof = None
     if rank == 0:
         st = tr.stage(0 if P == 1 else min(1, P - 1))
         try:
-            # dominant kernel = msg BF (33% of the step, profiles/r01_step_attribution.txt), timed
-            # with the step's concurrency: all 32 micro-batches launched on the 16 lanes with the
-            # step's grid (tiles per CTA), CUDA events around whole rounds (P == 1; else isolated)
+            # tf32 path: msg_bf_pair_tc (BF weight gradients once per undirected edge pair;
+            # the largest edge kernel of the step, profiles/r01_launch_shares_tf32_v14.txt),
+            # timed with the step's concurrency: all micro-batches launched on the step's lanes
+            # with the step's grid, CUDA events around whole rounds (P == 1; else isolated)
+            wk = 4 if args.precision == "tf32" else 2
             if P == 1:
-                ms_bf, ne, fl = st.time_edge_kernel(2, -1, iters=20)
+                ms_bf, ne, fl = st.time_edge_kernel(wk, -1, iters=20)
                 how = "all micro-batches per round on the step's lanes and grids (CUDA events per round)"
             else:
-                ms_bf, ne, fl = st.time_edge_kernel(2, 0, iters=50)
+                ms_bf, ne, fl = st.time_edge_kernel(wk, 0, iters=50)
                 how = "one micro-batch, back-to-back launches"
             achieved = fl / (ms_bf * 1e-3) / 1e12
-            iso_ms, iso_e, iso_fl = st.time_edge_kernel(2, 0, iters=50)
-            roof = {"kernel": "msg_bf_tc (tcgen05 kind::tf32)" if args.precision == "tf32" else "msg_bf_kernel (SIMT fp32)",
+            iso_ms, iso_e, iso_fl = st.time_edge_kernel(wk, 0, iters=50)
+            roof = {"kernel": ("msg_bf_pair_tc (tcgen05 kind::f16, bf16 operands, fp32 accumulate; per edge pair)"
+                               if args.precision == "tf32" else "msg_bf_kernel (SIMT fp32)"),
                     "bound": "tensor", "achieved": achieved,
                     "peak": peaks["bf16_tflops"], "unit": "TFLOP/s", "frac": achieved / peaks["bf16_tflops"],
                     "traffic": load_traffic(args.precision), "peak_source": f"{peak_src} bf16 dense (MEASURED_PEAKS.json)",
                     "timing": how, "round_ms": ms_bf, "edges_per_round": ne, "flops_per_round": fl,
+                    "flops_note": "executed MMA flops: (4RH + 4H^2) x 2 per edge pair = half of that per directed edge",
                     "isolated_launch_ms": iso_ms, "isolated_tflops": iso_fl / (iso_ms * 1e-3) / 1e12,
                     "fp32_simt_nominal_tflops": 74.4}
             fe = st.time_edge_kernel(0, 0, iters=50)
             roof["fe_kernel_tflops"] = fe[2] / (fe[0] * 1e-3) / 1e12
-            # step level: algorithmic edge-contraction FLOPs of all four phases,
-            # every layer and micro-batch, over the device-timed step
-            fl_all = iso_fl + fe[2] + sum(st.time_edge_kernel(w, 0, iters=5)[2] for w in (1, 3))
+            # step level: executed edge-contraction FLOPs of all four phases (pair mode:
+            # once per pair), every layer and micro-batch, over the device-timed step; and
+            # the directed-edge algorithm's count (every contraction per directed edge,
+            # DESIGN.md §4) over the same time = the rate that algorithm would need
+            per_mb = [st.time_edge_kernel(w, 0, iters=5) for w in (0, 1, 2, 3)]
+            fl_all = sum(x[2] for x in per_mb)
             if P == 1:
                 roof["step_edge_flops"] = fl_all * CONFIG["L"] * n_mb
                 roof["step_edge_tflops"] = roof["step_edge_flops"] / (ms_per_step * 1e-3) / 1e12
                 roof["step_edge_frac"] = roof["step_edge_tflops"] / peaks["bf16_tflops"]
+                e_mb = per_mb[0][1]
+                roof["directed_equiv_step_tflops"] = (DIRECTED_FLOP_PER_EDGE * e_mb * CONFIG["L"] * n_mb
+                                                      / (ms_per_step * 1e-3) / 1e12)
         except J.JanusError as ex:
             roof = {"error": str(ex)}
 

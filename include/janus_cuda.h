@@ -155,7 +155,9 @@ int janus_stage_grad_buffer(janus_stage* st, float** dptr, int64_t* count);
 int janus_stage_optimizer_step(janus_stage* st, const janus_opt* opt, void* stream);
 /* Time one edge kernel of the stage's first msg unit in isolation (CUDA
  * events on `stream`, back-to-back launches after one warm-up): which = 0 FE,
- * 1 FF, 2 BF, 3 BE.  Requires the phase's inputs to exist (run the step once
+ * 1 FF, 2 BF, 3 BE (tensor-core pair mode: 0 = filter + FE rows, 1 = FF rows,
+ * 2 / 3 = pair weight-gradient kernel + row kernel), 4 / 5 = the BF / BE pair
+ * weight-gradient kernel alone (pair mode only).  Requires the phase's inputs to exist (run the step once
  * first).  Returns the mean launch time, the launch's edge count and
  * algorithmic FLOPs (DESIGN.md §4 per-edge counts).  mb < 0: the step's
  * concurrency instead — every micro-batch (slot = mb) launched on lane

@@ -1134,10 +1134,17 @@ void launch_edge_kernel(janus_stage* st, int u, int which, int mb, int slot, int
     }
     return;
   }
-  if (use_tc(st) && st->pair_bfbe) {  // which 2 / 3: pair kernel (weight gradients) + row kernel
+  if (use_tc(st) && st->pair_bfbe) {  // which 2 / 3: pair kernel (weight gradients) + row kernel; 4 / 5: pair kernel alone
     const int N = g.n_atoms;
     const int grid = step_grid ? pair_grid(st, g) : std::max(1, std::min((g.n_pairs + edge_tc::TE - 1) / edge_tc::TE, 148));
     const float* wt = mp.pack + edge_tc::kWtOff / sizeof(float);
+    if (which == 4 && g.n_pairs > 0)
+      edge_tc::msg_bf_pair_tc<<<grid, edge_tc::NT, edge_tc::bf_pair_smem(), s>>>(eg, g.pcanon, g.n_pairs, mp, st->m.r_c, b.v, sc.s1,
+                                                                                 b.ff_a, sl.Fbar, sc.partial);
+    if (which == 5 && g.n_pairs > 0)
+      edge_tc::msg_be_pair_tc<<<grid, edge_tc::NT, edge_tc::be_pair_smem(), s>>>(eg, g.pcanon, g.n_pairs, mp, st->m.r_c, b.v, sc.s2,
+                                                                                 sc.partial);
+    if (which >= 4) return;
     if (which == 2) {
       if (g.n_pairs > 0)
         edge_tc::msg_bf_pair_tc<<<grid, edge_tc::NT, edge_tc::bf_pair_smem(), s>>>(eg, g.pcanon, g.n_pairs, mp, st->m.r_c, b.v, sc.s1,
@@ -1190,6 +1197,9 @@ void launch_edge_kernel(janus_stage* st, int u, int which, int mb, int slot, int
 }
 
 double kernel_flops_per_edge(const janus_stage* st, int which) {
+  const double RH = static_cast<double>(kR) * kH, HH = static_cast<double>(kH) * kH;
+  if (which == 4) return 0.5 * 2.0 * (4 * RH + 4 * HH);  // BF pair kernel: MMAs per pair, per directed edge
+  if (which == 5) return 0.5 * 2.0 * (2 * RH + 2 * HH);  // BE pair kernel
   const bool pairs = use_tc(st) && (which < 2 ? st->pair_feff : st->pair_bfbe);
   return pairs ? pair_flops_per_edge(which, kH, kR) : edge_kernel_flops_per_edge(which, kH, kR);
 }
@@ -1202,7 +1212,7 @@ int first_msg_unit(const janus_stage* st) {
 
 void stage_time_edge_kernel(janus_stage* st, int which, int mb, int slot, int iters, cudaStream_t s, float* avg_ms,
                             int64_t* edges, double* flops) {
-  if (iters < 1 || which < 0 || which > 3) throw domain_error("bad timing request");
+  if (iters < 1 || which < 0 || which > 5 || (which > 3 && !(use_tc(st) && st->pair_bfbe))) throw domain_error("bad timing request");
   const int u = first_msg_unit(st);
   cudaEvent_t a, z;
   JANUS_CUDA(cudaEventCreate(&a));
