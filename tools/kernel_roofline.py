@@ -1,10 +1,10 @@
 #!/usr/bin/env python3
-"""Per-kernel roofline table of the four tensor-core edge kernels on the C2
+"""Per-kernel roofline table of the tensor-core edge kernels (pair mode) on the C2
 workload (one B200): each kernel timed with the step's concurrency (all 32
 micro-batches launched on the 32 lanes with the step's grids, CUDA events
 around whole rounds; janus_stage_time_edge_kernel mb = -1) and as an
-isolated single-micro-batch launch; algorithmic FLOPs from DESIGN.md §3
-(the recomputed forward inside FF/BF/BE not counted); fraction of the
+isolated single-micro-batch launch; executed MMA FLOPs per directed edge
+(pair kernels: per pair / 2; stage.cu pair_flops_per_edge); fraction of the
 measured bf16 dense peak (MEASURED_PEAKS.json).  ncu metrics per kernel come
 from `--set full` captures (tools/capture_profiles.sh) and are merged in by
 --ncu-csv name=path pairs (raw page CSV)."""
@@ -18,7 +18,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import paper_2605_18404_b200 as J  # noqa: E402
 
-NAMES = ("msg_fe_tc", "msg_ff_tc", "msg_bf_tc", "msg_be_tc")
+# timing hook index -> what it launches (stage.cu launch_edge_kernel, pair mode)
+NAMES = {0: "msg_filter_tc + msg_fe_rows", 1: "msg_ff_rows", 2: "msg_bf_pair_tc + msg_bf_rows",
+         3: "msg_be_pair_tc + msg_be_rows", 4: "msg_bf_pair_tc", 5: "msg_be_pair_tc"}
 NCU = ("gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
        "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active",
        "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
@@ -49,7 +51,7 @@ def main():
     st = tr.stage(0)
     ncu = dict(x.split("=", 1) for x in args.ncu_csv)
     rows = []
-    for w, name in enumerate(NAMES):
+    for w, name in NAMES.items():
         ms, e, fl = st.time_edge_kernel(w, -1, iters=20)
         ims, ie, ifl = st.time_edge_kernel(w, 0, iters=50)
         r = {"kernel": name, "flop_per_edge": fl / e, "step_concurrency_tflops": fl / (ms * 1e-3) / 1e12,
