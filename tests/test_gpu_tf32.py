@@ -64,3 +64,63 @@ def test_tf32_edge_kernels_timed(janus, case):
         ms, ne, fl = st.time_edge_kernel(which, 0, iters=20)
         print(f"tc {name}: {ms * 1e3:.1f} us, {fl / ms / 1e9:.2f} TFLOP/s")
     st.close()
+
+
+def _run_stage(janus, m, params, b):
+    st = janus.Stage(m, params, 0, m.n_units, max_atoms=256, max_edges=256 * 120, max_struct=4)
+    st.load(0, b)
+    for ph in ("fe", "ff", "bf", "be"):
+        getattr(st, ph)(0)
+    E, _ = st.energy(0, b.n_struct)
+    F, _ = st.forces(0, b.n_atoms)
+    g = st.grads(0, 0)
+    st.close()
+    return E, F, g
+
+
+def test_tf32_directed_edge_kernels_match_oracle(janus, case, monkeypatch):
+    """The directed-edge tensor-core kernels (JANUS_FEFF_PAIR=0: every filter
+    per directed edge, edge_tc.cuh) stay an A/B path: same tolerances."""
+    m, params, batches, refs = case
+    monkeypatch.setenv("JANUS_FEFF_PAIR", "0")
+    for b, r in zip(batches, refs):
+        E, F, g = _run_stage(janus, m, params, b)
+        assert rel(E, r.E) < TOL_E and rel(F, r.F) < TOL_F and rel(g, r.grad) < TOL_G
+    monkeypatch.setenv("JANUS_FEFF_PAIR", "1")
+    monkeypatch.setenv("JANUS_BFBE_PAIR", "0")  # pair FE/FF, directed BF/BE
+    for b, r in zip(batches, refs):
+        E, F, g = _run_stage(janus, m, params, b)
+        assert rel(E, r.E) < TOL_E and rel(F, r.F) < TOL_F and rel(g, r.grad) < TOL_G
+
+
+def test_tf32_no_edges(janus, oracle, has_gpu):
+    """A dilute cell with no neighbour inside r_c (E = 0, no pairs): the pair
+    launches are skipped, the row kernels write zero messages and forces."""
+    if not has_gpu:
+        pytest.skip("no GPU")
+    m = janus.Model(L=2, H=64, R=64, precision=janus.PREC_TF32)
+    params = m.synth_params(5)
+    b = janus.synth_batch(m, [8], 0.0005, 21)
+    om = oracle.Model(L=m.L, H=m.H, R=m.R, n_species=m.n_species, r_c=m.r_c, w_E=m.w_E, w_F=m.w_F)
+    ob = oracle.Batch(b.pos, b.species, b.struct_id, b.cell, b.E_target.astype(float), b.F_target.astype(float))
+    nl = oracle.build_nbrlist(om, ob)
+    assert nl.n_edges == 0 and b.n_edges == 0, "expected an edgeless cell"
+    r = oracle.step(om, ob, nl, params.astype(np.float64))
+    E, F, g = _run_stage(janus, m, params, b)
+    assert rel(E, r.E) < TOL_E
+    assert np.abs(F).max() == 0.0
+    assert rel(g, r.grad) < TOL_G
+
+
+def test_tf32_pair_kernels_timed(janus, case):
+    m, params, batches, refs = case
+    b = janus.synth_batch(janus.Model(L=2), [256], 0.095, 9)
+    st = janus.Stage(m, params, 0, m.n_units, max_atoms=256, max_edges=256 * 120, max_struct=1)
+    st.load(0, b)
+    for ph in ("fe", "ff", "bf", "be"):
+        getattr(st, ph)(0)
+    for which, name in ((4, "bf pair"), (5, "be pair")):
+        ms, ne, fl = st.time_edge_kernel(which, 0, iters=20)
+        assert ne == b.n_edges and fl > 0 and ms > 0
+        print(f"tc {name}: {ms * 1e3:.1f} us, {fl / ms / 1e9:.2f} TFLOP/s")
+    st.close()
