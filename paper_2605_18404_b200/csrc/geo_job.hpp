@@ -16,6 +16,7 @@ struct GeoJob {
   int* src;
   float *d, *u, *c, *dc;
   int *pcanon, *pidx;                         // pair tables (pair_tc.cuh pairs_kernel)
+  float4* pgeo;                               // per pair: (d, c, c', i) (u, j)
 };
 constexpr int kMaxGeoJobs = 48;
 struct GeoJobs {

@@ -37,7 +37,7 @@ struct FilterJobs {
 };
 
 // grid (chunks, units): CTA (x, y) runs unit y over 128-pair chunks x, x + gridDim.x, ...
-__global__ void __launch_bounds__(NT, JANUS_FEFF_CTAS) msg_filter_tc(EdgeGeom g, const int* __restrict__ pcanon, int n_pairs,
+__global__ void __launch_bounds__(NT, JANUS_FEFF_CTAS) msg_filter_tc(EdgeGeom g, const float4* __restrict__ pg, int n_pairs,
                                                                     const __grid_constant__ FilterJobs J, float rc) {
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = align1024(sm_raw);
@@ -63,8 +63,8 @@ __global__ void __launch_bounds__(NT, JANUS_FEFF_CTAS) msg_filter_tc(EdgeGeom g,
   for (int ch = blockIdx.x; ch * TE < n_pairs; ch += gridDim.x) {
     const int p = ch * TE + c.e;
     const bool ok = p < n_pairs;
-    const int x = ok ? __ldg(pcanon + p) : 0;
-    const float d = ok ? __ldg(g.d + x) : 0.f, cc = ok ? __ldg(g.c + x) : 0.f, dc = ok ? __ldg(g.dc + x) : 0.f;
+    const float4 g0 = ok ? __ldg(pg + 2 * p) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float d = g0.x, cc = g0.y, dc = g0.z;
     {
       float ph[FPT], dph[FPT];
       basis(d, rc, f0, ph, dph);
@@ -148,6 +148,8 @@ __global__ void __launch_bounds__(1024) pairs_kernel(const __grid_constant__ nod
       jb.pcanon[pos] = e;
       jb.pidx[e] = pos;
       jb.pidx[r] = pos;
+      jb.pgeo[2 * pos] = make_float4(jb.d[e], jb.c[e], jb.dc[e], __int_as_float(jb.src[e]));
+      jb.pgeo[2 * pos + 1] = make_float4(jb.u[3 * e], jb.u[3 * e + 1], jb.u[3 * e + 2], __int_as_float(jb.col[e]));
     }
     base += total;
     __syncthreads();
@@ -303,7 +305,7 @@ __global__ void __launch_bounds__(256) msg_ff_rows(int n_atoms, const int* __res
 // kernels (edge_tc.cuh msg_bf_tc / msg_be_tc) but with no w / w' MMAs: the
 // per-row sums use the stored filters (msg_bf_rows / msg_be_rows).
 // Persistent CTAs, static chunk assignment => deterministic partials.
-__global__ void __launch_bounds__(NT, 1) msg_bf_pair_tc(EdgeGeom g, const int* __restrict__ pcanon, int n_pairs, MsgParams p,
+__global__ void __launch_bounds__(NT, 1) msg_bf_pair_tc(EdgeGeom g, const float4* __restrict__ pg, int n_pairs, MsgParams p,
                                                        float rc, const float* __restrict__ v, const float* __restrict__ vdot,
                                                        const float* __restrict__ am, const float* __restrict__ Fbar,
                                                        float* __restrict__ partial) {
@@ -340,14 +342,42 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_pair_tc(EdgeGeom g, const int* _
   for (int ch = blockIdx.x; ch * TE < n_pairs; ch += gridDim.x) {
     const int pp = ch * TE + c.e;
     const bool ok = pp < n_pairs;
-    const int x = ok ? __ldg(pcanon + pp) : 0;
-    const float d = ok ? __ldg(g.d + x) : 0.f, cc = ok ? __ldg(g.c + x) : 0.f, dc = ok ? __ldg(g.dc + x) : 0.f;
-    const int i = ok ? __ldg(g.src + x) : 0, j = ok ? __ldg(g.col + x) : 0;
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 g0 = ok ? __ldg(pg + 2 * pp) : z4, g1 = ok ? __ldg(pg + 2 * pp + 1) : z4;
+    const float d = g0.x, cc = g0.y, dc = g0.z;
+    const int i = ok ? __float_as_int(g0.w) : 0, j = ok ? __float_as_int(g1.w) : 0;
+    // the node-row gathers go first: their latency overlaps the basis and the z MMAs
+    float ai[FPT], aj[FPT], vi[FPT], vj[FPT];
+    gather32(am, i, f0, ai);
+    gather32(am, j, f0, aj);
+    gather32(v, i, f0, vi);
+    gather32(v, j, f0, vj);
+    float qb = 0.f;  // <Fbar_i - Fbar_j, u_x> (qb_rev = qb: u_rev = -u)
+    if (ok)
+      qb = fmaf(__ldg(Fbar + 3 * i) - __ldg(Fbar + 3 * j), g1.x,
+                fmaf(__ldg(Fbar + 3 * i + 1) - __ldg(Fbar + 3 * j + 1), g1.y,
+                     (__ldg(Fbar + 3 * i + 2) - __ldg(Fbar + 3 * j + 2)) * g1.z));
     {
       float ph[FPT], dph[FPT];
       basis(d, rc, f0, ph, dph);
       st_b16(B4, c.e, f0, ph);
       st_b16(B5, c.e, f0, dph);
+    }
+    {
+      float rho[FPT];
+#pragma unroll
+      for (int k = 0; k < FPT; ++k) rho[k] = fmaf(ai[k], vj[k], aj[k] * vi[k]);
+      gather32(vdot, i, f0, vi);
+      gather32(vdot, j, f0, vj);
+#pragma unroll
+      for (int k = 0; k < FPT; ++k) {
+        const float kap = fmaf(ai[k], vj[k], aj[k] * vi[k]);
+        const float r = rho[k];
+        rho[k] = qb * dc * r + cc * kap;  // mu
+        ai[k] = qb * cc * r;              // nu
+      }
+      st_b16(B2, c.e, f0, rho);  // mu (B of dB, A of sbar)
+      st_b16(B3, c.e, f0, ai);   // nu
     }
     tc::mbar_wait(&wbar, 0);
     c.publish();
@@ -355,24 +385,6 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_pair_tc(EdgeGeom g, const int* _
       mma_kb16(c.tmem + TM_Z, aB4, aW0b);
       mma_kb16(c.tmem + TM_ZP, aB5, aW0b);
       tc::commit(c.mbar);
-    }
-    float qb = 0.f;  // <Fbar_i - Fbar_j, u_x>; its loads and the gathers overlap the MMAs
-    if (ok)
-#pragma unroll
-      for (int k = 0; k < 3; ++k) qb = fmaf(__ldg(Fbar + 3 * i + k) - __ldg(Fbar + 3 * j + k), __ldg(g.u + 3 * x + k), qb);
-    float rho[FPT], kap[FPT];
-    {
-      float ai[FPT], aj[FPT], vi[FPT], vj[FPT];
-      gather32(am, i, f0, ai);
-      gather32(am, j, f0, aj);
-      gather32(v, i, f0, vi);
-      gather32(v, j, f0, vj);
-#pragma unroll
-      for (int k = 0; k < FPT; ++k) rho[k] = fmaf(ai[k], vj[k], aj[k] * vi[k]);
-      gather32(vdot, i, f0, vi);
-      gather32(vdot, j, f0, vj);
-#pragma unroll
-      for (int k = 0; k < FPT; ++k) kap[k] = fmaf(ai[k], vj[k], aj[k] * vi[k]);
     }
     c.wait_mma();
     {
@@ -386,14 +398,6 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_pair_tc(EdgeGeom g, const int* _
       }
       st_b16(B0, c.e, f0, z);   // s
       st_b16(B1, c.e, f0, zp);  // sdot
-#pragma unroll
-      for (int k = 0; k < FPT; ++k) {
-        const float r = rho[k];
-        rho[k] = qb * dc * r + cc * kap[k];  // mu
-        kap[k] = qb * cc * r;                // nu
-      }
-      st_b16(B2, c.e, f0, rho);
-      st_b16(B3, c.e, f0, kap);
     }
     c.publish();
     if (threadIdx.x == 0) {  // dB += s^T mu + sdot^T nu; sbar = mu B^T, sdotbar = nu B^T
@@ -442,7 +446,7 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_pair_tc(EdgeGeom g, const int* _
   teardown(c, 512);
 }
 
-__global__ void __launch_bounds__(NT, 1) msg_be_pair_tc(EdgeGeom g, const int* __restrict__ pcanon, int n_pairs, MsgParams p,
+__global__ void __launch_bounds__(NT, 1) msg_be_pair_tc(EdgeGeom g, const float4* __restrict__ pg, int n_pairs, MsgParams p,
                                                        float rc, const float* __restrict__ v, const float* __restrict__ bm,
                                                        float* __restrict__ partial) {
   extern __shared__ __align__(1024) uint8_t sm_raw[];
@@ -473,29 +477,30 @@ __global__ void __launch_bounds__(NT, 1) msg_be_pair_tc(EdgeGeom g, const int* _
   for (int ch = blockIdx.x; ch * TE < n_pairs; ch += gridDim.x) {
     const int pp = ch * TE + c.e;
     const bool ok = pp < n_pairs;
-    const int x = ok ? __ldg(pcanon + pp) : 0;
-    const float d = ok ? __ldg(g.d + x) : 0.f, cc = ok ? __ldg(g.c + x) : 0.f;
-    const int i = ok ? __ldg(g.src + x) : 0, j = ok ? __ldg(g.col + x) : 0;
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 g0 = ok ? __ldg(pg + 2 * pp) : z4;
+    const float d = g0.x, cc = g0.y;
+    const int i = ok ? __float_as_int(g0.w) : 0, j = ok ? __float_as_int(__ldg(&pg[2 * pp + 1].w)) : 0;
+    float gb[FPT];
     {
-      float ph[FPT], dph[FPT];
-      basis(d, rc, f0, ph, dph);
-      st_b16(B0, c.e, f0, ph);
+      float bi[FPT], bj[FPT], vi[FPT], vj[FPT];
+      gather32(bm, i, f0, bi);  // gathers first: their latency overlaps the basis
+      gather32(bm, j, f0, bj);
+      gather32(v, i, f0, vi);
+      gather32(v, j, f0, vj);
+      {
+        float ph[FPT], dph[FPT];
+        basis(d, rc, f0, ph, dph);
+        st_b16(B0, c.e, f0, ph);
+      }
+#pragma unroll
+      for (int k = 0; k < FPT; ++k) gb[k] = cc * fmaf(bi[k], vj[k], bj[k] * vi[k]);  // zero on padding (c = 0)
     }
     tc::mbar_wait(&wbar, 0);
     c.publish();
     if (threadIdx.x == 0) {
       mma_kb16(c.tmem + TM_Z, aB0, aW0b);
       tc::commit(c.mbar);
-    }
-    float gb[FPT];
-    {
-      float bi[FPT], bj[FPT], vi[FPT], vj[FPT];
-      gather32(bm, i, f0, bi);
-      gather32(bm, j, f0, bj);
-      gather32(v, i, f0, vi);
-      gather32(v, j, f0, vj);
-#pragma unroll
-      for (int k = 0; k < FPT; ++k) gb[k] = cc * fmaf(bi[k], vj[k], bj[k] * vi[k]);  // zero on padding (c = 0)
     }
     c.wait_mma();
     {

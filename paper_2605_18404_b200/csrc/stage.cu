@@ -367,6 +367,7 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
       g.dc = dalloc<float>(st, NE, false);
       g.pidx = dalloc<int>(st, NE, false);
       g.pcanon = dalloc<int>(st, NE / 2 + 1, false);
+      g.pgeo = dalloc<float4>(st, 2 * (NE / 2 + 1), false);
     }
     // slots
     st->slots.resize(static_cast<size_t>(d.n_slots));
@@ -643,6 +644,7 @@ void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_
       j.c = g.c;
       j.dc = g.dc;
       j.pcanon = g.pcanon;
+      j.pgeo = g.pgeo;
       j.pidx = g.pidx;
       defer->push_back(j);
     }
@@ -659,6 +661,13 @@ void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_
     J.j[0].n_edges = E;
     J.j[0].rev = g.rev;
     J.j[0].pcanon = g.pcanon;
+    J.j[0].pgeo = g.pgeo;
+    J.j[0].src = g.src;
+    J.j[0].col = g.col;
+    J.j[0].d = g.d;
+    J.j[0].u = g.u;
+    J.j[0].c = g.c;
+    J.j[0].dc = g.dc;
     J.j[0].pidx = g.pidx;
     edge_tc::pairs_kernel<<<1, 1024, 0, s>>>(J);
   }
@@ -709,7 +718,7 @@ void launch_filter(janus_stage* st, const DevGeo& g, Slot& sl, int u_only, cudaS
   if (J.n == 0 || g.n_pairs == 0) return;
   const int chunks = (g.n_pairs + edge_tc::TE - 1) / edge_tc::TE;
   const int gx = grid_x > 0 ? std::min(grid_x, chunks) : std::max(1, std::min(chunks, (chunks + st->tpc_fe - 1) / st->tpc_fe));
-  edge_tc::msg_filter_tc<<<dim3(gx, J.n), edge_tc::NT, edge_tc::filter_smem(), s>>>(edge_geom(g), g.pcanon, g.n_pairs, J,
+  edge_tc::msg_filter_tc<<<dim3(gx, J.n), edge_tc::NT, edge_tc::filter_smem(), s>>>(edge_geom(g), g.pgeo, g.n_pairs, J,
                                                                                      st->m.r_c);
   JANUS_LAUNCH_CHECK("msg_filter_tc");
 }
@@ -882,7 +891,7 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
           const int grid = pair_grid(st, g);
           const MsgParams mp = msg_params(st, u);
           if (g.n_pairs > 0 && !(prof_skip() & 4)) {
-            edge_tc::msg_bf_pair_tc<<<grid, edge_tc::NT, edge_tc::bf_pair_smem(), s>>>(eg, g.pcanon, g.n_pairs, mp, st->m.r_c, b.v,
+            edge_tc::msg_bf_pair_tc<<<grid, edge_tc::NT, edge_tc::bf_pair_smem(), s>>>(eg, g.pgeo, g.n_pairs, mp, st->m.r_c, b.v,
                                                                                        sc.s1, b.ff_a, Fbar, sc.partial);
             JANUS_LAUNCH_CHECK("msg_bf_pair_tc");
           }
@@ -997,7 +1006,7 @@ void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only, 
           const int grid = pair_grid(st, g);
           const MsgParams mp = msg_params(st, u);
           if (g.n_pairs > 0 && !(prof_skip() & 8)) {
-            edge_tc::msg_be_pair_tc<<<grid, edge_tc::NT, edge_tc::be_pair_smem(), s>>>(eg, g.pcanon, g.n_pairs, mp, st->m.r_c, b.v, bm,
+            edge_tc::msg_be_pair_tc<<<grid, edge_tc::NT, edge_tc::be_pair_smem(), s>>>(eg, g.pgeo, g.n_pairs, mp, st->m.r_c, b.v, bm,
                                                                                        sc.partial);
             JANUS_LAUNCH_CHECK("msg_be_pair_tc");
           }
@@ -1139,21 +1148,21 @@ void launch_edge_kernel(janus_stage* st, int u, int which, int mb, int slot, int
     const int grid = step_grid ? pair_grid(st, g) : std::max(1, std::min((g.n_pairs + edge_tc::TE - 1) / edge_tc::TE, 148));
     const float* wt = mp.pack + edge_tc::kWtOff / sizeof(float);
     if (which == 4 && g.n_pairs > 0)
-      edge_tc::msg_bf_pair_tc<<<grid, edge_tc::NT, edge_tc::bf_pair_smem(), s>>>(eg, g.pcanon, g.n_pairs, mp, st->m.r_c, b.v, sc.s1,
+      edge_tc::msg_bf_pair_tc<<<grid, edge_tc::NT, edge_tc::bf_pair_smem(), s>>>(eg, g.pgeo, g.n_pairs, mp, st->m.r_c, b.v, sc.s1,
                                                                                  b.ff_a, sl.Fbar, sc.partial);
     if (which == 5 && g.n_pairs > 0)
-      edge_tc::msg_be_pair_tc<<<grid, edge_tc::NT, edge_tc::be_pair_smem(), s>>>(eg, g.pcanon, g.n_pairs, mp, st->m.r_c, b.v, sc.s2,
+      edge_tc::msg_be_pair_tc<<<grid, edge_tc::NT, edge_tc::be_pair_smem(), s>>>(eg, g.pgeo, g.n_pairs, mp, st->m.r_c, b.v, sc.s2,
                                                                                  sc.partial);
     if (which >= 4) return;
     if (which == 2) {
       if (g.n_pairs > 0)
-        edge_tc::msg_bf_pair_tc<<<grid, edge_tc::NT, edge_tc::bf_pair_smem(), s>>>(eg, g.pcanon, g.n_pairs, mp, st->m.r_c, b.v, sc.s1,
+        edge_tc::msg_bf_pair_tc<<<grid, edge_tc::NT, edge_tc::bf_pair_smem(), s>>>(eg, g.pgeo, g.n_pairs, mp, st->m.r_c, b.v, sc.s1,
                                                                                    b.ff_a, sl.Fbar, sc.partial);
       edge_tc::msg_bf_rows<<<blocks(N, 8), 256, 0, s>>>(N, g.row_ptr, g.col, g.pidx, g.u, sl.Fbar, b.wf, b.wfp, b.v, sc.s1, b.ff_a, wt,
                                                          sc.s3, sc.s4, nullptr);
     } else {
       if (g.n_pairs > 0)
-        edge_tc::msg_be_pair_tc<<<grid, edge_tc::NT, edge_tc::be_pair_smem(), s>>>(eg, g.pcanon, g.n_pairs, mp, st->m.r_c, b.v, sc.s2,
+        edge_tc::msg_be_pair_tc<<<grid, edge_tc::NT, edge_tc::be_pair_smem(), s>>>(eg, g.pgeo, g.n_pairs, mp, st->m.r_c, b.v, sc.s2,
                                                                                    sc.partial);
       edge_tc::msg_be_rows<<<blocks(N, 8), 256, 0, s>>>(N, g.row_ptr, g.col, g.pidx, b.wf, sc.s2, wt, sc.s3, nullptr, nullptr);
     }

@@ -56,6 +56,7 @@ struct DevGeo {
   // undirected edge pairs (tensor-core FE / FF, pair_tc.cuh): canonical edge of
   // pair p, and pair of every directed edge
   int *pcanon = nullptr, *pidx = nullptr;
+  float4* pgeo = nullptr;  // per pair two float4: (d, c, c', bits of i), (u, bits of j) of the canonical edge
   int n_pairs = 0;
 };
 
