@@ -174,6 +174,7 @@ __device__ __forceinline__ float2 row_times_wt(float2 Y, const float* __restrict
 }
 
 // m_i = sum_e w_p(e) * v_j   (warp per row, 2 features per lane)
+template <int KF>  // edges whose gathers are in flight per step
 __global__ void __launch_bounds__(256) msg_fe_rows(int n_atoms, const int* __restrict__ row_ptr, const int* __restrict__ col,
                                                    const int* __restrict__ pidx, const float* __restrict__ w,
                                                    const float* __restrict__ v, float* __restrict__ m_out) {
@@ -185,16 +186,16 @@ __global__ void __launch_bounds__(256) msg_fe_rows(int n_atoms, const int* __res
     const int n = min(32, ee - e0);
     const int mp = lane < n ? __ldg(pidx + e0 + lane) : 0;
     const int mj = lane < n ? __ldg(col + e0 + lane) : 0;
-    for (int k0 = 0; k0 < n; k0 += 8) {  // 8 edges' loads in flight; masked tail
-      float2 a[8], b[8];
+    for (int k0 = 0; k0 < n; k0 += KF) {  // KF edges' loads in flight; masked tail
+      float2 a[KF], b[KF];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
+      for (int k = 0; k < KF; ++k) {
         const int pk = __shfl_sync(0xffffffffu, mp, k0 + k), jk = __shfl_sync(0xffffffffu, mj, k0 + k);
         a[k] = __ldg(reinterpret_cast<const float2*>(w + (size_t)pk * H) + lane);
         b[k] = __ldg(reinterpret_cast<const float2*>(v + (size_t)jk * H) + lane);
       }
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
+      for (int k = 0; k < KF; ++k)
         if (k0 + k < n) {
           acc.x = fmaf(a[k].x, b[k].x, acc.x);
           acc.y = fmaf(a[k].y, b[k].y, acc.y);
@@ -207,6 +208,7 @@ __global__ void __launch_bounds__(256) msg_fe_rows(int n_atoms, const int* __res
 // FF of a msg unit (warp per row): Y_i, F_i += sum_e (q_e + q_rev e) u_e, a_h += Y W^T.
 // The per-edge scalars of 32 edges are reduced across the warp by a
 // transposing butterfly (31 shuffles): lane k ends with edge k's total.
+template <int KF>  // edges whose gathers are in flight per step
 __global__ void __launch_bounds__(256) msg_ff_rows(int n_atoms, const int* __restrict__ row_ptr, const int* __restrict__ col,
                                                    const int* __restrict__ pidx, const float* __restrict__ uvec,
                                                    const float* __restrict__ w, const float* __restrict__ wp,
@@ -226,11 +228,11 @@ __global__ void __launch_bounds__(256) msg_ff_rows(int n_atoms, const int* __res
     const int mj = lane < n ? __ldg(col + e0 + lane) : 0;
     float part[32];
 #pragma unroll
-    for (int k0 = 0; k0 < 32; k0 += 8) {
+    for (int k0 = 0; k0 < 32; k0 += KF) {
       if (k0 < n) {  // warp-uniform
-        float2 a[8], b[8], c2[8], d2[8];
+        float2 a[KF], b[KF], c2[KF], d2[KF];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < KF; ++k) {
           const int pk = __shfl_sync(0xffffffffu, mp, k0 + k), jk = __shfl_sync(0xffffffffu, mj, k0 + k);
           a[k] = __ldg(reinterpret_cast<const float2*>(w + (size_t)pk * H) + lane);
           b[k] = __ldg(reinterpret_cast<const float2*>(wp + (size_t)pk * H) + lane);
@@ -238,7 +240,7 @@ __global__ void __launch_bounds__(256) msg_ff_rows(int n_atoms, const int* __res
           d2[k] = __ldg(reinterpret_cast<const float2*>(v + (size_t)jk * H) + lane);
         }
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < KF; ++k) {
           const bool ok = k0 + k < n;
           if (ok) {
             Y.x = fmaf(a[k].x, c2[k].x, Y.x);
@@ -250,7 +252,7 @@ __global__ void __launch_bounds__(256) msg_ff_rows(int n_atoms, const int* __res
         }
       } else {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) part[k0 + k] = 0.f;
+        for (int k = 0; k < KF; ++k) part[k0 + k] = 0.f;
       }
     }
     // transposing butterfly: after the step of width s, lane l keeps the
@@ -554,6 +556,7 @@ __global__ void __launch_bounds__(NT, 1) msg_be_pair_tc(EdgeGeom g, const float4
 
 // BF rows: mdot_i = sum_e qb_e w'_p v_j + w_p vdot_j ; X_i = sum_e qb_e w'_p am_j ;
 // inj = X W^T (hbar^F of the unit input), qb_e = <Fbar_i - Fbar_j, u_e>
+template <int KF>  // edges whose gathers are in flight per step
 __global__ void __launch_bounds__(256) msg_bf_rows(int n_atoms, const int* __restrict__ row_ptr, const int* __restrict__ col,
                                                    const int* __restrict__ pidx, const float* __restrict__ uvec,
                                                    const float* __restrict__ Fbar, const float* __restrict__ w,
@@ -578,11 +581,11 @@ __global__ void __launch_bounds__(256) msg_bf_rows(int n_atoms, const int* __res
       mq = fmaf(fi1 - __ldg(Fbar + 3 * mj + 1), __ldg(uvec + 3 * e + 1), mq);
       mq = fmaf(fi2 - __ldg(Fbar + 3 * mj + 2), __ldg(uvec + 3 * e + 2), mq);
     }
-    for (int k0 = 0; k0 < n; k0 += 8) {
-      float2 a[8], b[8], vv[8], dv[8], aj[8];
-      float q[8];
+    for (int k0 = 0; k0 < n; k0 += KF) {
+      float2 a[KF], b[KF], vv[KF], dv[KF], aj[KF];
+      float q[KF];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
+      for (int k = 0; k < KF; ++k) {
         const int pk = __shfl_sync(0xffffffffu, mp, k0 + k), jk = __shfl_sync(0xffffffffu, mj, k0 + k);
         q[k] = __shfl_sync(0xffffffffu, mq, k0 + k);
         a[k] = __ldg(reinterpret_cast<const float2*>(w + (size_t)pk * H) + lane);
@@ -592,7 +595,7 @@ __global__ void __launch_bounds__(256) msg_bf_rows(int n_atoms, const int* __res
         aj[k] = __ldg(reinterpret_cast<const float2*>(am + (size_t)jk * H) + lane);
       }
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
+      for (int k = 0; k < KF; ++k)
         if (k0 + k < n) {
           const float px = q[k] * b[k].x, py = q[k] * b[k].y;
           md.x = fmaf(px, vv[k].x, fmaf(a[k].x, dv[k].x, md.x));
@@ -608,6 +611,7 @@ __global__ void __launch_bounds__(256) msg_bf_rows(int n_atoms, const int* __res
 }
 
 // BE rows: Yb_i = sum_e w_p bm_j ; b_h += Yb W^T + inj
+template <int KF>  // edges whose gathers are in flight per step
 __global__ void __launch_bounds__(256) msg_be_rows(int n_atoms, const int* __restrict__ row_ptr, const int* __restrict__ col,
                                                    const int* __restrict__ pidx, const float* __restrict__ w,
                                                    const float* __restrict__ bm, const float* __restrict__ wt,
@@ -620,16 +624,16 @@ __global__ void __launch_bounds__(256) msg_be_rows(int n_atoms, const int* __res
     const int n = min(32, ee - e0);
     const int mp = lane < n ? __ldg(pidx + e0 + lane) : 0;
     const int mj = lane < n ? __ldg(col + e0 + lane) : 0;
-    for (int k0 = 0; k0 < n; k0 += 8) {
-      float2 a[8], b[8];
+    for (int k0 = 0; k0 < n; k0 += KF) {
+      float2 a[KF], b[KF];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
+      for (int k = 0; k < KF; ++k) {
         const int pk = __shfl_sync(0xffffffffu, mp, k0 + k), jk = __shfl_sync(0xffffffffu, mj, k0 + k);
         a[k] = __ldg(reinterpret_cast<const float2*>(w + (size_t)pk * H) + lane);
         b[k] = __ldg(reinterpret_cast<const float2*>(bm + (size_t)jk * H) + lane);
       }
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
+      for (int k = 0; k < KF; ++k)
         if (k0 + k < n) {
           acc.x = fmaf(a[k].x, b[k].x, acc.x);
           acc.y = fmaf(a[k].y, b[k].y, acc.y);

@@ -22,6 +22,15 @@
 #include "edge_kernels.cuh"
 #include "edge_tc.cuh"
 #include "pair_tc.cuh"
+
+// row kernels (pair_tc.cuh) by the stage's gathers-in-flight setting
+#define JANUS_ROWS(KERN, GRID, S, ...)                                          \
+  do {                                                                          \
+    if (st->rows_kf == 4)                                                       \
+      edge_tc::KERN<4><<<(GRID), 256, 0, (S)>>>(__VA_ARGS__);                   \
+    else                                                                        \
+      edge_tc::KERN<8><<<(GRID), 256, 0, (S)>>>(__VA_ARGS__);                   \
+  } while (0)
 #include "node_kernels.cuh"
 #include "wgrad_tc.cuh"
 #include "stage.cuh"
@@ -436,6 +445,7 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
     if (const char* e = std::getenv("JANUS_TPC_WG")) st->tpc_wg = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("JANUS_FEFF_PAIR")) st->pair_feff = std::atoi(e) != 0;  // A/B runs only
     st->pair_bfbe = st->pair_feff;
+    if (const char* e = std::getenv("JANUS_ROWS_KF")) st->rows_kf = std::atoi(e) == 4 ? 4 : 8;
     if (const char* e = std::getenv("JANUS_BFBE_PAIR")) st->pair_bfbe = st->pair_feff && std::atoi(e) != 0;
     for (Scratch& sc : st->lanes) {
       sc.wh = dalloc<float>(st, NH, false);
@@ -749,7 +759,7 @@ void stage_fe(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
         gemm(s, N, cur_h, W, nullptr, nullptr, nullptr, b.v);
         if (pairs) {
           if (!(prof_skip() & 1))
-            edge_tc::msg_fe_rows<<<blocks(N, 8), 256, 0, s>>>(N, g.row_ptr, g.col, g.pidx, b.wf, b.v, b.out_m);
+            JANUS_ROWS(msg_fe_rows, blocks(N, 8), s, N, g.row_ptr, g.col, g.pidx, b.wf, b.v, b.out_m);
         } else if (g.n_tiles > 0 && use_tc(st)) {
           if (!(prof_skip() & 1)) edge_tc::msg_fe_tc<<<fe_grid(st, g), edge_tc::NT, edge_tc::fe_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, msg_params(st, u),
                                                                                  st->m.r_c, b.v, b.out_m);
@@ -822,7 +832,7 @@ void stage_ff(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
         if (u == st->u1 - 1) copy(s, b.ff_a, wm, NH);  // a_m arrived through the ADJ_IN port
         if (use_tc(st) && st->pair_feff) {  // a_h += Y W^T fused into the row kernel
           if (!(prof_skip() & 2))
-            edge_tc::msg_ff_rows<<<blocks(N, 8), 256, 0, s>>>(N, g.row_ptr, g.col, g.pidx, g.u, b.wf, b.wfp, b.v, b.ff_a,
+            JANUS_ROWS(msg_ff_rows, blocks(N, 8), s, N, g.row_ptr, g.col, g.pidx, g.u, b.wf, b.wfp, b.v, b.ff_a,
                                                                msg_params(st, u).pack + edge_tc::kWtOff / sizeof(float),
                                                                b.ff_Y, sl.F, wh);
         } else if (g.n_tiles > 0 && use_tc(st)) {  // a_h += Y W^T fused into the tile epilogue
@@ -897,7 +907,7 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
           }
           if (g.n_pairs > 0 && !(prof_skip() & 128)) edge::reduce_partials_kernel<<<edge::reduce_grid(EC::PE), 256, 0, s>>>(sc.partial, grid, EC::PE, G2);
           if (!(prof_skip() & 4))
-            edge_tc::msg_bf_rows<<<blocks(N, 8), 256, 0, s>>>(N, g.row_ptr, g.col, g.pidx, g.u, Fbar, b.wf, b.wfp, b.v, sc.s1, b.ff_a,
+            JANUS_ROWS(msg_bf_rows, blocks(N, 8), s, N, g.row_ptr, g.col, g.pidx, g.u, Fbar, b.wf, b.wfp, b.v, sc.s1, b.ff_a,
                                                                mp.pack + edge_tc::kWtOff / sizeof(float), am, sc.s2, b.inj);
         } else if (g.n_tiles > 0 && use_tc(st)) {
           const int grid = tc_grid(st, g);
@@ -1012,7 +1022,7 @@ void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only, 
           }
           if (g.n_pairs > 0 && !(prof_skip() & 128)) edge::reduce_partials_kernel<<<edge::reduce_grid(EC::PE), 256, 0, s>>>(sc.partial, grid, EC::PE, G1);
           if (!(prof_skip() & 8))  // Yb; b_h += Yb W^T + hbar^F
-            edge_tc::msg_be_rows<<<blocks(N, 8), 256, 0, s>>>(N, g.row_ptr, g.col, g.pidx, b.wf, bm,
+            JANUS_ROWS(msg_be_rows, blocks(N, 8), s, N, g.row_ptr, g.col, g.pidx, b.wf, bm,
                                                                mp.pack + edge_tc::kWtOff / sizeof(float), sc.s1, b.inj, bh);
         } else if (g.n_tiles > 0 && use_tc(st)) {
           const int grid = tc_grid(st, g);
@@ -1136,9 +1146,9 @@ void launch_edge_kernel(janus_stage* st, int u, int which, int mb, int slot, int
     const int N = g.n_atoms;
     if (which == 0) {  // the filters of this unit (pair MMAs of FE and FF) + FE's row sums
       launch_filter(st, g, sl, u, s, step_grid ? 0 : (g.n_pairs + edge_tc::TE - 1) / edge_tc::TE);
-      edge_tc::msg_fe_rows<<<blocks(N, 8), 256, 0, s>>>(N, g.row_ptr, g.col, g.pidx, b.wf, b.v, sc.s3);
+      JANUS_ROWS(msg_fe_rows, blocks(N, 8), s, N, g.row_ptr, g.col, g.pidx, b.wf, b.v, sc.s3);
     } else {
-      edge_tc::msg_ff_rows<<<blocks(N, 8), 256, 0, s>>>(N, g.row_ptr, g.col, g.pidx, g.u, b.wf, b.wfp, b.v, b.ff_a,
+      JANUS_ROWS(msg_ff_rows, blocks(N, 8), s, N, g.row_ptr, g.col, g.pidx, g.u, b.wf, b.wfp, b.v, b.ff_a,
                                                          mp.pack + edge_tc::kWtOff / sizeof(float), sc.s3, sc.s5, sc.s4);
     }
     return;
@@ -1158,13 +1168,13 @@ void launch_edge_kernel(janus_stage* st, int u, int which, int mb, int slot, int
       if (g.n_pairs > 0)
         edge_tc::msg_bf_pair_tc<<<grid, edge_tc::NT, edge_tc::bf_pair_smem(), s>>>(eg, g.pgeo, g.n_pairs, mp, st->m.r_c, b.v, sc.s1,
                                                                                    b.ff_a, sl.Fbar, sc.partial);
-      edge_tc::msg_bf_rows<<<blocks(N, 8), 256, 0, s>>>(N, g.row_ptr, g.col, g.pidx, g.u, sl.Fbar, b.wf, b.wfp, b.v, sc.s1, b.ff_a, wt,
+      JANUS_ROWS(msg_bf_rows, blocks(N, 8), s, N, g.row_ptr, g.col, g.pidx, g.u, sl.Fbar, b.wf, b.wfp, b.v, sc.s1, b.ff_a, wt,
                                                          sc.s3, sc.s4, nullptr);
     } else {
       if (g.n_pairs > 0)
         edge_tc::msg_be_pair_tc<<<grid, edge_tc::NT, edge_tc::be_pair_smem(), s>>>(eg, g.pgeo, g.n_pairs, mp, st->m.r_c, b.v, sc.s2,
                                                                                    sc.partial);
-      edge_tc::msg_be_rows<<<blocks(N, 8), 256, 0, s>>>(N, g.row_ptr, g.col, g.pidx, b.wf, sc.s2, wt, sc.s3, nullptr, nullptr);
+      JANUS_ROWS(msg_be_rows, blocks(N, 8), s, N, g.row_ptr, g.col, g.pidx, b.wf, sc.s2, wt, sc.s3, nullptr, nullptr);
     }
     return;
   }

@@ -129,6 +129,7 @@ struct janus_stage {
   int tc_tile_max_chunks = 0;        // cost-chosen tiles: max 128-edge chunks (0: by mean degree)
   double tc_tile_ovh = 0.3;          // per-tile epilogue cost in chunk units
   bool pair_feff = true;             // TC FE / FF: filters once per edge pair (pair_tc.cuh); JANUS_FEFF_PAIR=0 -> directed-edge kernels
+  int rows_kf = 8;                   // row kernels: edges' gathers in flight per warp (JANUS_ROWS_KF=4 for A/B)
   bool pair_bfbe = true;             // TC BF / BE: weight gradients once per edge pair (needs pair_feff); JANUS_BFBE_PAIR=0 -> directed
   janus::LmBuilder* lm = nullptr;  // device neighbour-list builder (lazy, janus_stage_load without a CSR)
 
