@@ -650,6 +650,33 @@ __global__ void __launch_bounds__(256) reduce_partials_kernel(const float* __res
   }
 }
 
+// Few partials (the persistent pair / tile kernels' grids, <= kSeqPartials):
+// one thread per column sums the partials in order, 256 columns per CTA —
+// 33 CTAs for PE = 8320 instead of reduce_partials_kernel's 260.
+constexpr int kSeqPartials = 48;
+__global__ void __launch_bounds__(256) reduce_partials_seq_kernel(const float* __restrict__ partial, int n, int PE,
+                                                                  float* __restrict__ out) {
+  const int p = blockIdx.x * 256 + threadIdx.x;
+  if (p >= PE) return;
+  const float* src = partial + p;
+  float s = 0.f;
+  int t = 0;
+  for (; t + 4 <= n; t += 4) {
+    const float a = __ldg(src + (size_t)t * PE), b = __ldg(src + (size_t)(t + 1) * PE);
+    const float c = __ldg(src + (size_t)(t + 2) * PE), d = __ldg(src + (size_t)(t + 3) * PE);
+    s = (((s + a) + b) + c) + d;
+  }
+  for (; t < n; ++t) s += __ldg(src + (size_t)t * PE);
+  out[p] = s;
+}
+// out = sum over the n partials, fixed order for a given n
+inline void reduce_partials(const float* partial, int n, int PE, float* out, cudaStream_t s) {
+  if (n <= kSeqPartials)
+    reduce_partials_seq_kernel<<<(PE + 255) / 256, 256, 0, s>>>(partial, n, PE, out);
+  else
+    reduce_partials_kernel<<<reduce_grid(PE), 256, 0, s>>>(partial, n, PE, out);
+}
+
 template <int H, int R>
 constexpr size_t fe_smem() { return sizeof(float) * (R * H + H * H + 2 * H + R * LD + H * LD + TE); }
 template <int H, int R>

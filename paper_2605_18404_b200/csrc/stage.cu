@@ -905,7 +905,7 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
                                                                                        sc.s1, b.ff_a, Fbar, sc.partial);
             JANUS_LAUNCH_CHECK("msg_bf_pair_tc");
           }
-          if (g.n_pairs > 0 && !(prof_skip() & 128)) edge::reduce_partials_kernel<<<edge::reduce_grid(EC::PE), 256, 0, s>>>(sc.partial, grid, EC::PE, G2);
+          if (g.n_pairs > 0 && !(prof_skip() & 128)) edge::reduce_partials(sc.partial, grid, EC::PE, G2, s);
           if (!(prof_skip() & 4))
             JANUS_ROWS(msg_bf_rows, blocks(N, 8), s, N, g.row_ptr, g.col, g.pidx, g.u, Fbar, b.wf, b.wfp, b.v, sc.s1, b.ff_a,
                                                                mp.pack + edge_tc::kWtOff / sizeof(float), am, sc.s2, b.inj);
@@ -915,7 +915,7 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
                                                                           st->m.r_c, b.v, sc.s1, b.ff_a, Fbar, am, sc.s2,
                                                                           sc.partial, b.inj);  // + hbar^F = X W^T
           JANUS_LAUNCH_CHECK("msg_bf_tc");
-          if (!(prof_skip() & 128)) edge::reduce_partials_kernel<<<edge::reduce_grid(EC::PE), 256, 0, s>>>(sc.partial, grid, EC::PE, G2);
+          if (!(prof_skip() & 128)) edge::reduce_partials(sc.partial, grid, EC::PE, G2, s);
         } else if (g.n_tiles > 0) {
           edge::msg_bf_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::bf_smem<kH, kR>(), s>>>(
               eg, msg_params(st, u), st->m.r_c, b.v, sc.s1, b.ff_a, Fbar, am, sc.s2, sc.partial);
@@ -1020,7 +1020,7 @@ void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only, 
                                                                                        sc.partial);
             JANUS_LAUNCH_CHECK("msg_be_pair_tc");
           }
-          if (g.n_pairs > 0 && !(prof_skip() & 128)) edge::reduce_partials_kernel<<<edge::reduce_grid(EC::PE), 256, 0, s>>>(sc.partial, grid, EC::PE, G1);
+          if (g.n_pairs > 0 && !(prof_skip() & 128)) edge::reduce_partials(sc.partial, grid, EC::PE, G1, s);
           if (!(prof_skip() & 8))  // Yb; b_h += Yb W^T + hbar^F
             JANUS_ROWS(msg_be_rows, blocks(N, 8), s, N, g.row_ptr, g.col, g.pidx, b.wf, bm,
                                                                mp.pack + edge_tc::kWtOff / sizeof(float), sc.s1, b.inj, bh);
@@ -1030,7 +1030,7 @@ void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only, 
                                                                           st->m.r_c, b.v, bm, sc.s1, sc.partial,
                                                                           b.inj, bh);  // + b_h += Yb W^T + hbar^F
           JANUS_LAUNCH_CHECK("msg_be_tc");
-          if (!(prof_skip() & 128)) edge::reduce_partials_kernel<<<edge::reduce_grid(EC::PE), 256, 0, s>>>(sc.partial, grid, EC::PE, G1);
+          if (!(prof_skip() & 128)) edge::reduce_partials(sc.partial, grid, EC::PE, G1, s);
         } else if (g.n_tiles > 0) {
           edge::msg_be_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::be_smem<kH, kR>(), s>>>(
               eg, msg_params(st, u), st->m.r_c, b.v, bm, sc.s1, sc.partial);
