@@ -459,6 +459,28 @@ __device__ __forceinline__ void rowmm(const float (*X)[68], const float* Ms, int
     o[3] = fmaf(a, m.w, o[3]);
   }
 }
+// Same products in gemm_rows_kernel's summation order (even / odd k chains,
+// then their sum), so a fused v = h W is bit-identical to the row-GEMM launch
+// it replaces (pipeline stages that cannot fuse use the launch).
+__device__ __forceinline__ void rowmm_eo(const float (*X)[68], const float* Ms, int r, int c0, float (&o)[4]) {
+  float e[4] = {0.f, 0.f, 0.f, 0.f}, d[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 8
+  for (int k = 0; k < 64; k += 2) {
+    const float a0 = X[r][k], a1 = X[r][k + 1];
+    const float4 m0 = *reinterpret_cast<const float4*>(Ms + k * 64 + c0);
+    const float4 m1 = *reinterpret_cast<const float4*>(Ms + (k + 1) * 64 + c0);
+    e[0] = fmaf(a0, m0.x, e[0]);
+    e[1] = fmaf(a0, m0.y, e[1]);
+    e[2] = fmaf(a0, m0.z, e[2]);
+    e[3] = fmaf(a0, m0.w, e[3]);
+    d[0] = fmaf(a1, m1.x, d[0]);
+    d[1] = fmaf(a1, m1.y, d[1]);
+    d[2] = fmaf(a1, m1.z, d[2]);
+    d[3] = fmaf(a1, m1.w, d[3]);
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) o[q] = e[q] + d[q];
+}
 // Stage up to 4 [64][64] weight matrices into smem with every load in flight
 // at once (16 float4 per thread per matrix), then one barrier.
 // (cp.async: every 16 B copy of every matrix in flight at once, no registers;
@@ -494,17 +516,19 @@ __device__ __forceinline__ float4 row_get(const float* src, int i, int c0) {
   return __ldg(reinterpret_cast<const float4*>(src + (size_t)i * 64 + c0));
 }
 
-// FE: p = m U + ups ; h_out = h + SiLU(p) V
+// FE: p = m U + ups ; h_out = h + SiLU(p) V ; and, when the next unit is a
+// msg unit on the stage, its v = h_out Wn (saves that unit's row-GEMM launch)
 __global__ void __launch_bounds__(256) upd_fe_fused(int rows, const float* __restrict__ m, const float* __restrict__ h,
                                                     const float* __restrict__ U, const float* __restrict__ ups,
                                                     const float* __restrict__ V, float* __restrict__ p_out,
-                                                    float* __restrict__ h_out) {
+                                                    float* __restrict__ h_out, const float* __restrict__ Wn,
+                                                    float* __restrict__ v_out) {
   __shared__ __align__(16) float X[kRB][68];
   extern __shared__ __align__(16) float Ws[];
   const int i0 = blockIdx.x * kRB, r = threadIdx.x / 16, c0 = (threadIdx.x % 16) * 4, i = i0 + r;
   {
-    const float* mats[2] = {U, V};
-    stage_mats(Ws, mats, 2);
+    const float* mats[3] = {U, V, Wn};
+    stage_mats(Ws, mats, Wn ? 3 : 2);
   }
   row_load(X, m, i0, rows);
   stage_mats_wait();
@@ -524,6 +548,14 @@ __global__ void __launch_bounds__(256) upd_fe_fused(int rows, const float* __res
     const float4 hh = row_get(h, i, c0);
     o[0] += hh.x, o[1] += hh.y, o[2] += hh.z, o[3] += hh.w;
     row_store(h_out, i, c0, o);
+  }
+  if (Wn) {  // v = h_out Wn (padding rows: h = 0 loads, results not stored)
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) X[r][c0 + q] = o[q];
+    __syncthreads();
+    rowmm_eo(X, Ws + 2 * 4096, r, c0, o);
+    if (i < rows) row_store(v_out, i, c0, o);
   }
 }
 
@@ -566,14 +598,15 @@ __global__ void __launch_bounds__(256) upd_bf_fused(int rows, const float* __res
                                                     const float* __restrict__ Vt, const float* __restrict__ Ut,
                                                     const float* __restrict__ V, float* __restrict__ pbar,
                                                     float* __restrict__ pdbar, float* __restrict__ u,
-                                                    float* __restrict__ inj, float* ah) {
+                                                    float* __restrict__ inj, float* ah, const float* __restrict__ Wn,
+                                                    float* __restrict__ vdot_out) {
   __shared__ __align__(16) float X[kRB][68];
   __shared__ __align__(16) float Y[kRB][68];
   extern __shared__ __align__(16) float Ws[];
   const int i0 = blockIdx.x * kRB, r = threadIdx.x / 16, c0 = (threadIdx.x % 16) * 4, i = i0 + r;
   {
-    const float* mats[4] = {U, Vt, Ut, V};
-    stage_mats(Ws, mats, 4);
+    const float* mats[5] = {U, Vt, Ut, V, Wn};
+    stage_mats(Ws, mats, Wn ? 5 : 4);
   }
   row_load(X, am, i0, rows);
   stage_mats_wait();
@@ -609,6 +642,14 @@ __global__ void __launch_bounds__(256) upd_bf_fused(int rows, const float* __res
     const float4 a4 = row_get(ah, i, c0);
     o[0] += a4.x, o[1] += a4.y, o[2] += a4.z, o[3] += a4.w;
     row_store(ah, i, c0, o);
+  }
+  if (Wn) {  // the next msg unit's vdot = abar_h' Wn (saves its row-GEMM launch)
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) X[r][c0 + q] = o[q];
+    __syncthreads();
+    rowmm_eo(X, Ws + 4 * 4096, r, c0, o);
+    if (i < rows) row_store(vdot_out, i, c0, o);
   }
 }
 

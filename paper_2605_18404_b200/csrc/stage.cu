@@ -465,7 +465,8 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
     JANUS_CUDA(cudaFuncSetAttribute(edge::msg_ff_kernel<kH, kR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge::ff_smem<kH, kR>()));
     JANUS_CUDA(cudaFuncSetAttribute(edge::msg_bf_kernel<kH, kR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge::bf_smem<kH, kR>()));
     JANUS_CUDA(cudaFuncSetAttribute(edge::msg_be_kernel<kH, kR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge::be_smem<kH, kR>()));
-    JANUS_CUDA(cudaFuncSetAttribute(node::upd_bf_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)node::upd_smem(4)));
+    JANUS_CUDA(cudaFuncSetAttribute(node::upd_bf_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)node::upd_smem(5)));
+    JANUS_CUDA(cudaFuncSetAttribute(node::upd_fe_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)node::upd_smem(3)));
     JANUS_CUDA(cudaFuncSetAttribute(edge_tc::msg_fe_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge_tc::fe_smem()));
     JANUS_CUDA(cudaFuncSetAttribute(edge_tc::msg_ff_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge_tc::ff_smem()));
     JANUS_CUDA(cudaFuncSetAttribute(edge_tc::msg_filter_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge_tc::filter_smem()));
@@ -745,6 +746,7 @@ void stage_fe(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
   const float* cur_h = st->u0 > 0 ? port_h(sl.ports[JANUS_PORT_ACT_IN], N) : nullptr;
   const float* cur_m = st->in_has_m ? port_m(sl.ports[JANUS_PORT_ACT_IN], N) : nullptr;
   const bool pairs = use_tc(st) && st->pair_feff;
+  bool v_ready = false;  // the upd kernel before a msg unit already wrote its v
   if (pairs && g.n_pairs > 0 && !(prof_skip() & 1)) launch_filter(st, g, sl, -1, s);  // w, w' of every msg unit
   for (int u = st->u0; u < st->u1; ++u) {
     UnitBufs& b = sl.units[static_cast<size_t>(u - st->u0)];
@@ -756,7 +758,8 @@ void stage_fe(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
         break;
       case kMsg: {
         const float* W = P + R * H + H + H * H + H;
-        gemm(s, N, cur_h, W, nullptr, nullptr, nullptr, b.v);
+        if (!v_ready) gemm(s, N, cur_h, W, nullptr, nullptr, nullptr, b.v);
+        v_ready = false;
         if (pairs) {
           if (!(prof_skip() & 1))
             JANUS_ROWS(msg_fe_rows, blocks(N, 8), s, N, g.row_ptr, g.col, g.pidx, b.wf, b.v, b.out_m);
@@ -770,7 +773,14 @@ void stage_fe(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
       }
       case kUpd: {
         const float *Um = P, *ups = P + H * H, *V = P + H * H + H;
-        if (!(prof_skip() & 32)) node::upd_fe_fused<<<blocks(N, node::kRB), 256, node::upd_smem(2), s>>>(N, cur_m, cur_h, Um, ups, V, b.p, b.out_h);
+        // the next msg unit's v = h' W computed in the same kernel
+        const bool fuse = u + 1 < st->u1 && unit_kind(u + 1, L) == kMsg;
+        const float* Wn = fuse ? st->P(u + 1) + R * H + H + H * H + H : nullptr;
+        float* vn = fuse ? sl.units[static_cast<size_t>(u + 1 - st->u0)].v : nullptr;
+        if (!(prof_skip() & 32))
+          node::upd_fe_fused<<<blocks(N, node::kRB), 256, node::upd_smem(fuse ? 3 : 2), s>>>(N, cur_m, cur_h, Um, ups, V, b.p,
+                                                                                              b.out_h, Wn, vn);
+        v_ready = fuse;
         cur_h = b.out_h;
         cur_m = nullptr;
         break;
@@ -885,6 +895,7 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
     if (in.has_m) copy(s, am, port_m(in, N), NH);
     Fbar = port_v(in, N);
   }
+  bool vdot_ready = false;  // the upd kernel before a msg unit already wrote its vdot
   for (int u = st->u0; u < st->u1; ++u) {
     UnitBufs& b = sl.units[static_cast<size_t>(u - st->u0)];
     const float* P = st->P(u);
@@ -895,7 +906,8 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
         break;
       case kMsg: {
         const float* W = P + R * H + H + H * H + H;
-        gemm(s, N, ah, W, nullptr, nullptr, nullptr, sc.s1);  // vdot
+        if (!vdot_ready) gemm(s, N, ah, W, nullptr, nullptr, nullptr, sc.s1);  // vdot
+        vdot_ready = false;
         const bool pairs = use_tc(st) && st->pair_bfbe;
         if (pairs) {  // weight gradients once per pair + row sums from the stored filters (+ hbar^F = X W^T)
           const int grid = pair_grid(st, g);
@@ -933,8 +945,14 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
         const float *Um = P, *V = P + H * H + H;
         float *dU = G2, *dups = G2 + H * H, *dV = G2 + H * H + H;
         // pdot, r, pbar (s3), pdbar (s4), u (s5), mbar^F = pbar U^T, abar' = abar_h + u V
-        if (!(prof_skip() & 32)) node::upd_bf_fused<<<blocks(N, node::kRB), 256, node::upd_smem(4), s>>>(N, am, b.ff_a, b.p, Um, T + H * H, T, V, sc.s3, sc.s4,
-                                                                sc.s5, b.inj, ah);
+        // + the next msg unit's vdot = abar_h' W in the same kernel
+        const bool fuse = u + 1 < st->u1 && unit_kind(u + 1, L) == kMsg;
+        const float* Wn = fuse ? st->P(u + 1) + R * H + H + H * H + H : nullptr;
+        if (!(prof_skip() & 32))
+          node::upd_bf_fused<<<blocks(N, node::kRB), 256, node::upd_smem(fuse ? 5 : 4), s>>>(N, am, b.ff_a, b.p, Um, T + H * H, T, V,
+                                                                                              sc.s3, sc.s4, sc.s5, b.inj, ah, Wn,
+                                                                                              fuse ? sc.s1 : nullptr);
+        vdot_ready = fuse;
         wjobs(st, sc, s, N, {wjob(sc.s5, b.ff_a, dV),                                          // dV2 = u^T a'
                          wjob(in_m(st, sl, u, N), sc.s3, dU, am, sc.s4, false, sc.s3, dups)});  // dU2, dups2
         break;
