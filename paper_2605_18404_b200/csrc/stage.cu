@@ -1000,6 +1000,14 @@ void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only, 
     copy(s, bh, port_h(in, N), NH);
     if (in.has_m) copy(s, bm, port_m(in, N), NH);
   }
+  // a msg unit's dW1 job waits for the next (upd) unit's launch: its inputs
+  // (in_h, Yb in s1) are not touched by upd_be_fused, so one launch serves both
+  node::WJob pend{};
+  bool has_pend = false;
+  auto flush = [&] {
+    if (has_pend) wjobs(st, sc, s, N, {pend});
+    has_pend = false;
+  };
   for (int u = st->u1 - 1; u >= st->u0; --u) {
     UnitBufs& b = sl.units[static_cast<size_t>(u - st->u0)];
     const float* P = st->P(u);
@@ -1024,8 +1032,13 @@ void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only, 
         float *dU = G1, *dups = G1 + H * H, *dV = G1 + H * H + H;
         // pbar (s2) = (b' V^T) SiLU'(p); b_m = pbar U^T + mbar^F
         if (!(prof_skip() & 32)) node::upd_be_fused<<<blocks(N, node::kRB), 256, node::upd_smem(2), s>>>(N, bh, b.p, T + H * H, T, b.inj, sc.s2, bm);
-        wjobs(st, sc, s, N, {wjob(b.p, bh, dV, nullptr, nullptr, true),                                  // dV1 = SiLU(p)^T b'
-                         wjob(in_m(st, sl, u, N), sc.s2, dU, nullptr, nullptr, false, sc.s2, dups)});  // dU1, dups1
+        const node::WJob jv = wjob(b.p, bh, dV, nullptr, nullptr, true);                           // dV1 = SiLU(p)^T b'
+        const node::WJob ju = wjob(in_m(st, sl, u, N), sc.s2, dU, nullptr, nullptr, false, sc.s2, dups);  // dU1, dups1
+        if (has_pend)
+          wjobs(st, sc, s, N, {pend, jv, ju});
+        else
+          wjobs(st, sc, s, N, {jv, ju});
+        has_pend = false;
         break;
       }
       case kMsg: {
@@ -1057,17 +1070,21 @@ void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only, 
         } else {
           JANUS_CUDA(cudaMemsetAsync(sc.s1, 0, sizeof(float) * NH, s));
         }
-        wjobs(st, sc, s, N, {wjob(in_h(st, sl, u, N), sc.s1, G1 + EC::PE)});  // dW1 = h^T Yb
+        flush();
+        pend = wjob(in_h(st, sl, u, N), sc.s1, G1 + EC::PE);  // dW1 = h^T Yb (launched with the next upd's jobs)
+        has_pend = true;
         if (!pairs && !(g.n_tiles > 0 && use_tc(st))) gemm(s, N, sc.s1, T + H * H, nullptr, bh, b.inj, bh);  // b_h += Yb W^T + hbar^F
         break;
       }
       case kEmbed:
+        flush();
         species_sum(st, sc, s, g, bh, nullptr, G1);
         break;
     }
     JANUS_LAUNCH_CHECK("stage_be");
     (void)R;
   }
+  flush();
   if (st->u0 > 0) {
     const Port& out = sl.ports[JANUS_PORT_BADJ_OUT];
     copy(s, port_h(out, N), bh, NH);
