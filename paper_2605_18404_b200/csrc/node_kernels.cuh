@@ -598,8 +598,8 @@ __global__ void __launch_bounds__(256) upd_bf_fused(int rows, const float* __res
                                                     const float* __restrict__ Vt, const float* __restrict__ Ut,
                                                     const float* __restrict__ V, float* __restrict__ pbar,
                                                     float* __restrict__ pdbar, float* __restrict__ u,
-                                                    float* __restrict__ inj, float* ah, const float* __restrict__ Wn,
-                                                    float* __restrict__ vdot_out) {
+                                                    float* __restrict__ inj, const float* ah, float* ah_out,
+                                                    const float* __restrict__ Wn, float* __restrict__ vdot_out) {
   __shared__ __align__(16) float X[kRB][68];
   __shared__ __align__(16) float Y[kRB][68];
   extern __shared__ __align__(16) float Ws[];
@@ -641,7 +641,7 @@ __global__ void __launch_bounds__(256) upd_bf_fused(int rows, const float* __res
   if (i < rows) {
     const float4 a4 = row_get(ah, i, c0);
     o[0] += a4.x, o[1] += a4.y, o[2] += a4.z, o[3] += a4.w;
-    row_store(ah, i, c0, o);
+    row_store(ah_out, i, c0, o);  // ah_out may alias ah (same element, read first)
   }
   if (Wn) {  // the next msg unit's vdot = abar_h' Wn (saves its row-GEMM launch)
     __syncthreads();

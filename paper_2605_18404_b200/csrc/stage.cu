@@ -15,6 +15,7 @@
 #include <initializer_list>
 #include <limits>
 #include <stdexcept>
+#include <utility>
 #include <vector>
 
 #include "../../include/janus/errors.hpp"
@@ -449,6 +450,7 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
     if (const char* e = std::getenv("JANUS_BFBE_PAIR")) st->pair_bfbe = st->pair_feff && std::atoi(e) != 0;
     for (Scratch& sc : st->lanes) {
       sc.wh = dalloc<float>(st, NH, false);
+      sc.wh2 = dalloc<float>(st, NH, false);
       sc.wm = dalloc<float>(st, NH, false);
       sc.s1 = dalloc<float>(st, NH, false);
       sc.s2 = dalloc<float>(st, NH, false);
@@ -895,6 +897,16 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
     if (in.has_m) copy(s, am, port_m(in, N), NH);
     Fbar = port_v(in, N);
   }
+  // a_h ping-pongs between wh and wh2 at every upd unit, so a msg unit's
+  // weight-gradient job (which reads a_h at msg time) can wait for the next
+  // upd unit's launch
+  float* ah_alt = sc.wh2;
+  node::WJob pend{};
+  bool has_pend = false;
+  auto flush = [&] {
+    if (has_pend) wjobs(st, sc, s, N, {pend});
+    has_pend = false;
+  };
   bool vdot_ready = false;  // the upd kernel before a msg unit already wrote its vdot
   for (int u = st->u0; u < st->u1; ++u) {
     UnitBufs& b = sl.units[static_cast<size_t>(u - st->u0)];
@@ -903,6 +915,7 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
     float* G2 = ledger(st, st->g2, mb, u);
     switch (unit_kind(u, L)) {
       case kEmbed:
+        flush();
         break;
       case kMsg: {
         const float* W = P + R * H + H + H * H + H;
@@ -938,7 +951,9 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
           JANUS_CUDA(cudaMemsetAsync(sc.s2, 0, sizeof(float) * NH, s));
         }
         if (!pairs && !(g.n_tiles > 0 && use_tc(st))) gemm(s, N, sc.s2, T + H * H, nullptr, nullptr, nullptr, b.inj);  // hbar^F = X W^T
-        wjobs(st, sc, s, N, {wjob(in_h(st, sl, u, N), sc.s2, G2 + EC::PE, ah, b.ff_Y)});  // dW2 = h^T X + abar^T Y
+        flush();
+        pend = wjob(in_h(st, sl, u, N), sc.s2, G2 + EC::PE, ah, b.ff_Y);  // dW2 = h^T X + abar^T Y (with the next upd's jobs)
+        has_pend = true;
         break;
       }
       case kUpd: {
@@ -950,14 +965,21 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
         const float* Wn = fuse ? st->P(u + 1) + R * H + H + H * H + H : nullptr;
         if (!(prof_skip() & 32))
           node::upd_bf_fused<<<blocks(N, node::kRB), 256, node::upd_smem(fuse ? 5 : 4), s>>>(N, am, b.ff_a, b.p, Um, T + H * H, T, V,
-                                                                                              sc.s3, sc.s4, sc.s5, b.inj, ah, Wn,
+                                                                                              sc.s3, sc.s4, sc.s5, b.inj, ah, ah_alt, Wn,
                                                                                               fuse ? sc.s1 : nullptr);
         vdot_ready = fuse;
-        wjobs(st, sc, s, N, {wjob(sc.s5, b.ff_a, dV),                                          // dV2 = u^T a'
-                         wjob(in_m(st, sl, u, N), sc.s3, dU, am, sc.s4, false, sc.s3, dups)});  // dU2, dups2
+        std::swap(ah, ah_alt);
+        const node::WJob jv = wjob(sc.s5, b.ff_a, dV);                                       // dV2 = u^T a'
+        const node::WJob ju = wjob(in_m(st, sl, u, N), sc.s3, dU, am, sc.s4, false, sc.s3, dups);  // dU2, dups2
+        if (has_pend)
+          wjobs(st, sc, s, N, {pend, jv, ju});
+        else
+          wjobs(st, sc, s, N, {jv, ju});
+        has_pend = false;
         break;
       }
       case kReadout: {
+        flush();  // (its kernels rewrite s2)
         const float *O = P, *om = P + H * H + H;
         float *dO = G2, *dob = G2 + H * H, *dom = G2 + H * H + H;
         gemm(s, N, ah, O, nullptr, nullptr, nullptr, sc.s1);  // tdot
@@ -970,6 +992,7 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
     }
     JANUS_LAUNCH_CHECK("stage_bf");
   }
+  flush();
   if (st->u1 < st->U) {
     const Port& out = sl.ports[JANUS_PORT_TAN_OUT];
     copy(s, port_h(out, N), ah, NH);

@@ -81,7 +81,7 @@ struct Port {
 // Per-lane scratch: phases of different micro-batches may run concurrently on
 // different streams ("lanes") of one device; all transient buffers are per lane.
 struct Scratch {
-  float *wh = nullptr, *wm = nullptr, *s1 = nullptr, *s2 = nullptr, *s3 = nullptr, *s4 = nullptr, *s5 = nullptr;
+  float *wh = nullptr, *wh2 = nullptr, *wm = nullptr, *s1 = nullptr, *s2 = nullptr, *s3 = nullptr, *s4 = nullptr, *s5 = nullptr;
   float *partial = nullptr, *wpart = nullptr;
   unsigned* counter = nullptr;  // last-CTA-reduces launch counter (one launch at a time per lane)
 };
