@@ -347,9 +347,11 @@ def main():
             # timed with the step's concurrency: all micro-batches launched on the step's lanes
             # with the step's grid, CUDA events around whole rounds (P == 1; else isolated)
             wk = 4 if args.precision == "tf32" else 2
-            if P == 1:
-                ms_bf, ne, fl = st.time_edge_kernel(wk, -1, iters=20)
-                how = "all micro-batches per round on the step's lanes and grids (CUDA events per round)"
+            if P == 1:  # median of 5 timings of 20 rounds each (single timings vary by up to +-20%)
+                runs = sorted((st.time_edge_kernel(wk, -1, iters=20) for _ in range(5)), key=lambda x: x[0])
+                ms_bf, ne, fl = runs[2]
+                how = ("all micro-batches per round on the step's lanes and grids (CUDA events per round; "
+                       "median of 5 x 20 rounds)")
             else:
                 ms_bf, ne, fl = st.time_edge_kernel(wk, 0, iters=50)
                 how = "one micro-batch, back-to-back launches"
