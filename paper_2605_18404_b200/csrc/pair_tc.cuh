@@ -554,6 +554,31 @@ __global__ void __launch_bounds__(NT, 1) msg_be_pair_tc(EdgeGeom g, const float4
   teardown(c, 512);
 }
 
+// The BF / BE pair kernels' per-CTA partials, summed into the phase's ledger
+// slice by extra CTAs of the row kernel that follows (one thread per column,
+// partials in CTA order: the arithmetic of edge::reduce_partials_seq_kernel,
+// one launch fewer per pair kernel and no serial tail).
+struct PartialReduce {
+  const float* partial = nullptr;
+  int n = 0;
+  float* G = nullptr;
+};
+__host__ __device__ constexpr int reduce_blocks(const PartialReduce& r) { return r.G ? (PE + 255) / 256 : 0; }
+__device__ __forceinline__ void reduce_block(const PartialReduce& r, int blk) {
+  const int p = blk * 256 + static_cast<int>(threadIdx.x);
+  if (p >= PE) return;
+  const float* src = r.partial + p;
+  float s = 0.f;
+  int t = 0;
+  for (; t + 4 <= r.n; t += 4) {
+    const float a = __ldg(src + (size_t)t * PE), b = __ldg(src + (size_t)(t + 1) * PE);
+    const float c = __ldg(src + (size_t)(t + 2) * PE), d = __ldg(src + (size_t)(t + 3) * PE);
+    s = (((s + a) + b) + c) + d;
+  }
+  for (; t < r.n; ++t) s += __ldg(src + (size_t)t * PE);
+  r.G[p] = s;
+}
+
 // BF rows: mdot_i = sum_e qb_e w'_p v_j + w_p vdot_j ; X_i = sum_e qb_e w'_p am_j ;
 // inj = X W^T (hbar^F of the unit input), qb_e = <Fbar_i - Fbar_j, u_e>
 template <int KF>  // edges whose gathers are in flight per step
@@ -563,7 +588,13 @@ __global__ void __launch_bounds__(256) msg_bf_rows(int n_atoms, const int* __res
                                                    const float* __restrict__ wp, const float* __restrict__ v,
                                                    const float* __restrict__ vdot, const float* __restrict__ am,
                                                    const float* __restrict__ wt, float* __restrict__ mdot_out,
-                                                   float* __restrict__ X_out, float* __restrict__ inj) {
+                                                   float* __restrict__ X_out, float* __restrict__ inj,
+                                                   const __grid_constant__ PartialReduce red) {
+  const int row_blocks = (n_atoms + 7) / 8;
+  if (static_cast<int>(blockIdx.x) >= row_blocks) {
+    reduce_block(red, static_cast<int>(blockIdx.x) - row_blocks);
+    return;
+  }
   const int i = blockIdx.x * 8 + static_cast<int>(threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (i >= n_atoms) return;
   const int eb = __ldg(row_ptr + i), ee = __ldg(row_ptr + i + 1);
@@ -615,7 +646,13 @@ template <int KF>  // edges whose gathers are in flight per step
 __global__ void __launch_bounds__(256) msg_be_rows(int n_atoms, const int* __restrict__ row_ptr, const int* __restrict__ col,
                                                    const int* __restrict__ pidx, const float* __restrict__ w,
                                                    const float* __restrict__ bm, const float* __restrict__ wt,
-                                                   float* __restrict__ Yb_out, const float* __restrict__ inj, float* bh) {
+                                                   float* __restrict__ Yb_out, const float* __restrict__ inj, float* bh,
+                                                   const __grid_constant__ PartialReduce red) {
+  const int row_blocks = (n_atoms + 7) / 8;
+  if (static_cast<int>(blockIdx.x) >= row_blocks) {
+    reduce_block(red, static_cast<int>(blockIdx.x) - row_blocks);
+    return;
+  }
   const int i = blockIdx.x * 8 + static_cast<int>(threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (i >= n_atoms) return;
   const int eb = __ldg(row_ptr + i), ee = __ldg(row_ptr + i + 1);

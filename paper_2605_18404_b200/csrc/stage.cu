@@ -930,10 +930,13 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
                                                                                        sc.s1, b.ff_a, Fbar, sc.partial);
             JANUS_LAUNCH_CHECK("msg_bf_pair_tc");
           }
-          if (g.n_pairs > 0 && !(prof_skip() & 128)) edge::reduce_partials(sc.partial, grid, EC::PE, G2, s);
+          edge_tc::PartialReduce red;  // the partials' reduction rides in the row kernel's launch
+          if (g.n_pairs > 0 && !(prof_skip() & 128)) red = {sc.partial, grid, G2};
           if (!(prof_skip() & 4))
-            JANUS_ROWS(msg_bf_rows, blocks(N, 8), s, N, g.row_ptr, g.col, g.pidx, g.u, Fbar, b.wf, b.wfp, b.v, sc.s1, b.ff_a,
-                                                               mp.pack + edge_tc::kWtOff / sizeof(float), am, sc.s2, b.inj);
+            JANUS_ROWS(msg_bf_rows, blocks(N, 8) + edge_tc::reduce_blocks(red), s, N, g.row_ptr, g.col, g.pidx, g.u, Fbar, b.wf,
+                       b.wfp, b.v, sc.s1, b.ff_a, mp.pack + edge_tc::kWtOff / sizeof(float), am, sc.s2, b.inj, red);
+          else if (red.G)
+            edge::reduce_partials(sc.partial, grid, EC::PE, G2, s);
         } else if (g.n_tiles > 0 && use_tc(st)) {
           const int grid = tc_grid(st, g);
           if (!(prof_skip() & 4)) edge_tc::msg_bf_tc<<<grid, edge_tc::NT, edge_tc::bf_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, msg_params(st, u),
@@ -1074,10 +1077,13 @@ void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only, 
                                                                                        sc.partial);
             JANUS_LAUNCH_CHECK("msg_be_pair_tc");
           }
-          if (g.n_pairs > 0 && !(prof_skip() & 128)) edge::reduce_partials(sc.partial, grid, EC::PE, G1, s);
+          edge_tc::PartialReduce red;  // the partials' reduction rides in the row kernel's launch
+          if (g.n_pairs > 0 && !(prof_skip() & 128)) red = {sc.partial, grid, G1};
           if (!(prof_skip() & 8))  // Yb; b_h += Yb W^T + hbar^F
-            JANUS_ROWS(msg_be_rows, blocks(N, 8), s, N, g.row_ptr, g.col, g.pidx, b.wf, bm,
-                                                               mp.pack + edge_tc::kWtOff / sizeof(float), sc.s1, b.inj, bh);
+            JANUS_ROWS(msg_be_rows, blocks(N, 8) + edge_tc::reduce_blocks(red), s, N, g.row_ptr, g.col, g.pidx, b.wf, bm,
+                       mp.pack + edge_tc::kWtOff / sizeof(float), sc.s1, b.inj, bh, red);
+          else if (red.G)
+            edge::reduce_partials(sc.partial, grid, EC::PE, G1, s);
         } else if (g.n_tiles > 0 && use_tc(st)) {
           const int grid = tc_grid(st, g);
           if (!(prof_skip() & 8)) edge_tc::msg_be_tc<<<grid, edge_tc::NT, edge_tc::be_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, msg_params(st, u),
@@ -1227,12 +1233,13 @@ void launch_edge_kernel(janus_stage* st, int u, int which, int mb, int slot, int
         edge_tc::msg_bf_pair_tc<<<grid, edge_tc::NT, edge_tc::bf_pair_smem(), s>>>(eg, g.pgeo, g.n_pairs, mp, st->m.r_c, b.v, sc.s1,
                                                                                    b.ff_a, sl.Fbar, sc.partial);
       JANUS_ROWS(msg_bf_rows, blocks(N, 8), s, N, g.row_ptr, g.col, g.pidx, g.u, sl.Fbar, b.wf, b.wfp, b.v, sc.s1, b.ff_a, wt,
-                                                         sc.s3, sc.s4, nullptr);
+                                                         sc.s3, sc.s4, nullptr, edge_tc::PartialReduce{});
     } else {
       if (g.n_pairs > 0)
         edge_tc::msg_be_pair_tc<<<grid, edge_tc::NT, edge_tc::be_pair_smem(), s>>>(eg, g.pgeo, g.n_pairs, mp, st->m.r_c, b.v, sc.s2,
                                                                                    sc.partial);
-      JANUS_ROWS(msg_be_rows, blocks(N, 8), s, N, g.row_ptr, g.col, g.pidx, b.wf, sc.s2, wt, sc.s3, nullptr, nullptr);
+      JANUS_ROWS(msg_be_rows, blocks(N, 8), s, N, g.row_ptr, g.col, g.pidx, b.wf, sc.s2, wt, sc.s3, nullptr, nullptr,
+                 edge_tc::PartialReduce{});
     }
     return;
   }
