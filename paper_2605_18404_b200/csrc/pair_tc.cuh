@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(1024) pairs_kernel(const __grid_constant__ nod
   for (int e0 = 0; e0 < jb.n_edges; e0 += 1024) {
     const int e = e0 + static_cast<int>(threadIdx.x);
     const int r = e < jb.n_edges ? jb.rev[e] : -1;
-    const bool flag = e < jb.n_edges && e < r;
+    const bool flag = e < jb.n_edges && e < r && r < jb.n_edges;
     const unsigned bal = __ballot_sync(0xffffffffu, flag);
     if (lane == 0) wsum[warp] = __popc(bal);
     __syncthreads();
@@ -143,8 +143,8 @@ __global__ void __launch_bounds__(1024) pairs_kernel(const __grid_constant__ nod
       excl += w < warp ? s : 0;
       total += s;
     }
-    if (flag) {
-      const int pos = base + excl + __popc(bal & ((1u << lane) - 1u));
+    const int pos = base + excl + __popc(bal & ((1u << lane) - 1u));
+    if (flag && pos < (jb.n_edges >> 1)) {  // (a rev that is not an involution — host-checked at load — never writes past the tables)
       jb.pcanon[pos] = e;
       jb.pidx[e] = pos;
       jb.pidx[r] = pos;

@@ -594,6 +594,11 @@ void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_
   g.n_tiles = static_cast<int>(tiles.size()) - 1;
   g.n_tiles_tc = static_cast<int>(tiles_tc.size()) - 1;
   if (use_tc(st) && E % 2) throw domain_error("odd edge count: every edge needs a distinct reverse edge");
+  if (use_tc(st) && !dcsr)  // host CSR: the pair tables need rev to be a fixed-point-free involution
+    for (int e = 0; e < E; ++e) {
+      const int r = hb.rev[e];
+      if (r < 0 || r >= E || r == e || hb.rev[r] != e) throw domain_error("rev must pair every edge with a distinct reverse edge");
+    }
   g.n_pairs = E / 2;
   // one pinned image per load (alternating halves: the other may still feed
   // a queued copy), one host->device copy

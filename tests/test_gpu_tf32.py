@@ -124,3 +124,19 @@ def test_tf32_pair_kernels_timed(janus, case):
         assert ne == b.n_edges and fl > 0 and ms > 0
         print(f"tc {name}: {ms * 1e3:.1f} us, {fl / ms / 1e9:.2f} TFLOP/s")
     st.close()
+
+
+def test_tf32_rejects_unpaired_rev(janus, has_gpu):
+    """Tensor-core mode builds its edge-pair tables from rev: a host CSR whose
+    rev is not a fixed-point-free involution is rejected at load (domain error)."""
+    if not has_gpu:
+        pytest.skip("no GPU")
+    m = janus.Model(L=2, H=64, R=64, precision=janus.PREC_TF32)
+    params = m.synth_params(5)
+    b = janus.synth_batch(m, [24], 0.095, 3)
+    b.rev = b.rev.copy()
+    b.rev[0], b.rev[1] = 1, 0  # edges 0 and 1 are not each other's reverse
+    st = janus.Stage(m, params, 0, m.n_units, max_atoms=64, max_edges=64 * 120, max_struct=1)
+    with pytest.raises(janus.JanusError):
+        st.load(0, b)
+    st.close()
