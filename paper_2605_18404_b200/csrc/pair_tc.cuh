@@ -98,26 +98,30 @@ __global__ void __launch_bounds__(NT, JANUS_FEFF_CTAS) msg_filter_tc(EdgeGeom g,
       tc::commit(c.mbar);
     }
     c.wait_mma();
-    {
+    {  // w, w' into the (now free) operand tiles, swizzled plain rows (st_pl: conflict-free)
       float gg[FPT], gp[FPT];
       c.ld2(TM_G, TM_GP, gg, gp);
-      if (ok) {
-        float4* wo = reinterpret_cast<float4*>(wout + (size_t)p * H + f0);
-        float4* wpo = reinterpret_cast<float4*>(wpout + (size_t)p * H + f0);
 #pragma unroll
-        for (int q = 0; q < FPT / 4; ++q) {
-          float w4[4], p4[4];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const float gb = gg[4 * q + k] + be[f0 + 4 * q + k];
-            w4[k] = cc * gb;
-            p4[k] = dc * gb + cc * gp[4 * q + k];
-          }
-          wo[q] = make_float4(w4[0], w4[1], w4[2], w4[3]);
-          wpo[q] = make_float4(p4[0], p4[1], p4[2], p4[3]);
-        }
+      for (int k = 0; k < FPT; ++k) {
+        const float gb = gg[k] + be[f0 + k];
+        gg[k] = cc * gb;
+        gp[k] = dc * gb + cc * gp[k];
+      }
+      st_pl(T0, c.e, f0, gg);
+      st_pl(T1, c.e, f0, gp);
+    }
+    __syncthreads();
+    {  // coalesced copy-out: the chunk's pairs are contiguous rows of w / w' ([pair][64])
+      const int np = min(TE, n_pairs - ch * TE);
+      float4* wo = reinterpret_cast<float4*>(wout + (size_t)ch * TE * H);
+      float4* wpo = reinterpret_cast<float4*>(wpout + (size_t)ch * TE * H);
+      for (int x = threadIdx.x; x < np * 16; x += NT) {
+        const uint32_t o = off_pl(x >> 4, 4 * (x & 15));
+        wo[x] = *reinterpret_cast<const float4*>(T0 + o);
+        wpo[x] = *reinterpret_cast<const float4*>(T1 + o);
       }
     }
+    __syncthreads();  // T0 / T1 are the next chunk's operand tiles
   }
   teardown(c, 256);
 }
