@@ -197,3 +197,17 @@ def test_tensor_core_pipeline_lanes_bit_identical(janus, P, method, k):
         t.close()
     assert out[0][0] == out[1][0]
     assert np.array_equal(out[0][1], out[1][1]) and np.array_equal(out[0][2], out[1][2])
+
+
+@pytest.mark.parametrize("P,method", [(1, 0), (2, 1)])
+def test_tensor_core_trainer_ragged_matches_oracle(janus, data, P, method):
+    """Tensor-core mode through the executor on ragged micro-batches (27..40
+    atoms: every micro-batch has its own pair count, pair-kernel grid and
+    partial count): the summed gradient matches the fp64 oracle within the
+    tensor-core tolerance (tests/test_gpu_tf32.py: 2e-2 of the max)."""
+    m, params, batches, g_ref, _ = data
+    m_tc = janus.Model(L=m.L, H=m.H, R=m.R, precision=janus.PREC_TF32)
+    t, g, _, _ = run(janus, m_tc, params, batches, P, method, k=2 if method == 1 else 1)
+    t.close()
+    err = float(np.abs(g - g_ref).max() / np.abs(g_ref).max())
+    assert err < 2e-2, err
