@@ -227,7 +227,10 @@ int janus_trainer_step(janus_trainer* t, const janus_opt* opt, janus_step_stats*
  * and fill stats (loss read back).  Loads issued in between run beside the
  * step in flight (into the other geometry copy), so the next step's uploads,
  * neighbour lists and geometry overlap this step's device time (input
- * pipelining).  janus_trainer_step == step_async + wait. */
+ * pipelining).  Up to two steps may be in flight: janus_trainer_wait
+ * returns the oldest one (its loss terms are snapshotted on the device when
+ * the step ends), so a training loop can issue step k+1 before reading step k
+ * back.  janus_trainer_step == step_async + wait. */
 int janus_trainer_step_async(janus_trainer* t, const janus_opt* opt);
 int janus_trainer_wait(janus_trainer* t, janus_step_stats* stats);
 /* per compute instruction of the last timed step: [n][5] = device, kind, mb, start_us, end_us */

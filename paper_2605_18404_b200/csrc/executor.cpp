@@ -117,7 +117,13 @@ struct janus_trainer {
   janus::DepGraph graph;
   std::vector<janus::Rec> recs;
   bool recording = false;
-  bool pending = false;  // a step issued by trainer_step_async not yet waited for
+  // steps issued by trainer_step_async and not yet waited for (at most two: the
+  // host may issue step k+1 before reading step k back, so the GPU never idles
+  // on the host between steps); per issue parity: anchor / finish events and a
+  // device snapshot of the loss terms taken right after the step
+  int inflight = 0;
+  cudaEvent_t anchor_q[2] = {nullptr, nullptr}, finish_q[2] = {nullptr, nullptr}, done_q[2] = {nullptr, nullptr};
+  float* loss_snap[2] = {nullptr, nullptr};
   int64_t p2p_bytes = 0;
   int64_t kernel_count = -1;
   cudaGraphExec_t gexec = nullptr;               // instantiated step graph for key gkey (geometry parities)
@@ -580,6 +586,12 @@ janus_trainer* trainer_create(const janus_exec_desc& ed, const janus_stage_desc&
   JANUS_CUDA(cudaStreamCreateWithFlags(&t->root, cudaStreamNonBlocking));
   JANUS_CUDA(cudaEventCreate(&t->anchor));
   JANUS_CUDA(cudaEventCreate(&t->finish));
+  for (int q = 0; q < 2; ++q) {
+    JANUS_CUDA(cudaEventCreate(&t->anchor_q[q]));
+    JANUS_CUDA(cudaEventCreate(&t->finish_q[q]));
+    JANUS_CUDA(cudaEventCreateWithFlags(&t->done_q[q], cudaEventDisableTiming));
+    JANUS_CUDA(cudaMalloc(&t->loss_snap[q], sizeof(float) * 4 * static_cast<size_t>(std::max(1, ed.n_micro_batches))));
+  }
   auto make = [&](int b) {
     janus_stage_desc d = sd;
     d.unit_begin = t->plan.blocks[static_cast<size_t>(b)].first;
@@ -670,6 +682,12 @@ void trainer_destroy(janus_trainer* t) {
   if (t->root) cudaStreamDestroy(t->root);
   if (t->anchor) cudaEventDestroy(t->anchor);
   if (t->finish) cudaEventDestroy(t->finish);
+  for (int q = 0; q < 2; ++q) {
+    if (t->anchor_q[q]) cudaEventDestroy(t->anchor_q[q]);
+    if (t->finish_q[q]) cudaEventDestroy(t->finish_q[q]);
+    if (t->done_q[q]) cudaEventDestroy(t->done_q[q]);
+    if (t->loss_snap[q]) cudaFree(t->loss_snap[q]);
+  }
   delete t;
 }
 
@@ -774,7 +792,7 @@ void trainer_note_shape(janus_trainer* t, int mb, const janus_host_batch& hb, in
   if (cur != sh) {
     cur = sh;
     if (t->gexec || t->gexec_alt) {
-      if (t->pending) JANUS_CUDA(cudaEventSynchronize(t->finish));  // the old graph may still be running
+      if (t->inflight) JANUS_CUDA(cudaStreamSynchronize(t->root));  // the old graphs may still be running
       if (t->gexec) JANUS_CUDA(cudaGraphExecDestroy(t->gexec));
       if (t->gexec_alt) JANUS_CUDA(cudaGraphExecDestroy(t->gexec_alt));
       t->gexec = t->gexec_alt = nullptr;
@@ -833,7 +851,8 @@ cudaGraphExec_t capture_step(janus_trainer* t, const janus_opt& opt, int64_t* nk
 // their host-side cost with this step's device time.
 void trainer_step_async(janus_trainer* t, const janus_opt& opt) {
   JANUS_CUDA(cudaSetDevice(t->sd.device));
-  if (t->pending) throw state_error("a step is already in flight (call janus_trainer_wait)");
+  if (t->inflight >= 2) throw state_error("two steps are already in flight (call janus_trainer_wait)");
+  if (t->inflight && t->ed.record_timeline) throw state_error("a timed step is in flight (call janus_trainer_wait)");
   for (int m = 0; m < t->ed.n_micro_batches; ++m)
     if (t->n_atoms[static_cast<size_t>(m)] <= 0) throw state_error("micro-batch " + std::to_string(m) + " not loaded");
   // loads since the last step: the phases switch to the geometry copies they
@@ -882,6 +901,8 @@ void trainer_step_async(janus_trainer* t, const janus_opt& opt) {
   }
   t->recs.clear();
   t->recording = t->ed.record_timeline != 0;
+  const int q = static_cast<int>(t->nsteps & 1);
+  JANUS_CUDA(cudaEventRecord(t->anchor_q[q], t->root));
   if (exec) {
     JANUS_CUDA(cudaEventRecord(t->anchor, t->root));
     JANUS_CUDA(cudaGraphLaunch(exec, t->root));
@@ -892,21 +913,31 @@ void trainer_step_async(janus_trainer* t, const janus_opt& opt) {
     if (t->local) finalize_local(t, opt);
   }
   JANUS_CUDA(cudaEventRecord(t->finish, t->root));
+  JANUS_CUDA(cudaEventRecord(t->finish_q[q], t->root));  // (the device time ends here)
+  {  // the loss terms of this step, before the next step may overwrite them
+    const size_t n2 = 2 * static_cast<size_t>(t->ed.n_micro_batches);
+    janus_stage* top = t->E[static_cast<size_t>(t->P - 1)];
+    janus_stage* bot = t->F[0];
+    if (top) JANUS_CUDA(cudaMemcpyAsync(t->loss_snap[q], top->losses, sizeof(float) * n2, cudaMemcpyDeviceToDevice, t->root));
+    if (bot) JANUS_CUDA(cudaMemcpyAsync(t->loss_snap[q] + n2, bot->losses, sizeof(float) * n2, cudaMemcpyDeviceToDevice, t->root));
+  }
+  JANUS_CUDA(cudaEventRecord(t->done_q[q], t->root));
   if (t->step_end[0]) JANUS_CUDA(cudaEventRecord(t->step_end[t->nsteps & 1], t->root));
   ++t->nsteps;
-  t->pending = true;
+  ++t->inflight;
 }
 
 // Wait for the step in flight and report it (device time, bubbles, loss: the
 // per-micro-batch loss terms are read back here).
 void trainer_wait(janus_trainer* t, janus_step_stats* stats) {
   JANUS_CUDA(cudaSetDevice(t->sd.device));
-  if (!t->pending) throw state_error("no step in flight");
-  t->pending = false;
-  JANUS_CUDA(cudaEventSynchronize(t->finish));
-  t->recording = false;
+  if (t->inflight <= 0) throw state_error("no step in flight");
+  const int q = static_cast<int>((t->nsteps - t->inflight) & 1);  // the oldest step in flight
+  --t->inflight;
+  JANUS_CUDA(cudaEventSynchronize(t->done_q[q]));
+  if (t->inflight == 0) t->recording = false;
   float ms = 0.f;
-  JANUS_CUDA(cudaEventElapsedTime(&ms, t->anchor, t->finish));
+  JANUS_CUDA(cudaEventElapsedTime(&ms, t->anchor_q[q], t->finish_q[q]));
   janus_step_stats s{};
   s.makespan_ms = ms;
   s.p2p_bytes = t->p2p_bytes;
@@ -939,18 +970,15 @@ void trainer_wait(janus_trainer* t, janus_step_stats* stats) {
   double loss = 0;
   {
     const int n = t->ed.n_micro_batches;
-    std::vector<float> buf(2 * static_cast<size_t>(n));
+    std::vector<float> buf(4 * static_cast<size_t>(n));
     janus_stage* top = t->E[static_cast<size_t>(t->P - 1)];
     janus_stage* bot = t->F[0];
     std::vector<float> lE(static_cast<size_t>(n), 0.f), lF(static_cast<size_t>(n), 0.f);
-    if (top) {
-      JANUS_CUDA(cudaMemcpy(buf.data(), top->losses, sizeof(float) * 2 * n, cudaMemcpyDeviceToHost));
+    JANUS_CUDA(cudaMemcpy(buf.data(), t->loss_snap[q], sizeof(float) * 4 * n, cudaMemcpyDeviceToHost));
+    if (top)
       for (int m = 0; m < n; ++m) lE[static_cast<size_t>(m)] = buf[2 * static_cast<size_t>(m)];
-    }
-    if (bot) {
-      JANUS_CUDA(cudaMemcpy(buf.data(), bot->losses, sizeof(float) * 2 * n, cudaMemcpyDeviceToHost));
-      for (int m = 0; m < n; ++m) lF[static_cast<size_t>(m)] = buf[2 * static_cast<size_t>(m) + 1];
-    }
+    if (bot)
+      for (int m = 0; m < n; ++m) lF[static_cast<size_t>(m)] = buf[2 * static_cast<size_t>(n) + 2 * static_cast<size_t>(m) + 1];
     for (int m = 0; m < n; ++m) loss += static_cast<double>(lE[static_cast<size_t>(m)]) + lF[static_cast<size_t>(m)];
   }
   s.loss = loss;

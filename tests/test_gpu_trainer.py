@@ -211,3 +211,44 @@ def test_tensor_core_trainer_ragged_matches_oracle(janus, data, P, method):
     t.close()
     err = float(np.abs(g - g_ref).max() / np.abs(g_ref).max())
     assert err < 2e-2, err
+
+
+@pytest.mark.parametrize("graphs", [False, True])
+def test_two_steps_in_flight_bit_identical(janus, data, graphs):
+    """bench.py's e2e loop keeps two steps in flight (step k+1 issued before
+    step k's loss is read; step k+2's loads issued while k+1 runs): losses
+    (each read from its own step's snapshot) and parameters match the
+    synchronous loop bit for bit, with the batches changing every step."""
+    m, params, batches, _, _ = data
+    order = [batches, batches[::-1], batches, batches[::-1], batches]
+
+    def make():
+        return janus.Trainer(m, params, 1, janus.METHOD_SYMFOLD, len(batches), k=1, max_atoms=64,
+                             max_edges=64 * 120, graphs=graphs, lanes=2)
+
+    ta = make()
+    la = []
+    for bs in order:
+        ta.load_many(bs)
+        la.append(ta.step().loss)
+    pa = ta.params()
+
+    tb = make()
+    lb = []
+    tb.load_many(order[0])
+    tb.step_async()
+    tb.load_many(order[1])
+    tb.step_async()
+    with pytest.raises(janus.JanusError):
+        tb.step_async()  # at most two in flight
+    for bs in order[2:]:
+        lb.append(tb.wait().loss)
+        tb.load_many(bs)
+        tb.step_async()
+    lb.append(tb.wait().loss)
+    lb.append(tb.wait().loss)
+    pb = tb.params()
+    assert la == lb
+    assert np.array_equal(pa, pb)
+    ta.close()
+    tb.close()
