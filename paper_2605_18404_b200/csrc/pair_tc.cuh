@@ -126,37 +126,65 @@ __global__ void __launch_bounds__(NT, JANUS_FEFF_CTAS) msg_filter_tc(EdgeGeom g,
   teardown(c, 256);
 }
 
-// Pair tables of one micro-batch per CTA (1024 threads): canonical edges in
-// increasing edge order by a block-wide ballot scan, so pidx is deterministic.
-__global__ void __launch_bounds__(1024) pairs_kernel(const __grid_constant__ node::GeoJobs J) {
-  const node::GeoJob& jb = J.j[blockIdx.x];
+// Pair tables, two launches over (1024-edge chunk, micro-batch) CTAs:
+// pairs_count_kernel counts each chunk's canonical edges (e < rev e), then
+// pairs_kernel offsets its chunk by the counts of the chunks before it and
+// ranks the canonical edges with a block-wide ballot scan — canonical edges in
+// increasing edge order, so pidx is deterministic (and independent of the
+// chunking).  counts: [kMaxGeoJobs][chunks_cap].
+__device__ __forceinline__ bool is_canonical(const node::GeoJob& jb, int e, int& r) {
+  r = e < jb.n_edges ? jb.rev[e] : -1;
+  return e < jb.n_edges && e < r && r < jb.n_edges;
+}
+__global__ void __launch_bounds__(1024) pairs_count_kernel(const __grid_constant__ node::GeoJobs J, int* __restrict__ counts,
+                                                           int chunks_cap) {
+  const node::GeoJob& jb = J.j[blockIdx.y];
+  const int e0 = blockIdx.x * 1024;
+  if (e0 >= jb.n_edges) return;
   __shared__ int wsum[32];
+  int r;
+  const bool flag = is_canonical(jb, e0 + static_cast<int>(threadIdx.x), r);
+  const unsigned bal = __ballot_sync(0xffffffffu, flag);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = __popc(bal);
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    int v = wsum[threadIdx.x];
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) counts[blockIdx.y * chunks_cap + blockIdx.x] = v;
+  }
+}
+__global__ void __launch_bounds__(1024) pairs_kernel(const __grid_constant__ node::GeoJobs J, const int* __restrict__ counts,
+                                                     int chunks_cap) {
+  const node::GeoJob& jb = J.j[blockIdx.y];
+  const int e0 = blockIdx.x * 1024;
+  if (e0 >= jb.n_edges) return;
+  __shared__ int wsum[32];
+  __shared__ int base_s;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int base = 0;
-  for (int e0 = 0; e0 < jb.n_edges; e0 += 1024) {
-    const int e = e0 + static_cast<int>(threadIdx.x);
-    const int r = e < jb.n_edges ? jb.rev[e] : -1;
-    const bool flag = e < jb.n_edges && e < r && r < jb.n_edges;
-    const unsigned bal = __ballot_sync(0xffffffffu, flag);
-    if (lane == 0) wsum[warp] = __popc(bal);
-    __syncthreads();
-    int excl = 0, total = 0;
+  if (threadIdx.x < 32) {  // this chunk's offset: the counts of the chunks before it
+    int v = 0;
+    for (int c = lane; c < static_cast<int>(blockIdx.x); c += 32) v += counts[blockIdx.y * chunks_cap + c];
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) base_s = v;
+  }
+  const int e = e0 + static_cast<int>(threadIdx.x);
+  int r;
+  const bool flag = is_canonical(jb, e, r);
+  const unsigned bal = __ballot_sync(0xffffffffu, flag);
+  if (lane == 0) wsum[warp] = __popc(bal);
+  __syncthreads();
+  int excl = base_s;
 #pragma unroll 8
-    for (int w = 0; w < 32; ++w) {
-      const int s = wsum[w];
-      excl += w < warp ? s : 0;
-      total += s;
-    }
-    const int pos = base + excl + __popc(bal & ((1u << lane) - 1u));
-    if (flag && pos < (jb.n_edges >> 1)) {  // (a rev that is not an involution — host-checked at load — never writes past the tables)
-      jb.pcanon[pos] = e;
-      jb.pidx[e] = pos;
-      jb.pidx[r] = pos;
-      jb.pgeo[2 * pos] = make_float4(jb.d[e], jb.c[e], jb.dc[e], __int_as_float(jb.src[e]));
-      jb.pgeo[2 * pos + 1] = make_float4(jb.u[3 * e], jb.u[3 * e + 1], jb.u[3 * e + 2], __int_as_float(jb.col[e]));
-    }
-    base += total;
-    __syncthreads();
+  for (int w = 0; w < 32; ++w) excl += w < warp ? wsum[w] : 0;
+  const int pos = excl + __popc(bal & ((1u << lane) - 1u));
+  if (flag && pos < (jb.n_edges >> 1)) {  // (a rev that is not an involution — host-checked at load — never writes past the tables)
+    jb.pcanon[pos] = e;
+    jb.pidx[e] = pos;
+    jb.pidx[r] = pos;
+    jb.pgeo[2 * pos] = make_float4(jb.d[e], jb.c[e], jb.dc[e], __int_as_float(jb.src[e]));
+    jb.pgeo[2 * pos + 1] = make_float4(jb.u[3 * e], jb.u[3 * e + 1], jb.u[3 * e + 2], __int_as_float(jb.col[e]));
   }
 }
 

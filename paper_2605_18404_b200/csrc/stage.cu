@@ -427,6 +427,8 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
       sl.loss = nullptr;  // points into st->losses below
     }
     st->losses = dalloc<float>(st, 2 * static_cast<size_t>(d.n_slots), false);
+    st->pair_chunks_cap = static_cast<int>((NE + 1023) / 1024) + 1;
+    st->pair_counts = dalloc<int>(st, static_cast<size_t>(node::kMaxGeoJobs) * st->pair_chunks_cap, false);
     for (size_t x = 0; x < st->slots.size(); ++x) st->slots[x].loss = st->losses + 2 * x;
     st->lanes.resize(static_cast<size_t>(std::max(1, d.n_lanes)));
     // measured on the C2 bench (16 lanes): 128-edge tiles 1/1 -> 4735, 4/8 -> 5765;
@@ -504,6 +506,16 @@ size_t port_elems(const janus_stage* st, int port, int n) {
 }
 
 // ================================================================== LM
+// Edge-pair tables of the jobs' micro-batches (pair_tc.cuh): chunk counts, then ranks
+void launch_pairs(janus_stage* st, const node::GeoJobs& J, int max_edges_job, cudaStream_t s) {
+  const int chunks = (max_edges_job + 1023) / 1024;
+  if (chunks <= 0) return;
+  const dim3 grid(static_cast<unsigned>(chunks), static_cast<unsigned>(J.n));
+  edge_tc::pairs_count_kernel<<<grid, 1024, 0, s>>>(J, st->pair_counts, st->pair_chunks_cap);
+  edge_tc::pairs_kernel<<<grid, 1024, 0, s>>>(J, st->pair_counts, st->pair_chunks_cap);
+  JANUS_LAUNCH_CHECK("pairs");
+}
+
 void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_t s, bool sync,
                 const DevCsrSlice* dcsr, std::vector<node::GeoJob>* defer, int par) {
   if (mb < 0 || mb >= st->desc.n_micro_batches) throw domain_error("micro-batch index out of range");
@@ -687,7 +699,7 @@ void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_
     J.j[0].c = g.c;
     J.j[0].dc = g.dc;
     J.j[0].pidx = g.pidx;
-    edge_tc::pairs_kernel<<<1, 1024, 0, s>>>(J);
+    launch_pairs(st, J, E, s);
   }
   JANUS_LAUNCH_CHECK("geometry");
   // host arrays of the caller must stay valid until the stream reaches the
@@ -714,7 +726,11 @@ void stage_geometry_flush(janus_stage* st, std::vector<node::GeoJob>& jobs, cuda
     }
     J.total_edges = base;
     if (base > 0) node::geometry_batched_kernel<<<blocks(base, 256), 256, 0, s>>>(J);
-    if (base > 0 && use_tc(st)) edge_tc::pairs_kernel<<<J.n, 1024, 0, s>>>(J);
+    if (base > 0 && use_tc(st)) {
+      int emax = 0;
+      for (int k = 0; k < J.n; ++k) emax = std::max(emax, J.j[k].n_edges);
+      launch_pairs(st, J, emax, s);
+    }
     JANUS_LAUNCH_CHECK("geometry_batched");
   }
   jobs.clear();

@@ -131,6 +131,8 @@ struct janus_stage {
   bool pair_feff = true;             // TC FE / FF: filters once per edge pair (pair_tc.cuh); JANUS_FEFF_PAIR=0 -> directed-edge kernels
   int rows_kf = 8;                   // row kernels: edges' gathers in flight per warp (JANUS_ROWS_KF=4 for A/B)
   bool pair_bfbe = true;             // TC BF / BE: weight gradients once per edge pair (needs pair_feff); JANUS_BFBE_PAIR=0 -> directed
+  int* pair_counts = nullptr;      // pair tables: canonical edges per (job, 1024-edge chunk)
+  int pair_chunks_cap = 0;
   janus::LmBuilder* lm = nullptr;  // device neighbour-list builder (lazy, janus_stage_load without a CSR)
 
   float* P(int u) const { return params + uoff[static_cast<size_t>(u - u0)]; }
