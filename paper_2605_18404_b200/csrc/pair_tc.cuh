@@ -1,22 +1,30 @@
-// pair_tc.cuh — FE and FF of the msg unit split at the edge filter (JANUS_PREC_TF32).
+// pair_tc.cuh — the msg unit's four phases per undirected edge pair
+// (JANUS_PREC_TF32, the bench path).
 //
 // The filter w_e = c_e (SiLU(phi(d_e) A + alpha) B + beta) and its radial
 // derivative w'_e = dw/dd depend only on the edge length and the unit's
 // parameters, and d_e = d_rev(e): they are the same for an edge and its
 // reverse.  So the per-edge MMAs run once per undirected PAIR, for every msg
-// unit of the stage in ONE launch at the start of FE (msg_filter_tc), and the
-// two phases reduce over directed edges with no MMA at all:
+// unit of the stage in ONE launch at the start of FE (msg_filter_tc, tf32),
+// and FE / FF reduce over directed edges with no MMA at all:
 //
 //   FE  m_i = sum_{e in row i} w_p(e) * v_j                       (msg_fe_rows)
 //   FF  Y_i = sum_e w_p(e) * am_j ;  F_i += sum_e q_p(e) u_e ;  a_h += Y W^T
 //       q_e + q_rev(e) = < am_i v_j + am_j v_i , w'_e >          (msg_ff_rows)
 //
+// BF / BE: the weight gradients are linear in the per-edge adjoints with
+// pair-symmetric left factors, so msg_bf_pair_tc / msg_be_pair_tc (bf16
+// operands) sum both directions' adjoints and run the dB / sbar / dA MMAs once
+// per pair; the per-row sums read the stored filters (msg_bf_rows /
+// msg_be_rows, which also host the per-CTA partials' reduction).
+//
 // (reference: the four-phase math of SURVEY.md App. A / PAPER.md:171-178;
-// the directed-edge kernels in edge_tc.cuh compute the same sums).  Pair
+// the directed-edge kernels in edge_tc.cuh compute the same sums.)  Pair
 // tables: pcanon[p] = the canonical edge (e < rev e) of pair p, pidx[e] = p
-// for both directions (pairs_kernel, built at LM with the geometry).
-// Filters are stored fp32 [pair][64] per (slot, msg unit): the FE -> FF
-// activation the SPEC's fe_bytes accounts for.
+// for both directions, pgeo = the pair records (d, c, c', i | u, j)
+// (pairs_count_kernel + pairs_kernel, built at LM with the geometry).
+// Filters are stored fp32 [pair][64] per (slot, msg unit): the FE -> FF / BF
+// / BE activation the SPEC's fe_bytes accounts for.
 //
 // Row kernels: one warp per atom row, lane = 2 features; edges are summed in
 // CSR order (deterministic, independent of tiling and lanes).
