@@ -437,6 +437,10 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
     // its own lane (32 lanes: 1 -> 7760 vs 2 -> 7648; 16 lanes: 2 -> 7089 vs 1 -> 7066)
     st->tpc_fe = d.n_lanes >= 32 ? 1 : std::max(1, std::min(2, d.n_lanes / 8));
     st->tpc_wg = std::max(1, std::min(3, d.n_lanes / 5));
+    // pair mode at 32 lanes (one hardware queue per lane): 3 filter chunks and
+    // 5 BF / BE pair chunks per CTA (C2: 15182 -> 15527-15548 structures/s)
+    st->tpc_filter = d.n_lanes >= 32 ? 3 : st->tpc_fe;
+    if (d.n_lanes >= 32) st->tpc_wg = 5;
     // tensor-core tiles: runs of <= 8 rows with <= tc_tile_edges edges, cut into
     // 128-edge chunks (rows may straddle chunk boundaries: the segmented sums
     // and force sums carry across the chunks of a tile)
@@ -444,7 +448,7 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
     if (const char* e = std::getenv("JANUS_TC_TILE_EDGES")) st->tc_tile_edges = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("JANUS_TC_TILE_MAXCH")) st->tc_tile_max_chunks = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("JANUS_TC_TILE_OVH")) st->tc_tile_ovh = std::atof(e);
-    if (const char* e = std::getenv("JANUS_TPC_FE")) st->tpc_fe = std::max(1, std::atoi(e));  // tuning runs only
+    if (const char* e = std::getenv("JANUS_TPC_FE")) st->tpc_fe = st->tpc_filter = std::max(1, std::atoi(e));  // tuning runs only
     if (const char* e = std::getenv("JANUS_TPC_WG")) st->tpc_wg = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("JANUS_FEFF_PAIR")) st->pair_feff = std::atoi(e) != 0;  // A/B runs only
     st->pair_bfbe = st->pair_feff;
@@ -751,7 +755,7 @@ void launch_filter(janus_stage* st, const DevGeo& g, Slot& sl, int u_only, cudaS
   }
   if (J.n == 0 || g.n_pairs == 0) return;
   const int chunks = (g.n_pairs + edge_tc::TE - 1) / edge_tc::TE;
-  const int gx = grid_x > 0 ? std::min(grid_x, chunks) : std::max(1, std::min(chunks, (chunks + st->tpc_fe - 1) / st->tpc_fe));
+  const int gx = grid_x > 0 ? std::min(grid_x, chunks) : std::max(1, std::min(chunks, (chunks + st->tpc_filter - 1) / st->tpc_filter));
   edge_tc::msg_filter_tc<<<dim3(gx, J.n), edge_tc::NT, edge_tc::filter_smem(), s>>>(edge_geom(g), g.pgeo, g.n_pairs, J,
                                                                                      st->m.r_c);
   JANUS_LAUNCH_CHECK("msg_filter_tc");

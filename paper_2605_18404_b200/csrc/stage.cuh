@@ -125,6 +125,7 @@ struct janus_stage {
   janus::LoadLayout lay;           // upload block layout (capacity offsets)
   int64_t static_bytes = 0, arena_bytes = 0;
   int tpc_fe = 1, tpc_wg = 1;        // TC edge tiles per CTA: FE/FF, BF/BE (stage_create)
+  int tpc_filter = 1;                // pair mode: 128-pair chunks per filter CTA
   int tc_tile_edges = 0;             // TC tiles: 0 cost-chosen runs, > 0 greedy edge budget (tuning)
   int tc_tile_max_chunks = 0;        // cost-chosen tiles: max 128-edge chunks (0: by mean degree)
   double tc_tile_ovh = 0.3;          // per-tile epilogue cost in chunk units
