@@ -445,7 +445,8 @@ namespace node {
 // Row-local programs for the upd unit (p = mU + ups, y = SiLU(p) V): one CTA =
 // 16 atoms x 64 features, thread (row t/16, 4 columns); row vectors staged in
 // smem, weights read through L1.  Each replaces 3-5 separate launches.
-constexpr int kRB = 16;
+constexpr int kRB = 32;  // rows per CTA (kUT = 16 * kRB threads: 1 row x 4 columns each)
+constexpr int kUT = 16 * kRB;
 
 __device__ __forceinline__ void rowmm(const float (*X)[68], const float* Ms, int r, int c0, float (&o)[4]) {
   o[0] = o[1] = o[2] = o[3] = 0.f;
@@ -489,10 +490,9 @@ __device__ __forceinline__ void stage_mats(float* dst, const float* const* src, 
   for (int m = 0; m < n; ++m) {
     const float4* s4 = reinterpret_cast<const float4*>(src[m]);
     float4* d4 = reinterpret_cast<float4*>(dst + m * 4096);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint32_t da = static_cast<uint32_t>(__cvta_generic_to_shared(d4 + threadIdx.x + 256 * q));
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(da), "l"(s4 + threadIdx.x + 256 * q) : "memory");
+    for (int q = static_cast<int>(threadIdx.x); q < 1024; q += static_cast<int>(blockDim.x)) {
+      const uint32_t da = static_cast<uint32_t>(__cvta_generic_to_shared(d4 + q));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(da), "l"(s4 + q) : "memory");
     }
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
@@ -502,7 +502,7 @@ __device__ __forceinline__ void stage_mats_wait() { asm volatile("cp.async.wait_
 constexpr size_t upd_smem(int nmats) { return sizeof(float) * 4096 * nmats; }
 
 __device__ __forceinline__ void row_load(float (*X)[68], const float* __restrict__ src, int i0, int rows) {
-  for (int x = threadIdx.x; x < kRB * 16; x += 256) {
+  for (int x = threadIdx.x; x < kRB * 16; x += blockDim.x) {
     const int r = x / 16, q = x % 16;
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
     if (i0 + r < rows) v = __ldg(reinterpret_cast<const float4*>(src + (size_t)(i0 + r) * 64) + q);
@@ -518,7 +518,7 @@ __device__ __forceinline__ float4 row_get(const float* src, int i, int c0) {
 
 // FE: p = m U + ups ; h_out = h + SiLU(p) V ; and, when the next unit is a
 // msg unit on the stage, its v = h_out Wn (saves that unit's row-GEMM launch)
-__global__ void __launch_bounds__(256) upd_fe_fused(int rows, const float* __restrict__ m, const float* __restrict__ h,
+__global__ void __launch_bounds__(kUT) upd_fe_fused(int rows, const float* __restrict__ m, const float* __restrict__ h,
                                                     const float* __restrict__ U, const float* __restrict__ ups,
                                                     const float* __restrict__ V, float* __restrict__ p_out,
                                                     float* __restrict__ h_out, const float* __restrict__ Wn,
@@ -560,7 +560,7 @@ __global__ void __launch_bounds__(256) upd_fe_fused(int rows, const float* __res
 }
 
 // FF: ff_a = a' ; am = ((a' V^T) SiLU'(p)) U^T
-__global__ void __launch_bounds__(256) upd_ff_fused(int rows, const float* __restrict__ a, const float* __restrict__ p,
+__global__ void __launch_bounds__(kUT) upd_ff_fused(int rows, const float* __restrict__ a, const float* __restrict__ p,
                                                     const float* __restrict__ Vt, const float* __restrict__ Ut,
                                                     float* __restrict__ ff_a, float* __restrict__ am) {
   __shared__ __align__(16) float X[kRB][68];
@@ -593,7 +593,7 @@ __global__ void __launch_bounds__(256) upd_ff_fused(int rows, const float* __res
 
 // BF: pdot = abar_m U ; r = a' V^T ; pbar = r pdot SiLU''(p) ; pdbar = r SiLU'(p) ;
 //     u = SiLU'(p) pdot ; inj = pbar U^T ; abar_h += u V
-__global__ void __launch_bounds__(256) upd_bf_fused(int rows, const float* __restrict__ am, const float* __restrict__ ffa,
+__global__ void __launch_bounds__(kUT) upd_bf_fused(int rows, const float* __restrict__ am, const float* __restrict__ ffa,
                                                     const float* __restrict__ p, const float* __restrict__ U,
                                                     const float* __restrict__ Vt, const float* __restrict__ Ut,
                                                     const float* __restrict__ V, float* __restrict__ pbar,
@@ -654,7 +654,7 @@ __global__ void __launch_bounds__(256) upd_bf_fused(int rows, const float* __res
 }
 
 // BE: r = b' V^T ; pbar = r SiLU'(p) ; b_m = pbar U^T + inj
-__global__ void __launch_bounds__(256) upd_be_fused(int rows, const float* __restrict__ bh, const float* __restrict__ p,
+__global__ void __launch_bounds__(kUT) upd_be_fused(int rows, const float* __restrict__ bh, const float* __restrict__ p,
                                                     const float* __restrict__ Vt, const float* __restrict__ Ut,
                                                     const float* __restrict__ inj, float* __restrict__ pbar,
                                                     float* __restrict__ bm) {
