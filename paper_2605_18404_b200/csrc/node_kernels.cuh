@@ -445,8 +445,12 @@ namespace node {
 // Row-local programs for the upd unit (p = mU + ups, y = SiLU(p) V): one CTA =
 // 16 atoms x 64 features, thread (row t/16, 4 columns); row vectors staged in
 // smem, weights read through L1.  Each replaces 3-5 separate launches.
-constexpr int kRB = 32;  // rows per CTA (kUT = 16 * kRB threads: 1 row x 4 columns each)
-constexpr int kUT = 16 * kRB;
+// upd kernels: RB rows per CTA, 16 * RB threads (1 row x 4 columns each);
+// 32 rows for large micro-batches (half the CTAs and weight staging of 16:
+// C2 15515 -> 15765), 16 for small ones (more CTAs on a latency-bound chain)
+constexpr int kRB = 32;
+constexpr int kRBSmall = 16;
+inline int upd_rows_per_cta(int n_atoms) { return n_atoms >= 256 ? kRB : kRBSmall; }
 
 __device__ __forceinline__ void rowmm(const float (*X)[68], const float* Ms, int r, int c0, float (&o)[4]) {
   o[0] = o[1] = o[2] = o[3] = 0.f;
@@ -501,8 +505,9 @@ __device__ __forceinline__ void stage_mats(float* dst, const float* const* src, 
 __device__ __forceinline__ void stage_mats_wait() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 constexpr size_t upd_smem(int nmats) { return sizeof(float) * 4096 * nmats; }
 
+template <int RB>
 __device__ __forceinline__ void row_load(float (*X)[68], const float* __restrict__ src, int i0, int rows) {
-  for (int x = threadIdx.x; x < kRB * 16; x += blockDim.x) {
+  for (int x = threadIdx.x; x < RB * 16; x += blockDim.x) {
     const int r = x / 16, q = x % 16;
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
     if (i0 + r < rows) v = __ldg(reinterpret_cast<const float4*>(src + (size_t)(i0 + r) * 64) + q);
@@ -518,19 +523,20 @@ __device__ __forceinline__ float4 row_get(const float* src, int i, int c0) {
 
 // FE: p = m U + ups ; h_out = h + SiLU(p) V ; and, when the next unit is a
 // msg unit on the stage, its v = h_out Wn (saves that unit's row-GEMM launch)
-__global__ void __launch_bounds__(kUT) upd_fe_fused(int rows, const float* __restrict__ m, const float* __restrict__ h,
+template <int RB>
+__global__ void __launch_bounds__(16 * RB) upd_fe_fused(int rows, const float* __restrict__ m, const float* __restrict__ h,
                                                     const float* __restrict__ U, const float* __restrict__ ups,
                                                     const float* __restrict__ V, float* __restrict__ p_out,
                                                     float* __restrict__ h_out, const float* __restrict__ Wn,
                                                     float* __restrict__ v_out) {
-  __shared__ __align__(16) float X[kRB][68];
+  __shared__ __align__(16) float X[RB][68];
   extern __shared__ __align__(16) float Ws[];
-  const int i0 = blockIdx.x * kRB, r = threadIdx.x / 16, c0 = (threadIdx.x % 16) * 4, i = i0 + r;
+  const int i0 = blockIdx.x * RB, r = threadIdx.x / 16, c0 = (threadIdx.x % 16) * 4, i = i0 + r;
   {
     const float* mats[3] = {U, V, Wn};
     stage_mats(Ws, mats, Wn ? 3 : 2);
   }
-  row_load(X, m, i0, rows);
+  row_load<RB>(X, m, i0, rows);
   stage_mats_wait();
   __syncthreads();
   float o[4];
@@ -560,17 +566,18 @@ __global__ void __launch_bounds__(kUT) upd_fe_fused(int rows, const float* __res
 }
 
 // FF: ff_a = a' ; am = ((a' V^T) SiLU'(p)) U^T
-__global__ void __launch_bounds__(kUT) upd_ff_fused(int rows, const float* __restrict__ a, const float* __restrict__ p,
+template <int RB>
+__global__ void __launch_bounds__(16 * RB) upd_ff_fused(int rows, const float* __restrict__ a, const float* __restrict__ p,
                                                     const float* __restrict__ Vt, const float* __restrict__ Ut,
                                                     float* __restrict__ ff_a, float* __restrict__ am) {
-  __shared__ __align__(16) float X[kRB][68];
+  __shared__ __align__(16) float X[RB][68];
   extern __shared__ __align__(16) float Ws[];
-  const int i0 = blockIdx.x * kRB, r = threadIdx.x / 16, c0 = (threadIdx.x % 16) * 4, i = i0 + r;
+  const int i0 = blockIdx.x * RB, r = threadIdx.x / 16, c0 = (threadIdx.x % 16) * 4, i = i0 + r;
   {
     const float* mats[2] = {Vt, Ut};
     stage_mats(Ws, mats, 2);
   }
-  row_load(X, a, i0, rows);
+  row_load<RB>(X, a, i0, rows);
   stage_mats_wait();
   __syncthreads();
   if (i < rows) {
@@ -593,24 +600,25 @@ __global__ void __launch_bounds__(kUT) upd_ff_fused(int rows, const float* __res
 
 // BF: pdot = abar_m U ; r = a' V^T ; pbar = r pdot SiLU''(p) ; pdbar = r SiLU'(p) ;
 //     u = SiLU'(p) pdot ; inj = pbar U^T ; abar_h += u V
-__global__ void __launch_bounds__(kUT) upd_bf_fused(int rows, const float* __restrict__ am, const float* __restrict__ ffa,
+template <int RB>
+__global__ void __launch_bounds__(16 * RB) upd_bf_fused(int rows, const float* __restrict__ am, const float* __restrict__ ffa,
                                                     const float* __restrict__ p, const float* __restrict__ U,
                                                     const float* __restrict__ Vt, const float* __restrict__ Ut,
                                                     const float* __restrict__ V, float* __restrict__ pbar,
                                                     float* __restrict__ pdbar, float* __restrict__ u,
                                                     float* __restrict__ inj, const float* ah, float* ah_out,
                                                     const float* __restrict__ Wn, float* __restrict__ vdot_out) {
-  __shared__ __align__(16) float X[kRB][68];
-  __shared__ __align__(16) float Y[kRB][68];
+  __shared__ __align__(16) float X[RB][68];
+  __shared__ __align__(16) float Y[RB][68];
   extern __shared__ __align__(16) float Ws[];
-  const int i0 = blockIdx.x * kRB, r = threadIdx.x / 16, c0 = (threadIdx.x % 16) * 4, i = i0 + r;
+  const int i0 = blockIdx.x * RB, r = threadIdx.x / 16, c0 = (threadIdx.x % 16) * 4, i = i0 + r;
   {
     const float* mats[5] = {U, Vt, Ut, V, Wn};
     stage_mats(Ws, mats, Wn ? 5 : 4);
   }
-  row_load(X, am, i0, rows);
+  row_load<RB>(X, am, i0, rows);
   stage_mats_wait();
-  row_load(Y, ffa, i0, rows);
+  row_load<RB>(Y, ffa, i0, rows);
   __syncthreads();
   float pd[4], rr[4];
   rowmm(X, Ws, r, c0, pd);
@@ -654,18 +662,19 @@ __global__ void __launch_bounds__(kUT) upd_bf_fused(int rows, const float* __res
 }
 
 // BE: r = b' V^T ; pbar = r SiLU'(p) ; b_m = pbar U^T + inj
-__global__ void __launch_bounds__(kUT) upd_be_fused(int rows, const float* __restrict__ bh, const float* __restrict__ p,
+template <int RB>
+__global__ void __launch_bounds__(16 * RB) upd_be_fused(int rows, const float* __restrict__ bh, const float* __restrict__ p,
                                                     const float* __restrict__ Vt, const float* __restrict__ Ut,
                                                     const float* __restrict__ inj, float* __restrict__ pbar,
                                                     float* __restrict__ bm) {
-  __shared__ __align__(16) float X[kRB][68];
+  __shared__ __align__(16) float X[RB][68];
   extern __shared__ __align__(16) float Ws[];
-  const int i0 = blockIdx.x * kRB, r = threadIdx.x / 16, c0 = (threadIdx.x % 16) * 4, i = i0 + r;
+  const int i0 = blockIdx.x * RB, r = threadIdx.x / 16, c0 = (threadIdx.x % 16) * 4, i = i0 + r;
   {
     const float* mats[2] = {Vt, Ut};
     stage_mats(Ws, mats, 2);
   }
-  row_load(X, bh, i0, rows);
+  row_load<RB>(X, bh, i0, rows);
   stage_mats_wait();
   __syncthreads();
   float o[4];

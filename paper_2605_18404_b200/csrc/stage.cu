@@ -24,6 +24,15 @@
 #include "edge_tc.cuh"
 #include "pair_tc.cuh"
 
+// fused upd kernels by micro-batch size (node_kernels.cuh upd_rows_per_cta)
+#define JANUS_UPD(KERN, SMEM, S, ...)                                                                 \
+  do {                                                                                               \
+    if (node::upd_rows_per_cta(N) == node::kRB)                                                      \
+      node::KERN<node::kRB><<<blocks(N, node::kRB), 16 * node::kRB, (SMEM), (S)>>>(__VA_ARGS__);     \
+    else                                                                                             \
+      node::KERN<node::kRBSmall><<<blocks(N, node::kRBSmall), 16 * node::kRBSmall, (SMEM), (S)>>>(__VA_ARGS__); \
+  } while (0)
+
 // row kernels (pair_tc.cuh) by the stage's gathers-in-flight setting
 #define JANUS_ROWS(KERN, GRID, S, ...)                                          \
   do {                                                                          \
@@ -473,8 +482,10 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
     JANUS_CUDA(cudaFuncSetAttribute(edge::msg_ff_kernel<kH, kR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge::ff_smem<kH, kR>()));
     JANUS_CUDA(cudaFuncSetAttribute(edge::msg_bf_kernel<kH, kR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge::bf_smem<kH, kR>()));
     JANUS_CUDA(cudaFuncSetAttribute(edge::msg_be_kernel<kH, kR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge::be_smem<kH, kR>()));
-    JANUS_CUDA(cudaFuncSetAttribute(node::upd_bf_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)node::upd_smem(5)));
-    JANUS_CUDA(cudaFuncSetAttribute(node::upd_fe_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)node::upd_smem(3)));
+    JANUS_CUDA(cudaFuncSetAttribute(node::upd_bf_fused<node::kRB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)node::upd_smem(5)));
+    JANUS_CUDA(cudaFuncSetAttribute(node::upd_fe_fused<node::kRB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)node::upd_smem(3)));
+    JANUS_CUDA(cudaFuncSetAttribute(node::upd_bf_fused<node::kRBSmall>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)node::upd_smem(5)));
+    JANUS_CUDA(cudaFuncSetAttribute(node::upd_fe_fused<node::kRBSmall>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)node::upd_smem(3)));
     JANUS_CUDA(cudaFuncSetAttribute(edge_tc::msg_fe_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge_tc::fe_smem()));
     JANUS_CUDA(cudaFuncSetAttribute(edge_tc::msg_ff_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge_tc::ff_smem()));
     JANUS_CUDA(cudaFuncSetAttribute(edge_tc::msg_filter_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge_tc::filter_smem()));
@@ -805,7 +816,7 @@ void stage_fe(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
         const float* Wn = fuse ? st->P(u + 1) + R * H + H + H * H + H : nullptr;
         float* vn = fuse ? sl.units[static_cast<size_t>(u + 1 - st->u0)].v : nullptr;
         if (!(prof_skip() & 32))
-          node::upd_fe_fused<<<blocks(N, node::kRB), node::kUT, node::upd_smem(fuse ? 3 : 2), s>>>(N, cur_m, cur_h, Um, ups, V, b.p,
+          JANUS_UPD(upd_fe_fused, node::upd_smem(fuse ? 3 : 2), s, N, cur_m, cur_h, Um, ups, V, b.p,
                                                                                               b.out_h, Wn, vn);
         v_ready = fuse;
         cur_h = b.out_h;
@@ -862,7 +873,7 @@ void stage_ff(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
       case kUpd: {  // ff_a = a'; a_m = ((a' V^T) SiLU'(p)) U^T, written straight into the
                     // preceding msg unit's saved FF input when it is on this stage
         float* am_dst = (u - 1 >= st->u0) ? sl.units[static_cast<size_t>(u - 1 - st->u0)].ff_a : wm;
-        if (!(prof_skip() & 32)) node::upd_ff_fused<<<blocks(N, node::kRB), node::kUT, node::upd_smem(2), s>>>(N, wh, b.p, T + H * H, T, b.ff_a, am_dst);
+        if (!(prof_skip() & 32)) JANUS_UPD(upd_ff_fused, node::upd_smem(2), s, N, wh, b.p, T + H * H, T, b.ff_a, am_dst);
         break;
       }
       case kMsg: {
@@ -992,7 +1003,7 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
         const bool fuse = u + 1 < st->u1 && unit_kind(u + 1, L) == kMsg;
         const float* Wn = fuse ? st->P(u + 1) + R * H + H + H * H + H : nullptr;
         if (!(prof_skip() & 32))
-          node::upd_bf_fused<<<blocks(N, node::kRB), node::kUT, node::upd_smem(fuse ? 5 : 4), s>>>(N, am, b.ff_a, b.p, Um, T + H * H, T, V,
+          JANUS_UPD(upd_bf_fused, node::upd_smem(fuse ? 5 : 4), s, N, am, b.ff_a, b.p, Um, T + H * H, T, V,
                                                                                               sc.s3, sc.s4, sc.s5, b.inj, ah, ah_alt, Wn,
                                                                                               fuse ? sc.s1 : nullptr);
         vdot_ready = fuse;
@@ -1082,7 +1093,7 @@ void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only, 
       case kUpd: {
         float *dU = G1, *dups = G1 + H * H, *dV = G1 + H * H + H;
         // pbar (s2) = (b' V^T) SiLU'(p); b_m = pbar U^T + mbar^F
-        if (!(prof_skip() & 32)) node::upd_be_fused<<<blocks(N, node::kRB), node::kUT, node::upd_smem(2), s>>>(N, bh, b.p, T + H * H, T, b.inj, sc.s2, bm);
+        if (!(prof_skip() & 32)) JANUS_UPD(upd_be_fused, node::upd_smem(2), s, N, bh, b.p, T + H * H, T, b.inj, sc.s2, bm);
         const node::WJob jv = wjob(b.p, bh, dV, nullptr, nullptr, true);                           // dV1 = SiLU(p)^T b'
         const node::WJob ju = wjob(in_m(st, sl, u, N), sc.s2, dU, nullptr, nullptr, false, sc.s2, dups);  // dU1, dups1
         if (has_pend)
