@@ -521,6 +521,41 @@ __device__ __forceinline__ float4 row_get(const float* src, int i, int c0) {
   return __ldg(reinterpret_cast<const float4*>(src + (size_t)i * 64 + c0));
 }
 
+// out[i] = op(X[i]) M (+ bias) (+ add1[i]) (+ add2[i]) with RB rows per CTA
+// and M staged once per CTA by cp.async (gemm_rows_kernel: 4 rows per CTA,
+// each re-reading M through L1).  Same per-output arithmetic as
+// gemm_rows_kernel (even / odd k chains, then bias, add1, add2): bit-identical.
+template <int RB, typename InOp>
+__global__ void __launch_bounds__(16 * RB) gemm_rb_kernel(int rows, const float* __restrict__ X, const float* __restrict__ M,
+                                                          const float* __restrict__ bias, const float* add1, const float* add2,
+                                                          float* out, InOp op) {
+  __shared__ __align__(16) float Xs[RB][68];
+  extern __shared__ __align__(16) float Ws[];
+  const int i0 = blockIdx.x * RB, r = threadIdx.x / 16, c0 = (threadIdx.x % 16) * 4, i = i0 + r;
+  {
+    const float* mats[1] = {M};
+    stage_mats(Ws, mats, 1);
+  }
+  for (int x = threadIdx.x; x < RB * 64; x += blockDim.x) {
+    const int rr = x / 64, c = x % 64;
+    Xs[rr][c] = i0 + rr < rows ? op(i0 + rr, c, X[(size_t)(i0 + rr) * 64 + c]) : 0.f;
+  }
+  stage_mats_wait();
+  __syncthreads();
+  float o[4];
+  rowmm_eo(Xs, Ws, r, c0, o);
+  if (i >= rows) return;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const size_t idx = (size_t)i * 64 + c0 + q;
+    float y = o[q];
+    if (bias) y += bias[c0 + q];
+    if (add1) y += add1[idx];
+    if (add2) y += add2[idx];
+    out[idx] = y;
+  }
+}
+
 // FE: p = m U + ups ; h_out = h + SiLU(p) V ; and, when the next unit is a
 // msg unit on the stage, its v = h_out Wn (saves that unit's row-GEMM launch)
 template <int RB>

@@ -107,7 +107,14 @@ template <typename Op = node::InId>
 void gemm(cudaStream_t s, int rows, const float* X, const float* M, const float* bias, const float* add1,
           const float* add2, float* out, Op op = Op{}) {
   if (rows <= 0 || (prof_skip() & 64)) return;
-  node::gemm_rows_kernel<kH, Op><<<blocks(rows, 256 / kH), 256, 0, s>>>(rows, X, M, bias, add1, add2, out, op);
+  static const bool rows4 = std::getenv("JANUS_GEMM_ROWS4") != nullptr;  // A/B: the 4-rows-per-CTA kernel
+  if (rows4)
+    node::gemm_rows_kernel<kH, Op><<<blocks(rows, 256 / kH), 256, 0, s>>>(rows, X, M, bias, add1, add2, out, op);
+  else if (rows >= 256)
+    node::gemm_rb_kernel<node::kRB, Op><<<blocks(rows, node::kRB), 16 * node::kRB, node::upd_smem(1), s>>>(rows, X, M, bias, add1, add2, out, op);
+  else
+    node::gemm_rb_kernel<node::kRBSmall, Op><<<blocks(rows, node::kRBSmall), 16 * node::kRBSmall, node::upd_smem(1), s>>>(rows, X, M, bias, add1,
+                                                                                                                 add2, out, op);
   JANUS_LAUNCH_CHECK("gemm_rows");
 }
 
