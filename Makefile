@@ -30,6 +30,11 @@ OBJ := build/feff$(FEFF_CTAS)_obj
 LIB := build/feff$(FEFF_CTAS)/libjanus_b200.so
 NVFLAGS += -DJANUS_FEFF_CTAS=$(FEFF_CTAS)
 endif
+ifeq ($(PROFILE),1)  # attribution build (JANUS_PROF_SKIP), loaded via JANUS_LIB; never the product library
+OBJ := build/prof_obj
+LIB := build/prof/libjanus_b200.so
+NVFLAGS += -DJANUS_PROFILING
+endif
 ifeq ($(TRACE),1)  # phase-traced profiling build (edge_tc.cuh TC_MARK), loaded via JANUS_LIB
 OBJ := build/trace_obj
 LIB := build/trace/libjanus_b200.so

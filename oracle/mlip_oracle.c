@@ -699,3 +699,103 @@ void mo_adam(int64_t n, double* p, double* m1, double* m2, const double* g, doub
     p[i] -= lr * (m1[i] / c1) / (sqrt(m2[i] / c2) + eps);
   }
 }
+
+/* ------------------------------------------------------- synthetic inputs
+ * Restatement of the seeded synthetic data: SplitMix64 as
+ * reference rng.hpp:11-38 (next(), next() % n, 53-bit doubles), Box-Muller
+ * cosine branch on (1 - u1, u2), per-tensor streams seed ^ (tag * gamma).
+ * Lets the CPU reference arm build its inputs without the product library;
+ * tests/test_oracle.py pins it bit-for-bit to janus_synth_params / _cell. */
+typedef struct { uint64_t s; } mo_rng;
+static uint64_t rng_next(mo_rng* g) {
+  g->s += 0x9e3779b97f4a7c15ULL;
+  uint64_t x = g->s;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+static double rng_double(mo_rng* g) { return (double)(rng_next(g) >> 11) * 0x1.0p-53; }
+static double rng_normal(mo_rng* g) {
+  const double u1 = 1.0 - rng_double(g);
+  const double u2 = rng_double(g);
+  return sqrt(-2.0 * log(u1)) * cos(2.0 * 3.14159265358979323846 * u2);
+}
+
+void mo_synth_params(const mo_model* m, uint64_t seed, float* out) {
+  const int H = m->H, R = m->R, S = m->n_species, U = 2 * m->L + 2;
+  int64_t off = 0;
+  const double sH = 1.0 / sqrt((double)H), sR = 1.0 / sqrt((double)R);
+#define FILL(unit, tensor, n, sd)                                                              \
+  do {                                                                                         \
+    mo_rng g = {seed ^ (((uint64_t)(unit) * 16u + (uint64_t)(tensor) + 1u) * 0x9e3779b97f4a7c15ULL)}; \
+    for (int64_t x = 0; x < (int64_t)(n); ++x) out[off + x] = (float)((sd) * rng_normal(&g));  \
+    off += (int64_t)(n);                                                                       \
+  } while (0)
+  for (int u = 0; u < U; ++u) {
+    if (u == 0) {
+      FILL(u, 0, (int64_t)S * H, 1.0);
+    } else if (u == U - 1) {
+      FILL(u, 0, (int64_t)H * H, sH);
+      FILL(u, 1, H, 0.1);
+      FILL(u, 2, H, sH);
+      FILL(u, 3, S, 1.0);
+    } else if (u % 2 == 1) {
+      FILL(u, 0, (int64_t)R * H, sR);
+      FILL(u, 1, H, 0.1);
+      FILL(u, 2, (int64_t)H * H, sH);
+      FILL(u, 3, H, 0.1);
+      FILL(u, 4, (int64_t)H * H, sH);
+    } else {
+      FILL(u, 0, (int64_t)H * H, sH);
+      FILL(u, 1, H, 0.1);
+      FILL(u, 2, (int64_t)H * H, sH);
+    }
+  }
+#undef FILL
+}
+
+double mo_synth_cell(int n, double rho, int n_species, uint64_t seed, double* pos, int* species, float* E_target,
+                     float* F_target) {
+  if (n < 1 || !(rho > 0) || n_species < 1) return -1.0;
+  const double L = cbrt((double)n / rho);
+  double* sites = ALLOC(double, 3 * (int64_t)n);
+  int ns = 0;
+  int k = (int)lround(cbrt(n / 4.0));
+  if (k >= 1 && 4 * k * k * k == n) {
+    const double a = L / k;
+    const double basis[4][3] = {{0, 0, 0}, {0.5, 0.5, 0}, {0.5, 0, 0.5}, {0, 0.5, 0.5}};
+    for (int x = 0; x < k; ++x)
+      for (int y = 0; y < k; ++y)
+        for (int z = 0; z < k; ++z)
+          for (int q = 0; q < 4; ++q, ++ns) {
+            sites[3 * ns] = (x + basis[q][0]) * a;
+            sites[3 * ns + 1] = (y + basis[q][1]) * a;
+            sites[3 * ns + 2] = (z + basis[q][2]) * a;
+          }
+  } else {
+    k = (int)ceil(cbrt((double)n) - 1e-9);
+    const double a = L / k;
+    for (int x = 0; x < k && ns < n; ++x)
+      for (int y = 0; y < k && ns < n; ++y)
+        for (int z = 0; z < k && ns < n; ++z, ++ns) {
+          sites[3 * ns] = x * a;
+          sites[3 * ns + 1] = y * a;
+          sites[3 * ns + 2] = z * a;
+        }
+  }
+  mo_rng g = {seed};
+  const double sigma = 0.1 * L / cbrt((double)n);
+  for (int i = 0; i < n; ++i)
+    for (int c = 0; c < 3; ++c) {
+      double x = sites[3 * i + c] + sigma * rng_normal(&g);
+      x = fmod(x, L);
+      if (x < 0) x += L;
+      if (x >= L) x -= L;
+      pos[3 * i + c] = x;
+    }
+  for (int i = 0; i < n; ++i) species[i] = n_species <= 1 ? 0 : (int)(rng_next(&g) % (uint64_t)n_species);
+  *E_target = (float)(sqrt((double)n) * rng_normal(&g));
+  for (int x = 0; x < 3 * n; ++x) F_target[x] = (float)(0.1 * rng_normal(&g));
+  free(sites);
+  return L;
+}

@@ -82,6 +82,13 @@ int mo_energy(const mo_model* m, const mo_batch* b, int64_t n_edges, const int* 
 void mo_adam(int64_t n, double* p, double* m1, double* m2, const double* g, double lr, double beta1,
              double beta2, double eps, int step);
 
+/* Seeded synthetic inputs, bit-identical to the product's janus_synth_params /
+ * janus_synth_cell (SplitMix64 of reference rng.hpp:11-38).  mo_synth_cell
+ * returns the box length (-1 on bad arguments). */
+void mo_synth_params(const mo_model* m, uint64_t seed, float* out);
+double mo_synth_cell(int n, double rho, int n_species, uint64_t seed, double* pos, int* species, float* E_target,
+                     float* F_target);
+
 #ifdef __cplusplus
 }
 #endif

@@ -178,3 +178,44 @@ def adam(p, m1, m2, g, lr, beta1, beta2, eps, step_no):
     g = np.ascontiguousarray(g, dtype=np.float64)
     lib().mo_adam(ctypes.c_int64(p.size), _p(p), _p(m1), _p(m2), _p(g), ctypes.c_double(lr),
                   ctypes.c_double(beta1), ctypes.c_double(beta2), ctypes.c_double(eps), ctypes.c_int(step_no))
+
+
+def synth_params(model: Model, seed: int) -> np.ndarray:
+    """Seeded parameters, bit-identical to the product's janus_synth_params."""
+    out = np.zeros(model.param_count(), np.float32)
+    m = model.c()
+    L = lib()
+    L.mo_synth_params.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_void_p]
+    L.mo_synth_params(ctypes.byref(m), ctypes.c_uint64(seed), _p(out))
+    return out
+
+
+def synth_cell(n: int, rho: float, n_species: int, seed: int):
+    """(pos [n,3] f64, species [n] i32, box length, E_target f32, F_target [n,3] f32),
+    bit-identical to the product's janus_synth_cell."""
+    pos = np.zeros((n, 3), np.float64)
+    sp = np.zeros(n, np.int32)
+    Et = np.zeros(1, np.float32)
+    Ft = np.zeros((n, 3), np.float32)
+    L = lib()
+    L.mo_synth_cell.restype = ctypes.c_double
+    L.mo_synth_cell.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_int, ctypes.c_uint64, ctypes.c_void_p,
+                                ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+    box = L.mo_synth_cell(n, rho, n_species, ctypes.c_uint64(seed), _p(pos), _p(sp), _p(Et), _p(Ft))
+    if box < 0:
+        raise ValueError("synth_cell: bad arguments")
+    return pos, sp, box, float(Et[0]), Ft
+
+
+def synth_batch(model: Model, atoms_per_cell, rho: float, seed: int) -> Batch:
+    """The product's synth_batch (paper_2605_18404_b200.synth_batch) restated:
+    cell s of the batch is seeded with seed * 1000003 + s."""
+    if isinstance(atoms_per_cell, int):
+        atoms_per_cell = [atoms_per_cell]
+    P, S, SID, C, E, F = [], [], [], [], [], []
+    for s, n in enumerate(atoms_per_cell):
+        pos, sp, box, Et, Ft = synth_cell(n, rho, model.n_species, seed * 1000003 + s)
+        P.append(pos); S.append(sp); SID.append(np.full(n, s, np.int32)); C.append(box); E.append(Et)
+        F.append(Ft)
+    return Batch(np.concatenate(P), np.concatenate(S), np.concatenate(SID), np.array(C),
+                 np.array(E, np.float32).astype(np.float64), np.concatenate(F).astype(np.float64))

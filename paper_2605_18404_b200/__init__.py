@@ -16,11 +16,10 @@ from dataclasses import dataclass
 
 import numpy as np
 
-# One hardware work queue per compute lane: with the default 8 connections the
-# 32 lanes of a step share 8 queues and serialise falsely (measured: 14.0k ->
-# 15.2k structures/s on C2).  Takes effect if no CUDA context exists yet; the
-# library's load-time constructor does the same for C/C++ hosts.
-os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+# The library does not touch the process environment.  Applications running
+# many compute lanes should set CUDA_DEVICE_MAX_CONNECTIONS (one hardware work
+# queue per lane, e.g. 32) before the first CUDA context exists; bench.py and
+# the tests do.  janus_trainer_create warns on stderr when lanes exceed it.
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("JANUS_LIB") or os.path.join(_HERE, "libjanus_b200.so")  # JANUS_LIB: profiling builds only

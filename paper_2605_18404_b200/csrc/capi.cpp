@@ -16,11 +16,6 @@
 #include "../../include/janus/tuner.hpp"
 
 #include <cstdlib>
-
-// One hardware work queue per compute lane (the default 8 make the step's 32
-// lanes serialise falsely: DESIGN.md §4).  Runs at load time, before the
-// library creates a CUDA context; an explicit setting is kept.
-__attribute__((constructor)) static void janus_default_connections() { setenv("CUDA_DEVICE_MAX_CONNECTIONS", "32", 0); }
 #include "../../include/janus_cuda.h"
 #include "cuda_check.hpp"
 #include "executor.hpp"

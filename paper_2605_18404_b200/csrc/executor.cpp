@@ -124,6 +124,7 @@ struct janus_trainer {
   int inflight = 0;
   cudaEvent_t anchor_q[2] = {nullptr, nullptr}, finish_q[2] = {nullptr, nullptr}, done_q[2] = {nullptr, nullptr};
   float* loss_snap[2] = {nullptr, nullptr};
+  float* dopt = nullptr;                         // device {lr, beta1, beta2, eps}: written on root before every step
   int64_t p2p_bytes = 0;
   int64_t kernel_count = -1;
   cudaGraphExec_t gexec = nullptr;               // instantiated step graph for key gkey (geometry parities)
@@ -441,7 +442,7 @@ void execute(janus_trainer* t, const Instruction& in, const janus_opt& opt) {
         if (t->ed.dp_degree > 1)
           for (janus_stage* st : mine)
             JANUS_NCCL(ncclAllReduce(st->grad, st->grad, static_cast<size_t>(st->n_params), ncclFloat, ncclSum, t->comm->dp, dv.compute));
-        for (janus_stage* st : mine) stage_optimizer(st, opt, dv.compute);
+        for (janus_stage* st : mine) stage_optimizer(st, opt, dv.compute, t->dopt);
       });
       return;
     }
@@ -506,9 +507,9 @@ void finalize_local(janus_trainer* t, const janus_opt& opt) {
       stage_reduce_grads(f, t->root);
       add_into(e->grad, f->grad, e->n_params, t->root);
       JANUS_CUDA(cudaMemcpyAsync(f->grad, e->grad, sizeof(float) * e->n_params, cudaMemcpyDeviceToDevice, t->root));
-      stage_optimizer(f, opt, t->root);
+      stage_optimizer(f, opt, t->root, t->dopt);
     }
-    stage_optimizer(e, opt, t->root);
+    stage_optimizer(e, opt, t->root, t->dopt);
   }
 }
 
@@ -527,6 +528,17 @@ janus_trainer* trainer_create(const janus_exec_desc& ed, const janus_stage_desc&
   if (ed.dp_degree < 1) t->ed.dp_degree = 1;
   if (ed.lanes < 1) t->ed.lanes = 1;
   if (ed.n_micro_batches < 1) throw domain_error("n_micro_batches must be >= 1");
+  {  // lanes share the device's hardware work queues (CUDA default 8); the library
+     // leaves the environment to the application and only says so
+    const char* e = std::getenv("CUDA_DEVICE_MAX_CONNECTIONS");
+    const int conn = e ? std::atoi(e) : 8;
+    static bool warned = false;
+    if (t->ed.lanes > conn && !warned) {
+      warned = true;
+      std::fprintf(stderr, "janus: %d compute lanes share %d hardware work queues (set CUDA_DEVICE_MAX_CONNECTIONS=%d "
+                   "before the first CUDA context for one queue per lane)\n", t->ed.lanes, conn, std::min(32, t->ed.lanes));
+    }
+  }
   if (!t->local && !comm) throw config_error("NCCL mode needs a janus_comm");
   if (t->local && t->ed.dp_degree != 1) throw config_error("data parallelism needs NCCL mode");
   switch (ed.method) {
@@ -592,6 +604,7 @@ janus_trainer* trainer_create(const janus_exec_desc& ed, const janus_stage_desc&
     JANUS_CUDA(cudaEventCreateWithFlags(&t->done_q[q], cudaEventDisableTiming));
     JANUS_CUDA(cudaMalloc(&t->loss_snap[q], sizeof(float) * 4 * static_cast<size_t>(std::max(1, ed.n_micro_batches))));
   }
+  JANUS_CUDA(cudaMalloc(&t->dopt, sizeof(janus_opt)));
   auto make = [&](int b) {
     janus_stage_desc d = sd;
     d.unit_begin = t->plan.blocks[static_cast<size_t>(b)].first;
@@ -688,6 +701,7 @@ void trainer_destroy(janus_trainer* t) {
     if (t->done_q[q]) cudaEventDestroy(t->done_q[q]);
     if (t->loss_snap[q]) cudaFree(t->loss_snap[q]);
   }
+  if (t->dopt) cudaFree(t->dopt);
   delete t;
 }
 
@@ -902,6 +916,9 @@ void trainer_step_async(janus_trainer* t, const janus_opt& opt) {
   t->recs.clear();
   t->recording = t->ed.record_timeline != 0;
   const int q = static_cast<int>(t->nsteps & 1);
+  // this step's optimizer hyperparameters: captured graphs read them from the
+  // device buffer (pageable source: staged by the driver before the call returns)
+  JANUS_CUDA(cudaMemcpyAsync(t->dopt, &opt, sizeof(janus_opt), cudaMemcpyHostToDevice, t->root));
   JANUS_CUDA(cudaEventRecord(t->anchor_q[q], t->root));
   if (exec) {
     JANUS_CUDA(cudaEventRecord(t->anchor, t->root));

@@ -326,13 +326,15 @@ __global__ void ledger_reduce_kernel(int64_t n, int n_mb, const float* __restric
 
 __global__ void adam_tick_kernel(int* step) { *step += 1; }
 
-// Bias corrections from the device-side step counter so a captured step
-// (CUDA graph) replays correctly.
+// Bias corrections from the device-side step counter and the hyperparameters
+// {lr, beta1, beta2, eps} from a device buffer, so a captured step (CUDA
+// graph) replays correctly when the caller changes the learning rate.
 __global__ void adam_kernel(int64_t n, float* __restrict__ p, float* __restrict__ m1, float* __restrict__ m2,
-                            const float* __restrict__ g, float lr, float b1, float b2, float eps,
+                            const float* __restrict__ g, const float* __restrict__ hp,
                             const int* __restrict__ step) {
   const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= n) return;
+  const float lr = hp[0], b1 = hp[1], b2 = hp[2], eps = hp[3];
   const float t = static_cast<float>(*step);
   const float c1 = 1.0f - powf(b1, t), c2 = 1.0f - powf(b2, t);
   const float gg = g[x];

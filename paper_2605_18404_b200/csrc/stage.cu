@@ -90,11 +90,12 @@ size_t geo_index(const janus_stage* st, int mb, int par) {
 DevGeo& geo_of(janus_stage* st, int mb) { return st->geo[geo_index(st, mb, st->gpar[static_cast<size_t>(mb)])]; }
 const DevGeo& geo_of(const janus_stage* st, int mb) { return st->geo[geo_index(st, mb, st->gpar[static_cast<size_t>(mb)])]; }
 
-// Attribution switch for profiling runs ONLY (numerically invalid when set):
-// JANUS_PROF_SKIP bitmask drops launches — 1 FE, 2 FF, 4 BF, 8 BE tensor-core
-// edge kernels, 16 wgrad_multi, 32 fused upd kernels, 64 gemm_rows, 128
-// reduce_partials — so the step-time drop
-// measures each family's share of the concurrent step (tools/dbg).
+// Attribution switch, compiled into profiling builds ONLY (`make PROFILE=1`;
+// numerically invalid when set): JANUS_PROF_SKIP bitmask drops launches — 1
+// FE, 2 FF, 4 BF, 8 BE tensor-core edge kernels, 16 wgrad_multi, 32 fused upd
+// kernels, 64 gemm_rows, 128 reduce_partials — so the step-time drop measures
+// each family's share of the concurrent step.  The product build is constant 0.
+#ifdef JANUS_PROFILING
 int prof_skip() {
   static const int v = [] {
     const char* e = std::getenv("JANUS_PROF_SKIP");
@@ -102,6 +103,9 @@ int prof_skip() {
   }();
   return v;
 }
+#else
+constexpr int prof_skip() { return 0; }
+#endif
 
 template <typename Op = node::InId>
 void gemm(cudaStream_t s, int rows, const float* X, const float* M, const float* bias, const float* add1,
@@ -349,6 +353,7 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
     st->m1 = dalloc<float>(st, NP, true);
     st->m2 = dalloc<float>(st, NP, true);
     st->dstep = dalloc<int>(st, 1, true);
+    st->dopt = dalloc<float>(st, 4, true);
     st->g1 = dalloc<float>(st, NP * NMB, true);
     st->g2 = dalloc<float>(st, NP * NMB, true);
     JANUS_CUDA(cudaMemcpy(st->params, unit_params, NP * sizeof(float), cudaMemcpyHostToDevice));
@@ -1183,11 +1188,15 @@ void stage_reduce_grads(janus_stage* st, cudaStream_t s) {
   JANUS_LAUNCH_CHECK("ledger_reduce");
 }
 
-void stage_optimizer(janus_stage* st, const janus_opt& o, cudaStream_t s) {
+void stage_optimizer(janus_stage* st, const janus_opt& o, cudaStream_t s, const float* dhp) {
   ++st->adam_step;
+  if (!dhp) {  // direct (uncaptured) call: the hyperparameters go through the stage's own buffer
+    JANUS_CUDA(cudaMemcpyAsync(st->dopt, &o, sizeof(janus_opt), cudaMemcpyHostToDevice, s));
+    dhp = st->dopt;
+  }
   node::adam_tick_kernel<<<1, 1, 0, s>>>(st->dstep);
-  node::adam_kernel<<<blocks(st->n_params, 256), 256, 0, s>>>(st->n_params, st->params, st->m1, st->m2, st->grad, o.lr,
-                                                              o.beta1, o.beta2, o.eps, st->dstep);
+  node::adam_kernel<<<blocks(st->n_params, 256), 256, 0, s>>>(st->n_params, st->params, st->m1, st->m2, st->grad, dhp,
+                                                              st->dstep);
   JANUS_LAUNCH_CHECK("adam");
   refresh_transposes(st, s);
 }

@@ -112,6 +112,7 @@ struct janus_stage {
   std::vector<float*> tw;              // per unit: transposed weights block
   int adam_step = 0;
   int* dstep = nullptr;  // device-side Adam step (graph-replayable bias correction)
+  float* dopt = nullptr; // device-side {lr, beta1, beta2, eps} for direct optimizer calls
   // geometry per micro-batch, double-buffered: geo[par * n_mb + mb]; the
   // phases read parity gpar[mb] while a trainer load may fill the other one
   // (a step in flight keeps reading its own copy)

@@ -33,7 +33,10 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane = 0);
 void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only = false, int lane = 0);
 void add_into(float* dst, const float* src, int64_t n, cudaStream_t s);
 void stage_reduce_grads(janus_stage* st, cudaStream_t s);
-void stage_optimizer(janus_stage* st, const janus_opt& o, cudaStream_t s);
+// dhp: device {lr, beta1, beta2, eps} read by the Adam kernel at run time (the
+// trainer's buffer, written before every step so replayed graphs see the
+// current values); nullptr: o is copied into the stage's own buffer on s.
+void stage_optimizer(janus_stage* st, const janus_opt& o, cudaStream_t s, const float* dhp = nullptr);
 void stage_port(janus_stage* st, int mb, int slot, int port, void** dptr, size_t* bytes);
 
 // read-back helpers (synchronous on the stream)

@@ -3,6 +3,10 @@ import sys
 
 import pytest
 
+# the application's choice (the library leaves the environment alone): one
+# hardware work queue per compute lane, before any CUDA context exists
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 for p in (ROOT, os.path.join(ROOT, "oracle"), os.path.join(ROOT, "tests", "golden")):
     if p not in sys.path:

@@ -64,3 +64,18 @@ def test_trace_is_consistent(oracle):
     r = oracle.step(model, batch, oracle.build_nbrlist(model, batch), g["params"], want_trace=True)
     assert r.trace.shape == (model.n_units, 8, batch.n_atoms, model.H)
     assert np.abs(r.trace[1, 0]).max() > 0 and np.abs(r.trace[model.n_units - 2, 6]).max() > 0
+
+
+@pytest.mark.parametrize("n,rho,seed", [(64, 0.095, 7), (256, 0.095, 701), (250, 0.095, 3), (4096, 0.19, 9)])
+def test_oracle_synth_matches_product(janus, oracle, n, rho, seed):
+    """The oracle's own synthetic-input restatement (used by bench.py's CPU
+    reference arm, which must not load the product library) is bit-identical
+    to the product's janus_synth_cell / janus_synth_params."""
+    pos, sp, box, Et, Ft = oracle.synth_cell(n, rho, 4, seed)
+    p2, s2, b2, E2, F2 = janus.synth_cell(n, rho, 4, seed)
+    assert box == b2 and Et == E2
+    assert np.array_equal(pos, p2) and np.array_equal(sp, s2) and np.array_equal(Ft, F2)
+    for L, H in ((4, 64), (2, 256)):
+        om = oracle.Model(L=L, H=H)
+        jm = janus.Model(L=L, H=H)
+        assert np.array_equal(oracle.synth_params(om, seed), jm.synth_params(seed))
