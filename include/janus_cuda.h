@@ -297,6 +297,20 @@ int janus_schedule_validate(const char* text, int32_t* n_errors);
  * sum idle / (devices * makespan). */
 int janus_schedule_replay(const char* text, const double* t, double* makespan, double* bubble_ratio);
 
+/* Blocking-rendezvous check of the multi-process (one process per GPU)
+ * issue program of a schedule (include/janus/rendezvous.hpp): each rank's
+ * lanes (micro-batch m on lane m % lanes) and transfer streams are simulated
+ * with NCCL semantics (a send and its receive complete together, only when
+ * both are at the heads of their streams; collectives complete when the
+ * whole group is at them).  layout 0 = the executor's per-channel streams,
+ * 1 = one shared send and one shared receive stream per rank (round 1's
+ * layout, kept to show it deadlocks).  *ok = 1 when every op completes;
+ * stuck (may be NULL) receives the blocked stream heads otherwise.  Replaces
+ * nothing in the reference: its DepGraph (graph.hpp:87-118) assumes
+ * non-blocking channels. */
+int janus_schedule_check_rendezvous(const char* text, int32_t onef1b, int32_t lanes, int32_t dp, int32_t layout,
+                                    int32_t* ok, int64_t* completed, int64_t* total, char* stuck, int64_t cap);
+
 #ifdef __cplusplus
 }
 #endif

@@ -485,6 +485,20 @@ def schedule_replay(text: str, t_fe: float, t_ff: float, t_be: float, t_bf: floa
     return ms.value, br.value
 
 
+_sig("janus_schedule_check_rendezvous", c_int, ctypes.c_char_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+     ctypes.c_int32, c_vp, c_vp, c_vp, ctypes.c_char_p, c_i64)
+
+
+def check_rendezvous(text: str, onef1b: bool = False, lanes: int = 1, dp: int = 1, shared_streams: bool = False):
+    """Blocking-rendezvous simulation of the multi-process issue program ->
+    (ok, completed ops, total ops, stuck stream heads)."""
+    ok, done, tot = ctypes.c_int32(), c_i64(), c_i64()
+    buf = ctypes.create_string_buffer(4096)
+    check(_lib.janus_schedule_check_rendezvous(text.encode(), 1 if onef1b else 0, lanes, dp, 1 if shared_streams else 0,
+                                               ctypes.byref(ok), ctypes.byref(done), ctypes.byref(tot), buf, 4096))
+    return bool(ok.value), done.value, tot.value, buf.value.decode()
+
+
 def device_count() -> int:
     n = c_int()
     check(_lib.janus_device_count(ctypes.byref(n)))

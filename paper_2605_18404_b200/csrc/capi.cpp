@@ -12,6 +12,7 @@
 #include "../../include/janus/gars.hpp"
 #include "../../include/janus/model.hpp"
 #include "../../include/janus/render.hpp"
+#include "../../include/janus/rendezvous.hpp"
 #include "../../include/janus/schedule_gen.hpp"
 #include "../../include/janus/tuner.hpp"
 
@@ -467,6 +468,29 @@ int janus_schedule_replay(const char* text, const double* t, double* makespan, d
     const janus::BubbleReport b = janus::bubble_of(g, r, d);
     *makespan = r.makespan;
     *bubble_ratio = b.bubble_ratio;
+  });
+}
+
+int janus_schedule_check_rendezvous(const char* text, int32_t onef1b, int32_t lanes, int32_t dp, int32_t layout,
+                                    int32_t* ok, int64_t* completed, int64_t* total, char* stuck, int64_t cap) {
+  return guard([&] {
+    need(text, "text");
+    need(ok, "ok");
+    if (lanes < 1 || dp < 1 || layout < 0 || layout > 1) throw janus::domain_error("bad lanes / dp / layout");
+    const janus::Schedule s = janus::deserialize(text);
+    const int P = static_cast<int>(s.stage_map.size()) / 2;
+    if (P < 1 || s.num_devices() != P) throw janus::domain_error("rendezvous check needs a P-device, 2P-virtual-stage schedule");
+    const auto progs = janus::build_programs(s, P, onef1b != 0, lanes, dp,
+                                             layout == 0 ? janus::StreamLayout::kPerChannel : janus::StreamLayout::kSharedPair);
+    const janus::RendezvousReport r = janus::simulate(progs, P, s, onef1b != 0);
+    *ok = r.ok ? 1 : 0;
+    if (completed) *completed = r.completed;
+    if (total) *total = r.ops;
+    if (stuck && cap > 0) {
+      const size_t n = std::min(static_cast<size_t>(cap - 1), r.stuck.size());
+      std::memcpy(stuck, r.stuck.data(), n);
+      stuck[n] = 0;
+    }
   });
 }
 
