@@ -208,6 +208,8 @@ def main():
     ap.add_argument("--method", default=None, choices=[None, "symfold", "wavek", "onef1b"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fp32-path", action="store_true", help="skip the fp32 SIMT parity-path throughput")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "ipc"],
+                    help="N>1: NCCL over NVLink (one GPU per rank), or the same-GPU IPC harness (all ranks on GPU 0)")
     ap.add_argument("--lanes", type=int, default=32, help="concurrent micro-batch streams at N=1 (one per micro-batch)")
     ap.add_argument("--precision", default="tf32", choices=["tf32", "fp32"],
                     help="tf32: tcgen05 tensor-core edge kernels (tolerances in tests/test_gpu_tf32.py); "
@@ -264,20 +266,28 @@ def main():
     batches = [J.synth_batch(model, [CONFIG["atoms"]], CONFIG["rho"], CONFIG["seed"] * 100 + m) for m in range(n_mb)]
     cfg["edges_per_structure"] = batches[0].n_edges
     comm = None
+    device = local_rank if args.transport == "nccl" else 0
     if N > 1:
+        import tempfile
+
         import torch.distributed as dist
         dist.init_process_group("gloo", init_method="env://")
-        uid = J.Comm.unique_id() if rank == 0 else None
-        obj = [uid]
-        dist.broadcast_object_list(obj, src=0)
-        comm = J.Comm(obj[0], world, rank, local_rank)
+        if args.transport == "nccl":
+            uid = J.Comm.unique_id() if rank == 0 else None
+            obj = [uid]
+            dist.broadcast_object_list(obj, src=0)
+            comm = J.Comm(obj[0], world, rank, local_rank)
+        else:  # all ranks on GPU 0, blocking-rendezvous IPC transport (csrc/transport.hpp)
+            obj = [tempfile.mkdtemp(prefix="janus_ipc_") if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            comm = J.Comm.ipc(obj[0], world, rank, 0)
     method_name = args.method or ("wavek" if N > 1 else "symfold")
     method = {"symfold": J.METHOD_SYMFOLD, "wavek": J.METHOD_WAVEK, "onef1b": J.METHOD_ONEF1B}[method_name]
     P = N
     k = min(n_mb, 2 * P)
     max_edges = max(b.n_edges for b in batches) + 64
     tr = J.Trainer(model, params, P, method, n_mb, k=k, max_atoms=CONFIG["atoms"], max_edges=max_edges,
-                   max_struct=1, local=(N == 1), graphs=(N == 1), comm=comm, rank=rank, device=local_rank,
+                   max_struct=1, local=(N == 1), graphs=(N == 1), comm=comm, rank=rank, device=device,
                    lanes=(args.lanes if N == 1 else min(args.lanes, 8)))
     for m, b in enumerate(batches):
         tr.load(m, b)
@@ -291,7 +301,7 @@ def main():
 
     l2 = []
     times, launches, stats = [], 0, None
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(device) as clk:
         for _ in range(args.steps):
             flush_l2(l2)
             barrier()
@@ -466,7 +476,9 @@ def main():
                "data": "synthetic",
                "config": dict(cfg, precision=args.precision, parallelism=f"pp{P}" if P > 1 else "single-gpu", schedule=method_name,
                               wavek_k=k if method == J.METHOD_WAVEK else None, cuda_graph=(N == 1),
-                              lanes=(args.lanes if N == 1 else min(args.lanes, 8))),
+                              lanes=(args.lanes if N == 1 else min(args.lanes, 8)),
+                              transport=(None if N == 1 else "nccl (one GPU per rank)" if args.transport == "nccl"
+                                         else f"ipc ({N} processes on one GPU)")),
                "e2e": {"value": e2e_val, "unit": "structures/s", "h2d_bytes_per_step": h2d,
                        "d2h_bytes_per_step": 8 * n_mb + d2h_lm, "input_pipelined": True,
                        "neighbour_lists": "rebuilt on the GPU every step (device LM)"},

@@ -169,9 +169,17 @@ int janus_stage_time_edge_kernel(janus_stage* st, int which, int mb, int slot, i
 int janus_stage_memory(janus_stage* st, int64_t* static_bytes, int64_t* arena_bytes);
 
 /* ---- transports ---- */
-/* NCCL: one communicator per process group; id from rank 0 via any channel. */
+/* NCCL: one base communicator per process group (id from rank 0 via any
+ * channel); a trainer splits one 2-rank communicator per transfer channel
+ * (flow, from, to) plus the 1F1B pair / data-parallel groups. */
 int janus_nccl_unique_id(void* id_out /* 128 bytes */);
 int janus_comm_init_nccl(const void* id, int nranks, int rank, int device, janus_comm** out);
+/* Same-GPU multi-process transport (the test harness for the per-rank path on
+ * one GPU): N processes on ONE device exchange CUDA-IPC regions through files
+ * in `dir` (one exchange per trainer) and run NCCL's blocking-rendezvous
+ * semantics with stream memory operations (csrc/transport.hpp).  The trainer
+ * treats it exactly like an NCCL comm. */
+int janus_comm_init_ipc(const char* dir, int nranks, int rank, int device, janus_comm** out);
 int janus_comm_destroy(janus_comm* c);
 int janus_comm_send(janus_comm* c, const void* buf, size_t bytes, int peer, void* stream);
 int janus_comm_recv(janus_comm* c, void* buf, size_t bytes, int peer, void* stream);

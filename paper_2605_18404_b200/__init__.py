@@ -440,6 +440,16 @@ class Stage:
         check(_lib.janus_stage_params(self.h, _p(out), None))
         return out
 
+    def grad_buffer(self) -> np.ndarray:
+        """The reduced gradient OS applied (after any pair / data-parallel all-reduce)."""
+        ptr, n = c_vp(), c_i64()
+        check(_lib.janus_stage_grad_buffer(self.h, ctypes.byref(ptr), ctypes.byref(n)))
+        out = np.zeros(n.value, np.float32)
+        rt = cudart()
+        assert rt.cudaDeviceSynchronize() == 0
+        assert rt.cudaMemcpy(out.ctypes.data, ptr.value, out.nbytes, 2) == 0
+        return out
+
     def reduce_grads(self, stream=None):
         check(_lib.janus_stage_reduce_grads(self.h, stream))
 
@@ -561,6 +571,7 @@ _sig("janus_trainer_schedule_text", c_int, c_vp, c_vp, c_i64, c_vp)
 _sig("janus_trainer_plan", c_int, c_vp, c_vp)
 _sig("janus_nccl_unique_id", c_int, c_vp)
 _sig("janus_comm_init_nccl", c_int, c_vp, c_int, c_int, c_int, c_vp)
+_sig("janus_comm_init_ipc", c_int, ctypes.c_char_p, c_int, c_int, c_int, c_vp)
 _sig("janus_comm_destroy", c_int, c_vp)
 
 
@@ -575,13 +586,23 @@ class _StageView(Stage):
 
 
 class Comm:
-    """NCCL communicator (one per process; rank r holds pipeline device r % P)."""
+    """Per-rank communicator (one per process; rank r holds pipeline device
+    r % P of replica r // P): NCCL, or the same-GPU IPC transport (Comm.ipc)."""
 
-    def __init__(self, uid: bytes, nranks: int, rank: int, device: int):
+    def __init__(self, uid: bytes | None, nranks: int, rank: int, device: int, ipc_dir: str | None = None):
         h = c_vp()
-        buf = ctypes.create_string_buffer(uid, 128)
-        check(_lib.janus_comm_init_nccl(buf, nranks, rank, device, ctypes.byref(h)))
+        if ipc_dir is not None:
+            check(_lib.janus_comm_init_ipc(ipc_dir.encode(), nranks, rank, device, ctypes.byref(h)))
+        else:
+            buf = ctypes.create_string_buffer(uid, 128)
+            check(_lib.janus_comm_init_nccl(buf, nranks, rank, device, ctypes.byref(h)))
         self.h = h
+
+    @classmethod
+    def ipc(cls, rendezvous_dir: str, nranks: int, rank: int, device: int = 0) -> "Comm":
+        """N processes on ONE GPU with NCCL's blocking-rendezvous semantics
+        (CUDA IPC staging + stream memory operations; csrc/transport.hpp)."""
+        return cls(None, nranks, rank, device, ipc_dir=rendezvous_dir)
 
     @staticmethod
     def unique_id() -> bytes:

@@ -297,6 +297,12 @@ int janus_comm_init_nccl(const void* id, int nranks, int rank, int device, janus
     *out = janus::comm_init_nccl(id, nranks, rank, device);
   });
 }
+int janus_comm_init_ipc(const char* dir, int nranks, int rank, int device, janus_comm** out) {
+  return guard([&] {
+    need(out, "out");
+    *out = janus::comm_init_ipc(dir, nranks, rank, device);
+  });
+}
 int janus_comm_destroy(janus_comm* c) {
   return guard([&] { janus::comm_destroy(c); });
 }

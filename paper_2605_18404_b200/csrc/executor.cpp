@@ -15,8 +15,12 @@
 //   local: all P virtual devices in this process on one GPU, each with its own
 //          compute/send streams; a send is an async D2D copy into the peer's
 //          port followed by an event the receiver's compute stream waits on.
-//   NCCL : one process per GPU, ncclSend / ncclRecv on dedicated send / recv
-//          streams per rank, so transfers overlap compute (NVLink/NVSwitch).
+//   per-rank (one process per GPU, transport.hpp): every channel (flow, from,
+//          to) has its own communicator and its own stream at each end, so a
+//          blocking send / receive only ever waits for its own channel's
+//          FIFO (include/janus/rendezvous.hpp proves the program deadlock-free
+//          at create).  NCCL over NVLink, or the same-GPU IPC transport that
+//          lets N processes exercise this path on one GPU.
 // 1F1B-2nd runs the force half on
 // replicated parameters: FF recomputes FE from the block input (mirror
 // transfer), BF is followed by an injection-only BE whose block-input
@@ -45,13 +49,14 @@
 #include "stage.cuh"
 #include "stage_api.hpp"
 #include "nbrlist.hpp"
+#include "transport.hpp"
 
 namespace janus {
 namespace {
 
-// One channel per flow.  1F1B-2nd pairs two blocks per device pair, so its
-// mirror flows are split by block parity to keep per-channel order = mb order.
-enum Flow { kFlowAct = 0, kFlowAdj = 1, kFlowTan = 2, kFlowBadj = 3, kFlowMirror = 4, kFlowMirrorBack = 6, kNumFlows = 8 };
+// Channels (include/janus/rendezvous.hpp): flows act / adj / tan / badj plus
+// the 1F1B-2nd mirror flows, which pair two blocks per device pair and are
+// split by block parity to keep per-channel order = micro-batch order.
 
 inline void nccl_check(ncclResult_t r, const char* what) {
   if (r != ncclSuccess) throw nccl_error(std::string(what) + ": " + ncclGetErrorString(r));
@@ -60,14 +65,6 @@ inline void nccl_check(ncclResult_t r, const char* what) {
 
 }  // namespace
 }  // namespace janus
-
-struct janus_comm {
-  int nranks = 1, rank = 0, device = 0;
-  ncclComm_t base = nullptr;
-  ncclComm_t flow[janus::kNumFlows] = {};
-  ncclComm_t pair = nullptr;  // 1F1B-2nd replicated-parameter pairs
-  ncclComm_t dp = nullptr;    // data-parallel replicas of one stage
-};
 
 namespace janus {
 namespace {
@@ -107,6 +104,9 @@ struct janus_trainer {
   std::vector<int> E_dev, F_dev;                 // schedule device that holds E_b / F_b
   std::vector<janus_stage*> owned;
   std::vector<float*> mirror_buf;                // 1F1B: [block*n_mb + mb] cotangent from F_b
+  std::vector<janus::ChannelKey> chans;          // per-rank mode: every channel of the schedule
+  std::vector<cudaStream_t> chan_stream;         // per channel: this rank's end (nullptr: not a member)
+  std::unique_ptr<janus::Transport> xport;       // per-rank mode: NCCL or same-GPU IPC
   std::vector<void*> allocs;
   cudaStream_t root = nullptr;
   cudaEvent_t anchor = nullptr, finish = nullptr;
@@ -231,27 +231,45 @@ cudaStream_t lane_stream(const janus_trainer* t, const VDev& dv, int mb) {
 }
 int lane_index(const VDev& dv, int mb) { return (mb < 0 ? 0 : mb) % static_cast<int>(dv.lane.size()); }
 
+// per-rank mode: a payload leaves on its channel's own stream once the lane
+// that produced it got there
+void chan_send(janus_trainer* t, VDev& dv, int flow, int mb, const float* sp, size_t sb, int peer_dev) {
+  const int c = channel_index(t->chans, {flow, dv.id, peer_dev});
+  cudaStream_t cs = t->chan_stream[static_cast<size_t>(c)];
+  cudaEvent_t ready = next_event(t);
+  JANUS_CUDA(cudaEventRecord(ready, lane_stream(t, dv, mb)));
+  JANUS_CUDA(cudaStreamWaitEvent(cs, ready, 0));
+  t->p2p_bytes += static_cast<int64_t>(sb);
+  t->xport->send(c, sp, sb, peer_rank(t, peer_dev), cs);
+}
+// ... and lands on its channel's stream; the lane waits for it
+void chan_recv(janus_trainer* t, VDev& dv, int flow, int mb, float* dp, size_t db, int peer_dev) {
+  const int c = channel_index(t->chans, {flow, peer_dev, dv.id});
+  cudaStream_t cs = t->chan_stream[static_cast<size_t>(c)];
+  t->xport->recv(c, dp, db, peer_rank(t, peer_dev), cs);
+  cudaEvent_t done = next_event(t);
+  JANUS_CUDA(cudaEventRecord(done, cs));
+  JANUS_CUDA(cudaStreamWaitEvent(lane_stream(t, dv, mb), done, 0));
+}
+
 void do_send(janus_trainer* t, VDev& dv, int flow, int mb, janus_stage* src, int sport, janus_stage* dst, int dport,
              int from_b, int to_b, int peer_dev) {
   float* sp;
   size_t sb;
   port_ptr(src, mb, sport, &sp, &sb);
+  if (!t->local) return chan_send(t, dv, flow, mb, sp, sb, peer_dev);
   cudaEvent_t ready = next_event(t);
   JANUS_CUDA(cudaEventRecord(ready, lane_stream(t, dv, mb)));
   JANUS_CUDA(cudaStreamWaitEvent(dv.send, ready, 0));
   t->p2p_bytes += static_cast<int64_t>(sb);
-  if (t->local) {
-    float* dp;
-    size_t db;
-    port_ptr(dst, mb, dport, &dp, &db);
-    if (db != sb) throw state_error("port size mismatch between channel ends");
-    JANUS_CUDA(cudaMemcpyAsync(dp, sp, sb, cudaMemcpyDeviceToDevice, dv.send));
-    cudaEvent_t done = next_event(t);
-    JANUS_CUDA(cudaEventRecord(done, dv.send));
-    t->delivered[{flow, mb, from_b, to_b}] = done;
-  } else {
-    JANUS_NCCL(ncclSend(sp, sb, ncclChar, peer_rank(t, peer_dev), t->comm->flow[flow], dv.send));
-  }
+  float* dp;
+  size_t db;
+  port_ptr(dst, mb, dport, &dp, &db);
+  if (db != sb) throw state_error("port size mismatch between channel ends");
+  JANUS_CUDA(cudaMemcpyAsync(dp, sp, sb, cudaMemcpyDeviceToDevice, dv.send));
+  cudaEvent_t done = next_event(t);
+  JANUS_CUDA(cudaEventRecord(done, dv.send));
+  t->delivered[{flow, mb, from_b, to_b}] = done;
 }
 
 void do_recv(janus_trainer* t, VDev& dv, int flow, int mb, janus_stage* dst, int dport, int from_b, int to_b,
@@ -266,10 +284,7 @@ void do_recv(janus_trainer* t, VDev& dv, int flow, int mb, janus_stage* dst, int
     size_t db;
     port_ptr(dst, mb, dport, &dp, &db);
     if (db != bytes) throw state_error("port size mismatch between channel ends");
-    JANUS_NCCL(ncclRecv(dp, db, ncclChar, peer_rank(t, peer_dev), t->comm->flow[flow], dv.recv));
-    cudaEvent_t done = next_event(t);
-    JANUS_CUDA(cudaEventRecord(done, dv.recv));
-    JANUS_CUDA(cudaStreamWaitEvent(lane_stream(t, dv, mb), done, 0));
+    chan_recv(t, dv, flow, mb, dp, db, peer_dev);
   }
 }
 
@@ -293,19 +308,16 @@ void mirror_back_send(janus_trainer* t, VDev& dv, int b, int mb) {
   float* sp;
   size_t sb;
   port_ptr(f, mb, JANUS_PORT_BADJ_OUT, &sp, &sb);
+  if (!t->local) return chan_send(t, dv, kFlowMirrorBack + (b & 1), mb, sp, sb, t->E_dev[static_cast<size_t>(b)]);
   cudaEvent_t ready = next_event(t);
   JANUS_CUDA(cudaEventRecord(ready, lane_stream(t, dv, mb)));
   JANUS_CUDA(cudaStreamWaitEvent(dv.send, ready, 0));
   t->p2p_bytes += static_cast<int64_t>(sb);
   float* buf = t->mirror_buf[static_cast<size_t>(b) * t->ed.n_micro_batches + mb];
-  if (t->local) {
-    JANUS_CUDA(cudaMemcpyAsync(buf, sp, sb, cudaMemcpyDeviceToDevice, dv.send));
-    cudaEvent_t done = next_event(t);
-    JANUS_CUDA(cudaEventRecord(done, dv.send));
-    t->delivered[{kFlowMirrorBack, mb, b, b}] = done;
-  } else {
-    JANUS_NCCL(ncclSend(sp, sb, ncclChar, peer_rank(t, t->E_dev[static_cast<size_t>(b)]), t->comm->flow[kFlowMirrorBack + (b & 1)], dv.send));
-  }
+  JANUS_CUDA(cudaMemcpyAsync(buf, sp, sb, cudaMemcpyDeviceToDevice, dv.send));
+  cudaEvent_t done = next_event(t);
+  JANUS_CUDA(cudaEventRecord(done, dv.send));
+  t->delivered[{kFlowMirrorBack, mb, b, b}] = done;
 }
 void mirror_back_recv_add(janus_trainer* t, VDev& dv, int b, int mb) {
   if (b == 0) return;
@@ -320,10 +332,7 @@ void mirror_back_recv_add(janus_trainer* t, VDev& dv, int b, int mb) {
     JANUS_CUDA(cudaStreamWaitEvent(lane_stream(t, dv, mb), it->second, 0));
     t->delivered.erase(it);
   } else {
-    JANUS_NCCL(ncclRecv(buf, db, ncclChar, peer_rank(t, t->F_dev[static_cast<size_t>(b)]), t->comm->flow[kFlowMirrorBack + (b & 1)], dv.recv));
-    cudaEvent_t done = next_event(t);
-    JANUS_CUDA(cudaEventRecord(done, dv.recv));
-    JANUS_CUDA(cudaStreamWaitEvent(lane_stream(t, dv, mb), done, 0));
+    chan_recv(t, dv, kFlowMirrorBack + (b & 1), mb, buf, db, t->F_dev[static_cast<size_t>(b)]);
   }
   add_into(dp, buf, static_cast<int64_t>(db / sizeof(float)), lane_stream(t, dv, mb));
 }
@@ -437,11 +446,9 @@ void execute(janus_trainer* t, const Instruction& in, const janus_opt& opt) {
         }
         for (janus_stage* st : mine) stage_reduce_grads(st, dv.compute);
         if (t->onef1b)  // replicated parameters: energy and force copies sum their grads
-          for (janus_stage* st : mine)
-            JANUS_NCCL(ncclAllReduce(st->grad, st->grad, static_cast<size_t>(st->n_params), ncclFloat, ncclSum, t->comm->pair, dv.compute));
-        if (t->ed.dp_degree > 1)
-          for (janus_stage* st : mine)
-            JANUS_NCCL(ncclAllReduce(st->grad, st->grad, static_cast<size_t>(st->n_params), ncclFloat, ncclSum, t->comm->dp, dv.compute));
+          for (janus_stage* st : mine) t->xport->allreduce(0, st->grad, static_cast<size_t>(st->n_params), dv.compute);
+        if (t->ed.dp_degree > 1)  // PP x DP: replicas of this stage sum their grads (AR before OS)
+          for (janus_stage* st : mine) t->xport->allreduce(1, st->grad, static_cast<size_t>(st->n_params), dv.compute);
         for (janus_stage* st : mine) stage_optimizer(st, opt, dv.compute, t->dopt);
       });
       return;
@@ -481,6 +488,8 @@ void fork_join_begin(janus_trainer* t) {
     JANUS_CUDA(cudaStreamWaitEvent(d.send, t->anchor, 0));
     JANUS_CUDA(cudaStreamWaitEvent(d.recv, t->anchor, 0));
   }
+  for (cudaStream_t s : t->chan_stream)
+    if (s) JANUS_CUDA(cudaStreamWaitEvent(s, t->anchor, 0));
 }
 
 void fork_join_end(janus_trainer* t) {
@@ -488,6 +497,8 @@ void fork_join_end(janus_trainer* t) {
     std::vector<cudaStream_t> all = d.lane;
     all.push_back(d.send);
     all.push_back(d.recv);
+    for (cudaStream_t s : t->chan_stream)
+      if (s) all.push_back(s);
     for (cudaStream_t s : all) {
       cudaEvent_t e = next_event(t);
       JANUS_CUDA(cudaEventRecord(e, s));
@@ -636,13 +647,36 @@ janus_trainer* trainer_create(const janus_exec_desc& ed, const janus_stage_desc&
       }
     }
   }
-  if (!t->local && (t->onef1b || t->ed.dp_degree > 1)) {
-    // split sub-communicators: pairs (d, P-1-d) of one replica; replicas of one stage
-    const int d = t->my_dev;
-    const int pair_color = t->onef1b ? t->replica * t->P + std::min(d, t->P - 1 - d) : NCCL_SPLIT_NOCOLOR;
-    JANUS_NCCL(ncclCommSplit(comm->base, pair_color, rank, &comm->pair, nullptr));
-    const int dp_color = t->ed.dp_degree > 1 ? d : NCCL_SPLIT_NOCOLOR;
-    JANUS_NCCL(ncclCommSplit(comm->base, dp_color, rank, &comm->dp, nullptr));
+  if (!t->local) {
+    // the per-rank program must be deadlock-free under blocking P2P before anything is issued
+    const auto progs = build_programs(t->sched, t->P, t->onef1b, t->ed.lanes, t->ed.dp_degree, StreamLayout::kPerChannel);
+    const RendezvousReport rr = simulate(progs, t->P, t->sched, t->onef1b);
+    if (!rr.ok) throw deadlock_error("per-rank issue program cannot complete under blocking P2P:\n" + rr.stuck);
+    TransportPlan tp;
+    tp.chans = schedule_channels(t->sched, t->P, t->onef1b);
+    tp.P = t->P;
+    tp.dp = t->ed.dp_degree;
+    tp.rank = rank;
+    tp.pair_group = t->onef1b;
+    const int d = t->my_dev, base = t->replica * t->P;
+    if (t->onef1b) {  // ranks holding the two copies of this rank's blocks
+      for (int b = 0; b < t->P; ++b)
+        if (t->E_dev[static_cast<size_t>(b)] == d || t->F_dev[static_cast<size_t>(b)] == d) {
+          tp.pair_members.push_back(base + t->E_dev[static_cast<size_t>(b)]);
+          tp.pair_members.push_back(base + t->F_dev[static_cast<size_t>(b)]);
+        }
+      std::sort(tp.pair_members.begin(), tp.pair_members.end());
+      tp.pair_members.erase(std::unique(tp.pair_members.begin(), tp.pair_members.end()), tp.pair_members.end());
+      if (tp.pair_members.size() != 2) throw config_error("1F1B-2nd: a device must pair with exactly one other");
+    }
+    for (int q = 0; q < t->ed.dp_degree; ++q) tp.dp_members.push_back(q * t->P + d);
+    tp.max_payload = sizeof(float) * (static_cast<size_t>(sd.max_atoms) * sd.model.H * 2 + 3 * static_cast<size_t>(sd.max_atoms));
+    for (janus_stage* st : t->owned) tp.max_allreduce = std::max(tp.max_allreduce, sizeof(float) * static_cast<size_t>(st->n_params));
+    t->chans = tp.chans;
+    t->chan_stream.assign(t->chans.size(), nullptr);
+    for (size_t c = 0; c < t->chans.size(); ++c)
+      if (t->chans[c].from == d || t->chans[c].to == d) JANUS_CUDA(cudaStreamCreateWithFlags(&t->chan_stream[c], cudaStreamNonBlocking));
+    t->xport = make_transport(comm, tp);
   }
   // local issue order: a topological order of the full DAG (seq + data edges),
   // so every send is issued before its receive.
@@ -679,6 +713,9 @@ void trainer_destroy(janus_trainer* t) {
   if (t->load_done) cudaEventDestroy(t->load_done);
   for (cudaEvent_t e : t->step_end)
     if (e) cudaEventDestroy(e);
+  t->xport.reset();
+  for (cudaStream_t s : t->chan_stream)
+    if (s) cudaStreamDestroy(s);
   for (janus_stage* s : t->owned) stage_destroy(s);
   for (void* p : t->allocs) cudaFree(p);
   for (cudaEvent_t e : t->pool) cudaEventDestroy(e);
@@ -1053,35 +1090,47 @@ void nccl_unique_id(void* out) {
 janus_comm* comm_init_nccl(const void* id, int nranks, int rank, int device) {
   JANUS_CUDA(cudaSetDevice(device));
   auto c = std::make_unique<janus_comm>();
+  c->kind = 0;
   c->nranks = nranks;
   c->rank = rank;
   c->device = device;
   ncclUniqueId uid;
   std::memcpy(&uid, id, sizeof(uid));
   JANUS_NCCL(ncclCommInitRank(&c->base, nranks, uid, rank));
-  for (int f = 0; f < kNumFlows; ++f) JANUS_NCCL(ncclCommSplit(c->base, 0, rank, &c->flow[f], nullptr));
+  return c.release();
+}
+
+janus_comm* comm_init_ipc(const char* dir, int nranks, int rank, int device) {
+  if (!dir || !*dir) throw domain_error("IPC comm needs a rendezvous directory");
+  if (nranks < 1 || rank < 0 || rank >= nranks) throw domain_error("bad rank / nranks");
+  JANUS_CUDA(cudaSetDevice(device));
+  auto c = std::make_unique<janus_comm>();
+  c->kind = 1;
+  c->nranks = nranks;
+  c->rank = rank;
+  c->device = device;
+  c->dir = dir;
   return c.release();
 }
 
 void comm_destroy(janus_comm* c) {
   if (!c) return;
-  for (auto& f : c->flow)
-    if (f) ncclCommDestroy(f);
-  if (c->pair) ncclCommDestroy(c->pair);
-  if (c->dp) ncclCommDestroy(c->dp);
   if (c->base) ncclCommDestroy(c->base);
   delete c;
 }
 
 void comm_send(janus_comm* c, const void* buf, size_t bytes, int peer, cudaStream_t s) {
+  if (c->kind != 0) throw config_error("generic send needs an NCCL comm");
   JANUS_NCCL(ncclSend(buf, bytes, ncclChar, peer, c->base, s));
 }
 void comm_recv(janus_comm* c, void* buf, size_t bytes, int peer, cudaStream_t s) {
+  if (c->kind != 0) throw config_error("generic receive needs an NCCL comm");
   JANUS_NCCL(ncclRecv(buf, bytes, ncclChar, peer, c->base, s));
 }
 void comm_group_start() { JANUS_NCCL(ncclGroupStart()); }
 void comm_group_end() { JANUS_NCCL(ncclGroupEnd()); }
 void comm_allreduce_sum(janus_comm* c, float* buf, int64_t count, cudaStream_t s) {
+  if (c->kind != 0) throw config_error("generic all-reduce needs an NCCL comm");
   JANUS_NCCL(ncclAllReduce(buf, buf, static_cast<size_t>(count), ncclFloat, ncclSum, c->base, s));
 }
 

@@ -1,0 +1,64 @@
+"""One rank of the same-GPU multi-process harness (tests/test_gpu_multirank.py).
+
+Runs the per-rank (local_stages = 0) executor path exactly as a one-process-
+per-GPU job does — its own trainer holding only this rank's blocks, channel
+streams, blocking-rendezvous transfers and group all-reduces — but on the IPC
+transport, so N processes can share the one GPU this run has.
+
+  python tests/multirank_worker.py <json config> <rank> <out.npz>
+"""
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def batches_for(J, m, cfg, replica):
+    n = cfg["n_mb"]
+    return [J.synth_batch(m, cfg["atoms"][(replica * n + i) % len(cfg["atoms"])], 0.095, 100 + replica * n + i)
+            for i in range(n)]
+
+
+def main():
+    cfg = json.loads(sys.argv[1])
+    rank = int(sys.argv[2])
+    out = sys.argv[3]
+    import paper_2605_18404_b200 as J
+
+    P, D = cfg["P"], cfg["dp"]
+    world = P * D
+    m = J.Model(L=cfg["L"], H=64, R=64, precision=J.PREC_TF32 if cfg["prec"] == "tf32" else J.PREC_FP32)
+    params = m.synth_params(cfg["seed"])
+    comm = J.Comm.ipc(cfg["dir"], world, rank, 0)
+    tr = J.Trainer(m, params, P, cfg["method"], cfg["n_mb"], k=cfg.get("k", 1), max_atoms=cfg["max_atoms"],
+                   max_edges=cfg["max_atoms"] * 120, max_struct=2, local=False, comm=comm, rank=rank, device=0,
+                   dp=D, lanes=cfg["lanes"])
+    bs = batches_for(J, m, cfg, rank // P)
+    res = {}
+    losses = []
+    for step in range(cfg["steps"]):
+        tr.load_many(bs)
+        s = tr.step(lr=1e-3)
+        losses.append(s.loss)
+        res["p2p_bytes"] = s.p2p_bytes
+    for b in range(P):
+        for fr in (False, True):
+            try:
+                st = tr.stage(b, force_replica=fr)
+            except J.JanusError:
+                continue
+            tag = f"{'F' if fr else 'E'}{b}"
+            res[f"params_{tag}"] = st.params()
+            res[f"grads_{tag}"] = st.grad_buffer()
+    res["loss"] = np.array(losses)
+    tr.close()
+    comm.close()
+    np.savez(out, **res)
+
+
+if __name__ == "__main__":
+    main()
