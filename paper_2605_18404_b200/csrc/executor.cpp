@@ -671,7 +671,10 @@ janus_trainer* trainer_create(const janus_exec_desc& ed, const janus_stage_desc&
     }
     for (int q = 0; q < t->ed.dp_degree; ++q) tp.dp_members.push_back(q * t->P + d);
     tp.max_payload = sizeof(float) * (static_cast<size_t>(sd.max_atoms) * sd.model.H * 2 + 3 * static_cast<size_t>(sd.max_atoms));
-    for (janus_stage* st : t->owned) tp.max_allreduce = std::max(tp.max_allreduce, sizeof(float) * static_cast<size_t>(st->n_params));
+    // the IPC region layout must agree on every rank, so size the all-reduce
+    // staging from the whole partition, not from the blocks this rank holds
+    for (const auto& blk : t->plan.blocks)
+      tp.max_allreduce = std::max(tp.max_allreduce, sizeof(float) * static_cast<size_t>(mc.unit_param_offset(blk.second) - mc.unit_param_offset(blk.first)));
     t->chans = tp.chans;
     t->chan_stream.assign(t->chans.size(), nullptr);
     for (size_t c = 0; c < t->chans.size(); ++c)

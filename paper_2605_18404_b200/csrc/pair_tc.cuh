@@ -337,6 +337,93 @@ __global__ void __launch_bounds__(256) msg_ff_rows(int n_atoms, const int* __res
 }
 
 // ------------------------------------------------------------ BF / BE per pair
+// Per-pair adjoints in the WARP-PER-PAIR layout: warp w builds rows 8w..8w+7
+// of the chunk's bf16 adjoint tiles, lane l holding features 2l, 2l+1, so one
+// 8-byte load per lane fetches a whole 256 B node row (2 L1 lines per load
+// instruction).  The thread-per-edge layout the TMEM epilogues need had each
+// load instruction touch 32 different rows (32 L1 wavefronts; ~12k per chunk
+// for BF's six gathers, the kernels' top stall).  The arithmetic is the same
+// fp32 expression per element, so the tiles are bit-identical.
+struct PairRec {  // lanes 0..7: the scalars of pair 8w + lane
+  int i = 0, j = 0;
+  float c = 0.f, dc = 0.f, qb = 0.f;
+};
+__device__ __forceinline__ PairRec pair_rec(const float4* __restrict__ pg, int n_pairs, int p, const float* __restrict__ Fbar) {
+  PairRec r;
+  if (p < n_pairs) {
+    const float4 g0 = __ldg(pg + 2 * p), g1 = __ldg(pg + 2 * p + 1);
+    r.c = g0.y;
+    r.dc = g0.z;
+    r.i = __float_as_int(g0.w);
+    r.j = __float_as_int(g1.w);
+    if (Fbar)  // <Fbar_i - Fbar_j, u> (qb_rev = qb: u_rev = -u)
+      r.qb = fmaf(__ldg(Fbar + 3 * r.i) - __ldg(Fbar + 3 * r.j), g1.x,
+                  fmaf(__ldg(Fbar + 3 * r.i + 1) - __ldg(Fbar + 3 * r.j + 1), g1.y,
+                       (__ldg(Fbar + 3 * r.i + 2) - __ldg(Fbar + 3 * r.j + 2)) * g1.z));
+  }
+  return r;
+}
+__device__ __forceinline__ float2 ldrow2(const float* __restrict__ x, int row, int lane) {
+  return __ldg(reinterpret_cast<const float2*>(x + (size_t)row * H) + lane);
+}
+__device__ __forceinline__ void st_b16x2(uint8_t* t, int e, int f, float a, float b) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  *reinterpret_cast<uint32_t*>(t + off_b16(e, f)) = *reinterpret_cast<const uint32_t*>(&v);
+}
+// BF: mu -> tmu, nu -> tnu for the chunk's 128 pairs (all 16 warps)
+__device__ __forceinline__ void bf_adjoints_rows(const float4* __restrict__ pg, int n_pairs, int p0,
+                                                 const float* __restrict__ Fbar, const float* __restrict__ v,
+                                                 const float* __restrict__ vdot, const float* __restrict__ am, uint8_t* tmu,
+                                                 uint8_t* tnu) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const PairRec r = pair_rec(pg, n_pairs, lane < 8 ? p0 + 8 * warp + lane : n_pairs, Fbar);
+#pragma unroll
+  for (int b = 0; b < 2; ++b) {
+    float2 ai[4], aj[4], vi[4], vj[4], di[4], dj[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = __shfl_sync(0xffffffffu, r.i, 4 * b + k), j = __shfl_sync(0xffffffffu, r.j, 4 * b + k);
+      ai[k] = ldrow2(am, i, lane);
+      aj[k] = ldrow2(am, j, lane);
+      vi[k] = ldrow2(v, i, lane);
+      vj[k] = ldrow2(v, j, lane);
+      di[k] = ldrow2(vdot, i, lane);
+      dj[k] = ldrow2(vdot, j, lane);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float cc = __shfl_sync(0xffffffffu, r.c, 4 * b + k), dc = __shfl_sync(0xffffffffu, r.dc, 4 * b + k);
+      const float qb = __shfl_sync(0xffffffffu, r.qb, 4 * b + k);
+      const float rx = fmaf(ai[k].x, vj[k].x, aj[k].x * vi[k].x), ry = fmaf(ai[k].y, vj[k].y, aj[k].y * vi[k].y);
+      const float kx = fmaf(ai[k].x, dj[k].x, aj[k].x * di[k].x), ky = fmaf(ai[k].y, dj[k].y, aj[k].y * di[k].y);
+      const int e = 8 * warp + 4 * b + k;
+      st_b16x2(tmu, e, 2 * lane, qb * dc * rx + cc * kx, qb * dc * ry + cc * ky);
+      st_b16x2(tnu, e, 2 * lane, qb * cc * rx, qb * cc * ry);
+    }
+  }
+}
+// BE: gbar = c (bm_i v_j + bm_j v_i) -> tg
+__device__ __forceinline__ void be_adjoint_rows(const float4* __restrict__ pg, int n_pairs, int p0, const float* __restrict__ v,
+                                                const float* __restrict__ bm, uint8_t* tg) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const PairRec r = pair_rec(pg, n_pairs, lane < 8 ? p0 + 8 * warp + lane : n_pairs, nullptr);
+  float2 bi[8], bj[8], vi[8], vj[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int i = __shfl_sync(0xffffffffu, r.i, k), j = __shfl_sync(0xffffffffu, r.j, k);
+    bi[k] = ldrow2(bm, i, lane);
+    bj[k] = ldrow2(bm, j, lane);
+    vi[k] = ldrow2(v, i, lane);
+    vj[k] = ldrow2(v, j, lane);
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const float cc = __shfl_sync(0xffffffffu, r.c, k);
+    st_b16x2(tg, 8 * warp + k, 2 * lane, cc * fmaf(bi[k].x, vj[k].x, bj[k].x * vi[k].x),
+             cc * fmaf(bi[k].y, vj[k].y, bj[k].y * vi[k].y));
+  }
+}
+
 // The weight gradients are linear in the per-edge adjoints (mu, nu of BF;
 // gbar of BE) with pair-symmetric left factors (phi, phi', s, sdot, z, z'), so
 // they are accumulated once per pair on the SUMS of both directions:
@@ -385,42 +472,14 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_pair_tc(EdgeGeom g, const float4
     const int pp = ch * TE + c.e;
     const bool ok = pp < n_pairs;
     const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4 g0 = ok ? __ldg(pg + 2 * pp) : z4, g1 = ok ? __ldg(pg + 2 * pp + 1) : z4;
-    const float d = g0.x, cc = g0.y, dc = g0.z;
-    const int i = ok ? __float_as_int(g0.w) : 0, j = ok ? __float_as_int(g1.w) : 0;
-    // the node-row gathers go first: their latency overlaps the basis and the z MMAs
-    float ai[FPT], aj[FPT], vi[FPT], vj[FPT];
-    gather32(am, i, f0, ai);
-    gather32(am, j, f0, aj);
-    gather32(v, i, f0, vi);
-    gather32(v, j, f0, vj);
-    float qb = 0.f;  // <Fbar_i - Fbar_j, u_x> (qb_rev = qb: u_rev = -u)
-    if (ok)
-      qb = fmaf(__ldg(Fbar + 3 * i) - __ldg(Fbar + 3 * j), g1.x,
-                fmaf(__ldg(Fbar + 3 * i + 1) - __ldg(Fbar + 3 * j + 1), g1.y,
-                     (__ldg(Fbar + 3 * i + 2) - __ldg(Fbar + 3 * j + 2)) * g1.z));
+    const float d = ok ? __ldg(&pg[2 * pp].x) : z4.x;
     {
       float ph[FPT], dph[FPT];
       basis(d, rc, f0, ph, dph);
       st_b16(B4, c.e, f0, ph);
       st_b16(B5, c.e, f0, dph);
     }
-    {
-      float rho[FPT];
-#pragma unroll
-      for (int k = 0; k < FPT; ++k) rho[k] = fmaf(ai[k], vj[k], aj[k] * vi[k]);
-      gather32(vdot, i, f0, vi);
-      gather32(vdot, j, f0, vj);
-#pragma unroll
-      for (int k = 0; k < FPT; ++k) {
-        const float kap = fmaf(ai[k], vj[k], aj[k] * vi[k]);
-        const float r = rho[k];
-        rho[k] = qb * dc * r + cc * kap;  // mu
-        ai[k] = qb * cc * r;              // nu
-      }
-      st_b16(B2, c.e, f0, rho);  // mu (B of dB, A of sbar)
-      st_b16(B3, c.e, f0, ai);   // nu
-    }
+    bf_adjoints_rows(pg, n_pairs, ch * TE, Fbar, v, vdot, am, B2, B3);  // mu (B of dB, A of sbar), nu
     tc::mbar_wait(&wbar, 0);
     c.publish();
     if (threadIdx.x == 0) {
@@ -520,24 +579,13 @@ __global__ void __launch_bounds__(NT, 1) msg_be_pair_tc(EdgeGeom g, const float4
     const int pp = ch * TE + c.e;
     const bool ok = pp < n_pairs;
     const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4 g0 = ok ? __ldg(pg + 2 * pp) : z4;
-    const float d = g0.x, cc = g0.y;
-    const int i = ok ? __float_as_int(g0.w) : 0, j = ok ? __float_as_int(__ldg(&pg[2 * pp + 1].w)) : 0;
-    float gb[FPT];
+    const float d = ok ? __ldg(&pg[2 * pp].x) : z4.x;
     {
-      float bi[FPT], bj[FPT], vi[FPT], vj[FPT];
-      gather32(bm, i, f0, bi);  // gathers first: their latency overlaps the basis
-      gather32(bm, j, f0, bj);
-      gather32(v, i, f0, vi);
-      gather32(v, j, f0, vj);
-      {
-        float ph[FPT], dph[FPT];
-        basis(d, rc, f0, ph, dph);
-        st_b16(B0, c.e, f0, ph);
-      }
-#pragma unroll
-      for (int k = 0; k < FPT; ++k) gb[k] = cc * fmaf(bi[k], vj[k], bj[k] * vi[k]);  // zero on padding (c = 0)
+      float ph[FPT], dph[FPT];
+      basis(d, rc, f0, ph, dph);
+      st_b16(B0, c.e, f0, ph);
     }
+    be_adjoint_rows(pg, n_pairs, ch * TE, v, bm, B2);  // gbar (zero on padding: c = 0)
     tc::mbar_wait(&wbar, 0);
     c.publish();
     if (threadIdx.x == 0) {
@@ -554,7 +602,6 @@ __global__ void __launch_bounds__(NT, 1) msg_be_pair_tc(EdgeGeom g, const float4
         z[k] = zz * fsig(zz);
       }
       st_b16(B1, c.e, f0, z);  // s
-      st_b16(B2, c.e, f0, gb);
     }
     c.publish();
     if (threadIdx.x == 0) {

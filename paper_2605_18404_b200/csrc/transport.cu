@@ -1,6 +1,5 @@
 // transport.cu — NCCL and same-GPU IPC transports of the executor (see
 // transport.hpp for the channel and rendezvous semantics).
-#include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 #include <unistd.h>
@@ -78,31 +77,32 @@ class NcclTransport final : public Transport {
 };
 
 // ------------------------------------------------------------------- IPC
-using WaitFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
-using WriteFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
-
-WaitFn g_wait = nullptr;
-WriteFn g_write = nullptr;
-
-void load_memops() {
-  if (g_wait) return;
-  cudaDriverEntryPointQueryResult q1, q2;
-  void *w = nullptr, *v = nullptr;
-  JANUS_CUDA(cudaGetDriverEntryPoint("cuStreamWaitValue32", &w, cudaEnableDefault, &q1));
-  JANUS_CUDA(cudaGetDriverEntryPoint("cuStreamWriteValue32", &v, cudaEnableDefault, &q2));
-  if (!w || !v || q1 != cudaDriverEntryPointSuccess || q2 != cudaDriverEntryPointSuccess)
-    throw config_error("IPC transport: stream memory operations unavailable");
-  g_wait = reinterpret_cast<WaitFn>(w);
-  g_write = reinterpret_cast<WriteFn>(v);
+// Flag waits and posts are one-thread kernels, not stream memory operations: a
+// cuStreamWaitValue32 holds the head of its hardware work queue, and the
+// streams of a rank share a limited set of queues, so a blocked receive could
+// stall an unrelated lane behind it (and the lane the peer waits for: a
+// deadlock NCCL's kernel-based P2P does not have).  A spinning kernel only
+// occupies one SM slot, like NCCL's own P2P kernels.
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__global__ void flag_wait_kernel(const uint32_t* flag, uint32_t v) {
+  while (ld_acquire_sys(flag) < v) __nanosleep(256);
+}
+__global__ void flag_post_kernel(uint32_t* flag, uint32_t v) {
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(v) : "memory");
 }
 
 void wait_geq(cudaStream_t s, const uint32_t* addr, uint32_t v) {
-  if (g_wait(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr), v, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
-    throw cuda_error("cuStreamWaitValue32 failed");
+  flag_wait_kernel<<<1, 1, 0, s>>>(addr, v);
+  JANUS_LAUNCH_CHECK("flag_wait");
 }
 void write_val(cudaStream_t s, uint32_t* addr, uint32_t v) {
-  if (g_write(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr), v, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
-    throw cuda_error("cuStreamWriteValue32 failed");
+  flag_post_kernel<<<1, 1, 0, s>>>(addr, v);
+  JANUS_LAUNCH_CHECK("flag_post");
 }
 
 // File rendezvous in c->dir: every rank writes its blob, then reads all.
@@ -149,7 +149,6 @@ struct RegionHeader {
 class IpcTransport final : public Transport {
  public:
   IpcTransport(janus_comm* c, const TransportPlan& p) : c_(c), plan_(p) {
-    load_memops();
     nch_ = p.chans.size();
     slot_ = (std::max<size_t>(p.max_payload, 4) + 255) & ~static_cast<size_t>(255);
     ar_ = (std::max<size_t>(p.max_allreduce, 4) + 255) & ~static_cast<size_t>(255);

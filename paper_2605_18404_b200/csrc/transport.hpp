@@ -12,8 +12,9 @@
 //       (the test harness for the per-rank path when only one GPU exists).
 //       Each rank exports a device region (cudaIpcGetMemHandle) holding, per
 //       channel it receives on, a staging buffer and two flags; a send waits
-//       (cuStreamWaitValue32) until the receiver has POSTED the matching
-//       receive, copies into its staging buffer and raises SENT; the receive
+//       (a one-thread spin kernel, like NCCL's P2P kernels: no stream memory
+//       operation holding a hardware queue) until the receiver has POSTED the
+//       matching receive, copies into its staging buffer and raises SENT; the receive
 //       posts, waits for SENT and copies out.  That is NCCL's blocking
 //       rendezvous (no buffering ahead of the receive), so a program that runs
 //       here runs under NCCL and vice versa.  All-reduce: every member stages

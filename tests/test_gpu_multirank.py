@@ -34,7 +34,7 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 import multirank_worker as W  # noqa: E402
 
 
-def run_ranks(cfg, timeout=420):
+def run_ranks(cfg, timeout=int(os.environ.get("MULTIRANK_TIMEOUT", 420))):
     world = cfg["P"] * cfg["dp"]
     with tempfile.TemporaryDirectory() as d:
         cfg = dict(cfg, dir=d)
