@@ -40,6 +40,9 @@ sys.path.insert(0, ROOT)
 # 32 hardware work queues for the 32 compute lanes, before any CUDA context
 # exists (paper_2605_18404_b200/__init__.py sets the same default)
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+# eager kernel loading: the N>1 per-rank path blocks streams on peers, and a
+# lazily loaded kernel can deadlock its first launch against them
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 
 CONFIG = dict(L=4, H=64, R=64, r_c=5.0, atoms=256, rho=0.095, n_mb=32, seed=7)
 # per-layer edge-contraction FLOPs of the directed-edge algorithm, FE + FF + BF + BE

@@ -180,6 +180,11 @@ int janus_comm_init_nccl(const void* id, int nranks, int rank, int device, janus
  * semantics with stream memory operations (csrc/transport.hpp).  The trainer
  * treats it exactly like an NCCL comm. */
 int janus_comm_init_ipc(const char* dir, int nranks, int rank, int device, janus_comm** out);
+/* The same transport for N ranks that are THREADS of one process on one
+ * device (one CUDA context: the ranks' kernels run concurrently; separate
+ * processes on one GPU are time-sliced, csrc/transport.hpp).  The test harness
+ * of the per-rank path: every rank still builds its own per-rank trainer. */
+int janus_comm_init_threads(const char* dir, int nranks, int rank, int device, janus_comm** out);
 int janus_comm_destroy(janus_comm* c);
 int janus_comm_send(janus_comm* c, const void* buf, size_t bytes, int peer, void* stream);
 int janus_comm_recv(janus_comm* c, void* buf, size_t bytes, int peer, void* stream);

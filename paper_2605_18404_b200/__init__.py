@@ -20,6 +20,8 @@ import numpy as np
 # many compute lanes should set CUDA_DEVICE_MAX_CONNECTIONS (one hardware work
 # queue per lane, e.g. 32) before the first CUDA context exists; bench.py and
 # the tests do.  janus_trainer_create warns on stderr when lanes exceed it.
+# The per-rank (one process per GPU) path also needs CUDA_MODULE_LOADING=EAGER
+# and a hardware queue per stream; janus_trainer_create refuses to run without.
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("JANUS_LIB") or os.path.join(_HERE, "libjanus_b200.so")  # JANUS_LIB: profiling builds only
@@ -572,6 +574,7 @@ _sig("janus_trainer_plan", c_int, c_vp, c_vp)
 _sig("janus_nccl_unique_id", c_int, c_vp)
 _sig("janus_comm_init_nccl", c_int, c_vp, c_int, c_int, c_int, c_vp)
 _sig("janus_comm_init_ipc", c_int, ctypes.c_char_p, c_int, c_int, c_int, c_vp)
+_sig("janus_comm_init_threads", c_int, ctypes.c_char_p, c_int, c_int, c_int, c_vp)
 _sig("janus_comm_destroy", c_int, c_vp)
 
 
@@ -589,10 +592,12 @@ class Comm:
     """Per-rank communicator (one per process; rank r holds pipeline device
     r % P of replica r // P): NCCL, or the same-GPU IPC transport (Comm.ipc)."""
 
-    def __init__(self, uid: bytes | None, nranks: int, rank: int, device: int, ipc_dir: str | None = None):
+    def __init__(self, uid: bytes | None, nranks: int, rank: int, device: int, ipc_dir: str | None = None,
+                 threads: bool = False):
         h = c_vp()
         if ipc_dir is not None:
-            check(_lib.janus_comm_init_ipc(ipc_dir.encode(), nranks, rank, device, ctypes.byref(h)))
+            init = _lib.janus_comm_init_threads if threads else _lib.janus_comm_init_ipc
+            check(init(ipc_dir.encode(), nranks, rank, device, ctypes.byref(h)))
         else:
             buf = ctypes.create_string_buffer(uid, 128)
             check(_lib.janus_comm_init_nccl(buf, nranks, rank, device, ctypes.byref(h)))
@@ -603,6 +608,12 @@ class Comm:
         """N processes on ONE GPU with NCCL's blocking-rendezvous semantics
         (CUDA IPC staging + stream memory operations; csrc/transport.hpp)."""
         return cls(None, nranks, rank, device, ipc_dir=rendezvous_dir)
+
+    @classmethod
+    def threads(cls, rendezvous_dir: str, nranks: int, rank: int, device: int = 0) -> "Comm":
+        """N ranks as threads of THIS process on one GPU, same protocol (one CUDA
+        context, so the ranks' kernels run concurrently)."""
+        return cls(None, nranks, rank, device, ipc_dir=rendezvous_dir, threads=True)
 
     @staticmethod
     def unique_id() -> bytes:

@@ -300,7 +300,13 @@ int janus_comm_init_nccl(const void* id, int nranks, int rank, int device, janus
 int janus_comm_init_ipc(const char* dir, int nranks, int rank, int device, janus_comm** out) {
   return guard([&] {
     need(out, "out");
-    *out = janus::comm_init_ipc(dir, nranks, rank, device);
+    *out = janus::comm_init_ipc(dir, nranks, rank, device, false);
+  });
+}
+int janus_comm_init_threads(const char* dir, int nranks, int rank, int device, janus_comm** out) {
+  return guard([&] {
+    need(out, "out");
+    *out = janus::comm_init_ipc(dir, nranks, rank, device, true);
   });
 }
 int janus_comm_destroy(janus_comm* c) {

@@ -25,10 +25,15 @@
 // replicated parameters: FF recomputes FE from the block input (mirror
 // transfer), BF is followed by an injection-only BE whose block-input
 // cotangent is sent back to the energy device, and OS all-reduces the pair.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <mutex>
+#include <thread>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -145,6 +150,21 @@ struct janus_trainer {
   int64_t nsteps = 0;
   janus::LmBuilder* lm = nullptr;                // device neighbour lists (loads without a CSR)
   int lm_par = 0;                                 // CSR buffer of the next device LM build
+  // hang diagnostics (JANUS_HANG_REPORT=<seconds>, debugging aid, off by default):
+  // an event after every issued instruction; trainer_wait reports the first
+  // unfinished instruction per stream instead of blocking forever
+  double hang_s = 0;
+  cudaStream_t last_comm = nullptr;
+  struct Probe {
+    int kind, mb, dev;
+    cudaStream_t s;
+    cudaEvent_t e;
+  };
+  std::vector<Probe> probes;
+  std::mutex probe_mu;
+  std::atomic<int64_t> waited{0};
+  std::atomic<int64_t> issued{0};
+  std::string last_issued;
 };
 
 namespace janus {
@@ -241,12 +261,14 @@ void chan_send(janus_trainer* t, VDev& dv, int flow, int mb, const float* sp, si
   JANUS_CUDA(cudaStreamWaitEvent(cs, ready, 0));
   t->p2p_bytes += static_cast<int64_t>(sb);
   t->xport->send(c, sp, sb, peer_rank(t, peer_dev), cs);
+  t->last_comm = cs;
 }
 // ... and lands on its channel's stream; the lane waits for it
 void chan_recv(janus_trainer* t, VDev& dv, int flow, int mb, float* dp, size_t db, int peer_dev) {
   const int c = channel_index(t->chans, {flow, peer_dev, dv.id});
   cudaStream_t cs = t->chan_stream[static_cast<size_t>(c)];
   t->xport->recv(c, dp, db, peer_rank(t, peer_dev), cs);
+  t->last_comm = cs;
   cudaEvent_t done = next_event(t);
   JANUS_CUDA(cudaEventRecord(done, cs));
   JANUS_CUDA(cudaStreamWaitEvent(lane_stream(t, dv, mb), done, 0));
@@ -477,8 +499,81 @@ void issue_step(janus_trainer* t, const janus_opt& opt) {
   if (t->local) {
     for (int idx : t->order) execute(t, *t->graph.flat[static_cast<size_t>(idx)], opt);
   } else {
-    for (const Instruction& in : t->sched.device_lists[static_cast<size_t>(t->my_dev)]) execute(t, in, opt);
+    for (const Instruction& in : t->sched.device_lists[static_cast<size_t>(t->my_dev)]) {
+      t->last_comm = nullptr;
+      if (t->hang_s > 0) {
+        std::lock_guard<std::mutex> g(t->probe_mu);
+        t->last_issued = std::string(to_string(in.kind)) + " mb " + std::to_string(in.micro_batch) + " (list index " +
+                         std::to_string(t->issued.load()) + ")";
+      }
+      execute(t, in, opt);
+      ++t->issued;
+      if (t->hang_s > 0) {
+        cudaStream_t s = t->last_comm ? t->last_comm : lane_stream(t, t->devs[0], in.micro_batch);
+        cudaEvent_t e;
+        JANUS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        JANUS_CUDA(cudaEventRecord(e, s));
+        std::lock_guard<std::mutex> g(t->probe_mu);
+        t->probes.push_back({static_cast<int>(in.kind), in.micro_batch, in.device, s, e});
+      }
+    }
   }
+}
+
+// JANUS_HANG_REPORT: the first issued instruction per stream that has not finished
+std::string hang_report(janus_trainer* t) {
+  std::lock_guard<std::mutex> g(t->probe_mu);
+  std::string rep = "rank " + std::to_string(t->rank) + ": step did not finish (" + std::to_string(t->probes.size()) +
+                    " instructions issued); first unfinished instruction per stream:\n";
+  std::map<cudaStream_t, bool> seen;
+  for (size_t x = 0; x < t->probes.size(); ++x) {
+    const auto& p = t->probes[x];
+    if (seen[p.s] || cudaEventQuery(p.e) == cudaSuccess) continue;
+    seen[p.s] = true;
+    std::string sname = "?";
+    for (size_t l = 0; l < t->devs[0].lane.size(); ++l)
+      if (t->devs[0].lane[l] == p.s) sname = "lane" + std::to_string(l);
+    for (size_t c = 0; c < t->chan_stream.size(); ++c)
+      if (t->chan_stream[c] == p.s) sname = "chan" + std::to_string(c);
+    rep += "  #" + std::to_string(x) + " " + std::string(to_string(static_cast<InstrKind>(p.kind))) + " mb " +
+           std::to_string(p.mb) + " dev " + std::to_string(p.dev) + " on " + sname + "\n";
+  }
+  return rep;
+}
+
+// A watchdog per step (the host itself may block inside the issue loop once
+// the device stops draining its queues): after hang_s seconds without the
+// step being waited for, print the report and end the process.
+void hang_watchdog(janus_trainer* t, int64_t step) {
+  std::thread([t, step] {
+    std::this_thread::sleep_for(std::chrono::duration<double>(t->hang_s));
+    if (t->waited.load() > step) return;
+    {  // host-side facts first: CUDA calls below may block behind a stuck launch
+      const int64_t n = t->issued.load();
+      std::fprintf(stderr, "rank %d: step %lld not done after %.0f s; %lld instructions issued, last: %s\n", t->rank,
+                   static_cast<long long>(step), t->hang_s, static_cast<long long>(n), t->last_issued.c_str());
+      std::fflush(stderr);
+    }
+    if (t->xport) {
+      const std::string x = t->xport->debug_state();  // host-only in same-process mode
+      std::fprintf(stderr, "rank %d transport:\n%s", t->rank, x.c_str());
+      std::fflush(stderr);
+    }
+    const std::string rep = hang_report(t);
+    std::fprintf(stderr, "%s", rep.c_str());
+    std::fflush(stderr);
+    std::this_thread::sleep_for(std::chrono::seconds(3));  // let the other ranks of this process report too
+    std::_Exit(3);
+  }).detach();
+}
+
+void hang_wait(janus_trainer* t, cudaEvent_t ev) {
+  JANUS_CUDA(cudaEventSynchronize(ev));
+  if (t->hang_s <= 0) return;
+  ++t->waited;
+  std::lock_guard<std::mutex> g(t->probe_mu);
+  for (auto& p : t->probes) cudaEventDestroy(p.e);
+  t->probes.clear();
 }
 
 void fork_join_begin(janus_trainer* t) {
@@ -524,6 +619,35 @@ void finalize_local(janus_trainer* t, const janus_opt& opt) {
   }
 }
 
+// The per-rank path blocks streams on peers (NCCL P2P kernels, or the IPC
+// transport's waits), which is only safe when (a) every kernel is loaded
+// before the first step — lazy module loading (CUDA 12 default) loads a
+// kernel at its first launch and can wait for a running peer-blocked kernel:
+// the first step then deadlocks — and (b) each stream of this rank owns a
+// hardware work queue: a stream waiting on a peer at the head of a shared
+// queue stalls the unrelated streams behind it, which may be what the peer
+// waits for.  Both are process-wide settings read at context creation, so
+// the application sets them; the trainer refuses to run without them.
+void check_per_rank_runtime(const janus_trainer* t, int n_streams) {
+  using GetMode = CUresult (*)(CUmoduleLoadingMode*);
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuModuleGetLoadingMode", &fn, cudaEnableDefault, &q) == cudaSuccess && fn &&
+      q == cudaDriverEntryPointSuccess) {
+    CUmoduleLoadingMode mode;
+    if (reinterpret_cast<GetMode>(fn)(&mode) == CUDA_SUCCESS && mode == CU_MODULE_LAZY_LOADING)
+      throw config_error("per-rank mode needs eager kernel loading: set CUDA_MODULE_LOADING=EAGER before the first "
+                         "CUDA call of the process (lazy loading can deadlock the first step against a blocked peer)");
+  }
+  const char* e = std::getenv("CUDA_DEVICE_MAX_CONNECTIONS");
+  const int conn = e ? std::atoi(e) : 8;
+  if (conn < n_streams)
+    throw config_error("per-rank mode: rank " + std::to_string(t->rank) + " uses " + std::to_string(n_streams) +
+                       " streams but CUDA_DEVICE_MAX_CONNECTIONS=" + std::to_string(conn) +
+                       " hardware queues; set it to >= " + std::to_string(n_streams) +
+                       " (max 32) before the first CUDA call, or use fewer lanes");
+}
+
 }  // namespace
 
 // ================================================================ create
@@ -532,6 +656,7 @@ janus_trainer* trainer_create(const janus_exec_desc& ed, const janus_stage_desc&
   auto t = std::make_unique<janus_trainer>();
   t->ed = ed;
   t->sd = sd;
+  if (const char* h = std::getenv("JANUS_HANG_REPORT")) t->hang_s = std::atof(h);
   t->P = ed.n_stages;
   t->method = ed.method;
   t->local = ed.local_stages != 0;
@@ -679,6 +804,9 @@ janus_trainer* trainer_create(const janus_exec_desc& ed, const janus_stage_desc&
     t->chan_stream.assign(t->chans.size(), nullptr);
     for (size_t c = 0; c < t->chans.size(); ++c)
       if (t->chans[c].from == d || t->chans[c].to == d) JANUS_CUDA(cudaStreamCreateWithFlags(&t->chan_stream[c], cudaStreamNonBlocking));
+    int n_streams = static_cast<int>(t->devs[0].lane.size()) + 4;  // lanes, send, recv, root, load
+    for (cudaStream_t cs : t->chan_stream) n_streams += cs ? 1 : 0;
+    check_per_rank_runtime(t.get(), n_streams);
     t->xport = make_transport(comm, tp);
   }
   // local issue order: a topological order of the full DAG (seq + data edges),
@@ -955,6 +1083,10 @@ void trainer_step_async(janus_trainer* t, const janus_opt& opt) {
   }
   t->recs.clear();
   t->recording = t->ed.record_timeline != 0;
+  if (t->hang_s > 0) {
+    t->issued = 0;
+    hang_watchdog(t, t->nsteps);
+  }
   const int q = static_cast<int>(t->nsteps & 1);
   // this step's optimizer hyperparameters: captured graphs read them from the
   // device buffer (pageable source: staged by the driver before the call returns)
@@ -991,7 +1123,7 @@ void trainer_wait(janus_trainer* t, janus_step_stats* stats) {
   if (t->inflight <= 0) throw state_error("no step in flight");
   const int q = static_cast<int>((t->nsteps - t->inflight) & 1);  // the oldest step in flight
   --t->inflight;
-  JANUS_CUDA(cudaEventSynchronize(t->done_q[q]));
+  hang_wait(t, t->done_q[q]);
   if (t->inflight == 0) t->recording = false;
   float ms = 0.f;
   JANUS_CUDA(cudaEventElapsedTime(&ms, t->anchor_q[q], t->finish_q[q]));
@@ -1103,12 +1235,12 @@ janus_comm* comm_init_nccl(const void* id, int nranks, int rank, int device) {
   return c.release();
 }
 
-janus_comm* comm_init_ipc(const char* dir, int nranks, int rank, int device) {
+janus_comm* comm_init_ipc(const char* dir, int nranks, int rank, int device, bool same_process) {
   if (!dir || !*dir) throw domain_error("IPC comm needs a rendezvous directory");
   if (nranks < 1 || rank < 0 || rank >= nranks) throw domain_error("bad rank / nranks");
   JANUS_CUDA(cudaSetDevice(device));
   auto c = std::make_unique<janus_comm>();
-  c->kind = 1;
+  c->kind = same_process ? 2 : 1;
   c->nranks = nranks;
   c->rank = rank;
   c->device = device;

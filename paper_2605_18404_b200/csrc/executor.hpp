@@ -24,7 +24,7 @@ void trainer_plan(janus_trainer* t, int32_t* out);
 
 void nccl_unique_id(void* out);
 janus_comm* comm_init_nccl(const void* id, int nranks, int rank, int device);
-janus_comm* comm_init_ipc(const char* dir, int nranks, int rank, int device);
+janus_comm* comm_init_ipc(const char* dir, int nranks, int rank, int device, bool same_process);
 void comm_destroy(janus_comm* c);
 void comm_send(janus_comm* c, const void* buf, size_t bytes, int peer, cudaStream_t s);
 void comm_recv(janus_comm* c, void* buf, size_t bytes, int peer, cudaStream_t s);

@@ -1,5 +1,6 @@
 // transport.cu — NCCL and same-GPU IPC transports of the executor (see
 // transport.hpp for the channel and rendezvous semantics).
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 #include <unistd.h>
@@ -7,6 +8,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <iterator>
@@ -96,13 +98,50 @@ __global__ void flag_post_kernel(uint32_t* flag, uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(v) : "memory");
 }
 
+// Waits are stream memory operations (the GPU front end polls the flag; no SM
+// is held).  Each of a rank's streams must own a hardware queue
+// (CUDA_DEVICE_MAX_CONNECTIONS >= streams, checked by the trainer), or a
+// blocked wait stalls the streams queued behind it; the spin kernels above
+// (NCCL's mechanism) have the same requirement and hold an SM slot, so they
+// are kept only as the fallback when stream memory operations are unavailable.
+using WaitFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using WriteFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WaitFn g_wait = nullptr;
+WriteFn g_write = nullptr;
+bool g_kernel_waits = false;
+
+void load_memops() {
+  if (g_wait) return;
+  static_assert(sizeof(void*) == 8);
+  cudaDriverEntryPointQueryResult q1, q2;
+  void *w = nullptr, *v = nullptr;
+  if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &w, cudaEnableDefault, &q1) != cudaSuccess ||
+      cudaGetDriverEntryPoint("cuStreamWriteValue32", &v, cudaEnableDefault, &q2) != cudaSuccess || !w || !v ||
+      q1 != cudaDriverEntryPointSuccess || q2 != cudaDriverEntryPointSuccess) {
+    g_kernel_waits = true;  // (the entry point pointers stay set so this runs once)
+    w = v = reinterpret_cast<void*>(1);
+  }
+  g_wait = reinterpret_cast<WaitFn>(w);
+  g_write = reinterpret_cast<WriteFn>(v);
+}
+
 void wait_geq(cudaStream_t s, const uint32_t* addr, uint32_t v) {
-  flag_wait_kernel<<<1, 1, 0, s>>>(addr, v);
-  JANUS_LAUNCH_CHECK("flag_wait");
+  if (g_kernel_waits) {
+    flag_wait_kernel<<<1, 1, 0, s>>>(addr, v);
+    JANUS_LAUNCH_CHECK("flag_wait");
+    return;
+  }
+  if (g_wait(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr), v, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+    throw cuda_error("cuStreamWaitValue32 failed");
 }
 void write_val(cudaStream_t s, uint32_t* addr, uint32_t v) {
-  flag_post_kernel<<<1, 1, 0, s>>>(addr, v);
-  JANUS_LAUNCH_CHECK("flag_post");
+  if (g_kernel_waits) {
+    flag_post_kernel<<<1, 1, 0, s>>>(addr, v);
+    JANUS_LAUNCH_CHECK("flag_post");
+    return;
+  }
+  if (g_write(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(addr), v, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+    throw cuda_error("cuStreamWriteValue32 failed");
 }
 
 // File rendezvous in c->dir: every rank writes its blob, then reads all.
@@ -144,11 +183,14 @@ __global__ void sum_members_kernel(size_t n, float* __restrict__ out, const floa
 struct RegionHeader {
   cudaIpcMemHandle_t handle;
   uint64_t bytes;
+  uint64_t ptr;        // same-process ranks (threads): the region's address itself
+  uint64_t hflags;     // same-process ranks: the flags' mapped host block (host address)
 };
 
 class IpcTransport final : public Transport {
  public:
   IpcTransport(janus_comm* c, const TransportPlan& p) : c_(c), plan_(p) {
+    load_memops();
     nch_ = p.chans.size();
     slot_ = (std::max<size_t>(p.max_payload, 4) + 255) & ~static_cast<size_t>(255);
     ar_ = (std::max<size_t>(p.max_allreduce, 4) + 255) & ~static_cast<size_t>(255);
@@ -157,16 +199,37 @@ class IpcTransport final : public Transport {
     flags_bytes_ = ((2 * nch_ + 4) * sizeof(uint32_t) + 4095) & ~static_cast<size_t>(4095);
     const size_t bytes = flags_bytes_ + nch_ * slot_ + 2 * ar_ + 2 * 64 * sizeof(float*);
     JANUS_CUDA(cudaMalloc(&mine_, bytes));
-    JANUS_CUDA(cudaMemset(mine_, 0, bytes));
-    JANUS_CUDA(cudaDeviceSynchronize());
+    {  // (no device-wide synchronisation: ranks sharing this context may already be running)
+      cudaStream_t z;
+      JANUS_CUDA(cudaStreamCreateWithFlags(&z, cudaStreamNonBlocking));
+      JANUS_CUDA(cudaMemsetAsync(mine_, 0, bytes, z));
+      JANUS_CUDA(cudaStreamSynchronize(z));
+      JANUS_CUDA(cudaStreamDestroy(z));
+    }
     RegionHeader h{};
-    JANUS_CUDA(cudaIpcGetMemHandle(&h.handle, mine_));
+    if (!same_process()) JANUS_CUDA(cudaIpcGetMemHandle(&h.handle, mine_));
     h.bytes = bytes;
+    h.ptr = reinterpret_cast<uint64_t>(mine_);
+    if (same_process()) {  // flags in mapped pinned host memory: readable by the hang report without CUDA calls
+      JANUS_CUDA(cudaHostAlloc(&hflags_mine_, flags_bytes_, cudaHostAllocMapped | cudaHostAllocPortable));
+      std::memset(hflags_mine_, 0, flags_bytes_);
+      h.hflags = reinterpret_cast<uint64_t>(hflags_mine_);
+    }
     const std::string tag = "t" + std::to_string(c->generation++);
     tag_ = tag;
     const auto all = exchange(c, tag, std::string(reinterpret_cast<const char*>(&h), sizeof(h)));
     base_.assign(static_cast<size_t>(c->nranks), nullptr);
+    hflags_.assign(static_cast<size_t>(c->nranks), nullptr);
+    dflags_.assign(static_cast<size_t>(c->nranks), nullptr);
     for (int r = 0; r < c->nranks; ++r) {
+      if (same_process()) {
+        RegionHeader o{};
+        std::memcpy(&o, all[static_cast<size_t>(r)].data(), sizeof(o));
+        hflags_[static_cast<size_t>(r)] = reinterpret_cast<uint32_t*>(o.hflags);
+        void* dp = nullptr;
+        JANUS_CUDA(cudaHostGetDevicePointer(&dp, hflags_[static_cast<size_t>(r)], 0));
+        dflags_[static_cast<size_t>(r)] = static_cast<uint32_t*>(dp);
+      }
       if (r == c->rank) {
         base_[static_cast<size_t>(r)] = static_cast<uint8_t*>(mine_);
         continue;
@@ -175,8 +238,8 @@ class IpcTransport final : public Transport {
       if (all[static_cast<size_t>(r)].size() != sizeof(o)) throw state_error("IPC rendezvous: bad region record");
       std::memcpy(&o, all[static_cast<size_t>(r)].data(), sizeof(o));
       if (o.bytes != bytes) throw state_error("IPC transport: ranks disagree on the region layout");
-      void* p2 = nullptr;
-      JANUS_CUDA(cudaIpcOpenMemHandle(&p2, o.handle, cudaIpcMemLazyEnablePeerAccess));
+      void* p2 = reinterpret_cast<void*>(o.ptr);
+      if (!same_process()) JANUS_CUDA(cudaIpcOpenMemHandle(&p2, o.handle, cudaIpcMemLazyEnablePeerAccess));
       base_[static_cast<size_t>(r)] = static_cast<uint8_t*>(p2);
     }
     send_seq_.assign(nch_, 0);
@@ -199,12 +262,14 @@ class IpcTransport final : public Transport {
     } catch (...) {
     }
     for (int r = 0; r < c_->nranks; ++r)
-      if (r != c_->rank && base_[static_cast<size_t>(r)]) cudaIpcCloseMemHandle(base_[static_cast<size_t>(r)]);
+      if (r != c_->rank && base_[static_cast<size_t>(r)] && !same_process()) cudaIpcCloseMemHandle(base_[static_cast<size_t>(r)]);
     cudaFree(mine_);
+    if (hflags_mine_) cudaFreeHost(hflags_mine_);
   }
   void send(int c, const void* buf, size_t bytes, int peer, cudaStream_t s) override {
     check_payload(bytes);
     const uint32_t k = ++send_seq_.at(static_cast<size_t>(c));
+    log_ += " S" + std::to_string(c) + "#" + std::to_string(k);
     wait_geq(s, flag(peer, 2 * c), k);  // the receiver posted receive k
     JANUS_CUDA(cudaMemcpyAsync(staging(peer, c), buf, bytes, cudaMemcpyDeviceToDevice, s));
     write_val(s, flag(peer, 2 * c + 1), k);  // sent k (fenced after the copy)
@@ -212,9 +277,27 @@ class IpcTransport final : public Transport {
   void recv(int c, void* buf, size_t bytes, int, cudaStream_t s) override {
     check_payload(bytes);
     const uint32_t k = ++recv_seq_.at(static_cast<size_t>(c));
+    log_ += " R" + std::to_string(c) + "#" + std::to_string(k);
     write_val(s, flag(c_->rank, 2 * c), k);
     wait_geq(s, flag(c_->rank, 2 * c + 1), k);
     JANUS_CUDA(cudaMemcpyAsync(buf, staging(c_->rank, c), bytes, cudaMemcpyDeviceToDevice, s));
+  }
+  std::string debug_state() override {
+    std::string out;
+    if (same_process()) {
+      for (int r = 0; r < c_->nranks; ++r) {
+        const volatile uint32_t* f = hflags_[static_cast<size_t>(r)];
+        out += "  rank " + std::to_string(r) + " flags [posted,sent] per channel:";
+        for (size_t c = 0; c < nch_; ++c) out += " " + std::to_string(f[2 * c]) + "," + std::to_string(f[2 * c + 1]);
+        out += "\n";
+      }
+    }
+    out += "  my send seq:";
+    for (size_t c = 0; c < nch_; ++c) out += " " + std::to_string(send_seq_[c]);
+    out += "\n  my recv seq:";
+    for (size_t c = 0; c < nch_; ++c) out += " " + std::to_string(recv_seq_[c]);
+    out += "\n  issued:" + log_ + "\n";
+    return out;
   }
   void allreduce(int group, float* buf, size_t n, cudaStream_t s) override {
     const std::vector<int>& mem = group == 0 ? plan_.pair_members : plan_.dp_members;
@@ -232,10 +315,14 @@ class IpcTransport final : public Transport {
   }
 
  private:
+  bool same_process() const { return c_->kind == 2; }
   void check_payload(size_t bytes) const {
     if (bytes > slot_) throw config_error("IPC payload larger than the channel staging buffer");
   }
-  uint32_t* flag(int rank, int i) const { return reinterpret_cast<uint32_t*>(base_[static_cast<size_t>(rank)]) + i; }
+  uint32_t* flag(int rank, int i) const {
+    if (same_process()) return dflags_[static_cast<size_t>(rank)] + i;
+    return reinterpret_cast<uint32_t*>(base_[static_cast<size_t>(rank)]) + i;
+  }
   uint8_t* staging(int rank, int c) const { return base_[static_cast<size_t>(rank)] + flags_bytes_ + static_cast<size_t>(c) * slot_; }
   uint8_t* ar_buf(int rank, int g) const { return base_[static_cast<size_t>(rank)] + flags_bytes_ + nch_ * slot_ + static_cast<size_t>(g) * ar_; }
 
@@ -245,6 +332,9 @@ class IpcTransport final : public Transport {
   size_t nch_ = 0, slot_ = 0, ar_ = 0, flags_bytes_ = 0;
   void* mine_ = nullptr;
   std::vector<uint8_t*> base_;
+  void* hflags_mine_ = nullptr;
+  std::vector<uint32_t*> hflags_, dflags_;  // same-process ranks: flags (host view, device view)
+  std::string log_;                         // host log of issued transfers (hang report)
   std::vector<uint32_t> send_seq_, recv_seq_;
   uint32_t ar_gen_[2] = {0, 0};
   const float** srcs_[2] = {nullptr, nullptr};
@@ -253,7 +343,7 @@ class IpcTransport final : public Transport {
 }  // namespace
 
 std::unique_ptr<Transport> make_transport(janus_comm* c, const TransportPlan& plan) {
-  if (c->kind == 1) return std::make_unique<IpcTransport>(c, plan);
+  if (c->kind == 1 || c->kind == 2) return std::make_unique<IpcTransport>(c, plan);
   return std::make_unique<NcclTransport>(c, plan);
 }
 

@@ -21,6 +21,12 @@
 //       its buffer, raises READY, waits for all members' READY, sums the
 //       members' buffers in rank order (identical bits on every rank) and
 //       raises DONE; a member re-stages only after all members' DONE.
+//       kind 2 runs the same protocol for ranks that are threads of ONE
+//       process (the regions are exchanged as plain device addresses): the
+//       ranks share a CUDA context, so their kernels run concurrently, which
+//       separate processes on one GPU without MPS cannot (time-sliced
+//       contexts: a rank blocked on its peer can stall the GPU, which is why
+//       NCCL refuses two ranks on one device).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -33,7 +39,7 @@
 #include "../../include/janus/rendezvous.hpp"
 
 struct janus_comm {
-  int kind = 0;  // 0 NCCL, 1 IPC (same-GPU multi-process)
+  int kind = 0;  // 0 NCCL, 1 IPC (same-GPU multi-process), 2 same-GPU ranks as threads of one process
   int nranks = 1, rank = 0, device = 0;
   ncclComm_t base = nullptr;  // NCCL
   std::string dir;            // IPC: rendezvous directory (one file per rank and exchange)
@@ -50,6 +56,8 @@ class Transport {
   virtual void recv(int c, void* buf, size_t bytes, int peer, cudaStream_t s) = 0;
   /// Sum over the group's members (0: 1F1B-2nd energy / force pair, 1: data-parallel replicas).
   virtual void allreduce(int group, float* buf, size_t n, cudaStream_t s) = 0;
+  /// Hang diagnostics (JANUS_HANG_REPORT): a readable dump of the transport's state.
+  virtual std::string debug_state() { return ""; }
 };
 
 /// Channel layout of one trainer: chans = schedule_channels(); members of the

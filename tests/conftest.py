@@ -6,6 +6,9 @@ import pytest
 # the application's choice (the library leaves the environment alone): one
 # hardware work queue per compute lane, before any CUDA context exists
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+# and eager kernel loading, which the per-rank (peer-blocking) path requires
+# (executor.cpp check_per_rank_runtime)
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 for p in (ROOT, os.path.join(ROOT, "oracle"), os.path.join(ROOT, "tests", "golden")):

@@ -23,27 +23,27 @@ def batches_for(J, m, cfg, replica):
             for i in range(n)]
 
 
-def main():
-    cfg = json.loads(sys.argv[1])
-    rank = int(sys.argv[2])
-    out = sys.argv[3]
-    import paper_2605_18404_b200 as J
-
+def run_rank(J, cfg, rank, comm, barrier=None):
+    """One rank's whole job on an existing communicator: its own per-rank
+    trainer (local=False), cfg["steps"] steps, then its blocks' parameters and
+    reduced gradients."""
     P, D = cfg["P"], cfg["dp"]
-    world = P * D
     m = J.Model(L=cfg["L"], H=64, R=64, precision=J.PREC_TF32 if cfg["prec"] == "tf32" else J.PREC_FP32)
     params = m.synth_params(cfg["seed"])
-    comm = J.Comm.ipc(cfg["dir"], world, rank, 0)
     tr = J.Trainer(m, params, P, cfg["method"], cfg["n_mb"], k=cfg.get("k", 1), max_atoms=cfg["max_atoms"],
                    max_edges=cfg["max_atoms"] * 120, max_struct=2, local=False, comm=comm, rank=rank, device=0,
                    dp=D, lanes=cfg["lanes"])
+    print(f"rank {rank}: trainer created", flush=True)
     bs = batches_for(J, m, cfg, rank // P)
     res = {}
     losses = []
     for step in range(cfg["steps"]):
         tr.load_many(bs)
+        if barrier:  # thread ranks share one CUDA context: no rank may spin on a peer while another
+            barrier()  # is still inside an allocating (possibly device-synchronising) call
         s = tr.step(lr=1e-3)
         losses.append(s.loss)
+        print(f"rank {rank}: step {step} done", flush=True)
         res["p2p_bytes"] = s.p2p_bytes
     for b in range(P):
         for fr in (False, True):
@@ -56,6 +56,21 @@ def main():
             res[f"grads_{tag}"] = st.grad_buffer()
     res["loss"] = np.array(losses)
     tr.close()
+    return res
+
+
+def main():
+    import faulthandler
+
+    if int(os.environ.get("WORKER_DUMP", 0)) > 0:  # the harness's timeout: show where this rank is stuck
+        faulthandler.dump_traceback_later(int(os.environ["WORKER_DUMP"]), exit=False)
+    cfg = json.loads(sys.argv[1])
+    rank = int(sys.argv[2])
+    out = sys.argv[3]
+    import paper_2605_18404_b200 as J
+
+    comm = J.Comm.ipc(cfg["dir"], cfg["P"] * cfg["dp"], rank, 0)
+    res = run_rank(J, cfg, rank, comm)
     comm.close()
     np.savez(out, **res)
 

@@ -16,7 +16,15 @@ the code an 8-GPU job runs over NCCL.  Checks:
   stage replicas all-reduce before OS; parameters match the local-mode run of
   all micro-batches within fp32 re-association error (the replica sums are
   added in a different order than the micro-batch-ordered ledger);
-* bench.py --gpus 2 under torchrun on the IPC transport prints its line.
+* bench.py --gpus 2 under torchrun on the IPC transport prints its line;
+* the same per-rank path with the ranks as threads of one process
+  (Comm.threads), and the trainer's refusal to run peer-blocking streams on
+  shared hardware queues.
+
+Two process-wide CUDA settings are required for any peer-blocking path
+(NCCL's too) and are set by conftest.py: CUDA_MODULE_LOADING=EAGER (a
+lazily loaded kernel's first launch can wait behind a kernel blocked on a
+peer) and CUDA_DEVICE_MAX_CONNECTIONS >= the rank's streams.
 """
 import json
 import os
@@ -34,27 +42,80 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 import multirank_worker as W  # noqa: E402
 
 
+def run_ranks_threads(cfg, timeout=int(os.environ.get("MULTIRANK_TIMEOUT", 420))):
+    """All ranks as THREADS of this process on the one GPU (Comm.threads): each
+    builds its own per-rank trainer; ctypes releases the GIL, so the ranks
+    issue concurrently.  A rank that hangs ends the process after `timeout`
+    seconds with the executor's hang report (JANUS_HANG_REPORT)."""
+    import threading
+
+    import paper_2605_18404_b200 as J
+    world = cfg["P"] * cfg["dp"]
+    os.environ["JANUS_HANG_REPORT"] = str(timeout)
+    try:
+        with tempfile.TemporaryDirectory() as d:
+            cfg = dict(cfg, dir=d)
+            res, errs = [None] * world, [None] * world
+            bar = threading.Barrier(world)
+
+            def one(r):
+                try:
+                    comm = J.Comm.threads(d, world, r, 0)
+                    try:
+                        res[r] = W.run_rank(J, cfg, r, comm, barrier=lambda: bar.wait(timeout))
+                    finally:
+                        comm.close()
+                except Exception as ex:  # noqa: BLE001
+                    errs[r] = ex
+
+            ts = [threading.Thread(target=one, args=(r,)) for r in range(world)]
+            for t in ts:
+                t.start()
+            for t in ts:
+                t.join()
+            for r in range(world):
+                assert errs[r] is None, f"rank {r}: {errs[r]!r}"
+            return res
+    finally:
+        os.environ.pop("JANUS_HANG_REPORT", None)
+
+
 def run_ranks(cfg, timeout=int(os.environ.get("MULTIRANK_TIMEOUT", 420))):
+    """All ranks as separate PROCESSES on the one GPU (Comm.ipc, CUDA-IPC
+    regions; the contexts are time-sliced).  The env of conftest.py (eager
+    kernel loading, a hardware queue per stream) is inherited."""
     world = cfg["P"] * cfg["dp"]
     with tempfile.TemporaryDirectory() as d:
         cfg = dict(cfg, dir=d)
-        procs, outs = [], []
+        procs, outs, logs = [], [], []
+        env = dict(os.environ, WORKER_DUMP=str(max(10, timeout - 15)),  # python stacks before the kill
+                   JANUS_HANG_REPORT=str(max(5, timeout - 25)))  # and the unfinished instructions
         for r in range(world):
             out = os.path.join(d, f"out{r}.npz")
             outs.append(out)
+            logs.append(open(os.path.join(d, f"log{r}.txt"), "w+"))
             procs.append(subprocess.Popen([sys.executable, os.path.join(ROOT, "tests", "multirank_worker.py"),
-                                           json.dumps(cfg), str(r), out], cwd=ROOT, stdout=subprocess.PIPE,
-                                          stderr=subprocess.STDOUT, text=True, start_new_session=True))
-        logs = []
+                                           json.dumps(cfg), str(r), out], cwd=ROOT, stdout=logs[-1],
+                                          stderr=subprocess.STDOUT, text=True, start_new_session=True, env=env))
+        timed_out = False
         try:
             for p in procs:
-                logs.append(p.communicate(timeout=timeout)[0])
+                p.wait(timeout=timeout)
+        except subprocess.TimeoutExpired:
+            timed_out = True
         finally:
             for p in procs:
                 if p.poll() is None:
                     os.killpg(p.pid, 9)
+                    p.wait()
+        texts = []
+        for f in logs:
+            f.seek(0)
+            texts.append(f.read())
+            f.close()
         for r, p in enumerate(procs):
-            assert p.returncode == 0, f"rank {r} failed:\n{logs[r][-3000:]}"
+            assert p.returncode == 0, f"rank {r} failed{' (timeout)' if timed_out else ''}:\n" + \
+                "\n".join(f"--- rank {q}\n{t[-2500:]}" for q, t in enumerate(texts))
         return [dict(np.load(o)) for o in outs]
 
 
@@ -124,6 +185,27 @@ def test_pp_dp_2x2(janus, gpu, method):
         assert np.array_equal(ranks[b][f"params_E{b}"], ranks[2 + b][f"params_E{b}"])
     loss = np.sum([r["loss"] for r in ranks], axis=0)
     np.testing.assert_allclose(loss, ref_loss, rtol=1e-5)
+
+
+@pytest.mark.parametrize("P,method,k", [(2, 0, 1), (4, 1, 4)])
+def test_thread_ranks_bit_identical_to_local(janus, gpu, P, method, k):
+    """The same per-rank path with the ranks as threads of one process
+    (Comm.threads: one CUDA context, the ranks' kernels run concurrently)."""
+    cfg = dict(BASE, P=P, method=method, k=k)
+    ranks = run_ranks_threads(cfg)
+    ref, ref_loss = run_local(janus, cfg)
+    for b in range(P):
+        assert np.array_equal(gather(ranks, f"params_E{b}"), ref[f"params_E{b}"]), f"block {b} params"
+        assert np.array_equal(gather(ranks, f"grads_E{b}"), ref[f"grads_E{b}"]), f"block {b} grads"
+    np.testing.assert_allclose(np.sum([r["loss"] for r in ranks], axis=0), ref_loss, rtol=1e-6)
+
+
+def test_per_rank_runtime_checks(janus, gpu):
+    """Per-rank mode refuses a process whose streams would share hardware
+    queues (a peer-blocked stream could stall the stream its peer waits for)."""
+    cfg = dict(BASE, P=2, method=0, k=1, lanes=40)
+    with pytest.raises(AssertionError, match="CUDA_DEVICE_MAX_CONNECTIONS"):
+        run_ranks_threads(cfg, timeout=60)
 
 
 def free_port():
