@@ -12,6 +12,13 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 # system 2.27 would make a later `import torch` bind its libnccl.so.2 SONAME to
 # 2.27 and fail (ncclDevCommCreate), which breaks torchrun launches.
 NCCL_HOME ?= $(shell python -c "import nvidia.nccl as n; print(n.__path__[0])" 2>/dev/null)
+# cuBLAS (generic-width path GEMMs): the torch-bundled copy too, for the same SONAME reason
+CUBLAS_HOME ?= $(shell python -c "import nvidia.cublas as n; print(n.__path__[0])" 2>/dev/null)
+ifneq ($(CUBLAS_HOME),)
+CUBLAS_LINK := -L$(CUBLAS_HOME)/lib -l:libcublas.so.12 -Xlinker -rpath -Xlinker $(CUBLAS_HOME)/lib
+else
+CUBLAS_LINK := -lcublas
+endif
 ifneq ($(NCCL_HOME),)
 NCCL_INC := -I$(NCCL_HOME)/include
 NCCL_LINK := -L$(NCCL_HOME)/lib -l:libnccl.so.2 -Xlinker -rpath -Xlinker $(NCCL_HOME)/lib
@@ -62,7 +69,7 @@ $(OBJ)/%.cpp.o: $(SRC)/%.cpp $(HDRS) | $(OBJ)
 
 $(LIB): $(OBJS)
 	mkdir -p $(dir $@)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) $(NCCL_LINK) -lcudart
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) $(NCCL_LINK) $(CUBLAS_LINK) -lcudart
 
 oracle:
 	$(MAKE) -s -C oracle

@@ -32,6 +32,7 @@
 #include <vector>
 
 #include "janus/ir.hpp"
+#include "janus/slots.hpp"
 
 namespace janus {
 
@@ -120,7 +121,7 @@ enum class StreamLayout {
 /// mirror transfers at FE / FF / BF / BE; OS joins the lanes on lane 0 and
 /// runs the group all-reduces: group 0 = 1F1B pair, 1 = data-parallel).
 inline std::vector<RankProgram> build_programs(const Schedule& s, int P, bool onef1b, int lanes, int dp,
-                                               StreamLayout layout) {
+                                               StreamLayout layout, bool pooled_slots = true) {
   const std::vector<ChannelKey> chans = schedule_channels(s, P, onef1b);
   const int nch = static_cast<int>(chans.size());
   std::vector<RankProgram> progs;
@@ -147,7 +148,17 @@ inline std::vector<RankProgram> build_programs(const Schedule& s, int P, bool on
         push(lane(mb), StreamOp{StreamOp::kWork, -1, mb, {tail(recv_stream(ch))}, "wait " + what});
       };
       auto work = [&](int mb, const std::string& what) { push(lane(mb), StreamOp{StreamOp::kWork, -1, mb, {}, what}); };
-      for (const Instruction& in : s.device_lists[static_cast<size_t>(d)]) {
+      // ops each instruction pushed (for the activation slot pool's waits below)
+      const auto& dl = s.device_lists[static_cast<size_t>(d)];
+      std::vector<std::vector<std::pair<int, int>>> pushed(dl.size());
+      auto sizes = [&] {
+        std::vector<int> z;
+        for (const auto& st : pg.streams) z.push_back(static_cast<int>(st.size()));
+        return z;
+      };
+      for (size_t ii = 0; ii < dl.size(); ++ii) {
+        const Instruction& in = dl[ii];
+        const std::vector<int> before = sizes();
         const int mb = in.micro_batch;
         const int b = in.virtual_stage < P ? in.virtual_stage : 2 * P - 1 - in.virtual_stage;
         const std::string tag = std::string(to_string(in.kind)) + " mb" + std::to_string(mb) + " vs" + std::to_string(in.virtual_stage);
@@ -188,6 +199,34 @@ inline std::vector<RankProgram> build_programs(const Schedule& s, int P, bool on
               if (is_send(in.kind)) send({f, from, to}, mb, tag);
               else recv({f, from, to}, mb, tag);
             }
+        }
+        for (size_t st = 0; st < pg.streams.size(); ++st)
+          for (int x = before[st]; x < static_cast<int>(pg.streams[st].size()); ++x) pushed[ii].push_back({static_cast<int>(st), x});
+      }
+      if (pooled_slots) {
+        // slot reuse (executor.cpp slot_of): every op of an instruction that
+        // uses a reused slot waits for the previous occupant's release, the
+        // last op of its last instruction (a superset of the executor's waits)
+        std::vector<const Instruction*> ord;
+        for (const Instruction& in : dl) ord.push_back(&in);
+        auto held = [&](int obj) {
+          return obj < P ? energy_device(s, obj) == d : force_device(s, P, obj - P) == d;
+        };
+        const SlotPlan sp = plan_slots(ord, s, P, onef1b, false, 0, false, held, lanes);
+        std::vector<int> objs;
+        for (size_t ii = 0; ii < dl.size(); ++ii) {
+          slot_touches(dl[ii], s, P, onef1b, false, &objs);
+          for (int o : objs) {
+            if (!held(o)) continue;
+            const int prev = sp.prev.at({o, dl[ii].micro_batch});
+            if (prev < 0) continue;
+            const auto& rel = pushed[static_cast<size_t>(sp.last.at({o, prev}))];
+            if (rel.empty()) continue;
+            for (const auto& op : pushed[ii]) {
+              auto& deps = pg.streams[static_cast<size_t>(op.first)][static_cast<size_t>(op.second)].deps;
+              if (op.first != rel.back().first) deps.push_back(rel.back());
+            }
+          }
         }
       }
       progs.push_back(std::move(pg));

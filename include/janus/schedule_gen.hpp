@@ -163,6 +163,13 @@ struct PhaseTimes {
     if (!(t_FE < t_FF && t_FF < t_BE && t_BE < t_BF))
       throw domain_error("PhaseTimes: partial order t_FE < t_FF < t_BE < t_BF violated");
   }
+  /// Measured phase times (a timeline's means) need not follow the paper's
+  /// partial order; a cost model only needs them positive.
+  void check_positive() const {
+    const std::array<double, 4> v{t_FE, t_FF, t_BE, t_BF};
+    for (double x : v)
+      if (!(x > 0) || !std::isfinite(x)) throw domain_error("PhaseTimes: times must be positive and finite");
+  }
   double of(InstrKind k) const {
     switch (k) {
       case InstrKind::FE: return t_FE;
@@ -279,7 +286,7 @@ inline int wavek_phase_rank(InstrKind k) {
 /// order of that simulation, so it is a projection of one topological order
 /// (deadlock-free); the emitted text uses the SymFold instruction set.
 inline Schedule wavek_with_policy(int P, int N_mb, int k, const WaveKOptions& opt) {
-  opt.times.check();
+  opt.times.check_positive();  // measured times may break the paper's partial order
   const std::vector<WaveKUnit> units = pass4_decompose(N_mb, k);
   const Schedule base = symfold(P, N_mb);
   GroupedSchedule grouped = collect_groups(base);

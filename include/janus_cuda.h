@@ -47,6 +47,9 @@ typedef struct {
   int32_t n_slots;                          /* in-flight activation slots */
   int32_t device;                           /* CUDA ordinal */
   int32_t n_lanes;                          /* concurrent micro-batch lanes (scratch sets), >= 1 */
+  int32_t kernels;                          /* 0 = auto: the fused H=64 kernels when H = R = 64, else the
+                                               generic-width GEMM path (any H in {64,128,256}, any R);
+                                               1 = the generic-width path at any width */
 } janus_stage_desc;
 
 /* Host-side micro-batch: the LM payload.  Neighbour list in CSR by receiver
@@ -210,6 +213,12 @@ typedef struct {
   int32_t lanes;           /* compute streams per device; micro-batch m runs on lane m % lanes.
                               1 = strict list order (pipeline/bubble studies); >1 overlaps
                               independent micro-batches (throughput at P=1) */
+  int32_t unfolded_slots;  /* 0 (default) = activation slots pooled per stage by the schedule's
+                              live micro-batches (include/janus/slots.hpp); 1 = one slot per
+                              micro-batch (the unfolded baseline for memory studies) */
+  double phase_us[4];      /* WaveK's list-schedule cost model: measured per-stage phase times
+                              {FE, FF, BE, BF} (e.g. a timeline step's means); all 0 = the
+                              paper's UMA-1.2B ratios */
 } janus_exec_desc;
 
 typedef struct {
@@ -220,6 +229,8 @@ typedef struct {
   int64_t kernel_launches; /* kernels issued by the last step */
   int64_t peak_bytes[64];  /* per device: static + arena bytes of its stages */
   double loss;             /* sum of loss_E + loss_F held by this process */
+  int64_t act_bytes[64];   /* per device: activation slot pool bytes (part of peak_bytes) */
+  int32_t act_slots[64];   /* per device: slots of its largest pool (live micro-batches) */
 } janus_step_stats;
 
 typedef struct janus_trainer janus_trainer;
@@ -323,6 +334,15 @@ int janus_schedule_replay(const char* text, const double* t, double* makespan, d
  * non-blocking channels. */
 int janus_schedule_check_rendezvous(const char* text, int32_t onef1b, int32_t lanes, int32_t dp, int32_t layout,
                                     int32_t* ok, int64_t* completed, int64_t* total, char* stuck, int64_t cap);
+
+/* Activation slot pool per device of a schedule (include/janus/slots.hpp):
+ * the most micro-batches live at once on one of the device's stage objects
+ * under the SPEC lifetime rule, in the executor's issue
+ * order (local = all stages in one process, else each device's own list),
+ * at least min(lanes, micro-batches) per pool (concurrent lanes);
+ * unfolded = 1 gives one slot per micro-batch.  slots[n_devices]. */
+int janus_schedule_slot_pool(const char* text, int32_t onef1b, int32_t local, int32_t unfolded, int32_t lanes,
+                             int32_t* slots, int32_t cap, int32_t* n_devices);
 
 #ifdef __cplusplus
 }

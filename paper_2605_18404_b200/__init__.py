@@ -50,7 +50,7 @@ class StageDesc(ctypes.Structure):
     _fields_ = [("model", ModelDesc), ("unit_begin", ctypes.c_int32), ("unit_end", ctypes.c_int32),
                 ("max_atoms", ctypes.c_int32), ("max_edges", ctypes.c_int32), ("max_struct", ctypes.c_int32),
                 ("n_micro_batches", ctypes.c_int32), ("n_slots", ctypes.c_int32), ("device", ctypes.c_int32),
-                ("n_lanes", ctypes.c_int32)]
+                ("n_lanes", ctypes.c_int32), ("kernels", ctypes.c_int32)]
 
 
 class HostBatch(ctypes.Structure):
@@ -143,6 +143,7 @@ class Model:
     w_E: float = 1.0
     w_F: float = 10.0
     precision: int = PREC_FP32
+    generic: bool = False  # force the generic-width GEMM path (automatic when H or R != 64)
 
     def desc(self) -> ModelDesc:
         return ModelDesc(self.L, self.H, self.R, self.n_species, self.r_c, self.w_E, self.w_F, self.precision)
@@ -380,7 +381,8 @@ class Stage:
         o0, o1 = model.unit_offset(u0), model.unit_offset(u1)
         self.param_slice = slice(o0, o1)
         sl = np.ascontiguousarray(params_all[o0:o1], np.float32)
-        self.desc = StageDesc(model.desc(), u0, u1, max_atoms, max_edges, max_struct, n_mb, n_slots, device, 1)
+        self.desc = StageDesc(model.desc(), u0, u1, max_atoms, max_edges, max_struct, n_mb, n_slots, device, 1,
+                              1 if model.generic else 0)
         h = c_vp()
         check(_lib.janus_stage_create(ctypes.byref(self.desc), _p(sl), ctypes.byref(h)))
         self.h = h
@@ -511,6 +513,20 @@ def check_rendezvous(text: str, onef1b: bool = False, lanes: int = 1, dp: int = 
     return bool(ok.value), done.value, tot.value, buf.value.decode()
 
 
+_sig("janus_schedule_slot_pool", c_int, ctypes.c_char_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+     ctypes.c_int32, c_vp, ctypes.c_int32, c_vp)
+
+
+def slot_pool(text: str, onef1b: bool = False, local: bool = True, unfolded: bool = False, lanes: int = 1):
+    """Activation slots per device the executor allocates for a schedule
+    (include/janus/slots.hpp): the live micro-batches of its largest pool."""
+    out = np.zeros(64, np.int32)
+    n = ctypes.c_int32()
+    check(_lib.janus_schedule_slot_pool(text.encode(), 1 if onef1b else 0, 1 if local else 0, 1 if unfolded else 0,
+                                        lanes, _p(out), 64, ctypes.byref(n)))
+    return out[:n.value].tolist()
+
+
 def device_count() -> int:
     n = c_int()
     check(_lib.janus_device_count(ctypes.byref(n)))
@@ -552,13 +568,15 @@ def d2d(dst: int, src: int, nbytes: int) -> None:
 # ------------------------------------------------------------------ trainer
 class StepStats(ctypes.Structure):
     _fields_ = [("makespan_ms", c_d), ("bubble_ratio", c_d), ("busy_ms", c_d * 64), ("p2p_bytes", c_i64),
-                ("kernel_launches", c_i64), ("peak_bytes", c_i64 * 64), ("loss", c_d)]
+                ("kernel_launches", c_i64), ("peak_bytes", c_i64 * 64), ("loss", c_d), ("act_bytes", c_i64 * 64),
+                ("act_slots", ctypes.c_int32 * 64)]
 
 
 class ExecDesc(ctypes.Structure):
     _fields_ = [("n_stages", ctypes.c_int32), ("method", ctypes.c_int32), ("wavek_k", ctypes.c_int32),
                 ("n_micro_batches", ctypes.c_int32), ("local_stages", ctypes.c_int32), ("use_graphs", ctypes.c_int32),
-                ("dp_degree", ctypes.c_int32), ("record_timeline", ctypes.c_int32), ("lanes", ctypes.c_int32)]
+                ("dp_degree", ctypes.c_int32), ("record_timeline", ctypes.c_int32), ("lanes", ctypes.c_int32),
+                ("unfolded_slots", ctypes.c_int32), ("phase_us", ctypes.c_double * 4)]
 
 
 _sig("janus_trainer_create", c_int, c_vp, c_vp, c_vp, c_vp, c_int, c_vp)
@@ -633,12 +651,15 @@ class Trainer:
     def __init__(self, model: Model, params: np.ndarray, P: int, method: int, n_mb: int, k: int = 1,
                  max_atoms: int = 256, max_edges: int = 256 * 120, max_struct: int = 8, local: bool = True,
                  graphs: bool = False, timeline: bool = False, dp: int = 1, comm: "Comm | None" = None,
-                 rank: int = 0, device: int = 0, lanes: int = 1):
+                 rank: int = 0, device: int = 0, lanes: int = 1, unfolded: bool = False, phase_us=None):
+        """unfolded=True: one activation slot per micro-batch instead of the
+        schedule-sized pool (include/janus/slots.hpp), for memory A/B studies.
+        phase_us = measured (FE, FF, BE, BF) times for WaveK's cost model."""
         self.model, self.P, self.n_mb = model, P, n_mb
         self.ed = ExecDesc(P, method, k, n_mb, 1 if local else 0, 1 if graphs else 0, dp, 1 if timeline else 0,
-                           lanes)
+                           lanes, 1 if unfolded else 0, (ctypes.c_double * 4)(*(phase_us or (0, 0, 0, 0))))
         self.sd = StageDesc(model.desc(), 0, model.n_units, max_atoms, max_edges, max_struct, n_mb, n_mb, device,
-                            lanes)
+                            lanes, 1 if model.generic else 0)
         p = np.ascontiguousarray(params, np.float32)
         h = c_vp()
         check(_lib.janus_trainer_create(ctypes.byref(self.ed), ctypes.byref(self.sd), _p(p),

@@ -506,6 +506,23 @@ int janus_schedule_check_rendezvous(const char* text, int32_t onef1b, int32_t la
   });
 }
 
+int janus_schedule_slot_pool(const char* text, int32_t onef1b, int32_t local, int32_t unfolded, int32_t lanes,
+                             int32_t* slots, int32_t cap, int32_t* n_devices) {
+  return guard([&] {
+    need(text, "text");
+    need(slots, "slots");
+    const janus::Schedule s = janus::deserialize(text);
+    const int P = static_cast<int>(s.stage_map.size()) / 2;
+    if (P < 1) throw janus::domain_error("slot pool needs a 2P-virtual-stage schedule");
+    int n_mb = 0;
+    for (const auto& dl : s.device_lists)
+      for (const auto& in : dl) n_mb = std::max(n_mb, in.micro_batch + 1);
+    const std::vector<int> v = janus::slot_pool_sizes(s, P, onef1b != 0, local != 0, unfolded != 0, n_mb, std::max(1, lanes));
+    if (n_devices) *n_devices = static_cast<int32_t>(v.size());
+    for (size_t d = 0; d < v.size() && static_cast<int32_t>(d) < cap; ++d) slots[d] = v[d];
+  });
+}
+
 // ------------------------------------------------------------------ GARS
 namespace {
 std::vector<janus::gars::AtomGraph> graphs_of(const int32_t* atoms, int32_t M) {

@@ -49,6 +49,7 @@
 #include "../../include/janus/graph.hpp"
 #include "../../include/janus/model.hpp"
 #include "../../include/janus/schedule_gen.hpp"
+#include "../../include/janus/slots.hpp"
 #include "../../include/janus_cuda.h"
 #include "cuda_check.hpp"
 #include "stage.cuh"
@@ -138,6 +139,14 @@ struct janus_trainer {
   std::vector<int> gkey_alt;
   int64_t kernel_count_alt = -1;
   janus_step_stats last{};
+  // activation slot pool (include/janus/slots.hpp): slot per (object, mb),
+  // release events, and per step which streams already waited on a release
+  janus::SlotPlan slotplan;
+  std::map<janus_stage*, int> obj_of;
+  std::map<std::pair<int, int>, cudaEvent_t> rel_ev;
+  std::map<std::pair<int, int>, std::vector<cudaStream_t>> slot_waited;
+  std::map<std::pair<int, int>, cudaStream_t> slot_last;
+  int reserved_streams = 0;                      // per-rank mode: streams counted against the process's hardware queues
   std::vector<int> n_atoms;                      // per mb (for port sizes on the receive side)
   std::vector<std::array<int, 5>> shape;         // per (parity, mb): atoms, edges, structs, tiles, TC tiles (graph validity)
   // double-buffered geometry: a load fills the copy the step in flight does not
@@ -227,9 +236,30 @@ bool route(janus_trainer* t, const Instruction& in, int* flow, End* src, End* ds
   return true;
 }
 
-void port_ptr(janus_stage* st, int mb, int port, float** p, size_t* bytes) {
+// The activation slot of (stage object, micro-batch) for a use on stream s.
+// A reused slot makes every stream that touches it wait once for the previous
+// occupant's release (recorded after that occupant's last use).
+int slot_of(janus_trainer* t, janus_stage* st, int mb, cudaStream_t s) {
+  const auto o = t->obj_of.find(st);
+  if (o == t->obj_of.end()) throw state_error("stage object without a slot plan");
+  const std::pair<int, int> k{o->second, mb};
+  const auto it = t->slotplan.slot.find(k);
+  if (it == t->slotplan.slot.end()) throw state_error("slot plan misses a use of micro-batch " + std::to_string(mb));
+  const int prev = t->slotplan.prev.at(k);
+  if (prev >= 0) {
+    std::vector<cudaStream_t>& w = t->slot_waited[k];
+    if (std::find(w.begin(), w.end(), s) == w.end()) {
+      JANUS_CUDA(cudaStreamWaitEvent(s, t->rel_ev.at({k.first, prev}), 0));
+      w.push_back(s);
+    }
+  }
+  t->slot_last[k] = s;
+  return it->second;
+}
+
+void port_ptr(janus_trainer* t, janus_stage* st, int mb, int port, cudaStream_t s, float** p, size_t* bytes) {
   void* d = nullptr;
-  stage_port(st, mb, mb, port, &d, bytes);
+  stage_port(st, mb, slot_of(t, st, mb, s), port, &d, bytes);
   *p = static_cast<float*>(d);
 }
 
@@ -278,15 +308,18 @@ void do_send(janus_trainer* t, VDev& dv, int flow, int mb, janus_stage* src, int
              int from_b, int to_b, int peer_dev) {
   float* sp;
   size_t sb;
-  port_ptr(src, mb, sport, &sp, &sb);
-  if (!t->local) return chan_send(t, dv, flow, mb, sp, sb, peer_dev);
+  if (!t->local) {
+    port_ptr(t, src, mb, sport, t->chan_stream[static_cast<size_t>(channel_index(t->chans, {flow, dv.id, peer_dev}))], &sp, &sb);
+    return chan_send(t, dv, flow, mb, sp, sb, peer_dev);
+  }
+  port_ptr(t, src, mb, sport, dv.send, &sp, &sb);
   cudaEvent_t ready = next_event(t);
   JANUS_CUDA(cudaEventRecord(ready, lane_stream(t, dv, mb)));
   JANUS_CUDA(cudaStreamWaitEvent(dv.send, ready, 0));
   t->p2p_bytes += static_cast<int64_t>(sb);
   float* dp;
   size_t db;
-  port_ptr(dst, mb, dport, &dp, &db);
+  port_ptr(t, dst, mb, dport, dv.send, &dp, &db);
   if (db != sb) throw state_error("port size mismatch between channel ends");
   JANUS_CUDA(cudaMemcpyAsync(dp, sp, sb, cudaMemcpyDeviceToDevice, dv.send));
   cudaEvent_t done = next_event(t);
@@ -304,7 +337,7 @@ void do_recv(janus_trainer* t, VDev& dv, int flow, int mb, janus_stage* dst, int
   } else {
     float* dp;
     size_t db;
-    port_ptr(dst, mb, dport, &dp, &db);
+    port_ptr(t, dst, mb, dport, t->chan_stream[static_cast<size_t>(channel_index(t->chans, {flow, peer_dev, dv.id}))], &dp, &db);
     if (db != bytes) throw state_error("port size mismatch between channel ends");
     chan_recv(t, dv, flow, mb, dp, db, peer_dev);
   }
@@ -329,8 +362,12 @@ void mirror_back_send(janus_trainer* t, VDev& dv, int b, int mb) {
   janus_stage* f = t->F[static_cast<size_t>(b)];
   float* sp;
   size_t sb;
-  port_ptr(f, mb, JANUS_PORT_BADJ_OUT, &sp, &sb);
-  if (!t->local) return chan_send(t, dv, kFlowMirrorBack + (b & 1), mb, sp, sb, t->E_dev[static_cast<size_t>(b)]);
+  if (!t->local) {
+    const int c = channel_index(t->chans, {kFlowMirrorBack + (b & 1), dv.id, t->E_dev[static_cast<size_t>(b)]});
+    port_ptr(t, f, mb, JANUS_PORT_BADJ_OUT, t->chan_stream[static_cast<size_t>(c)], &sp, &sb);
+    return chan_send(t, dv, kFlowMirrorBack + (b & 1), mb, sp, sb, t->E_dev[static_cast<size_t>(b)]);
+  }
+  port_ptr(t, f, mb, JANUS_PORT_BADJ_OUT, dv.send, &sp, &sb);
   cudaEvent_t ready = next_event(t);
   JANUS_CUDA(cudaEventRecord(ready, lane_stream(t, dv, mb)));
   JANUS_CUDA(cudaStreamWaitEvent(dv.send, ready, 0));
@@ -346,7 +383,7 @@ void mirror_back_recv_add(janus_trainer* t, VDev& dv, int b, int mb) {
   janus_stage* e = t->E[static_cast<size_t>(b)];
   float* dp;
   size_t db;
-  port_ptr(e, mb, JANUS_PORT_BADJ_OUT, &dp, &db);
+  port_ptr(t, e, mb, JANUS_PORT_BADJ_OUT, lane_stream(t, dv, mb), &dp, &db);
   float* buf = t->mirror_buf[static_cast<size_t>(b) * t->ed.n_micro_batches + mb];
   if (t->local) {
     const auto it = t->delivered.find({kFlowMirrorBack, mb, b, b});
@@ -385,8 +422,8 @@ void local_handoff(janus_trainer* t, VDev& dv, int mb, int from_vs, int to_vs) {
   if (src == dst) return;
   float *a, *b;
   size_t na, nb;
-  port_ptr(src, mb, sp, &a, &na);
-  port_ptr(dst, mb, dp, &b, &nb);
+  port_ptr(t, src, mb, sp, lane_stream(t, dv, mb), &a, &na);
+  port_ptr(t, dst, mb, dp, lane_stream(t, dv, mb), &b, &nb);
   if (na != nb) throw state_error("local hand-off size mismatch");
   JANUS_CUDA(cudaMemcpyAsync(b, a, na, cudaMemcpyDeviceToDevice, lane_stream(t, dv, mb)));
 }
@@ -417,7 +454,8 @@ void execute(janus_trainer* t, const Instruction& in, const janus_opt& opt) {
       return;  // geometry is uploaded to every stage by janus_trainer_load
     case InstrKind::FE: {
       const int b = block_of(t, in.virtual_stage);
-      timed(t, dv, in, [&] { stage_fe(t->E[static_cast<size_t>(b)], mb, mb, cs, ln); });
+      janus_stage* e = t->E[static_cast<size_t>(b)];
+      timed(t, dv, in, [&] { stage_fe(e, mb, slot_of(t, e, mb, cs), cs, ln); });
       local_handoff(t, dv, mb, in.virtual_stage, in.virtual_stage + 1);
       if (t->onef1b) mirror_act_send(t, dv, b, mb);
       return;
@@ -427,8 +465,9 @@ void execute(janus_trainer* t, const Instruction& in, const janus_opt& opt) {
       janus_stage* f = t->F[static_cast<size_t>(b)];
       if (t->onef1b) mirror_act_recv(t, dv, b, mb);
       timed(t, dv, in, [&] {
-        if (in.has_flag(kFlagRecompute)) stage_fe(f, mb, mb, cs, ln);  // regenerate FE activations
-        stage_ff(f, mb, mb, cs, ln);
+        const int sl = slot_of(t, f, mb, cs);
+        if (in.has_flag(kFlagRecompute)) stage_fe(f, mb, sl, cs, ln);  // regenerate FE activations
+        stage_ff(f, mb, sl, cs, ln);
       });
       local_handoff(t, dv, mb, in.virtual_stage, in.virtual_stage + 1);
       return;
@@ -437,8 +476,9 @@ void execute(janus_trainer* t, const Instruction& in, const janus_opt& opt) {
       const int b = block_of(t, in.virtual_stage);
       janus_stage* f = t->F[static_cast<size_t>(b)];
       timed(t, dv, in, [&] {
-        stage_bf(f, mb, mb, cs, ln);
-        if (t->onef1b) stage_be(f, mb, mb, cs, /*inj_only=*/true, ln);
+        const int sl = slot_of(t, f, mb, cs);
+        stage_bf(f, mb, sl, cs, ln);
+        if (t->onef1b) stage_be(f, mb, sl, cs, /*inj_only=*/true, ln);
       });
       if (t->onef1b) mirror_back_send(t, dv, b, mb);
       local_handoff(t, dv, mb, in.virtual_stage, in.virtual_stage - 1);
@@ -447,7 +487,8 @@ void execute(janus_trainer* t, const Instruction& in, const janus_opt& opt) {
     case InstrKind::BE: {
       const int b = block_of(t, in.virtual_stage);
       timed(t, dv, in, [&] {
-        stage_be(t->E[static_cast<size_t>(b)], mb, mb, cs, false, ln);
+        janus_stage* e = t->E[static_cast<size_t>(b)];
+        stage_be(e, mb, slot_of(t, e, mb, cs), cs, false, ln);
         if (t->onef1b) mirror_back_recv_add(t, dv, b, mb);
       });
       local_handoff(t, dv, mb, in.virtual_stage, in.virtual_stage - 1);
@@ -496,8 +537,19 @@ void issue_step(janus_trainer* t, const janus_opt& opt) {
   t->pool_next = 0;
   t->delivered.clear();
   t->p2p_bytes = 0;
+  t->slot_waited.clear();
+  t->slot_last.clear();
+  size_t pos = 0;
+  auto release = [&] {  // occupants whose last use was this instruction hand their slot on
+    for (const auto& k : t->slotplan.release_after[pos])
+      JANUS_CUDA(cudaEventRecord(t->rel_ev.at(k), t->slot_last.at(k)));
+    ++pos;
+  };
   if (t->local) {
-    for (int idx : t->order) execute(t, *t->graph.flat[static_cast<size_t>(idx)], opt);
+    for (int idx : t->order) {
+      execute(t, *t->graph.flat[static_cast<size_t>(idx)], opt);
+      release();
+    }
   } else {
     for (const Instruction& in : t->sched.device_lists[static_cast<size_t>(t->my_dev)]) {
       t->last_comm = nullptr;
@@ -507,6 +559,7 @@ void issue_step(janus_trainer* t, const janus_opt& opt) {
                          std::to_string(t->issued.load()) + ")";
       }
       execute(t, in, opt);
+      release();
       ++t->issued;
       if (t->hang_s > 0) {
         cudaStream_t s = t->last_comm ? t->last_comm : lane_stream(t, t->devs[0], in.micro_batch);
@@ -628,6 +681,10 @@ void finalize_local(janus_trainer* t, const janus_opt& opt) {
 // queue stalls the unrelated streams behind it, which may be what the peer
 // waits for.  Both are process-wide settings read at context creation, so
 // the application sets them; the trainer refuses to run without them.
+// streams held by the per-rank trainers of this process: ranks run as threads
+// of one process share its context's hardware queues
+std::atomic<int> g_peer_streams{0};
+
 void check_per_rank_runtime(const janus_trainer* t, int n_streams) {
   using GetMode = CUresult (*)(CUmoduleLoadingMode*);
   void* fn = nullptr;
@@ -646,6 +703,14 @@ void check_per_rank_runtime(const janus_trainer* t, int n_streams) {
                        " streams but CUDA_DEVICE_MAX_CONNECTIONS=" + std::to_string(conn) +
                        " hardware queues; set it to >= " + std::to_string(n_streams) +
                        " (max 32) before the first CUDA call, or use fewer lanes");
+  const int before = g_peer_streams.fetch_add(n_streams);
+  if (before + n_streams > conn) {
+    g_peer_streams.fetch_sub(n_streams);
+    throw config_error("per-rank mode: the ranks of this process use " + std::to_string(before + n_streams) +
+                       " streams in one CUDA context but CUDA_DEVICE_MAX_CONNECTIONS=" + std::to_string(conn) +
+                       " hardware queues (a peer-blocked stream would stall the streams sharing its queue); run "
+                       "fewer ranks per process or fewer lanes");
+  }
 }
 
 }  // namespace
@@ -679,7 +744,13 @@ janus_trainer* trainer_create(const janus_exec_desc& ed, const janus_stage_desc&
   if (t->local && t->ed.dp_degree != 1) throw config_error("data parallelism needs NCCL mode");
   switch (ed.method) {
     case 0: t->sched = symfold(t->P, ed.n_micro_batches); break;
-    case 1: t->sched = wavek(t->P, ed.n_micro_batches, ed.wavek_k); break;
+    case 1: {
+      WaveKOptions wo;  // measured phase times when the caller has them (SPEC.md:578-637 tuner input)
+      if (ed.phase_us[0] > 0 || ed.phase_us[1] > 0 || ed.phase_us[2] > 0 || ed.phase_us[3] > 0)
+        wo.times = PhaseTimes{ed.phase_us[0], ed.phase_us[1], ed.phase_us[2], ed.phase_us[3]};
+      t->sched = wavek(t->P, ed.n_micro_batches, ed.wavek_k, wo);
+      break;
+    }
     case 2: t->sched = onef1b_2nd(t->P, ed.n_micro_batches); break;
     case 4: t->sched = hanayo_2nd(t->P, ed.n_micro_batches); break;  // V-shape + wave order, FF recompute
     default: throw domain_error("unknown method");
@@ -741,24 +812,52 @@ janus_trainer* trainer_create(const janus_exec_desc& ed, const janus_stage_desc&
     JANUS_CUDA(cudaMalloc(&t->loss_snap[q], sizeof(float) * 4 * static_cast<size_t>(std::max(1, ed.n_micro_batches))));
   }
   JANUS_CUDA(cudaMalloc(&t->dopt, sizeof(janus_opt)));
-  auto make = [&](int b) {
+  // local issue order: a topological order of the full DAG (seq + data edges),
+  // so every send is issued before its receive.
+  t->graph = build_dependencies(t->sched);
+  if (t->local) t->order = local_issue_order(t->graph);
+  // activation slot pools: sized by the micro-batches live at once on each
+  // stage object in this process's issue order (include/janus/slots.hpp)
+  {
+    std::vector<const Instruction*> ord;
+    if (t->local)
+      for (int idx : t->order) ord.push_back(t->graph.flat[static_cast<size_t>(idx)]);
+    else
+      for (const Instruction& in : t->sched.device_lists[static_cast<size_t>(t->my_dev)]) ord.push_back(&in);
+    const int P = t->P;
+    auto held = [&](int obj) {
+      if (t->local) return true;
+      const int b = obj < P ? obj : obj - P;
+      return obj < P ? t->E_dev[static_cast<size_t>(b)] == t->my_dev : t->F_dev[static_cast<size_t>(b)] == t->my_dev;
+    };
+    t->slotplan = plan_slots(ord, t->sched, P, t->onef1b, t->local, ed.n_micro_batches, ed.unfolded_slots != 0, held,
+                             t->ed.lanes);
+  }
+  auto make = [&](int b, int obj) {
     janus_stage_desc d = sd;
     d.unit_begin = t->plan.blocks[static_cast<size_t>(b)].first;
     d.unit_end = t->plan.blocks[static_cast<size_t>(b)].second;
     d.n_micro_batches = ed.n_micro_batches;
-    d.n_slots = ed.n_micro_batches;
+    d.n_slots = std::max(1, t->slotplan.n_slots[static_cast<size_t>(obj)]);
     d.n_lanes = std::max(1, t->ed.lanes);
     const int64_t off = mc.unit_param_offset(d.unit_begin);
     janus_stage* st = stage_create(d, all_params + off);
     t->owned.push_back(st);
+    t->obj_of[st] = obj;
     return st;
   };
   for (int b = 0; b < t->P; ++b) {
     const bool e_here = t->local || t->E_dev[static_cast<size_t>(b)] == t->my_dev;
     const bool f_here = t->local || t->F_dev[static_cast<size_t>(b)] == t->my_dev;
-    if (e_here) t->E[static_cast<size_t>(b)] = make(b);
-    if (f_here) t->F[static_cast<size_t>(b)] = (t->onef1b ? make(b) : t->E[static_cast<size_t>(b)]);
+    if (e_here) t->E[static_cast<size_t>(b)] = make(b, slot_obj_energy(b, t->P, t->onef1b));
+    if (f_here) t->F[static_cast<size_t>(b)] = (t->onef1b ? make(b, slot_obj_force(b, t->P, t->onef1b)) : t->E[static_cast<size_t>(b)]);
   }
+  for (const auto& kv : t->slotplan.prev)
+    if (kv.second >= 0 && !t->rel_ev.count({kv.first.first, kv.second})) {
+      cudaEvent_t e;
+      JANUS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      t->rel_ev[{kv.first.first, kv.second}] = e;
+    }
   if (t->onef1b) {
     t->mirror_buf.assign(static_cast<size_t>(t->P) * ed.n_micro_batches, nullptr);
     const size_t bytes = sizeof(float) * static_cast<size_t>(sd.max_atoms) * sd.model.H * 2;
@@ -807,27 +906,8 @@ janus_trainer* trainer_create(const janus_exec_desc& ed, const janus_stage_desc&
     int n_streams = static_cast<int>(t->devs[0].lane.size()) + 4;  // lanes, send, recv, root, load
     for (cudaStream_t cs : t->chan_stream) n_streams += cs ? 1 : 0;
     check_per_rank_runtime(t.get(), n_streams);
+    t->reserved_streams = n_streams;
     t->xport = make_transport(comm, tp);
-  }
-  // local issue order: a topological order of the full DAG (seq + data edges),
-  // so every send is issued before its receive.
-  t->graph = build_dependencies(t->sched);
-  if (t->local) {
-    const int n = t->graph.size();
-    std::vector<int> indeg(static_cast<size_t>(n));
-    std::vector<std::vector<int>> succ(static_cast<size_t>(n));
-    for (int i = 0; i < n; ++i) {
-      indeg[static_cast<size_t>(i)] = static_cast<int>(t->graph.preds[static_cast<size_t>(i)].size());
-      for (int p : t->graph.preds[static_cast<size_t>(i)]) succ[static_cast<size_t>(p)].push_back(i);
-    }
-    std::vector<int> q;
-    for (int i = 0; i < n; ++i)
-      if (indeg[static_cast<size_t>(i)] == 0) q.push_back(i);
-    for (size_t h = 0; h < q.size(); ++h)
-      for (int x : succ[static_cast<size_t>(q[h])])
-        if (--indeg[static_cast<size_t>(x)] == 0) q.push_back(x);
-    if (static_cast<int>(q.size()) != n) throw deadlock_error("schedule dependency graph has a cycle");
-    t->order = std::move(q);
   }
   t->n_atoms.assign(static_cast<size_t>(ed.n_micro_batches), 0);
   JANUS_CUDA(cudaDeviceSynchronize());
@@ -836,6 +916,7 @@ janus_trainer* trainer_create(const janus_exec_desc& ed, const janus_stage_desc&
 
 void trainer_destroy(janus_trainer* t) {
   if (!t) return;
+  if (t->reserved_streams) g_peer_streams.fetch_sub(t->reserved_streams);
   cudaSetDevice(t->sd.device);
   cudaDeviceSynchronize();
   if (t->gexec) cudaGraphExecDestroy(t->gexec);
@@ -850,6 +931,7 @@ void trainer_destroy(janus_trainer* t) {
   for (janus_stage* s : t->owned) stage_destroy(s);
   for (void* p : t->allocs) cudaFree(p);
   for (cudaEvent_t e : t->pool) cudaEventDestroy(e);
+  for (auto& kv : t->rel_ev) cudaEventDestroy(kv.second);
   for (auto& r : t->recs) {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
@@ -1152,7 +1234,11 @@ void trainer_wait(janus_trainer* t, janus_step_stats* stats) {
       if (t->E[static_cast<size_t>(b)] == st) dev = t->E_dev[static_cast<size_t>(b)];
       else if (t->F[static_cast<size_t>(b)] == st) dev = t->F_dev[static_cast<size_t>(b)];
     }
-    if (dev < 64) s.peak_bytes[dev] += st->static_bytes + st->arena_bytes;
+    if (dev < 64) {
+      s.peak_bytes[dev] += st->static_bytes + st->arena_bytes;
+      s.act_bytes[dev] += st->pool_bytes;
+      s.act_slots[dev] = std::max<int32_t>(s.act_slots[dev], static_cast<int32_t>(st->slots.size()));
+    }
   }
   // losses held here: L_E on the readout stage, L_F on the stage holding block 0's force replica
   // (slot == micro-batch; one contiguous copy per stage, summed in micro-batch order)

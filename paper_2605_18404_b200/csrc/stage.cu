@@ -18,6 +18,8 @@
 #include <utility>
 #include <vector>
 
+#include <cublas_v2.h>
+
 #include "../../include/janus/errors.hpp"
 
 #include "edge_kernels.cuh"
@@ -42,6 +44,7 @@
       edge_tc::KERN<8><<<(GRID), 256, 0, (S)>>>(__VA_ARGS__);                   \
   } while (0)
 #include "node_kernels.cuh"
+#include "wide.cuh"
 #include "wgrad_tc.cuh"
 #include "stage.cuh"
 #include "stage_api.hpp"
@@ -66,6 +69,12 @@ int64_t unit_param_offset(const janus_model_desc& m, int u) {
 }
 
 namespace {
+
+#define JANUS_BLAS(x)                                                                                   \
+  do {                                                                                                  \
+    const cublasStatus_t st_ = (x);                                                                     \
+    if (st_ != CUBLAS_STATUS_SUCCESS) throw cuda_error(std::string(#x) + ": cuBLAS status " + std::to_string(static_cast<int>(st_))); \
+  } while (0)
 
 constexpr int kH = 64;
 constexpr int kR = 64;
@@ -250,8 +259,8 @@ void refresh_transposes(janus_stage* st, cudaStream_t s) {
 
 // pointer into a port for the actual atom count n
 float* port_h(const Port& p, int) { return p.buf; }
-float* port_m(const Port& p, int n) { return p.buf + static_cast<size_t>(n) * kH; }
-float* port_v(const Port& p, int n) { return p.buf + static_cast<size_t>(n) * kH * (p.has_m ? 2 : 1); }
+float* port_m(const Port& p, int n) { return p.buf + static_cast<size_t>(n) * p.H; }
+float* port_v(const Port& p, int n) { return p.buf + static_cast<size_t>(n) * p.H * (p.has_m ? 2 : 1); }
 
 const float* in_h(const janus_stage* st, const Slot& sl, int u, int n) {
   if (u == st->u0) return port_h(sl.ports[JANUS_PORT_ACT_IN], n);
@@ -270,6 +279,8 @@ float* ledger(janus_stage* st, float* base, int mb, int u) {
 }
 
 bool use_tc(const janus_stage* st) { return st->m.precision == JANUS_PREC_TF32; }
+// undirected edge-pair tables (pair_tc.cuh): the tensor-core H=64 kernels and the generic-width path
+bool needs_pairs(const janus_stage* st) { return use_tc(st) || st->wide; }
 // Tensor-core edge grids.  CTAs loop over tiles (static assignment), so a CTA
 // may take several: its fixed costs (weight TMA, TMEM alloc, first dependent
 // loads and, for BF/BE, the weight-gradient partial write-out and its share of
@@ -320,7 +331,11 @@ LoadLayout load_layout(const janus_stage_desc& d) {
 
 janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
   const janus_model_desc& m = d.model;
-  if (m.H != kH || m.R != kR) throw config_error("this build supports H=64, R=64 (got H=" + std::to_string(m.H) + ", R=" + std::to_string(m.R) + ")");
+  const bool wide = d.kernels == 1 || m.H != kH || m.R != kR;
+  if (d.kernels < 0 || d.kernels > 1) throw config_error("kernels must be 0 (auto) or 1 (generic width)");
+  if (wide && m.H != 64 && m.H != 128 && m.H != 256)
+    throw config_error("hidden width H must be 64, 128 or 256 (got H=" + std::to_string(m.H) + ")");
+  if (wide && (m.R < 2 || m.R > 1024)) throw config_error("basis size R must be in [2, 1024]");
   if (m.L < 1 || m.n_species < 1 || m.n_species > 256) throw config_error("bad model shape");
   if (m.precision != JANUS_PREC_FP32 && m.precision != JANUS_PREC_TF32) throw config_error("unknown precision");
   const int U = 2 * m.L + 2;
@@ -332,6 +347,7 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
   try {
     st->desc = d;
     st->m = m;
+    st->wide = wide;
     st->u0 = d.unit_begin;
     st->u1 = d.unit_end;
     st->U = U;
@@ -347,7 +363,7 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
     st->n_params = off;
     const size_t NP = static_cast<size_t>(off), NMB = static_cast<size_t>(d.n_micro_batches);
     const size_t NA = static_cast<size_t>(d.max_atoms), NE = static_cast<size_t>(d.max_edges);
-    const size_t NH = NA * kH;
+    const size_t NH = NA * static_cast<size_t>(m.H);
     st->params = dalloc<float>(st, NP, true);
     st->grad = dalloc<float>(st, NP, true);
     st->m1 = dalloc<float>(st, NP, true);
@@ -361,7 +377,7 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
       const UnitKind k = unit_kind(u, m.L);
       // msg: [Bt | Wt | tensor-core pack]; upd: [Ut | Vt]; readout: [Ot]
       const size_t n = k == kMsg ? 2 * kH * kH + edge_tc::kPackBytes / sizeof(float) : (k == kReadout ? 1 : 2) * kH * kH;
-      st->tw.push_back(k == kEmbed ? nullptr : dalloc<float>(st, n, true));
+      st->tw.push_back(k == kEmbed || wide ? nullptr : dalloc<float>(st, n, true));
     }
     // geometry per micro-batch
     st->geo.resize(2 * NMB);
@@ -400,7 +416,9 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
       g.pcanon = dalloc<int>(st, NE / 2 + 1, false);
       g.pgeo = dalloc<float4>(st, 2 * (NE / 2 + 1), false);
     }
-    // slots
+    // activation slot pool (the executor sizes it by the schedule's in-flight
+    // micro-batches, include/janus/slots.hpp)
+    const int64_t arena0 = st->arena_bytes;
     st->slots.resize(static_cast<size_t>(d.n_slots));
     for (auto& sl : st->slots) {
       sl.units.resize(static_cast<size_t>(st->u1 - st->u0));
@@ -414,9 +432,9 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
             b.ff_a = dalloc<float>(st, NH, false);
             b.ff_Y = dalloc<float>(st, NH, false);
             b.inj = dalloc<float>(st, NH, false);
-            if (m.precision == JANUS_PREC_TF32) {
-              b.wf = dalloc<float>(st, (NE / 2 + 1) * kH, false);
-              b.wfp = dalloc<float>(st, (NE / 2 + 1) * kH, false);
+            if (m.precision == JANUS_PREC_TF32 || wide) {
+              b.wf = dalloc<float>(st, (NE / 2 + 1) * m.H, false);
+              b.wfp = dalloc<float>(st, (NE / 2 + 1) * m.H, false);
             }
             break;
           case kUpd:
@@ -438,19 +456,23 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
         Port& port = sl.ports[p];
         port.has_m = at_input ? st->in_has_m : st->out_has_m;
         port.has_vec = (p >= JANUS_PORT_ADJ_IN && p <= JANUS_PORT_TAN_OUT);
+        port.H = m.H;
         port.buf = dalloc<float>(st, NH * (port.has_m ? 2 : 1) + (port.has_vec ? 3 * NA : 0), false);
       }
-      sl.F = dalloc<float>(st, 3 * NA, false);
-      sl.Fbar = dalloc<float>(st, 3 * NA, false);
-      sl.e_atom = dalloc<float>(st, NA, false);
-      sl.E = dalloc<float>(st, static_cast<size_t>(d.max_struct), false);
-      sl.eps = dalloc<float>(st, static_cast<size_t>(d.max_struct), false);
-      sl.loss = nullptr;  // points into st->losses below
     }
-    st->losses = dalloc<float>(st, 2 * static_cast<size_t>(d.n_slots), false);
+    st->pool_bytes = st->arena_bytes - arena0;
+    st->outs.resize(NMB);
+    for (MbOut& mo : st->outs) {
+      mo.F = dalloc<float>(st, 3 * NA, false);
+      mo.Fbar = dalloc<float>(st, 3 * NA, false);
+      mo.e_atom = dalloc<float>(st, NA, false);
+      mo.E = dalloc<float>(st, static_cast<size_t>(d.max_struct), false);
+      mo.eps = dalloc<float>(st, static_cast<size_t>(d.max_struct), false);
+    }
+    st->losses = dalloc<float>(st, 2 * NMB, false);
     st->pair_chunks_cap = static_cast<int>((NE + 1023) / 1024) + 1;
     st->pair_counts = dalloc<int>(st, static_cast<size_t>(node::kMaxGeoJobs) * st->pair_chunks_cap, false);
-    for (size_t x = 0; x < st->slots.size(); ++x) st->slots[x].loss = st->losses + 2 * x;
+    for (size_t x = 0; x < NMB; ++x) st->outs[x].loss = st->losses + 2 * x;
     st->lanes.resize(static_cast<size_t>(std::max(1, d.n_lanes)));
     // measured on the C2 bench (16 lanes): 128-edge tiles 1/1 -> 4735, 4/8 -> 5765;
     // multi-chunk tiles (~2 chunks) 2/4 -> 6363, 2/3 -> 6467 structures/s
@@ -484,10 +506,31 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
       sc.s3 = dalloc<float>(st, NH, false);
       sc.s4 = dalloc<float>(st, NH, false);
       sc.s5 = dalloc<float>(st, NH, false);
+      if (wide) {  // per-pair operand stacks + this lane's cuBLAS handle (fixed workspace: graph-capture safe)
+        const size_t P2 = NE + 2;
+        sc.phi2 = dalloc<float>(st, P2 * static_cast<size_t>(m.R), false);
+        sc.z2 = dalloc<float>(st, P2 * static_cast<size_t>(m.H), false);
+        sc.a2 = dalloc<float>(st, P2 * static_cast<size_t>(m.H), false);
+        sc.b2 = dalloc<float>(st, P2 * static_cast<size_t>(m.H), false);
+        constexpr size_t kWs = 32u << 20;
+        sc.blas_ws = dalloc<uint8_t>(st, kWs, false);
+        cublasHandle_t h = nullptr;
+        JANUS_BLAS(cublasCreate(&h));
+        sc.blas = h;
+        JANUS_BLAS(cublasSetWorkspace(h, sc.blas_ws, kWs));
+        JANUS_BLAS(cublasSetPointerMode(h, CUBLAS_POINTER_MODE_HOST));
+        continue;
+      }
       sc.partial = dalloc<float>(st, NA * static_cast<size_t>(EC::PE), false);
       const size_t chunks = (NA + node::kWChunk - 1) / node::kWChunk;
       sc.wpart = dalloc<float>(st, 3 * chunks * std::max<size_t>(kH * kH + 2 * kH, static_cast<size_t>(m.n_species) * kH), false);
       sc.counter = dalloc<unsigned>(st, 1, false);
+    }
+    if (wide) {
+      const size_t n1 = std::max(NE, NA) + 2;
+      st->ones = dalloc<float>(st, n1, true);
+      wide::fill_kernel<<<blocks(static_cast<int64_t>(n1), 256), 256>>>(static_cast<int64_t>(n1), st->ones, 1.0f);
+      JANUS_LAUNCH_CHECK("ones");
     }
     JANUS_CUDA(cudaFuncSetAttribute(edge_tc::wgrad_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge_tc::wgrad_tc_smem()));
     JANUS_CUDA(cudaFuncSetAttribute(edge::msg_fe_kernel<kH, kR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge::fe_smem<kH, kR>()));
@@ -505,9 +548,11 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
     JANUS_CUDA(cudaFuncSetAttribute(edge_tc::msg_be_pair_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge_tc::be_pair_smem()));
     JANUS_CUDA(cudaFuncSetAttribute(edge_tc::msg_bf_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge_tc::bf_smem()));
     JANUS_CUDA(cudaFuncSetAttribute(edge_tc::msg_be_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge_tc::be_smem()));
-    refresh_transposes(st, nullptr);
+    if (!wide) refresh_transposes(st, nullptr);
     JANUS_CUDA(cudaDeviceSynchronize());
   } catch (...) {
+    for (auto& sc : st->lanes)
+      if (sc.blas) cublasDestroy(static_cast<cublasHandle_t>(sc.blas));
     for (void* p : st->allocs) cudaFree(p);
     for (void* p : st->host_allocs) cudaFreeHost(p);
     delete st;
@@ -521,6 +566,8 @@ void stage_destroy(janus_stage* st) {
   cudaSetDevice(st->desc.device);
   cudaDeviceSynchronize();
   delete st->lm;
+  for (auto& sc : st->lanes)
+    if (sc.blas) cublasDestroy(static_cast<cublasHandle_t>(sc.blas));
   for (void* p : st->allocs) cudaFree(p);
   for (void* p : st->host_allocs) cudaFreeHost(p);
   delete st;
@@ -529,7 +576,7 @@ void stage_destroy(janus_stage* st) {
 size_t port_elems(const janus_stage* st, int port, int n) {
   const Port& p = st->slots[0].ports[port];
   if (!p.buf) return 0;
-  return static_cast<size_t>(n) * kH * (p.has_m ? 2 : 1) + (p.has_vec ? 3 * static_cast<size_t>(n) : 0);
+  return static_cast<size_t>(n) * p.H * (p.has_m ? 2 : 1) + (p.has_vec ? 3 * static_cast<size_t>(n) : 0);
 }
 
 // ================================================================== LM
@@ -632,8 +679,8 @@ void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_
   g.n_struct = hb.n_struct;
   g.n_tiles = static_cast<int>(tiles.size()) - 1;
   g.n_tiles_tc = static_cast<int>(tiles_tc.size()) - 1;
-  if (use_tc(st) && E % 2) throw domain_error("odd edge count: every edge needs a distinct reverse edge");
-  if (use_tc(st) && !dcsr)  // host CSR: the pair tables need rev to be a fixed-point-free involution
+  if (needs_pairs(st) && E % 2) throw domain_error("odd edge count: every edge needs a distinct reverse edge");
+  if (needs_pairs(st) && !dcsr)  // host CSR: the pair tables need rev to be a fixed-point-free involution
     for (int e = 0; e < E; ++e) {
       const int r = hb.rev[e];
       if (r < 0 || r >= E || r == e || hb.rev[r] != e) throw domain_error("rev must pair every edge with a distinct reverse edge");
@@ -712,7 +759,7 @@ void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_
   if (E > 0)
     node::geometry_kernel<<<blocks(E, 256), 256, 0, s>>>(N, E, g.row_ptr, g.col, g.shift, g.pos, g.struct_id, g.cell,
                                                          static_cast<double>(st->m.r_c), g.src, g.d, g.u, g.c, g.dc);
-  if (E > 0 && use_tc(st)) {
+  if (E > 0 && needs_pairs(st)) {
     node::GeoJobs J{};
     J.n = 1;
     J.j[0].n_edges = E;
@@ -753,7 +800,7 @@ void stage_geometry_flush(janus_stage* st, std::vector<node::GeoJob>& jobs, cuda
     }
     J.total_edges = base;
     if (base > 0) node::geometry_batched_kernel<<<blocks(base, 256), 256, 0, s>>>(J);
-    if (base > 0 && use_tc(st)) {
+    if (base > 0 && needs_pairs(st)) {
       int emax = 0;
       for (int k = 0; k < J.n; ++k) emax = std::max(emax, J.j[k].n_edges);
       launch_pairs(st, J, emax, s);
@@ -784,12 +831,16 @@ void launch_filter(janus_stage* st, const DevGeo& g, Slot& sl, int u_only, cudaS
   JANUS_LAUNCH_CHECK("msg_filter_tc");
 }
 
+#include "stage_wide.inc"
+
 // ================================================================== FE
 void stage_fe(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
   check_mb_slot(st, mb, slot);
+  if (st->wide) return wide_fe(st, mb, slot, s, lane);
   Scratch& sc = lane_of(st, lane);
   const DevGeo& g = geo_of(st, mb);
   Slot& sl = st->slots[static_cast<size_t>(slot)];
+  MbOut& mo = st->outs[static_cast<size_t>(mb)];
   sl.mb = mb;
   const int N = g.n_atoms, H = kH, R = kR, L = st->m.L;
   const EdgeGeom eg = edge_geom(g);
@@ -838,9 +889,9 @@ void stage_fe(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
       case kReadout: {
         const float *O = P, *o = P + H * H, *om = P + H * H + H, *bias = P + H * H + 2 * H;
         gemm(s, N, cur_h, O, o, nullptr, nullptr, b.p);
-        node::readout_energy_kernel<kH><<<blocks(N, 8), 256, 0, s>>>(N, b.p, om, bias, g.species, sl.e_atom);
-        node::energy_loss_kernel<<<1, 128, 0, s>>>(g.n_struct, g.struct_ptr, sl.e_atom, g.E_target, st->m.w_E, sl.E,
-                                                   sl.eps, sl.loss);
+        node::readout_energy_kernel<kH><<<blocks(N, 8), 256, 0, s>>>(N, b.p, om, bias, g.species, mo.e_atom);
+        node::energy_loss_kernel<<<1, 128, 0, s>>>(g.n_struct, g.struct_ptr, mo.e_atom, g.E_target, st->m.w_E, mo.E,
+                                                   mo.eps, mo.loss);
         break;
       }
     }
@@ -856,21 +907,23 @@ void stage_fe(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
 // ================================================================== FF
 void stage_ff(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
   check_mb_slot(st, mb, slot);
+  if (st->wide) return wide_ff(st, mb, slot, s, lane);
   Scratch& sc = lane_of(st, lane);
   const DevGeo& g = geo_of(st, mb);
   Slot& sl = st->slots[static_cast<size_t>(slot)];
+  MbOut& mo = st->outs[static_cast<size_t>(mb)];
   const int N = g.n_atoms, H = kH, R = kR, L = st->m.L;
   const size_t NH = static_cast<size_t>(N) * H;
   const EdgeGeom eg = edge_geom(g);
   float* wh = sc.wh;
   float* wm = sc.wm;
   if (st->has_readout) {
-    JANUS_CUDA(cudaMemsetAsync(sl.F, 0, sizeof(float) * 3 * N, s));
+    JANUS_CUDA(cudaMemsetAsync(mo.F, 0, sizeof(float) * 3 * N, s));
   } else {
     const Port& in = sl.ports[JANUS_PORT_ADJ_IN];
     copy(s, wh, port_h(in, N), NH);
     if (in.has_m) copy(s, wm, port_m(in, N), NH);
-    copy(s, sl.F, port_v(in, N), 3 * static_cast<size_t>(N));
+    copy(s, mo.F, port_v(in, N), 3 * static_cast<size_t>(N));
   }
   for (int u = st->u1 - 1; u >= st->u0; --u) {
     UnitBufs& b = sl.units[static_cast<size_t>(u - st->u0)];
@@ -894,13 +947,13 @@ void stage_ff(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
           if (!(prof_skip() & 2))
             JANUS_ROWS(msg_ff_rows, blocks(N, 8), s, N, g.row_ptr, g.col, g.pidx, g.u, b.wf, b.wfp, b.v, b.ff_a,
                                                                msg_params(st, u).pack + edge_tc::kWtOff / sizeof(float),
-                                                               b.ff_Y, sl.F, wh);
+                                                               b.ff_Y, mo.F, wh);
         } else if (g.n_tiles > 0 && use_tc(st)) {  // a_h += Y W^T fused into the tile epilogue
           if (!(prof_skip() & 2)) edge_tc::msg_ff_tc<<<fe_grid(st, g), edge_tc::NT, edge_tc::ff_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, msg_params(st, u),
-                                                                                 st->m.r_c, b.v, b.ff_a, b.ff_Y, sl.F, wh);
+                                                                                 st->m.r_c, b.v, b.ff_a, b.ff_Y, mo.F, wh);
         } else {
           if (g.n_tiles > 0)
-            edge::msg_ff_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::ff_smem<kH, kR>(), s>>>(eg, msg_params(st, u), st->m.r_c, b.v, b.ff_a, b.ff_Y, sl.F);
+            edge::msg_ff_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::ff_smem<kH, kR>(), s>>>(eg, msg_params(st, u), st->m.r_c, b.v, b.ff_a, b.ff_Y, mo.F);
           else
             JANUS_CUDA(cudaMemsetAsync(b.ff_Y, 0, sizeof(float) * NH, s));
           gemm(s, N, b.ff_Y, T + H * H, nullptr, wh, nullptr, wh);  // a_h += Y W^T
@@ -917,9 +970,9 @@ void stage_ff(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
     const Port& out = sl.ports[JANUS_PORT_ADJ_OUT];
     copy(s, port_h(out, N), wh, NH);
     if (out.has_m) copy(s, port_m(out, N), wm, NH);
-    copy(s, port_v(out, N), sl.F, 3 * static_cast<size_t>(N));
+    copy(s, port_v(out, N), mo.F, 3 * static_cast<size_t>(N));
   } else {  // forces complete on stage 0: L_F seed
-    node::force_loss_kernel<<<1, 1024, 0, s>>>(3 * N, sl.F, g.F_target, st->m.w_F, sl.Fbar, sl.loss + 1);
+    node::force_loss_kernel<<<1, 1024, 0, s>>>(3 * N, mo.F, g.F_target, st->m.w_F, mo.Fbar, mo.loss + 1);
     JANUS_LAUNCH_CHECK("force_loss");
   }
 }
@@ -927,15 +980,17 @@ void stage_ff(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
 // ================================================================== BF
 void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
   check_mb_slot(st, mb, slot);
+  if (st->wide) return wide_bf(st, mb, slot, s, lane);
   Scratch& sc = lane_of(st, lane);
   const DevGeo& g = geo_of(st, mb);
   Slot& sl = st->slots[static_cast<size_t>(slot)];
+  MbOut& mo = st->outs[static_cast<size_t>(mb)];
   const int N = g.n_atoms, H = kH, R = kR, L = st->m.L;
   const size_t NH = static_cast<size_t>(N) * H;
   const EdgeGeom eg = edge_geom(g);
   float* ah = sc.wh;
   float* am = sc.wm;
-  const float* Fbar = sl.Fbar;
+  const float* Fbar = mo.Fbar;
   JANUS_CUDA(cudaMemsetAsync(st->g2 + static_cast<size_t>(mb) * st->n_params, 0, sizeof(float) * st->n_params, s));
   if (st->u0 == 0) {
     JANUS_CUDA(cudaMemsetAsync(ah, 0, sizeof(float) * NH, s));
@@ -1055,9 +1110,11 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
 // ================================================================== BE
 void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only, int lane) {
   check_mb_slot(st, mb, slot);
+  if (st->wide) return wide_be(st, mb, slot, s, inj_only, lane);
   Scratch& sc = lane_of(st, lane);
   const DevGeo& g = geo_of(st, mb);
   Slot& sl = st->slots[static_cast<size_t>(slot)];
+  MbOut& mo = st->outs[static_cast<size_t>(mb)];
   const int N = g.n_atoms, H = kH, R = kR, L = st->m.L;
   const size_t NH = static_cast<size_t>(N) * H;
   const EdgeGeom eg = edge_geom(g);
@@ -1095,11 +1152,11 @@ void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only, 
         }
         const float* om = P + H * H + H;
         float *dO = G1, *dob = G1 + H * H, *dom = G1 + H * H + H, *dbias = G1 + H * H + 2 * H;
-        node::ro_be_ew_kernel<kH><<<blocks(NH, 256), 256, 0, s>>>(static_cast<int>(NH), b.p, om, sl.eps, g.struct_id,
+        node::ro_be_ew_kernel<kH><<<blocks(NH, 256), 256, 0, s>>>(static_cast<int>(NH), b.p, om, mo.eps, g.struct_id,
                                                                   sc.s1, sc.s2);
         gemm(s, N, sc.s1, T, nullptr, b.inj, nullptr, bh);  // b_h = tbar O^T + hbar^F
         wjobs(st, sc, s, N, {wjob(in_h(st, sl, u, N), sc.s1, dO, nullptr, nullptr, false, sc.s1, dob, sc.s2, dom)});
-        species_sum(st, sc, s, g, nullptr, sl.eps, dbias);
+        species_sum(st, sc, s, g, nullptr, mo.eps, dbias);
         break;
       }
       case kUpd: {
@@ -1198,7 +1255,7 @@ void stage_optimizer(janus_stage* st, const janus_opt& o, cudaStream_t s, const 
   node::adam_kernel<<<blocks(st->n_params, 256), 256, 0, s>>>(st->n_params, st->params, st->m1, st->m2, st->grad, dhp,
                                                               st->dstep);
   JANUS_LAUNCH_CHECK("adam");
-  refresh_transposes(st, s);
+  if (!st->wide) refresh_transposes(st, s);
 }
 
 void stage_port(janus_stage* st, int mb, int slot, int port, void** dptr, size_t* bytes) {
@@ -1252,8 +1309,10 @@ double edge_kernel_flops_per_edge(int which, int H, int R) {
 // lane `lane`: step_grid = the grid the step uses (tiles per CTA), else one
 // tile per CTA on the full grid.  Inputs must exist (run the step first).
 void launch_edge_kernel(janus_stage* st, int u, int which, int mb, int slot, int lane, cudaStream_t s, bool step_grid) {
+  if (st->wide) throw config_error("edge-kernel timing hooks cover the fused H=64 kernels only");
   const DevGeo& g = geo_of(st, mb);
   Slot& sl = st->slots[static_cast<size_t>(slot)];
+  MbOut& mo = st->outs[static_cast<size_t>(mb)];
   UnitBufs& b = sl.units[static_cast<size_t>(u - st->u0)];
   const EdgeGeom eg = edge_geom(g);
   const MsgParams mp = msg_params(st, u);
@@ -1275,7 +1334,7 @@ void launch_edge_kernel(janus_stage* st, int u, int which, int mb, int slot, int
     const float* wt = mp.pack + edge_tc::kWtOff / sizeof(float);
     if (which == 4 && g.n_pairs > 0)
       edge_tc::msg_bf_pair_tc<<<grid, edge_tc::NT, edge_tc::bf_pair_smem(), s>>>(eg, g.pgeo, g.n_pairs, mp, st->m.r_c, b.v, sc.s1,
-                                                                                 b.ff_a, sl.Fbar, sc.partial);
+                                                                                 b.ff_a, mo.Fbar, sc.partial);
     if (which == 5 && g.n_pairs > 0)
       edge_tc::msg_be_pair_tc<<<grid, edge_tc::NT, edge_tc::be_pair_smem(), s>>>(eg, g.pgeo, g.n_pairs, mp, st->m.r_c, b.v, sc.s2,
                                                                                  sc.partial);
@@ -1283,8 +1342,8 @@ void launch_edge_kernel(janus_stage* st, int u, int which, int mb, int slot, int
     if (which == 2) {
       if (g.n_pairs > 0)
         edge_tc::msg_bf_pair_tc<<<grid, edge_tc::NT, edge_tc::bf_pair_smem(), s>>>(eg, g.pgeo, g.n_pairs, mp, st->m.r_c, b.v, sc.s1,
-                                                                                   b.ff_a, sl.Fbar, sc.partial);
-      JANUS_ROWS(msg_bf_rows, blocks(N, 8), s, N, g.row_ptr, g.col, g.pidx, g.u, sl.Fbar, b.wf, b.wfp, b.v, sc.s1, b.ff_a, wt,
+                                                                                   b.ff_a, mo.Fbar, sc.partial);
+      JANUS_ROWS(msg_bf_rows, blocks(N, 8), s, N, g.row_ptr, g.col, g.pidx, g.u, mo.Fbar, b.wf, b.wfp, b.v, sc.s1, b.ff_a, wt,
                                                          sc.s3, sc.s4, nullptr, edge_tc::PartialReduce{});
     } else {
       if (g.n_pairs > 0)
@@ -1307,7 +1366,7 @@ void launch_edge_kernel(janus_stage* st, int u, int which, int mb, int slot, int
         break;
       case 2:
         edge_tc::msg_bf_tc<<<grid, edge_tc::NT, edge_tc::bf_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, sc.s1, b.ff_a,
-                                                                        sl.Fbar, sc.s3, sc.s4, sc.partial, nullptr);
+                                                                        mo.Fbar, sc.s3, sc.s4, sc.partial, nullptr);
         break;
       default:
         edge_tc::msg_be_tc<<<grid, edge_tc::NT, edge_tc::be_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, sc.s2, sc.s3, sc.partial, nullptr, nullptr);
@@ -1324,7 +1383,7 @@ void launch_edge_kernel(janus_stage* st, int u, int which, int mb, int slot, int
       break;
     case 2:
       edge::msg_bf_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::bf_smem<kH, kR>(), s>>>(eg, mp, st->m.r_c, b.v, sc.s1, b.ff_a,
-                                                                                     sl.Fbar, sc.s3, sc.s4, sc.partial);
+                                                                                     mo.Fbar, sc.s3, sc.s4, sc.partial);
       break;
     default:
       edge::msg_be_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::be_smem<kH, kR>(), s>>>(eg, mp, st->m.r_c, b.v, sc.s2, sc.s3, sc.partial);
@@ -1380,7 +1439,7 @@ void stage_time_edge_kernel(janus_stage* st, int which, int mb, int slot, int it
     auto round = [&] {
       JANUS_CUDA(cudaEventRecord(ev[0], s));
       for (int l = 0; l < L; ++l) JANUS_CUDA(cudaStreamWaitEvent(ls[static_cast<size_t>(l)], ev[0], 0));
-      for (int m = 0; m < n_mb; ++m) launch_edge_kernel(st, u, which, m, m, m % L, ls[static_cast<size_t>(m % L)], true);
+      for (int m = 0; m < n_mb; ++m) launch_edge_kernel(st, u, which, m, m % static_cast<int>(st->slots.size()), m % L, ls[static_cast<size_t>(m % L)], true);
       for (int l = 0; l < L; ++l) {
         JANUS_CUDA(cudaEventRecord(ev[static_cast<size_t>(l) + 1], ls[static_cast<size_t>(l)]));
         JANUS_CUDA(cudaStreamWaitEvent(s, ev[static_cast<size_t>(l) + 1], 0));
@@ -1413,19 +1472,19 @@ int stage_slot_of_mb(const janus_stage* st, int mb) {
 
 void stage_energy(janus_stage* st, int mb, float* E_host, float* loss_E, cudaStream_t s) {
   if (!st->has_readout) throw state_error("energies live on the stage holding the readout unit");
-  const Slot& sl = st->slots[static_cast<size_t>(stage_slot_of_mb(st, mb))];
+  const MbOut& mo = st->outs[static_cast<size_t>(mb)];
   const int ns = geo_of(st, mb).n_struct;
-  if (E_host) JANUS_CUDA(cudaMemcpyAsync(E_host, sl.E, sizeof(float) * ns, cudaMemcpyDeviceToHost, s));
-  if (loss_E) JANUS_CUDA(cudaMemcpyAsync(loss_E, sl.loss, sizeof(float), cudaMemcpyDeviceToHost, s));
+  if (E_host) JANUS_CUDA(cudaMemcpyAsync(E_host, mo.E, sizeof(float) * ns, cudaMemcpyDeviceToHost, s));
+  if (loss_E) JANUS_CUDA(cudaMemcpyAsync(loss_E, mo.loss, sizeof(float), cudaMemcpyDeviceToHost, s));
   JANUS_CUDA(cudaStreamSynchronize(s));
 }
 
 void stage_forces(janus_stage* st, int mb, float* F_host, float* loss_F, cudaStream_t s) {
   if (!st->has_embed) throw state_error("complete forces live on stage 0");
-  const Slot& sl = st->slots[static_cast<size_t>(stage_slot_of_mb(st, mb))];
+  const MbOut& mo = st->outs[static_cast<size_t>(mb)];
   const int n = geo_of(st, mb).n_atoms;
-  if (F_host) JANUS_CUDA(cudaMemcpyAsync(F_host, sl.F, sizeof(float) * 3 * n, cudaMemcpyDeviceToHost, s));
-  if (loss_F) JANUS_CUDA(cudaMemcpyAsync(loss_F, sl.loss + 1, sizeof(float), cudaMemcpyDeviceToHost, s));
+  if (F_host) JANUS_CUDA(cudaMemcpyAsync(F_host, mo.F, sizeof(float) * 3 * n, cudaMemcpyDeviceToHost, s));
+  if (loss_F) JANUS_CUDA(cudaMemcpyAsync(loss_F, mo.loss + 1, sizeof(float), cudaMemcpyDeviceToHost, s));
   JANUS_CUDA(cudaStreamSynchronize(s));
 }
 

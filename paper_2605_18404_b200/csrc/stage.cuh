@@ -76,6 +76,7 @@ struct UnitBufs {  // per slot, per unit
 struct Port {
   float* buf = nullptr;  // [h | m | vec3] packed for the actual n_atoms
   bool has_m = false, has_vec = false;
+  int H = 64;            // row width of h / m
 };
 
 // Per-lane scratch: phases of different micro-batches may run concurrently on
@@ -84,18 +85,27 @@ struct Scratch {
   float *wh = nullptr, *wh2 = nullptr, *wm = nullptr, *s1 = nullptr, *s2 = nullptr, *s3 = nullptr, *s4 = nullptr, *s5 = nullptr;
   float *partial = nullptr, *wpart = nullptr;
   unsigned* counter = nullptr;  // last-CTA-reduces launch counter (one launch at a time per lane)
+  // generic-width path (stage_wide.inc): [2 pairs][R] basis stack, three
+  // [2 pairs][H] operand stacks, and the lane's cuBLAS handle + workspace
+  float *phi2 = nullptr, *z2 = nullptr, *a2 = nullptr, *b2 = nullptr;
+  void* blas = nullptr;
+  void* blas_ws = nullptr;
 };
 
 struct Slot {
   std::vector<UnitBufs> units;
   Port ports[8];
+  int mb = -1;             // latest occupant
+};
+
+// Per-micro-batch outputs (not pooled: small, and read back after the step)
+struct MbOut {
   float* F = nullptr;      // running force [N*3]
   float* Fbar = nullptr;   // stage 0: force-loss seed
   float* e_atom = nullptr; // readout per-atom energies
   float* E = nullptr;      // [n_struct]
   float* eps = nullptr;    // [n_struct]
   float* loss = nullptr;   // [2] loss_E, loss_F
-  int mb = -1;
 };
 
 }  // namespace janus
@@ -118,13 +128,15 @@ struct janus_stage {
   // (a step in flight keeps reading its own copy)
   std::vector<janus::DevGeo> geo;
   std::vector<int> gpar;
-  std::vector<janus::Slot> slots;
+  std::vector<janus::Slot> slots;   // activation slot pool (n_slots; include/janus/slots.hpp)
+  std::vector<janus::MbOut> outs;   // per micro-batch outputs
   std::vector<janus::Scratch> lanes;
-  float* losses = nullptr;  // [n_slots][2] loss_E, loss_F (slot.loss points here)
+  float* losses = nullptr;  // [n_mb][2] loss_E, loss_F (outs[mb].loss points here)
   std::vector<void*> allocs;
   std::vector<void*> host_allocs;  // pinned (cudaHostAlloc)
   janus::LoadLayout lay;           // upload block layout (capacity offsets)
-  int64_t static_bytes = 0, arena_bytes = 0;
+  int64_t static_bytes = 0, arena_bytes = 0;  // parameters / optimizer / ledgers; everything else
+  int64_t pool_bytes = 0;                     // of arena_bytes: the activation slot pool
   int tpc_fe = 1, tpc_wg = 1;        // TC edge tiles per CTA: FE/FF, BF/BE (stage_create)
   int tpc_filter = 1;                // pair mode: 128-pair chunks per filter CTA
   int tc_tile_edges = 0;             // TC tiles: 0 cost-chosen runs, > 0 greedy edge budget (tuning)
@@ -136,6 +148,8 @@ struct janus_stage {
   int* pair_counts = nullptr;      // pair tables: canonical edges per (job, 1024-edge chunk)
   int pair_chunks_cap = 0;
   janus::LmBuilder* lm = nullptr;  // device neighbour-list builder (lazy, janus_stage_load without a CSR)
+  bool wide = false;               // generic-width phases (stage_wide.inc) instead of the fused H=64 kernels
+  float* ones = nullptr;           // wide: ones vector (column sums as GEMMs)
 
   float* P(int u) const { return params + uoff[static_cast<size_t>(u - u0)]; }
 

@@ -1,0 +1,409 @@
+// wide.cuh — device kernels of the generic-width stage path (any hidden width
+// H = 32·V, V in {2, 4, 8}; any basis size R): configs[2]'s deep model (L=32,
+// H=256) and the cross-check of the fused H=64 kernels.
+//
+// The fused H=64 kernels (pair_tc.cuh, edge_tc.cuh) keep a whole 128-pair
+// filter chain in shared memory and TMEM.  At H=256 a chunk's B alone is
+// 256 KB, so this path splits every phase at its contractions instead:
+//   * per-pair contractions of a 128..27k-pair batch are dense GEMMs on
+//     stacked operands ([phi; phi'] A, [s; sdot] B, [mu; nu] B^T, and the
+//     weight gradients [s; sdot]^T [mu; nu], [phi; phi']^T [zbar; zbar'] with
+//     K = 2 x pairs), issued through the stage's GEMM seam (stage_wide.inc);
+//   * everything between them is one streaming elementwise kernel per step
+//     (coalesced, one pass over [pairs x H]);
+//   * the CSR gathers / scatters (m, Y, X, mdot, Y_b, forces) are warp-per-row
+//     kernels: lane l owns features [l V, l V + V) of every row, so each edge
+//     moves whole node rows in single coalesced 32 x V-float transactions, and
+//     the per-edge force scalars are warp reductions (fixed order).
+// Math: oracle/mlip_oracle.c (the same definitions), pair form as DESIGN §3.0.
+#pragma once
+
+#include "common.cuh"
+
+namespace janus {
+namespace wide {
+
+using dev::d2silu;
+using dev::dsilu;
+using dev::silu;
+
+template <int V>
+__device__ __forceinline__ void ldv(const float* __restrict__ p, float (&x)[V]) {
+  if constexpr (V % 4 == 0) {
+#pragma unroll
+    for (int q = 0; q < V / 4; ++q) {
+      const float4 t = __ldg(reinterpret_cast<const float4*>(p) + q);
+      x[4 * q] = t.x;
+      x[4 * q + 1] = t.y;
+      x[4 * q + 2] = t.z;
+      x[4 * q + 3] = t.w;
+    }
+  } else if constexpr (V == 2) {
+    const float2 t = __ldg(reinterpret_cast<const float2*>(p));
+    x[0] = t.x;
+    x[1] = t.y;
+  } else {
+#pragma unroll
+    for (int q = 0; q < V; ++q) x[q] = __ldg(p + q);
+  }
+}
+
+template <int V>
+__device__ __forceinline__ void stv(float* __restrict__ p, const float (&x)[V]) {
+  if constexpr (V % 4 == 0) {
+#pragma unroll
+    for (int q = 0; q < V / 4; ++q)
+      reinterpret_cast<float4*>(p)[q] = make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
+  } else if constexpr (V == 2) {
+    *reinterpret_cast<float2*>(p) = make_float2(x[0], x[1]);
+  } else {
+#pragma unroll
+    for (int q = 0; q < V; ++q) p[q] = x[q];
+  }
+}
+
+struct PairRec {  // pgeo (pair_tc.cuh pairs_kernel): (d, c, c', i | u, j) of the canonical edge
+  float d, c, dc, ux, uy, uz;
+  int i, j;
+};
+__device__ __forceinline__ PairRec pair_rec(const float4* __restrict__ pgeo, int p) {
+  const float4 a = __ldg(pgeo + 2 * p), b = __ldg(pgeo + 2 * p + 1);
+  return PairRec{a.x, a.y, a.z, b.x, b.y, b.z, __float_as_int(a.w), __float_as_int(b.w)};
+}
+
+// ---------------------------------------------------------------- pairs
+// phi2 = [phi; phi'] [2 P][R] (Gaussian basis of the pair length and its d/dd)
+__global__ void basis2_kernel(int P, int R, const float4* __restrict__ pgeo, float rc, float* __restrict__ phi2) {
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x >= static_cast<int64_t>(P) * R) return;
+  const int p = static_cast<int>(x / R), k = static_cast<int>(x % R);
+  const float d = __ldg(pgeo + 2 * p).x;
+  const float delta = rc / (R - 1);
+  const float gamma = 1.0f / (2.0f * delta * delta);
+  const float t = d - k * delta;
+  const float e = expf(-gamma * t * t);
+  phi2[x] = e;
+  phi2[static_cast<int64_t>(P) * R + x] = -2.0f * gamma * t * e;
+}
+
+// FE / BF: z2 = [phi A; phi' A] -> a2 = [s; sdot] = [SiLU(z + alpha); SiLU'(z + alpha) z']
+__global__ void act2_kernel(int64_t PH, int H, const float* __restrict__ z2, const float* __restrict__ alpha,
+                            float* __restrict__ a2) {
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x >= PH) return;
+  const float z = z2[x] + __ldg(alpha + x % H), zp = z2[PH + x];
+  a2[x] = silu(z);
+  a2[PH + x] = dsilu(z) * zp;
+}
+
+// BE: a = SiLU(z + alpha) (first half only)
+__global__ void act1_kernel(int64_t PH, int H, const float* __restrict__ z, const float* __restrict__ alpha,
+                            float* __restrict__ a) {
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x >= PH) return;
+  a[x] = silu(z[x] + __ldg(alpha + x % H));
+}
+
+// FE: g2 = [s B; sdot B] -> w = c (g + beta), w' = c' (g + beta) + c g'
+__global__ void filter_out_kernel(int64_t PH, int H, const float* __restrict__ g2, const float* __restrict__ beta,
+                                  const float4* __restrict__ pgeo, float* __restrict__ wf, float* __restrict__ wfp) {
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x >= PH) return;
+  const float4 r = __ldg(pgeo + 2 * (x / H));
+  const float g = g2[x] + __ldg(beta + x % H), gp = g2[PH + x];
+  wf[x] = r.y * g;
+  wfp[x] = r.z * g + r.y * gp;
+}
+
+// BF per pair (warp per pair): rho = a_m[i] v_j + a_m[j] v_i, kappa = a_m[i] vdot_j + a_m[j] vdot_i,
+// qbar = <Fbar_i - Fbar_j, u>, mu = qbar c' rho + c kappa, nu = qbar c rho -> mn = [mu; nu]
+template <int V>
+__global__ void __launch_bounds__(256) bf_pair_kernel(int P, const float4* __restrict__ pgeo,
+                                                      const float* __restrict__ am, const float* __restrict__ v,
+                                                      const float* __restrict__ vd, const float* __restrict__ Fbar,
+                                                      float* __restrict__ mn) {
+  constexpr int H = 32 * V;
+  const int p = static_cast<int>((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5), l = threadIdx.x & 31;
+  if (p >= P) return;
+  const PairRec r = pair_rec(pgeo, p);
+  const float qb = (__ldg(Fbar + 3 * r.i) - __ldg(Fbar + 3 * r.j)) * r.ux +
+                   (__ldg(Fbar + 3 * r.i + 1) - __ldg(Fbar + 3 * r.j + 1)) * r.uy +
+                   (__ldg(Fbar + 3 * r.i + 2) - __ldg(Fbar + 3 * r.j + 2)) * r.uz;
+  float ai[V], aj[V], vi[V], vj[V], di[V], dj[V];
+  const size_t oi = static_cast<size_t>(r.i) * H + l * V, oj = static_cast<size_t>(r.j) * H + l * V;
+  ldv<V>(am + oi, ai);
+  ldv<V>(am + oj, aj);
+  ldv<V>(v + oi, vi);
+  ldv<V>(v + oj, vj);
+  ldv<V>(vd + oi, di);
+  ldv<V>(vd + oj, dj);
+  float mu[V], nu[V];
+#pragma unroll
+  for (int q = 0; q < V; ++q) {
+    const float rho = ai[q] * vj[q] + aj[q] * vi[q];
+    const float kap = ai[q] * dj[q] + aj[q] * di[q];
+    mu[q] = qb * r.dc * rho + r.c * kap;
+    nu[q] = qb * r.c * rho;
+  }
+  const size_t o = static_cast<size_t>(p) * H + l * V;
+  stv<V>(mn + o, mu);
+  stv<V>(mn + static_cast<size_t>(P) * H + o, nu);
+}
+
+// BF: sb2 = [sbar; sdotbar] = [mu B^T; nu B^T], z2 = raw [phi A; phi' A] ->
+// zb2 = [zbar; zbar'] = [sbar SiLU'(z) + sdotbar SiLU''(z) z'; sdotbar SiLU'(z)]
+__global__ void bf_zbar_kernel(int64_t PH, int H, const float* __restrict__ sb2, const float* __restrict__ z2,
+                               const float* __restrict__ alpha, float* __restrict__ zb2) {
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x >= PH) return;
+  const float z = z2[x] + __ldg(alpha + x % H), zp = z2[PH + x];
+  const float sb = sb2[x], sdb = sb2[PH + x], ds = dsilu(z);
+  zb2[x] = sb * ds + sdb * d2silu(z) * zp;
+  zb2[PH + x] = sdb * ds;
+}
+
+// BE per pair (warp per pair): gbar = c (b_m[i] v_j + b_m[j] v_i)
+template <int V>
+__global__ void __launch_bounds__(256) be_pair_kernel(int P, const float4* __restrict__ pgeo,
+                                                      const float* __restrict__ bm, const float* __restrict__ v,
+                                                      float* __restrict__ gbar) {
+  constexpr int H = 32 * V;
+  const int p = static_cast<int>((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5), l = threadIdx.x & 31;
+  if (p >= P) return;
+  const PairRec r = pair_rec(pgeo, p);
+  float bi[V], bj[V], vi[V], vj[V], o[V];
+  const size_t oi = static_cast<size_t>(r.i) * H + l * V, oj = static_cast<size_t>(r.j) * H + l * V;
+  ldv<V>(bm + oi, bi);
+  ldv<V>(bm + oj, bj);
+  ldv<V>(v + oi, vi);
+  ldv<V>(v + oj, vj);
+#pragma unroll
+  for (int q = 0; q < V; ++q) o[q] = r.c * (bi[q] * vj[q] + bj[q] * vi[q]);
+  stv<V>(gbar + static_cast<size_t>(p) * H + l * V, o);
+}
+
+// BE: zbar = sbar SiLU'(z + alpha)  (in place on sbar)
+__global__ void be_zbar_kernel(int64_t PH, int H, float* __restrict__ sb, const float* __restrict__ z,
+                               const float* __restrict__ alpha) {
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x >= PH) return;
+  sb[x] *= dsilu(z[x] + __ldg(alpha + x % H));
+}
+
+// ------------------------------------------------------------ row kernels
+// warp per CSR row i (receiver); lane l owns features [l V, l V + V)
+// FE: m_i = sum_e w_p(e) v_j  (BE: Y_b,i = sum_e w_p b_m[j])
+template <int V>
+__global__ void __launch_bounds__(256) fe_rows_kernel(int N, const int* __restrict__ row_ptr, const int* __restrict__ col,
+                                                      const int* __restrict__ pidx, const float* __restrict__ wf,
+                                                      const float* __restrict__ v, float* __restrict__ m) {
+  constexpr int H = 32 * V;
+  const int i = static_cast<int>((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5), l = threadIdx.x & 31;
+  if (i >= N) return;
+  float acc[V] = {};
+  const int e1 = __ldg(row_ptr + i + 1);
+#pragma unroll 2
+  for (int e = __ldg(row_ptr + i); e < e1; ++e) {
+    float w[V], x[V];
+    ldv<V>(wf + static_cast<size_t>(__ldg(pidx + e)) * H + l * V, w);
+    ldv<V>(v + static_cast<size_t>(__ldg(col + e)) * H + l * V, x);
+#pragma unroll
+    for (int q = 0; q < V; ++q) acc[q] += w[q] * x[q];
+  }
+  stv<V>(m + static_cast<size_t>(i) * H + l * V, acc);
+}
+
+// FF: Y_i = sum_e w_p a_m[j];  F_i += sum_e <a_m[i] v_j + a_m[j] v_i, w'_p> u_e
+template <int V>
+__global__ void __launch_bounds__(256) ff_rows_kernel(int N, const int* __restrict__ row_ptr, const int* __restrict__ col,
+                                                      const int* __restrict__ pidx, const float* __restrict__ u,
+                                                      const float* __restrict__ wf, const float* __restrict__ wfp,
+                                                      const float* __restrict__ v, const float* __restrict__ am,
+                                                      float* __restrict__ Y, float* __restrict__ F) {
+  constexpr int H = 32 * V;
+  const int i = static_cast<int>((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5), l = threadIdx.x & 31;
+  if (i >= N) return;
+  float ai[V], vi[V], acc[V] = {};
+  ldv<V>(am + static_cast<size_t>(i) * H + l * V, ai);
+  ldv<V>(v + static_cast<size_t>(i) * H + l * V, vi);
+  float fx = 0.f, fy = 0.f, fz = 0.f;
+  const int e1 = __ldg(row_ptr + i + 1);
+#pragma unroll 2
+  for (int e = __ldg(row_ptr + i); e < e1; ++e) {
+    const size_t op = static_cast<size_t>(__ldg(pidx + e)) * H + l * V, oj = static_cast<size_t>(__ldg(col + e)) * H + l * V;
+    float w[V], wp[V], aj[V], vj[V];
+    ldv<V>(wf + op, w);
+    ldv<V>(wfp + op, wp);
+    ldv<V>(am + oj, aj);
+    ldv<V>(v + oj, vj);
+    float q = 0.f;
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      acc[k] += w[k] * aj[k];
+      q += (ai[k] * vj[k] + aj[k] * vi[k]) * wp[k];
+    }
+    q = dev::warp_sum(q);
+    fx += q * __ldg(u + 3 * e);
+    fy += q * __ldg(u + 3 * e + 1);
+    fz += q * __ldg(u + 3 * e + 2);
+  }
+  stv<V>(Y + static_cast<size_t>(i) * H + l * V, acc);
+  if (l == 0) {
+    F[3 * i] += fx;
+    F[3 * i + 1] += fy;
+    F[3 * i + 2] += fz;
+  }
+}
+
+// BF: mdot_i = sum_e qbar_e w'_p v_j + w_p vdot_j;  X_i = sum_e qbar_e w'_p a_m[j]
+template <int V>
+__global__ void __launch_bounds__(256) bf_rows_kernel(int N, const int* __restrict__ row_ptr, const int* __restrict__ col,
+                                                      const int* __restrict__ pidx, const float* __restrict__ u,
+                                                      const float* __restrict__ Fbar, const float* __restrict__ wf,
+                                                      const float* __restrict__ wfp, const float* __restrict__ v,
+                                                      const float* __restrict__ vd, const float* __restrict__ am,
+                                                      float* __restrict__ mdot, float* __restrict__ X) {
+  constexpr int H = 32 * V;
+  const int i = static_cast<int>((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5), l = threadIdx.x & 31;
+  if (i >= N) return;
+  float md[V] = {}, xs[V] = {};
+  const float fix = __ldg(Fbar + 3 * i), fiy = __ldg(Fbar + 3 * i + 1), fiz = __ldg(Fbar + 3 * i + 2);
+  const int e1 = __ldg(row_ptr + i + 1);
+#pragma unroll 2
+  for (int e = __ldg(row_ptr + i); e < e1; ++e) {
+    const int j = __ldg(col + e);
+    const float qb = (fix - __ldg(Fbar + 3 * j)) * __ldg(u + 3 * e) + (fiy - __ldg(Fbar + 3 * j + 1)) * __ldg(u + 3 * e + 1) +
+                     (fiz - __ldg(Fbar + 3 * j + 2)) * __ldg(u + 3 * e + 2);
+    const size_t op = static_cast<size_t>(__ldg(pidx + e)) * H + l * V, oj = static_cast<size_t>(j) * H + l * V;
+    float w[V], wp[V], vj[V], dj[V], aj[V];
+    ldv<V>(wf + op, w);
+    ldv<V>(wfp + op, wp);
+    ldv<V>(v + oj, vj);
+    ldv<V>(vd + oj, dj);
+    ldv<V>(am + oj, aj);
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      md[k] += qb * wp[k] * vj[k] + w[k] * dj[k];
+      xs[k] += qb * wp[k] * aj[k];
+    }
+  }
+  stv<V>(mdot + static_cast<size_t>(i) * H + l * V, md);
+  stv<V>(X + static_cast<size_t>(i) * H + l * V, xs);
+}
+
+// (BE's Y_b,i = sum_e w_p b_m[j] is fe_rows_kernel with x = b_m)
+
+// ------------------------------------------------------------- node kernels
+__global__ void embed_kernel(int64_t NH, int H, const int* __restrict__ species, const float* __restrict__ Emb,
+                             float* __restrict__ h) {
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x < NH) h[x] = __ldg(Emb + static_cast<int64_t>(__ldg(species + x / H)) * H + x % H);
+}
+
+// p += bias (per column); sp = SiLU(p)
+__global__ void bias_silu_kernel(int64_t NH, int H, float* __restrict__ p, const float* __restrict__ bias,
+                                 float* __restrict__ sp) {
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x >= NH) return;
+  const float y = p[x] + __ldg(bias + x % H);
+  p[x] = y;
+  if (sp) sp[x] = silu(y);
+}
+
+// x *= SiLU'(p)
+__global__ void mul_dsilu_kernel(int64_t NH, float* __restrict__ x, const float* __restrict__ p) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < NH) x[i] *= dsilu(p[i]);
+}
+
+// BF upd: pb = r pdot SiLU''(p), pdb = r SiLU'(p), spd = SiLU'(p) pdot
+__global__ void bf_upd_ew_kernel(int64_t NH, const float* __restrict__ r, const float* __restrict__ pdot,
+                                 const float* __restrict__ p, float* __restrict__ pb, float* __restrict__ pdb,
+                                 float* __restrict__ spd) {
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x >= NH) return;
+  const float pp = p[x], pd = pdot[x], rr = r[x], ds = dsilu(pp);
+  pb[x] = rr * pd * d2silu(pp);
+  pdb[x] = rr * ds;
+  spd[x] = ds * pd;
+}
+
+// BE upd: pb = r SiLU'(p), sp = SiLU(p)
+__global__ void be_upd_ew_kernel(int64_t NH, const float* __restrict__ r, const float* __restrict__ p,
+                                 float* __restrict__ pb, float* __restrict__ sp) {
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x >= NH) return;
+  const float pp = p[x];
+  pb[x] = r[x] * dsilu(pp);
+  sp[x] = silu(pp);
+}
+
+// readout FE (warp per atom): t += o; e_i = bias[Z_i] + sum_k SiLU(t_k) omega_k (fixed-order warp sum)
+__global__ void ro_fe_kernel(int N, int H, float* __restrict__ t, const float* __restrict__ o,
+                             const float* __restrict__ om, const float* __restrict__ bias,
+                             const int* __restrict__ species, float* __restrict__ e_atom) {
+  const int i = static_cast<int>((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5), l = threadIdx.x & 31;
+  if (i >= N) return;
+  float acc = 0.f;
+  for (int k = l; k < H; k += 32) {
+    const float y = t[static_cast<size_t>(i) * H + k] + __ldg(o + k);
+    t[static_cast<size_t>(i) * H + k] = y;
+    acc += silu(y) * __ldg(om + k);
+  }
+  acc = dev::warp_sum(acc);
+  if (l == 0) e_atom[i] = acc + __ldg(bias + __ldg(species + i));
+}
+
+// readout FF: out = SiLU'(t) omega
+__global__ void ro_ff_ew_kernel(int64_t NH, int H, const float* __restrict__ t, const float* __restrict__ om,
+                                float* __restrict__ out) {
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x < NH) out[x] = dsilu(t[x]) * __ldg(om + x % H);
+}
+
+// readout BF: x1 = tdot SiLU'(t) (-> domega), tau = tdot omega SiLU''(t), y = SiLU'(t) omega
+__global__ void ro_bf_ew_kernel(int64_t NH, int H, const float* __restrict__ tdot, const float* __restrict__ t,
+                                const float* __restrict__ om, float* __restrict__ x1, float* __restrict__ tau,
+                                float* __restrict__ y) {
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x >= NH) return;
+  const float tt = t[x], td = tdot[x], w = __ldg(om + x % H), ds = dsilu(tt);
+  x1[x] = td * ds;
+  tau[x] = td * w * d2silu(tt);
+  y[x] = ds * w;
+}
+
+// readout BE: tb = eps_s SiLU'(t) omega, x2 = eps_s SiLU(t)
+__global__ void ro_be_ew_kernel(int64_t NH, int H, const float* __restrict__ t, const float* __restrict__ om,
+                                const float* __restrict__ eps, const int* __restrict__ struct_id,
+                                float* __restrict__ tb, float* __restrict__ x2) {
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x >= NH) return;
+  const float ep = __ldg(eps + __ldg(struct_id + x / H)), tt = t[x];
+  tb[x] = ep * dsilu(tt) * __ldg(om + x % H);
+  x2[x] = ep * silu(tt);
+}
+
+// out[z][k] += sum_{Z_i = z} x[i][k] (x != null, cols = H) or
+// out[z] += sum_{Z_i = z} eps[s(i)] (x == null, cols = 1); atoms in order
+__global__ void species_sum_kernel(int N, int S, int cols, const int* __restrict__ species, const float* __restrict__ x,
+                                   const float* __restrict__ eps, const int* __restrict__ struct_id,
+                                   float* __restrict__ out) {
+  const int z = blockIdx.y;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (z >= S || k >= cols) return;
+  float acc = 0.f;
+  for (int i = 0; i < N; ++i) {
+    if (__ldg(species + i) != z) continue;
+    acc += x ? x[static_cast<size_t>(i) * cols + k] : __ldg(eps + __ldg(struct_id + i));
+  }
+  out[static_cast<size_t>(z) * cols + k] += acc;
+}
+
+__global__ void fill_kernel(int64_t n, float* __restrict__ p, float v) {
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x < n) p[x] = v;
+}
+
+}  // namespace wide
+}  // namespace janus

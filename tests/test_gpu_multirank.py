@@ -187,10 +187,12 @@ def test_pp_dp_2x2(janus, gpu, method):
     np.testing.assert_allclose(loss, ref_loss, rtol=1e-5)
 
 
-@pytest.mark.parametrize("P,method,k", [(2, 0, 1), (4, 1, 4)])
+@pytest.mark.parametrize("P,method,k", [(2, 0, 1), (2, 1, 2), (2, 2, 1)])
 def test_thread_ranks_bit_identical_to_local(janus, gpu, P, method, k):
     """The same per-rank path with the ranks as threads of one process
-    (Comm.threads: one CUDA context, the ranks' kernels run concurrently)."""
+    (Comm.threads: one CUDA context, the ranks' kernels run concurrently).
+    All ranks' streams share the context's hardware queues, so only P=2 fits
+    (P=4 is refused: test_thread_ranks_share_hardware_queues)."""
     cfg = dict(BASE, P=P, method=method, k=k)
     ranks = run_ranks_threads(cfg)
     ref, ref_loss = run_local(janus, cfg)
@@ -198,6 +200,15 @@ def test_thread_ranks_bit_identical_to_local(janus, gpu, P, method, k):
         assert np.array_equal(gather(ranks, f"params_E{b}"), ref[f"params_E{b}"]), f"block {b} params"
         assert np.array_equal(gather(ranks, f"grads_E{b}"), ref[f"grads_E{b}"]), f"block {b} grads"
     np.testing.assert_allclose(np.sum([r["loss"] for r in ranks], axis=0), ref_loss, rtol=1e-6)
+
+
+def test_thread_ranks_share_hardware_queues(janus, gpu):
+    """Four ranks as threads of one process need more streams than the
+    context's 32 hardware queues: refused at create (a peer-blocked stream
+    would stall the unrelated streams sharing its queue — measured: a hang)."""
+    cfg = dict(BASE, P=4, method=1, k=4)
+    with pytest.raises(AssertionError, match="ranks of this process"):
+        run_ranks_threads(cfg, timeout=60)
 
 
 def test_per_rank_runtime_checks(janus, gpu):

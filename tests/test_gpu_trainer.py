@@ -252,3 +252,33 @@ def test_two_steps_in_flight_bit_identical(janus, data, graphs):
     assert np.array_equal(pa, pb)
     ta.close()
     tb.close()
+
+
+@pytest.mark.parametrize("P,method,k", [(2, 0, 1), (4, 0, 1), (4, 1, 4), (4, 2, 1), (4, 4, 1)])
+def test_slot_pool_folds_memory_bit_identically(janus, data, P, method, k):
+    """The activation arena is a pool sized by the schedule's live
+    micro-batches (include/janus/slots.hpp): fewer slots and
+    bytes than one slot per micro-batch, the predicted slot count per device,
+    and the same bits (reused slots wait for their previous occupant)."""
+    m, params, batches, _, _ = data
+    batches8 = batches + batches
+    res = {}
+    for unfolded in (False, True):
+        t = janus.Trainer(m, params, P, method, len(batches8), k=k, max_atoms=64, max_edges=64 * 120,
+                          unfolded=unfolded)
+        for i, b in enumerate(batches8):
+            t.load(i, b)
+        st = [t.step(lr=1e-3) for _ in range(2)]
+        g = np.concatenate([reduced_grad(janus, t.stage(b)) for b in range(P)])
+        res[unfolded] = (g, t.params(), st[-1], t.schedule_text())
+        t.close()
+    g0, p0, s0, text = res[False]
+    g1, p1, s1, _ = res[True]
+    assert np.array_equal(g0, g1) and np.array_equal(p0, p1)
+    pred = janus.slot_pool(text, onef1b=(method == janus.METHOD_ONEF1B), local=True)
+    assert list(s0.act_slots[:P]) == pred
+    assert all(s1.act_slots[d] == len(batches8) for d in range(P))
+    assert sum(s0.act_bytes[:P]) <= sum(s1.act_bytes[:P])
+    if sum(pred) < P * len(batches8):  # WaveK(k=P) keeps 2P = all 8 micro-batches live
+        assert sum(s0.act_bytes[:P]) < sum(s1.act_bytes[:P])
+        assert max(s0.peak_bytes[:P]) < max(s1.peak_bytes[:P])

@@ -9,7 +9,12 @@ order (lanes = 1), per-instruction CUDA-event timeline.  For each schedule:
     mean phase times (graph.hpp:168 replay, the reference's own model);
   * peak live activation bytes per stage from the SPEC lifetime rule
     (FE activations live FE->BE, FF intermediates FF->BF, BF->BE
-    injections BF->BE) evaluated on the measured timeline, + static bytes.
+    injections BF->BE) evaluated on the measured timeline, + static bytes;
+  * the executor's MEASURED allocation per device: activation slot pool
+    (slots = live micro-batches, include/janus/slots.hpp) and its bytes, next
+    to the unfolded arena (one slot per micro-batch) of the same stages.
+WaveK's list schedule is generated from the SymFold run's measured phase
+means (janus_exec_desc.phase_us), not the paper's ratios.
 Virtual devices share the SMs of one GPU, so measured bubbles include
 contention; the replay column is the schedule's intrinsic bubble.
 Usage: python tools/pipeline_report.py [--out gpurun_out/pipeline_report.json]
@@ -84,9 +89,10 @@ def peak_live(tl, dev, sizes):
     return peak
 
 
-def run(model, params, batches, P, method, k, steps=3, warmup=2):
-    t = J.Trainer(model, params, P, method, len(batches), k=k, max_atoms=batches[0].n_atoms,
-                  max_edges=max(b.n_edges for b in batches) + 64, max_struct=1, timeline=True, lanes=1)
+def run(model, params, batches, P, method, k, steps=3, warmup=2, phase_us=None):
+    kw = dict(k=k, max_atoms=batches[0].n_atoms, max_edges=max(b.n_edges for b in batches) + 64, max_struct=1,
+              lanes=1, phase_us=phase_us)
+    t = J.Trainer(model, params, P, method, len(batches), timeline=True, **kw)
     for i, b in enumerate(batches):
         t.load(i, b)
     for _ in range(warmup):
@@ -115,8 +121,20 @@ def run(model, params, batches, P, method, k, steps=3, warmup=2):
             for q, x in enumerate(activation_bytes(model, int(plan[b][0]), int(plan[b][1]), batches[0].n_atoms)):
                 sizes[q] += x
         peak = peak_live(tl, dv, sizes)
-        mem.append({"device": dv, "static_plus_arena_bytes": int(s.peak_bytes[dv]), "peak_live_activation_bytes": int(peak)})
+        mem.append({"device": dv, "static_plus_arena_bytes": int(s.peak_bytes[dv]), "peak_live_activation_bytes": int(peak),
+                    "activation_slots": int(s.act_slots[dv]), "activation_pool_bytes": int(s.act_bytes[dv])})
+    # the unfolded arena (one slot per micro-batch) of the same stages, for comparison
+    tu = J.Trainer(model, params, P, method, len(batches), unfolded=True, **kw)
+    for i, b in enumerate(batches):
+        tu.load(i, b)
+    su = tu.step()
+    tu.close()
+    for dv in range(P):
+        mem[dv]["unfolded_pool_bytes"] = int(su.act_bytes[dv])
+        mem[dv]["unfolded_static_plus_arena_bytes"] = int(su.peak_bytes[dv])
     out = {"P": P, "method": {0: "symfold", 1: "wavek", 2: "onef1b_2nd", 4: "hanayo_2nd"}[method], "k": k,
+           "wavek_phase_us": list(phase_us) if phase_us else None,
+           "peak_hbm_bytes_max_device": max(m["static_plus_arena_bytes"] for m in mem),
            "makespan_ms": s.makespan_ms, "structures_per_s": len(batches) / (s.makespan_ms / 1e3),
            "bubble_measured": s.bubble_ratio, "busy_ms": [s.busy_ms[d] for d in range(P)],
            "phase_mean_us": {k2: v * 1e3 / 1e3 for k2, v in phase.items()},
@@ -148,12 +166,16 @@ def main():
     batches = [J.synth_batch(model, [256], 0.095, 700 + m) for m in range(args.nmb)]
     rows = []
     for P in [int(x) for x in args.Ps.split(",")]:
-        for method, k in ((J.METHOD_ONEF1B, 1), (J.METHOD_HANAYO, 1), (J.METHOD_SYMFOLD, 1), (J.METHOD_WAVEK, P),
+        ph = None
+        for method, k in ((J.METHOD_SYMFOLD, 1), (J.METHOD_ONEF1B, 1), (J.METHOD_HANAYO, 1), (J.METHOD_WAVEK, P),
                           (J.METHOD_WAVEK, 2 * P)):
-            r = run(model, params, batches, P, method, k)
+            r = run(model, params, batches, P, method, k, phase_us=ph if method == J.METHOD_WAVEK else None)
+            if method == J.METHOD_SYMFOLD:  # WaveK's cost model: this box's measured phase means
+                m = r["phase_mean_us"]
+                ph = (m["FE"], m["FF"], m["BE"], m["BF"])
             rows.append(r)
             print(json.dumps({x: r[x] for x in ("P", "method", "k", "makespan_ms", "structures_per_s", "bubble_measured",
-                                                "bubble_replay")}), flush=True)
+                                                "bubble_replay", "peak_hbm_bytes_max_device")}), flush=True)
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     json.dump({"config": "C2: L=4 H=64 R=64, 256-atom cells, N_mb=%d, tf32, 1 GPU, lanes=1" % args.nmb, "rows": rows},
               open(args.out, "w"), indent=1)
