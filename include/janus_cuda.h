@@ -30,7 +30,11 @@ extern "C" {
 #define JANUS_ABI_VERSION 1
 
 /* precision of the per-edge contractions */
-enum { JANUS_PREC_FP32 = 0, JANUS_PREC_TF32 = 1 };
+/* FP32: fp32 arithmetic throughout (SIMT kernels / fp32 GEMMs); TF32: tf32
+ * tensor-core contractions (bf16 operands in the gradient-only BF/BE pair
+ * kernels), fp32 accumulate; FP32_EMU: fp32 accuracy on the tensor cores
+ * (BF16x9 emulated fp32 GEMMs, generic-width path only). */
+enum { JANUS_PREC_FP32 = 0, JANUS_PREC_TF32 = 1, JANUS_PREC_FP32_EMU = 2 };
 
 typedef struct {
   int32_t L, H, R, n_species;

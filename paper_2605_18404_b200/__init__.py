@@ -35,7 +35,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 c_int, c_i64, c_u64, c_f, c_d, c_vp, c_sz = (ctypes.c_int, ctypes.c_int64, ctypes.c_uint64, ctypes.c_float,
                                               ctypes.c_double, ctypes.c_void_p, ctypes.c_size_t)
 
-PREC_FP32, PREC_TF32 = 0, 1
+PREC_FP32, PREC_TF32, PREC_FP32_EMU = 0, 1, 2
 (PORT_ACT_IN, PORT_ACT_OUT, PORT_ADJ_IN, PORT_ADJ_OUT, PORT_TAN_IN, PORT_TAN_OUT, PORT_BADJ_IN,
  PORT_BADJ_OUT) = range(8)
 METHOD_SYMFOLD, METHOD_WAVEK, METHOD_ONEF1B, METHOD_FIRST, METHOD_HANAYO = 0, 1, 2, 3, 4

@@ -366,6 +366,42 @@ __device__ __forceinline__ void basis(float d, float rc, int f0, float (&p)[FPT]
   }
 }
 
+// The same basis with 3 exponentials instead of FPT: in units of delta,
+// x_j = d / delta - (f0 + j) and phi_j = exp(-x_j^2 / 2), so neighbouring
+// features differ by the factor phi_{j+1} / phi_j = exp(x_j - 1/2) (and
+// phi_{j-1} / phi_j = exp(-x_j - 1/2)), which itself shrinks by e^-1 per
+// step.  Starting at the feature nearest the peak every factor is <= 1, so
+// the recurrence never overflows and underflows only where the basis is ~0.
+// Error: ~FPT^2/2 ulp relative (< 1e-5), far below the bf16 / tf32 operand
+// rounding these values get.  (ncu: the per-element __expf of basis() were
+// ~10% of the pair kernels' stall samples, all on the MUFU pipe.)
+__device__ __forceinline__ void basis_fast(float d, float rc, int f0, float (&p)[FPT], float (&dp)[FPT]) {
+  const float delta = rc / (R - 1);
+  const float gamma = 1.0f / (2.0f * delta * delta);
+  const float u = d / delta - static_cast<float>(f0);
+  const int js = min(max(__float2int_rn(u), 0), FPT - 1);
+  const float xs = u - static_cast<float>(js);
+  const float ps = __expf(-0.5f * xs * xs);
+  float up = __expf(xs - 0.5f), dn = __expf(-xs - 0.5f);
+  constexpr float kE1 = 0.36787944117144233f;  // e^-1
+#pragma unroll
+  for (int j = 0; j < FPT; ++j) {
+    if (j == js) p[j] = ps;
+    if (j > js) {
+      p[j] = p[j - 1] * up;
+      up *= kE1;
+    }
+  }
+#pragma unroll
+  for (int j = FPT - 2; j >= 0; --j)
+    if (j < js) {
+      p[j] = p[j + 1] * dn;
+      dn *= kE1;
+    }
+#pragma unroll
+  for (int j = 0; j < FPT; ++j) dp[j] = -2.0f * gamma * (d - (f0 + j) * delta) * p[j];
+}
+
 __device__ __forceinline__ void setup(Ctx& c, uint32_t* tmem_slot, uint32_t ncols) {
   c.e = threadIdx.x & 127;
   c.q = threadIdx.x >> 7;
@@ -413,6 +449,15 @@ __device__ __forceinline__ float edge_qbar(const EdgeGeom& g, const ES& s, const
 
 // fast sigmoid for the tf32 path; SiLU and its derivatives derive from one s
 __device__ __forceinline__ float fsig(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
+// one-MUFU sigmoid for the gradient-only BF / BE pair kernels, whose results
+// become bf16 operands: sigma(x) = (1 + tanh(x / 2)) / 2 with tanh.approx
+// (abs error ~2^-12 in sigma, below bf16's 2^-9 relative rounding) instead of
+// ex2 + rcp — the pair kernels' epilogues were MUFU-throttled (ncu: mio stalls).
+__device__ __forceinline__ float fsig_t(float x) {
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * x));
+  return fmaf(0.5f, t, 0.5f);
+}
 
 // ----------------------------------------------------------------------- FE
 // m_i = sum_{e in row i} w_e * v[col e], w = c (SiLU(phi A + alpha) B + beta)

@@ -174,6 +174,7 @@ struct janus_trainer {
   std::atomic<int64_t> waited{0};
   std::atomic<int64_t> issued{0};
   std::string last_issued;
+  std::shared_ptr<std::atomic<bool>> alive = std::make_shared<std::atomic<bool>>(true);  // for the watchdog threads
 };
 
 namespace janus {
@@ -598,9 +599,11 @@ std::string hang_report(janus_trainer* t) {
 // the device stops draining its queues): after hang_s seconds without the
 // step being waited for, print the report and end the process.
 void hang_watchdog(janus_trainer* t, int64_t step) {
-  std::thread([t, step] {
-    std::this_thread::sleep_for(std::chrono::duration<double>(t->hang_s));
-    if (t->waited.load() > step) return;
+  std::shared_ptr<std::atomic<bool>> alive = t->alive;  // the trainer may be destroyed before this wakes
+  const double hang_s = t->hang_s;
+  std::thread([t, step, alive, hang_s] {
+    std::this_thread::sleep_for(std::chrono::duration<double>(hang_s));
+    if (!alive->load() || t->waited.load() > step) return;
     {  // host-side facts first: CUDA calls below may block behind a stuck launch
       const int64_t n = t->issued.load();
       std::fprintf(stderr, "rank %d: step %lld not done after %.0f s; %lld instructions issued, last: %s\n", t->rank,
@@ -916,6 +919,7 @@ janus_trainer* trainer_create(const janus_exec_desc& ed, const janus_stage_desc&
 
 void trainer_destroy(janus_trainer* t) {
   if (!t) return;
+  t->alive->store(false);
   if (t->reserved_streams) g_peer_streams.fetch_sub(t->reserved_streams);
   cudaSetDevice(t->sd.device);
   cudaDeviceSynchronize();

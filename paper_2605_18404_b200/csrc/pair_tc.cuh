@@ -475,7 +475,7 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_pair_tc(EdgeGeom g, const float4
     const float d = ok ? __ldg(&pg[2 * pp].x) : z4.x;
     {
       float ph[FPT], dph[FPT];
-      basis(d, rc, f0, ph, dph);
+      basis_fast(d, rc, f0, ph, dph);
       st_b16(B4, c.e, f0, ph);
       st_b16(B5, c.e, f0, dph);
     }
@@ -493,7 +493,7 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_pair_tc(EdgeGeom g, const float4
       c.ld2(TM_Z, TM_ZP, z, zp);
 #pragma unroll
       for (int k = 0; k < FPT; ++k) {
-        const float zz = z[k] + al[f0 + k], s1 = fsig(zz);
+        const float zz = z[k] + al[f0 + k], s1 = fsig_t(zz);
         z[k] = zz * s1;
         zp[k] = s1 * (1.0f + zz * (1.0f - s1)) * zp[k];
       }
@@ -517,7 +517,7 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_pair_tc(EdgeGeom g, const float4
       c.ld2(TM_G, TM_GP, sb, sdb);
 #pragma unroll
       for (int k = 0; k < FPT; ++k) {
-        const float zz = z[k] + al[f0 + k], s1 = fsig(zz);
+        const float zz = z[k] + al[f0 + k], s1 = fsig_t(zz);
         const float ds = s1 * (1.0f + zz * (1.0f - s1));
         const float d2s = s1 * (1.0f - s1) * (2.0f + zz * (1.0f - 2.0f * s1));
         z[k] = sb[k] * ds + sdb[k] * d2s * zp[k];  // zbar
@@ -582,7 +582,7 @@ __global__ void __launch_bounds__(NT, 1) msg_be_pair_tc(EdgeGeom g, const float4
     const float d = ok ? __ldg(&pg[2 * pp].x) : z4.x;
     {
       float ph[FPT], dph[FPT];
-      basis(d, rc, f0, ph, dph);
+      basis_fast(d, rc, f0, ph, dph);
       st_b16(B0, c.e, f0, ph);
     }
     be_adjoint_rows(pg, n_pairs, ch * TE, v, bm, B2);  // gbar (zero on padding: c = 0)
@@ -599,7 +599,7 @@ __global__ void __launch_bounds__(NT, 1) msg_be_pair_tc(EdgeGeom g, const float4
 #pragma unroll
       for (int k = 0; k < FPT; ++k) {
         const float zz = z[k] + al[f0 + k];
-        z[k] = zz * fsig(zz);
+        z[k] = zz * fsig_t(zz);
       }
       st_b16(B1, c.e, f0, z);  // s
     }
@@ -616,7 +616,7 @@ __global__ void __launch_bounds__(NT, 1) msg_be_pair_tc(EdgeGeom g, const float4
       c.ld2(TM_Z, TM_G, z, sb);
 #pragma unroll
       for (int k = 0; k < FPT; ++k) {
-        const float zz = z[k] + al[f0 + k], s1 = fsig(zz);
+        const float zz = z[k] + al[f0 + k], s1 = fsig_t(zz);
         z[k] = sb[k] * (s1 * (1.0f + zz * (1.0f - s1)));
       }
       st_b16(B3, c.e, f0, z);  // zbar

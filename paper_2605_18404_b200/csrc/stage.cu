@@ -331,13 +331,14 @@ LoadLayout load_layout(const janus_stage_desc& d) {
 
 janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
   const janus_model_desc& m = d.model;
-  const bool wide = d.kernels == 1 || m.H != kH || m.R != kR;
+  const bool wide = d.kernels == 1 || m.H != kH || m.R != kR || m.precision == JANUS_PREC_FP32_EMU;
   if (d.kernels < 0 || d.kernels > 1) throw config_error("kernels must be 0 (auto) or 1 (generic width)");
   if (wide && m.H != 64 && m.H != 128 && m.H != 256)
     throw config_error("hidden width H must be 64, 128 or 256 (got H=" + std::to_string(m.H) + ")");
   if (wide && (m.R < 2 || m.R > 1024)) throw config_error("basis size R must be in [2, 1024]");
   if (m.L < 1 || m.n_species < 1 || m.n_species > 256) throw config_error("bad model shape");
-  if (m.precision != JANUS_PREC_FP32 && m.precision != JANUS_PREC_TF32) throw config_error("unknown precision");
+  if (m.precision != JANUS_PREC_FP32 && m.precision != JANUS_PREC_TF32 && m.precision != JANUS_PREC_FP32_EMU)
+    throw config_error("unknown precision");
   const int U = 2 * m.L + 2;
   if (d.unit_begin < 0 || d.unit_end > U || d.unit_begin >= d.unit_end) throw domain_error("bad unit range");
   if (d.max_atoms < 1 || d.max_edges < 0 || d.max_struct < 1 || d.n_micro_batches < 1 || d.n_slots < 1)
@@ -519,6 +520,7 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
         sc.blas = h;
         JANUS_BLAS(cublasSetWorkspace(h, sc.blas_ws, kWs));
         JANUS_BLAS(cublasSetPointerMode(h, CUBLAS_POINTER_MODE_HOST));
+        if (m.precision == JANUS_PREC_FP32_EMU) JANUS_BLAS(cublasSetEmulationStrategy(h, CUBLAS_EMULATION_STRATEGY_EAGER));
         continue;
       }
       sc.partial = dalloc<float>(st, NA * static_cast<size_t>(EC::PE), false);

@@ -6,6 +6,8 @@ deep model (H=256) and any H in {64, 128, 256}, against the fp64 oracle.
 * tf32 (PREC_TF32: the same GEMMs on tf32 tensor-core math, fp32 accumulate):
   E 2e-3, F and gradients 2e-2 (the tensor-core tolerance of
   tests/test_gpu_tf32.py).
+* fp32-emulated (PREC_FP32_EMU: BF16x9 fp32 emulation on the tensor cores):
+  the fp32 tolerances.
 * Staged (P virtual stages, mid-layer splits) == unstaged, bit for bit, and
   pooled activation slots == one slot per micro-batch.
 * At H=64 the generic path agrees with the fused H=64 kernels.
@@ -42,11 +44,11 @@ def run_stage(janus, m, params, batches, max_atoms=64):
     return st
 
 
-@pytest.mark.parametrize("H,R,prec", [(64, 64, 0), (128, 32, 0), (256, 64, 0), (256, 64, 1)])
+@pytest.mark.parametrize("H,R,prec", [(64, 64, 0), (128, 32, 0), (256, 64, 0), (256, 64, 1), (64, 64, 2), (256, 64, 2)])
 def test_wide_matches_oracle(janus, oracle, has_gpu, H, R, prec):
     if not has_gpu:
         pytest.skip("no GPU")
-    tol_e, tol_f = (1e-5, 1e-4) if prec == janus.PREC_FP32 else (2e-3, 2e-2)
+    tol_e, tol_f = (2e-3, 2e-2) if prec == janus.PREC_TF32 else (1e-5, 1e-4)
     m = janus.Model(L=2, H=H, R=R, precision=prec, generic=True)
     params = m.synth_params(5)
     batches = [janus.synth_batch(m, [24, 30], 0.095, 31), janus.synth_batch(m, [40], 0.095, 32)]

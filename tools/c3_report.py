@@ -51,20 +51,22 @@ def main():
     ap.add_argument("--nmb", type=int, default=16)
     ap.add_argument("--atoms", type=int, default=512)
     ap.add_argument("--L", type=int, default=32)
-    ap.add_argument("--prec", default="tf32")
+    ap.add_argument("--prec", default="tf32", choices=["tf32", "fp32", "emu"])
+    ap.add_argument("--H", type=int, default=256)
+    ap.add_argument("--methods", default="all", help="all | symfold (P>1 comparisons off)")
     ap.add_argument("--lanes", type=int, default=8)
     ap.add_argument("--Ps", default="1,8")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "c3_report.json"))
     a = ap.parse_args()
-    prec = J.PREC_TF32 if a.prec == "tf32" else J.PREC_FP32
-    model = J.Model(L=a.L, H=256, R=64, precision=prec)
+    prec = {"tf32": J.PREC_TF32, "fp32": J.PREC_FP32, "emu": J.PREC_FP32_EMU}[a.prec]
+    model = J.Model(L=a.L, H=a.H, R=64, precision=prec, generic=True)
     params = model.synth_params(3)
     t0 = time.time()
     batches = [J.synth_batch(model, [a.atoms], 0.095, 900 + m) for m in range(a.nmb)]
     rows = []
     for P in [int(x) for x in a.Ps.split(",")]:
         cases = [(J.METHOD_SYMFOLD, 1, False), (J.METHOD_SYMFOLD, 1, True)]
-        if P > 1:
+        if P > 1 and a.methods == "all":
             cases += [(J.METHOD_ONEF1B, 1, False), (J.METHOD_WAVEK, P, False)]
         for method, k, unf in cases:
             lanes = a.lanes if P == 1 else 1
@@ -72,7 +74,7 @@ def main():
             rows.append(r)
             print(json.dumps({x: r[x] for x in ("P", "method", "unfolded_slots", "lanes", "structures_per_s",
                                                 "peak_hbm_bytes_max_device")}), flush=True)
-    res = {"config": f"configs[2]: L={a.L} H=256 R=64 r_c=5, {a.atoms}-atom cells (rho 0.095), N_mb={a.nmb}, "
+    res = {"config": f"L={a.L} H={a.H} R=64 r_c=5, {a.atoms}-atom cells (rho 0.095), N_mb={a.nmb}, "
                      f"{a.prec}, generic-width path, 1 B200 (P virtual stages, 1 lane for P > 1)",
            "edges_per_structure": int(batches[0].n_edges), "wall_s": time.time() - t0, "rows": rows}
     os.makedirs(os.path.dirname(a.out), exist_ok=True)
