@@ -435,12 +435,15 @@ def main():
         except J.JanusError as ex:
             roof = {"error": str(ex)}
 
-    # the fp32 SIMT parity path (north_star tolerances 1e-5 / 1e-4) on the same
-    # workload, device-timed the same way: the throughput that meets the tight
-    # tolerance, beside the tensor-core headline
+    # the fp32 path (north_star tolerances 1e-5 / 1e-4) on the same workload,
+    # device-timed the same way: the throughput that meets the tight tolerance,
+    # beside the tensor-core headline.  The generic-width path in fp32 (batched
+    # per-pair GEMMs, stage_wide.inc) measured 3523 structures/s against the
+    # fused fp32 SIMT kernels' 1481, so it is the fp32 path
     fp32_path = None
     if rank == 0 and N == 1 and args.precision == "tf32" and not args.no_fp32_path:
-        m32 = J.Model(L=CONFIG["L"], H=CONFIG["H"], R=CONFIG["R"], r_c=CONFIG["r_c"], precision=J.PREC_FP32)
+        m32 = J.Model(L=CONFIG["L"], H=CONFIG["H"], R=CONFIG["R"], r_c=CONFIG["r_c"], precision=J.PREC_FP32,
+                      generic=True)
         t32 = J.Trainer(m32, params, P, method, n_mb, k=k, max_atoms=CONFIG["atoms"], max_edges=max_edges,
                         max_struct=1, local=True, graphs=True, rank=0, device=local_rank, lanes=args.lanes)
         for m, b in enumerate(batches):
@@ -454,7 +457,7 @@ def main():
         t32.close()
         ms32 = sum(ts32) / len(ts32)
         fp32_path = {"value": n_mb / (ms32 * 1e-3), "unit": "structures/s", "ms_per_step": ms32, "steps": len(ts32),
-                     "dtype": "fp32 SIMT (FFMA) for every contraction",
+                     "dtype": "fp32 for every contraction (generic-width path: fp32 GEMMs, compute type 32F)",
                      "tolerance": "E rel 1e-5, F and gradients 1e-4 of max (tests/test_gpu_bench_parity.py)"}
 
     cpu = None

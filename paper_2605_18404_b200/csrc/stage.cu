@@ -513,6 +513,7 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
         sc.z2 = dalloc<float>(st, P2 * static_cast<size_t>(m.H), false);
         sc.a2 = dalloc<float>(st, P2 * static_cast<size_t>(m.H), false);
         sc.b2 = dalloc<float>(st, P2 * static_cast<size_t>(m.H), false);
+        sc.cspart = dalloc<float>(st, static_cast<size_t>(wide::kColChunks) * m.H, false);
         constexpr size_t kWs = 32u << 20;
         sc.blas_ws = dalloc<uint8_t>(st, kWs, false);
         cublasHandle_t h = nullptr;
@@ -527,12 +528,6 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
       const size_t chunks = (NA + node::kWChunk - 1) / node::kWChunk;
       sc.wpart = dalloc<float>(st, 3 * chunks * std::max<size_t>(kH * kH + 2 * kH, static_cast<size_t>(m.n_species) * kH), false);
       sc.counter = dalloc<unsigned>(st, 1, false);
-    }
-    if (wide) {
-      const size_t n1 = std::max(NE, NA) + 2;
-      st->ones = dalloc<float>(st, n1, true);
-      wide::fill_kernel<<<blocks(static_cast<int64_t>(n1), 256), 256>>>(static_cast<int64_t>(n1), st->ones, 1.0f);
-      JANUS_LAUNCH_CHECK("ones");
     }
     JANUS_CUDA(cudaFuncSetAttribute(edge_tc::wgrad_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge_tc::wgrad_tc_smem()));
     JANUS_CUDA(cudaFuncSetAttribute(edge::msg_fe_kernel<kH, kR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge::fe_smem<kH, kR>()));

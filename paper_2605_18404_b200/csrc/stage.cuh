@@ -87,7 +87,7 @@ struct Scratch {
   unsigned* counter = nullptr;  // last-CTA-reduces launch counter (one launch at a time per lane)
   // generic-width path (stage_wide.inc): [2 pairs][R] basis stack, three
   // [2 pairs][H] operand stacks, and the lane's cuBLAS handle + workspace
-  float *phi2 = nullptr, *z2 = nullptr, *a2 = nullptr, *b2 = nullptr;
+  float *phi2 = nullptr, *z2 = nullptr, *a2 = nullptr, *b2 = nullptr, *cspart = nullptr;
   void* blas = nullptr;
   void* blas_ws = nullptr;
 };
@@ -149,7 +149,6 @@ struct janus_stage {
   int pair_chunks_cap = 0;
   janus::LmBuilder* lm = nullptr;  // device neighbour-list builder (lazy, janus_stage_load without a CSR)
   bool wide = false;               // generic-width phases (stage_wide.inc) instead of the fused H=64 kernels
-  float* ones = nullptr;           // wide: ones vector (column sums as GEMMs)
 
   float* P(int u) const { return params + uoff[static_cast<size_t>(u - u0)]; }
 

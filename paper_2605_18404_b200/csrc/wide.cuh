@@ -191,26 +191,64 @@ __global__ void be_zbar_kernel(int64_t PH, int H, float* __restrict__ sb, const 
 }
 
 // ------------------------------------------------------------ row kernels
-// warp per CSR row i (receiver); lane l owns features [l V, l V + V)
+// kWpr warps per CSR row i (receiver), 2 rows per 256-thread block: warp q of
+// a row takes the row's edges e0 + q, e0 + q + kWpr, ...; lane l owns features
+// [l V, l V + V) of every node row, so each edge moves whole rows in single
+// coalesced 32 x V-float transactions.  The kWpr partials are summed in warp
+// order through shared memory (deterministic; 4x the warps of one warp per
+// row, which left ~3 warps per SM at 512-atom micro-batches).
+constexpr int kWpr = 4;
+inline int rows_grid(int N) { return (N + 256 / (32 * kWpr) - 1) / (256 / (32 * kWpr)); }
+
+template <int V>
+__device__ __forceinline__ void row_reduce_store(float (&acc)[V], float* __restrict__ out, int i, int N, bool add = false) {
+  constexpr int H = 32 * V;
+  __shared__ float part[8][H];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, q = w % kWpr;
+#pragma unroll
+  for (int k = 0; k < V; ++k) part[w][l * V + k] = acc[k];
+  __syncthreads();
+  if (q == 0 && i < N) {
+    float o[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      float x = part[w][l * V + k];
+#pragma unroll
+      for (int r = 1; r < kWpr; ++r) x += part[w + r][l * V + k];
+      o[k] = x;
+    }
+    if (add) {
+      float prev[V];
+      ldv<V>(out + static_cast<size_t>(i) * H + l * V, prev);
+#pragma unroll
+      for (int k = 0; k < V; ++k) o[k] += prev[k];
+    }
+    stv<V>(out + static_cast<size_t>(i) * H + l * V, o);
+  }
+  __syncthreads();
+}
+
 // FE: m_i = sum_e w_p(e) v_j  (BE: Y_b,i = sum_e w_p b_m[j])
 template <int V>
 __global__ void __launch_bounds__(256) fe_rows_kernel(int N, const int* __restrict__ row_ptr, const int* __restrict__ col,
                                                       const int* __restrict__ pidx, const float* __restrict__ wf,
                                                       const float* __restrict__ v, float* __restrict__ m) {
   constexpr int H = 32 * V;
-  const int i = static_cast<int>((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5), l = threadIdx.x & 31;
-  if (i >= N) return;
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, q = w % kWpr;
+  const int i = blockIdx.x * (8 / kWpr) + w / kWpr;
   float acc[V] = {};
-  const int e1 = __ldg(row_ptr + i + 1);
+  if (i < N) {
+    const int e1 = __ldg(row_ptr + i + 1);
 #pragma unroll 2
-  for (int e = __ldg(row_ptr + i); e < e1; ++e) {
-    float w[V], x[V];
-    ldv<V>(wf + static_cast<size_t>(__ldg(pidx + e)) * H + l * V, w);
-    ldv<V>(v + static_cast<size_t>(__ldg(col + e)) * H + l * V, x);
+    for (int e = __ldg(row_ptr + i) + q; e < e1; e += kWpr) {
+      float wv[V], x[V];
+      ldv<V>(wf + static_cast<size_t>(__ldg(pidx + e)) * H + l * V, wv);
+      ldv<V>(v + static_cast<size_t>(__ldg(col + e)) * H + l * V, x);
 #pragma unroll
-    for (int q = 0; q < V; ++q) acc[q] += w[q] * x[q];
+      for (int k = 0; k < V; ++k) acc[k] += wv[k] * x[k];
+    }
   }
-  stv<V>(m + static_cast<size_t>(i) * H + l * V, acc);
+  row_reduce_store<V>(acc, m, i, N);
 }
 
 // FF: Y_i = sum_e w_p a_m[j];  F_i += sum_e <a_m[i] v_j + a_m[j] v_i, w'_p> u_e
@@ -221,37 +259,47 @@ __global__ void __launch_bounds__(256) ff_rows_kernel(int N, const int* __restri
                                                       const float* __restrict__ v, const float* __restrict__ am,
                                                       float* __restrict__ Y, float* __restrict__ F) {
   constexpr int H = 32 * V;
-  const int i = static_cast<int>((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5), l = threadIdx.x & 31;
-  if (i >= N) return;
-  float ai[V], vi[V], acc[V] = {};
-  ldv<V>(am + static_cast<size_t>(i) * H + l * V, ai);
-  ldv<V>(v + static_cast<size_t>(i) * H + l * V, vi);
+  __shared__ float fpart[8][3];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, q = w % kWpr;
+  const int i = blockIdx.x * (8 / kWpr) + w / kWpr;
+  float acc[V] = {};
   float fx = 0.f, fy = 0.f, fz = 0.f;
-  const int e1 = __ldg(row_ptr + i + 1);
+  if (i < N) {
+    float ai[V], vi[V];
+    ldv<V>(am + static_cast<size_t>(i) * H + l * V, ai);
+    ldv<V>(v + static_cast<size_t>(i) * H + l * V, vi);
+    const int e1 = __ldg(row_ptr + i + 1);
 #pragma unroll 2
-  for (int e = __ldg(row_ptr + i); e < e1; ++e) {
-    const size_t op = static_cast<size_t>(__ldg(pidx + e)) * H + l * V, oj = static_cast<size_t>(__ldg(col + e)) * H + l * V;
-    float w[V], wp[V], aj[V], vj[V];
-    ldv<V>(wf + op, w);
-    ldv<V>(wfp + op, wp);
-    ldv<V>(am + oj, aj);
-    ldv<V>(v + oj, vj);
-    float q = 0.f;
+    for (int e = __ldg(row_ptr + i) + q; e < e1; e += kWpr) {
+      const size_t op = static_cast<size_t>(__ldg(pidx + e)) * H + l * V, oj = static_cast<size_t>(__ldg(col + e)) * H + l * V;
+      float wv[V], wp[V], aj[V], vj[V];
+      ldv<V>(wf + op, wv);
+      ldv<V>(wfp + op, wp);
+      ldv<V>(am + oj, aj);
+      ldv<V>(v + oj, vj);
+      float qq = 0.f;
 #pragma unroll
-    for (int k = 0; k < V; ++k) {
-      acc[k] += w[k] * aj[k];
-      q += (ai[k] * vj[k] + aj[k] * vi[k]) * wp[k];
+      for (int k = 0; k < V; ++k) {
+        acc[k] += wv[k] * aj[k];
+        qq += (ai[k] * vj[k] + aj[k] * vi[k]) * wp[k];
+      }
+      qq = dev::warp_sum(qq);
+      fx += qq * __ldg(u + 3 * e);
+      fy += qq * __ldg(u + 3 * e + 1);
+      fz += qq * __ldg(u + 3 * e + 2);
     }
-    q = dev::warp_sum(q);
-    fx += q * __ldg(u + 3 * e);
-    fy += q * __ldg(u + 3 * e + 1);
-    fz += q * __ldg(u + 3 * e + 2);
   }
-  stv<V>(Y + static_cast<size_t>(i) * H + l * V, acc);
   if (l == 0) {
-    F[3 * i] += fx;
-    F[3 * i + 1] += fy;
-    F[3 * i + 2] += fz;
+    fpart[w][0] = fx;
+    fpart[w][1] = fy;
+    fpart[w][2] = fz;
+  }
+  row_reduce_store<V>(acc, Y, i, N);  // (its barriers also publish fpart)
+  if (q == 0 && l < 3 && i < N) {
+    float f = fpart[w][l];
+#pragma unroll
+    for (int r = 1; r < kWpr; ++r) f += fpart[w + r][l];
+    F[3 * i + l] += f;
   }
 }
 
@@ -264,31 +312,33 @@ __global__ void __launch_bounds__(256) bf_rows_kernel(int N, const int* __restri
                                                       const float* __restrict__ vd, const float* __restrict__ am,
                                                       float* __restrict__ mdot, float* __restrict__ X) {
   constexpr int H = 32 * V;
-  const int i = static_cast<int>((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5), l = threadIdx.x & 31;
-  if (i >= N) return;
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, q = w % kWpr;
+  const int i = blockIdx.x * (8 / kWpr) + w / kWpr;
   float md[V] = {}, xs[V] = {};
-  const float fix = __ldg(Fbar + 3 * i), fiy = __ldg(Fbar + 3 * i + 1), fiz = __ldg(Fbar + 3 * i + 2);
-  const int e1 = __ldg(row_ptr + i + 1);
+  if (i < N) {
+    const float fix = __ldg(Fbar + 3 * i), fiy = __ldg(Fbar + 3 * i + 1), fiz = __ldg(Fbar + 3 * i + 2);
+    const int e1 = __ldg(row_ptr + i + 1);
 #pragma unroll 2
-  for (int e = __ldg(row_ptr + i); e < e1; ++e) {
-    const int j = __ldg(col + e);
-    const float qb = (fix - __ldg(Fbar + 3 * j)) * __ldg(u + 3 * e) + (fiy - __ldg(Fbar + 3 * j + 1)) * __ldg(u + 3 * e + 1) +
-                     (fiz - __ldg(Fbar + 3 * j + 2)) * __ldg(u + 3 * e + 2);
-    const size_t op = static_cast<size_t>(__ldg(pidx + e)) * H + l * V, oj = static_cast<size_t>(j) * H + l * V;
-    float w[V], wp[V], vj[V], dj[V], aj[V];
-    ldv<V>(wf + op, w);
-    ldv<V>(wfp + op, wp);
-    ldv<V>(v + oj, vj);
-    ldv<V>(vd + oj, dj);
-    ldv<V>(am + oj, aj);
+    for (int e = __ldg(row_ptr + i) + q; e < e1; e += kWpr) {
+      const int j = __ldg(col + e);
+      const float qb = (fix - __ldg(Fbar + 3 * j)) * __ldg(u + 3 * e) + (fiy - __ldg(Fbar + 3 * j + 1)) * __ldg(u + 3 * e + 1) +
+                       (fiz - __ldg(Fbar + 3 * j + 2)) * __ldg(u + 3 * e + 2);
+      const size_t op = static_cast<size_t>(__ldg(pidx + e)) * H + l * V, oj = static_cast<size_t>(j) * H + l * V;
+      float wv[V], wp[V], vj[V], dj[V], aj[V];
+      ldv<V>(wf + op, wv);
+      ldv<V>(wfp + op, wp);
+      ldv<V>(v + oj, vj);
+      ldv<V>(vd + oj, dj);
+      ldv<V>(am + oj, aj);
 #pragma unroll
-    for (int k = 0; k < V; ++k) {
-      md[k] += qb * wp[k] * vj[k] + w[k] * dj[k];
-      xs[k] += qb * wp[k] * aj[k];
+      for (int k = 0; k < V; ++k) {
+        md[k] += qb * wp[k] * vj[k] + wv[k] * dj[k];
+        xs[k] += qb * wp[k] * aj[k];
+      }
     }
   }
-  stv<V>(mdot + static_cast<size_t>(i) * H + l * V, md);
-  stv<V>(X + static_cast<size_t>(i) * H + l * V, xs);
+  row_reduce_store<V>(md, mdot, i, N);
+  row_reduce_store<V>(xs, X, i, N);
 }
 
 // (BE's Y_b,i = sum_e w_p b_m[j] is fe_rows_kernel with x = b_m)
@@ -385,19 +435,59 @@ __global__ void ro_be_ew_kernel(int64_t NH, int H, const float* __restrict__ t, 
 }
 
 // out[z][k] += sum_{Z_i = z} x[i][k] (x != null, cols = H) or
-// out[z] += sum_{Z_i = z} eps[s(i)] (x == null, cols = 1); atoms in order
-__global__ void species_sum_kernel(int N, int S, int cols, const int* __restrict__ species, const float* __restrict__ x,
-                                   const float* __restrict__ eps, const int* __restrict__ struct_id,
-                                   float* __restrict__ out) {
-  const int z = blockIdx.y;
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (z >= S || k >= cols) return;
+// out[z] += sum_{Z_i = z} eps[s(i)] (x == null, cols = 1).  Block (32-column
+// strip, species z), 8 warps: lane = column, warp w takes atoms i = w mod 8,
+// the 8 partials are summed in warp order (deterministic).
+__global__ void __launch_bounds__(256) species_sum_kernel(int N, int S, int cols, const int* __restrict__ species,
+                                                          const float* __restrict__ x, const float* __restrict__ eps,
+                                                          const int* __restrict__ struct_id, float* __restrict__ out) {
+  __shared__ float part[8][33];
+  const int z = blockIdx.y, l = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int k = blockIdx.x * 32 + l;
   float acc = 0.f;
-  for (int i = 0; i < N; ++i) {
-    if (__ldg(species + i) != z) continue;
-    acc += x ? x[static_cast<size_t>(i) * cols + k] : __ldg(eps + __ldg(struct_id + i));
+  if (k < cols)
+    for (int i = w; i < N; i += 8) {
+      if (__ldg(species + i) != z) continue;
+      acc += x ? __ldg(x + static_cast<size_t>(i) * cols + k) : __ldg(eps + __ldg(struct_id + i));
+    }
+  part[w][l] = acc;
+  __syncthreads();
+  if (w == 0 && k < cols) {
+    float s = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s += part[q][l];
+    out[static_cast<size_t>(z) * cols + k] += s;
   }
-  out[static_cast<size_t>(z) * cols + k] += acc;
+}
+
+// Column sums of X[rows][cols] in two deterministic launches: block (strip of
+// 32 columns, chunk g of rows) -> part[g][cols] (8 warps interleave rows, summed
+// in warp order), then out[c] += sum_g part[g][c] in chunk order.
+constexpr int kColChunks = 64;
+__global__ void __launch_bounds__(256) colsum_part_kernel(int rows, int cols, const float* __restrict__ X,
+                                                          float* __restrict__ part) {
+  __shared__ float red[8][33];
+  const int l = threadIdx.x & 31, w = threadIdx.x >> 5, k = blockIdx.x * 32 + l, g = blockIdx.y;
+  const int per = (rows + gridDim.y - 1) / gridDim.y, r0 = g * per, r1 = min(rows, r0 + per);
+  float acc = 0.f;
+  if (k < cols)
+#pragma unroll 4
+    for (int r = r0 + w; r < r1; r += 8) acc += __ldg(X + static_cast<size_t>(r) * cols + k);
+  red[w][l] = acc;
+  __syncthreads();
+  if (w == 0 && k < cols) {
+    float s = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s += red[q][l];
+    part[static_cast<size_t>(g) * cols + k] = s;
+  }
+}
+__global__ void colsum_final_kernel(int cols, int chunks, const float* __restrict__ part, float* __restrict__ out) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= cols) return;
+  float s = 0.f;
+  for (int g = 0; g < chunks; ++g) s += part[static_cast<size_t>(g) * cols + k];
+  out[k] += s;
 }
 
 __global__ void fill_kernel(int64_t n, float* __restrict__ p, float v) {

@@ -86,11 +86,13 @@ def bench_case(janus, oracle, has_gpu):
     return m, params, batches, refs
 
 
-@pytest.mark.parametrize("prec", ["tf32", "fp32"])
-def test_bench_config_matches_oracle(janus, oracle, bench_case, prec):
+@pytest.mark.parametrize("prec,generic", [("tf32", False), ("fp32", False), ("fp32", True)])
+def test_bench_config_matches_oracle(janus, oracle, bench_case, prec, generic):
+    """generic: the fp32 path bench.py reports beside the headline (the
+    generic-width GEMM path, stage_wide.inc) at the fp32 tolerances."""
     m0, params, batches, refs = bench_case
     m = janus.Model(L=m0.L, H=m0.H, R=m0.R, r_c=m0.r_c,
-                    precision=janus.PREC_TF32 if prec == "tf32" else janus.PREC_FP32)
+                    precision=janus.PREC_TF32 if prec == "tf32" else janus.PREC_FP32, generic=generic)
     lr = 1e-3
     tr, stats = run_trainer(janus, m, params, batches, lanes=32, lr=lr)
     compare(janus, m, tr, batches, refs, prec, "bench config (L=4, 256-atom fcc, 32 lanes, device LM, graphs)")
@@ -127,12 +129,12 @@ def test_bench_config_graph_replay_stable(janus, bench_case):
     tr.close()
 
 
-@pytest.mark.parametrize("prec", ["tf32", "fp32"])
-def test_c4_mixed_cells_match_oracle(janus, oracle, has_gpu, prec):
+@pytest.mark.parametrize("prec,generic", [("tf32", False), ("fp32", False), ("fp32", True)])
+def test_c4_mixed_cells_match_oracle(janus, oracle, has_gpu, prec, generic):
     """configs[3]'s mixed 128-1024-atom cells, two per micro-batch."""
     if not has_gpu:
         pytest.skip("no GPU")
-    m = janus.Model(L=4, H=64, R=64, precision=janus.PREC_TF32 if prec == "tf32" else janus.PREC_FP32)
+    m = janus.Model(L=4, H=64, R=64, precision=janus.PREC_TF32 if prec == "tf32" else janus.PREC_FP32, generic=generic)
     params = m.synth_params(8)
     batches = [janus.synth_batch(m, [128, 1024], 0.095, 31), janus.synth_batch(m, [686, 250], 0.095, 32)]
     refs = oracle_steps(oracle, m, batches, params)

@@ -73,8 +73,8 @@ def run_ranks_threads(cfg, timeout=int(os.environ.get("MULTIRANK_TIMEOUT", 420))
                 t.start()
             for t in ts:
                 t.join()
-            for r in range(world):
-                assert errs[r] is None, f"rank {r}: {errs[r]!r}"
+            bad = [f"rank {r}: {e!r}" for r, e in enumerate(errs) if e is not None]
+            assert not bad, "\n".join(bad)
             return res
     finally:
         os.environ.pop("JANUS_HANG_REPORT", None)
