@@ -313,18 +313,21 @@ void do_send(janus_trainer* t, VDev& dv, int flow, int mb, janus_stage* src, int
     port_ptr(t, src, mb, sport, t->chan_stream[static_cast<size_t>(channel_index(t->chans, {flow, dv.id, peer_dev}))], &sp, &sb);
     return chan_send(t, dv, flow, mb, sp, sb, peer_dev);
   }
-  port_ptr(t, src, mb, sport, dv.send, &sp, &sb);
+  // local: the copy runs on this channel's own stream, so a copy waiting for
+  // the receiver's slot (slots.hpp) never holds up another channel's copies
+  cudaStream_t cs = t->chan_stream[static_cast<size_t>(channel_index(t->chans, {flow, dv.id, peer_dev}))];
+  port_ptr(t, src, mb, sport, cs, &sp, &sb);
   cudaEvent_t ready = next_event(t);
   JANUS_CUDA(cudaEventRecord(ready, lane_stream(t, dv, mb)));
-  JANUS_CUDA(cudaStreamWaitEvent(dv.send, ready, 0));
+  JANUS_CUDA(cudaStreamWaitEvent(cs, ready, 0));
   t->p2p_bytes += static_cast<int64_t>(sb);
   float* dp;
   size_t db;
-  port_ptr(t, dst, mb, dport, dv.send, &dp, &db);
+  port_ptr(t, dst, mb, dport, cs, &dp, &db);
   if (db != sb) throw state_error("port size mismatch between channel ends");
-  JANUS_CUDA(cudaMemcpyAsync(dp, sp, sb, cudaMemcpyDeviceToDevice, dv.send));
+  JANUS_CUDA(cudaMemcpyAsync(dp, sp, sb, cudaMemcpyDeviceToDevice, cs));
   cudaEvent_t done = next_event(t);
-  JANUS_CUDA(cudaEventRecord(done, dv.send));
+  JANUS_CUDA(cudaEventRecord(done, cs));
   t->delivered[{flow, mb, from_b, to_b}] = done;
 }
 
@@ -368,15 +371,17 @@ void mirror_back_send(janus_trainer* t, VDev& dv, int b, int mb) {
     port_ptr(t, f, mb, JANUS_PORT_BADJ_OUT, t->chan_stream[static_cast<size_t>(c)], &sp, &sb);
     return chan_send(t, dv, kFlowMirrorBack + (b & 1), mb, sp, sb, t->E_dev[static_cast<size_t>(b)]);
   }
-  port_ptr(t, f, mb, JANUS_PORT_BADJ_OUT, dv.send, &sp, &sb);
+  cudaStream_t cs = t->chan_stream[static_cast<size_t>(
+      channel_index(t->chans, {kFlowMirrorBack + (b & 1), dv.id, t->E_dev[static_cast<size_t>(b)]}))];
+  port_ptr(t, f, mb, JANUS_PORT_BADJ_OUT, cs, &sp, &sb);
   cudaEvent_t ready = next_event(t);
   JANUS_CUDA(cudaEventRecord(ready, lane_stream(t, dv, mb)));
-  JANUS_CUDA(cudaStreamWaitEvent(dv.send, ready, 0));
+  JANUS_CUDA(cudaStreamWaitEvent(cs, ready, 0));
   t->p2p_bytes += static_cast<int64_t>(sb);
   float* buf = t->mirror_buf[static_cast<size_t>(b) * t->ed.n_micro_batches + mb];
-  JANUS_CUDA(cudaMemcpyAsync(buf, sp, sb, cudaMemcpyDeviceToDevice, dv.send));
+  JANUS_CUDA(cudaMemcpyAsync(buf, sp, sb, cudaMemcpyDeviceToDevice, cs));
   cudaEvent_t done = next_event(t);
-  JANUS_CUDA(cudaEventRecord(done, dv.send));
+  JANUS_CUDA(cudaEventRecord(done, cs));
   t->delivered[{kFlowMirrorBack, mb, b, b}] = done;
 }
 void mirror_back_recv_add(janus_trainer* t, VDev& dv, int b, int mb) {
@@ -818,7 +823,12 @@ janus_trainer* trainer_create(const janus_exec_desc& ed, const janus_stage_desc&
   // local issue order: a topological order of the full DAG (seq + data edges),
   // so every send is issued before its receive.
   t->graph = build_dependencies(t->sched);
-  if (t->local) t->order = local_issue_order(t->graph);
+  if (t->local) {
+    t->order = local_issue_order(t->graph);
+    t->chans = schedule_channels(t->sched, t->P, t->onef1b);  // one copy stream per channel (do_send)
+    t->chan_stream.assign(t->chans.size(), nullptr);
+    for (auto& cs : t->chan_stream) JANUS_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  }
   // activation slot pools: sized by the micro-batches live at once on each
   // stage object in this process's issue order (include/janus/slots.hpp)
   {
