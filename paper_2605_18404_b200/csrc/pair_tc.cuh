@@ -434,7 +434,19 @@ __device__ __forceinline__ void be_adjoint_rows(const float4* __restrict__ pg, i
 // kernels (edge_tc.cuh msg_bf_tc / msg_be_tc) but with no w / w' MMAs: the
 // per-row sums use the stored filters (msg_bf_rows / msg_be_rows).
 // Persistent CTAs, static chunk assignment => deterministic partials.
-__global__ void __launch_bounds__(NT, 1) msg_bf_pair_tc(EdgeGeom g, const float4* __restrict__ pg, int n_pairs, MsgParams p,
+// Register caps of the BF / BE pair kernels.  At the launch bound's 128
+// registers x 512 threads a pair CTA holds the SM's whole register file, so
+// nothing else (row / upd kernels of the other lanes) can share its SM while
+// it waits on gathers and MMAs.  Measured (tools/ab_libs.sh, two runs each):
+// 128/128 17534-17545, BF 96 / BE 64 17428-17455, 96/96 17681-17702,
+// 96/80 17756-17759 structures/s (no spills; BF would spill below 96).
+#ifndef JANUS_BF_MAXNREG
+#define JANUS_BF_MAXNREG 96
+#endif
+#ifndef JANUS_BE_MAXNREG
+#define JANUS_BE_MAXNREG 80
+#endif
+__global__ void __maxnreg__(JANUS_BF_MAXNREG) msg_bf_pair_tc(EdgeGeom g, const float4* __restrict__ pg, int n_pairs, MsgParams p,
                                                        float rc, const float* __restrict__ v, const float* __restrict__ vdot,
                                                        const float* __restrict__ am, const float* __restrict__ Fbar,
                                                        float* __restrict__ partial) {
@@ -547,7 +559,7 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_pair_tc(EdgeGeom g, const float4
   teardown(c, 512);
 }
 
-__global__ void __launch_bounds__(NT, 1) msg_be_pair_tc(EdgeGeom g, const float4* __restrict__ pg, int n_pairs, MsgParams p,
+__global__ void __maxnreg__(JANUS_BE_MAXNREG) msg_be_pair_tc(EdgeGeom g, const float4* __restrict__ pg, int n_pairs, MsgParams p,
                                                        float rc, const float* __restrict__ v, const float* __restrict__ bm,
                                                        float* __restrict__ partial) {
   extern __shared__ __align__(1024) uint8_t sm_raw[];

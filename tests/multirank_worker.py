@@ -59,16 +59,55 @@ def run_rank(J, cfg, rank, comm, barrier=None):
     return res
 
 
+def run_threads(J, cfg, timeout):
+    """All ranks as THREADS of this (fresh) process on the one GPU
+    (Comm.threads): each builds its own per-rank trainer; ctypes releases the
+    GIL, so the ranks issue concurrently.  Returns per-rank results or raises
+    with every rank's error."""
+    import tempfile
+    import threading
+
+    world = cfg["P"] * cfg["dp"]
+    with tempfile.TemporaryDirectory() as d:
+        res, errs = [None] * world, [None] * world
+        bar = threading.Barrier(world)
+
+        def one(r):
+            try:
+                comm = J.Comm.threads(d, world, r, 0)
+                try:
+                    res[r] = run_rank(J, cfg, r, comm, barrier=lambda: bar.wait(timeout))
+                finally:
+                    comm.close()
+            except Exception as ex:  # noqa: BLE001
+                errs[r] = ex
+
+        ts = [threading.Thread(target=one, args=(r,)) for r in range(world)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        bad = [f"rank {r}: {e!r}" for r, e in enumerate(errs) if e is not None]
+        if bad:
+            raise RuntimeError("\n".join(bad))
+        return res
+
+
 def main():
     import faulthandler
 
     if int(os.environ.get("WORKER_DUMP", 0)) > 0:  # the harness's timeout: show where this rank is stuck
         faulthandler.dump_traceback_later(int(os.environ["WORKER_DUMP"]), exit=False)
     cfg = json.loads(sys.argv[1])
-    rank = int(sys.argv[2])
-    out = sys.argv[3]
     import paper_2605_18404_b200 as J
 
+    if sys.argv[2] == "threads":  # every rank as a thread of this process: out = prefix of per-rank files
+        res = run_threads(J, cfg, int(os.environ.get("THREAD_BARRIER_TIMEOUT", 120)))
+        for r, x in enumerate(res):
+            np.savez(f"{sys.argv[3]}.{r}.npz", **x)
+        return
+    rank = int(sys.argv[2])
+    out = sys.argv[3]
     comm = J.Comm.ipc(cfg["dir"], cfg["P"] * cfg["dp"], rank, 0)
     res = run_rank(J, cfg, rank, comm)
     comm.close()

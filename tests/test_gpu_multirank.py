@@ -43,41 +43,20 @@ import multirank_worker as W  # noqa: E402
 
 
 def run_ranks_threads(cfg, timeout=int(os.environ.get("MULTIRANK_TIMEOUT", 420))):
-    """All ranks as THREADS of this process on the one GPU (Comm.threads): each
-    builds its own per-rank trainer; ctypes releases the GIL, so the ranks
-    issue concurrently.  A rank that hangs ends the process after `timeout`
-    seconds with the executor's hang report (JANUS_HANG_REPORT)."""
-    import threading
-
-    import paper_2605_18404_b200 as J
+    """All ranks as THREADS of one process on the one GPU (Comm.threads).  The
+    process is a fresh one (tests/multirank_worker.py threads): the ranks share
+    its CUDA context, and CUDA maps streams to hardware queues in creation
+    order over the context's life, so a long-lived test process could make
+    two live peer-blocking streams share a queue.  A rank that hangs ends the
+    worker after `timeout` s with the executor's hang report."""
     world = cfg["P"] * cfg["dp"]
-    os.environ["JANUS_HANG_REPORT"] = str(timeout)
-    try:
-        with tempfile.TemporaryDirectory() as d:
-            cfg = dict(cfg, dir=d)
-            res, errs = [None] * world, [None] * world
-            bar = threading.Barrier(world)
-
-            def one(r):
-                try:
-                    comm = J.Comm.threads(d, world, r, 0)
-                    try:
-                        res[r] = W.run_rank(J, cfg, r, comm, barrier=lambda: bar.wait(timeout))
-                    finally:
-                        comm.close()
-                except Exception as ex:  # noqa: BLE001
-                    errs[r] = ex
-
-            ts = [threading.Thread(target=one, args=(r,)) for r in range(world)]
-            for t in ts:
-                t.start()
-            for t in ts:
-                t.join()
-            bad = [f"rank {r}: {e!r}" for r, e in enumerate(errs) if e is not None]
-            assert not bad, "\n".join(bad)
-            return res
-    finally:
-        os.environ.pop("JANUS_HANG_REPORT", None)
+    with tempfile.TemporaryDirectory() as d:
+        prefix = os.path.join(d, "out")
+        env = dict(os.environ, JANUS_HANG_REPORT=str(max(5, timeout - 25)), THREAD_BARRIER_TIMEOUT=str(min(120, timeout)))
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "multirank_worker.py"), json.dumps(cfg), "threads",
+                            prefix], cwd=ROOT, capture_output=True, text=True, timeout=timeout + 30, env=env)
+        assert r.returncode == 0, (r.stdout[-2000:] + r.stderr[-4000:])
+        return [dict(np.load(f"{prefix}.{q}.npz")) for q in range(world)]
 
 
 def run_ranks(cfg, timeout=int(os.environ.get("MULTIRANK_TIMEOUT", 420))):
