@@ -19,6 +19,7 @@
 #include <vector>
 
 #include <cublas_v2.h>
+#include <dlfcn.h>
 
 #include "../../include/janus/errors.hpp"
 
@@ -521,7 +522,14 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
         sc.blas = h;
         JANUS_BLAS(cublasSetWorkspace(h, sc.blas_ws, kWs));
         JANUS_BLAS(cublasSetPointerMode(h, CUBLAS_POINTER_MODE_HOST));
-        if (m.precision == JANUS_PREC_FP32_EMU) JANUS_BLAS(cublasSetEmulationStrategy(h, CUBLAS_EMULATION_STRATEGY_EAGER));
+        if (m.precision == JANUS_PREC_FP32_EMU) {
+          // cuBLAS >= 12.9 only; resolved at run time, since a host that loads
+          // an older libcublas first (e.g. torch's bundled 12.8) must still load us
+          using SetEmu = cublasStatus_t (*)(cublasHandle_t, cublasEmulationStrategy_t);
+          auto fn = reinterpret_cast<SetEmu>(dlsym(RTLD_DEFAULT, "cublasSetEmulationStrategy"));
+          if (!fn) throw config_error("JANUS_PREC_FP32_EMU needs cuBLAS >= 12.9 (BF16x9 emulation)");
+          JANUS_BLAS(fn(h, CUBLAS_EMULATION_STRATEGY_EAGER));
+        }
         continue;
       }
       sc.partial = dalloc<float>(st, NA * static_cast<size_t>(EC::PE), false);

@@ -52,8 +52,13 @@ def test_wide_matches_oracle(janus, oracle, has_gpu, H, R, prec):
     m = janus.Model(L=2, H=H, R=R, precision=prec, generic=True)
     params = m.synth_params(5)
     batches = [janus.synth_batch(m, [24, 30], 0.095, 31), janus.synth_batch(m, [40], 0.095, 32)]
+    try:
+        st = run_stage(janus, m, params, batches)
+    except janus.JanusError as ex:  # BF16x9 emulation: the process's libcublas may predate 12.9
+        if "needs cuBLAS >= 12.9" in str(ex):
+            pytest.skip(str(ex))
+        raise
     refs = oracle_refs(janus, oracle, m, params, batches)
-    st = run_stage(janus, m, params, batches)
     for i, (b, r) in enumerate(zip(batches, refs)):
         E, lE = st.energy(i, b.n_struct)
         F, lF = st.forces(i, b.n_atoms)
