@@ -81,6 +81,7 @@ def run_threads(J, cfg, timeout):
                     comm.close()
             except Exception as ex:  # noqa: BLE001
                 errs[r] = ex
+                print(f"rank {r} error: {ex!r}", file=sys.stderr, flush=True)
 
         ts = [threading.Thread(target=one, args=(r,)) for r in range(world)]
         for t in ts:

@@ -186,8 +186,15 @@ def test_thread_ranks_share_hardware_queues(janus, gpu):
     context's 32 hardware queues: refused at create (a peer-blocked stream
     would stall the unrelated streams sharing its queue — measured: a hang)."""
     cfg = dict(BASE, P=4, method=1, k=4)
-    with pytest.raises(AssertionError, match="ranks of this process"):
-        run_ranks_threads(cfg, timeout=60)
+    env = dict(os.environ, THREAD_BARRIER_TIMEOUT="20")
+    try:  # the refused rank reports at create; its peers then give up at the barrier (or hang in teardown)
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "multirank_worker.py"), json.dumps(cfg), "threads",
+                            "/tmp/unused"], cwd=ROOT, capture_output=True, text=True, timeout=60, env=env)
+        out = r.stdout + r.stderr
+        assert r.returncode != 0
+    except subprocess.TimeoutExpired as ex:
+        out = "".join(x.decode(errors="replace") if isinstance(x, bytes) else (x or "") for x in (ex.stdout, ex.stderr))
+    assert "ranks of this process" in out, out[-3000:]
 
 
 def test_per_rank_runtime_checks(janus, gpu):
