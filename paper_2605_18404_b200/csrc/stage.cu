@@ -47,6 +47,10 @@
 #include "node_kernels.cuh"
 #include "wide.cuh"
 #include "wgrad_tc.cuh"
+#include "upd_tc.cuh"
+#ifndef JANUS_UPD_TC
+#define JANUS_UPD_TC 1  // tf32 mode: upd units on tcgen05 (upd_tc.cuh); 0 = the SIMT kernels (A/B builds)
+#endif
 #include "stage.cuh"
 #include "stage_api.hpp"
 #include "nbrlist.hpp"
@@ -243,10 +247,12 @@ void refresh_transposes(janus_stage* st, cudaStream_t s) {
         node::transpose_kernel<kH><<<b, 256, 0, s>>>(P + R * H + H + H * H + H, t + H * H);
         edge_tc::pack_msg_weights<<<b, 256, 0, s>>>(P, P + R * H, P + R * H + H, P + R * H + H + H * H,
                                                      P + R * H + H + H * H + H, t + 2 * H * H);
+        upd_tc::pack_msg_w<<<b, 256, 0, s>>>(P + R * H + H + H * H + H, t + 2 * H * H);
         break;
       case kUpd:
         node::transpose_kernel<kH><<<b, 256, 0, s>>>(P, t);
         node::transpose_kernel<kH><<<b, 256, 0, s>>>(P + H * H + H, t + H * H);
+        upd_tc::pack_upd_weights<<<b, 256, 0, s>>>(P, P + H * H + H, t + 2 * H * H);
         break;
       case kReadout:
         node::transpose_kernel<kH><<<b, 256, 0, s>>>(P, t);
@@ -378,7 +384,10 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
     for (int u = st->u0; u < st->u1; ++u) {
       const UnitKind k = unit_kind(u, m.L);
       // msg: [Bt | Wt | tensor-core pack]; upd: [Ut | Vt]; readout: [Ot]
-      const size_t n = k == kMsg ? 2 * kH * kH + edge_tc::kPackBytes / sizeof(float) : (k == kReadout ? 1 : 2) * kH * kH;
+      // + the tensor-core node images: msg [W | W_lo] after its pack, upd the 8-tile image (upd_tc.cuh)
+      const size_t n = k == kMsg    ? 2 * kH * kH + upd_tc::kMsgPackBytes / sizeof(float)
+                       : k == kUpd  ? 2 * kH * kH + upd_tc::kUpdPackBytes / sizeof(float)
+                                    : static_cast<size_t>(kH) * kH;
       st->tw.push_back(k == kEmbed || wide ? nullptr : dalloc<float>(st, n, true));
     }
     // geometry per micro-batch
@@ -553,6 +562,11 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
     JANUS_CUDA(cudaFuncSetAttribute(edge_tc::msg_be_pair_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge_tc::be_pair_smem()));
     JANUS_CUDA(cudaFuncSetAttribute(edge_tc::msg_bf_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge_tc::bf_smem()));
     JANUS_CUDA(cudaFuncSetAttribute(edge_tc::msg_be_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)edge_tc::be_smem()));
+    JANUS_CUDA(cudaFuncSetAttribute(upd_tc::upd_fe_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_tc::upd_tc_smem(6, 2)));
+    JANUS_CUDA(cudaFuncSetAttribute(upd_tc::upd_ff_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_tc::upd_tc_smem(4, 2)));
+    JANUS_CUDA(cudaFuncSetAttribute(upd_tc::upd_bf_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_tc::upd_tc_smem(5, 2)));
+    JANUS_CUDA(cudaFuncSetAttribute(upd_tc::upd_be_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_tc::upd_tc_smem(2, 1)));
+    JANUS_CUDA(cudaFuncSetAttribute(upd_tc::rows_w_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_tc::upd_tc_smem(2, 2)));
     if (!wide) refresh_transposes(st, nullptr);
     JANUS_CUDA(cudaDeviceSynchronize());
   } catch (...) {
@@ -864,7 +878,13 @@ void stage_fe(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
         break;
       case kMsg: {
         const float* W = P + R * H + H + H * H + H;
-        if (!v_ready) gemm(s, N, cur_h, W, nullptr, nullptr, nullptr, b.v);
+        if (v_ready) {
+        } else if (use_tc(st) && JANUS_UPD_TC) {  // the fused next-v product's bits (upd_tc.cuh rows_w_tc)
+          upd_tc::rows_w_tc<<<blocks(N, 128), edge_tc::NT, upd_tc::upd_tc_smem(2, 2), s>>>(N, cur_h, msg_params(st, u).pack,
+                                                                                         1, b.v);
+        } else {
+          gemm(s, N, cur_h, W, nullptr, nullptr, nullptr, b.v);
+        }
         v_ready = false;
         if (pairs) {
           if (!(prof_skip() & 1))
@@ -883,9 +903,14 @@ void stage_fe(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
         const bool fuse = u + 1 < st->u1 && unit_kind(u + 1, L) == kMsg;
         const float* Wn = fuse ? st->P(u + 1) + R * H + H + H * H + H : nullptr;
         float* vn = fuse ? sl.units[static_cast<size_t>(u + 1 - st->u0)].v : nullptr;
-        if (!(prof_skip() & 32))
-          JANUS_UPD(upd_fe_fused, node::upd_smem(fuse ? 3 : 2), s, N, cur_m, cur_h, Um, ups, V, b.p,
-                                                                                              b.out_h, Wn, vn);
+        if (prof_skip() & 32) {
+        } else if (use_tc(st) && JANUS_UPD_TC) {  // upd_tc.cuh: 128 atoms per CTA, 3xTF32 tcgen05 chain
+          const float* T = st->tw[static_cast<size_t>(u - st->u0)];
+          upd_tc::upd_fe_tc<<<blocks(N, 128), edge_tc::NT, upd_tc::upd_tc_smem(6, 2), s>>>(
+              N, cur_m, cur_h, T + 2 * H * H, ups, b.p, b.out_h, fuse ? msg_params(st, u + 1).pack : nullptr, vn);
+        } else {
+          JANUS_UPD(upd_fe_fused, node::upd_smem(fuse ? 3 : 2), s, N, cur_m, cur_h, Um, ups, V, b.p, b.out_h, Wn, vn);
+        }
         v_ready = fuse;
         cur_h = b.out_h;
         cur_m = nullptr;
@@ -943,7 +968,13 @@ void stage_ff(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
       case kUpd: {  // ff_a = a'; a_m = ((a' V^T) SiLU'(p)) U^T, written straight into the
                     // preceding msg unit's saved FF input when it is on this stage
         float* am_dst = (u - 1 >= st->u0) ? sl.units[static_cast<size_t>(u - 1 - st->u0)].ff_a : wm;
-        if (!(prof_skip() & 32)) JANUS_UPD(upd_ff_fused, node::upd_smem(2), s, N, wh, b.p, T + H * H, T, b.ff_a, am_dst);
+        if (prof_skip() & 32) {
+        } else if (use_tc(st) && JANUS_UPD_TC) {
+          upd_tc::upd_ff_tc<<<blocks(N, 128), edge_tc::NT, upd_tc::upd_tc_smem(4, 2), s>>>(N, wh, b.p, T + 2 * H * H, b.ff_a,
+                                                                                         am_dst);
+        } else {
+          JANUS_UPD(upd_ff_fused, node::upd_smem(2), s, N, wh, b.p, T + H * H, T, b.ff_a, am_dst);
+        }
         break;
       }
       case kMsg: {
@@ -1027,7 +1058,13 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
         break;
       case kMsg: {
         const float* W = P + R * H + H + H * H + H;
-        if (!vdot_ready) gemm(s, N, ah, W, nullptr, nullptr, nullptr, sc.s1);  // vdot
+        if (vdot_ready) {
+        } else if (use_tc(st) && JANUS_UPD_TC) {  // vdot with the fused product's bits
+          upd_tc::rows_w_tc<<<blocks(N, 128), edge_tc::NT, upd_tc::upd_tc_smem(2, 2), s>>>(N, ah, msg_params(st, u).pack,
+                                                                                         0, sc.s1);
+        } else {
+          gemm(s, N, ah, W, nullptr, nullptr, nullptr, sc.s1);  // vdot
+        }
         vdot_ready = false;
         const bool pairs = use_tc(st) && st->pair_bfbe;
         if (pairs) {  // weight gradients once per pair + row sums from the stored filters (+ hbar^F = X W^T)
@@ -1074,10 +1111,15 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
         // + the next msg unit's vdot = abar_h' W in the same kernel
         const bool fuse = u + 1 < st->u1 && unit_kind(u + 1, L) == kMsg;
         const float* Wn = fuse ? st->P(u + 1) + R * H + H + H * H + H : nullptr;
-        if (!(prof_skip() & 32))
-          JANUS_UPD(upd_bf_fused, node::upd_smem(fuse ? 5 : 4), s, N, am, b.ff_a, b.p, Um, T + H * H, T, V,
-                                                                                              sc.s3, sc.s4, sc.s5, b.inj, ah, ah_alt, Wn,
-                                                                                              fuse ? sc.s1 : nullptr);
+        if (prof_skip() & 32) {
+        } else if (use_tc(st) && JANUS_UPD_TC) {
+          upd_tc::upd_bf_tc<<<blocks(N, 128), edge_tc::NT, upd_tc::upd_tc_smem(5, 2), s>>>(
+              N, am, b.ff_a, b.p, T + 2 * H * H, sc.s3, sc.s4, sc.s5, b.inj, ah, ah_alt,
+              fuse ? msg_params(st, u + 1).pack : nullptr, fuse ? sc.s1 : nullptr);
+        } else {
+          JANUS_UPD(upd_bf_fused, node::upd_smem(fuse ? 5 : 4), s, N, am, b.ff_a, b.p, Um, T + H * H, T, V, sc.s3, sc.s4,
+                    sc.s5, b.inj, ah, ah_alt, Wn, fuse ? sc.s1 : nullptr);
+        }
         vdot_ready = fuse;
         std::swap(ah, ah_alt);
         const node::WJob jv = wjob(sc.s5, b.ff_a, dV);                                       // dV2 = u^T a'
@@ -1167,7 +1209,13 @@ void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only, 
       case kUpd: {
         float *dU = G1, *dups = G1 + H * H, *dV = G1 + H * H + H;
         // pbar (s2) = (b' V^T) SiLU'(p); b_m = pbar U^T + mbar^F
-        if (!(prof_skip() & 32)) JANUS_UPD(upd_be_fused, node::upd_smem(2), s, N, bh, b.p, T + H * H, T, b.inj, sc.s2, bm);
+        if (prof_skip() & 32) {
+        } else if (use_tc(st) && JANUS_UPD_TC) {
+          upd_tc::upd_be_tc<<<blocks(N, 128), edge_tc::NT, upd_tc::upd_tc_smem(2, 1), s>>>(N, bh, b.p, T + 2 * H * H, b.inj,
+                                                                                          sc.s2, bm);
+        } else {
+          JANUS_UPD(upd_be_fused, node::upd_smem(2), s, N, bh, b.p, T + H * H, T, b.inj, sc.s2, bm);
+        }
         const node::WJob jv = wjob(b.p, bh, dV, nullptr, nullptr, true);                           // dV1 = SiLU(p)^T b'
         const node::WJob ju = wjob(in_m(st, sl, u, N), sc.s2, dU, nullptr, nullptr, false, sc.s2, dups);  // dU1, dups1
         if (has_pend)
