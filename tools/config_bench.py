@@ -8,7 +8,7 @@ tf32 tensor-core path, device-built neighbour lists:
   C4  L=4 H=64, mixed 128..1024-atom cells packed by GARS into 16 micro-batches
   C5  L=4 H=64, 4096-atom cells at rho 0.19 (~100 neighbours), 8 micro-batches
 
-(C3's H=256 needs 256-wide edge tiles: not built.)  One JSON
+(C3, H=256, runs on the generic-width path: tools/c3_report.py.)  One JSON
 line per config: structures/s, atoms/s, edges/s and step-level edge TFLOP/s.
 """
 import json
