@@ -286,6 +286,12 @@ float* ledger(janus_stage* st, float* base, int mb, int u) {
 }
 
 bool use_tc(const janus_stage* st) { return st->m.precision == JANUS_PREC_TF32; }
+// tf32 mode: the upd units (and unfused msg v / vdot) on tcgen05 from 128-atom
+// micro-batches; below one full 128-row CTA the SIMT kernels' 16-row CTAs win
+// the latency-bound chain (C1, 64-atom cells: 7100 vs 6630 structures/s;
+// C2 17630 vs 18990).  A function of the micro-batch only, so every stage of
+// a staged run picks the same kernels (bit-identical to unstaged).
+bool upd_on_tc(const janus_stage* st, int N) { return use_tc(st) && JANUS_UPD_TC && N >= 128; }
 // undirected edge-pair tables (pair_tc.cuh): the tensor-core H=64 kernels and the generic-width path
 bool needs_pairs(const janus_stage* st) { return use_tc(st) || st->wide; }
 // Tensor-core edge grids.  CTAs loop over tiles (static assignment), so a CTA
@@ -879,7 +885,7 @@ void stage_fe(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
       case kMsg: {
         const float* W = P + R * H + H + H * H + H;
         if (v_ready) {
-        } else if (use_tc(st) && JANUS_UPD_TC) {  // the fused next-v product's bits (upd_tc.cuh rows_w_tc)
+        } else if (upd_on_tc(st, N)) {  // the fused next-v product's bits (upd_tc.cuh rows_w_tc)
           upd_tc::rows_w_tc<<<blocks(N, 128), edge_tc::NT, upd_tc::upd_tc_smem(2, 2), s>>>(N, cur_h, msg_params(st, u).pack,
                                                                                          1, b.v);
         } else {
@@ -904,7 +910,7 @@ void stage_fe(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
         const float* Wn = fuse ? st->P(u + 1) + R * H + H + H * H + H : nullptr;
         float* vn = fuse ? sl.units[static_cast<size_t>(u + 1 - st->u0)].v : nullptr;
         if (prof_skip() & 32) {
-        } else if (use_tc(st) && JANUS_UPD_TC) {  // upd_tc.cuh: 128 atoms per CTA, 3xTF32 tcgen05 chain
+        } else if (upd_on_tc(st, N)) {  // upd_tc.cuh: 128 atoms per CTA, 3xTF32 tcgen05 chain
           const float* T = st->tw[static_cast<size_t>(u - st->u0)];
           upd_tc::upd_fe_tc<<<blocks(N, 128), edge_tc::NT, upd_tc::upd_tc_smem(6, 2), s>>>(
               N, cur_m, cur_h, T + 2 * H * H, ups, b.p, b.out_h, fuse ? msg_params(st, u + 1).pack : nullptr, vn);
@@ -969,7 +975,7 @@ void stage_ff(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
                     // preceding msg unit's saved FF input when it is on this stage
         float* am_dst = (u - 1 >= st->u0) ? sl.units[static_cast<size_t>(u - 1 - st->u0)].ff_a : wm;
         if (prof_skip() & 32) {
-        } else if (use_tc(st) && JANUS_UPD_TC) {
+        } else if (upd_on_tc(st, N)) {
           upd_tc::upd_ff_tc<<<blocks(N, 128), edge_tc::NT, upd_tc::upd_tc_smem(4, 2), s>>>(N, wh, b.p, T + 2 * H * H, b.ff_a,
                                                                                          am_dst);
         } else {
@@ -1059,7 +1065,7 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
       case kMsg: {
         const float* W = P + R * H + H + H * H + H;
         if (vdot_ready) {
-        } else if (use_tc(st) && JANUS_UPD_TC) {  // vdot with the fused product's bits
+        } else if (upd_on_tc(st, N)) {  // vdot with the fused product's bits
           upd_tc::rows_w_tc<<<blocks(N, 128), edge_tc::NT, upd_tc::upd_tc_smem(2, 2), s>>>(N, ah, msg_params(st, u).pack,
                                                                                          0, sc.s1);
         } else {
@@ -1112,7 +1118,7 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
         const bool fuse = u + 1 < st->u1 && unit_kind(u + 1, L) == kMsg;
         const float* Wn = fuse ? st->P(u + 1) + R * H + H + H * H + H : nullptr;
         if (prof_skip() & 32) {
-        } else if (use_tc(st) && JANUS_UPD_TC) {
+        } else if (upd_on_tc(st, N)) {
           upd_tc::upd_bf_tc<<<blocks(N, 128), edge_tc::NT, upd_tc::upd_tc_smem(5, 2), s>>>(
               N, am, b.ff_a, b.p, T + 2 * H * H, sc.s3, sc.s4, sc.s5, b.inj, ah, ah_alt,
               fuse ? msg_params(st, u + 1).pack : nullptr, fuse ? sc.s1 : nullptr);
@@ -1210,7 +1216,7 @@ void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only, 
         float *dU = G1, *dups = G1 + H * H, *dV = G1 + H * H + H;
         // pbar (s2) = (b' V^T) SiLU'(p); b_m = pbar U^T + mbar^F
         if (prof_skip() & 32) {
-        } else if (use_tc(st) && JANUS_UPD_TC) {
+        } else if (upd_on_tc(st, N)) {
           upd_tc::upd_be_tc<<<blocks(N, 128), edge_tc::NT, upd_tc::upd_tc_smem(2, 1), s>>>(N, bh, b.p, T + 2 * H * H, b.inj,
                                                                                           sc.s2, bm);
         } else {

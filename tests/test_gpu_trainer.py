@@ -173,19 +173,21 @@ def test_pipelined_loads_bit_identical(janus, data, graphs):
     tb.close()
 
 
-@pytest.mark.parametrize("P,method,k", [(4, 1, 8), (2, 0, 1)])
-def test_tensor_core_pipeline_lanes_bit_identical(janus, P, method, k):
+@pytest.mark.parametrize("P,method,k,atoms", [(4, 1, 8, 64), (2, 0, 1, 64), (4, 1, 8, 128), (3, 0, 1, 128)])
+def test_tensor_core_pipeline_lanes_bit_identical(janus, P, method, k, atoms):
     """The N>1 bench configuration on one GPU: tensor-core kernels, device-built
     neighbour lists, P pipeline stages with 8 compute lanes per stage and
-    double-buffered loads — bit-identical to one stage with the same lanes."""
+    double-buffered loads — bit-identical to one stage with the same lanes.
+    128-atom cells take the tcgen05 upd kernels (upd_tc.cuh), including the
+    unfused next-v products at stage starts; 64-atom cells the SIMT ones."""
     if not janus.device_count():
         pytest.skip("no GPU")
     m = janus.Model(L=2, H=64, R=64, precision=janus.PREC_TF32)
     params = m.synth_params(8)
-    bs = [janus.synth_batch(m, [64 + 8 * (i % 3)], 0.095, 300 + i, device_nl=True) for i in range(16)]
+    bs = [janus.synth_batch(m, [atoms + 8 * (i % 3)], 0.095, 300 + i, device_nl=True) for i in range(16)]
     out = []
     for PP, meth, kk in ((1, janus.METHOD_SYMFOLD, 1), (P, method, k)):
-        t = janus.Trainer(m, params, PP, meth, len(bs), k=kk, max_atoms=96, max_edges=96 * 80, lanes=8,
+        t = janus.Trainer(m, params, PP, meth, len(bs), k=kk, max_atoms=atoms + 32, max_edges=(atoms + 32) * 80, lanes=8,
                           graphs=True)
         t.load_many(bs)
         losses = []
