@@ -450,6 +450,7 @@ __global__ void __maxnreg__(JANUS_BF_MAXNREG) msg_bf_pair_tc(EdgeGeom g, const f
                                                        float rc, const float* __restrict__ v, const float* __restrict__ vdot,
                                                        const float* __restrict__ am, const float* __restrict__ Fbar,
                                                        float* __restrict__ partial) {
+  TC_DECL;
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = align1024(sm_raw);
   uint8_t* W2b = sm;  // bf16 weights in pack order: B | A^T | B^T
@@ -475,6 +476,7 @@ __global__ void __maxnreg__(JANUS_BF_MAXNREG) msg_bf_pair_tc(EdgeGeom g, const f
   load_weights_b16(W2b, p.pack, al, be, &wbar);
   if (threadIdx.x < 128) csa[threadIdx.x] = 0.f;
   setup(c, &tslot, 512);
+  TC_M();
   const uint32_t aW0b = tc::smem_u32(W0b), aW2b = tc::smem_u32(W2b);
   const uint32_t aB0 = tc::smem_u32(B0), aB1 = tc::smem_u32(B1), aB2 = tc::smem_u32(B2), aB3 = tc::smem_u32(B3);
   const uint32_t aB4 = tc::smem_u32(B4), aB5 = tc::smem_u32(B5);
@@ -491,15 +493,19 @@ __global__ void __maxnreg__(JANUS_BF_MAXNREG) msg_bf_pair_tc(EdgeGeom g, const f
       st_b16(B4, c.e, f0, ph);
       st_b16(B5, c.e, f0, dph);
     }
+    TC_M();
     bf_adjoints_rows(pg, n_pairs, ch * TE, Fbar, v, vdot, am, B2, B3);  // mu (B of dB, A of sbar), nu
+    TC_M();
     tc::mbar_wait(&wbar, 0);
     c.publish();
+    TC_M();
     if (threadIdx.x == 0) {
       mma_kb16(c.tmem + TM_Z, aB4, aW0b);
       mma_kb16(c.tmem + TM_ZP, aB5, aW0b);
       tc::commit(c.mbar);
     }
     c.wait_mma();
+    TC_M();
     {
       float z[FPT], zp[FPT];
       c.ld2(TM_Z, TM_ZP, z, zp);
@@ -521,7 +527,9 @@ __global__ void __maxnreg__(JANUS_BF_MAXNREG) msg_bf_pair_tc(EdgeGeom g, const f
       tc::commit(c.mbar);
     }
     b16_colsum_add(B2, csb);  // dbeta += sum mu
+    TC_M();
     c.wait_mma();
+    TC_M();
     __syncthreads();  // column sums done: B2, B3 may be rewritten
     {
       float z[FPT], zp[FPT], sb[FPT], sdb[FPT];
@@ -545,7 +553,9 @@ __global__ void __maxnreg__(JANUS_BF_MAXNREG) msg_bf_pair_tc(EdgeGeom g, const f
       tc::commit(c.mbar);
     }
     b16_colsum_add(B2, csa);  // dalpha += sum zbar
+    TC_M();
     c.wait_mma();
+    TC_M();
     first = false;
     __syncthreads();
   }
@@ -555,13 +565,17 @@ __global__ void __maxnreg__(JANUS_BF_MAXNREG) msg_bf_pair_tc(EdgeGeom g, const f
     teardown(c, 512);
     return;
   }
-  write_partial(c, part, B0, csa, csb);
+  TC_M();
+  write_partial(c, part, B0, csa, csb TC_PASS);
+  TC_M();
+  TC_DUMP("bf_pair");
   teardown(c, 512);
 }
 
 __global__ void __maxnreg__(JANUS_BE_MAXNREG) msg_be_pair_tc(EdgeGeom g, const float4* __restrict__ pg, int n_pairs, MsgParams p,
                                                        float rc, const float* __restrict__ v, const float* __restrict__ bm,
                                                        float* __restrict__ partial) {
+  TC_DECL;
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = align1024(sm_raw);
   uint8_t* W2b = sm;
@@ -649,7 +663,7 @@ __global__ void __maxnreg__(JANUS_BE_MAXNREG) msg_be_pair_tc(EdgeGeom g, const f
     teardown(c, 512);
     return;
   }
-  write_partial(c, part, B0, csa, csb);
+  write_partial(c, part, B0, csa, csb TC_PASS);
   teardown(c, 512);
 }
 

@@ -56,12 +56,17 @@ def measure(name, model, params, batches, lanes=None, steps=10, warmup=3):
 
 
 def main():
+    only = sys.argv[sys.argv.index("--only") + 1] if "--only" in sys.argv else None
     model = J.Model(L=4, H=64, R=64, r_c=5.0, precision=J.PREC_TF32)
     params = model.synth_params(7)
-    measure("C1: 64-atom cells, N_mb=4", model, params,
-            [J.synth_batch(model, [64], 0.095, 10 + i, device_nl=True) for i in range(4)])
-    measure("C2: 256-atom cells, N_mb=32", model, params,
-            [J.synth_batch(model, [256], 0.095, 700 + i, device_nl=True) for i in range(32)])
+    if only in (None, "C1"):
+        measure("C1: 64-atom cells, N_mb=4", model, params,
+                [J.synth_batch(model, [64], 0.095, 10 + i, device_nl=True) for i in range(4)])
+    if only in (None, "C2"):
+        measure("C2: 256-atom cells, N_mb=32", model, params,
+                [J.synth_batch(model, [256], 0.095, 700 + i, device_nl=True) for i in range(32)])
+    if only is not None:
+        return
     rng = np.random.default_rng(11)
     sizes = [int(x) for x in rng.choice(C4_SIZES, size=64)]
     cells = [J.synth_cell(n, 0.095, model.n_species, 50000 + i) for i, n in enumerate(sizes)]
