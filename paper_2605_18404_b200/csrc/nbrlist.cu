@@ -13,12 +13,13 @@
 //   bin      : atom -> (structure, cell) with a wrap index; counting sort of
 //              atoms by cell (positions copied cell-major so a stencil walk
 //              reads contiguous memory)
-//   count    : one warp per atom walks the (2m+1)^3 stencil of cells
+//   walk_pad : one warp per atom walks the (2m+1)^3 stencil of cells once,
+//              counts its row and keeps the 64-bit keys (j, s) of rows up to
+//              kPadCap rank-sorted in a padded per-atom buffer (keys are
+//              unique, so rank = #smaller keys is a permutation) — the cell
+//              order inside a bin (from atomics) never reaches the output
 //   scan     : row_ptr (single CTA, deterministic)
-//   fill     : the same walk writes 64-bit keys (j, s) at warp-ballot
-//              positions; the row is then rank-sorted in shared memory (keys
-//              are unique, so rank = #smaller keys is a permutation) — the
-//              cell order inside a bin (from atomics) never reaches the output
+//   compact  : padded rows -> CSR (a row over kPadCap is walked again)
 //   rev      : binary search of (i, -s) in row j's sorted keys
 // Cells are >= r_c (1 + 1e-6) wide, so the rounding of the binning can move a
 // pair by at most one cell and a 3x3x3 stencil still covers it; boxes smaller
@@ -50,6 +51,7 @@ struct StructMeta {  // per structure, built on the host from the box lengths
 
 constexpr int kWarps = 8;        // warps per CTA in the row kernels
 constexpr int kSortCap = 512;    // keys per warp staged in shared memory
+constexpr int kPadCap = 128;     // sorted keys per atom kept by the single-walk pass (denser rows re-walk)
 
 __device__ __forceinline__ int floordiv(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
 
@@ -219,35 +221,10 @@ __device__ __forceinline__ void walk(int i, const double* __restrict__ pos, cons
       const int *__restrict__ cell_of, const int4 *__restrict__ cw, const int *__restrict__ cell_start,         \
       const int *__restrict__ c_atom, const double *__restrict__ c_pos, const int4 *__restrict__ c_w, double rc2
 
-__global__ void __launch_bounds__(kWarps * 32) count_kernel(int n, NBR_WALK_PARAMS, int* __restrict__ deg) {
-  const int lane = threadIdx.x & 31;
-  const int i = blockIdx.x * kWarps + (threadIdx.x >> 5);
-  if (i >= n) return;
-  int cnt = 0;
-  walk(i, NBR_WALK_ARGS, lane, [&](bool hit, unsigned long long) { cnt += hit; });
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-  if (lane == 0) deg[i] = cnt;
-}
-
-__global__ void __launch_bounds__(kWarps * 32) fill_kernel(int n, NBR_WALK_PARAMS, const int* __restrict__ row_ptr,
-                                                           int max_edges, unsigned long long* __restrict__ tmp,
-                                                           unsigned long long* __restrict__ skey,
-                                                           int* __restrict__ col, int* __restrict__ shift) {
-  __shared__ unsigned long long sk[kWarps][kSortCap];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int i = blockIdx.x * kWarps + w;
-  if (i >= n || row_ptr[n] > max_edges) return;
-  const int base = row_ptr[i], deg = row_ptr[i + 1] - base;
-  const bool in_smem = deg <= kSortCap;
-  unsigned long long* buf = in_smem ? sk[w] : tmp + base;
-  int cnt = 0;  // warp-uniform running count
-  walk(i, NBR_WALK_ARGS, lane, [&](bool hit, unsigned long long key) {
-    const unsigned m = __ballot_sync(0xffffffffu, hit);
-    if (hit) buf[cnt + __popc(m & ((1u << lane) - 1u))] = key;
-    cnt += __popc(m);
-  });
-  __syncwarp();
+// rank-sort the warp's n keys in buf (unique) and emit them at row offset base
+__device__ __forceinline__ void emit_sorted(const unsigned long long* buf, int deg, int base, int lane,
+                                            unsigned long long* __restrict__ skey, int* __restrict__ col,
+                                            int* __restrict__ shift) {
   for (int k = lane; k < deg; k += 32) {
     const unsigned long long key = buf[k];
     int rank = 0;
@@ -259,6 +236,68 @@ __global__ void __launch_bounds__(kWarps * 32) fill_kernel(int n, NBR_WALK_PARAM
     shift[3 * e + 1] = static_cast<int>((key >> 8) & 0xff) - 128;
     shift[3 * e + 2] = static_cast<int>(key & 0xff) - 128;
   }
+}
+
+// Single walk per atom: count the row and, when it has <= kPadCap neighbours
+// (every row at the configs' densities), keep its keys sorted in a padded
+// per-atom buffer, so the CSR needs no second walk (compact_kernel).  Rows
+// above kPadCap are only counted here and re-walked by compact_kernel.
+__global__ void __launch_bounds__(kWarps * 32) walk_pad_kernel(int n, NBR_WALK_PARAMS, int* __restrict__ deg,
+                                                               unsigned long long* __restrict__ pad) {
+  __shared__ unsigned long long sk[kWarps][kPadCap];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int i = blockIdx.x * kWarps + w;
+  if (i >= n) return;
+  int cnt = 0;
+  walk(i, NBR_WALK_ARGS, lane, [&](bool hit, unsigned long long key) {
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    const int slot = cnt + __popc(m & ((1u << lane) - 1u));
+    if (hit && slot < kPadCap) sk[w][slot] = key;
+    cnt += __popc(m);
+  });
+  __syncwarp();
+  if (lane == 0) deg[i] = cnt;
+  if (cnt > kPadCap) return;
+  for (int k = lane; k < cnt; k += 32) {
+    const unsigned long long key = sk[w][k];
+    int rank = 0;
+    for (int q = 0; q < cnt; ++q) rank += sk[w][q] < key;
+    pad[static_cast<size_t>(i) * kPadCap + rank] = key;
+  }
+}
+
+// CSR from the padded rows (rows over kPadCap: walk again, sort through tmp)
+__global__ void __launch_bounds__(kWarps * 32) compact_kernel(int n, NBR_WALK_PARAMS, const int* __restrict__ row_ptr,
+                                                              int max_edges, const unsigned long long* __restrict__ pad,
+                                                              unsigned long long* __restrict__ tmp,
+                                                              unsigned long long* __restrict__ skey,
+                                                              int* __restrict__ col, int* __restrict__ shift) {
+  __shared__ unsigned long long sk[kWarps][kSortCap];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int i = blockIdx.x * kWarps + w;
+  if (i >= n || row_ptr[n] > max_edges) return;
+  const int base = row_ptr[i], deg = row_ptr[i + 1] - base;
+  if (deg <= kPadCap) {
+    for (int k = lane; k < deg; k += 32) {
+      const unsigned long long key = pad[static_cast<size_t>(i) * kPadCap + k];
+      const int e = base + k;
+      skey[e] = key;
+      col[e] = static_cast<int>(key >> 24);
+      shift[3 * e + 0] = static_cast<int>((key >> 16) & 0xff) - 128;
+      shift[3 * e + 1] = static_cast<int>((key >> 8) & 0xff) - 128;
+      shift[3 * e + 2] = static_cast<int>(key & 0xff) - 128;
+    }
+    return;
+  }
+  unsigned long long* buf = deg <= kSortCap ? sk[w] : tmp + base;
+  int cnt = 0;  // warp-uniform running count
+  walk(i, NBR_WALK_ARGS, lane, [&](bool hit, unsigned long long key) {
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    if (hit) buf[cnt + __popc(m & ((1u << lane) - 1u))] = key;
+    cnt += __popc(m);
+  });
+  __syncwarp();
+  emit_sorted(buf, deg, base, lane, skey, col, shift);
 }
 
 __global__ void __launch_bounds__(kWarps * 32) rev_kernel(int n, const int* __restrict__ row_ptr, int max_edges,
@@ -315,7 +354,7 @@ struct janus_nbrlist {
   int *cell_of = nullptr, *c_atom = nullptr, *deg = nullptr, *err = nullptr;
   int4 *cw = nullptr, *c_w = nullptr;
   double* c_pos = nullptr;
-  unsigned long long *tmp = nullptr, *skey = nullptr;
+  unsigned long long *tmp = nullptr, *skey = nullptr, *pad = nullptr;  // pad: [atoms][kPadCap] sorted rows (walk_pad)
   int* h_small = nullptr;  // pinned: [0] = E, [1] = err
   bool pending = false;    // enqueued, not yet finished
 };
@@ -353,6 +392,7 @@ janus_nbrlist* nbrlist_create(int max_atoms, int max_struct, int max_edges, int 
     nl->c_pos = dev_alloc<double>(3 * static_cast<size_t>(max_atoms));
     nl->tmp = dev_alloc<unsigned long long>(max_edges);
     nl->skey = dev_alloc<unsigned long long>(max_edges);
+    nl->pad = dev_alloc<unsigned long long>(static_cast<size_t>(max_atoms) * nbr::kPadCap);
   } catch (...) {
     nbrlist_destroy(nl);
     throw;
@@ -368,7 +408,7 @@ void nbrlist_destroy(janus_nbrlist* nl) {
                   static_cast<void*>(nl->cell_start), static_cast<void*>(nl->cell_of), static_cast<void*>(nl->c_atom),
                   static_cast<void*>(nl->deg), static_cast<void*>(nl->err), static_cast<void*>(nl->cw),
                   static_cast<void*>(nl->c_w), static_cast<void*>(nl->c_pos), static_cast<void*>(nl->tmp),
-                  static_cast<void*>(nl->skey)})
+                  static_cast<void*>(nl->skey), static_cast<void*>(nl->pad)})
     if (p) cudaFree(p);
   if (nl->h_meta) cudaFreeHost(nl->h_meta);
   if (nl->h_small) cudaFreeHost(nl->h_small);
@@ -419,9 +459,9 @@ void nbrlist_enqueue(janus_nbrlist* nl, int n, int n_struct, const double* pos, 
                                                     nl->c_atom, nl->c_pos, nl->c_w);
   const int rb = nblk(n, nbr::kWarps), rt = nbr::kWarps * 32;
 #define NBR_ARGS pos, struct_id, nl->meta, nl->cell_of, nl->cw, nl->cell_start, nl->c_atom, nl->c_pos, nl->c_w, rc2
-  nbr::count_kernel<<<rb, rt, 0, s>>>(n, NBR_ARGS, nl->deg);
+  nbr::walk_pad_kernel<<<rb, rt, 0, s>>>(n, NBR_ARGS, nl->deg, nl->pad);
   nbr::scan_kernel<<<1, 1024, 0, s>>>(n, nl->deg, row_ptr);
-  nbr::fill_kernel<<<rb, rt, 0, s>>>(n, NBR_ARGS, row_ptr, nl->max_edges, nl->tmp, nl->skey, col, shift);
+  nbr::compact_kernel<<<rb, rt, 0, s>>>(n, NBR_ARGS, row_ptr, nl->max_edges, nl->pad, nl->tmp, nl->skey, col, shift);
 #undef NBR_ARGS
   nbr::rev_kernel<<<rb, rt, 0, s>>>(n, row_ptr, nl->max_edges, nl->skey, rev, nl->err);
   JANUS_LAUNCH_CHECK("nbrlist");

@@ -42,6 +42,9 @@ CASES = [
     ("C4 mixed sizes", [128, 250, 256, 432, 500, 1024], 0.095),
     ("box smaller than r_c (5x5x5 images)", [3, 5], 0.095),
     ("dilute, empty rows", [20], 0.004),
+    # ~160 neighbours per atom: rows above nbrlist.cu's kPadCap (128) take the re-walk path
+    ("very dense rows (> kPadCap)", [400], 0.30),
+    ("dense rows over kSortCap (512)", [1200], 0.99),
 ]
 
 
@@ -49,8 +52,8 @@ CASES = [
 def test_device_nbrlist_bit_exact(gpu, oracle, name, sizes, rho):
     janus = gpu
     pos, sid, cell = cells(janus, sizes, rho, 11)
-    host = janus.nbrlist(pos, sid, cell, 5.0, max_edges=len(pos) * 400)
-    dev = janus.nbrlist_device(pos, sid, cell, 5.0, max_edges=len(pos) * 400)
+    host = janus.nbrlist(pos, sid, cell, 5.0, max_edges=len(pos) * 700)
+    dev = janus.nbrlist_device(pos, sid, cell, 5.0, max_edges=len(pos) * 700)
     assert_same(dev, host)
     if len(pos) <= 1100:  # the oracle's O(N^2) build: keep the CPU part short
         om = oracle.Model(L=1, H=64, R=64, n_species=4, r_c=5.0, w_E=1.0, w_F=10.0)
