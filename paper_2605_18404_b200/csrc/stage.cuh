@@ -88,6 +88,7 @@ struct Scratch {
   // generic-width path (stage_wide.inc): [2 pairs][R] basis stack, three
   // [2 pairs][H] operand stacks, and the lane's cuBLAS handle + workspace
   float *phi2 = nullptr, *z2 = nullptr, *a2 = nullptr, *b2 = nullptr, *cspart = nullptr;
+  unsigned* cstick = nullptr;  // column-sum tickets (one per 32-column strip, zero between launches)
   void* blas = nullptr;
   void* blas_ws = nullptr;
 };

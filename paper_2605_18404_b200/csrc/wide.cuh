@@ -460,13 +460,18 @@ __global__ void __launch_bounds__(256) species_sum_kernel(int N, int S, int cols
   }
 }
 
-// Column sums of X[rows][cols] in two deterministic launches: block (strip of
-// 32 columns, chunk g of rows) -> part[g][cols] (8 warps interleave rows, summed
-// in warp order), then out[c] += sum_g part[g][c] in chunk order.
+// Column sums out[c] += sum_r X[r][c] in ONE deterministic launch: block
+// (strip of 32 columns, chunk g of rows) sums its rows (8 warps interleave,
+// combined in warp order) into part[g][c]; the last block of a strip to
+// finish (atomic ticket, counter reset by it) adds the chunks' partials in
+// chunk order.  The arrival order decides only WHICH block sums, never the
+// order of the sum.
 constexpr int kColChunks = 64;
-__global__ void __launch_bounds__(256) colsum_part_kernel(int rows, int cols, const float* __restrict__ X,
-                                                          float* __restrict__ part) {
+__global__ void __launch_bounds__(256) colsum_kernel(int rows, int cols, const float* __restrict__ X,
+                                                     float* __restrict__ part, unsigned* __restrict__ ticket,
+                                                     float* __restrict__ out) {
   __shared__ float red[8][33];
+  __shared__ bool last;
   const int l = threadIdx.x & 31, w = threadIdx.x >> 5, k = blockIdx.x * 32 + l, g = blockIdx.y;
   const int per = (rows + gridDim.y - 1) / gridDim.y, r0 = g * per, r1 = min(rows, r0 + per);
   float acc = 0.f;
@@ -475,19 +480,24 @@ __global__ void __launch_bounds__(256) colsum_part_kernel(int rows, int cols, co
     for (int r = r0 + w; r < r1; r += 8) acc += __ldg(X + static_cast<size_t>(r) * cols + k);
   red[w][l] = acc;
   __syncthreads();
-  if (w == 0 && k < cols) {
-    float s = 0.f;
+  if (w == 0) {
+    float sum = 0.f;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) s += red[q][l];
-    part[static_cast<size_t>(g) * cols + k] = s;
+    for (int q = 0; q < 8; ++q) sum += red[q][l];
+    if (k < cols) part[static_cast<size_t>(g) * cols + k] = sum;
+    __threadfence();
   }
-}
-__global__ void colsum_final_kernel(int cols, int chunks, const float* __restrict__ part, float* __restrict__ out) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= cols) return;
-  float s = 0.f;
-  for (int g = 0; g < chunks; ++g) s += part[static_cast<size_t>(g) * cols + k];
-  out[k] += s;
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(ticket + blockIdx.x, 1u) == gridDim.y - 1;
+  __syncthreads();
+  if (!last || w != 0) return;
+  __threadfence();
+  if (k < cols) {
+    float sum = 0.f;
+    for (int q = 0; q < static_cast<int>(gridDim.y); ++q) sum += __ldcg(part + static_cast<size_t>(q) * cols + k);
+    out[k] += sum;
+  }
+  if (l == 0) ticket[blockIdx.x] = 0u;  // ready for the next launch on this lane
 }
 
 __global__ void fill_kernel(int64_t n, float* __restrict__ p, float v) {
