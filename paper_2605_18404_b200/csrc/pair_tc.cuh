@@ -371,12 +371,15 @@ __device__ __forceinline__ void st_b16x2(uint8_t* t, int e, int f, float a, floa
   *reinterpret_cast<uint32_t*>(t + off_b16(e, f)) = *reinterpret_cast<const uint32_t*>(&v);
 }
 // BF: mu -> tmu, nu -> tnu for the chunk's 128 pairs (all 16 warps)
-__device__ __forceinline__ void bf_adjoints_rows(const float4* __restrict__ pg, int n_pairs, int p0,
-                                                 const float* __restrict__ Fbar, const float* __restrict__ v,
+// the record of the pair this lane (0..7) holds in chunk p0 (zeros past the end)
+__device__ __forceinline__ PairRec chunk_rec(const float4* __restrict__ pg, int n_pairs, int p0, const float* __restrict__ Fbar) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  return pair_rec(pg, n_pairs, lane < 8 ? p0 + 8 * warp + lane : n_pairs, Fbar);
+}
+__device__ __forceinline__ void bf_adjoints_rows(const PairRec& r, const float* __restrict__ v,
                                                  const float* __restrict__ vdot, const float* __restrict__ am, uint8_t* tmu,
                                                  uint8_t* tnu) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const PairRec r = pair_rec(pg, n_pairs, lane < 8 ? p0 + 8 * warp + lane : n_pairs, Fbar);
 #pragma unroll
   for (int b = 0; b < 2; ++b) {
     float2 ai[4], aj[4], vi[4], vj[4], di[4], dj[4];
@@ -403,10 +406,9 @@ __device__ __forceinline__ void bf_adjoints_rows(const float4* __restrict__ pg, 
   }
 }
 // BE: gbar = c (bm_i v_j + bm_j v_i) -> tg
-__device__ __forceinline__ void be_adjoint_rows(const float4* __restrict__ pg, int n_pairs, int p0, const float* __restrict__ v,
+__device__ __forceinline__ void be_adjoint_rows(const PairRec& r, const float* __restrict__ v,
                                                 const float* __restrict__ bm, uint8_t* tg) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const PairRec r = pair_rec(pg, n_pairs, lane < 8 ? p0 + 8 * warp + lane : n_pairs, nullptr);
   float2 bi[8], bj[8], vi[8], vj[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
@@ -439,9 +441,11 @@ __device__ __forceinline__ void be_adjoint_rows(const float4* __restrict__ pg, i
 // nothing else (row / upd kernels of the other lanes) can share its SM while
 // it waits on gathers and MMAs.  Measured (tools/ab_libs.sh, two runs each):
 // 128/128 17534-17545, BF 96 / BE 64 17428-17455, 96/96 17681-17702,
-// 96/80 17756-17759 structures/s (no spills; BF would spill below 96).
+// 96/80 17756-17759 structures/s (no spills; BF would spill below 96).  With
+// the next chunk's records prefetched (below) BF needs 104 (ab4: 19034 vs
+// 18977-19019 without the prefetch, within noise).
 #ifndef JANUS_BF_MAXNREG
-#define JANUS_BF_MAXNREG 96
+#define JANUS_BF_MAXNREG 104
 #endif
 #ifndef JANUS_BE_MAXNREG
 #define JANUS_BE_MAXNREG 80
@@ -482,11 +486,13 @@ __global__ void __maxnreg__(JANUS_BF_MAXNREG) msg_bf_pair_tc(EdgeGeom g, const f
   const uint32_t aB4 = tc::smem_u32(B4), aB5 = tc::smem_u32(B5);
   bool first = true;
   const int f0 = FPT * c.q;
+  // the next chunk's pair records (with qbar) and edge lengths are loaded while
+  // the current chunk runs its MMAs and epilogues: two dependent L2 round
+  // trips fewer at the head of every chunk (phase trace: ~2k + 3.3k cycles)
+  auto edge_d = [&](int ch) { return ch * TE + c.e < n_pairs ? __ldg(&pg[2 * (ch * TE + c.e)].x) : 0.f; };
+  PairRec rec = chunk_rec(pg, n_pairs, blockIdx.x * TE, Fbar);
+  float d = edge_d(blockIdx.x);
   for (int ch = blockIdx.x; ch * TE < n_pairs; ch += gridDim.x) {
-    const int pp = ch * TE + c.e;
-    const bool ok = pp < n_pairs;
-    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-    const float d = ok ? __ldg(&pg[2 * pp].x) : z4.x;
     {
       float ph[FPT], dph[FPT];
       basis_fast(d, rc, f0, ph, dph);
@@ -494,7 +500,9 @@ __global__ void __maxnreg__(JANUS_BF_MAXNREG) msg_bf_pair_tc(EdgeGeom g, const f
       st_b16(B5, c.e, f0, dph);
     }
     TC_M();
-    bf_adjoints_rows(pg, n_pairs, ch * TE, Fbar, v, vdot, am, B2, B3);  // mu (B of dB, A of sbar), nu
+    bf_adjoints_rows(rec, v, vdot, am, B2, B3);  // mu (B of dB, A of sbar), nu
+    rec = chunk_rec(pg, n_pairs, (ch + gridDim.x) * TE, Fbar);
+    d = edge_d(ch + gridDim.x);
     TC_M();
     tc::mbar_wait(&wbar, 0);
     c.publish();
@@ -601,17 +609,18 @@ __global__ void __maxnreg__(JANUS_BE_MAXNREG) msg_be_pair_tc(EdgeGeom g, const f
   const uint32_t aB0 = tc::smem_u32(B0), aB1 = tc::smem_u32(B1), aB2 = tc::smem_u32(B2), aB3 = tc::smem_u32(B3);
   bool first = true;
   const int f0 = FPT * c.q;
+  auto edge_d = [&](int ch) { return ch * TE + c.e < n_pairs ? __ldg(&pg[2 * (ch * TE + c.e)].x) : 0.f; };
+  PairRec rec = chunk_rec(pg, n_pairs, blockIdx.x * TE, nullptr);  // next chunk's: prefetched below
+  float d = edge_d(blockIdx.x);
   for (int ch = blockIdx.x; ch * TE < n_pairs; ch += gridDim.x) {
-    const int pp = ch * TE + c.e;
-    const bool ok = pp < n_pairs;
-    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-    const float d = ok ? __ldg(&pg[2 * pp].x) : z4.x;
     {
       float ph[FPT], dph[FPT];
       basis_fast(d, rc, f0, ph, dph);
       st_b16(B0, c.e, f0, ph);
     }
-    be_adjoint_rows(pg, n_pairs, ch * TE, v, bm, B2);  // gbar (zero on padding: c = 0)
+    be_adjoint_rows(rec, v, bm, B2);  // gbar (zero on padding: c = 0)
+    rec = chunk_rec(pg, n_pairs, (ch + gridDim.x) * TE, nullptr);
+    d = edge_d(ch + gridDim.x);
     tc::mbar_wait(&wbar, 0);
     c.publish();
     if (threadIdx.x == 0) {
