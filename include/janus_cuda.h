@@ -240,6 +240,14 @@ typedef struct {
 typedef struct janus_trainer janus_trainer;
 int janus_trainer_create(const janus_exec_desc* ed, const janus_stage_desc* sd, const float* all_params,
                          janus_comm* comm, int rank, janus_trainer** out);
+/* The same trainer executing a caller's schedule (the reference text format,
+ * ir.hpp:253-359; e.g. one built with transform::priority_topo_order): a
+ * validated second-order schedule over ed->n_stages devices and
+ * ed->n_micro_batches micro-batches; its stage map selects the folded
+ * (SymFold / WaveK / Hanayo) or the 1F1B-2nd layout, ed->method is ignored.
+ * Used by include/janus/train.hpp's train_step. */
+int janus_trainer_create_from_text(const janus_exec_desc* ed, const janus_stage_desc* sd, const float* all_params,
+                                   const char* schedule_text, janus_comm* comm, int rank, janus_trainer** out);
 int janus_trainer_destroy(janus_trainer* t);
 int janus_trainer_load(janus_trainer* t, int mb, const janus_host_batch* hb);
 /* LM of n micro-batches (mbs[k] <- hbs[k]).  Each micro-batch's geometry is

@@ -340,6 +340,18 @@ int janus_trainer_create(const janus_exec_desc* ed, const janus_stage_desc* sd, 
     *out = janus::trainer_create(*ed, *sd, all_params, comm, rank);
   });
 }
+int janus_trainer_create_from_text(const janus_exec_desc* ed, const janus_stage_desc* sd, const float* all_params,
+                                   const char* schedule_text, janus_comm* comm, int rank, janus_trainer** out) {
+  return guard([&] {
+    need(ed, "exec desc");
+    need(sd, "stage desc");
+    need(all_params, "all_params");
+    need(schedule_text, "schedule text");
+    need(out, "out");
+    *out = nullptr;
+    *out = janus::trainer_create(*ed, *sd, all_params, comm, rank, schedule_text);
+  });
+}
 int janus_trainer_destroy(janus_trainer* t) {
   return guard([&] { janus::trainer_destroy(t); });
 }

@@ -725,7 +725,7 @@ void check_per_rank_runtime(const janus_trainer* t, int n_streams) {
 
 // ================================================================ create
 janus_trainer* trainer_create(const janus_exec_desc& ed, const janus_stage_desc& sd, const float* all_params,
-                              janus_comm* comm, int rank) {
+                              janus_comm* comm, int rank, const char* schedule_text) {
   auto t = std::make_unique<janus_trainer>();
   t->ed = ed;
   t->sd = sd;
@@ -734,6 +734,17 @@ janus_trainer* trainer_create(const janus_exec_desc& ed, const janus_stage_desc&
   t->method = ed.method;
   t->local = ed.local_stages != 0;
   t->onef1b = ed.method == 2;
+  Schedule given;
+  if (schedule_text) {  // a caller's schedule (train.hpp): its stage map decides the layout
+    given = deserialize(schedule_text);
+    if (given.pipeline_degree != ed.n_stages || given.num_micro_batches != ed.n_micro_batches)
+      throw config_error("schedule text: P / micro-batches differ from the exec desc");
+    if (given.order != ScheduleOrder::second_order) throw config_error("schedule text: a second-order schedule is required");
+    bool folded = true;
+    for (int b = 0; b < t->P; ++b)
+      folded = folded && given.stage_map[static_cast<size_t>(b)] == given.stage_map[static_cast<size_t>(2 * t->P - 1 - b)];
+    t->onef1b = !folded;
+  }
   if (ed.dp_degree < 1) t->ed.dp_degree = 1;
   if (ed.lanes < 1) t->ed.lanes = 1;
   if (ed.n_micro_batches < 1) throw domain_error("n_micro_batches must be >= 1");
@@ -750,7 +761,8 @@ janus_trainer* trainer_create(const janus_exec_desc& ed, const janus_stage_desc&
   }
   if (!t->local && !comm) throw config_error("NCCL mode needs a janus_comm");
   if (t->local && t->ed.dp_degree != 1) throw config_error("data parallelism needs NCCL mode");
-  switch (ed.method) {
+  switch (schedule_text ? -1 : ed.method) {
+    case -1: t->sched = std::move(given); break;
     case 0: t->sched = symfold(t->P, ed.n_micro_batches); break;
     case 1: {
       WaveKOptions wo;  // measured phase times when the caller has them (SPEC.md:578-637 tuner input)

@@ -10,7 +10,8 @@
 namespace janus {
 
 janus_trainer* trainer_create(const janus_exec_desc& ed, const janus_stage_desc& sd, const float* all_params,
-                              janus_comm* comm, int rank);
+                              janus_comm* comm, int rank,
+                              const char* schedule_text = nullptr);
 void trainer_destroy(janus_trainer* t);
 void trainer_load(janus_trainer* t, int mb, const janus_host_batch& hb);
 void trainer_load_many(janus_trainer* t, int n, const int* mbs, const janus_host_batch* hbs);
