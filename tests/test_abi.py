@@ -113,3 +113,20 @@ def test_torch_imports_after_library():
             "assert d.is_nccl_available(); print(J.lib().janus_abi_version())")
     r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr[-1500:]
+
+
+def test_cpp_train_step_header_builds(janus):
+    """include/janus/train.hpp (SURVEY §8(b) train_step) and the pure C++ host
+    program compile and link against the library with g++ alone (run on the
+    GPU by tests/test_gpu_cpp_api.py)."""
+    import os
+    import subprocess
+    import tempfile
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib = os.path.join(root, "paper_2605_18404_b200")
+    with tempfile.TemporaryDirectory() as d:
+        r = subprocess.run(["g++", "-std=c++20", "-O1", "-Wall", "-Werror", "-I" + os.path.join(root, "include"),
+                            "-I/usr/local/cuda/include", os.path.join(root, "tools", "cpp", "train_step_demo.cpp"),
+                            "-L" + lib, "-l:libjanus_b200.so", "-Wl,-rpath," + lib, "-o", os.path.join(d, "demo")],
+                           capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr[-3000:]
