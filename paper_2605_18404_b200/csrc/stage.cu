@@ -531,6 +531,7 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
         sc.b2 = dalloc<float>(st, P2 * static_cast<size_t>(m.H), false);
         sc.cspart = dalloc<float>(st, static_cast<size_t>(wide::kColChunks) * m.H, false);
         sc.cstick = dalloc<unsigned>(st, static_cast<size_t>(m.H / 32), false);  // dalloc zeroes
+        sc.wslices = dalloc<float>(st, (P2 / 2048 + 2) * static_cast<size_t>(std::max(m.H, m.R)) * m.H, false);
         constexpr size_t kWs = 32u << 20;
         sc.blas_ws = dalloc<uint8_t>(st, kWs, false);
         cublasHandle_t h = nullptr;

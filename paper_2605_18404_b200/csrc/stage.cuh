@@ -89,6 +89,7 @@ struct Scratch {
   // [2 pairs][H] operand stacks, and the lane's cuBLAS handle + workspace
   float *phi2 = nullptr, *z2 = nullptr, *a2 = nullptr, *b2 = nullptr, *cspart = nullptr;
   unsigned* cstick = nullptr;  // column-sum tickets (one per 32-column strip, zero between launches)
+  float* wslices = nullptr;    // K-slice products of the long weight-gradient GEMMs (gemm_tn_long)
   void* blas = nullptr;
   void* blas_ws = nullptr;
 };

@@ -500,6 +500,15 @@ __global__ void __launch_bounds__(256) colsum_kernel(int rows, int cols, const f
   if (l == 0) ticket[blockIdx.x] = 0u;  // ready for the next launch on this lane
 }
 
+// C[x] += sum_b W[b][x] over the K slices of gemm_tn_long, in slice order
+__global__ void sum_slices_kernel(int64_t n, int slices, const float* __restrict__ W, float* __restrict__ C) {
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x >= n) return;
+  float acc = 0.f;
+  for (int b = 0; b < slices; ++b) acc += W[static_cast<size_t>(b) * n + x];
+  C[x] += acc;
+}
+
 __global__ void fill_kernel(int64_t n, float* __restrict__ p, float v) {
   const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (x < n) p[x] = v;
