@@ -381,9 +381,10 @@ __global__ void geometry_kernel(int n_atoms, int n_edges, const int* __restrict_
   u_out[3 * e + 0] = (float)(rx / d);
   u_out[3 * e + 1] = (float)(ry / d);
   u_out[3 * e + 2] = (float)(rz / d);
-  const double arg = 3.14159265358979323846 * d / rc;
-  c_out[e] = d < rc ? (float)(0.5 * (cos(arg) + 1.0)) : 0.f;
-  dc_out[e] = d < rc ? (float)(-0.5 * (3.14159265358979323846 / rc) * sin(arg)) : 0.f;
+  double sn, cs;  // sin / cos of pi d / r_c, one fp64 sincospi (not two calls)
+  sincospi(d / rc, &sn, &cs);
+  c_out[e] = d < rc ? (float)(0.5 * (cs + 1.0)) : 0.f;
+  dc_out[e] = d < rc ? (float)(-0.5 * (3.14159265358979323846 / rc) * sn) : 0.f;
 }
 
 // Batched LM geometry: one launch for the micro-batches of one load.  Per
@@ -432,9 +433,10 @@ __global__ void geometry_batched_kernel(const __grid_constant__ GeoJobs J) {
   jb.u[3 * e + 0] = (float)(rx / d);
   jb.u[3 * e + 1] = (float)(ry / d);
   jb.u[3 * e + 2] = (float)(rz / d);
-  const double arg = 3.14159265358979323846 * d / J.rc;
-  jb.c[e] = d < J.rc ? (float)(0.5 * (cos(arg) + 1.0)) : 0.f;
-  jb.dc[e] = d < J.rc ? (float)(-0.5 * (3.14159265358979323846 / J.rc) * sin(arg)) : 0.f;
+  double sn, cs;  // sin / cos of pi d / r_c, one fp64 sincospi (not two calls)
+  sincospi(d / J.rc, &sn, &cs);
+  jb.c[e] = d < J.rc ? (float)(0.5 * (cs + 1.0)) : 0.f;
+  jb.dc[e] = d < J.rc ? (float)(-0.5 * (3.14159265358979323846 / J.rc) * sn) : 0.f;
 }
 
 }  // namespace node
