@@ -431,6 +431,14 @@ int janus_trainer_plan(janus_trainer* t, int32_t* unit_ranges) {
 }
 
 // ------------------------------------------------------------ diagnostics
+int janus_gemm_tc_probe(int32_t rows, int32_t K, int32_t N, int32_t pair, const float* A, const float* W, float* D) {
+  return guard([&] {
+    need(A, "A");
+    need(W, "W");
+    need(D, "D");
+    janus::gemm_tc_probe(rows, K, N, pair, A, W, D);
+  });
+}
 int janus_tc_probe(const int32_t* args, const float* A, const float* B, float* D) {
   return guard([&] {
     need(args, "args");

@@ -48,6 +48,7 @@
 #include "wide.cuh"
 #include "wgrad_tc.cuh"
 #include "upd_tc.cuh"
+#include "gemm_tc_host.hpp"
 #ifndef JANUS_UPD_TC
 #define JANUS_UPD_TC 1  // tf32 mode: upd units on tcgen05 (upd_tc.cuh); 0 = the SIMT kernels (A/B builds)
 #endif
@@ -236,6 +237,19 @@ MsgParams msg_params(const janus_stage* st, int u) {
 
 // transposed copies: msg [Bt|Wt], upd [Ut|Vt], readout [Ot]
 void refresh_transposes(janus_stage* st, cudaStream_t s) {
+  if (st->wide) {  // generic width: only the tf32 GEMMs' K-major weights (A^T, B^T) of msg units
+    if (!st->wide_tc) return;
+    const int H = st->m.H, R = st->m.R;
+    for (int u = st->u0; u < st->u1; ++u) {
+      if (unit_kind(u, st->m.L) != kMsg) continue;
+      float* t = st->tw[static_cast<size_t>(u - st->u0)];
+      const float* P = st->P(u);
+      wide::transpose_any_kernel<<<blocks(static_cast<int64_t>(R) * H, 256), 256, 0, s>>>(R, H, P, t);
+      wide::transpose_any_kernel<<<blocks(static_cast<int64_t>(H) * H, 256), 256, 0, s>>>(H, H, P + R * H + H, t + H * R);
+    }
+    JANUS_LAUNCH_CHECK("transpose_wide");
+    return;
+  }
   const int H = kH, R = kR;
   for (int u = st->u0; u < st->u1; ++u) {
     float* t = st->tw[static_cast<size_t>(u - st->u0)];
@@ -362,6 +376,7 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
     st->desc = d;
     st->m = m;
     st->wide = wide;
+    st->wide_tc = wide && m.precision == JANUS_PREC_TF32;
     st->u0 = d.unit_begin;
     st->u1 = d.unit_end;
     st->U = U;
@@ -394,7 +409,12 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
       const size_t n = k == kMsg    ? 2 * kH * kH + upd_tc::kMsgPackBytes / sizeof(float)
                        : k == kUpd  ? 2 * kH * kH + upd_tc::kUpdPackBytes / sizeof(float)
                                     : static_cast<size_t>(kH) * kH;
-      st->tw.push_back(k == kEmbed || wide ? nullptr : dalloc<float>(st, n, true));
+      if (wide) {  // tf32: msg units keep [A^T (H x R) | B^T (H x H)] for the TMA-fed GEMMs
+        const bool tcw = k == kMsg && m.precision == JANUS_PREC_TF32;
+        st->tw.push_back(tcw ? dalloc<float>(st, static_cast<size_t>(m.H) * (m.R + m.H), true) : nullptr);
+        continue;
+      }
+      st->tw.push_back(k == kEmbed ? nullptr : dalloc<float>(st, n, true));
     }
     // geometry per micro-batch
     st->geo.resize(2 * NMB);
@@ -539,6 +559,15 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
         sc.blas = h;
         JANUS_BLAS(cublasSetWorkspace(h, sc.blas_ws, kWs));
         JANUS_BLAS(cublasSetPointerMode(h, CUBLAS_POINTER_MODE_HOST));
+        if (st->wide_tc) {  // tensor maps of the lane's operand stacks (capacity rows; OOB rows read as zero)
+          auto put = [](TMap& d, const CUtensorMap& m) { std::memcpy(d.bytes, &m, sizeof(m)); };
+          const int rows = static_cast<int>(P2);
+          put(sc.tm_phi2_pair, gemm_tc::make_tmap(sc.phi2, rows, m.R, 64));
+          put(sc.tm_phi2_plain, gemm_tc::make_tmap(sc.phi2, rows, m.R, 128));
+          put(sc.tm_a2_pair, gemm_tc::make_tmap(sc.a2, rows, m.H, 64));
+          put(sc.tm_b2_pair, gemm_tc::make_tmap(sc.b2, rows, m.H, 64));
+          put(sc.tm_b2_plain, gemm_tc::make_tmap(sc.b2, rows, m.H, 128));
+        }
         if (m.precision == JANUS_PREC_FP32_EMU) {
           // cuBLAS >= 12.9 only; resolved at run time, since a host that loads
           // an older libcublas first (e.g. torch's bundled 12.8) must still load us
@@ -575,7 +604,21 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
     JANUS_CUDA(cudaFuncSetAttribute(upd_tc::upd_bf_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_tc::upd_tc_smem(5, 2)));
     JANUS_CUDA(cudaFuncSetAttribute(upd_tc::upd_be_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_tc::upd_tc_smem(2, 1)));
     JANUS_CUDA(cudaFuncSetAttribute(upd_tc::rows_w_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)upd_tc::upd_tc_smem(2, 2)));
-    if (!wide) refresh_transposes(st, nullptr);
+    if (st->wide_tc) {  // weight maps: A^T and B^T (transposed copies) and B itself, per msg unit
+      st->tm_w.resize(3 * static_cast<size_t>(st->u1 - st->u0));
+      for (int u = st->u0; u < st->u1; ++u) {
+        if (unit_kind(u, m.L) != kMsg) continue;
+        const float* t = st->tw[static_cast<size_t>(u - st->u0)];
+        const float* B = st->P(u) + m.R * m.H + m.H;
+        TMap* w = &st->tm_w[3 * static_cast<size_t>(u - st->u0)];
+        const CUtensorMap at = gemm_tc::make_tmap(t, m.H, m.R, m.H), bt = gemm_tc::make_tmap(t + m.H * m.R, m.H, m.H, m.H),
+                          bb = gemm_tc::make_tmap(B, m.H, m.H, m.H);
+        std::memcpy(w[0].bytes, &at, sizeof(at));
+        std::memcpy(w[1].bytes, &bt, sizeof(bt));
+        std::memcpy(w[2].bytes, &bb, sizeof(bb));
+      }
+    }
+    refresh_transposes(st, nullptr);
     JANUS_CUDA(cudaDeviceSynchronize());
   } catch (...) {
     for (auto& sc : st->lanes)
@@ -1316,7 +1359,7 @@ void stage_optimizer(janus_stage* st, const janus_opt& o, cudaStream_t s, const 
   node::adam_kernel<<<blocks(st->n_params, 256), 256, 0, s>>>(st->n_params, st->params, st->m1, st->m2, st->grad, dhp,
                                                               st->dstep);
   JANUS_LAUNCH_CHECK("adam");
-  if (!st->wide) refresh_transposes(st, s);
+  refresh_transposes(st, s);
 }
 
 void stage_port(janus_stage* st, int mb, int slot, int port, void** dptr, size_t* bytes) {

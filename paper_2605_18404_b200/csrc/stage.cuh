@@ -79,6 +79,11 @@ struct Port {
   int H = 64;            // row width of h / m
 };
 
+// a CUtensorMap (128 B, 64 B aligned) kept opaque here (gemm_tc_host.hpp encodes it)
+struct alignas(64) TMap {
+  unsigned char bytes[128];
+};
+
 // Per-lane scratch: phases of different micro-batches may run concurrently on
 // different streams ("lanes") of one device; all transient buffers are per lane.
 struct Scratch {
@@ -90,6 +95,9 @@ struct Scratch {
   float *phi2 = nullptr, *z2 = nullptr, *a2 = nullptr, *b2 = nullptr, *cspart = nullptr;
   unsigned* cstick = nullptr;  // column-sum tickets (one per 32-column strip, zero between launches)
   float* wslices = nullptr;    // K-slice products of the long weight-gradient GEMMs (gemm_tn_long)
+  // tf32: tensor maps of this lane's operand stacks for the TMA-fed GEMMs (gemm_tc.cuh):
+  // phi2 / a2 / b2 with 64-row boxes (pair tiles) and phi2 / b2 with 128-row boxes (plain tiles)
+  TMap tm_phi2_pair, tm_a2_pair, tm_b2_pair, tm_phi2_plain, tm_b2_plain;
   void* blas = nullptr;
   void* blas_ws = nullptr;
 };
@@ -151,6 +159,8 @@ struct janus_stage {
   int pair_chunks_cap = 0;
   janus::LmBuilder* lm = nullptr;  // device neighbour-list builder (lazy, janus_stage_load without a CSR)
   bool wide = false;               // generic-width phases (stage_wide.inc) instead of the fused H=64 kernels
+  bool wide_tc = false;            // wide + tf32: per-pair GEMMs on gemm_tc.cuh with fused epilogues
+  std::vector<janus::TMap> tm_w;   // wide_tc, per unit (msg: 3 maps): A^T [H x R], B^T [H x H], B [H x H]
 
   float* P(int u) const { return params + uoff[static_cast<size_t>(u - u0)]; }
 

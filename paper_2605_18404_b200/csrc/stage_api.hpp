@@ -53,5 +53,6 @@ void stage_time_edge_kernel(janus_stage* st, int which, int mb, int slot, int it
 
 // tcgen05 layer self-test (tc_probe.cu)
 void tc_probe(const int* args, const float* A, const float* B, float* D);
+void gemm_tc_probe(int rows, int K, int N, int pair, const float* A, const float* W, float* D);
 
 }  // namespace janus

@@ -11,6 +11,7 @@
 #include "../../include/janus/errors.hpp"
 #include "cuda_check.hpp"
 #include "tc.cuh"
+#include "gemm_tc_host.hpp"
 
 namespace janus {
 namespace {
@@ -125,6 +126,27 @@ void tc_probe(const int* args, const float* A, const float* B, float* D) {
   JANUS_CUDA(cudaMemcpy(D, dD, 128 * p.N * 4, cudaMemcpyDeviceToHost));
   cudaFree(dA);
   cudaFree(dB);
+  cudaFree(dD);
+}
+
+// gemm_tc.cuh self-test: D = A . W^T through the TMA + tcgen05 pipeline with
+// the plain store epilogue (pair = 1: A and D stacked [2P x K] / [2P x N]).
+void gemm_tc_probe(int rows, int K, int N, int pair, const float* A, const float* W, float* D) {
+  const int arows = pair ? 2 * rows : rows;
+  float *dA, *dW, *dD;
+  JANUS_CUDA(cudaMalloc(&dA, sizeof(float) * arows * K));
+  JANUS_CUDA(cudaMalloc(&dW, sizeof(float) * N * K));
+  JANUS_CUDA(cudaMalloc(&dD, sizeof(float) * arows * N));
+  JANUS_CUDA(cudaMemcpy(dA, A, sizeof(float) * arows * K, cudaMemcpyHostToDevice));
+  JANUS_CUDA(cudaMemcpy(dW, W, sizeof(float) * N * K, cudaMemcpyHostToDevice));
+  JANUS_CUDA(cudaMemset(dD, 0, sizeof(float) * arows * N));
+  const CUtensorMap ta = gemm_tc::make_tmap(dA, arows, K, pair ? 64 : 128);
+  const CUtensorMap tw = gemm_tc::make_tmap(dW, N, K, N);
+  gemm_tc::launch(ta, tw, gemm_tc::Problem{rows, K, N, pair}, gemm_tc::EpiStore{dD, N}, nullptr);
+  JANUS_CUDA(cudaDeviceSynchronize());
+  JANUS_CUDA(cudaMemcpy(D, dD, sizeof(float) * arows * N, cudaMemcpyDeviceToHost));
+  cudaFree(dA);
+  cudaFree(dW);
   cudaFree(dD);
 }
 

@@ -509,6 +509,14 @@ __global__ void sum_slices_kernel(int64_t n, int slices, const float* __restrict
   C[x] += acc;
 }
 
+// dst[c][r] = src[r][c] for a [rows x cols] matrix (weight transposes, once per optimizer step)
+__global__ void transpose_any_kernel(int rows, int cols, const float* __restrict__ src, float* __restrict__ dst) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= rows * cols) return;
+  const int r = x / cols, c = x % cols;
+  dst[static_cast<size_t>(c) * rows + r] = src[x];
+}
+
 __global__ void fill_kernel(int64_t n, float* __restrict__ p, float v) {
   const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (x < n) p[x] = v;

@@ -93,3 +93,29 @@ def test_probe_sw128(janus, has_gpu, name):
     lanes, err = lane_map(D, ref(tf32(A), tf32(B)))
     print(f"{name} sw128: rel err {err:.2e}; |D| max {np.abs(D).max():.3f}; lanes[:20] {lanes[:20]}")
     assert err < 1e-3
+
+
+def gemm_probe(janus, rows, K, N, pair, A, W):
+    fn = janus.lib().janus_gemm_tc_probe
+    fn.argtypes = [ctypes.c_int32] * 4 + [ctypes.c_void_p] * 3
+    A = np.ascontiguousarray(A, np.float32)
+    W = np.ascontiguousarray(W, np.float32)
+    D = np.zeros((A.shape[0], N), np.float32)
+    janus.check(fn(rows, K, N, pair, A.ctypes.data, W.ctypes.data, D.ctypes.data))
+    return D
+
+
+@pytest.mark.parametrize("rows,K,N,pair", [(200, 64, 256, 0), (300, 256, 256, 0), (128, 256, 64, 0), (77, 64, 128, 0),
+                                           (100, 64, 256, 1), (130, 256, 256, 1), (64, 32, 64, 1)])
+def test_tma_gemm_matches_numpy(janus, has_gpu, rows, K, N, pair):
+    """gemm_tc.cuh: TMA (SWIZZLE_128B tensor maps) + tcgen05 kind::tf32,
+    warp-specialised pipeline; pair mode stacks [value; derivative] rows.
+    Against numpy on tf32-truncated inputs (fp32 accumulate)."""
+    if not has_gpu:
+        pytest.skip("no GPU")
+    rng = np.random.default_rng(rows * 7 + K)
+    A = rng.standard_normal(((2 if pair else 1) * rows, K)).astype(np.float32)
+    W = rng.standard_normal((N, K)).astype(np.float32)
+    D = gemm_probe(janus, rows, K, N, pair, A, W)
+    ref = tf32(A) @ tf32(W).T
+    assert np.abs(D - ref).max() <= 1e-4 * np.abs(ref).max()

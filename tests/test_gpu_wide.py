@@ -44,7 +44,8 @@ def run_stage(janus, m, params, batches, max_atoms=64):
     return st
 
 
-@pytest.mark.parametrize("H,R,prec", [(64, 64, 0), (128, 32, 0), (256, 64, 0), (256, 64, 1), (64, 64, 2), (256, 64, 2)])
+@pytest.mark.parametrize("H,R,prec", [(64, 64, 0), (128, 32, 0), (256, 64, 0), (256, 64, 1), (128, 64, 1), (64, 64, 1),
+                                      (64, 64, 2), (256, 64, 2)])
 def test_wide_matches_oracle(janus, oracle, has_gpu, H, R, prec):
     if not has_gpu:
         pytest.skip("no GPU")
@@ -90,13 +91,14 @@ def test_wide_h64_agrees_with_fused_kernels(janus, has_gpu):
         assert rel(a, b) < tol
 
 
-@pytest.mark.parametrize("P,method", [(2, 0), (4, 0), (4, 1), (3, 4)])
-def test_wide_pipeline_bit_identical(janus, has_gpu, P, method):
+@pytest.mark.parametrize("P,method,prec", [(2, 0, 0), (4, 0, 0), (4, 1, 0), (3, 4, 0), (3, 0, 1), (4, 1, 1)])
+def test_wide_pipeline_bit_identical(janus, has_gpu, P, method, prec):
     """L=3, H=256: staged (incl. mid-layer splits), pooled slots, WaveK /
-    Hanayo orders — all equal to P=1 bit for bit."""
+    Hanayo orders — all equal to P=1 bit for bit (prec 1: the TMA-fed
+    tcgen05 GEMMs of gemm_tc.cuh)."""
     if not has_gpu:
         pytest.skip("no GPU")
-    m = janus.Model(L=3, H=256, R=64, generic=True)
+    m = janus.Model(L=3, H=256, R=64, generic=True, precision=prec)
     params = m.synth_params(13)
     batches = [janus.synth_batch(m, [n], 0.095, 50 + i) for i, n in enumerate([32, 40, 27, 36, 30, 33])]
     res = []
