@@ -55,8 +55,8 @@ struct EpiStore {  // D = the accumulator (pair mode: stacked like A)
   float* D;
   int ld;
   __device__ void operator()(int rows_total, int p, int half, int P, int c0, const float (&own)[32], const float (&)[32]) const {
+    if (p >= rows_total) return;  // plain tiles past the last row
     const int r = half ? P + p : p;
-    (void)rows_total;
     float4* o = reinterpret_cast<float4*>(D + static_cast<size_t>(r) * ld + c0);
 #pragma unroll
     for (int j = 0; j < 8; ++j) o[j] = make_float4(own[4 * j], own[4 * j + 1], own[4 * j + 2], own[4 * j + 3]);
