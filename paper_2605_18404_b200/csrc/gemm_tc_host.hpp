@@ -41,33 +41,20 @@ inline CUtensorMap make_tmap(const float* base, int rows, int K, int box_rows) {
   return m;
 }
 
-// D = A . W^T: A [rows or 2P x K] (map with box rows 128 plain / 64 pair),
-// W [N x K]; one 128-row tile per CTA
+// D = A . W^T: A [rows or 2P x K] (map with box rows 128 plain / 16 pair),
+// W [N x K] (box rows N); one 128-row tile per CTA
 template <class Epi>
 void launch(const CUtensorMap& tmA, const CUtensorMap& tmW, const Problem& pb, const Epi& epi, cudaStream_t s) {
   if (pb.K % kKB || (pb.N != 64 && pb.N != 128 && pb.N != 256)) throw domain_error("gemm_tc: unsupported K / N");
   const int tiles = pb.pair ? (pb.rows + 63) / 64 : (pb.rows + 127) / 128;
   if (tiles <= 0) return;
-  const int KB = pb.K / kKB;
-  if (KB <= 2) {
-    constexpr int S = 2;
-    static bool attr = false;
-    if (!attr) {
-      JANUS_CUDA(cudaFuncSetAttribute(gemm_nt_kernel<S, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(smem_bytes(S, 256))));
-      attr = true;
-    }
-    gemm_nt_kernel<S, Epi><<<tiles, kThreads, smem_bytes(S, pb.N), s>>>(tmA, tmW, pb, epi);
-  } else {
-    constexpr int S = 4;
-    static bool attr = false;
-    if (!attr) {
-      JANUS_CUDA(cudaFuncSetAttribute(gemm_nt_kernel<S, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(smem_bytes(S, 256))));
-      attr = true;
-    }
-    gemm_nt_kernel<S, Epi><<<tiles, kThreads, smem_bytes(S, pb.N), s>>>(tmA, tmW, pb, epi);
+  static bool attr = false;
+  if (!attr) {
+    JANUS_CUDA(cudaFuncSetAttribute(gemm_nt_kernel<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem_bytes(256))));
+    attr = true;
   }
+  gemm_nt_kernel<Epi><<<tiles, kThreads, smem_bytes(pb.N), s>>>(tmA, tmW, pb, epi);
   JANUS_LAUNCH_CHECK("gemm_tc");
 }
 

@@ -458,9 +458,7 @@ __global__ void __maxnreg__(JANUS_BF_MAXNREG) msg_bf_pair_tc(EdgeGeom g, const f
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = align1024(sm_raw);
   uint8_t* W2b = sm;  // bf16 weights in pack order: B | A^T | B^T
-  uint8_t* W0b = W2b + kW2bBytes;
-  uint8_t* W1b = W0b + kW2bBytes;
-  (void)W1b;
+  uint8_t* W0b = W2b + kW2bBytes;  // W1b (A^T) follows W0b
   uint8_t* B0 = sm + 2 * kWTile;  // bf16: s          (write_partial scratch: B0..B2)
   uint8_t* B1 = B0 + kBTile;      //       sdot
   uint8_t* B2 = B1 + kBTile;      //       mu, then zbar

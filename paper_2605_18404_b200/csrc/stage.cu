@@ -562,10 +562,10 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
         if (st->wide_tc) {  // tensor maps of the lane's operand stacks (capacity rows; OOB rows read as zero)
           auto put = [](TMap& d, const CUtensorMap& m) { std::memcpy(d.bytes, &m, sizeof(m)); };
           const int rows = static_cast<int>(P2);
-          put(sc.tm_phi2_pair, gemm_tc::make_tmap(sc.phi2, rows, m.R, 64));
+          put(sc.tm_phi2_pair, gemm_tc::make_tmap(sc.phi2, rows, m.R, 16));
           put(sc.tm_phi2_plain, gemm_tc::make_tmap(sc.phi2, rows, m.R, 128));
-          put(sc.tm_a2_pair, gemm_tc::make_tmap(sc.a2, rows, m.H, 64));
-          put(sc.tm_b2_pair, gemm_tc::make_tmap(sc.b2, rows, m.H, 64));
+          put(sc.tm_a2_pair, gemm_tc::make_tmap(sc.a2, rows, m.H, 16));
+          put(sc.tm_b2_pair, gemm_tc::make_tmap(sc.b2, rows, m.H, 16));
           put(sc.tm_b2_plain, gemm_tc::make_tmap(sc.b2, rows, m.H, 128));
         }
         if (m.precision == JANUS_PREC_FP32_EMU) {

@@ -96,7 +96,7 @@ struct Scratch {
   unsigned* cstick = nullptr;  // column-sum tickets (one per 32-column strip, zero between launches)
   float* wslices = nullptr;    // K-slice products of the long weight-gradient GEMMs (gemm_tn_long)
   // tf32: tensor maps of this lane's operand stacks for the TMA-fed GEMMs (gemm_tc.cuh):
-  // phi2 / a2 / b2 with 64-row boxes (pair tiles) and phi2 / b2 with 128-row boxes (plain tiles)
+  // phi2 / a2 / b2 with 16-row boxes (pair tiles) and phi2 / b2 with 128-row boxes (plain tiles)
   TMap tm_phi2_pair, tm_a2_pair, tm_b2_pair, tm_phi2_plain, tm_b2_plain;
   void* blas = nullptr;
   void* blas_ws = nullptr;

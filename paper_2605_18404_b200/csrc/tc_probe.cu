@@ -140,7 +140,7 @@ void gemm_tc_probe(int rows, int K, int N, int pair, const float* A, const float
   JANUS_CUDA(cudaMemcpy(dA, A, sizeof(float) * arows * K, cudaMemcpyHostToDevice));
   JANUS_CUDA(cudaMemcpy(dW, W, sizeof(float) * N * K, cudaMemcpyHostToDevice));
   JANUS_CUDA(cudaMemset(dD, 0, sizeof(float) * arows * N));
-  const CUtensorMap ta = gemm_tc::make_tmap(dA, arows, K, pair ? 64 : 128);
+  const CUtensorMap ta = gemm_tc::make_tmap(dA, arows, K, pair ? 16 : 128);
   const CUtensorMap tw = gemm_tc::make_tmap(dW, N, K, N);
   gemm_tc::launch(ta, tw, gemm_tc::Problem{rows, K, N, pair}, gemm_tc::EpiStore{dD, N}, nullptr);
   JANUS_CUDA(cudaDeviceSynchronize());

@@ -462,11 +462,16 @@ __global__ void __launch_bounds__(256) species_sum_kernel(int N, int S, int cols
 
 // Column sums out[c] += sum_r X[r][c] in ONE deterministic launch: block
 // (strip of 32 columns, chunk g of rows) sums its rows (8 warps interleave,
-// combined in warp order) into part[g][c]; the last block of a strip to
-// finish (atomic ticket, counter reset by it) adds the chunks' partials in
-// chunk order.  The arrival order decides only WHICH block sums, never the
-// order of the sum.
-constexpr int kColChunks = 64;
+// up to kColRows / 8 independent loads in flight per thread, combined in warp
+// order) into part[g][c]; the last block of a strip to finish (atomic ticket,
+// counter reset by it) adds the chunks' partials — warp w the chunks w, w + 8,
+// ..., then the 8 warp sums in warp order (a single thread walking all
+// chunks was the long pole).  The arrival order decides only WHICH block
+// sums, never the order of the sum.  256-row chunks: inside the 8-lane
+// configs[2] step 64-row chunks (4x the blocks) measured 148.5 vs 152.6
+// structures/s; 512 / 1024 rows are within noise of 256.
+constexpr int kColChunks = 256;
+constexpr int kColRows = 256;
 __global__ void __launch_bounds__(256) colsum_kernel(int rows, int cols, const float* __restrict__ X,
                                                      float* __restrict__ part, unsigned* __restrict__ ticket,
                                                      float* __restrict__ out) {
@@ -476,7 +481,7 @@ __global__ void __launch_bounds__(256) colsum_kernel(int rows, int cols, const f
   const int per = (rows + gridDim.y - 1) / gridDim.y, r0 = g * per, r1 = min(rows, r0 + per);
   float acc = 0.f;
   if (k < cols)
-#pragma unroll 4
+#pragma unroll 8
     for (int r = r0 + w; r < r1; r += 8) acc += __ldg(X + static_cast<size_t>(r) * cols + k);
   red[w][l] = acc;
   __syncthreads();
@@ -490,14 +495,21 @@ __global__ void __launch_bounds__(256) colsum_kernel(int rows, int cols, const f
   __syncthreads();
   if (threadIdx.x == 0) last = atomicAdd(ticket + blockIdx.x, 1u) == gridDim.y - 1;
   __syncthreads();
-  if (!last || w != 0) return;
+  if (!last) return;
   __threadfence();
-  if (k < cols) {
-    float sum = 0.f;
-    for (int q = 0; q < static_cast<int>(gridDim.y); ++q) sum += __ldcg(part + static_cast<size_t>(q) * cols + k);
-    out[k] += sum;
+  float sum = 0.f;
+  if (k < cols)
+#pragma unroll 8
+    for (int q = w; q < static_cast<int>(gridDim.y); q += 8) sum += __ldcg(part + static_cast<size_t>(q) * cols + k);
+  red[w][l] = sum;
+  __syncthreads();
+  if (w == 0) {
+    float tot = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) tot += red[q][l];
+    if (k < cols) out[k] += tot;
+    if (l == 0) ticket[blockIdx.x] = 0u;  // ready for the next launch on this lane
   }
-  if (l == 0) ticket[blockIdx.x] = 0u;  // ready for the next launch on this lane
 }
 
 // C[x] += sum_b W[b][x] over the K slices of gemm_tn_long, in slice order
