@@ -186,7 +186,9 @@ void wjobs(const janus_stage* st, Scratch& sc, cudaStream_t s, int rows, std::in
   for (const auto& j : list) J.j[k++] = j;
   static const bool simt_only = std::getenv("JANUS_WGRAD_SIMT") != nullptr;  // comparison runs
   if (use_tc(st) && !simt_only) {
-    edge_tc::wgrad_tc_kernel<<<J.n, edge_tc::kWgT, edge_tc::wgrad_tc_smem(), s>>>(rows, J);
+    bool cs = false;
+    for (int q = 0; q < J.n; ++q) cs = cs || J.j[q].x1 || J.j[q].x2;
+    edge_tc::wgrad_tc_kernel<<<dim3(static_cast<unsigned>(J.n), cs ? 2u : 1u), edge_tc::kWgT, edge_tc::wgrad_tc_smem(), s>>>(rows, J);
   } else {
     const dim3 grid(9u, static_cast<unsigned>(J.n));  // 8 row blocks of the gradient + 1 column-sum block
     node::wgrad_multi_kernel<<<grid, 256, 0, s>>>(rows, J, sc.wpart, sc.counter);

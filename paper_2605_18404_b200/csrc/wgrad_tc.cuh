@@ -19,6 +19,36 @@ constexpr size_t wgrad_tc_smem() { return 2 * kTile + 1024; }
 
 constexpr int kWgT = 512;  // threads: 4 float4 of a and of b per thread per 128-atom block
 
+// Column sums of x1 / x2 (grid.y = 1 CTAs; they ran after the MMA loop, as
+// 2 x 8 dependent L2 round trips, until round 2): thread = (matrix, row
+// quarter, column), 16 loads in flight, each column summed in row order
+// within its quarter and the quarters combined in a fixed order — the same
+// sums as before, bit for bit.
+__device__ __forceinline__ void colsums(int rows, const node::WJob& jb, float (*csp)[2][64]) {
+  const int tid = static_cast<int>(threadIdx.x), w = tid >> 8, qr = (tid >> 6) & 3, c = tid & 63;
+  const int r0 = (rows * qr) >> 2, r1 = (rows * (qr + 1)) >> 2;
+  const float* X = w ? jb.x2 : jb.x1;
+  float s = 0.f;
+  if (X) {
+    int i = r0;
+    for (; i + 16 <= r1; i += 16) {
+      float v[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) v[u] = __ldg(X + (size_t)(i + u) * 64 + c);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) s += v[u];
+    }
+    for (; i < r1; ++i) s += __ldg(X + (size_t)i * 64 + c);
+  }
+  csp[qr][w][c] = s;
+  __syncthreads();
+  if (tid < 128) {
+    const int ww = tid >> 6, cc = tid & 63;
+    float* out = ww ? jb.cs2 : jb.cs1;
+    if ((ww ? jb.x2 : jb.x1) && out) out[cc] = (csp[0][ww][cc] + csp[1][ww][cc]) + (csp[2][ww][cc] + csp[3][ww][cc]);
+  }
+}
+
 __global__ void __launch_bounds__(kWgT, 1) wgrad_tc_kernel(int rows, node::WJobs jobs) {
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = align1024(sm_raw);
@@ -29,6 +59,10 @@ __global__ void __launch_bounds__(kWgT, 1) wgrad_tc_kernel(int rows, node::WJobs
   __shared__ float csp[4][2][64];
   const node::WJob& jb = jobs.j[blockIdx.x];
   const int tid = static_cast<int>(threadIdx.x), warp = tid >> 5, lane = tid & 31;
+  if (blockIdx.y == 1) {  // the job's column sums, beside the MMA CTA instead of after it
+    colsums(rows, jb, csp);
+    return;
+  }
   if (tid == 0) tc::mbar_init(&mbar, 1);
   if (warp == 0) tc::tmem_alloc(&tslot, 64);
   tc::fence_before();
@@ -100,33 +134,6 @@ __global__ void __launch_bounds__(kWgT, 1) wgrad_tc_kernel(int rows, node::WJobs
 #pragma unroll
         for (int j = 0; j < 4; ++j) o[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
       }
-    }
-  }
-  // column sums of x1 / x2: 4 row quarters per column, combined in a fixed order
-  if (jb.x1 || jb.x2) {
-    const int qr = (tid >> 6) & 3, c = tid & 63;
-    const int r0 = (rows * qr) >> 2, r1 = (rows * (qr + 1)) >> 2;
-    for (int w = 0; w < 2 && tid < 256; ++w) {
-      const float* X = w ? jb.x2 : jb.x1;
-      float s = 0.f;
-      if (X) {
-        int i = r0;
-        for (; i + 8 <= r1; i += 8) {
-          float v[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) v[u] = __ldg(X + (size_t)(i + u) * 64 + c);
-#pragma unroll
-          for (int u = 0; u < 8; ++u) s += v[u];
-        }
-        for (; i < r1; ++i) s += __ldg(X + (size_t)i * 64 + c);
-      }
-      csp[qr][w][c] = s;
-    }
-    __syncthreads();
-    if (tid < 128) {
-      const int w = tid >> 6, c = tid & 63;
-      float* out = w ? jb.cs2 : jb.cs1;
-      if ((w ? jb.x2 : jb.x1) && out) out[c] = (csp[0][w][c] + csp[1][w][c]) + (csp[2][w][c] + csp[3][w][c]);
     }
   }
   tc::fence_before();

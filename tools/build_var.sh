@@ -6,4 +6,4 @@ build_var ()
     mkdir -p $d;
     /usr/local/cuda/bin/nvcc -I/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/include -Iinclude -std=c++20 -O3 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC --expt-relaxed-constexpr $2 -c paper_2605_18404_b200/csrc/stage.cu -o $d/stage.cu.o && objs=$(ls build/obj/*.o | grep -v stage.cu.o) && /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $d/libjanus_b200.so $d/stage.cu.o $objs -L/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/lib -l:libnccl.so.2 -Xlinker -rpath -Xlinker /opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/lib -L/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/cublas/lib -l:libcublas.so.12 -Xlinker -rpath -Xlinker /opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/cublas/lib -lcudart
 }
-build_var "$@"
+if [ $# -gt 0 ]; then build_var "$@"; fi
