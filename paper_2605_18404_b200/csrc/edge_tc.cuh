@@ -789,7 +789,7 @@ __device__ __forceinline__ void fm_colsum_add(const uint8_t* t, float* acc) {
 // smem (`scratch` = the operand tiles, free by now) and leave with coalesced
 // float4 stores.
 __device__ __forceinline__ void write_partial(Ctx& c, float* part, uint8_t* scratch, const float* csa,
-                                              const float* csb TC_ARGS) {
+                                              const float* csb, uint32_t tm_ag, uint32_t tm_bg TC_ARGS) {
   constexpr int LDP = 68;  // padded row: the 8 rows of an STS.128 phase hit distinct banks
   float* stg = reinterpret_cast<float*>(scratch);  // [2][64][LDP] dA, dB rows
   tc::fence_before();
@@ -798,7 +798,7 @@ __device__ __forceinline__ void write_partial(Ctx& c, float* part, uint8_t* scra
   TC_M();
   {
     float va[FPT], vb[FPT];
-    c.ld2(TM_AG, TM_BG, va, vb);
+    c.ld2(tm_ag, tm_bg, va, vb);
     if (c.lane < 16) {
       const int r = 16 * (c.warp & 3) + c.lane;
       float4* pa = reinterpret_cast<float4*>(stg + r * LDP + FPT * c.q);
@@ -983,7 +983,7 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int4* __res
     teardown(c, 512);
     return;
   }
-  write_partial(c, part, T0, csa, csb TC_PASS);
+  write_partial(c, part, T0, csa, csb, TM_AG, TM_BG TC_PASS);
   TC_M();
   teardown(c, 512);
   TC_M();
@@ -1190,7 +1190,7 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int4* __res
     teardown(c, 512);
     return;
   }
-  write_partial(c, part, T0, csa, csb TC_PASS);
+  write_partial(c, part, T0, csa, csb, TM_AG, TM_BG TC_PASS);
   TC_M();
   teardown(c, 512);
   TC_M();

@@ -444,11 +444,32 @@ __device__ __forceinline__ void be_adjoint_rows(const PairRec& r, const float* _
 // 96/80 17756-17759 structures/s (no spills; BF would spill below 96).  With
 // the next chunk's records prefetched (below) BF needs 104 (ab4: 19034 vs
 // 18977-19019 without the prefetch, within noise).
+// With 256 TMEM columns (below) BF holds z, z' in registers across the
+// second MMA group: 104 spills, 112 spills 48 B; 120 is spill-free (tools/
+// ab_libs.sh, device structures/s, two runs: 512 columns at 104 registers
+// 19052 / 19010; 256 columns at 112: 19114 / 19110, 120: 19097 / 19093,
+// 128: 19147 / 19192 — all within ~0.5%).
 #ifndef JANUS_BF_MAXNREG
-#define JANUS_BF_MAXNREG 104
+#define JANUS_BF_MAXNREG 120
 #endif
 #ifndef JANUS_BE_MAXNREG
 #define JANUS_BE_MAXNREG 80
+#endif
+// TMEM: 256 columns per pair CTA (JANUS_PAIR_TMEM256, the default) instead of
+// 512, so a pair CTA leaves half of its SM's tensor memory to the other lanes'
+// tcgen05 kernels (filter / upd / the other pair kernel), which otherwise
+// spin in tcgen05.alloc beside it.  BE: z | sbar | dA | dB.  BF keeps z, z'
+// in registers from epilogue 1 to epilogue 2, so sbar, sdotbar reuse z, z''s
+// columns: z | z' (then sbar | sdotbar) | dA | dB.
+#ifndef JANUS_PAIR_TMEM256
+#define JANUS_PAIR_TMEM256 1
+#endif
+#if JANUS_PAIR_TMEM256
+constexpr uint32_t kPairCols = 256, PT_Z = 0, PT_ZP = 64, PT_G = 0, PT_GP = 64, PT_AG = 128, PT_BG = 192;
+constexpr uint32_t BT_Z = 0, BT_G = 64, BT_AG = 128, BT_BG = 192;
+#else
+constexpr uint32_t kPairCols = 512, PT_Z = TM_Z, PT_ZP = TM_ZP, PT_G = TM_G, PT_GP = TM_GP, PT_AG = TM_AG, PT_BG = TM_BG;
+constexpr uint32_t BT_Z = TM_Z, BT_G = TM_G, BT_AG = TM_AG, BT_BG = TM_BG;
 #endif
 __global__ void __maxnreg__(JANUS_BF_MAXNREG) msg_bf_pair_tc(EdgeGeom g, const float4* __restrict__ pg, int n_pairs, MsgParams p,
                                                        float rc, const float* __restrict__ v, const float* __restrict__ vdot,
@@ -477,7 +498,7 @@ __global__ void __maxnreg__(JANUS_BF_MAXNREG) msg_bf_pair_tc(EdgeGeom g, const f
   c.mbar = &mbar;
   load_weights_b16(W2b, p.pack, al, be, &wbar);
   if (threadIdx.x < 128) csa[threadIdx.x] = 0.f;
-  setup(c, &tslot, 512);
+  setup(c, &tslot, kPairCols);
   TC_M();
   const uint32_t aW0b = tc::smem_u32(W0b), aW2b = tc::smem_u32(W2b);
   const uint32_t aB0 = tc::smem_u32(B0), aB1 = tc::smem_u32(B1), aB2 = tc::smem_u32(B2), aB3 = tc::smem_u32(B3);
@@ -506,30 +527,32 @@ __global__ void __maxnreg__(JANUS_BF_MAXNREG) msg_bf_pair_tc(EdgeGeom g, const f
     c.publish();
     TC_M();
     if (threadIdx.x == 0) {
-      mma_kb16(c.tmem + TM_Z, aB4, aW0b);
-      mma_kb16(c.tmem + TM_ZP, aB5, aW0b);
+      mma_kb16(c.tmem + PT_Z, aB4, aW0b);
+      mma_kb16(c.tmem + PT_ZP, aB5, aW0b);
       tc::commit(c.mbar);
     }
     c.wait_mma();
     TC_M();
+    float z[FPT], zp[FPT];  // raw z, z' (bias included), kept for epilogue 2
     {
-      float z[FPT], zp[FPT];
-      c.ld2(TM_Z, TM_ZP, z, zp);
+      float sv[FPT], sd[FPT];
+      c.ld2(PT_Z, PT_ZP, z, zp);
 #pragma unroll
       for (int k = 0; k < FPT; ++k) {
         const float zz = z[k] + al[f0 + k], s1 = fsig_t(zz);
-        z[k] = zz * s1;
-        zp[k] = s1 * (1.0f + zz * (1.0f - s1)) * zp[k];
+        z[k] = zz;
+        sv[k] = zz * s1;
+        sd[k] = s1 * (1.0f + zz * (1.0f - s1)) * zp[k];
       }
-      st_b16(B0, c.e, f0, z);   // s
-      st_b16(B1, c.e, f0, zp);  // sdot
+      st_b16(B0, c.e, f0, sv);  // s
+      st_b16(B1, c.e, f0, sd);  // sdot
     }
     c.publish();
     if (threadIdx.x == 0) {  // dB += s^T mu + sdot^T nu; sbar = mu B^T, sdotbar = nu B^T
-      mma_wg_b16(c.tmem + TM_BG, aB0, aB2, !first);
-      mma_wg_b16(c.tmem + TM_BG, aB1, aB3, true);
-      mma_kb16(c.tmem + TM_G, aB2, aW2b);
-      mma_kb16(c.tmem + TM_GP, aB3, aW2b);
+      mma_wg_b16(c.tmem + PT_BG, aB0, aB2, !first);
+      mma_wg_b16(c.tmem + PT_BG, aB1, aB3, true);
+      mma_kb16(c.tmem + PT_G, aB2, aW2b);
+      mma_kb16(c.tmem + PT_GP, aB3, aW2b);
       tc::commit(c.mbar);
     }
     b16_colsum_add(B2, csb);  // dbeta += sum mu
@@ -538,12 +561,11 @@ __global__ void __maxnreg__(JANUS_BF_MAXNREG) msg_bf_pair_tc(EdgeGeom g, const f
     TC_M();
     __syncthreads();  // column sums done: B2, B3 may be rewritten
     {
-      float z[FPT], zp[FPT], sb[FPT], sdb[FPT];
-      c.ld2(TM_Z, TM_ZP, z, zp);
-      c.ld2(TM_G, TM_GP, sb, sdb);
+      float sb[FPT], sdb[FPT];
+      c.ld2(PT_G, PT_GP, sb, sdb);
 #pragma unroll
       for (int k = 0; k < FPT; ++k) {
-        const float zz = z[k] + al[f0 + k], s1 = fsig_t(zz);
+        const float zz = z[k], s1 = fsig_t(zz);
         const float ds = s1 * (1.0f + zz * (1.0f - s1));
         const float d2s = s1 * (1.0f - s1) * (2.0f + zz * (1.0f - 2.0f * s1));
         z[k] = sb[k] * ds + sdb[k] * d2s * zp[k];  // zbar
@@ -554,8 +576,8 @@ __global__ void __maxnreg__(JANUS_BF_MAXNREG) msg_bf_pair_tc(EdgeGeom g, const f
     }
     c.publish();
     if (threadIdx.x == 0) {  // dA += phi^T zbar + phi'^T zbar'
-      mma_wg_b16(c.tmem + TM_AG, aB4, aB2, !first);
-      mma_wg_b16(c.tmem + TM_AG, aB5, aB3, true);
+      mma_wg_b16(c.tmem + PT_AG, aB4, aB2, !first);
+      mma_wg_b16(c.tmem + PT_AG, aB5, aB3, true);
       tc::commit(c.mbar);
     }
     b16_colsum_add(B2, csa);  // dalpha += sum zbar
@@ -568,14 +590,14 @@ __global__ void __maxnreg__(JANUS_BF_MAXNREG) msg_bf_pair_tc(EdgeGeom g, const f
   float* part = partial + (size_t)blockIdx.x * PE;
   if (first) {
     for (int x = threadIdx.x; x < PE; x += NT) part[x] = 0.f;
-    teardown(c, 512);
+    teardown(c, kPairCols);
     return;
   }
   TC_M();
-  write_partial(c, part, B0, csa, csb TC_PASS);
+  write_partial(c, part, B0, csa, csb, PT_AG, PT_BG TC_PASS);
   TC_M();
   TC_DUMP("bf_pair");
-  teardown(c, 512);
+  teardown(c, kPairCols);
 }
 
 __global__ void __maxnreg__(JANUS_BE_MAXNREG) msg_be_pair_tc(EdgeGeom g, const float4* __restrict__ pg, int n_pairs, MsgParams p,
@@ -602,7 +624,7 @@ __global__ void __maxnreg__(JANUS_BE_MAXNREG) msg_be_pair_tc(EdgeGeom g, const f
   c.mbar = &mbar;
   load_weights_b16(W2b, p.pack, al, be, &wbar);
   if (threadIdx.x < 128) csa[threadIdx.x] = 0.f;
-  setup(c, &tslot, 512);
+  setup(c, &tslot, kPairCols);
   const uint32_t aW0b = tc::smem_u32(W0b), aW2b = tc::smem_u32(W2b);
   const uint32_t aB0 = tc::smem_u32(B0), aB1 = tc::smem_u32(B1), aB2 = tc::smem_u32(B2), aB3 = tc::smem_u32(B3);
   bool first = true;
@@ -622,13 +644,13 @@ __global__ void __maxnreg__(JANUS_BE_MAXNREG) msg_be_pair_tc(EdgeGeom g, const f
     tc::mbar_wait(&wbar, 0);
     c.publish();
     if (threadIdx.x == 0) {
-      mma_kb16(c.tmem + TM_Z, aB0, aW0b);
+      mma_kb16(c.tmem + BT_Z, aB0, aW0b);
       tc::commit(c.mbar);
     }
     c.wait_mma();
     {
       float z[FPT];
-      c.ld(TM_Z, z);
+      c.ld(BT_Z, z);
 #pragma unroll
       for (int k = 0; k < FPT; ++k) {
         const float zz = z[k] + al[f0 + k];
@@ -638,15 +660,15 @@ __global__ void __maxnreg__(JANUS_BE_MAXNREG) msg_be_pair_tc(EdgeGeom g, const f
     }
     c.publish();
     if (threadIdx.x == 0) {
-      mma_wg_b16(c.tmem + TM_BG, aB1, aB2, !first);  // dB += s^T gbar
-      mma_kb16(c.tmem + TM_G, aB2, aW2b);            // sbar = gbar B^T
+      mma_wg_b16(c.tmem + BT_BG, aB1, aB2, !first);  // dB += s^T gbar
+      mma_kb16(c.tmem + BT_G, aB2, aW2b);            // sbar = gbar B^T
       tc::commit(c.mbar);
     }
     b16_colsum_add(B2, csb);  // dbeta += sum gbar
     c.wait_mma();
     {
       float z[FPT], sb[FPT];
-      c.ld2(TM_Z, TM_G, z, sb);
+      c.ld2(BT_Z, BT_G, z, sb);
 #pragma unroll
       for (int k = 0; k < FPT; ++k) {
         const float zz = z[k] + al[f0 + k], s1 = fsig_t(zz);
@@ -656,7 +678,7 @@ __global__ void __maxnreg__(JANUS_BE_MAXNREG) msg_be_pair_tc(EdgeGeom g, const f
     }
     c.publish();
     if (threadIdx.x == 0) {
-      mma_wg_b16(c.tmem + TM_AG, aB0, aB3, !first);  // dA += phi^T zbar
+      mma_wg_b16(c.tmem + BT_AG, aB0, aB3, !first);  // dA += phi^T zbar
       tc::commit(c.mbar);
     }
     b16_colsum_add(B3, csa);  // dalpha += sum zbar
@@ -667,11 +689,11 @@ __global__ void __maxnreg__(JANUS_BE_MAXNREG) msg_be_pair_tc(EdgeGeom g, const f
   float* part = partial + (size_t)blockIdx.x * PE;
   if (first) {
     for (int x = threadIdx.x; x < PE; x += NT) part[x] = 0.f;
-    teardown(c, 512);
+    teardown(c, kPairCols);
     return;
   }
-  write_partial(c, part, B0, csa, csb TC_PASS);
-  teardown(c, 512);
+  write_partial(c, part, B0, csa, csb, BT_AG, BT_BG TC_PASS);
+  teardown(c, kPairCols);
 }
 
 // The BF / BE pair kernels' per-CTA partials, summed into the phase's ledger

@@ -18,3 +18,8 @@ for k in msg_bf_pair_tc msg_be_pair_tc msg_filter_tc msg_fe_rows msg_ff_rows msg
 done
 timeout 300 ncu --set full --clock-control none -k regex:"walk_pad" -c 1 -o $out/${tag}_walk_pad python tools/e2e_probe.py --steps 1 > $out/${tag}_ncu_walk.log 2>&1
 ls -la $out | grep $tag
+# summaries on the box; keep only the top kernel's report (gpurun returns <= 64 MiB)
+python tools/ncu_summary.py $out/${tag}_*.ncu-rep > $out/${tag}_ncu_summary.json 2> $out/${tag}_ncu_summary.err
+for f in $out/${tag}_*.ncu-rep; do
+  case $f in *msg_bf_pair_tc*) ;; *) rm -f $f ;; esac
+done

@@ -160,6 +160,9 @@ def main():
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "pipeline_report.json"))
     ap.add_argument("--Ps", default="2,4,8")
     ap.add_argument("--nmb", type=int, default=32)
+    ap.add_argument("--kmult", default="0.5,1,2,4",
+                    help="WaveK candidate unit sizes k = m P (divisors of N_mb only): the paper's offline sweep "
+                         "(PAPER.md:865, 'evaluate a few candidate k values ... and select the best')")
     args = ap.parse_args()
     model = J.Model(L=4, H=64, R=64, precision=J.PREC_TF32)
     params = model.synth_params(7)
@@ -167,8 +170,10 @@ def main():
     rows = []
     for P in [int(x) for x in args.Ps.split(",")]:
         ph = None
-        for method, k in ((J.METHOD_SYMFOLD, 1), (J.METHOD_ONEF1B, 1), (J.METHOD_HANAYO, 1), (J.METHOD_WAVEK, P),
-                          (J.METHOD_WAVEK, 2 * P)):
+        ks = sorted({max(1, int(round(float(f) * P))) for f in args.kmult.split(",")})
+        ks = [k for k in ks if k <= args.nmb and args.nmb % k == 0]
+        cases = [(J.METHOD_SYMFOLD, 1), (J.METHOD_ONEF1B, 1), (J.METHOD_HANAYO, 1)] + [(J.METHOD_WAVEK, k) for k in ks]
+        for method, k in cases:
             r = run(model, params, batches, P, method, k, phase_us=ph if method == J.METHOD_WAVEK else None)
             if method == J.METHOD_SYMFOLD:  # WaveK's cost model: this box's measured phase means
                 m = r["phase_mean_us"]
@@ -176,9 +181,17 @@ def main():
             rows.append(r)
             print(json.dumps({x: r[x] for x in ("P", "method", "k", "makespan_ms", "structures_per_s", "bubble_measured",
                                                 "bubble_replay", "peak_hbm_bytes_max_device")}), flush=True)
+    summary = []
+    for P in sorted({r["P"] for r in rows}):
+        sf = next(r for r in rows if r["P"] == P and r["method"] == "symfold")
+        wk = max((r for r in rows if r["P"] == P and r["method"] == "wavek"), key=lambda r: r["structures_per_s"])
+        summary.append({"P": P, "symfold": sf["structures_per_s"], "wavek_best_k": wk["k"],
+                        "wavek_best": wk["structures_per_s"], "wavek_over_symfold": wk["structures_per_s"] / sf["structures_per_s"],
+                        "bubble_symfold": sf["bubble_measured"], "bubble_wavek_best": wk["bubble_measured"]})
+        print(json.dumps(summary[-1]), flush=True)
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
-    json.dump({"config": "C2: L=4 H=64 R=64, 256-atom cells, N_mb=%d, tf32, 1 GPU, lanes=1" % args.nmb, "rows": rows},
-              open(args.out, "w"), indent=1)
+    json.dump({"config": "C2: L=4 H=64 R=64, 256-atom cells, N_mb=%d, tf32, 1 GPU, lanes=1" % args.nmb, "rows": rows,
+               "wavek_sweep": summary}, open(args.out, "w"), indent=1)
 
 
 if __name__ == "__main__":
