@@ -168,6 +168,7 @@ __device__ __forceinline__ void chunk_basis(const EdgeGeom& g, float rc, int c0,
 template <int H, int R>
 __global__ void __launch_bounds__(NT) msg_fe_kernel(EdgeGeom g, MsgParams p, float rc, const float* __restrict__ v,
                                                     float* __restrict__ m_out) {
+  JANUS_GDC_WAIT();
   using C = Cfg<H, R>;
   extern __shared__ __align__(16) float sm[];
   float* sA = sm;
@@ -231,6 +232,7 @@ template <int H, int R>
 __global__ void __launch_bounds__(NT) msg_ff_kernel(EdgeGeom g, MsgParams p, float rc, const float* __restrict__ v,
                                                     const float* __restrict__ am, float* __restrict__ Y_out,
                                                     float* __restrict__ F) {
+  JANUS_GDC_WAIT();
   using C = Cfg<H, R>;
   extern __shared__ __align__(16) float sm[];
   float* sA = sm;
@@ -336,6 +338,7 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_kernel(EdgeGeom g, MsgParams p, 
                                                        const float* __restrict__ am, const float* __restrict__ Fbar,
                                                        float* __restrict__ mdot_out, float* __restrict__ X_out,
                                                        float* __restrict__ partial) {
+  JANUS_GDC_WAIT();
   using C = Cfg<H, R>;
   extern __shared__ __align__(16) float sm[];
   float* sA = sm;
@@ -505,6 +508,7 @@ template <int H, int R>
 __global__ void __launch_bounds__(NT) msg_be_kernel(EdgeGeom g, MsgParams p, float rc, const float* __restrict__ v,
                                                     const float* __restrict__ bm, float* __restrict__ Yb_out,
                                                     float* __restrict__ partial) {
+  JANUS_GDC_WAIT();
   using C = Cfg<H, R>;
   extern __shared__ __align__(16) float sm[];
   float* sA = sm;
@@ -630,6 +634,7 @@ constexpr int kReduceCols = 32;
 inline int reduce_grid(int PE) { return (PE + kReduceCols - 1) / kReduceCols; }
 __global__ void __launch_bounds__(256) reduce_partials_kernel(const float* __restrict__ partial, int n_tiles, int PE,
                                                               float* __restrict__ out) {
+  JANUS_GDC_WAIT();
   __shared__ float red[8][kReduceCols + 1];
   const int c = threadIdx.x & 31, grp = threadIdx.x >> 5;
   const int p = blockIdx.x * kReduceCols + c;
@@ -656,6 +661,7 @@ __global__ void __launch_bounds__(256) reduce_partials_kernel(const float* __res
 constexpr int kSeqPartials = 48;
 __global__ void __launch_bounds__(256) reduce_partials_seq_kernel(const float* __restrict__ partial, int n, int PE,
                                                                   float* __restrict__ out) {
+  JANUS_GDC_WAIT();
   const int p = blockIdx.x * 256 + threadIdx.x;
   if (p >= PE) return;
   const float* src = partial + p;

@@ -166,6 +166,7 @@ constexpr uint32_t kPackBytes = kW1bOff + kW2bBytes;
 
 __global__ void pack_msg_weights(const float* __restrict__ A, const float* __restrict__ alpha, const float* __restrict__ B,
                                  const float* __restrict__ beta, const float* __restrict__ W, float* __restrict__ pack) {
+  JANUS_GDC_WAIT();
   uint8_t* dst = reinterpret_cast<uint8_t*>(pack);
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x < 64 * 64) {
@@ -463,6 +464,7 @@ __device__ __forceinline__ float fsig_t(float x) {
 // m_i = sum_{e in row i} w_e * v[col e], w = c (SiLU(phi A + alpha) B + beta)
 __global__ void __launch_bounds__(NT, JANUS_FEFF_CTAS) msg_fe_tc(EdgeGeom g, const int4* __restrict__ tiles, int n_tiles, MsgParams p,
                                                float rc, const float* __restrict__ v, float* __restrict__ m_out) {
+  JANUS_GDC_WAIT();
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = align1024(sm_raw);
   TC_DECL;
@@ -568,6 +570,7 @@ __global__ void __launch_bounds__(NT, JANUS_FEFF_CTAS) msg_ff_tc(EdgeGeom g, con
                                                float rc, const float* __restrict__ v, const float* __restrict__ am,
                                                float* __restrict__ Y_out, float* __restrict__ F,
                                                float* ah) {
+  JANUS_GDC_WAIT();
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = align1024(sm_raw);
   uint8_t* W0 = sm;
@@ -839,6 +842,7 @@ __global__ void __launch_bounds__(NT, 1) msg_be_tc(EdgeGeom g, const int4* __res
                                                   float rc, const float* __restrict__ v, const float* __restrict__ bm,
                                                   float* __restrict__ Yb_out, float* __restrict__ partial,
                                                   const float* __restrict__ inj, float* bh) {
+  JANUS_GDC_WAIT();
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = align1024(sm_raw);
   TC_DECL;
@@ -1002,6 +1006,7 @@ __global__ void __launch_bounds__(NT, 1) msg_bf_tc(EdgeGeom g, const int4* __res
                                                   float* __restrict__ mdot_out, float* __restrict__ X_out,
                                                   float* __restrict__ partial,
                                                   float* __restrict__ inj) {
+  JANUS_GDC_WAIT();
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = align1024(sm_raw);
   TC_DECL;

@@ -47,6 +47,7 @@ template <int H, typename InOp>
 __global__ void __launch_bounds__(256) gemm_rows_kernel(int rows, const float* __restrict__ X, const float* __restrict__ M,
                                                         const float* __restrict__ bias, const float* add1, const float* add2,
                                                         float* out, InOp op) {
+  JANUS_GDC_WAIT();
   constexpr int RB = 256 / H;
   __shared__ __align__(16) float sx[RB][H];
   const int r0 = blockIdx.x * RB;
@@ -81,6 +82,7 @@ __global__ void __launch_bounds__(256) wgrad_partial_kernel(int rows, const floa
                                                             const float* __restrict__ a2, const float* __restrict__ b2,
                                                             const float* __restrict__ x1, const float* __restrict__ x2,
                                                             float* __restrict__ part, InOp op) {
+  JANUS_GDC_WAIT();
   static_assert(H == 64, "tile mapping assumes H = 64");
   __shared__ __align__(16) float sa[kWChunk][H + 4];
   __shared__ __align__(16) float sb[kWChunk][H + 4];
@@ -156,6 +158,7 @@ __global__ void __launch_bounds__(256) wgrad_partial_kernel(int rows, const floa
 template <int H>
 __global__ void wgrad_final_kernel(int n_chunks, const float* __restrict__ part, float* __restrict__ G,
                                    float* __restrict__ cs_out1, float* __restrict__ cs_out2) {
+  JANUS_GDC_WAIT();
   const int o = blockIdx.x * blockDim.x + threadIdx.x;
   constexpr int W = H * H + 2 * H;
   if (o >= W) return;
@@ -173,6 +176,7 @@ template <int H>
 __global__ void species_sum_partial_kernel(int rows, int S, const int* __restrict__ species, const float* __restrict__ x,
                                            const float* __restrict__ eps, const int* __restrict__ struct_id,
                                            float* __restrict__ part) {
+  JANUS_GDC_WAIT();
   const int i0 = blockIdx.x * kWChunk;
   const int n = min(kWChunk, rows - i0);
   for (int o = threadIdx.x; o < S * H; o += blockDim.x) {
@@ -190,6 +194,7 @@ __global__ void species_sum_partial_kernel(int rows, int S, const int* __restric
 template <int H>
 __global__ void species_sum_final_kernel(int n_chunks, int S, int stride_out, const float* __restrict__ part,
                                          float* __restrict__ out) {
+  JANUS_GDC_WAIT();
   const int o = blockIdx.x * blockDim.x + threadIdx.x;
   if (o >= S * H) return;
   const int z = o / H, k = o % H;
@@ -204,6 +209,7 @@ __global__ void species_sum_final_kernel(int n_chunks, int S, int stride_out, co
 __global__ void upd_bf_ew_kernel(int n, const float* __restrict__ r, const float* __restrict__ pdot,
                                  const float* __restrict__ p, float* __restrict__ pbar, float* __restrict__ pdbar,
                                  float* __restrict__ u) {
+  JANUS_GDC_WAIT();
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= n) return;
   const float pp = p[x], ds = dev::dsilu(pp);
@@ -214,6 +220,7 @@ __global__ void upd_bf_ew_kernel(int n, const float* __restrict__ r, const float
 
 // upd BE: pbar = r SiLU'(p)
 __global__ void upd_be_ew_kernel(int n, const float* __restrict__ r, const float* __restrict__ p, float* __restrict__ pbar) {
+  JANUS_GDC_WAIT();
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= n) return;
   pbar[x] = r[x] * dev::dsilu(p[x]);
@@ -224,6 +231,7 @@ template <int H>
 __global__ void ro_bf_ew_kernel(int n, const float* __restrict__ tdot, const float* __restrict__ t,
                                 const float* __restrict__ omega, float* __restrict__ tau, float* __restrict__ w2,
                                 float* __restrict__ sw) {
+  JANUS_GDC_WAIT();
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= n) return;
   const int k = x % H;
@@ -238,6 +246,7 @@ template <int H>
 __global__ void ro_be_ew_kernel(int n, const float* __restrict__ t, const float* __restrict__ omega,
                                 const float* __restrict__ eps, const int* __restrict__ struct_id, float* __restrict__ tbar,
                                 float* __restrict__ es) {
+  JANUS_GDC_WAIT();
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= n) return;
   const int i = x / H, k = x % H;
@@ -250,6 +259,7 @@ __global__ void ro_be_ew_kernel(int n, const float* __restrict__ t, const float*
 template <int H>
 __global__ void embed_fe_kernel(int n_atoms, const int* __restrict__ species, const float* __restrict__ Emb,
                                 float* __restrict__ h) {
+  JANUS_GDC_WAIT();
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= n_atoms * H) return;
   const int i = x / H, k = x % H;
@@ -261,6 +271,7 @@ template <int H>
 __global__ void readout_energy_kernel(int n_atoms, const float* __restrict__ t, const float* __restrict__ omega,
                                       const float* __restrict__ bias, const int* __restrict__ species,
                                       float* __restrict__ e_atom) {
+  JANUS_GDC_WAIT();
   const int i = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x & 31;
   if (i >= n_atoms) return;
   float s = 0.f;
@@ -274,6 +285,7 @@ __global__ void readout_energy_kernel(int n_atoms, const float* __restrict__ t, 
 __global__ void energy_loss_kernel(int n_struct, const int* __restrict__ struct_ptr, const float* __restrict__ e_atom,
                                    const float* __restrict__ E_target, float w_E, float* __restrict__ E,
                                    float* __restrict__ eps, float* __restrict__ loss_E) {
+  JANUS_GDC_WAIT();
   for (int s = threadIdx.x; s < n_struct; s += blockDim.x) {
     float acc = 0.f;
     for (int i = struct_ptr[s]; i < struct_ptr[s + 1]; ++i) acc += e_atom[i];
@@ -294,6 +306,7 @@ __global__ void energy_loss_kernel(int n_struct, const int* __restrict__ struct_
 // Fbar = 2 w_F (F - F*); loss_F = sum w_F |F - F*|^2 (single CTA, fixed tree)
 __global__ void force_loss_kernel(int n3, const float* __restrict__ F, const float* __restrict__ F_target, float w_F,
                                   float* __restrict__ Fbar, float* __restrict__ loss_F) {
+  JANUS_GDC_WAIT();
   __shared__ float red[1024];
   float l = 0.f;
   for (int x = threadIdx.x; x < n3; x += blockDim.x) {
@@ -314,6 +327,7 @@ __global__ void force_loss_kernel(int n3, const float* __restrict__ F, const flo
 // g = sum_mb (g1[mb] + g2[mb]) in micro-batch order (schedule-independent)
 __global__ void ledger_reduce_kernel(int64_t n, int n_mb, const float* __restrict__ g1, const float* __restrict__ g2,
                                      float* __restrict__ g) {
+  JANUS_GDC_WAIT();
   const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= n) return;
   float s = 0.f;
@@ -324,7 +338,8 @@ __global__ void ledger_reduce_kernel(int64_t n, int n_mb, const float* __restric
   g[x] = s;
 }
 
-__global__ void adam_tick_kernel(int* step) { *step += 1; }
+__global__ void adam_tick_kernel(int* step) {
+  JANUS_GDC_WAIT(); *step += 1; }
 
 // Bias corrections from the device-side step counter and the hyperparameters
 // {lr, beta1, beta2, eps} from a device buffer, so a captured step (CUDA
@@ -332,6 +347,7 @@ __global__ void adam_tick_kernel(int* step) { *step += 1; }
 __global__ void adam_kernel(int64_t n, float* __restrict__ p, float* __restrict__ m1, float* __restrict__ m2,
                             const float* __restrict__ g, const float* __restrict__ hp,
                             const int* __restrict__ step) {
+  JANUS_GDC_WAIT();
   const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= n) return;
   const float lr = hp[0], b1 = hp[1], b2 = hp[2], eps = hp[3];
@@ -348,6 +364,7 @@ __global__ void adam_kernel(int64_t n, float* __restrict__ p, float* __restrict_
 // dst[c][r] = src[r][c] for a square H x H block
 template <int H>
 __global__ void transpose_kernel(const float* __restrict__ src, float* __restrict__ dst) {
+  JANUS_GDC_WAIT();
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= H * H) return;
   const int r = x / H, c = x % H;
@@ -363,6 +380,7 @@ __global__ void geometry_kernel(int n_atoms, int n_edges, const int* __restrict_
                                 const int* __restrict__ struct_id, const double* __restrict__ cell, double rc,
                                 int* __restrict__ src, float* __restrict__ d_out, float* __restrict__ u_out,
                                 float* __restrict__ c_out, float* __restrict__ dc_out) {
+  JANUS_GDC_WAIT();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n_edges) return;
   int lo = 0, hi = n_atoms;  // largest i with row_ptr[i] <= e
@@ -392,6 +410,7 @@ __global__ void geometry_kernel(int n_atoms, int n_edges, const int* __restrict_
 // rebased, then the same per-edge geometry as geometry_kernel.  The job table
 // travels as a kernel parameter.
 __global__ void geometry_batched_kernel(const __grid_constant__ GeoJobs J) {
+  JANUS_GDC_WAIT();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= J.total_edges) return;
   int k = 0;
@@ -533,6 +552,7 @@ template <int RB, typename InOp>
 __global__ void __launch_bounds__(16 * RB) gemm_rb_kernel(int rows, const float* __restrict__ X, const float* __restrict__ M,
                                                           const float* __restrict__ bias, const float* add1, const float* add2,
                                                           float* out, InOp op) {
+  JANUS_GDC_WAIT();
   __shared__ __align__(16) float Xs[RB][68];
   extern __shared__ __align__(16) float Ws[];
   const int i0 = blockIdx.x * RB, r = threadIdx.x / 16, c0 = (threadIdx.x % 16) * 4, i = i0 + r;
@@ -568,6 +588,7 @@ __global__ void __launch_bounds__(16 * RB) upd_fe_fused(int rows, const float* _
                                                     const float* __restrict__ V, float* __restrict__ p_out,
                                                     float* __restrict__ h_out, const float* __restrict__ Wn,
                                                     float* __restrict__ v_out) {
+  JANUS_GDC_WAIT();
   __shared__ __align__(16) float X[RB][68];
   extern __shared__ __align__(16) float Ws[];
   const int i0 = blockIdx.x * RB, r = threadIdx.x / 16, c0 = (threadIdx.x % 16) * 4, i = i0 + r;
@@ -609,6 +630,7 @@ template <int RB>
 __global__ void __launch_bounds__(16 * RB) upd_ff_fused(int rows, const float* __restrict__ a, const float* __restrict__ p,
                                                     const float* __restrict__ Vt, const float* __restrict__ Ut,
                                                     float* __restrict__ ff_a, float* __restrict__ am) {
+  JANUS_GDC_WAIT();
   __shared__ __align__(16) float X[RB][68];
   extern __shared__ __align__(16) float Ws[];
   const int i0 = blockIdx.x * RB, r = threadIdx.x / 16, c0 = (threadIdx.x % 16) * 4, i = i0 + r;
@@ -647,6 +669,7 @@ __global__ void __launch_bounds__(16 * RB) upd_bf_fused(int rows, const float* _
                                                     float* __restrict__ pdbar, float* __restrict__ u,
                                                     float* __restrict__ inj, const float* ah, float* ah_out,
                                                     const float* __restrict__ Wn, float* __restrict__ vdot_out) {
+  JANUS_GDC_WAIT();
   __shared__ __align__(16) float X[RB][68];
   __shared__ __align__(16) float Y[RB][68];
   extern __shared__ __align__(16) float Ws[];
@@ -706,6 +729,7 @@ __global__ void __launch_bounds__(16 * RB) upd_be_fused(int rows, const float* _
                                                     const float* __restrict__ Vt, const float* __restrict__ Ut,
                                                     const float* __restrict__ inj, float* __restrict__ pbar,
                                                     float* __restrict__ bm) {
+  JANUS_GDC_WAIT();
   __shared__ __align__(16) float X[RB][68];
   extern __shared__ __align__(16) float Ws[];
   const int i0 = blockIdx.x * RB, r = threadIdx.x / 16, c0 = (threadIdx.x % 16) * 4, i = i0 + r;
@@ -756,6 +780,7 @@ struct WJobs {
 // output is summed by one thread in atom order => deterministic.
 __global__ void __launch_bounds__(256) wgrad_multi_kernel(int rows, WJobs jobs, float* __restrict__ /*part*/,
                                                           unsigned* __restrict__ /*counter*/) {
+  JANUS_GDC_WAIT();
   constexpr int H = 64;
   __shared__ __align__(16) float sa[kWChunk][8];
   __shared__ __align__(16) float sb[kWChunk][H + 4];

@@ -47,6 +47,7 @@ struct FilterJobs {
 // grid (chunks, units): CTA (x, y) runs unit y over 128-pair chunks x, x + gridDim.x, ...
 __global__ void __launch_bounds__(NT, JANUS_FEFF_CTAS) msg_filter_tc(EdgeGeom g, const float4* __restrict__ pg, int n_pairs,
                                                                     const __grid_constant__ FilterJobs J, float rc) {
+  JANUS_GDC_WAIT();
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = align1024(sm_raw);
   uint8_t* W0 = sm;            // A^T
@@ -146,6 +147,7 @@ __device__ __forceinline__ bool is_canonical(const node::GeoJob& jb, int e, int&
 }
 __global__ void __launch_bounds__(1024) pairs_count_kernel(const __grid_constant__ node::GeoJobs J, int* __restrict__ counts,
                                                            int chunks_cap) {
+  JANUS_GDC_WAIT();
   const node::GeoJob& jb = J.j[blockIdx.y];
   const int e0 = blockIdx.x * 1024;
   if (e0 >= jb.n_edges) return;
@@ -164,6 +166,7 @@ __global__ void __launch_bounds__(1024) pairs_count_kernel(const __grid_constant
 }
 __global__ void __launch_bounds__(1024) pairs_kernel(const __grid_constant__ node::GeoJobs J, const int* __restrict__ counts,
                                                      int chunks_cap) {
+  JANUS_GDC_WAIT();
   const node::GeoJob& jb = J.j[blockIdx.y];
   const int e0 = blockIdx.x * 1024;
   if (e0 >= jb.n_edges) return;
@@ -218,6 +221,7 @@ template <int KF>  // edges whose gathers are in flight per step
 __global__ void __launch_bounds__(256) msg_fe_rows(int n_atoms, const int* __restrict__ row_ptr, const int* __restrict__ col,
                                                    const int* __restrict__ pidx, const float* __restrict__ w,
                                                    const float* __restrict__ v, float* __restrict__ m_out) {
+  JANUS_GDC_WAIT();
   const int i = blockIdx.x * 8 + static_cast<int>(threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (i >= n_atoms) return;
   const int eb = __ldg(row_ptr + i), ee = __ldg(row_ptr + i + 1);
@@ -255,6 +259,7 @@ __global__ void __launch_bounds__(256) msg_ff_rows(int n_atoms, const int* __res
                                                    const float* __restrict__ v, const float* __restrict__ am,
                                                    const float* __restrict__ wt, float* __restrict__ Y_out,
                                                    float* __restrict__ F, float* ah) {
+  JANUS_GDC_WAIT();
   const int i = blockIdx.x * 8 + static_cast<int>(threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (i >= n_atoms) return;
   const int eb = __ldg(row_ptr + i), ee = __ldg(row_ptr + i + 1);
@@ -475,6 +480,7 @@ __global__ void __maxnreg__(JANUS_BF_MAXNREG) msg_bf_pair_tc(EdgeGeom g, const f
                                                        float rc, const float* __restrict__ v, const float* __restrict__ vdot,
                                                        const float* __restrict__ am, const float* __restrict__ Fbar,
                                                        float* __restrict__ partial) {
+  JANUS_GDC_WAIT();
   TC_DECL;
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = align1024(sm_raw);
@@ -603,6 +609,7 @@ __global__ void __maxnreg__(JANUS_BF_MAXNREG) msg_bf_pair_tc(EdgeGeom g, const f
 __global__ void __maxnreg__(JANUS_BE_MAXNREG) msg_be_pair_tc(EdgeGeom g, const float4* __restrict__ pg, int n_pairs, MsgParams p,
                                                        float rc, const float* __restrict__ v, const float* __restrict__ bm,
                                                        float* __restrict__ partial) {
+  JANUS_GDC_WAIT();
   TC_DECL;
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = align1024(sm_raw);
@@ -732,6 +739,7 @@ __global__ void __launch_bounds__(256) msg_bf_rows(int n_atoms, const int* __res
                                                    const float* __restrict__ wt, float* __restrict__ mdot_out,
                                                    float* __restrict__ X_out, float* __restrict__ inj,
                                                    const __grid_constant__ PartialReduce red) {
+  JANUS_GDC_WAIT();
   const int row_blocks = (n_atoms + 7) / 8;
   if (static_cast<int>(blockIdx.x) >= row_blocks) {
     reduce_block(red, static_cast<int>(blockIdx.x) - row_blocks);
@@ -790,6 +798,7 @@ __global__ void __launch_bounds__(256) msg_be_rows(int n_atoms, const int* __res
                                                    const float* __restrict__ bm, const float* __restrict__ wt,
                                                    float* __restrict__ Yb_out, const float* __restrict__ inj, float* bh,
                                                    const __grid_constant__ PartialReduce red) {
+  JANUS_GDC_WAIT();
   const int row_blocks = (n_atoms + 7) / 8;
   if (static_cast<int>(blockIdx.x) >= row_blocks) {
     reduce_block(red, static_cast<int>(blockIdx.x) - row_blocks);

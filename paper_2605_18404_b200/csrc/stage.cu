@@ -31,18 +31,18 @@
 #define JANUS_UPD(KERN, SMEM, S, ...)                                                                 \
   do {                                                                                               \
     if (node::upd_rows_per_cta(N) == node::kRB)                                                      \
-      node::KERN<node::kRB><<<blocks(N, node::kRB), 16 * node::kRB, (SMEM), (S)>>>(__VA_ARGS__);     \
+      janus::pdl(node::KERN<node::kRB>, blocks(N, node::kRB), 16 * node::kRB, (SMEM), (S))(__VA_ARGS__);     \
     else                                                                                             \
-      node::KERN<node::kRBSmall><<<blocks(N, node::kRBSmall), 16 * node::kRBSmall, (SMEM), (S)>>>(__VA_ARGS__); \
+      janus::pdl(node::KERN<node::kRBSmall>, blocks(N, node::kRBSmall), 16 * node::kRBSmall, (SMEM), (S))(__VA_ARGS__); \
   } while (0)
 
 // row kernels (pair_tc.cuh) by the stage's gathers-in-flight setting
 #define JANUS_ROWS(KERN, GRID, S, ...)                                          \
   do {                                                                          \
     if (st->rows_kf == 4)                                                       \
-      edge_tc::KERN<4><<<(GRID), 256, 0, (S)>>>(__VA_ARGS__);                   \
+      janus::pdl(edge_tc::KERN<4>, (GRID), 256, 0, (S))(__VA_ARGS__);                   \
     else                                                                        \
-      edge_tc::KERN<8><<<(GRID), 256, 0, (S)>>>(__VA_ARGS__);                   \
+      janus::pdl(edge_tc::KERN<8>, (GRID), 256, 0, (S))(__VA_ARGS__);                   \
   } while (0)
 #include "node_kernels.cuh"
 #include "wide.cuh"
@@ -128,11 +128,11 @@ void gemm(cudaStream_t s, int rows, const float* X, const float* M, const float*
   if (rows <= 0 || (prof_skip() & 64)) return;
   static const bool rows4 = std::getenv("JANUS_GEMM_ROWS4") != nullptr;  // A/B: the 4-rows-per-CTA kernel
   if (rows4)
-    node::gemm_rows_kernel<kH, Op><<<blocks(rows, 256 / kH), 256, 0, s>>>(rows, X, M, bias, add1, add2, out, op);
+    janus::pdl(node::gemm_rows_kernel<kH, Op>, blocks(rows, 256 / kH), 256, 0, s)(rows, X, M, bias, add1, add2, out, op);
   else if (rows >= 256)
-    node::gemm_rb_kernel<node::kRB, Op><<<blocks(rows, node::kRB), 16 * node::kRB, node::upd_smem(1), s>>>(rows, X, M, bias, add1, add2, out, op);
+    janus::pdl(node::gemm_rb_kernel<node::kRB, Op>, blocks(rows, node::kRB), 16 * node::kRB, node::upd_smem(1), s)(rows, X, M, bias, add1, add2, out, op);
   else
-    node::gemm_rb_kernel<node::kRBSmall, Op><<<blocks(rows, node::kRBSmall), 16 * node::kRBSmall, node::upd_smem(1), s>>>(rows, X, M, bias, add1,
+    janus::pdl(node::gemm_rb_kernel<node::kRBSmall, Op>, blocks(rows, node::kRBSmall), 16 * node::kRBSmall, node::upd_smem(1), s)(rows, X, M, bias, add1,
                                                                                                                  add2, out, op);
   JANUS_LAUNCH_CHECK("gemm_rows");
 }
@@ -150,8 +150,8 @@ template <typename Op = node::InId>
 void wgrad(Scratch& sc, cudaStream_t s, int rows, const float* a, const float* b, const float* a2, const float* b2,
            float* G, Op op = Op{}, Colsums cs = {}) {
   const int chunks = blocks(rows, node::kWChunk);
-  node::wgrad_partial_kernel<kH, Op><<<chunks, 256, 0, s>>>(rows, a, b, a2, b2, cs.x1, cs.x2, sc.wpart, op);
-  node::wgrad_final_kernel<kH><<<blocks(kH * kH + 2 * kH, 256), 256, 0, s>>>(chunks, sc.wpart, G, cs.out1, cs.out2);
+  janus::pdl(node::wgrad_partial_kernel<kH, Op>, chunks, 256, 0, s)(rows, a, b, a2, b2, cs.x1, cs.x2, sc.wpart, op);
+  janus::pdl(node::wgrad_final_kernel<kH>, blocks(kH * kH + 2 * kH, 256), 256, 0, s)(chunks, sc.wpart, G, cs.out1, cs.out2);
   JANUS_LAUNCH_CHECK("wgrad");
 }
 
@@ -188,10 +188,10 @@ void wjobs(const janus_stage* st, Scratch& sc, cudaStream_t s, int rows, std::in
   if (use_tc(st) && !simt_only) {
     bool cs = false;
     for (int q = 0; q < J.n; ++q) cs = cs || J.j[q].x1 || J.j[q].x2;
-    edge_tc::wgrad_tc_kernel<<<dim3(static_cast<unsigned>(J.n), cs ? 2u : 1u), edge_tc::kWgT, edge_tc::wgrad_tc_smem(), s>>>(rows, J);
+    janus::pdl(edge_tc::wgrad_tc_kernel, dim3(static_cast<unsigned>(J.n), cs ? 2u : 1u), edge_tc::kWgT, edge_tc::wgrad_tc_smem(), s)(rows, J);
   } else {
     const dim3 grid(9u, static_cast<unsigned>(J.n));  // 8 row blocks of the gradient + 1 column-sum block
-    node::wgrad_multi_kernel<<<grid, 256, 0, s>>>(rows, J, sc.wpart, sc.counter);
+    janus::pdl(node::wgrad_multi_kernel, grid, 256, 0, s)(rows, J, sc.wpart, sc.counter);
   }
   JANUS_LAUNCH_CHECK("wgrad");
 }
@@ -199,8 +199,8 @@ void wjobs(const janus_stage* st, Scratch& sc, cudaStream_t s, int rows, std::in
 // out[z][k] = sum_{Z_i = z} x[i][k]; x == null: out[z] = sum_{Z_i = z} eps[s(i)]
 void species_sum(janus_stage* st, Scratch& sc, cudaStream_t s, const DevGeo& g, const float* x, const float* eps, float* out) {
   const int chunks = blocks(g.n_atoms, node::kWChunk), S = st->m.n_species;
-  node::species_sum_partial_kernel<kH><<<chunks, 256, 0, s>>>(g.n_atoms, S, g.species, x, eps, g.struct_id, sc.wpart);
-  node::species_sum_final_kernel<kH><<<blocks(S * kH, 256), 256, 0, s>>>(chunks, S, x ? kH : 1, sc.wpart, out);
+  janus::pdl(node::species_sum_partial_kernel<kH>, chunks, 256, 0, s)(g.n_atoms, S, g.species, x, eps, g.struct_id, sc.wpart);
+  janus::pdl(node::species_sum_final_kernel<kH>, blocks(S * kH, 256), 256, 0, s)(chunks, S, x ? kH : 1, sc.wpart, out);
   JANUS_LAUNCH_CHECK("species_sum");
 }
 
@@ -246,8 +246,8 @@ void refresh_transposes(janus_stage* st, cudaStream_t s) {
       if (unit_kind(u, st->m.L) != kMsg) continue;
       float* t = st->tw[static_cast<size_t>(u - st->u0)];
       const float* P = st->P(u);
-      wide::transpose_any_kernel<<<blocks(static_cast<int64_t>(R) * H, 256), 256, 0, s>>>(R, H, P, t);
-      wide::transpose_any_kernel<<<blocks(static_cast<int64_t>(H) * H, 256), 256, 0, s>>>(H, H, P + R * H + H, t + H * R);
+      janus::pdl(wide::transpose_any_kernel, blocks(static_cast<int64_t>(R) * H, 256), 256, 0, s)(R, H, P, t);
+      janus::pdl(wide::transpose_any_kernel, blocks(static_cast<int64_t>(H) * H, 256), 256, 0, s)(H, H, P + R * H + H, t + H * R);
     }
     JANUS_LAUNCH_CHECK("transpose_wide");
     return;
@@ -259,19 +259,19 @@ void refresh_transposes(janus_stage* st, cudaStream_t s) {
     const int b = blocks(H * H, 256);
     switch (unit_kind(u, st->m.L)) {
       case kMsg:
-        node::transpose_kernel<kH><<<b, 256, 0, s>>>(P + R * H + H, t);
-        node::transpose_kernel<kH><<<b, 256, 0, s>>>(P + R * H + H + H * H + H, t + H * H);
-        edge_tc::pack_msg_weights<<<b, 256, 0, s>>>(P, P + R * H, P + R * H + H, P + R * H + H + H * H,
+        janus::pdl(node::transpose_kernel<kH>, b, 256, 0, s)(P + R * H + H, t);
+        janus::pdl(node::transpose_kernel<kH>, b, 256, 0, s)(P + R * H + H + H * H + H, t + H * H);
+        janus::pdl(edge_tc::pack_msg_weights, b, 256, 0, s)(P, P + R * H, P + R * H + H, P + R * H + H + H * H,
                                                      P + R * H + H + H * H + H, t + 2 * H * H);
-        upd_tc::pack_msg_w<<<b, 256, 0, s>>>(P + R * H + H + H * H + H, t + 2 * H * H);
+        janus::pdl(upd_tc::pack_msg_w, b, 256, 0, s)(P + R * H + H + H * H + H, t + 2 * H * H);
         break;
       case kUpd:
-        node::transpose_kernel<kH><<<b, 256, 0, s>>>(P, t);
-        node::transpose_kernel<kH><<<b, 256, 0, s>>>(P + H * H + H, t + H * H);
-        upd_tc::pack_upd_weights<<<b, 256, 0, s>>>(P, P + H * H + H, t + 2 * H * H);
+        janus::pdl(node::transpose_kernel<kH>, b, 256, 0, s)(P, t);
+        janus::pdl(node::transpose_kernel<kH>, b, 256, 0, s)(P + H * H + H, t + H * H);
+        janus::pdl(upd_tc::pack_upd_weights, b, 256, 0, s)(P, P + H * H + H, t + 2 * H * H);
         break;
       case kReadout:
-        node::transpose_kernel<kH><<<b, 256, 0, s>>>(P, t);
+        janus::pdl(node::transpose_kernel<kH>, b, 256, 0, s)(P, t);
         break;
       default:
         break;
@@ -657,8 +657,8 @@ void launch_pairs(janus_stage* st, const node::GeoJobs& J, int max_edges_job, cu
   const int chunks = (max_edges_job + 1023) / 1024;
   if (chunks <= 0) return;
   const dim3 grid(static_cast<unsigned>(chunks), static_cast<unsigned>(J.n));
-  edge_tc::pairs_count_kernel<<<grid, 1024, 0, s>>>(J, st->pair_counts, st->pair_chunks_cap);
-  edge_tc::pairs_kernel<<<grid, 1024, 0, s>>>(J, st->pair_counts, st->pair_chunks_cap);
+  janus::pdl(edge_tc::pairs_count_kernel, grid, 1024, 0, s)(J, st->pair_counts, st->pair_chunks_cap);
+  janus::pdl(edge_tc::pairs_kernel, grid, 1024, 0, s)(J, st->pair_counts, st->pair_chunks_cap);
   JANUS_LAUNCH_CHECK("pairs");
 }
 
@@ -829,7 +829,7 @@ void stage_load(janus_stage* st, int mb, const janus_host_batch& hb, cudaStream_
   if (dcsr)  // the device-built CSR replaces the (unused) host regions of the block
     csr_slice_copy(*dcsr->csr, dcsr->atom0, dcsr->edge0, E, g.col, g.rev, g.shift, s);
   if (E > 0)
-    node::geometry_kernel<<<blocks(E, 256), 256, 0, s>>>(N, E, g.row_ptr, g.col, g.shift, g.pos, g.struct_id, g.cell,
+    janus::pdl(node::geometry_kernel, blocks(E, 256), 256, 0, s)(N, E, g.row_ptr, g.col, g.shift, g.pos, g.struct_id, g.cell,
                                                          static_cast<double>(st->m.r_c), g.src, g.d, g.u, g.c, g.dc);
   if (E > 0 && needs_pairs(st)) {
     node::GeoJobs J{};
@@ -871,7 +871,7 @@ void stage_geometry_flush(janus_stage* st, std::vector<node::GeoJob>& jobs, cuda
       base += J.j[k].n_edges;
     }
     J.total_edges = base;
-    if (base > 0) node::geometry_batched_kernel<<<blocks(base, 256), 256, 0, s>>>(J);
+    if (base > 0) janus::pdl(node::geometry_batched_kernel, blocks(base, 256), 256, 0, s)(J);
     if (base > 0 && needs_pairs(st)) {
       int emax = 0;
       for (int k = 0; k < J.n; ++k) emax = std::max(emax, J.j[k].n_edges);
@@ -898,7 +898,7 @@ void launch_filter(janus_stage* st, const DevGeo& g, Slot& sl, int u_only, cudaS
   if (J.n == 0 || g.n_pairs == 0) return;
   const int chunks = (g.n_pairs + edge_tc::TE - 1) / edge_tc::TE;
   const int gx = grid_x > 0 ? std::min(grid_x, chunks) : std::max(1, std::min(chunks, (chunks + st->tpc_filter - 1) / st->tpc_filter));
-  edge_tc::msg_filter_tc<<<dim3(gx, J.n), edge_tc::NT, edge_tc::filter_smem(), s>>>(edge_geom(g), g.pgeo, g.n_pairs, J,
+  janus::pdl(edge_tc::msg_filter_tc, dim3(gx, J.n), edge_tc::NT, edge_tc::filter_smem(), s)(edge_geom(g), g.pgeo, g.n_pairs, J,
                                                                                      st->m.r_c);
   JANUS_LAUNCH_CHECK("msg_filter_tc");
 }
@@ -926,14 +926,14 @@ void stage_fe(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
     const float* P = st->P(u);
     switch (unit_kind(u, L)) {
       case kEmbed:
-        node::embed_fe_kernel<kH><<<blocks(N * H, 256), 256, 0, s>>>(N, g.species, P, b.out_h);
+        janus::pdl(node::embed_fe_kernel<kH>, blocks(N * H, 256), 256, 0, s)(N, g.species, P, b.out_h);
         cur_h = b.out_h;
         break;
       case kMsg: {
         const float* W = P + R * H + H + H * H + H;
         if (v_ready) {
         } else if (upd_on_tc(st, N)) {  // the fused next-v product's bits (upd_tc.cuh rows_w_tc)
-          upd_tc::rows_w_tc<<<blocks(N, 128), edge_tc::NT, upd_tc::upd_tc_smem(2, 2), s>>>(N, cur_h, msg_params(st, u).pack,
+          janus::pdl(upd_tc::rows_w_tc, blocks(N, 128), edge_tc::NT, upd_tc::upd_tc_smem(2, 2), s)(N, cur_h, msg_params(st, u).pack,
                                                                                          1, b.v);
         } else {
           gemm(s, N, cur_h, W, nullptr, nullptr, nullptr, b.v);
@@ -943,10 +943,10 @@ void stage_fe(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
           if (!(prof_skip() & 1))
             JANUS_ROWS(msg_fe_rows, blocks(N, 8), s, N, g.row_ptr, g.col, g.pidx, b.wf, b.v, b.out_m);
         } else if (g.n_tiles > 0 && use_tc(st)) {
-          if (!(prof_skip() & 1)) edge_tc::msg_fe_tc<<<fe_grid(st, g), edge_tc::NT, edge_tc::fe_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, msg_params(st, u),
+          if (!(prof_skip() & 1)) janus::pdl(edge_tc::msg_fe_tc, fe_grid(st, g), edge_tc::NT, edge_tc::fe_smem(), s)(eg, g.tile_tc, g.n_tiles_tc, msg_params(st, u),
                                                                                  st->m.r_c, b.v, b.out_m);
         } else if (g.n_tiles > 0)
-          edge::msg_fe_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::fe_smem<kH, kR>(), s>>>(eg, msg_params(st, u), st->m.r_c, b.v, b.out_m);
+          janus::pdl(edge::msg_fe_kernel<kH, kR>, g.n_tiles, edge::NT, edge::fe_smem<kH, kR>(), s)(eg, msg_params(st, u), st->m.r_c, b.v, b.out_m);
         cur_m = b.out_m;
         break;
       }
@@ -959,7 +959,7 @@ void stage_fe(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
         if (prof_skip() & 32) {
         } else if (upd_on_tc(st, N)) {  // upd_tc.cuh: 128 atoms per CTA, 3xTF32 tcgen05 chain
           const float* T = st->tw[static_cast<size_t>(u - st->u0)];
-          upd_tc::upd_fe_tc<<<blocks(N, 128), edge_tc::NT, upd_tc::upd_tc_smem(6, 2), s>>>(
+          janus::pdl(upd_tc::upd_fe_tc, blocks(N, 128), edge_tc::NT, upd_tc::upd_tc_smem(6, 2), s)(
               N, cur_m, cur_h, T + 2 * H * H, ups, b.p, b.out_h, fuse ? msg_params(st, u + 1).pack : nullptr, vn);
         } else {
           JANUS_UPD(upd_fe_fused, node::upd_smem(fuse ? 3 : 2), s, N, cur_m, cur_h, Um, ups, V, b.p, b.out_h, Wn, vn);
@@ -972,8 +972,8 @@ void stage_fe(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
       case kReadout: {
         const float *O = P, *o = P + H * H, *om = P + H * H + H, *bias = P + H * H + 2 * H;
         gemm(s, N, cur_h, O, o, nullptr, nullptr, b.p);
-        node::readout_energy_kernel<kH><<<blocks(N, 8), 256, 0, s>>>(N, b.p, om, bias, g.species, mo.e_atom);
-        node::energy_loss_kernel<<<1, 128, 0, s>>>(g.n_struct, g.struct_ptr, mo.e_atom, g.E_target, st->m.w_E, mo.E,
+        janus::pdl(node::readout_energy_kernel<kH>, blocks(N, 8), 256, 0, s)(N, b.p, om, bias, g.species, mo.e_atom);
+        janus::pdl(node::energy_loss_kernel, 1, 128, 0, s)(g.n_struct, g.struct_ptr, mo.e_atom, g.E_target, st->m.w_E, mo.E,
                                                    mo.eps, mo.loss);
         break;
       }
@@ -1023,7 +1023,7 @@ void stage_ff(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
         float* am_dst = (u - 1 >= st->u0) ? sl.units[static_cast<size_t>(u - 1 - st->u0)].ff_a : wm;
         if (prof_skip() & 32) {
         } else if (upd_on_tc(st, N)) {
-          upd_tc::upd_ff_tc<<<blocks(N, 128), edge_tc::NT, upd_tc::upd_tc_smem(4, 2), s>>>(N, wh, b.p, T + 2 * H * H, b.ff_a,
+          janus::pdl(upd_tc::upd_ff_tc, blocks(N, 128), edge_tc::NT, upd_tc::upd_tc_smem(4, 2), s)(N, wh, b.p, T + 2 * H * H, b.ff_a,
                                                                                          am_dst);
         } else {
           JANUS_UPD(upd_ff_fused, node::upd_smem(2), s, N, wh, b.p, T + H * H, T, b.ff_a, am_dst);
@@ -1038,11 +1038,11 @@ void stage_ff(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
                                                                msg_params(st, u).pack + edge_tc::kWtOff / sizeof(float),
                                                                b.ff_Y, mo.F, wh);
         } else if (g.n_tiles > 0 && use_tc(st)) {  // a_h += Y W^T fused into the tile epilogue
-          if (!(prof_skip() & 2)) edge_tc::msg_ff_tc<<<fe_grid(st, g), edge_tc::NT, edge_tc::ff_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, msg_params(st, u),
+          if (!(prof_skip() & 2)) janus::pdl(edge_tc::msg_ff_tc, fe_grid(st, g), edge_tc::NT, edge_tc::ff_smem(), s)(eg, g.tile_tc, g.n_tiles_tc, msg_params(st, u),
                                                                                  st->m.r_c, b.v, b.ff_a, b.ff_Y, mo.F, wh);
         } else {
           if (g.n_tiles > 0)
-            edge::msg_ff_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::ff_smem<kH, kR>(), s>>>(eg, msg_params(st, u), st->m.r_c, b.v, b.ff_a, b.ff_Y, mo.F);
+            janus::pdl(edge::msg_ff_kernel<kH, kR>, g.n_tiles, edge::NT, edge::ff_smem<kH, kR>(), s)(eg, msg_params(st, u), st->m.r_c, b.v, b.ff_a, b.ff_Y, mo.F);
           else
             JANUS_CUDA(cudaMemsetAsync(b.ff_Y, 0, sizeof(float) * NH, s));
           gemm(s, N, b.ff_Y, T + H * H, nullptr, wh, nullptr, wh);  // a_h += Y W^T
@@ -1061,7 +1061,7 @@ void stage_ff(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
     if (out.has_m) copy(s, port_m(out, N), wm, NH);
     copy(s, port_v(out, N), mo.F, 3 * static_cast<size_t>(N));
   } else {  // forces complete on stage 0: L_F seed
-    node::force_loss_kernel<<<1, 1024, 0, s>>>(3 * N, mo.F, g.F_target, st->m.w_F, mo.Fbar, mo.loss + 1);
+    janus::pdl(node::force_loss_kernel, 1, 1024, 0, s)(3 * N, mo.F, g.F_target, st->m.w_F, mo.Fbar, mo.loss + 1);
     JANUS_LAUNCH_CHECK("force_loss");
   }
 }
@@ -1113,7 +1113,7 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
         const float* W = P + R * H + H + H * H + H;
         if (vdot_ready) {
         } else if (upd_on_tc(st, N)) {  // vdot with the fused product's bits
-          upd_tc::rows_w_tc<<<blocks(N, 128), edge_tc::NT, upd_tc::upd_tc_smem(2, 2), s>>>(N, ah, msg_params(st, u).pack,
+          janus::pdl(upd_tc::rows_w_tc, blocks(N, 128), edge_tc::NT, upd_tc::upd_tc_smem(2, 2), s)(N, ah, msg_params(st, u).pack,
                                                                                          0, sc.s1);
         } else {
           gemm(s, N, ah, W, nullptr, nullptr, nullptr, sc.s1);  // vdot
@@ -1124,7 +1124,7 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
           const int grid = pair_grid(st, g);
           const MsgParams mp = msg_params(st, u);
           if (g.n_pairs > 0 && !(prof_skip() & 4)) {
-            edge_tc::msg_bf_pair_tc<<<grid, edge_tc::NT, edge_tc::bf_pair_smem(), s>>>(eg, g.pgeo, g.n_pairs, mp, st->m.r_c, b.v,
+            janus::pdl(edge_tc::msg_bf_pair_tc, grid, edge_tc::NT, edge_tc::bf_pair_smem(), s)(eg, g.pgeo, g.n_pairs, mp, st->m.r_c, b.v,
                                                                                        sc.s1, b.ff_a, Fbar, sc.partial);
             JANUS_LAUNCH_CHECK("msg_bf_pair_tc");
           }
@@ -1137,16 +1137,16 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
             edge::reduce_partials(sc.partial, grid, EC::PE, G2, s);
         } else if (g.n_tiles > 0 && use_tc(st)) {
           const int grid = tc_grid(st, g);
-          if (!(prof_skip() & 4)) edge_tc::msg_bf_tc<<<grid, edge_tc::NT, edge_tc::bf_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, msg_params(st, u),
+          if (!(prof_skip() & 4)) janus::pdl(edge_tc::msg_bf_tc, grid, edge_tc::NT, edge_tc::bf_smem(), s)(eg, g.tile_tc, g.n_tiles_tc, msg_params(st, u),
                                                                           st->m.r_c, b.v, sc.s1, b.ff_a, Fbar, am, sc.s2,
                                                                           sc.partial, b.inj);  // + hbar^F = X W^T
           JANUS_LAUNCH_CHECK("msg_bf_tc");
           if (!(prof_skip() & 128)) edge::reduce_partials(sc.partial, grid, EC::PE, G2, s);
         } else if (g.n_tiles > 0) {
-          edge::msg_bf_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::bf_smem<kH, kR>(), s>>>(
+          janus::pdl(edge::msg_bf_kernel<kH, kR>, g.n_tiles, edge::NT, edge::bf_smem<kH, kR>(), s)(
               eg, msg_params(st, u), st->m.r_c, b.v, sc.s1, b.ff_a, Fbar, am, sc.s2, sc.partial);
           JANUS_LAUNCH_CHECK("msg_bf");
-          edge::reduce_partials_kernel<<<edge::reduce_grid(EC::PE), 256, 0, s>>>(sc.partial, g.n_tiles, EC::PE, G2);
+          janus::pdl(edge::reduce_partials_kernel, edge::reduce_grid(EC::PE), 256, 0, s)(sc.partial, g.n_tiles, EC::PE, G2);
         } else {
           JANUS_CUDA(cudaMemsetAsync(am, 0, sizeof(float) * NH, s));
           JANUS_CUDA(cudaMemsetAsync(sc.s2, 0, sizeof(float) * NH, s));
@@ -1166,7 +1166,7 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
         const float* Wn = fuse ? st->P(u + 1) + R * H + H + H * H + H : nullptr;
         if (prof_skip() & 32) {
         } else if (upd_on_tc(st, N)) {
-          upd_tc::upd_bf_tc<<<blocks(N, 128), edge_tc::NT, upd_tc::upd_tc_smem(5, 2), s>>>(
+          janus::pdl(upd_tc::upd_bf_tc, blocks(N, 128), edge_tc::NT, upd_tc::upd_tc_smem(5, 2), s)(
               N, am, b.ff_a, b.p, T + 2 * H * H, sc.s3, sc.s4, sc.s5, b.inj, ah, ah_alt,
               fuse ? msg_params(st, u + 1).pack : nullptr, fuse ? sc.s1 : nullptr);
         } else {
@@ -1189,7 +1189,7 @@ void stage_bf(janus_stage* st, int mb, int slot, cudaStream_t s, int lane) {
         const float *O = P, *om = P + H * H + H;
         float *dO = G2, *dob = G2 + H * H, *dom = G2 + H * H + H;
         gemm(s, N, ah, O, nullptr, nullptr, nullptr, sc.s1);  // tdot
-        node::ro_bf_ew_kernel<kH><<<blocks(NH, 256), 256, 0, s>>>(static_cast<int>(NH), sc.s1, b.p, om, sc.s2,
+        janus::pdl(node::ro_bf_ew_kernel<kH>, blocks(NH, 256), 256, 0, s)(static_cast<int>(NH), sc.s1, b.p, om, sc.s2,
                                                                   sc.s3, sc.s4);
         gemm(s, N, sc.s2, T, nullptr, nullptr, nullptr, b.inj);  // hbar^F = tau O^T
         wjobs(st, sc, s, N, {wjob(ah, sc.s4, dO, in_h(st, sl, u, N), sc.s2, false, sc.s3, dom, sc.s2, dob)});
@@ -1252,7 +1252,7 @@ void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only, 
         }
         const float* om = P + H * H + H;
         float *dO = G1, *dob = G1 + H * H, *dom = G1 + H * H + H, *dbias = G1 + H * H + 2 * H;
-        node::ro_be_ew_kernel<kH><<<blocks(NH, 256), 256, 0, s>>>(static_cast<int>(NH), b.p, om, mo.eps, g.struct_id,
+        janus::pdl(node::ro_be_ew_kernel<kH>, blocks(NH, 256), 256, 0, s)(static_cast<int>(NH), b.p, om, mo.eps, g.struct_id,
                                                                   sc.s1, sc.s2);
         gemm(s, N, sc.s1, T, nullptr, b.inj, nullptr, bh);  // b_h = tbar O^T + hbar^F
         wjobs(st, sc, s, N, {wjob(in_h(st, sl, u, N), sc.s1, dO, nullptr, nullptr, false, sc.s1, dob, sc.s2, dom)});
@@ -1264,7 +1264,7 @@ void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only, 
         // pbar (s2) = (b' V^T) SiLU'(p); b_m = pbar U^T + mbar^F
         if (prof_skip() & 32) {
         } else if (upd_on_tc(st, N)) {
-          upd_tc::upd_be_tc<<<blocks(N, 128), edge_tc::NT, upd_tc::upd_tc_smem(2, 1), s>>>(N, bh, b.p, T + 2 * H * H, b.inj,
+          janus::pdl(upd_tc::upd_be_tc, blocks(N, 128), edge_tc::NT, upd_tc::upd_tc_smem(2, 1), s)(N, bh, b.p, T + 2 * H * H, b.inj,
                                                                                           sc.s2, bm);
         } else {
           JANUS_UPD(upd_be_fused, node::upd_smem(2), s, N, bh, b.p, T + H * H, T, b.inj, sc.s2, bm);
@@ -1284,7 +1284,7 @@ void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only, 
           const int grid = pair_grid(st, g);
           const MsgParams mp = msg_params(st, u);
           if (g.n_pairs > 0 && !(prof_skip() & 8)) {
-            edge_tc::msg_be_pair_tc<<<grid, edge_tc::NT, edge_tc::be_pair_smem(), s>>>(eg, g.pgeo, g.n_pairs, mp, st->m.r_c, b.v, bm,
+            janus::pdl(edge_tc::msg_be_pair_tc, grid, edge_tc::NT, edge_tc::be_pair_smem(), s)(eg, g.pgeo, g.n_pairs, mp, st->m.r_c, b.v, bm,
                                                                                        sc.partial);
             JANUS_LAUNCH_CHECK("msg_be_pair_tc");
           }
@@ -1297,16 +1297,16 @@ void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only, 
             edge::reduce_partials(sc.partial, grid, EC::PE, G1, s);
         } else if (g.n_tiles > 0 && use_tc(st)) {
           const int grid = tc_grid(st, g);
-          if (!(prof_skip() & 8)) edge_tc::msg_be_tc<<<grid, edge_tc::NT, edge_tc::be_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, msg_params(st, u),
+          if (!(prof_skip() & 8)) janus::pdl(edge_tc::msg_be_tc, grid, edge_tc::NT, edge_tc::be_smem(), s)(eg, g.tile_tc, g.n_tiles_tc, msg_params(st, u),
                                                                           st->m.r_c, b.v, bm, sc.s1, sc.partial,
                                                                           b.inj, bh);  // + b_h += Yb W^T + hbar^F
           JANUS_LAUNCH_CHECK("msg_be_tc");
           if (!(prof_skip() & 128)) edge::reduce_partials(sc.partial, grid, EC::PE, G1, s);
         } else if (g.n_tiles > 0) {
-          edge::msg_be_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::be_smem<kH, kR>(), s>>>(
+          janus::pdl(edge::msg_be_kernel<kH, kR>, g.n_tiles, edge::NT, edge::be_smem<kH, kR>(), s)(
               eg, msg_params(st, u), st->m.r_c, b.v, bm, sc.s1, sc.partial);
           JANUS_LAUNCH_CHECK("msg_be");
-          edge::reduce_partials_kernel<<<edge::reduce_grid(EC::PE), 256, 0, s>>>(sc.partial, g.n_tiles, EC::PE, G1);
+          janus::pdl(edge::reduce_partials_kernel, edge::reduce_grid(EC::PE), 256, 0, s)(sc.partial, g.n_tiles, EC::PE, G1);
         } else {
           JANUS_CUDA(cudaMemsetAsync(sc.s1, 0, sizeof(float) * NH, s));
         }
@@ -1334,19 +1334,20 @@ void stage_be(janus_stage* st, int mb, int slot, cudaStream_t s, bool inj_only, 
 
 // dst[x] += src[x]
 __global__ void add_kernel(int64_t n, float* __restrict__ dst, const float* __restrict__ src) {
+  JANUS_GDC_WAIT();
   const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (x < n) dst[x] += src[x];
 }
 
 void add_into(float* dst, const float* src, int64_t n, cudaStream_t s) {
   if (n <= 0) return;
-  add_kernel<<<blocks(n, 256), 256, 0, s>>>(n, dst, src);
+  janus::pdl(add_kernel, blocks(n, 256), 256, 0, s)(n, dst, src);
   JANUS_LAUNCH_CHECK("add");
 }
 
 // ============================================================ grads / OS
 void stage_reduce_grads(janus_stage* st, cudaStream_t s) {
-  node::ledger_reduce_kernel<<<blocks(st->n_params, 256), 256, 0, s>>>(st->n_params, st->desc.n_micro_batches, st->g1,
+  janus::pdl(node::ledger_reduce_kernel, blocks(st->n_params, 256), 256, 0, s)(st->n_params, st->desc.n_micro_batches, st->g1,
                                                                        st->g2, st->grad);
   JANUS_LAUNCH_CHECK("ledger_reduce");
 }
@@ -1357,8 +1358,8 @@ void stage_optimizer(janus_stage* st, const janus_opt& o, cudaStream_t s, const 
     JANUS_CUDA(cudaMemcpyAsync(st->dopt, &o, sizeof(janus_opt), cudaMemcpyHostToDevice, s));
     dhp = st->dopt;
   }
-  node::adam_tick_kernel<<<1, 1, 0, s>>>(st->dstep);
-  node::adam_kernel<<<blocks(st->n_params, 256), 256, 0, s>>>(st->n_params, st->params, st->m1, st->m2, st->grad, dhp,
+  janus::pdl(node::adam_tick_kernel, 1, 1, 0, s)(st->dstep);
+  janus::pdl(node::adam_kernel, blocks(st->n_params, 256), 256, 0, s)(st->n_params, st->params, st->m1, st->m2, st->grad, dhp,
                                                               st->dstep);
   JANUS_LAUNCH_CHECK("adam");
   refresh_transposes(st, s);
@@ -1439,21 +1440,21 @@ void launch_edge_kernel(janus_stage* st, int u, int which, int mb, int slot, int
     const int grid = step_grid ? pair_grid(st, g) : std::max(1, std::min((g.n_pairs + edge_tc::TE - 1) / edge_tc::TE, 148));
     const float* wt = mp.pack + edge_tc::kWtOff / sizeof(float);
     if (which == 4 && g.n_pairs > 0)
-      edge_tc::msg_bf_pair_tc<<<grid, edge_tc::NT, edge_tc::bf_pair_smem(), s>>>(eg, g.pgeo, g.n_pairs, mp, st->m.r_c, b.v, sc.s1,
+      janus::pdl(edge_tc::msg_bf_pair_tc, grid, edge_tc::NT, edge_tc::bf_pair_smem(), s)(eg, g.pgeo, g.n_pairs, mp, st->m.r_c, b.v, sc.s1,
                                                                                  b.ff_a, mo.Fbar, sc.partial);
     if (which == 5 && g.n_pairs > 0)
-      edge_tc::msg_be_pair_tc<<<grid, edge_tc::NT, edge_tc::be_pair_smem(), s>>>(eg, g.pgeo, g.n_pairs, mp, st->m.r_c, b.v, sc.s2,
+      janus::pdl(edge_tc::msg_be_pair_tc, grid, edge_tc::NT, edge_tc::be_pair_smem(), s)(eg, g.pgeo, g.n_pairs, mp, st->m.r_c, b.v, sc.s2,
                                                                                  sc.partial);
     if (which >= 4) return;
     if (which == 2) {
       if (g.n_pairs > 0)
-        edge_tc::msg_bf_pair_tc<<<grid, edge_tc::NT, edge_tc::bf_pair_smem(), s>>>(eg, g.pgeo, g.n_pairs, mp, st->m.r_c, b.v, sc.s1,
+        janus::pdl(edge_tc::msg_bf_pair_tc, grid, edge_tc::NT, edge_tc::bf_pair_smem(), s)(eg, g.pgeo, g.n_pairs, mp, st->m.r_c, b.v, sc.s1,
                                                                                    b.ff_a, mo.Fbar, sc.partial);
       JANUS_ROWS(msg_bf_rows, blocks(N, 8), s, N, g.row_ptr, g.col, g.pidx, g.u, mo.Fbar, b.wf, b.wfp, b.v, sc.s1, b.ff_a, wt,
                                                          sc.s3, sc.s4, nullptr, edge_tc::PartialReduce{});
     } else {
       if (g.n_pairs > 0)
-        edge_tc::msg_be_pair_tc<<<grid, edge_tc::NT, edge_tc::be_pair_smem(), s>>>(eg, g.pgeo, g.n_pairs, mp, st->m.r_c, b.v, sc.s2,
+        janus::pdl(edge_tc::msg_be_pair_tc, grid, edge_tc::NT, edge_tc::be_pair_smem(), s)(eg, g.pgeo, g.n_pairs, mp, st->m.r_c, b.v, sc.s2,
                                                                                    sc.partial);
       JANUS_ROWS(msg_be_rows, blocks(N, 8), s, N, g.row_ptr, g.col, g.pidx, b.wf, sc.s2, wt, sc.s3, nullptr, nullptr,
                  edge_tc::PartialReduce{});
@@ -1465,34 +1466,34 @@ void launch_edge_kernel(janus_stage* st, int u, int which, int mb, int slot, int
     const int fgrid = step_grid ? fe_grid(st, g) : g.n_tiles_tc;
     switch (which) {
       case 0:
-        edge_tc::msg_fe_tc<<<fgrid, edge_tc::NT, edge_tc::fe_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, sc.s3);
+        janus::pdl(edge_tc::msg_fe_tc, fgrid, edge_tc::NT, edge_tc::fe_smem(), s)(eg, g.tile_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, sc.s3);
         break;
       case 1:
-        edge_tc::msg_ff_tc<<<fgrid, edge_tc::NT, edge_tc::ff_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, b.ff_a, sc.s3, sc.s5, nullptr);
+        janus::pdl(edge_tc::msg_ff_tc, fgrid, edge_tc::NT, edge_tc::ff_smem(), s)(eg, g.tile_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, b.ff_a, sc.s3, sc.s5, nullptr);
         break;
       case 2:
-        edge_tc::msg_bf_tc<<<grid, edge_tc::NT, edge_tc::bf_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, sc.s1, b.ff_a,
+        janus::pdl(edge_tc::msg_bf_tc, grid, edge_tc::NT, edge_tc::bf_smem(), s)(eg, g.tile_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, sc.s1, b.ff_a,
                                                                         mo.Fbar, sc.s3, sc.s4, sc.partial, nullptr);
         break;
       default:
-        edge_tc::msg_be_tc<<<grid, edge_tc::NT, edge_tc::be_smem(), s>>>(eg, g.tile_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, sc.s2, sc.s3, sc.partial, nullptr, nullptr);
+        janus::pdl(edge_tc::msg_be_tc, grid, edge_tc::NT, edge_tc::be_smem(), s)(eg, g.tile_tc, g.n_tiles_tc, mp, st->m.r_c, b.v, sc.s2, sc.s3, sc.partial, nullptr, nullptr);
         break;
     }
     return;
   }
   switch (which) {
     case 0:
-      edge::msg_fe_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::fe_smem<kH, kR>(), s>>>(eg, mp, st->m.r_c, b.v, sc.s3);
+      janus::pdl(edge::msg_fe_kernel<kH, kR>, g.n_tiles, edge::NT, edge::fe_smem<kH, kR>(), s)(eg, mp, st->m.r_c, b.v, sc.s3);
       break;
     case 1:
-      edge::msg_ff_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::ff_smem<kH, kR>(), s>>>(eg, mp, st->m.r_c, b.v, b.ff_a, sc.s3, sc.s5);
+      janus::pdl(edge::msg_ff_kernel<kH, kR>, g.n_tiles, edge::NT, edge::ff_smem<kH, kR>(), s)(eg, mp, st->m.r_c, b.v, b.ff_a, sc.s3, sc.s5);
       break;
     case 2:
-      edge::msg_bf_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::bf_smem<kH, kR>(), s>>>(eg, mp, st->m.r_c, b.v, sc.s1, b.ff_a,
+      janus::pdl(edge::msg_bf_kernel<kH, kR>, g.n_tiles, edge::NT, edge::bf_smem<kH, kR>(), s)(eg, mp, st->m.r_c, b.v, sc.s1, b.ff_a,
                                                                                      mo.Fbar, sc.s3, sc.s4, sc.partial);
       break;
     default:
-      edge::msg_be_kernel<kH, kR><<<g.n_tiles, edge::NT, edge::be_smem<kH, kR>(), s>>>(eg, mp, st->m.r_c, b.v, sc.s2, sc.s3, sc.partial);
+      janus::pdl(edge::msg_be_kernel<kH, kR>, g.n_tiles, edge::NT, edge::be_smem<kH, kR>(), s)(eg, mp, st->m.r_c, b.v, sc.s2, sc.s3, sc.partial);
       break;
   }
 }

@@ -54,6 +54,7 @@ __device__ __forceinline__ void put_b(uint8_t* dst, int tile, int n, int k, floa
 
 // U, V: [64][64] row-major (upd parameters); pack: kUpdPackBytes
 __global__ void pack_upd_weights(const float* __restrict__ U, const float* __restrict__ V, float* __restrict__ pack) {
+  JANUS_GDC_WAIT();
   uint8_t* dst = reinterpret_cast<uint8_t*>(pack);
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= 64 * 64) return;
@@ -71,6 +72,7 @@ __global__ void pack_upd_weights(const float* __restrict__ U, const float* __res
 
 // the msg unit's W as the B operand of X.W (hi, lo) at kWkOff of its pack
 __global__ void pack_msg_w(const float* __restrict__ W, float* __restrict__ pack) {
+  JANUS_GDC_WAIT();
   uint8_t* dst = reinterpret_cast<uint8_t*>(pack) + kWkOff;
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= 64 * 64) return;
@@ -158,6 +160,7 @@ __global__ void __launch_bounds__(NT, 1) upd_fe_tc(int rows, const float* __rest
                                                    const float* __restrict__ upack, const float* __restrict__ ups,
                                                    float* __restrict__ p_out, float* __restrict__ h_out,
                                                    const float* __restrict__ wpack, float* __restrict__ v_out) {
+  JANUS_GDC_WAIT();
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = edge_tc::align1024(sm_raw);
   uint8_t* W = sm;                  // U, U_lo, V, V_lo, [Wn, Wn_lo]
@@ -225,6 +228,7 @@ __global__ void __launch_bounds__(NT, 1) upd_fe_tc(int rows, const float* __rest
 __global__ void __launch_bounds__(NT, 1) upd_ff_tc(int rows, const float* __restrict__ a, const float* __restrict__ p,
                                                    const float* __restrict__ upack, float* __restrict__ ff_a,
                                                    float* __restrict__ am) {
+  JANUS_GDC_WAIT();
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = edge_tc::align1024(sm_raw);
   uint8_t* W = sm;  // V^T, V^T_lo, U^T, U^T_lo
@@ -280,6 +284,7 @@ __global__ void __launch_bounds__(NT, 1) upd_bf_tc(int rows, const float* __rest
                                                    float* __restrict__ u, float* __restrict__ inj, const float* ah,
                                                    float* ah_out, const float* __restrict__ wpack,
                                                    float* __restrict__ vdot_out) {
+  JANUS_GDC_WAIT();
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = edge_tc::align1024(sm_raw);
   uint8_t* W = sm;  // U, V^T, U^T, V, [Wn]
@@ -369,6 +374,7 @@ __global__ void __launch_bounds__(NT, 1) upd_bf_tc(int rows, const float* __rest
 __global__ void __launch_bounds__(NT, 1) upd_be_tc(int rows, const float* __restrict__ bh, const float* __restrict__ p,
                                                    const float* __restrict__ upack, const float* __restrict__ inj,
                                                    float* __restrict__ pbar, float* __restrict__ bm) {
+  JANUS_GDC_WAIT();
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = edge_tc::align1024(sm_raw);
   uint8_t* W = sm;  // V^T, U^T
@@ -429,6 +435,7 @@ __global__ void __launch_bounds__(NT, 1) upd_be_tc(int rows, const float* __rest
 // runs stay bit-identical to unstaged ones.
 __global__ void __launch_bounds__(NT, 1) rows_w_tc(int rows, const float* __restrict__ X, const float* __restrict__ wpack,
                                                    int split3, float* __restrict__ out) {
+  JANUS_GDC_WAIT();
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = edge_tc::align1024(sm_raw);
   uint8_t* W = sm;  // W, W_lo

@@ -50,6 +50,7 @@ __device__ __forceinline__ void colsums(int rows, const node::WJob& jb, float (*
 }
 
 __global__ void __launch_bounds__(kWgT, 1) wgrad_tc_kernel(int rows, node::WJobs jobs) {
+  JANUS_GDC_WAIT();
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = align1024(sm_raw);
   uint8_t* TA = sm;          // a^T [64 features][128 atoms]

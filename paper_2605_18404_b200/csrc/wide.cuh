@@ -74,6 +74,7 @@ __device__ __forceinline__ PairRec pair_rec(const float4* __restrict__ pgeo, int
 // ---------------------------------------------------------------- pairs
 // phi2 = [phi; phi'] [2 P][R] (Gaussian basis of the pair length and its d/dd)
 __global__ void basis2_kernel(int P, int R, const float4* __restrict__ pgeo, float rc, float* __restrict__ phi2) {
+  JANUS_GDC_WAIT();
   const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (x >= static_cast<int64_t>(P) * R) return;
   const int p = static_cast<int>(x / R), k = static_cast<int>(x % R);
@@ -89,6 +90,7 @@ __global__ void basis2_kernel(int P, int R, const float4* __restrict__ pgeo, flo
 // FE / BF: z2 = [phi A; phi' A] -> a2 = [s; sdot] = [SiLU(z + alpha); SiLU'(z + alpha) z']
 __global__ void act2_kernel(int64_t PH, int H, const float* __restrict__ z2, const float* __restrict__ alpha,
                             float* __restrict__ a2) {
+  JANUS_GDC_WAIT();
   const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (x >= PH) return;
   const float z = z2[x] + __ldg(alpha + x % H), zp = z2[PH + x];
@@ -99,6 +101,7 @@ __global__ void act2_kernel(int64_t PH, int H, const float* __restrict__ z2, con
 // BE: a = SiLU(z + alpha) (first half only)
 __global__ void act1_kernel(int64_t PH, int H, const float* __restrict__ z, const float* __restrict__ alpha,
                             float* __restrict__ a) {
+  JANUS_GDC_WAIT();
   const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (x >= PH) return;
   a[x] = silu(z[x] + __ldg(alpha + x % H));
@@ -107,6 +110,7 @@ __global__ void act1_kernel(int64_t PH, int H, const float* __restrict__ z, cons
 // FE: g2 = [s B; sdot B] -> w = c (g + beta), w' = c' (g + beta) + c g'
 __global__ void filter_out_kernel(int64_t PH, int H, const float* __restrict__ g2, const float* __restrict__ beta,
                                   const float4* __restrict__ pgeo, float* __restrict__ wf, float* __restrict__ wfp) {
+  JANUS_GDC_WAIT();
   const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (x >= PH) return;
   const float4 r = __ldg(pgeo + 2 * (x / H));
@@ -122,6 +126,7 @@ __global__ void __launch_bounds__(256) bf_pair_kernel(int P, const float4* __res
                                                       const float* __restrict__ am, const float* __restrict__ v,
                                                       const float* __restrict__ vd, const float* __restrict__ Fbar,
                                                       float* __restrict__ mn) {
+  JANUS_GDC_WAIT();
   constexpr int H = 32 * V;
   const int p = static_cast<int>((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5), l = threadIdx.x & 31;
   if (p >= P) return;
@@ -154,6 +159,7 @@ __global__ void __launch_bounds__(256) bf_pair_kernel(int P, const float4* __res
 // zb2 = [zbar; zbar'] = [sbar SiLU'(z) + sdotbar SiLU''(z) z'; sdotbar SiLU'(z)]
 __global__ void bf_zbar_kernel(int64_t PH, int H, const float* __restrict__ sb2, const float* __restrict__ z2,
                                const float* __restrict__ alpha, float* __restrict__ zb2) {
+  JANUS_GDC_WAIT();
   const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (x >= PH) return;
   const float z = z2[x] + __ldg(alpha + x % H), zp = z2[PH + x];
@@ -167,6 +173,7 @@ template <int V>
 __global__ void __launch_bounds__(256) be_pair_kernel(int P, const float4* __restrict__ pgeo,
                                                       const float* __restrict__ bm, const float* __restrict__ v,
                                                       float* __restrict__ gbar) {
+  JANUS_GDC_WAIT();
   constexpr int H = 32 * V;
   const int p = static_cast<int>((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5), l = threadIdx.x & 31;
   if (p >= P) return;
@@ -185,6 +192,7 @@ __global__ void __launch_bounds__(256) be_pair_kernel(int P, const float4* __res
 // BE: zbar = sbar SiLU'(z + alpha)  (in place on sbar)
 __global__ void be_zbar_kernel(int64_t PH, int H, float* __restrict__ sb, const float* __restrict__ z,
                                const float* __restrict__ alpha) {
+  JANUS_GDC_WAIT();
   const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (x >= PH) return;
   sb[x] *= dsilu(z[x] + __ldg(alpha + x % H));
@@ -233,6 +241,7 @@ template <int V>
 __global__ void __launch_bounds__(256) fe_rows_kernel(int N, const int* __restrict__ row_ptr, const int* __restrict__ col,
                                                       const int* __restrict__ pidx, const float* __restrict__ wf,
                                                       const float* __restrict__ v, float* __restrict__ m) {
+  JANUS_GDC_WAIT();
   constexpr int H = 32 * V;
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31, q = w % kWpr;
   const int i = blockIdx.x * (8 / kWpr) + w / kWpr;
@@ -258,6 +267,7 @@ __global__ void __launch_bounds__(256) ff_rows_kernel(int N, const int* __restri
                                                       const float* __restrict__ wf, const float* __restrict__ wfp,
                                                       const float* __restrict__ v, const float* __restrict__ am,
                                                       float* __restrict__ Y, float* __restrict__ F) {
+  JANUS_GDC_WAIT();
   constexpr int H = 32 * V;
   __shared__ float fpart[8][3];
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31, q = w % kWpr;
@@ -311,6 +321,7 @@ __global__ void __launch_bounds__(256) bf_rows_kernel(int N, const int* __restri
                                                       const float* __restrict__ wfp, const float* __restrict__ v,
                                                       const float* __restrict__ vd, const float* __restrict__ am,
                                                       float* __restrict__ mdot, float* __restrict__ X) {
+  JANUS_GDC_WAIT();
   constexpr int H = 32 * V;
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31, q = w % kWpr;
   const int i = blockIdx.x * (8 / kWpr) + w / kWpr;
@@ -346,6 +357,7 @@ __global__ void __launch_bounds__(256) bf_rows_kernel(int N, const int* __restri
 // ------------------------------------------------------------- node kernels
 __global__ void embed_kernel(int64_t NH, int H, const int* __restrict__ species, const float* __restrict__ Emb,
                              float* __restrict__ h) {
+  JANUS_GDC_WAIT();
   const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (x < NH) h[x] = __ldg(Emb + static_cast<int64_t>(__ldg(species + x / H)) * H + x % H);
 }
@@ -353,6 +365,7 @@ __global__ void embed_kernel(int64_t NH, int H, const int* __restrict__ species,
 // p += bias (per column); sp = SiLU(p)
 __global__ void bias_silu_kernel(int64_t NH, int H, float* __restrict__ p, const float* __restrict__ bias,
                                  float* __restrict__ sp) {
+  JANUS_GDC_WAIT();
   const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (x >= NH) return;
   const float y = p[x] + __ldg(bias + x % H);
@@ -362,6 +375,7 @@ __global__ void bias_silu_kernel(int64_t NH, int H, float* __restrict__ p, const
 
 // x *= SiLU'(p)
 __global__ void mul_dsilu_kernel(int64_t NH, float* __restrict__ x, const float* __restrict__ p) {
+  JANUS_GDC_WAIT();
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < NH) x[i] *= dsilu(p[i]);
 }
@@ -370,6 +384,7 @@ __global__ void mul_dsilu_kernel(int64_t NH, float* __restrict__ x, const float*
 __global__ void bf_upd_ew_kernel(int64_t NH, const float* __restrict__ r, const float* __restrict__ pdot,
                                  const float* __restrict__ p, float* __restrict__ pb, float* __restrict__ pdb,
                                  float* __restrict__ spd) {
+  JANUS_GDC_WAIT();
   const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (x >= NH) return;
   const float pp = p[x], pd = pdot[x], rr = r[x], ds = dsilu(pp);
@@ -381,6 +396,7 @@ __global__ void bf_upd_ew_kernel(int64_t NH, const float* __restrict__ r, const 
 // BE upd: pb = r SiLU'(p), sp = SiLU(p)
 __global__ void be_upd_ew_kernel(int64_t NH, const float* __restrict__ r, const float* __restrict__ p,
                                  float* __restrict__ pb, float* __restrict__ sp) {
+  JANUS_GDC_WAIT();
   const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (x >= NH) return;
   const float pp = p[x];
@@ -392,6 +408,7 @@ __global__ void be_upd_ew_kernel(int64_t NH, const float* __restrict__ r, const 
 __global__ void ro_fe_kernel(int N, int H, float* __restrict__ t, const float* __restrict__ o,
                              const float* __restrict__ om, const float* __restrict__ bias,
                              const int* __restrict__ species, float* __restrict__ e_atom) {
+  JANUS_GDC_WAIT();
   const int i = static_cast<int>((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5), l = threadIdx.x & 31;
   if (i >= N) return;
   float acc = 0.f;
@@ -407,6 +424,7 @@ __global__ void ro_fe_kernel(int N, int H, float* __restrict__ t, const float* _
 // readout FF: out = SiLU'(t) omega
 __global__ void ro_ff_ew_kernel(int64_t NH, int H, const float* __restrict__ t, const float* __restrict__ om,
                                 float* __restrict__ out) {
+  JANUS_GDC_WAIT();
   const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (x < NH) out[x] = dsilu(t[x]) * __ldg(om + x % H);
 }
@@ -415,6 +433,7 @@ __global__ void ro_ff_ew_kernel(int64_t NH, int H, const float* __restrict__ t, 
 __global__ void ro_bf_ew_kernel(int64_t NH, int H, const float* __restrict__ tdot, const float* __restrict__ t,
                                 const float* __restrict__ om, float* __restrict__ x1, float* __restrict__ tau,
                                 float* __restrict__ y) {
+  JANUS_GDC_WAIT();
   const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (x >= NH) return;
   const float tt = t[x], td = tdot[x], w = __ldg(om + x % H), ds = dsilu(tt);
@@ -427,6 +446,7 @@ __global__ void ro_bf_ew_kernel(int64_t NH, int H, const float* __restrict__ tdo
 __global__ void ro_be_ew_kernel(int64_t NH, int H, const float* __restrict__ t, const float* __restrict__ om,
                                 const float* __restrict__ eps, const int* __restrict__ struct_id,
                                 float* __restrict__ tb, float* __restrict__ x2) {
+  JANUS_GDC_WAIT();
   const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (x >= NH) return;
   const float ep = __ldg(eps + __ldg(struct_id + x / H)), tt = t[x];
@@ -441,6 +461,7 @@ __global__ void ro_be_ew_kernel(int64_t NH, int H, const float* __restrict__ t, 
 __global__ void __launch_bounds__(256) species_sum_kernel(int N, int S, int cols, const int* __restrict__ species,
                                                           const float* __restrict__ x, const float* __restrict__ eps,
                                                           const int* __restrict__ struct_id, float* __restrict__ out) {
+  JANUS_GDC_WAIT();
   __shared__ float part[8][33];
   const int z = blockIdx.y, l = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int k = blockIdx.x * 32 + l;
@@ -475,6 +496,7 @@ constexpr int kColRows = 256;
 __global__ void __launch_bounds__(256) colsum_kernel(int rows, int cols, const float* __restrict__ X,
                                                      float* __restrict__ part, unsigned* __restrict__ ticket,
                                                      float* __restrict__ out) {
+  JANUS_GDC_WAIT();
   __shared__ float red[8][33];
   __shared__ bool last;
   const int l = threadIdx.x & 31, w = threadIdx.x >> 5, k = blockIdx.x * 32 + l, g = blockIdx.y;
@@ -514,6 +536,7 @@ __global__ void __launch_bounds__(256) colsum_kernel(int rows, int cols, const f
 
 // C[x] += sum_b W[b][x] over the K slices of gemm_tn_long, in slice order
 __global__ void sum_slices_kernel(int64_t n, int slices, const float* __restrict__ W, float* __restrict__ C) {
+  JANUS_GDC_WAIT();
   const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (x >= n) return;
   float acc = 0.f;
@@ -523,6 +546,7 @@ __global__ void sum_slices_kernel(int64_t n, int slices, const float* __restrict
 
 // dst[c][r] = src[r][c] for a [rows x cols] matrix (weight transposes, once per optimizer step)
 __global__ void transpose_any_kernel(int rows, int cols, const float* __restrict__ src, float* __restrict__ dst) {
+  JANUS_GDC_WAIT();
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= rows * cols) return;
   const int r = x / cols, c = x % cols;
@@ -530,6 +554,7 @@ __global__ void transpose_any_kernel(int rows, int cols, const float* __restrict
 }
 
 __global__ void fill_kernel(int64_t n, float* __restrict__ p, float v) {
+  JANUS_GDC_WAIT();
   const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (x < n) p[x] = v;
 }
