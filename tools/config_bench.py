@@ -57,14 +57,25 @@ def measure(name, model, params, batches, lanes=None, steps=10, warmup=3):
 
 def main():
     only = sys.argv[sys.argv.index("--only") + 1] if "--only" in sys.argv else None
-    model = J.Model(L=4, H=64, R=64, r_c=5.0, precision=J.PREC_TF32)
+    # --fp32: the generic-width fp32 path (bench.py's fp32_parity_path); --steps / --warmup: shorter runs (ncu)
+    kw = {}
+    if "--steps" in sys.argv:
+        kw["steps"] = int(sys.argv[sys.argv.index("--steps") + 1])
+    if "--warmup" in sys.argv:
+        kw["warmup"] = int(sys.argv[sys.argv.index("--warmup") + 1])
+    if "--fp32" in sys.argv:
+        model = J.Model(L=4, H=64, R=64, r_c=5.0, precision=J.PREC_FP32, generic=True)
+    elif "--generic" in sys.argv:  # the generic-width path in tf32 (configs[2]'s path) on these configs
+        model = J.Model(L=4, H=64, R=64, r_c=5.0, precision=J.PREC_TF32, generic=True)
+    else:
+        model = J.Model(L=4, H=64, R=64, r_c=5.0, precision=J.PREC_TF32)
     params = model.synth_params(7)
     if only in (None, "C1"):
         measure("C1: 64-atom cells, N_mb=4", model, params,
-                [J.synth_batch(model, [64], 0.095, 10 + i, device_nl=True) for i in range(4)])
+                [J.synth_batch(model, [64], 0.095, 10 + i, device_nl=True) for i in range(4)], **kw)
     if only in (None, "C2"):
         measure("C2: 256-atom cells, N_mb=32", model, params,
-                [J.synth_batch(model, [256], 0.095, 700 + i, device_nl=True) for i in range(32)])
+                [J.synth_batch(model, [256], 0.095, 700 + i, device_nl=True) for i in range(32)], **kw)
     if only is not None:
         return
     rng = np.random.default_rng(11)
