@@ -39,6 +39,7 @@
 
 #include "../../include/janus/errors.hpp"
 #include "../../include/janus_cuda.h"
+#include "common.cuh"
 #include "cuda_check.hpp"
 #include "nbrlist.hpp"
 
@@ -73,6 +74,7 @@ __device__ __forceinline__ unsigned long long make_key(int j, int sx, int sy, in
 __global__ void bin_kernel(int n, const double* __restrict__ pos, const int* __restrict__ struct_id,
                            const StructMeta* __restrict__ meta, int* __restrict__ cell_of, int4* __restrict__ cw,
                            int* __restrict__ cell_count) {
+  JANUS_GDC_WAIT();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const StructMeta sm = meta[struct_id[i]];
@@ -94,6 +96,7 @@ __global__ void bin_kernel(int n, const double* __restrict__ pos, const int* __r
 
 // exclusive scan of n ints into out[0..n] (out[n] = total), one CTA of 1024
 __global__ void scan_kernel(int n, const int* __restrict__ in, int* __restrict__ out) {
+  JANUS_GDC_WAIT();
   __shared__ int warp_tot[32];
   __shared__ int carry;
   if (threadIdx.x == 0) carry = 0;
@@ -134,6 +137,7 @@ __global__ void scatter_kernel(int n, const double* __restrict__ pos, const int*
                                const int4* __restrict__ cw, const int* __restrict__ cell_start,
                                int* __restrict__ cursor, int* __restrict__ c_atom, double* __restrict__ c_pos,
                                int4* __restrict__ c_w) {
+  JANUS_GDC_WAIT();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int cid = cell_of[i];
@@ -252,6 +256,7 @@ __device__ __forceinline__ void emit_sorted(const unsigned long long* buf, int d
 // above kPadCap are only counted here and re-walked by compact_kernel.
 __global__ void __launch_bounds__(kWarps * 32) walk_pad_kernel(int n, NBR_WALK_PARAMS, int* __restrict__ deg,
                                                                unsigned long long* __restrict__ pad) {
+  JANUS_GDC_WAIT();
   __shared__ unsigned long long sk[kWarps][kPadCap];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int i = blockIdx.x * kWarps + w;
@@ -280,6 +285,7 @@ __global__ void __launch_bounds__(kWarps * 32) compact_kernel(int n, NBR_WALK_PA
                                                               unsigned long long* __restrict__ tmp,
                                                               unsigned long long* __restrict__ skey,
                                                               int* __restrict__ col, int* __restrict__ shift) {
+  JANUS_GDC_WAIT();
   __shared__ unsigned long long sk[kWarps][kSortCap];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int i = blockIdx.x * kWarps + w;
@@ -311,6 +317,7 @@ __global__ void __launch_bounds__(kWarps * 32) compact_kernel(int n, NBR_WALK_PA
 __global__ void __launch_bounds__(kWarps * 32) rev_kernel(int n, const int* __restrict__ row_ptr, int max_edges,
                                                           const unsigned long long* __restrict__ skey,
                                                           int* __restrict__ rev, int* __restrict__ err) {
+  JANUS_GDC_WAIT();
   const int lane = threadIdx.x & 31;
   const int i = blockIdx.x * kWarps + (threadIdx.x >> 5);
   if (i >= n || row_ptr[n] > max_edges) return;
@@ -340,6 +347,7 @@ __global__ void __launch_bounds__(kWarps * 32) rev_kernel(int n, const int* __re
 __global__ void slice_kernel(int E, int atom0, int edge0, const int* __restrict__ col, const int* __restrict__ rev,
                              const int* __restrict__ shift, int* __restrict__ col_o, int* __restrict__ rev_o,
                              int* __restrict__ shift_o) {
+  JANUS_GDC_WAIT();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= E) return;
   col_o[e] = col[edge0 + e] - atom0;
@@ -461,17 +469,17 @@ void nbrlist_enqueue(janus_nbrlist* nl, int n, int n_struct, const double* pos, 
   JANUS_CUDA(cudaMemsetAsync(nl->cursor, 0, sizeof(int) * cells, s));
   JANUS_CUDA(cudaMemsetAsync(nl->err, 0, sizeof(int), s));
   const double rc2 = rc * rc;
-  nbr::bin_kernel<<<nblk(n, 256), 256, 0, s>>>(n, pos, struct_id, nl->meta, nl->cell_of, nl->cw, nl->cell_count);
-  nbr::scan_kernel<<<1, 1024, 0, s>>>(cells, nl->cell_count, nl->cell_start);
-  nbr::scatter_kernel<<<nblk(n, 256), 256, 0, s>>>(n, pos, nl->cell_of, nl->cw, nl->cell_start, nl->cursor,
+  janus::pdl(nbr::bin_kernel, nblk(n, 256), 256, 0, s)(n, pos, struct_id, nl->meta, nl->cell_of, nl->cw, nl->cell_count);
+  janus::pdl(nbr::scan_kernel, 1, 1024, 0, s)(cells, nl->cell_count, nl->cell_start);
+  janus::pdl(nbr::scatter_kernel, nblk(n, 256), 256, 0, s)(n, pos, nl->cell_of, nl->cw, nl->cell_start, nl->cursor,
                                                     nl->c_atom, nl->c_pos, nl->c_w);
   const int rb = nblk(n, nbr::kWarps), rt = nbr::kWarps * 32;
 #define NBR_ARGS pos, struct_id, nl->meta, nl->cell_of, nl->cw, nl->cell_start, nl->c_atom, nl->c_pos, nl->c_w, rc2
-  nbr::walk_pad_kernel<<<rb, rt, 0, s>>>(n, NBR_ARGS, nl->deg, nl->pad);
-  nbr::scan_kernel<<<1, 1024, 0, s>>>(n, nl->deg, row_ptr);
-  nbr::compact_kernel<<<rb, rt, 0, s>>>(n, NBR_ARGS, row_ptr, nl->max_edges, nl->pad, nl->tmp, nl->skey, col, shift);
+  janus::pdl(nbr::walk_pad_kernel, rb, rt, 0, s)(n, NBR_ARGS, nl->deg, nl->pad);
+  janus::pdl(nbr::scan_kernel, 1, 1024, 0, s)(n, nl->deg, row_ptr);
+  janus::pdl(nbr::compact_kernel, rb, rt, 0, s)(n, NBR_ARGS, row_ptr, nl->max_edges, nl->pad, nl->tmp, nl->skey, col, shift);
 #undef NBR_ARGS
-  nbr::rev_kernel<<<rb, rt, 0, s>>>(n, row_ptr, nl->max_edges, nl->skey, rev, nl->err);
+  janus::pdl(nbr::rev_kernel, rb, rt, 0, s)(n, row_ptr, nl->max_edges, nl->skey, rev, nl->err);
   JANUS_LAUNCH_CHECK("nbrlist");
   JANUS_CUDA(cudaMemcpyAsync(nl->h_small, row_ptr + n, sizeof(int), cudaMemcpyDeviceToHost, s));
   JANUS_CUDA(cudaMemcpyAsync(nl->h_small + 1, nl->err, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -589,7 +597,7 @@ int LmBuilder::build(const janus_host_batch* hbs, int nb, double rc, int b, cuda
 
 void csr_slice_copy(const DevCsr& src, int atom0, int edge0, int E, int* col, int* rev, int* shift, cudaStream_t s) {
   if (E <= 0) return;
-  nbr::slice_kernel<<<nblk(E, 256), 256, 0, s>>>(E, atom0, edge0, src.col, src.rev, src.shift, col, rev, shift);
+  janus::pdl(nbr::slice_kernel, nblk(E, 256), 256, 0, s)(E, atom0, edge0, src.col, src.rev, src.shift, col, rev, shift);
   JANUS_LAUNCH_CHECK("csr slice");
 }
 
