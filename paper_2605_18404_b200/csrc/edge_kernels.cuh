@@ -678,9 +678,9 @@ __global__ void __launch_bounds__(256) reduce_partials_seq_kernel(const float* _
 // out = sum over the n partials, fixed order for a given n
 inline void reduce_partials(const float* partial, int n, int PE, float* out, cudaStream_t s) {
   if (n <= kSeqPartials)
-    reduce_partials_seq_kernel<<<(PE + 255) / 256, 256, 0, s>>>(partial, n, PE, out);
+    janus::pdl(reduce_partials_seq_kernel, (PE + 255) / 256, 256, 0, s)(partial, n, PE, out);
   else
-    reduce_partials_kernel<<<reduce_grid(PE), 256, 0, s>>>(partial, n, PE, out);
+    janus::pdl(reduce_partials_kernel, reduce_grid(PE), 256, 0, s)(partial, n, PE, out);
 }
 
 template <int H, int R>

@@ -260,6 +260,7 @@ template <class Epi>
 __global__ void __launch_bounds__(kThreads, 1) gemm_nt_kernel(const __grid_constant__ CUtensorMap tmA,
                                                                       const __grid_constant__ CUtensorMap tmW, Problem pb,
                                                                       Epi epi) {
+  JANUS_GDC_WAIT();
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = sm_raw + ((1024u - (tc::smem_u32(sm_raw) & 1023u)) & 1023u);
   const uint32_t slabA = 128 * 128, slabW = static_cast<uint32_t>(pb.N) * 128, sbytes = slabA + slabW;

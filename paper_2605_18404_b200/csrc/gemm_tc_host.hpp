@@ -54,7 +54,7 @@ void launch(const CUtensorMap& tmA, const CUtensorMap& tmW, const Problem& pb, c
                                     static_cast<int>(smem_bytes(256))));
     attr = true;
   }
-  gemm_nt_kernel<Epi><<<tiles, kThreads, smem_bytes(pb.N), s>>>(tmA, tmW, pb, epi);
+  janus::pdl(gemm_nt_kernel<Epi>, tiles, kThreads, smem_bytes(pb.N), s)(tmA, tmW, pb, epi);
   JANUS_LAUNCH_CHECK("gemm_tc");
 }
 

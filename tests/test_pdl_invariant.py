@@ -14,8 +14,8 @@ import re
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CSRC = os.path.join(ROOT, "paper_2605_18404_b200", "csrc")
 KERNEL_FILES = ["edge_kernels.cuh", "edge_tc.cuh", "pair_tc.cuh", "upd_tc.cuh", "wgrad_tc.cuh", "node_kernels.cuh",
-                "wide.cuh", "stage.cu", "nbrlist.cu"]
-LAUNCH_FILES = ["stage.cu", "stage_wide.inc", "nbrlist.cu"]
+                "wide.cuh", "stage.cu", "nbrlist.cu", "gemm_tc.cuh"]
+LAUNCH_FILES = ["stage.cu", "stage_wide.inc", "nbrlist.cu", "gemm_tc_host.hpp", "edge_kernels.cuh"]
 
 
 def kernels(text):
