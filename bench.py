@@ -54,9 +54,9 @@ METRIC = "structures/sec"
 
 def load_traffic(precision):
     """DRAM bytes per launch of the roofline kernel from the committed ncu --set full
-    capture (profiles/r01_roofline_traffic.json); None when absent or for another kernel."""
+    capture (profiles/r02_roofline_traffic.json); None when absent or for another kernel."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_roofline_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r02_roofline_traffic.json")) as f:
             t = json.load(f)
         return t["dram_bytes_per_launch"] if precision == "tf32" and t.get("kernel", "").endswith("msg_bf_pair_tc") else None
     except (OSError, ValueError, KeyError):
