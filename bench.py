@@ -457,7 +457,8 @@ def main():
         t32.close()
         ms32 = sum(ts32) / len(ts32)
         fp32_path = {"value": n_mb / (ms32 * 1e-3), "unit": "structures/s", "ms_per_step": ms32, "steps": len(ts32),
-                     "dtype": "fp32 for every contraction (generic-width path: fp32 GEMMs, compute type 32F)",
+                     "dtype": ("fp32-accurate: per-pair products 3xTF32 on tcgen05 (gemm_tc split3), weight-gradient "
+                               "and node GEMMs fp32 SIMT (cuBLAS compute type 32F); generic-width path"),
                      "tolerance": "E rel 1e-5, F and gradients 1e-4 of max (tests/test_gpu_bench_parity.py)"}
 
     cpu = None

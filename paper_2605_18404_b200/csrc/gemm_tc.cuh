@@ -33,11 +33,18 @@ namespace gemm_tc {
 constexpr int kKB = 32;  // floats per K block (one 128 B SW128 slab)
 
 struct Problem {
-  int rows;      // plain mode: rows of A / D; pair mode: pairs P (A, D have 2P rows)
-  int K;         // multiple of 32
-  int N;         // 64, 128 or 256 (one N tile)
-  int pair;      // 1: pair-mode tiles (64 pairs = 128 rows)
+  int rows;        // plain mode: rows of A / D; pair mode: pairs P (A, D have 2P rows)
+  int K;           // multiple of 32
+  int N;           // 64, 128 or 256 (one N tile)
+  int pair;        // 1: pair-mode tiles (64 pairs = 128 rows)
+  int split3 = 0;  // 1: 3xTF32 (fp32-accurate): x = hi + lo split in shared memory, D = lo.Whi + hi.Wlo + hi.Whi
 };
+
+__device__ __forceinline__ float tf32_hi(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
 
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint64_t* mbar) {
   asm volatile(
@@ -102,6 +109,8 @@ __device__ __forceinline__ void wload(const float* src, float (&v)[32], float4* 
 // halves of a warp take different formulas).  Per-column bias vectors are
 // read as 8 warp-uniform float4s per chunk.
 __device__ __forceinline__ float sig_fast(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
+// the 3xTF32 (fp32-tolerance) launches use the accurate sigmoid
+__device__ __forceinline__ float sig_sel(float x, int exact) { return exact ? 1.0f / (1.0f + expf(-x)) : sig_fast(x); }
 __device__ __forceinline__ void load_cols(const float* v, int c0, float (&o)[32]) {
   const float4* v4 = reinterpret_cast<const float4*>(v + c0);
 #pragma unroll
@@ -133,6 +142,7 @@ struct EpiAct2 {
   float* z2;  // optional raw copy (BF needs z, z' again for zbar)
   const float* alpha;
   int ld;
+  int exact = 0;
   __device__ void operator()(int p, int half, int P, bool ok, int c0, const float (&own)[32], const float (&oth)[32],
                              float4* stg) const {
     const size_t off = static_cast<size_t>(half ? P + p : p) * ld + c0;
@@ -141,7 +151,7 @@ struct EpiAct2 {
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       const float zz = (half ? oth[j] : own[j]) + o[j];
-      const float sg = sig_fast(zz), zs = zz * sg;
+      const float sg = sig_sel(zz, exact), zs = zz * sg;
       o[j] = half ? (sg + zs * (1.0f - sg)) * own[j] : zs;  // SiLU'(z) z' : SiLU(z)
     }
     wstore(ok ? a2 + off : nullptr, o, stg);
@@ -174,6 +184,7 @@ struct EpiZbar {
   const float* z2;
   const float* alpha;
   int ld;
+  int exact = 0;
   __device__ void operator()(int p, int half, int P, bool ok, int c0, const float (&own)[32], const float (&oth)[32],
                              float4* stg) const {
     const size_t off = static_cast<size_t>(half ? P + p : p) * ld + c0;
@@ -185,7 +196,7 @@ struct EpiZbar {
     for (int j = 0; j < 32; ++j) {
       const float zx = __shfl_xor_sync(0xffffffffu, zo[j], 16);
       const float zz = (half ? zx : zo[j]) + o[j];
-      const float sg = sig_fast(zz), u = 1.0f - sg;
+      const float sg = sig_sel(zz, exact), u = 1.0f - sg;
       const float ds = sg * (1.0f + zz * u);                                          // SiLU'
       const float d2 = half ? 0.0f : sg * u * (2.0f + zz * (1.0f - 2.0f * sg)) * zx;  // SiLU'' z' (value rows)
       o[j] = own[j] * ds + oth[j] * d2;
@@ -200,6 +211,7 @@ struct EpiAct1 {
   float* zraw;
   const float* alpha;
   int ld;
+  int exact = 0;
   __device__ void operator()(int r, int, int, bool ok, int c0, const float (&own)[32], const float (&)[32],
                              float4* stg) const {
     const size_t off = static_cast<size_t>(r) * ld + c0;
@@ -208,7 +220,7 @@ struct EpiAct1 {
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       const float zz = own[j] + o[j];
-      o[j] = zz * sig_fast(zz);
+      o[j] = zz * sig_sel(zz, exact);
     }
     wstore(ok ? a + off : nullptr, o, stg);
     if (zraw) wstore(ok ? zraw + off : nullptr, own, stg);
@@ -221,6 +233,7 @@ struct EpiBeZbar {
   const float* z;
   const float* alpha;
   int ld;
+  int exact = 0;
   __device__ void operator()(int r, int, int, bool ok, int c0, const float (&own)[32], const float (&)[32],
                              float4* stg) const {
     const size_t off = static_cast<size_t>(r) * ld + c0;
@@ -230,7 +243,7 @@ struct EpiBeZbar {
     load_cols(alpha, c0, o);
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
-      const float zz = zr[j] + o[j], sg = sig_fast(zz);
+      const float zz = zr[j] + o[j], sg = sig_sel(zz, exact);
       o[j] = own[j] * sg * (1.0f + zz * (1.0f - sg));
     }
     wstore(ok ? zb + off : nullptr, o, stg);
@@ -254,7 +267,10 @@ struct EpiBeZbar {
 // column half w / 4.
 constexpr int kThreads = 256;
 constexpr int kStages = 2;
-constexpr size_t smem_bytes(int N) { return static_cast<size_t>(kStages) * (128 * 128 + N * 128) + 1024; }
+// per stage: A slab (128 rows x 128 B) + W slab (N x 128 B); 3xTF32 adds their lo parts
+constexpr size_t smem_bytes(int N, int split3 = 0) {
+  return static_cast<size_t>(kStages) * (128 * 128 + N * 128) * (split3 ? 2 : 1) + 1024;
+}
 
 template <class Epi>
 __global__ void __launch_bounds__(kThreads, 1) gemm_nt_kernel(const __grid_constant__ CUtensorMap tmA,
@@ -264,7 +280,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_nt_kernel(const __grid_const
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = sm_raw + ((1024u - (tc::smem_u32(sm_raw) & 1023u)) & 1023u);
   const uint32_t slabA = 128 * 128, slabW = static_cast<uint32_t>(pb.N) * 128, sbytes = slabA + slabW;
-  __shared__ __align__(8) uint64_t full[kStages], empty[kStages], accum;
+  const uint32_t lo_off = kStages * sbytes;  // 3xTF32: the lo parts of stage s at lo_off + s * sbytes
+  __shared__ __align__(8) uint64_t full[kStages], empty[kStages], split[kStages], accum;
   __shared__ uint32_t tslot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int KB = pb.K / kKB;
@@ -272,6 +289,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_nt_kernel(const __grid_const
     for (int s = 0; s < kStages; ++s) {
       tc::mbar_init(&full[s], 1);
       tc::mbar_init(&empty[s], 1);
+      tc::mbar_init(&split[s], 6);  // 3xTF32: one arrive per split warp (warps 2..7)
     }
     tc::mbar_init(&accum, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -303,17 +321,48 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_nt_kernel(const __grid_const
     const uint32_t idesc = tc::idesc_tf32(128, pb.N, false, false);
     for (int kb = 0; kb < KB; ++kb) {
       const int s = kb % kStages;
-      tc::mbar_wait(&full[s], (kb / kStages) & 1);
+      tc::mbar_wait(pb.split3 ? &split[s] : &full[s], (kb / kStages) & 1);
       tc::fence_after();
       const uint32_t a = tc::smem_u32(sm + s * sbytes);
       const uint64_t da = tc::smem_desc(a, 16, 1024, 2), dw = tc::smem_desc(a + slabA, 16, 1024, 2);
+      if (pb.split3) {  // lo.Whi + hi.Wlo + hi.Whi (small terms first)
+        const uint64_t dal = tc::smem_desc(a + lo_off, 16, 1024, 2), dwl = tc::smem_desc(a + lo_off + slabA, 16, 1024, 2);
 #pragma unroll
-      for (int k = 0; k < kKB / 8; ++k)
-        tc::mma_tf32(tmem, da + static_cast<uint64_t>((32 * k) >> 4), dw + static_cast<uint64_t>((32 * k) >> 4), idesc,
-                     (kb > 0 || k > 0) ? 1u : 0u);
+        for (int k = 0; k < kKB / 8; ++k) {
+          const uint64_t o = static_cast<uint64_t>((32 * k) >> 4);
+          tc::mma_tf32(tmem, dal + o, dw + o, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+          tc::mma_tf32(tmem, da + o, dwl + o, idesc, 1u);
+          tc::mma_tf32(tmem, da + o, dw + o, idesc, 1u);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < kKB / 8; ++k)
+          tc::mma_tf32(tmem, da + static_cast<uint64_t>((32 * k) >> 4), dw + static_cast<uint64_t>((32 * k) >> 4), idesc,
+                       (kb > 0 || k > 0) ? 1u : 0u);
+      }
       tc::commit(&empty[s]);
     }
     tc::commit(&accum);
+  } else if (warp >= 2 && pb.split3) {
+    // 3xTF32 split of each landed stage: hi = rna_tf32(x) in place, lo = x - hi into the lo slabs
+    // (elementwise, so the SW128 layout carries over); then visible to the tensor core
+    const int st = static_cast<int>(threadIdx.x) - 64;  // 0..191
+    for (int kb = 0; kb < KB; ++kb) {
+      const int s = kb % kStages;
+      tc::mbar_wait(&full[s], (kb / kStages) & 1);
+      float4* hi = reinterpret_cast<float4*>(sm + s * sbytes);
+      float4* lo = reinterpret_cast<float4*>(sm + lo_off + s * sbytes);
+      const int n4 = static_cast<int>(sbytes / 16);
+      for (int x = st; x < n4; x += 192) {
+        const float4 v = hi[x];
+        const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+        hi[x] = h;
+        lo[x] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+      }
+      tc::fence_async_smem();
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tc::smem_u32(&split[s])) : "memory");
+    }
   }
   __syncwarp();
   tc::mbar_wait(&accum, 0);

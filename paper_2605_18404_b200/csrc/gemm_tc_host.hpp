@@ -51,10 +51,10 @@ void launch(const CUtensorMap& tmA, const CUtensorMap& tmW, const Problem& pb, c
   static bool attr = false;
   if (!attr) {
     JANUS_CUDA(cudaFuncSetAttribute(gemm_nt_kernel<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(smem_bytes(256))));
+                                    static_cast<int>(smem_bytes(256, 1))));
     attr = true;
   }
-  janus::pdl(gemm_nt_kernel<Epi>, tiles, kThreads, smem_bytes(pb.N), s)(tmA, tmW, pb, epi);
+  janus::pdl(gemm_nt_kernel<Epi>, tiles, kThreads, smem_bytes(pb.N, pb.split3), s)(tmA, tmW, pb, epi);
   JANUS_LAUNCH_CHECK("gemm_tc");
 }
 

@@ -378,7 +378,11 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
     st->desc = d;
     st->m = m;
     st->wide = wide;
-    st->wide_tc = wide && m.precision == JANUS_PREC_TF32;
+#ifndef JANUS_WIDE_SPLIT3
+#define JANUS_WIDE_SPLIT3 1  // plain fp32 generic path: per-pair GEMMs as 3xTF32 on gemm_tc (0: cuBLAS fp32 SIMT)
+#endif
+    st->wide_split3 = (JANUS_WIDE_SPLIT3 && wide && m.precision == JANUS_PREC_FP32) ? 1 : 0;
+    st->wide_tc = wide && (m.precision == JANUS_PREC_TF32 || st->wide_split3);
     st->u0 = d.unit_begin;
     st->u1 = d.unit_end;
     st->U = U;
@@ -412,7 +416,7 @@ janus_stage* stage_create(const janus_stage_desc& d, const float* unit_params) {
                        : k == kUpd  ? 2 * kH * kH + upd_tc::kUpdPackBytes / sizeof(float)
                                     : static_cast<size_t>(kH) * kH;
       if (wide) {  // tf32: msg units keep [A^T (H x R) | B^T (H x H)] for the TMA-fed GEMMs
-        const bool tcw = k == kMsg && m.precision == JANUS_PREC_TF32;
+        const bool tcw = k == kMsg && st->wide_tc;  // (tf32, or the 3xTF32 fp32 path)
         st->tw.push_back(tcw ? dalloc<float>(st, static_cast<size_t>(m.H) * (m.R + m.H), true) : nullptr);
         continue;
       }

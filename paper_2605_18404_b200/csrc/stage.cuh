@@ -159,7 +159,8 @@ struct janus_stage {
   int pair_chunks_cap = 0;
   janus::LmBuilder* lm = nullptr;  // device neighbour-list builder (lazy, janus_stage_load without a CSR)
   bool wide = false;               // generic-width phases (stage_wide.inc) instead of the fused H=64 kernels
-  bool wide_tc = false;            // wide + tf32: per-pair GEMMs on gemm_tc.cuh with fused epilogues
+  bool wide_tc = false;            // wide + tf32 (or fp32, 3xTF32): per-pair GEMMs on gemm_tc.cuh with fused epilogues
+  int wide_split3 = 0;             // wide + plain fp32: those GEMMs in 3xTF32 (fp32-tolerance) with exact sigmoids
   std::vector<janus::TMap> tm_w;   // wide_tc, per unit (msg: 3 maps): A^T [H x R], B^T [H x H], B [H x H]
 
   float* P(int u) const { return params + uoff[static_cast<size_t>(u - u0)]; }
