@@ -282,8 +282,9 @@ int janus_trainer_plan(janus_trainer* t, int32_t* unit_ranges /* [P][2] */);
  * 128 lanes x N fp32 columns. */
 int janus_tc_probe(const int32_t* args, const float* A, const float* B, float* D);
 /* gemm_tc.cuh self-test (tests/test_gpu_tc.py): D = A . W^T through the TMA-fed
- * tcgen05 GEMM (tf32).  pair = 1: A [2 rows x K] and D [2 rows x N] are the
- * stacked [value; derivative] layout of the generic-width path. */
+ * tcgen05 GEMM.  pair bit 0 = 1: A [2 rows x K] and D [2 rows x N] are the
+ * stacked [value; derivative] layout of the generic-width path; bit 1 = 1:
+ * 3xTF32 (fp32-accurate) instead of tf32. */
 int janus_gemm_tc_probe(int32_t rows, int32_t K, int32_t N, int32_t pair, const float* A, const float* W, float* D);
 
 /* ---- GARS micro-batch packing (host only; include/janus/gars.hpp) ----

@@ -130,8 +130,10 @@ void tc_probe(const int* args, const float* A, const float* B, float* D) {
 }
 
 // gemm_tc.cuh self-test: D = A . W^T through the TMA + tcgen05 pipeline with
-// the plain store epilogue (pair = 1: A and D stacked [2P x K] / [2P x N]).
-void gemm_tc_probe(int rows, int K, int N, int pair, const float* A, const float* W, float* D) {
+// the plain store epilogue.  mode bit 0 = pair (A and D stacked [2P x K] /
+// [2P x N]), bit 1 = 3xTF32 split (Problem::split3).
+void gemm_tc_probe(int rows, int K, int N, int mode, const float* A, const float* W, float* D) {
+  const int pair = mode & 1;
   const int arows = pair ? 2 * rows : rows;
   float *dA, *dW, *dD;
   JANUS_CUDA(cudaMalloc(&dA, sizeof(float) * arows * K));
@@ -142,7 +144,7 @@ void gemm_tc_probe(int rows, int K, int N, int pair, const float* A, const float
   JANUS_CUDA(cudaMemset(dD, 0, sizeof(float) * arows * N));
   const CUtensorMap ta = gemm_tc::make_tmap(dA, arows, K, pair ? 16 : 128);
   const CUtensorMap tw = gemm_tc::make_tmap(dW, N, K, N);
-  gemm_tc::launch(ta, tw, gemm_tc::Problem{rows, K, N, pair}, gemm_tc::EpiStore{dD, N}, nullptr);
+  gemm_tc::launch(ta, tw, gemm_tc::Problem{rows, K, N, pair, (mode >> 1) & 1}, gemm_tc::EpiStore{dD, N}, nullptr);
   JANUS_CUDA(cudaDeviceSynchronize());
   JANUS_CUDA(cudaMemcpy(D, dD, sizeof(float) * arows * N, cudaMemcpyDeviceToHost));
   cudaFree(dA);

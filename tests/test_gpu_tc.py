@@ -119,3 +119,25 @@ def test_tma_gemm_matches_numpy(janus, has_gpu, rows, K, N, pair):
     D = gemm_probe(janus, rows, K, N, pair, A, W)
     ref = tf32(A) @ tf32(W).T
     assert np.abs(D - ref).max() <= 1e-4 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("rows,K,N,pair", [(200, 64, 256, 0), (300, 256, 256, 0), (77, 64, 128, 0), (100, 64, 256, 1),
+                                           (130, 256, 64, 1)])
+def test_tma_gemm_split3_is_fp32_accurate(janus, has_gpu, rows, K, N, pair):
+    """gemm_tc.cuh 3xTF32 mode (Problem::split3, the fp32-tolerance path's
+    per-pair products): against an fp64 reference it is ~fp32-accurate
+    (4e-6 of max at K <= 256, the error scale of an fp32 accumulation), where
+    single-pass tf32 is ~7e-4."""
+    if not has_gpu:
+        pytest.skip("no GPU")
+    rng = np.random.default_rng(rows * 11 + K)
+    A = rng.standard_normal(((2 if pair else 1) * rows, K)).astype(np.float32)
+    W = rng.standard_normal((N, K)).astype(np.float32)
+    ref = A.astype(np.float64) @ W.astype(np.float64).T
+    scale = np.abs(ref).max()
+    D3 = gemm_probe(janus, rows, K, N, pair | 2, A, W)
+    D1 = gemm_probe(janus, rows, K, N, pair, A, W)
+    e3, e1 = np.abs(D3 - ref).max() / scale, np.abs(D1 - ref).max() / scale
+    print(f"3xTF32 rel err {e3:.2e}, tf32 {e1:.2e}")
+    assert e3 <= 4e-6
+    assert e1 > 50 * e3
