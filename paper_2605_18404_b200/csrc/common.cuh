@@ -72,7 +72,7 @@ struct PdlLaunch {
     cfg.attrs = nullptr;
     cfg.numAttrs = 0;
 #endif
-    (void)cudaLaunchKernelEx(&cfg, k, std::forward<A>(a)...);  // errors surface through cudaGetLastError like <<<>>>
+    JANUS_CUDA(cudaLaunchKernelEx(&cfg, k, std::forward<A>(a)...));  // a failed launch throws (cuda_error)
   }
 };
 template <typename... P>
